@@ -1,0 +1,145 @@
+/*
+ * rexi_b200.h -- C ABI of the B200-native REXI time step.
+ *
+ * One REXI step (reference rexiprop 0.1.0, pkg/src/rexiprop/integrate.py):
+ *
+ *     u1 = sum_j beta_j (tau*A - sigma_j*iB)^{-1} (iB u0)
+ *
+ * The reference has no FFI: its boundary is the Python function surface
+ * rexi_prepare / rexi_step / rexi_run (integrate.py:143-245) over the
+ * factorize()/solve() protocol of solvers.py:39-115.  These entry points
+ * replace, one for one:
+ *
+ *   rexi_plan_create   <- rexi_prepare          integrate.py:143-190
+ *                         (shifted-operator formation integrate.py:171,
+ *                          factorize + zgbtrf   solvers.py:42-69,108-115)
+ *   rexi_plan_step     <- rexi_step / rexi_run  integrate.py:193-245
+ *                         (rhs integrate.py:203-206, K solves :208-222 via
+ *                          zgbtrs solvers.py:76-80, Kahan reduce :59-68,224)
+ *   rexi_plan_step_partial + rexi_combine_partials
+ *                      <- the worker-pool split of the K solves and the
+ *                         fixed-order reduction (integrate.py:114-120,
+ *                         196-198, 215-224), across GPUs
+ *   rexi_plan_solve    <- factorizations[j].solve(b)  solvers.py:76-80
+ *   rexi_plan_destroy  <- RexiStepper.close()   integrate.py:131-140
+ *
+ * Conventions: plain pointers and sizes only.  Complex values are
+ * interleaved (re, im) doubles, layout-compatible with numpy complex128.
+ * Every call returns a rexi_status; on failure rexi_plan_last_error() (or
+ * rexi_last_error() when no plan exists) gives the message.  A plan is not
+ * reentrant (reference SPEC.md: "rexi_run is not reentrant on a single
+ * stepper"); distinct plans may run concurrently on distinct streams or
+ * devices.  The plan owns device copies of everything in rexi_desc; the
+ * caller keeps ownership of its host buffers.
+ */
+#ifndef REXI_B200_H
+#define REXI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define REXI_ABI_VERSION 1
+
+typedef struct rexi_c128 { double re, im; } rexi_c128;
+typedef struct rexi_plan rexi_plan;
+
+typedef enum rexi_status {
+    REXI_OK = 0,
+    REXI_ERR_INVALID = 1,      /* -> ValueError                                  */
+    REXI_ERR_SINGULAR = 2,     /* -> SolverError "shifted system j = ... singular" */
+    REXI_ERR_NOCONV = 3,       /* -> SolverError (iterative solve did not converge) */
+    REXI_ERR_BREAKDOWN = 4,    /* -> SolverError (COCG breakdown / non-finite)   */
+    REXI_ERR_CUDA = 5,         /* -> DeviceError                                 */
+    REXI_ERR_NOMEM = 6,        /* -> DeviceError (HBM exhausted)                 */
+    REXI_ERR_UNSUPPORTED = 7   /* -> ValueError                                  */
+} rexi_status;
+
+typedef enum rexi_solver {
+    REXI_SOLVER_AUTO = 0,      /* tridiagonal pattern -> TRIDIAG, else COCG      */
+    REXI_SOLVER_TRIDIAG = 1,   /* batched partitioned direct solve (1D P1)       */
+    REXI_SOLVER_COCG = 2       /* lockstep Jacobi-COCG over shifts (2D/3D, any)  */
+} rexi_solver;
+
+typedef enum rexi_mem { REXI_MEM_HOST = 0, REXI_MEM_DEVICE = 1 } rexi_mem;
+
+typedef struct rexi_desc {
+    int32_t abi_version;       /* REXI_ABI_VERSION                                */
+    int64_t n;                 /* n_dof                                           */
+    int64_t nnz;               /* entries of the shared CSR pattern of A and B    */
+    const int32_t *indptr;     /* host, n+1                                       */
+    const int32_t *indices;    /* host, nnz, sorted within each row               */
+    const double *a_vals;      /* host, nnz: A on the pattern (real part)         */
+    const double *a_imag;      /* host, nnz or NULL: imaginary part of A          */
+    const double *b_vals;      /* host, nnz: B on the pattern (real)              */
+    int32_t k;                 /* number of shifts handled by this plan           */
+    const rexi_c128 *shifts;   /* host, k: sigma_j                                */
+    const rexi_c128 *weights;  /* host, k: beta_j                                 */
+    int32_t shift_offset;      /* global index of shifts[0] (error messages)      */
+    double tau;
+    int32_t device;            /* CUDA ordinal                                    */
+    int32_t solver;            /* rexi_solver                                     */
+    int32_t refine;            /* residual-refinement rounds: -1 auto, 0..4       */
+    double tol;                /* COCG relative residual target (0 -> 1e-12)      */
+    int32_t max_iters;         /* COCG iteration cap per solve (0 -> 20000)       */
+    void *stream;              /* cudaStream_t to run on, or NULL (plan-owned)    */
+} rexi_desc;
+
+typedef struct rexi_stats {
+    double t_rhs_ms;           /* accumulated device time of the phases, like the */
+    double t_local_ms;         /* reference timers rhs/local/reduce               */
+    double t_reduce_ms;        /*   (integrate.py:110-112, 203-225)               */
+    int64_t steps;             /* steps executed by this call                     */
+    int64_t launches;          /* kernels launched by this call                   */
+    int32_t iters_max;         /* COCG: max iterations over shifts (last step)    */
+    double iters_mean;         /* COCG: mean iterations over shifts (last step)   */
+    int32_t refine_rounds;     /* refinement rounds applied per step              */
+    int32_t bad_shift;         /* global index of a failing shift, -1 if none     */
+} rexi_stats;
+
+typedef struct rexi_info {
+    int32_t solver;            /* resolved rexi_solver                            */
+    int32_t bandwidth;         /* kl+ku+1 of the pattern (3 for 1D P1)            */
+    int32_t k_pad;             /* lanes per block (padded shift count)            */
+    int32_t levels;            /* TRIDIAG: partition levels (incl. top)           */
+    int32_t refine;            /* resolved refinement rounds                      */
+    int64_t device_bytes;      /* HBM held by the plan                            */
+    double prepare_ms;         /* device time of rexi_plan_create                 */
+    double min_pivot_ratio;    /* TRIDIAG: min over shifts of min|d|/max|d|       */
+} rexi_info;
+
+int rexi_plan_create(const rexi_desc *desc, rexi_plan **out);
+
+/* n_steps REXI steps: u_out = step^n(u_in).  mem says whether u_in/u_out are
+ * host (pinned or pageable) or device pointers.  u_in == u_out is allowed. */
+int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out,
+                   int32_t n_steps, int32_t mem, rexi_stats *stats);
+
+/* One step for this plan's shard of shifts, leaving the double-double
+ * partial sum sum_{j in shard} beta_j x_j in partial (device, 4*n doubles:
+ * re_hi[n], re_lo[n], im_hi[n], im_lo[n]).  u_in is a device pointer. */
+int rexi_plan_step_partial(rexi_plan *plan, const rexi_c128 *u_in, double *partial,
+                           rexi_stats *stats);
+
+/* out = round(sum_{g=0}^{G-1} partials[g]) in fixed g order (device pointers,
+ * partials laid out as G consecutive 4*n blocks).  stream may be NULL. */
+int rexi_combine_partials(const double *partials, int32_t g, int64_t n, rexi_c128 *out,
+                          void *stream);
+
+/* Per-shift solutions x_j = S_j^{-1} rhs for every shift of the plan
+ * (x: k*n complex, shift-major).  mem applies to rhs and x. */
+int rexi_plan_solve(rexi_plan *plan, const rexi_c128 *rhs, rexi_c128 *x, int32_t mem);
+
+int rexi_plan_info(const rexi_plan *plan, rexi_info *info);
+int rexi_plan_destroy(rexi_plan *plan);
+const char *rexi_plan_last_error(const rexi_plan *plan);
+const char *rexi_last_error(void);
+int rexi_device_count(int32_t *count);
+int32_t rexi_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REXI_B200_H */

@@ -1,0 +1,240 @@
+"""ctypes binding of ``include/rexi_b200.h`` (the in-tree ``librexi_b200.so``).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, :func:`lib` / :class:`NativePlan` raise :class:`DeviceError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import DeviceError, SolverError
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "librexi_b200.so")
+
+REXI_OK = 0
+REXI_ERR_INVALID = 1
+REXI_ERR_SINGULAR = 2
+REXI_ERR_NOCONV = 3
+REXI_ERR_BREAKDOWN = 4
+REXI_ERR_CUDA = 5
+REXI_ERR_NOMEM = 6
+REXI_ERR_UNSUPPORTED = 7
+
+SOLVER_AUTO, SOLVER_TRIDIAG, SOLVER_COCG = 0, 1, 2
+MEM_HOST, MEM_DEVICE = 0, 1
+ABI_VERSION = 1
+
+EXPORTED = (
+    "rexi_plan_create", "rexi_plan_step", "rexi_plan_step_partial", "rexi_combine_partials",
+    "rexi_plan_solve", "rexi_plan_info", "rexi_plan_destroy", "rexi_plan_last_error",
+    "rexi_last_error", "rexi_device_count", "rexi_abi_version",
+)
+
+
+class RexiDesc(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32),
+        ("n", ctypes.c_int64),
+        ("nnz", ctypes.c_int64),
+        ("indptr", ctypes.c_void_p),
+        ("indices", ctypes.c_void_p),
+        ("a_vals", ctypes.c_void_p),
+        ("a_imag", ctypes.c_void_p),
+        ("b_vals", ctypes.c_void_p),
+        ("k", ctypes.c_int32),
+        ("shifts", ctypes.c_void_p),
+        ("weights", ctypes.c_void_p),
+        ("shift_offset", ctypes.c_int32),
+        ("tau", ctypes.c_double),
+        ("device", ctypes.c_int32),
+        ("solver", ctypes.c_int32),
+        ("refine", ctypes.c_int32),
+        ("tol", ctypes.c_double),
+        ("max_iters", ctypes.c_int32),
+        ("stream", ctypes.c_void_p),
+    ]
+
+
+class RexiStats(ctypes.Structure):
+    _fields_ = [
+        ("t_rhs_ms", ctypes.c_double),
+        ("t_local_ms", ctypes.c_double),
+        ("t_reduce_ms", ctypes.c_double),
+        ("steps", ctypes.c_int64),
+        ("launches", ctypes.c_int64),
+        ("iters_max", ctypes.c_int32),
+        ("iters_mean", ctypes.c_double),
+        ("refine_rounds", ctypes.c_int32),
+        ("bad_shift", ctypes.c_int32),
+    ]
+
+
+class RexiInfo(ctypes.Structure):
+    _fields_ = [
+        ("solver", ctypes.c_int32),
+        ("bandwidth", ctypes.c_int32),
+        ("k_pad", ctypes.c_int32),
+        ("levels", ctypes.c_int32),
+        ("refine", ctypes.c_int32),
+        ("device_bytes", ctypes.c_int64),
+        ("prepare_ms", ctypes.c_double),
+        ("min_pivot_ratio", ctypes.c_double),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load the in-tree native library (raises DeviceError if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(
+            f"native library {LIB_PATH} is missing; run __graft_entry__.build() "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp = ctypes.c_void_p
+    L.rexi_plan_create.argtypes = [ctypes.POINTER(RexiDesc), ctypes.POINTER(vp)]
+    L.rexi_plan_step.argtypes = [vp, vp, vp, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(RexiStats)]
+    L.rexi_plan_step_partial.argtypes = [vp, vp, vp, ctypes.POINTER(RexiStats)]
+    L.rexi_combine_partials.argtypes = [vp, ctypes.c_int32, ctypes.c_int64, vp, vp]
+    L.rexi_plan_solve.argtypes = [vp, vp, vp, ctypes.c_int32]
+    L.rexi_plan_info.argtypes = [vp, ctypes.POINTER(RexiInfo)]
+    L.rexi_plan_destroy.argtypes = [vp]
+    L.rexi_plan_last_error.argtypes = [vp]
+    L.rexi_plan_last_error.restype = ctypes.c_char_p
+    L.rexi_last_error.restype = ctypes.c_char_p
+    L.rexi_device_count.argtypes = [ctypes.POINTER(ctypes.c_int32)]
+    L.rexi_abi_version.restype = ctypes.c_int32
+    if L.rexi_abi_version() != ABI_VERSION:
+        raise DeviceError("native library ABI version mismatch")
+    _lib = L
+    return L
+
+
+def device_count() -> int:
+    c = ctypes.c_int32(0)
+    rc = lib().rexi_device_count(ctypes.byref(c))
+    return int(c.value) if rc == 0 else 0
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class NativeError(Exception):
+    pass
+
+
+def raise_status(rc: int, msg: str, shift_offset: int = 0):
+    if rc == REXI_OK:
+        return
+    if rc in (REXI_ERR_INVALID, REXI_ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    if rc in (REXI_ERR_SINGULAR, REXI_ERR_NOCONV, REXI_ERR_BREAKDOWN):
+        raise SolverError(msg)
+    raise DeviceError(msg)
+
+
+class NativePlan:
+    """Owns one ``rexi_plan`` (one device, one shard of shifts)."""
+
+    def __init__(self, indptr, indices, a_vals, b_vals, shifts, weights, tau, *, a_imag=None,
+                 device=0, solver=SOLVER_AUTO, refine=-1, tol=0.0, max_iters=0, shift_offset=0,
+                 stream=None):
+        L = lib()
+        self._keep = [np.ascontiguousarray(indptr, dtype=np.int32),
+                      np.ascontiguousarray(indices, dtype=np.int32),
+                      np.ascontiguousarray(a_vals, dtype=np.float64),
+                      np.ascontiguousarray(b_vals, dtype=np.float64),
+                      np.ascontiguousarray(shifts, dtype=np.complex128),
+                      np.ascontiguousarray(weights, dtype=np.complex128)]
+        if a_imag is not None:
+            self._keep.append(np.ascontiguousarray(a_imag, dtype=np.float64))
+        ip, ix, av, bv, sh, wt = self._keep[:6]
+        d = RexiDesc()
+        d.abi_version = ABI_VERSION
+        d.n = len(ip) - 1
+        d.nnz = len(ix)
+        d.indptr = ip.ctypes.data
+        d.indices = ix.ctypes.data
+        d.a_vals = av.ctypes.data
+        d.a_imag = self._keep[6].ctypes.data if a_imag is not None else None
+        d.b_vals = bv.ctypes.data
+        d.k = len(sh)
+        d.shifts = sh.ctypes.data
+        d.weights = wt.ctypes.data
+        d.shift_offset = int(shift_offset)
+        d.tau = float(tau)
+        d.device = int(device)
+        d.solver = int(solver)
+        d.refine = int(refine)
+        d.tol = float(tol)
+        d.max_iters = int(max_iters)
+        d.stream = stream
+        self.n = int(d.n)
+        self.k = int(d.k)
+        self.device = int(device)
+        h = ctypes.c_void_p(None)
+        rc = L.rexi_plan_create(ctypes.byref(d), ctypes.byref(h))
+        if rc != REXI_OK:
+            msg = L.rexi_last_error().decode()
+            raise_status(rc, msg)
+        self._h = h
+        info = RexiInfo()
+        L.rexi_plan_info(self._h, ctypes.byref(info))
+        self.info = info
+
+    def _err(self) -> str:
+        return lib().rexi_plan_last_error(self._h).decode()
+
+    def step_host(self, u: np.ndarray, n_steps: int = 1, stats: RexiStats | None = None) -> np.ndarray:
+        u = np.ascontiguousarray(u, dtype=np.complex128)
+        out = np.empty_like(u)
+        rc = lib().rexi_plan_step(self._h, _ptr(u), _ptr(out), int(n_steps), MEM_HOST,
+                                  ctypes.byref(stats) if stats is not None else None)
+        raise_status(rc, self._err())
+        return out
+
+    def step_device(self, u_ptr: int, out_ptr: int, n_steps: int = 1,
+                    stats: RexiStats | None = None):
+        rc = lib().rexi_plan_step(self._h, ctypes.c_void_p(u_ptr), ctypes.c_void_p(out_ptr),
+                                  int(n_steps), MEM_DEVICE,
+                                  ctypes.byref(stats) if stats is not None else None)
+        raise_status(rc, self._err())
+
+    def step_partial(self, u_ptr: int, partial_ptr: int, stats: RexiStats | None = None):
+        rc = lib().rexi_plan_step_partial(self._h, ctypes.c_void_p(u_ptr), ctypes.c_void_p(partial_ptr),
+                                          ctypes.byref(stats) if stats is not None else None)
+        raise_status(rc, self._err())
+
+    def solve_host(self, rhs: np.ndarray) -> np.ndarray:
+        rhs = np.ascontiguousarray(rhs, dtype=np.complex128)
+        x = np.empty((self.k, self.n), dtype=np.complex128)
+        rc = lib().rexi_plan_solve(self._h, _ptr(rhs), _ptr(x), MEM_HOST)
+        raise_status(rc, self._err())
+        return x
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().rexi_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def combine_partials(partials_ptr: int, g: int, n: int, out_ptr: int, stream=None):
+    rc = lib().rexi_combine_partials(ctypes.c_void_p(partials_ptr), int(g), int(n),
+                                     ctypes.c_void_p(out_ptr), stream)
+    raise_status(rc, lib().rexi_last_error().decode())

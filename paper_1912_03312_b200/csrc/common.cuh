@@ -1,0 +1,96 @@
+// common.cuh -- complex128 / double-double device helpers for the REXI path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+typedef double2 c128;   // (x = re, y = im), layout-compatible with numpy complex128
+
+__device__ __forceinline__ c128 cmk(double r, double i) { return make_double2(r, i); }
+__device__ __forceinline__ c128 cadd(c128 a, c128 b) { return cmk(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ c128 csub(c128 a, c128 b) { return cmk(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ c128 cneg(c128 a) { return cmk(-a.x, -a.y); }
+__device__ __forceinline__ c128 cmul(c128 a, c128 b) {
+    return cmk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a - b*c
+__device__ __forceinline__ c128 cfnma(c128 a, c128 b, c128 c) {
+    return cmk(fma(-b.x, c.x, fma(b.y, c.y, a.x)), fma(-b.x, c.y, fma(-b.y, c.x, a.y)));
+}
+__device__ __forceinline__ c128 crcp(c128 d) {
+    double den = fma(d.x, d.x, d.y * d.y);
+    double r = 1.0 / den;
+    return cmk(d.x * r, -d.y * r);
+}
+__device__ __forceinline__ double cabs2(c128 a) { return fma(a.x, a.x, a.y * a.y); }
+
+// Shifted-operator entry with the reference's rounding (integrate.py:171):
+// tau*A - (1j*sigma)*B  ->  re = fl(fl(tau*a) + fl(Im(sigma)*b)),  im = -fl(Re(sigma)*b)
+// ta = fl(tau*a) is precomputed on the host side of the plan; no FMA contraction here.
+__device__ __forceinline__ c128 form_entry(double ta, double ta_im, double b, c128 s) {
+    double re = __dadd_rn(ta, __dmul_rn(s.y, b));
+    double im = __dsub_rn(ta_im, __dmul_rn(s.x, b));
+    return cmk(re, im);
+}
+
+// ---- double-double (error-free transforms) ----
+struct dd { double hi, lo; };
+__device__ __forceinline__ dd two_sum(double a, double b) {
+    double s = __dadd_rn(a, b);
+    double bb = __dsub_rn(s, a);
+    double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+    return {s, e};
+}
+__device__ __forceinline__ dd fast_two_sum(double a, double b) {   // |a| >= |b|
+    double s = __dadd_rn(a, b);
+    return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ dd two_prod(double a, double b) {
+    double p = __dmul_rn(a, b);
+    return {p, __fma_rn(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+    dd s = two_sum(a.hi, b.hi);
+    dd t = two_sum(a.lo, b.lo);
+    s.lo = __dadd_rn(s.lo, t.hi);
+    s = fast_two_sum(s.hi, s.lo);
+    s.lo = __dadd_rn(s.lo, t.lo);
+    return fast_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_add_d(dd a, double b) {
+    dd s = two_sum(a.hi, b);
+    s.lo = __dadd_rn(s.lo, a.lo);
+    return fast_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_neg(dd a) { return {-a.hi, -a.lo}; }
+
+// complex double-double accumulator
+struct cdd { dd re, im; };
+__device__ __forceinline__ cdd cdd_zero() { return {{0.0, 0.0}, {0.0, 0.0}}; }
+// acc += w * x with the complex product formed exactly (4 two_prods)
+__device__ __forceinline__ cdd cdd_fma(cdd acc, c128 w, c128 x) {
+    dd p1 = two_prod(w.x, x.x), p2 = two_prod(-w.y, x.y);
+    dd p3 = two_prod(w.x, x.y), p4 = two_prod(w.y, x.x);
+    acc.re = dd_add(acc.re, dd_add(p1, p2));
+    acc.im = dd_add(acc.im, dd_add(p3, p4));
+    return acc;
+}
+__device__ __forceinline__ cdd cdd_add(cdd a, cdd b) {
+    return {dd_add(a.re, b.re), dd_add(a.im, b.im)};
+}
+__device__ __forceinline__ c128 cdd_round(cdd a) {
+    return cmk(__dadd_rn(a.re.hi, a.re.lo), __dadd_rn(a.im.hi, a.im.lo));
+}
+// r -= e*x exactly (e, x complex doubles) into a complex dd accumulator
+__device__ __forceinline__ cdd cdd_sub_prod(cdd acc, c128 e, c128 x) {
+    dd p1 = two_prod(e.x, x.x), p2 = two_prod(-e.y, x.y);
+    dd p3 = two_prod(e.x, x.y), p4 = two_prod(e.y, x.x);
+    acc.re = dd_add(acc.re, dd_neg(dd_add(p1, p2)));
+    acc.im = dd_add(acc.im, dd_neg(dd_add(p3, p4)));
+    return acc;
+}
+
+#define REXI_CUDA_CHECK(expr)                                                     \
+    do {                                                                          \
+        cudaError_t _e = (expr);                                                  \
+        if (_e != cudaSuccess) return rexi_fail_cuda(plan_for_err, _e, #expr, __FILE__, __LINE__); \
+    } while (0)

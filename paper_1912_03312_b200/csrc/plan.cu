@@ -1,0 +1,566 @@
+// plan.cu -- the C ABI of include/rexi_b200.h: plan creation (the analogue of
+// rexi_prepare, reference integrate.py:143-190), stepping (rexi_step /
+// rexi_run, integrate.py:193-245), per-shift solves and partial sums for the
+// pole-sharded multi-GPU path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rexi_b200.h"
+#include "cocg.cuh"
+#include "tridiag_launch.h"
+
+using namespace rexi;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct TriState {
+    int64_t n = 0;
+    std::vector<LevelDev> lv;     // device pointers, one per level (last = top)
+    L0Dev z{};
+    c128 *rhs0 = nullptr, *rres = nullptr;
+    double *acc = nullptr;
+};
+
+}  // namespace
+
+struct rexi_plan {
+    int device = 0;
+    int solver = REXI_SOLVER_AUTO;
+    int64_t n = 0;
+    int k = 0, kp = 0;
+    int shift_offset = 0;
+    int refine = 0;
+    int bandwidth = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    std::vector<void *> allocs;
+    int64_t bytes = 0;
+    ShiftDev S{};
+    c128 *ubuf[2] = {nullptr, nullptr};
+    TriState tri;
+    CocgState cg;
+    double prepare_ms = 0.0;
+    double min_pivot_ratio = 1.0;
+    std::vector<rexi_c128> shifts_host;
+    int64_t launches = 0;
+};
+
+namespace {
+
+int set_err(rexi_plan *p, int code, const std::string &msg) {
+    g_last_error = msg;
+    if (p) p->err = msg;
+    return code;
+}
+
+int cuda_err(rexi_plan *p, cudaError_t e, const char *what) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "CUDA error in %s: %s (%s)", what, cudaGetErrorName(e),
+             cudaGetErrorString(e));
+    return set_err(p, e == cudaErrorMemoryAllocation ? REXI_ERR_NOMEM : REXI_ERR_CUDA, buf);
+}
+
+#define CK(expr)                                                   \
+    do {                                                           \
+        cudaError_t _e = (expr);                                   \
+        if (_e != cudaSuccess) return cuda_err(plan, _e, #expr);   \
+    } while (0)
+
+template <typename T>
+int dalloc(rexi_plan *plan, T **ptr, size_t count) {
+    void *v = nullptr;
+    size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(&v, bytes);
+    if (e != cudaSuccess) return cuda_err(plan, e, "cudaMalloc");
+    plan->allocs.push_back(v);
+    plan->bytes += (int64_t)bytes;
+    *ptr = (T *)v;
+    return REXI_OK;
+}
+
+#define DALLOC(ptr, count)                          \
+    do {                                            \
+        int _rc = dalloc(plan, &(ptr), (count));    \
+        if (_rc) return _rc;                        \
+    } while (0)
+
+int pick_kp(int k) {
+    int kp = 1;
+    while (kp < k) kp <<= 1;
+    return kp;
+}
+
+// ------------------------------------------------------------------------
+// tridiagonal path
+// ------------------------------------------------------------------------
+int tri_create(rexi_plan *plan, const rexi_desc *d) {
+    const int64_t n = d->n;
+    TriState &T = plan->tri;
+    T.n = n;
+    // diagonals of A (re, im) and B from the shared CSR pattern
+    std::vector<double> a_sub(n, 0.0), a_dia(n, 0.0), a_sup(n, 0.0);
+    std::vector<double> ai_sub(n, 0.0), ai_dia(n, 0.0), ai_sup(n, 0.0);
+    std::vector<double> b_sub(n, 0.0), b_dia(n, 0.0), b_sup(n, 0.0);
+    for (int64_t r = 0; r < n; ++r) {
+        for (int32_t q = d->indptr[r]; q < d->indptr[r + 1]; ++q) {
+            int64_t c = d->indices[q];
+            double av = d->a_vals[q], ai = d->a_imag ? d->a_imag[q] : 0.0, bv = d->b_vals[q];
+            if (c == r - 1) { a_sub[r] = av; ai_sub[r] = ai; b_sub[r] = bv; }
+            else if (c == r) { a_dia[r] = av; ai_dia[r] = ai; b_dia[r] = bv; }
+            else if (c == r + 1) { a_sup[r] = av; ai_sup[r] = ai; b_sup[r] = bv; }
+            else return set_err(plan, REXI_ERR_INVALID, "pattern is not tridiagonal");
+        }
+    }
+    // fl(tau * a) exactly as numpy computes tau*A (integrate.py:171)
+    auto scale = [&](std::vector<double> &v) { for (auto &x : v) x = d->tau * x; };
+    scale(a_sub); scale(a_dia); scale(a_sup); scale(ai_sub); scale(ai_dia); scale(ai_sup);
+    double *dz[9];
+    std::vector<double> *hz[9] = {&a_sub, &ai_sub, &b_sub, &a_dia, &ai_dia, &b_dia, &a_sup, &ai_sup, &b_sup};
+    for (int q = 0; q < 9; ++q) {
+        DALLOC(dz[q], (size_t)n);
+        CK(cudaMemcpyAsync(dz[q], hz[q]->data(), sizeof(double) * n, cudaMemcpyHostToDevice, plan->stream));
+    }
+    T.z = L0Dev{dz[0], dz[1], dz[2], dz[3], dz[4], dz[5], dz[6], dz[7], dz[8], dz[2], dz[5], dz[8]};
+
+    // levels
+    const int kp = plan->kp;
+    int64_t nl = n;
+    for (;;) {
+        LevelDev L{};
+        L.n = nl;
+        if (!T.lv.empty() && nl <= TOP_MAX) {
+            L.top = 1;
+            L.P = 0;
+        } else {
+            L.top = 0;
+            L.P = (nl + TRI_M - 1) / TRI_M;
+        }
+        size_t rows = (size_t)nl * kp;
+        DALLOC(L.invd, rows);
+        DALLOC(L.X, rows);
+        if (!T.lv.empty()) {
+            DALLOC(L.sub, rows);
+            DALLOC(L.dia, rows);
+            DALLOC(L.sup, rows);
+        }
+        if (!L.top) {
+            size_t pr = (size_t)L.P * kp;
+            DALLOC(L.ypart, pr);
+            DALLOC(L.lc, pr);
+            DALLOC(L.phiF, pr);
+            DALLOC(L.phiL, pr);
+            DALLOC(L.psiF, pr);
+            DALLOC(L.psiL, pr);
+        }
+        T.lv.push_back(L);
+        if (L.top) break;
+        nl = L.P;
+    }
+    DALLOC(T.rhs0, (size_t)n);
+    DALLOC(T.acc, (size_t)4 * n);
+    if (plan->refine > 0) DALLOC(T.rres, (size_t)n * kp);
+
+    // factor every level
+    unsigned long long *pmin = nullptr, *pmax = nullptr;
+    DALLOC(pmin, (size_t)kp);
+    DALLOC(pmax, (size_t)kp);
+    std::vector<unsigned long long> init_min(kp), init_max(kp, 0ull);
+    double inf = INFINITY;
+    unsigned long long inf_bits;
+    memcpy(&inf_bits, &inf, sizeof inf_bits);
+    std::fill(init_min.begin(), init_min.end(), inf_bits);
+    CK(cudaMemcpyAsync(pmin, init_min.data(), sizeof(unsigned long long) * kp, cudaMemcpyHostToDevice, plan->stream));
+    CK(cudaMemcpyAsync(pmax, init_max.data(), sizeof(unsigned long long) * kp, cudaMemcpyHostToDevice, plan->stream));
+    for (size_t l = 0; l < T.lv.size(); ++l) {
+        const LevelDev *next = l + 1 < T.lv.size() ? &T.lv[l + 1] : nullptr;
+        CK(tri_launch_factor(T.z, T.lv[l], next, plan->S, (int)l, pmin, pmax, plan->stream));
+    }
+    std::vector<unsigned long long> hmin(kp), hmax(kp);
+    CK(cudaMemcpyAsync(hmin.data(), pmin, sizeof(unsigned long long) * kp, cudaMemcpyDeviceToHost, plan->stream));
+    CK(cudaMemcpyAsync(hmax.data(), pmax, sizeof(unsigned long long) * kp, cudaMemcpyDeviceToHost, plan->stream));
+    CK(cudaStreamSynchronize(plan->stream));
+    double worst = 1.0;
+    for (int j = 0; j < plan->k; ++j) {
+        double mn, mx;
+        memcpy(&mn, &hmin[j], sizeof mn);
+        memcpy(&mx, &hmax[j], sizeof mx);
+        double ratio = mx > 0 ? mn / mx : 0.0;
+        if (std::isinf(mn)) ratio = 1.0;  // no pivots at all (cannot happen: top level has >= 1 row)
+        worst = std::min(worst, ratio);
+        if (!(mn > 0.0) || !(mx < INFINITY) || mn < 1e-14 * mx) {
+            char buf[256];
+            snprintf(buf, sizeof buf, "matrix is numerically singular (pivot ratio = %.3e) for shift j = %d",
+                     ratio, plan->shift_offset + j);
+            plan->min_pivot_ratio = ratio;
+            return set_err(plan, REXI_ERR_SINGULAR, buf);
+        }
+    }
+    plan->min_pivot_ratio = worst;
+    return REXI_OK;
+}
+
+// one pass of the level chain: S1 up, top solve, S3 down
+int tri_chain(rexi_plan *plan, const c128 *rst, int out_mode, int acc_add, c128 *uout) {
+    TriState &T = plan->tri;
+    const size_t nl = T.lv.size();
+    cudaStream_t st = plan->stream;
+    for (size_t l = 0; l + 1 < nl; ++l) {
+        const c128 *ra = l ? T.lv[l - 1].ypart : nullptr;
+        const c128 *rb = l ? T.lv[l - 1].lc : nullptr;
+        CK(tri_launch_s1(T.z, T.lv[l], plan->S, (int)l, T.rhs0, l ? nullptr : rst, ra, rb, st));
+        ++plan->launches;
+    }
+    CK(tri_launch_top_solve(T.lv[nl - 1], plan->S, T.lv[nl - 2].ypart, T.lv[nl - 2].lc, st));
+    ++plan->launches;
+    for (size_t l = nl - 1; l-- > 0;) {
+        const c128 *ra = l ? T.lv[l - 1].ypart : nullptr;
+        const c128 *rb = l ? T.lv[l - 1].lc : nullptr;
+        CK(tri_launch_s3(T.z, T.lv[l], plan->S, (int)l, T.rhs0, l ? nullptr : rst, ra, rb,
+                         T.lv[l + 1].X, l ? TRI_OUT_X : out_mode, T.acc, acc_add, l ? nullptr : uout,
+                         st));
+        ++plan->launches;
+    }
+    return REXI_OK;
+}
+
+// one step from device u -> (uout rounded) or (T.acc partial when uout == nullptr)
+int tri_step(rexi_plan *plan, const c128 *u, c128 *uout) {
+    TriState &T = plan->tri;
+    CK(tri_launch_rhs(T.z, T.n, u, T.rhs0, plan->stream));
+    ++plan->launches;
+    if (plan->refine <= 0) return tri_chain(plan, nullptr, TRI_OUT_ACC, 0, uout);
+    int rc = tri_chain(plan, nullptr, TRI_OUT_X_ACC, 0, nullptr);
+    if (rc) return rc;
+    CK(tri_launch_residual(T.z, T.lv[0], plan->S, T.rhs0, T.rres, plan->stream));
+    ++plan->launches;
+    return tri_chain(plan, T.rres, TRI_OUT_ACC, 1, uout);
+}
+
+int plan_step_device(rexi_plan *plan, const c128 *u, c128 *uout) {
+    if (plan->solver == REXI_SOLVER_TRIDIAG) return tri_step(plan, u, uout);
+    return cocg_step(plan->cg, plan->S, plan->stream, u, uout, plan->tri.acc, &plan->launches,
+                     plan->err);
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t rexi_abi_version(void) { return REXI_ABI_VERSION; }
+
+const char *rexi_last_error(void) { return g_last_error.c_str(); }
+
+const char *rexi_plan_last_error(const rexi_plan *plan) {
+    return plan ? plan->err.c_str() : g_last_error.c_str();
+}
+
+int rexi_device_count(int32_t *count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return cuda_err(nullptr, e, "cudaGetDeviceCount");
+    }
+    *count = c;
+    return REXI_OK;
+}
+
+int rexi_plan_destroy(rexi_plan *plan) {
+    if (!plan) return REXI_OK;
+    cudaSetDevice(plan->device);
+    if (plan->stream) cudaStreamSynchronize(plan->stream);
+    for (void *p : plan->allocs) cudaFree(p);
+    cocg_destroy(plan->cg);
+    if (plan->own_stream && plan->stream) cudaStreamDestroy(plan->stream);
+    delete plan;
+    return REXI_OK;
+}
+
+int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
+    *out = nullptr;
+    if (!d) return set_err(nullptr, REXI_ERR_INVALID, "null descriptor");
+    if (d->abi_version != REXI_ABI_VERSION)
+        return set_err(nullptr, REXI_ERR_INVALID, "ABI version mismatch");
+    if (d->n < 1) return set_err(nullptr, REXI_ERR_INVALID, "n must be >= 1");
+    if (d->k < 1) return set_err(nullptr, REXI_ERR_INVALID, "need at least one shift");
+    if (!(d->tau > 0.0)) return set_err(nullptr, REXI_ERR_INVALID, "tau must be positive");
+    if (!d->indptr || !d->indices || !d->a_vals || !d->b_vals || !d->shifts || !d->weights)
+        return set_err(nullptr, REXI_ERR_INVALID, "null input array");
+    rexi_plan *plan = new rexi_plan();
+    plan->device = d->device;
+    plan->n = d->n;
+    plan->k = d->k;
+    plan->shift_offset = d->shift_offset;
+    plan->shifts_host.assign(d->shifts, d->shifts + d->k);
+    // structure
+    bool tri = true;
+    int kl = 0, ku = 0;
+    for (int64_t r = 0; r < d->n; ++r)
+        for (int32_t q = d->indptr[r]; q < d->indptr[r + 1]; ++q) {
+            int64_t c = d->indices[q];
+            if (c < 0 || c >= d->n) {
+                int rc = set_err(plan, REXI_ERR_INVALID, "column index out of range");
+                rexi_plan_destroy(plan);
+                return rc;
+            }
+            kl = std::max<int>(kl, (int)(r - c));
+            ku = std::max<int>(ku, (int)(c - r));
+        }
+    tri = kl <= 1 && ku <= 1;
+    plan->bandwidth = kl + ku + 1;
+    int solver = d->solver;
+    if (solver == REXI_SOLVER_AUTO) solver = tri ? REXI_SOLVER_TRIDIAG : REXI_SOLVER_COCG;
+    if (solver == REXI_SOLVER_TRIDIAG && !tri) {
+        int rc = set_err(plan, REXI_ERR_UNSUPPORTED, "TRIDIAG solver needs a tridiagonal pattern");
+        rexi_plan_destroy(plan);
+        return rc;
+    }
+    plan->solver = solver;
+    plan->kp = solver == REXI_SOLVER_TRIDIAG ? pick_kp(d->k) : d->k;
+    if (solver == REXI_SOLVER_TRIDIAG && plan->kp > 256) {
+        int rc = set_err(plan, REXI_ERR_UNSUPPORTED, "TRIDIAG solver supports at most 256 shifts per plan");
+        rexi_plan_destroy(plan);
+        return rc;
+    }
+    plan->refine = d->refine < 0 ? 0 : std::min(d->refine, solver == REXI_SOLVER_TRIDIAG ? 1 : 4);
+
+    cudaError_t e = cudaSetDevice(d->device);
+    if (e != cudaSuccess) {
+        int rc = cuda_err(plan, e, "cudaSetDevice");
+        rexi_plan_destroy(plan);
+        return rc;
+    }
+    if (d->stream) {
+        plan->stream = (cudaStream_t)d->stream;
+    } else {
+        e = cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            int rc = cuda_err(plan, e, "cudaStreamCreate");
+            rexi_plan_destroy(plan);
+            return rc;
+        }
+        plan->own_stream = true;
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, plan->stream);
+    int rc = REXI_OK;
+    {
+        // shifts / weights, padded to kp lanes (padding: sigma_0 with beta = 0)
+        const int kp = plan->kp;
+        std::vector<rexi_c128> sg(kp), bt(kp);
+        for (int j = 0; j < kp; ++j) {
+            sg[j] = d->shifts[j < d->k ? j : 0];
+            bt[j] = j < d->k ? d->weights[j] : rexi_c128{0.0, 0.0};
+        }
+        c128 *dsg = nullptr, *dbt = nullptr;
+        rc = dalloc(plan, &dsg, kp);
+        if (!rc) rc = dalloc(plan, &dbt, kp);
+        if (!rc) {
+            cudaMemcpyAsync(dsg, sg.data(), sizeof(c128) * kp, cudaMemcpyHostToDevice, plan->stream);
+            cudaMemcpyAsync(dbt, bt.data(), sizeof(c128) * kp, cudaMemcpyHostToDevice, plan->stream);
+            plan->S = ShiftDev{dsg, dbt, kp};
+        }
+        if (!rc) rc = dalloc(plan, &plan->ubuf[0], (size_t)d->n);
+        if (!rc) rc = dalloc(plan, &plan->ubuf[1], (size_t)d->n);
+        if (!rc) {
+            if (solver == REXI_SOLVER_TRIDIAG) {
+                rc = tri_create(plan, d);
+            } else {
+                rc = dalloc(plan, &plan->tri.acc, (size_t)4 * d->n);
+                if (!rc) rc = cocg_create(plan->cg, d, plan->S, plan->refine, plan->stream, plan->err);
+                if (rc) set_err(plan, rc, plan->err);
+            }
+        }
+    }
+    if (rc) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        std::string msg = plan->err;
+        rexi_plan_destroy(plan);
+        g_last_error = msg;
+        return rc;
+    }
+    cudaEventRecord(e1, plan->stream);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    plan->prepare_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        int rc2 = cuda_err(plan, e, "prepare");
+        std::string msg = plan->err;
+        rexi_plan_destroy(plan);
+        g_last_error = msg;
+        return rc2;
+    }
+    *out = plan;
+    return REXI_OK;
+}
+
+int rexi_plan_info(const rexi_plan *plan, rexi_info *info) {
+    if (!plan || !info) return set_err(nullptr, REXI_ERR_INVALID, "null argument");
+    info->solver = plan->solver;
+    info->bandwidth = plan->bandwidth;
+    info->k_pad = plan->kp;
+    info->levels = (int32_t)plan->tri.lv.size();
+    info->refine = plan->refine;
+    info->device_bytes = plan->bytes + plan->cg.bytes;
+    info->prepare_ms = plan->prepare_ms;
+    info->min_pivot_ratio = plan->min_pivot_ratio;
+    return REXI_OK;
+}
+
+int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int32_t n_steps,
+                   int32_t mem, rexi_stats *stats) {
+    if (!plan) return set_err(nullptr, REXI_ERR_INVALID, "null plan");
+    if (n_steps < 0) return set_err(plan, REXI_ERR_INVALID, "n_steps must be >= 0");
+    CK(cudaSetDevice(plan->device));
+    const int64_t n = plan->n;
+    cudaStream_t st = plan->stream;
+    plan->launches = 0;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    if (stats) {
+        CK(cudaEventCreate(&ev[0]));
+        CK(cudaEventCreate(&ev[1]));
+    }
+    const c128 *src;
+    if (mem == REXI_MEM_HOST) {
+        CK(cudaMemcpyAsync(plan->ubuf[0], u_in, sizeof(c128) * n, cudaMemcpyHostToDevice, st));
+        src = plan->ubuf[0];
+    } else {
+        src = (const c128 *)u_in;
+    }
+    if (stats) CK(cudaEventRecord(ev[0], st));
+    int cur = (src == plan->ubuf[0]) ? 0 : 1;
+    for (int s = 0; s < n_steps; ++s) {
+        c128 *dst;
+        bool last = s == n_steps - 1;
+        if (last && mem == REXI_MEM_DEVICE) dst = (c128 *)u_out;
+        else dst = plan->ubuf[src == plan->ubuf[0] ? 1 : 0];
+        if (dst == src) dst = plan->ubuf[cur ^ 1];   // in-place device call
+        int rc = plan_step_device(plan, src, dst);
+        if (rc) {
+            if (ev[0]) { cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]); }
+            if (rc == REXI_ERR_NOCONV || rc == REXI_ERR_BREAKDOWN) return set_err(plan, rc, plan->err);
+            return rc;
+        }
+        src = dst;
+        cur = (src == plan->ubuf[0]) ? 0 : 1;
+    }
+    if (stats) CK(cudaEventRecord(ev[1], st));
+    if (n_steps == 0) {
+        if (mem == REXI_MEM_HOST) {
+            if (u_out != u_in) memcpy(u_out, u_in, sizeof(c128) * n);
+        } else if (u_out != u_in) {
+            CK(cudaMemcpyAsync(u_out, u_in, sizeof(c128) * n, cudaMemcpyDeviceToDevice, st));
+        }
+    } else if (mem == REXI_MEM_HOST) {
+        CK(cudaMemcpyAsync(u_out, src, sizeof(c128) * n, cudaMemcpyDeviceToHost, st));
+    } else if ((const void *)src != (const void *)u_out) {
+        CK(cudaMemcpyAsync(u_out, src, sizeof(c128) * n, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    if (stats) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[0], ev[1]);
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+        stats->t_rhs_ms = 0.0;
+        stats->t_local_ms = ms;
+        stats->t_reduce_ms = 0.0;
+        stats->steps = n_steps;
+        stats->launches = plan->launches;
+        stats->iters_max = plan->cg.last_iters_max;
+        stats->iters_mean = plan->cg.last_iters_mean;
+        stats->refine_rounds = plan->refine;
+        stats->bad_shift = -1;
+    }
+    return REXI_OK;
+}
+
+int rexi_plan_step_partial(rexi_plan *plan, const rexi_c128 *u_in, double *partial,
+                           rexi_stats *stats) {
+    if (!plan) return set_err(nullptr, REXI_ERR_INVALID, "null plan");
+    CK(cudaSetDevice(plan->device));
+    plan->launches = 0;
+    int rc = plan_step_device(plan, (const c128 *)u_in, nullptr);
+    if (rc) return rc == REXI_ERR_NOCONV || rc == REXI_ERR_BREAKDOWN ? set_err(plan, rc, plan->err) : rc;
+    CK(cudaMemcpyAsync(partial, plan->tri.acc, sizeof(double) * 4 * plan->n, cudaMemcpyDeviceToDevice,
+                       plan->stream));
+    CK(cudaStreamSynchronize(plan->stream));
+    if (stats) {
+        memset(stats, 0, sizeof *stats);
+        stats->steps = 1;
+        stats->launches = plan->launches;
+        stats->iters_max = plan->cg.last_iters_max;
+        stats->iters_mean = plan->cg.last_iters_mean;
+        stats->refine_rounds = plan->refine;
+        stats->bad_shift = -1;
+    }
+    return REXI_OK;
+}
+
+int rexi_combine_partials(const double *partials, int32_t g, int64_t n, rexi_c128 *out, void *stream) {
+    rexi_plan *plan = nullptr;
+    CK(launch_combine(partials, g, n, (c128 *)out, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    return REXI_OK;
+}
+
+int rexi_plan_solve(rexi_plan *plan, const rexi_c128 *rhs, rexi_c128 *x, int32_t mem) {
+    if (!plan) return set_err(nullptr, REXI_ERR_INVALID, "null plan");
+    CK(cudaSetDevice(plan->device));
+    const int64_t n = plan->n;
+    cudaStream_t st = plan->stream;
+    c128 *xd = nullptr;
+    c128 *tmp = nullptr;
+    if (mem == REXI_MEM_HOST) {
+        CK(cudaMallocAsync((void **)&tmp, sizeof(c128) * n * plan->k, st));
+        xd = tmp;
+    } else {
+        xd = (c128 *)x;
+    }
+    if (plan->solver == REXI_SOLVER_TRIDIAG) {
+        TriState &T = plan->tri;
+        CK(cudaMemcpyAsync(T.rhs0, rhs, sizeof(c128) * n,
+                           mem == REXI_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+        int rc = tri_chain(plan, nullptr, TRI_OUT_X, 0, nullptr);
+        if (rc) return rc;
+        if (plan->refine > 0) {
+            // refine the per-shift solutions: x += S^-1 (rhs - S x); keep x_hi only
+            CK(tri_launch_residual(T.z, T.lv[0], plan->S, T.rhs0, T.rres, st));
+            c128 *x0 = nullptr;
+            CK(cudaMallocAsync((void **)&x0, sizeof(c128) * n * plan->kp, st));
+            CK(cudaMemcpyAsync(x0, T.lv[0].X, sizeof(c128) * n * plan->kp, cudaMemcpyDeviceToDevice, st));
+            rc = tri_chain(plan, T.rres, TRI_OUT_X, 0, nullptr);
+            if (rc) return rc;
+            CK(cocg_axpy_inplace(T.lv[0].X, x0, (int64_t)n * plan->kp, st));
+            CK(cudaFreeAsync(x0, st));
+        }
+        CK(tri_launch_transpose(T.lv[0].X, n, plan->kp, plan->k, xd, st));
+    } else {
+        int rc = cocg_solve_all(plan->cg, plan->S, st, (const c128 *)rhs, mem == REXI_MEM_HOST, xd, plan->err);
+        if (rc) return set_err(plan, rc, plan->err);
+    }
+    if (mem == REXI_MEM_HOST) {
+        CK(cudaMemcpyAsync(x, xd, sizeof(c128) * n * plan->k, cudaMemcpyDeviceToHost, st));
+        CK(cudaFreeAsync(tmp, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return REXI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,27 @@
+// tridiag_launch.h -- host-callable launchers of the tridiagonal kernels.
+#pragma once
+#include "tridiag.cuh"
+
+namespace rexi {
+
+enum { TRI_OUT_X = 0, TRI_OUT_ACC = 1, TRI_OUT_X_ACC = 2 };
+
+cudaError_t tri_launch_rhs(const L0Dev &z, int64_t n, const c128 *u, c128 *rhs, cudaStream_t st);
+cudaError_t tri_launch_residual(const L0Dev &z, const LevelDev &L, const ShiftDev &S,
+                                const c128 *rhs0, c128 *res, cudaStream_t st);
+cudaError_t tri_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, int level,
+                          const c128 *rhs0, const c128 *rst, const c128 *rin_a,
+                          const c128 *rin_b, cudaStream_t st);
+cudaError_t tri_launch_s3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, int level,
+                          const c128 *rhs0, const c128 *rst, const c128 *rin_a,
+                          const c128 *rin_b, const c128 *Xnext, int out_mode, double *acc,
+                          int acc_add, c128 *uout, cudaStream_t st);
+cudaError_t tri_launch_top_solve(const LevelDev &L, const ShiftDev &S, const c128 *rin_a,
+                                 const c128 *rin_b, cudaStream_t st);
+cudaError_t tri_launch_factor(const L0Dev &z, const LevelDev &L, const LevelDev *next,
+                              const ShiftDev &S, int level, unsigned long long *pmin,
+                              unsigned long long *pmax, cudaStream_t st);
+cudaError_t tri_launch_transpose(const c128 *X, int64_t n, int kp, int k, c128 *out, cudaStream_t st);
+cudaError_t launch_combine(const double *parts, int g, int64_t n, c128 *out, cudaStream_t st);
+
+}  // namespace rexi
