@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""bench.py -- REXI steps/s on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One "step" is one full REXI time step u1 = sum_j beta_j S_j^{-1}(iB u0) over
+the whole workload.  Default workload = BASELINE.json configs[1] (the metric's
+"1M DOF, K=64" case): 1D P1, n = 2^20 nodes (1,048,574 DOF), K = 64, tau = 0.5,
+with the parity-correct setting (one double-double refinement round, which
+brings the GPU result to the truth oracle; the reference's own fp64 path sits
+2.4e-7 away from it).  Synthetic inputs: seeded fixtures (paper_1912_03312_b200/
+fixtures.py), poles frozen from the reference's generator.
+
+N > 1 (torchrun, one rank per GPU): the K shifts are sharded across ranks;
+each step every rank computes its double-double partial sum and one NCCL
+all_gather + fixed-order combine produces u1 on every rank (strong scaling:
+the work per step is fixed).
+
+--impl reference: the reference's CPU algorithm (the C restatement in oracle/
+of zgbtrf/zgbtrs + fl(beta x) + Kahan, all host threads) on the same config;
+rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "REXI steps/s (1M DOF, K=64)"
+UNIT = "steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--refine", type=int, default=-1, help="-1: auto (parity-correct)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps")
+    return ap.parse_args()
+
+
+def workload_name(cfg, refine):
+    n, k = cfg.system.n_dof, cfg.approx.K
+    dims = {1: "1D", 2: "2D", 3: "3D"}[cfg.mesh.d]
+    return (f"{cfg.name}: {dims} P1 Schroedinger REXI step, {n} DOF, nnz {cfg.system.A.nnz}, "
+            f"K={k}, tau={cfg.tau}, refine={refine}")
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons, sampled every 200 ms."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def kernel_bytes(name, n, k):
+    """Algorithmic HBM bytes per launch of the level-0 kernels:
+    16 B per (row, shift) for every per-shift complex array touched, plus the
+    shared per-row inputs: rhs 16 B, 6 coefficient arrays 48 B (A re/im, B of
+    the two off-diagonals), output 16 B or the dd partial 32 B."""
+    per_shift = {"s1_l0": 1, "s3_l0_acc": 1, "s3_l0_xacc": 2, "s3_l0_x": 2, "s1_l0_res": 2,
+                 "s3_l0_res_acc": 2, "residual": 2}
+    shared = {"s1_l0": 16 + 48, "s3_l0_acc": 16 + 48 + 32, "s3_l0_xacc": 16 + 48 + 32,
+              "s3_l0_x": 16 + 48, "s1_l0_res": 48, "s3_l0_res_acc": 48 + 32 + 32,
+              "residual": 16 + 72, "rhs": 16 + 16 + 24}
+    if name == "rhs":
+        return shared["rhs"] * n
+    if name not in per_shift:
+        return None
+    return per_shift[name] * 16 * n * k + shared[name] * n
+
+
+def load_traffic(name):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(name)
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg, steps=2):
+    """The reference algorithm restated in C (oracle/, kind "port"), timed on
+    this host's cores: factor once (not timed), then `steps` full steps."""
+    from oracle.oracle import OraclePlan
+    cores = os.cpu_count() or 1
+    orc = OraclePlan(cfg.system, cfg.approx, cfg.tau, nthreads=cores)
+    u = cfg.u0
+    orc.step(u)                                    # warm
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        u = orc.step(u)
+    dt = time.perf_counter() - t0
+    orc.close()
+    return {"value": steps / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{steps} full {cfg.name} steps (all {cfg.approx.K} shifts, {cfg.system.n_dof} DOF) "
+                      "through oracle/rexi_oracle.c (zgbtf2/zgbtrs restated, fl(beta x), Kahan), "
+                      f"OpenMP over shifts on {cores} threads"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_1912_03312_b200 import fixtures
+    from oracle.oracle import OraclePlan
+    cfg = fixtures.build_config(args.config)
+    cores = os.cpu_count() or 1
+    orc = OraclePlan(cfg.system, cfg.approx, cfg.tau, nthreads=cores)
+    u = cfg.u0
+    for _ in range(args.warmup):
+        u = orc.step(u)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        u = orc.step(u)
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "complex128",
+            "data": "synthetic (seeded fixtures, poles frozen from the reference generator)",
+            "config": {"workload": workload_name(cfg, "n/a (direct LU)"), "parallelism": "host threads"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} full steps, reference algorithm restated in C "
+                                       "(oracle/rexi_oracle.c), OpenMP over shifts"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1912_03312_b200 import fixtures, rexi_prepare, rexi_step
+    from paper_1912_03312_b200.distributed import ShardedStepper
+    from paper_1912_03312_b200 import _native
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = fixtures.build_config(args.config)
+    n, k = cfg.system.n_dof, cfg.approx.K
+    refine = args.refine
+    if refine < 0:
+        refine = 1 if cfg.tau * cfg.sr > 5e3 else 0
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    u0 = torch.from_numpy(cfg.u0).to(f"cuda:{local}")
+    ua = u0.clone()
+    ub = torch.empty_like(u0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    if world == 1:
+        from paper_1912_03312_b200._pattern import shared_pattern
+        ip, ix, ar, ai, br = shared_pattern(cfg.system.A, cfg.system.B)
+        plan = _native.NativePlan(ip, ix, ar, br, cfg.approx.shifts, cfg.approx.weights, cfg.tau,
+                                  a_imag=ai, device=local, refine=refine, stream=sptr)
+
+        def run(nsteps, src, dst):
+            st = _native.RexiStats()
+            plan.step_device(src.data_ptr(), dst.data_ptr(), nsteps, st)
+            return int(st.launches)
+    else:
+        sh = ShardedStepper(cfg.system, cfg.approx, cfg.tau, rank=rank, world=world, device=local,
+                            refine=refine, stream=sptr)
+        plan = sh.plan
+
+        def run(nsteps, src, dst):
+            a, b = src, dst
+            for s in range(nsteps):
+                sh.step(a, b)
+                a, b = b, a
+            if nsteps % 2 == 0:
+                dst.copy_(a)
+            return int(nsteps * 0)  # counted below from the profile pass
+
+    # warm-up
+    run(args.warmup, ua, ub)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        launches = run(args.steps, ua, ub)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        # profiled pass (same K steps): per-kernel device time for the roofline
+        plan.profile(True)
+        run(args.steps, ua, ub)
+        torch.cuda.synchronize()
+        prof = plan.profile_report()
+        plan.profile(False)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches = sum(c for c, _ in prof.values()) if launches == 0 else launches
+    value = args.steps / (ms / 1e3)
+
+    # end-to-end through the public API, host (pinned) buffers, H2D + D2H every step
+    e2e = None
+    if world == 1:
+        stp = rexi_prepare(cfg.system, cfg.approx, cfg.tau, sr_value=cfg.sr,
+                           override_admissibility=True, device=local, refine=refine)
+        pin_in = torch.from_numpy(cfg.u0).pin_memory()
+        u_host = pin_in.numpy()
+        ke = args.e2e_steps or args.steps
+        rexi_step(stp, u_host)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            u_host = rexi_step(stp, u_host)      # H2D of u, one step, D2H of u1
+        dt = time.perf_counter() - t0
+        stp.close()
+        e2e = {"value": ke / dt, "unit": UNIT, "h2d_bytes_per_step": 16 * n,
+               "d2h_bytes_per_step": 16 * n, "api": "paper_1912_03312_b200.rexi_step(numpy)",
+               "timing": "host wall clock around synchronous calls"}
+
+    # roofline of the dominant kernel
+    peak, peak_src = measured_peak()
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
+    roof = None
+    if dom is not None:
+        name, (cnt, tot) = dom
+        kshard = len(sh.shards[rank]) if world > 1 else k
+        b = kernel_bytes(name, n, kshard)
+        avg_ms = tot / max(cnt, 1)
+        ach = (b / (avg_ms / 1e3)) / 1e9 if b else None
+        roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": (ach / peak) if ach else None, "traffic": load_traffic(name),
+                "algorithmic_bytes_per_launch": b, "avg_launch_ms": avg_ms,
+                "share_of_step": tot / sum(t for _, t in prof.values()), "peak_source": peak_src}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                cpu = cpu_baseline(cfg)
+            except Exception as exc:  # the baseline must not kill the bench line
+                cpu = {"error": str(exc)}
+        step_bytes = 80 * n + 32 * k * n
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "complex128",
+            "data": "synthetic (seeded fixtures, poles frozen from the reference generator)",
+            "config": {"workload": workload_name(cfg, refine), "n_dof": n, "K": k, "tau": cfg.tau,
+                       "refine": refine, "parallelism": f"pole-shard x{world}" if world > 1 else "1 GPU",
+                       "l2": "per-shift arrays (1.07 GB/level-0 array) exceed the 126 MB L2"},
+            "e2e": e2e,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "kernels": {kname: {"launches": c, "total_ms": t} for kname, (c, t) in prof.items()},
+            "step_algorithmic_GBps": step_bytes / (ms / args.steps / 1e3) / 1e9,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        sh.close()
+        dist.destroy_process_group()
+    else:
+        plan.close()
+
+
+if __name__ == "__main__":
+    main()

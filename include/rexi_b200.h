@@ -133,6 +133,12 @@ int rexi_combine_partials(const double *partials, int32_t g, int64_t n, rexi_c12
 int rexi_plan_solve(rexi_plan *plan, const rexi_c128 *rhs, rexi_c128 *x, int32_t mem);
 
 int rexi_plan_info(const rexi_plan *plan, rexi_info *info);
+
+/* Per-kernel device-time profiling with CUDA events on the plan's stream
+ * (used by bench.py for the roofline).  enable resets the counters; the
+ * report is text lines "<kernel> <launches> <total_ms>". */
+int rexi_plan_profile(rexi_plan *plan, int32_t enable);
+int rexi_plan_profile_report(rexi_plan *plan, char *buf, int64_t len);
 int rexi_plan_destroy(rexi_plan *plan);
 const char *rexi_plan_last_error(const rexi_plan *plan);
 const char *rexi_last_error(void);

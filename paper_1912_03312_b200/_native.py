@@ -32,7 +32,8 @@ ABI_VERSION = 1
 EXPORTED = (
     "rexi_plan_create", "rexi_plan_step", "rexi_plan_step_partial", "rexi_combine_partials",
     "rexi_plan_solve", "rexi_plan_info", "rexi_plan_destroy", "rexi_plan_last_error",
-    "rexi_last_error", "rexi_device_count", "rexi_abi_version",
+    "rexi_last_error", "rexi_device_count", "rexi_abi_version", "rexi_plan_profile",
+    "rexi_plan_profile_report",
 )
 
 
@@ -113,6 +114,8 @@ def lib():
     L.rexi_last_error.restype = ctypes.c_char_p
     L.rexi_device_count.argtypes = [ctypes.POINTER(ctypes.c_int32)]
     L.rexi_abi_version.restype = ctypes.c_int32
+    L.rexi_plan_profile.argtypes = [vp, ctypes.c_int32]
+    L.rexi_plan_profile_report.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
     if L.rexi_abi_version() != ABI_VERSION:
         raise DeviceError("native library ABI version mismatch")
     _lib = L
@@ -221,6 +224,20 @@ class NativePlan:
         rc = lib().rexi_plan_solve(self._h, _ptr(rhs), _ptr(x), MEM_HOST)
         raise_status(rc, self._err())
         return x
+
+    def profile(self, enable: bool = True):
+        """Per-kernel CUDA-event timing on the plan's stream (resets counters)."""
+        raise_status(lib().rexi_plan_profile(self._h, 1 if enable else 0), self._err())
+
+    def profile_report(self) -> dict:
+        """{kernel: (launches, total_ms)} since the last profile(True)."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        raise_status(lib().rexi_plan_profile_report(self._h, buf, len(buf)), self._err())
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.split()
+            out[name] = (int(cnt), float(ms))
+        return out
 
     def close(self):
         if getattr(self, "_h", None):

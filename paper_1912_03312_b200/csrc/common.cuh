@@ -94,3 +94,45 @@ __device__ __forceinline__ cdd cdd_sub_prod(cdd acc, c128 e, c128 x) {
         cudaError_t _e = (expr);                                                  \
         if (_e != cudaSuccess) return rexi_fail_cuda(plan_for_err, _e, #expr, __FILE__, __LINE__); \
     } while (0)
+
+// ---- TMA bulk copy (cp.async.bulk) + mbarrier helpers (sm_90+/sm_100a) ----
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// global -> shared bulk copy, completion signalled on bar (bytes % 16 == 0, 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// ---- sloppy double-double accumulation of fp64 terms (error-free TwoSum) ----
+struct ddacc { double hi, lo; };
+__device__ __forceinline__ void ddacc_add(ddacc &s, double t) {
+    dd r = two_sum(s.hi, t);
+    s.hi = r.hi;
+    s.lo = __dadd_rn(s.lo, r.lo);
+}

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -52,9 +53,61 @@ struct rexi_plan {
     double min_pivot_ratio = 1.0;
     std::vector<rexi_c128> shifts_host;
     int64_t launches = 0;
+    // optional per-kernel CUDA-event profiling (rexi_plan_profile)
+    bool prof = false;
+    struct Rec { const char *name; cudaEvent_t a, b; };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    std::map<std::string, std::pair<int64_t, double>> prof_acc;
 };
 
 namespace {
+
+cudaEvent_t prof_event(rexi_plan *p) {
+    if (!p->pool.empty()) {
+        cudaEvent_t e = p->pool.back();
+        p->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    rexi_plan *p;
+    const char *name;
+    cudaEvent_t a = nullptr;
+    ProfScope(rexi_plan *p_, const char *n) : p(p_), name(n) {
+        ++p->launches;
+        if (p->prof) {
+            a = prof_event(p);
+            cudaEventRecord(a, p->stream);
+        }
+    }
+    ~ProfScope() {
+        if (p->prof) {
+            cudaEvent_t b = prof_event(p);
+            cudaEventRecord(b, p->stream);
+            p->pending.push_back({name, a, b});
+        }
+    }
+};
+
+void prof_flush(rexi_plan *p) {
+    if (p->pending.empty()) return;
+    cudaStreamSynchronize(p->stream);
+    for (auto &r : p->pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        auto &acc = p->prof_acc[r.name];
+        acc.first += 1;
+        acc.second += ms;
+        p->pool.push_back(r.a);
+        p->pool.push_back(r.b);
+    }
+    p->pending.clear();
+}
 
 int set_err(rexi_plan *p, int code, const std::string &msg) {
     g_last_error = msg;
@@ -167,7 +220,11 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
     }
     DALLOC(T.rhs0, (size_t)n);
     DALLOC(T.acc, (size_t)4 * n);
-    if (plan->refine > 0) DALLOC(T.rres, (size_t)n * kp);
+    if (plan->refine > 0) {
+        DALLOC(T.rres, (size_t)n * kp);
+        DALLOC(T.lv[0].ypdd, (size_t)T.lv[0].P * kp);
+        DALLOC(T.lv[0].lcdd, (size_t)T.lv[0].P * kp);
+    }
 
     // factor every level
     unsigned long long *pmin = nullptr, *pmax = nullptr;
@@ -216,32 +273,99 @@ int tri_chain(rexi_plan *plan, const c128 *rst, int out_mode, int acc_add, c128 
     for (size_t l = 0; l + 1 < nl; ++l) {
         const c128 *ra = l ? T.lv[l - 1].ypart : nullptr;
         const c128 *rb = l ? T.lv[l - 1].lc : nullptr;
+        ProfScope ps(plan, l ? "s1_lv" : (rst ? "s1_l0_res" : "s1_l0"));
         CK(tri_launch_s1(T.z, T.lv[l], plan->S, (int)l, T.rhs0, l ? nullptr : rst, ra, rb, st));
-        ++plan->launches;
     }
-    CK(tri_launch_top_solve(T.lv[nl - 1], plan->S, T.lv[nl - 2].ypart, T.lv[nl - 2].lc, st));
-    ++plan->launches;
+    {
+        ProfScope ps(plan, "top");
+        CK(tri_launch_top_solve(T.lv[nl - 1], plan->S, T.lv[nl - 2].ypart, T.lv[nl - 2].lc, st));
+    }
     for (size_t l = nl - 1; l-- > 0;) {
         const c128 *ra = l ? T.lv[l - 1].ypart : nullptr;
         const c128 *rb = l ? T.lv[l - 1].lc : nullptr;
+        const char *nm = l ? "s3_lv"
+                           : (rst ? "s3_l0_res_acc"
+                                  : (out_mode == TRI_OUT_ACC ? "s3_l0_acc"
+                                                             : (out_mode == TRI_OUT_X ? "s3_l0_x" : "s3_l0_xacc")));
+        ProfScope ps(plan, nm);
         CK(tri_launch_s3(T.z, T.lv[l], plan->S, (int)l, T.rhs0, l ? nullptr : rst, ra, rb,
                          T.lv[l + 1].X, l ? TRI_OUT_X : out_mode, T.acc, acc_add, l ? nullptr : uout,
                          st));
-        ++plan->launches;
     }
+    return REXI_OK;
+}
+
+// levels 1..top (S1 up, top solve, S3 down); level-1 rhs from level 0's
+// ypart/lc, or from its double-double pieces in the correction pass
+int tri_mid(rexi_plan *plan, bool dd) {
+    TriState &T = plan->tri;
+    const size_t nl = T.lv.size();
+    cudaStream_t st = plan->stream;
+    for (size_t l = 1; l + 1 < nl; ++l) {
+        ProfScope ps(plan, "s1_lv");
+        if (l == 1 && dd) CK(tri_launch_lv_dd(T.lv[1], plan->S, 1, T.lv[0].ypdd, T.lv[0].lcdd, nullptr, st));
+        else CK(tri_launch_s1(T.z, T.lv[l], plan->S, (int)l, nullptr, nullptr, T.lv[l - 1].ypart,
+                              T.lv[l - 1].lc, st));
+    }
+    {
+        ProfScope ps(plan, "top");
+        if (nl == 2 && dd) CK(tri_launch_top_solve_dd(T.lv[1], plan->S, T.lv[0].ypdd, T.lv[0].lcdd, st));
+        else CK(tri_launch_top_solve(T.lv[nl - 1], plan->S, T.lv[nl - 2].ypart, T.lv[nl - 2].lc, st));
+    }
+    for (size_t l = nl - 1; l-- > 1;) {
+        ProfScope ps(plan, "s3_lv");
+        if (l == 1 && dd) CK(tri_launch_lv_dd(T.lv[1], plan->S, 3, T.lv[0].ypdd, T.lv[0].lcdd, T.lv[2].X, st));
+        else CK(tri_launch_s3(T.z, T.lv[l], plan->S, (int)l, nullptr, nullptr, T.lv[l - 1].ypart,
+                              T.lv[l - 1].lc, T.lv[l + 1].X, TRI_OUT_X, nullptr, 0, nullptr, st));
+    }
+    return REXI_OK;
+}
+
+// v2 step: TMA-fed level-0 kernels
+int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
+    TriState &T = plan->tri;
+    cudaStream_t st = plan->stream;
+    {
+        ProfScope ps(plan, "rhs");
+        CK(tri_launch_rhs(T.z, T.n, u, T.rhs0, st));
+    }
+    {
+        ProfScope ps(plan, "l0_s1");
+        CK(l0_launch_s1(T.z, T.lv[0], plan->S, T.rhs0, st));
+    }
+    int rc = tri_mid(plan, false);
+    if (rc) return rc;
+    if (plan->refine <= 0) {
+        ProfScope ps(plan, "l0_s3acc");
+        CK(l0_launch_s3acc(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, uout, st));
+        return REXI_OK;
+    }
+    {
+        ProfScope ps(plan, "l0_k2");
+        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres, st));
+    }
+    rc = tri_mid(plan, true);
+    if (rc) return rc;
+    ProfScope ps(plan, "l0_k3");
+    CK(l0_launch_k3(T.z, T.lv[0], plan->S, T.lv[1].X, T.rres, T.acc, uout, st));
     return REXI_OK;
 }
 
 // one step from device u -> (uout rounded) or (T.acc partial when uout == nullptr)
 int tri_step(rexi_plan *plan, const c128 *u, c128 *uout) {
     TriState &T = plan->tri;
-    CK(tri_launch_rhs(T.z, T.n, u, T.rhs0, plan->stream));
-    ++plan->launches;
+    if (l0v2_supported(plan->kp)) return tri_step_v2(plan, u, uout);
+    {
+        ProfScope ps(plan, "rhs");
+        CK(tri_launch_rhs(T.z, T.n, u, T.rhs0, plan->stream));
+    }
     if (plan->refine <= 0) return tri_chain(plan, nullptr, TRI_OUT_ACC, 0, uout);
     int rc = tri_chain(plan, nullptr, TRI_OUT_X_ACC, 0, nullptr);
     if (rc) return rc;
-    CK(tri_launch_residual(T.z, T.lv[0], plan->S, T.rhs0, T.rres, plan->stream));
-    ++plan->launches;
+    {
+        ProfScope ps(plan, "residual");
+        CK(tri_launch_residual(T.z, T.lv[0], plan->S, T.rhs0, T.rres, plan->stream));
+    }
     return tri_chain(plan, T.rres, TRI_OUT_ACC, 1, uout);
 }
 
@@ -280,6 +404,8 @@ int rexi_plan_destroy(rexi_plan *plan) {
     if (plan->stream) cudaStreamSynchronize(plan->stream);
     for (void *p : plan->allocs) cudaFree(p);
     cocg_destroy(plan->cg);
+    for (auto &r : plan->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : plan->pool) cudaEventDestroy(e);
     if (plan->own_stream && plan->stream) cudaStreamDestroy(plan->stream);
     delete plan;
     return REXI_OK;
@@ -410,6 +536,29 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
     return REXI_OK;
 }
 
+int rexi_plan_profile(rexi_plan *plan, int32_t enable) {
+    if (!plan) return set_err(nullptr, REXI_ERR_INVALID, "null plan");
+    prof_flush(plan);
+    plan->prof = enable != 0;
+    plan->prof_acc.clear();
+    return REXI_OK;
+}
+
+int rexi_plan_profile_report(rexi_plan *plan, char *buf, int64_t len) {
+    if (!plan || !buf || len <= 0) return set_err(plan, REXI_ERR_INVALID, "bad arguments");
+    prof_flush(plan);
+    std::string s;
+    char line[256];
+    for (auto &kv : plan->prof_acc) {
+        snprintf(line, sizeof line, "%s %lld %.6f\n", kv.first.c_str(), (long long)kv.second.first,
+                 kv.second.second);
+        s += line;
+    }
+    if ((int64_t)s.size() + 1 > len) return set_err(plan, REXI_ERR_INVALID, "buffer too small");
+    memcpy(buf, s.c_str(), s.size() + 1);
+    return REXI_OK;
+}
+
 int rexi_plan_info(const rexi_plan *plan, rexi_info *info) {
     if (!plan || !info) return set_err(nullptr, REXI_ERR_INVALID, "null argument");
     info->solver = plan->solver;
@@ -473,6 +622,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
         CK(cudaMemcpyAsync(u_out, src, sizeof(c128) * n, cudaMemcpyDeviceToDevice, st));
     }
     CK(cudaStreamSynchronize(st));
+    prof_flush(plan);
     if (stats) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev[0], ev[1]);
@@ -501,6 +651,7 @@ int rexi_plan_step_partial(rexi_plan *plan, const rexi_c128 *u_in, double *parti
     CK(cudaMemcpyAsync(partial, plan->tri.acc, sizeof(double) * 4 * plan->n, cudaMemcpyDeviceToDevice,
                        plan->stream));
     CK(cudaStreamSynchronize(plan->stream));
+    prof_flush(plan);
     if (stats) {
         memset(stats, 0, sizeof *stats);
         stats->steps = 1;

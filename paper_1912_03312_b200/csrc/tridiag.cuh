@@ -28,7 +28,7 @@ namespace rexi {
 
 constexpr int TRI_M = 16;        // block size (rows per block, incl. the interface row)
 constexpr int TRI_THREADS = 256; // CTA size
-constexpr int TOP_MAX = 64;      // direct-solve threshold
+constexpr int TOP_MAX = 1;       // recurse until a single interface row remains
 
 struct L0Dev {
     const double *ta_sub, *ta_sub_im, *b_sub;   // entry (i, i-1); row 0 holds 0
@@ -46,6 +46,7 @@ struct LevelDev {
     c128 *ypart, *lc;               // S1 outputs: next-level rhs = ypart + lc  [P][kp]
     c128 *X;                        // solution  [n][kp]
     c128 *phiF, *phiL, *psiF, *psiL;// factor tips [P][kp]
+    cdd *ypdd, *lcdd;               // refinement (level 0): dd reduced rhs of the correction
 };
 
 struct ShiftDev {

@@ -24,4 +24,21 @@ cudaError_t tri_launch_factor(const L0Dev &z, const LevelDev &L, const LevelDev 
 cudaError_t tri_launch_transpose(const c128 *X, int64_t n, int kp, int k, c128 *out, cudaStream_t st);
 cudaError_t launch_combine(const double *parts, int g, int64_t n, c128 *out, cudaStream_t st);
 
+// levels >= 1 reading the double-double reduced rhs of the correction pass
+cudaError_t tri_launch_lv_dd(const LevelDev &L, const ShiftDev &S, int phase, const cdd *rdd_a,
+                             const cdd *rdd_b, const c128 *Xnext, cudaStream_t st);
+cudaError_t tri_launch_top_solve_dd(const LevelDev &L, const ShiftDev &S, const cdd *rdd_a,
+                                    const cdd *rdd_b, cudaStream_t st);
+
+// TMA-fed level-0 kernels (tridiag_l0.cu)
+bool l0v2_supported(int kp);
+cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
+                         cudaStream_t st);
+cudaError_t l0_launch_s3acc(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
+                            const c128 *X1, double *acc, c128 *uout, cudaStream_t st);
+cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
+                         const c128 *X1, double *acc, c128 *rres, cudaStream_t st);
+cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *X1,
+                         const c128 *rres, double *acc, c128 *uout, cudaStream_t st);
+
 }  // namespace rexi

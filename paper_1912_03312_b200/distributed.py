@@ -1,0 +1,113 @@
+"""Pole-parallel ("time-parallel") REXI across GPUs, one process per GPU.
+
+The reference splits the K shifted solves over a thread pool in contiguous
+chunks and reduces on the coordinating thread in fixed ascending-j order
+(``integrate.py:114-120, 196-198, 215-224``); the paper runs the same split
+over MPI ranks with one reduce per step (``PAPER.md:112-129, 1133-1137``).
+
+Here each rank owns a shard of the shifts (one native plan on its GPU),
+produces the double-double partial sum of its shard, and one collective per
+step -- ``all_gather`` of the (hi, lo) partials over NCCL/NVLink -- is
+followed by a fixed-rank-order double-double combine on every rank.  Because
+the partials are double-double and combined in a fixed order, the result is
+independent of the number of GPUs to ~1e-30 relative (the reference's
+worker-count determinism contract, ``test_integrate.py:268-274``), which a
+plain fp64 ``all_reduce`` would not give (the weights reach 1.7e7 and the
+terms cancel to O(1)).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from ._pattern import shared_pattern
+
+
+def shard_indices(k: int, world: int, cost=None):
+    """Shift indices per rank.
+
+    Without a cost model: contiguous, balanced chunks (``np.array_split``,
+    the reference's chunking, ``integrate.py:117``) -- right for the direct
+    1D solver whose cost is identical per shift.  With per-shift costs
+    (e.g. measured COCG iteration counts): longest-processing-time-first
+    assignment, each rank's list sorted ascending.
+    """
+    if world < 1:
+        raise ValueError(f"world size must be >= 1, got {world}")
+    if cost is None:
+        return [list(map(int, c)) for c in np.array_split(np.arange(k), world)]
+    cost = np.asarray(cost, dtype=float)
+    order = np.argsort(-cost, kind="stable")
+    load = np.zeros(world)
+    out = [[] for _ in range(world)]
+    for j in order:
+        r = int(np.argmin(load))
+        out[r].append(int(j))
+        load[r] += cost[j]
+    return [sorted(o) for o in out]
+
+
+def dd_combine_host(parts: np.ndarray) -> np.ndarray:
+    """Reference (host, numpy) semantics of ``rexi_combine_partials`` for the
+    CPU tests of the multi-rank logic: parts (G, 4, n) -> complex128 (n,)."""
+    def two_sum(a, b):
+        s = a + b
+        bb = s - a
+        return s, (a - (s - bb)) + (b - bb)
+
+    def dd_add(ah, al, bh, bl):
+        sh, sl = two_sum(ah, bh)
+        th, tl = two_sum(al, bl)
+        sl = sl + th
+        s2 = sh + sl
+        sl = sl - (s2 - sh)
+        sh = s2
+        sl = sl + tl
+        s3 = sh + sl
+        return s3, sl - (s3 - sh)
+
+    n = parts.shape[2]
+    rh = np.zeros(n); rl = np.zeros(n); ih = np.zeros(n); il = np.zeros(n)
+    for g in range(parts.shape[0]):
+        rh, rl = dd_add(rh, rl, parts[g, 0], parts[g, 1])
+        ih, il = dd_add(ih, il, parts[g, 2], parts[g, 3])
+    return (rh + rl) + 1j * (ih + il)
+
+
+class ShardedStepper:
+    """This rank's shard of one REXI step.  ``step(u, out)`` takes and writes
+    device tensors (complex128, length n) on this rank's GPU."""
+
+    def __init__(self, sysm, approx, tau, *, rank: int, world: int, device: int,
+                 refine: int = -1, solver: int = _native.SOLVER_AUTO, cost=None, group=None,
+                 stream=None, tol: float = 0.0, max_iters: int = 0):
+        import torch
+        self.rank, self.world, self.group = rank, world, group
+        shifts = np.asarray(approx.shifts, dtype=complex)
+        weights = np.asarray(approx.weights, dtype=complex)
+        self.shards = shard_indices(len(shifts), world, cost)
+        idx = self.shards[rank]
+        indptr, indices, a_re, a_im, b_re = shared_pattern(sysm.A, sysm.B)
+        self.n = int(sysm.n_dof)
+        self.plan = _native.NativePlan(indptr, indices, a_re, b_re, shifts[idx], weights[idx], tau,
+                                       a_imag=a_im, device=device, solver=solver, refine=refine,
+                                       shift_offset=idx[0] if idx else 0, stream=stream, tol=tol,
+                                       max_iters=max_iters)
+        dev = torch.device("cuda", device)
+        self.parts = torch.empty((world, 4, self.n), dtype=torch.float64, device=dev)
+        self.mine = torch.empty((4, self.n), dtype=torch.float64, device=dev)
+        self.stream = stream
+
+    def step(self, u, out):
+        import torch.distributed as dist
+        self.plan.step_partial(u.data_ptr(), self.mine.data_ptr())
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.parts.view(-1), self.mine.view(-1), group=self.group)
+        else:
+            self.parts[0].copy_(self.mine)
+        _native.combine_partials(self.parts.data_ptr(), self.world, self.n, out.data_ptr(),
+                                 self.stream)
+
+    def close(self):
+        self.plan.close()
