@@ -176,17 +176,29 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
     // fl(tau * a) exactly as numpy computes tau*A (integrate.py:171)
     auto scale = [&](std::vector<double> &v) { for (auto &x : v) x = d->tau * x; };
     scale(a_sub); scale(a_dia); scale(a_sup); scale(ai_sub); scale(ai_dia); scale(ai_sup);
+    // TMA-fed level 0: pad to a multiple of the block size with decoupled unit
+    // rows (zero couplings, diagonal 1, rhs 0) so every level-0 block is full
+    int64_t n0 = n;
+    if (l0v2_supported(plan->kp)) {
+        n0 = (n + TRI_M - 1) / TRI_M * TRI_M;
+        for (auto *v : {&a_sub, &a_dia, &a_sup, &ai_sub, &ai_dia, &ai_sup, &b_sub, &b_dia, &b_sup})
+            v->resize(n0, 0.0);
+        for (int64_t r = n; r < n0; ++r) a_dia[r] = 1.0;
+    }
     double *dz[9];
     std::vector<double> *hz[9] = {&a_sub, &ai_sub, &b_sub, &a_dia, &ai_dia, &b_dia, &a_sup, &ai_sup, &b_sup};
+    // padded so that the level-0 kernels' TMA row ranges never leave the allocation
+    const int64_t pad = l0_row_padding();
     for (int q = 0; q < 9; ++q) {
-        DALLOC(dz[q], (size_t)n);
-        CK(cudaMemcpyAsync(dz[q], hz[q]->data(), sizeof(double) * n, cudaMemcpyHostToDevice, plan->stream));
+        DALLOC(dz[q], (size_t)(n0 + pad));
+        CK(cudaMemsetAsync(dz[q], 0, sizeof(double) * (n0 + pad), plan->stream));
+        CK(cudaMemcpyAsync(dz[q], hz[q]->data(), sizeof(double) * n0, cudaMemcpyHostToDevice, plan->stream));
     }
     T.z = L0Dev{dz[0], dz[1], dz[2], dz[3], dz[4], dz[5], dz[6], dz[7], dz[8], dz[2], dz[5], dz[8]};
 
     // levels
     const int kp = plan->kp;
-    int64_t nl = n;
+    int64_t nl = n0;
     for (;;) {
         LevelDev L{};
         L.n = nl;
@@ -218,10 +230,11 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
         if (L.top) break;
         nl = L.P;
     }
-    DALLOC(T.rhs0, (size_t)n);
+    DALLOC(T.rhs0, (size_t)(n0 + pad));
+    CK(cudaMemsetAsync(T.rhs0, 0, sizeof(c128) * (n0 + pad), plan->stream));
     DALLOC(T.acc, (size_t)4 * n);
     if (plan->refine > 0) {
-        DALLOC(T.rres, (size_t)n * kp);
+        DALLOC(T.rres, (size_t)n0 * kp);
         DALLOC(T.lv[0].ypdd, (size_t)T.lv[0].P * kp);
         DALLOC(T.lv[0].lcdd, (size_t)T.lv[0].P * kp);
     }
@@ -337,17 +350,17 @@ int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
     if (rc) return rc;
     if (plan->refine <= 0) {
         ProfScope ps(plan, "l0_s3acc");
-        CK(l0_launch_s3acc(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, uout, st));
+        CK(l0_launch_s3acc(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, uout, T.n, st));
         return REXI_OK;
     }
     {
         ProfScope ps(plan, "l0_k2");
-        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres, st));
+        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres, T.n, st));
     }
     rc = tri_mid(plan, true);
     if (rc) return rc;
     ProfScope ps(plan, "l0_k3");
-    CK(l0_launch_k3(T.z, T.lv[0], plan->S, T.lv[1].X, T.rres, T.acc, uout, st));
+    CK(l0_launch_k3(T.z, T.lv[0], plan->S, T.lv[1].X, T.rres, T.acc, uout, T.n, st));
     return REXI_OK;
 }
 

@@ -1,72 +1,179 @@
-// tridiag_l0.cu -- level-0 kernels of the 1D path, TMA-fed (v2).
+// tridiag_l0.cu -- level-0 kernels of the 1D path, TMA-fed.
 //
-// Every CTA owns a tile of T_r = (L0_NT / kp) * M consecutive rows for all kp
-// shift lanes.  Per-shift arrays are [row][kp], so the tile of the inverse
+// Every CTA owns a tile of T = (L0_NT / kp) * M consecutive rows for all kp
+// shift lanes.  Per-shift arrays are [row][kp], so a CTA's tile of inverse
 // pivots (and of the stored residual) is ONE contiguous range of
-// T_r*kp*16 = L0_NT*M*16 = 32 KB: a single cp.async.bulk (TMA bulk copy)
-// stages it into shared memory, completion on an mbarrier.  Each thread then
-// runs the forward/backward sweeps of one block (M rows) for one shift out of
-// shared memory, so the long dependent row chain no longer serialises HBM
-// loads.  Shared per-row inputs (rhs, the A/B off-diagonals) are broadcast
-// __ldg loads.
+// T*kp*16 = L0_NT*M*16 = 32 KB; the shared per-row inputs (rhs and the A/B
+// diagonals, fl(tau*A) precomputed) are contiguous ranges too.  One thread
+// issues the cp.async.bulk (TMA bulk) copies, completion on one mbarrier;
+// then each thread runs the forward/backward sweeps of one block (M rows) for
+// one shift entirely out of shared memory (no global load inside the
+// dependent row chain).  Full blocks take a predicate-free path.
 //
-// Kernels (refine = 0):  S1 (reduce) ... levels >= 1 ... S3ACC (solve + sum)
-// Kernels (refine = 1):  S1 ... K2 (solve + sum + dd residual + correction
-//                        reduce) ... levels >= 1 ... K3 (correction solve + sum)
+// refine = 0:  S1 (reduce) ... levels >= 1 ... S3ACC (solve + beta-sum)
+// refine = 1:  S1 ... K2 (solve + beta-sum + dd residual + correction reduce)
+//              ... levels >= 1 (correction) ... K3 (correction solve + sum)
 #include "tridiag.cuh"
 #include "tridiag_launch.h"
 
 namespace rexi {
 
-constexpr int L0_NT = 128;    // threads per CTA
+constexpr int L0_NT = 128;      // threads per CTA
+constexpr int L0_ROWPAD = 2;    // extra staged rows (next interface row + 16-B rounding)
 
 struct L0Args {
     L0Dev z;
     LevelDev L;
     ShiftDev S;
-    const c128 *rhs0;     // [n]
+    const c128 *rhs0;     // [n (+pad)]
     const c128 *X1;       // next-level solution [P][kp]
     const c128 *rres_in;  // K3
     c128 *rres_out;       // K2
-    double *acc;          // dd partial SoA 4*n
+    double *acc;          // dd partial SoA 4*nout
     c128 *uout;
+    int64_t nout;         // real n (level 0 is padded to a multiple of M)
     int acc_add;
     int final_out;
 };
 
-struct L0Smem {
-    uint64_t bar;
-    uint64_t pad;
+// shared-memory view of the staged per-row inputs (local row index)
+struct RowView {
+    const c128 *rhs;
+    const double *sr, *si, *sb;   // sub  : fl(tau a), fl(tau a_im), b
+    const double *dr, *di, *db;   // diag
+    const double *ur, *ui, *ub;   // sup
+    __device__ __forceinline__ c128 sub(int lr, c128 sg) const { return form_entry(sr[lr], si[lr], sb[lr], sg); }
+    __device__ __forceinline__ c128 dia(int lr, c128 sg) const { return form_entry(dr[lr], di[lr], db[lr], sg); }
+    __device__ __forceinline__ c128 sup(int lr, c128 sg) const { return form_entry(ur[lr], ui[lr], ub[lr], sg); }
 };
 
-template <int M>
-__device__ __forceinline__ int rows_per_cta(int kp) { return (L0_NT / kp) * M; }
+enum { ST_RHS = 1, ST_DIA = 2, ST_TILE2 = 4 };
 
-// stage nt tiles of per-shift data (rows [row0, row1)) into shared memory
-__device__ __forceinline__ void stage_tiles(uint64_t *bar, c128 *t0, const c128 *g0, c128 *t1,
-                                            const c128 *g1, int64_t row0, int64_t row1, int kp) {
+struct L0Layout {
+    int kp, T, Tp;
+    c128 *t0, *t1;
+    RowView rv;
+};
+
+__device__ __forceinline__ L0Layout carve(unsigned char *smem, int kp, int M, int flags) {
+    L0Layout l;
+    l.kp = kp;
+    l.T = (L0_NT / kp) * M;
+    l.Tp = l.T + L0_ROWPAD;
+    unsigned char *p = smem + 128;
+    l.t0 = reinterpret_cast<c128 *>(p);
+    p += (size_t)l.T * kp * sizeof(c128);
+    l.t1 = nullptr;
+    if (flags & ST_TILE2) {
+        l.t1 = reinterpret_cast<c128 *>(p);
+        p += (size_t)l.T * kp * sizeof(c128);
+    }
+    RowView &r = l.rv;
+    r.rhs = nullptr;
+    if (flags & ST_RHS) {
+        r.rhs = reinterpret_cast<const c128 *>(p);
+        p += (size_t)l.Tp * sizeof(c128);
+    }
+    double *d = reinterpret_cast<double *>(p);
+    r.sr = d; d += l.Tp; r.si = d; d += l.Tp; r.sb = d; d += l.Tp;
+    r.ur = d; d += l.Tp; r.ui = d; d += l.Tp; r.ub = d; d += l.Tp;
+    r.dr = r.di = r.db = nullptr;
+    if (flags & ST_DIA) { r.dr = d; d += l.Tp; r.di = d; d += l.Tp; r.db = d; d += l.Tp; }
+    return l;
+}
+
+__host__ __device__ inline size_t l0_smem_bytes(int kp, int M, int flags) {
+    size_t T = (size_t)(L0_NT / kp) * M, Tp = T + L0_ROWPAD;
+    size_t b = 128 + T * kp * 16 * ((flags & ST_TILE2) ? 2 : 1);
+    if (flags & ST_RHS) b += Tp * 16;
+    b += Tp * 8 * ((flags & ST_DIA) ? 9 : 6);
+    return b;
+}
+
+// one thread: init the mbarrier, then issue every bulk copy of this CTA
+__device__ __forceinline__ void l0_stage(unsigned char *smem, const L0Layout &l, const L0Args &a,
+                                         const c128 *g_t0, const c128 *g_t1, int64_t row0, int flags) {
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint32_t bytes = (uint32_t)((row1 - row0) * kp * sizeof(c128));
-        mbar_expect_tx(bar, g1 ? 2 * bytes : bytes);
-        bulk_g2s(t0, g0 + row0 * kp, bytes, bar);
-        if (g1) bulk_g2s(t1, g1 + row0 * kp, bytes, bar);
+        const int64_t n = a.L.n;
+        const int64_t row1 = min(row0 + (int64_t)l.T, n);
+        const uint32_t tb = (uint32_t)((row1 - row0) * l.kp * sizeof(c128));
+        const uint32_t rb8 = (uint32_t)(l.Tp * 8), rb16 = (uint32_t)(l.Tp * 16);
+        uint32_t total = tb * ((flags & ST_TILE2) ? 2 : 1) + ((flags & ST_RHS) ? rb16 : 0) +
+                         rb8 * ((flags & ST_DIA) ? 9 : 6);
+        mbar_expect_tx(bar, total);
+        bulk_g2s(l.t0, g_t0 + row0 * l.kp, tb, bar);
+        if (flags & ST_TILE2) bulk_g2s(l.t1, g_t1 + row0 * l.kp, tb, bar);
+        if (flags & ST_RHS) bulk_g2s((void *)l.rv.rhs, a.rhs0 + row0, rb16, bar);
+        bulk_g2s((void *)l.rv.sr, a.z.ta_sub + row0, rb8, bar);
+        bulk_g2s((void *)l.rv.si, a.z.ta_sub_im + row0, rb8, bar);
+        bulk_g2s((void *)l.rv.sb, a.z.b_sub + row0, rb8, bar);
+        bulk_g2s((void *)l.rv.ur, a.z.ta_sup + row0, rb8, bar);
+        bulk_g2s((void *)l.rv.ui, a.z.ta_sup_im + row0, rb8, bar);
+        bulk_g2s((void *)l.rv.ub, a.z.b_sup + row0, rb8, bar);
+        if (flags & ST_DIA) {
+            bulk_g2s((void *)l.rv.dr, a.z.ta_dia + row0, rb8, bar);
+            bulk_g2s((void *)l.rv.di, a.z.ta_dia_im + row0, rb8, bar);
+            bulk_g2s((void *)l.rv.db, a.z.b_dia + row0, rb8, bar);
+        }
     }
 }
 
-// beta-weighted sum over the kp shift lanes of every tile row, fixed order,
-// fp64 products accumulated with error-free TwoSum; writes acc or uout
+// forward sweep y_q = invd_q (d_q - a_q y_{q-1}), y[0] = left halo
+template <int M, bool FULL, typename RhsF>
+__device__ __forceinline__ void sweep_fwd(c128 (&y)[M], const c128 *ti, int kp, const RowView &rv,
+                                          int lr0, int cnt, c128 sg, RhsF rhs) {
+#pragma unroll
+    for (int q = 1; q < M; ++q) {
+        if (FULL || q <= cnt) {
+            const int lr = lr0 + q;
+            y[q] = cmul(ti[q * kp], cfnma(rhs(q), rv.sub(lr, sg), y[q - 1]));
+        }
+    }
+}
+
+// backward sweep x_q = y_q - invd_q (c_q x_{q+1}), x_{cnt+1} = xn; out(q, x_q)
+template <int M, bool FULL, typename OutF>
+__device__ __forceinline__ void sweep_bwd(c128 (&y)[M], const c128 *ti, int kp, const RowView &rv,
+                                          int lr0, int cnt, c128 sg, c128 xn, OutF out) {
+    c128 xnext = xn;
+#pragma unroll
+    for (int q = M - 1; q >= 1; --q) {
+        if (FULL || q <= cnt) {
+            const int lr = lr0 + q;
+            xnext = cfnma(y[q], ti[q * kp], cmul(rv.sup(lr, sg), xnext));
+            y[q] = xnext;
+            out(q, xnext);
+        } else {
+            out(q, cmk(0.0, 0.0));
+        }
+    }
+}
+
+template <int M, bool FULL>
+__device__ __forceinline__ c128 pick_last(const c128 (&y)[M], int cnt) {
+    if (FULL) return y[M - 1];
+    c128 v = y[0];
+#pragma unroll
+    for (int q = 1; q < M; ++q)
+        if (q == cnt) v = y[q];
+    return v;
+}
+
+// beta-weighted sum over the kp lanes of every tile row (fixed order, fp64
+// products accumulated with error-free TwoSum, lanes combined in dd)
 template <int M>
 __device__ __forceinline__ void reduce_rows(const c128 *tile, const L0Args &a, int64_t row0) {
     const int kp = a.S.kp;
-    const int rows = rows_per_cta<M>(kp);
+    const int rows = (L0_NT / kp) * M;
     const int tpr = L0_NT / rows > 0 ? L0_NT / rows : 1;
     const int sub = threadIdx.x % tpr;
-    const int64_t n = a.L.n;
+    const int64_t n = a.nout;
     for (int r = threadIdx.x / tpr; r < rows; r += L0_NT / tpr) {
         ddacc re = {0.0, 0.0}, im = {0.0, 0.0};
         for (int jj = sub; jj < kp; jj += tpr) {
@@ -103,7 +210,7 @@ __device__ __forceinline__ void reduce_rows(const c128 *tile, const L0Args &a, i
     }
 }
 
-// error-free accumulation of -e*x into a complex double-double (Dot2 style)
+// acc -= e*x, error-free (Dot2 style) into complex double-double accumulators
 __device__ __forceinline__ void dot2_sub(ddacc &re, ddacc &im, c128 e, c128 x) {
     dd p;
     p = two_prod(e.x, x.x); ddacc_add(re, -p.hi); re.lo = __dsub_rn(re.lo, p.lo);
@@ -112,331 +219,252 @@ __device__ __forceinline__ void dot2_sub(ddacc &re, ddacc &im, c128 e, c128 x) {
     p = two_prod(e.y, x.x); ddacc_add(im, -p.hi); im.lo = __dsub_rn(im.lo, p.lo);
 }
 
+struct Ctx {
+    int kp, b, j, cnt, lr0;
+    int64_t p, P, base, row0;
+    bool active;
+    c128 sg;
+};
+
+__device__ __forceinline__ Ctx make_ctx(const L0Args &a, int M) {
+    Ctx c;
+    c.kp = a.S.kp;
+    const int bpc = L0_NT / c.kp;
+    c.b = threadIdx.x / c.kp;
+    c.j = threadIdx.x % c.kp;
+    c.P = a.L.P;
+    c.row0 = (int64_t)blockIdx.x * bpc * M;
+    c.p = (int64_t)blockIdx.x * bpc + c.b;
+    c.active = c.p < c.P;
+    c.base = c.p * M;
+    c.cnt = c.active ? (int)min((int64_t)M, a.L.n - c.base) - 1 : -1;
+    c.lr0 = c.b * M;
+    c.sg = a.S.sigma[c.j];
+    return c;
+}
+
+// Level 0 is padded to a multiple of M (decoupled unit rows), so every
+// level-0 block is full and only the predicate-free instantiations exist.
+
 // ---------------------------------------------------------------------------
 // S1: interior solves with zero halos -> reduced rhs (ypart, lc)
 // ---------------------------------------------------------------------------
-template <int M>
-__global__ void __launch_bounds__(L0_NT) k_l0_s1(L0Args a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    L0Smem *sm = reinterpret_cast<L0Smem *>(smem_raw);
-    c128 *tinv = reinterpret_cast<c128 *>(smem_raw + 128);
-    const int kp = a.S.kp;
-    const int bpc = L0_NT / kp;
-    const int b = threadIdx.x / kp, j = threadIdx.x % kp;
-    const int64_t n = a.L.n, P = a.L.P;
-    const int64_t row0 = (int64_t)blockIdx.x * bpc * M;
-    const int64_t row1 = min(row0 + (int64_t)bpc * M, n);
-    stage_tiles(&sm->bar, tinv, a.L.invd, nullptr, nullptr, row0, row1, kp);
-    const int64_t p = (int64_t)blockIdx.x * bpc + b;
-    const bool active = p < P;
-    const int64_t base = p * M;
-    const int cnt = active ? (int)min((int64_t)M, n - base) - 1 : -1;
-    const c128 sg = a.S.sigma[j];
-    const c128 *ti = tinv + (size_t)b * M * kp + j;
-    mbar_wait(&sm->bar, 0);
-    if (!active) return;
-
+template <int M, bool FULL>
+__device__ __forceinline__ void s1_body(const L0Args &a, const L0Layout &l, const Ctx &c) {
+    const c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
+    const RowView &rv = l.rv;
     c128 y[M];
     y[0] = cmk(0.0, 0.0);
-#pragma unroll
-    for (int q = 1; q < M; ++q) {
-        y[q] = cmk(0.0, 0.0);
-        if (q <= cnt) {
-            const int64_t i = base + q;
-            const c128 ai = form_entry(__ldg(a.z.ta_sub + i), __ldg(a.z.ta_sub_im + i), __ldg(a.z.b_sub + i), sg);
-            y[q] = cmul(ti[q * kp], cfnma(a.rhs0[i], ai, y[q - 1]));
-        }
-    }
-    c128 ylast = y[0];
-#pragma unroll
-    for (int q = 1; q < M; ++q)
-        if (q == cnt) ylast = y[q];
-    c128 xnext = cmk(0.0, 0.0);
-#pragma unroll
-    for (int q = M - 1; q >= 1; --q) {
-        if (q <= cnt) {
-            const int64_t i = base + q;
-            const c128 ci = form_entry(__ldg(a.z.ta_sup + i), __ldg(a.z.ta_sup_im + i), __ldg(a.z.b_sup + i), sg);
-            xnext = cfnma(y[q], ti[q * kp], cmul(ci, xnext));
-            y[q] = xnext;
-        }
-    }
-    const c128 yfirst = cnt >= 1 ? y[1] : cmk(0.0, 0.0);
-    const c128 cs = form_entry(__ldg(a.z.ta_sup + base), __ldg(a.z.ta_sup_im + base), __ldg(a.z.b_sup + base), sg);
-    a.L.ypart[p * kp + j] = cfnma(a.rhs0[base], cs, yfirst);
-    if (p + 1 < P) {
-        const int64_t s1 = base + M;
-        const c128 an = form_entry(__ldg(a.z.ta_sub + s1), __ldg(a.z.ta_sub_im + s1), __ldg(a.z.b_sub + s1), sg);
-        a.L.lc[(p + 1) * kp + j] = cneg(cmul(an, ylast));
-    }
-    if (p == 0) a.L.lc[j] = cmk(0.0, 0.0);
+    sweep_fwd<M, FULL>(y, ti, c.kp, rv, c.lr0, c.cnt, c.sg, [&](int q) { return rv.rhs[c.lr0 + q]; });
+    const c128 ylast = pick_last<M, FULL>(y, c.cnt);
+    sweep_bwd<M, FULL>(y, ti, c.kp, rv, c.lr0, c.cnt, c.sg, cmk(0.0, 0.0), [](int, c128) {});
+    const c128 yfirst = c.cnt >= 1 ? y[1] : cmk(0.0, 0.0);
+    const int kp = c.kp, j = c.j;
+    a.L.ypart[c.p * kp + j] = cfnma(rv.rhs[c.lr0], rv.sup(c.lr0, c.sg), yfirst);
+    if (c.p + 1 < c.P) a.L.lc[(c.p + 1) * kp + j] = cneg(cmul(rv.sub(c.lr0 + M, c.sg), ylast));
+    if (c.p == 0) a.L.lc[j] = cmk(0.0, 0.0);
+}
+
+template <int M>
+__global__ void __launch_bounds__(L0_NT, 3) k_l0_s1(L0Args a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const L0Layout l = carve(smem, a.S.kp, M, ST_RHS);
+    const Ctx c = make_ctx(a, M);
+    l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, ST_RHS);
+    mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
+    if (!c.active) return;
+    s1_body<M, true>(a, l, c);
 }
 
 // ---------------------------------------------------------------------------
-// S3ACC: solve with the interface values known, beta-weighted sum -> out
+// S3ACC: solve with known interface values, beta-weighted sum -> out
 // ---------------------------------------------------------------------------
+template <int M, bool FULL>
+__device__ __forceinline__ void s3_body(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
+                                        c128 xn) {
+    c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
+    const RowView &rv = l.rv;
+    const int kp = c.kp;
+    c128 y[M];
+    y[0] = xs;
+    sweep_fwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, [&](int q) { return rv.rhs[c.lr0 + q]; });
+    // x overwrites the consumed inverse pivot of its own lane
+    sweep_bwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, xn, [&](int q, c128 x) { ti[q * kp] = x; });
+    ti[0] = xs;
+}
+
 template <int M>
-__global__ void __launch_bounds__(L0_NT) k_l0_s3acc(L0Args a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    L0Smem *sm = reinterpret_cast<L0Smem *>(smem_raw);
-    c128 *tinv = reinterpret_cast<c128 *>(smem_raw + 128);
-    const int kp = a.S.kp;
-    const int bpc = L0_NT / kp;
-    const int b = threadIdx.x / kp, j = threadIdx.x % kp;
-    const int64_t n = a.L.n, P = a.L.P;
-    const int64_t row0 = (int64_t)blockIdx.x * bpc * M;
-    const int64_t row1 = min(row0 + (int64_t)bpc * M, n);
-    stage_tiles(&sm->bar, tinv, a.L.invd, nullptr, nullptr, row0, row1, kp);
-    const int64_t p = (int64_t)blockIdx.x * bpc + b;
-    const bool active = p < P;
-    const int64_t base = p * M;
-    const int cnt = active ? (int)min((int64_t)M, n - base) - 1 : -1;
-    const c128 sg = a.S.sigma[j];
-    c128 *ti = tinv + (size_t)b * M * kp + j;
+__global__ void __launch_bounds__(L0_NT, 4) k_l0_s3acc(L0Args a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const L0Layout l = carve(smem, a.S.kp, M, ST_RHS);
+    const Ctx c = make_ctx(a, M);
+    l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, ST_RHS);
     c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
-    if (active) {
-        xs = a.X1[p * kp + j];
-        if (p + 1 < P) xn = a.X1[(p + 1) * kp + j];
+    if (c.active) {
+        xs = a.X1[c.p * c.kp + c.j];
+        if (c.p + 1 < c.P) xn = a.X1[(c.p + 1) * c.kp + c.j];
     }
-    mbar_wait(&sm->bar, 0);
-    if (active) {
-        c128 y[M];
-        y[0] = xs;
-#pragma unroll
-        for (int q = 1; q < M; ++q) {
-            y[q] = cmk(0.0, 0.0);
-            if (q <= cnt) {
-                const int64_t i = base + q;
-                const c128 ai = form_entry(__ldg(a.z.ta_sub + i), __ldg(a.z.ta_sub_im + i), __ldg(a.z.b_sub + i), sg);
-                y[q] = cmul(ti[q * kp], cfnma(a.rhs0[i], ai, y[q - 1]));
-            }
-        }
-        c128 xnext = xn;
-#pragma unroll
-        for (int q = M - 1; q >= 1; --q) {
-            c128 v = cmk(0.0, 0.0);
-            if (q <= cnt) {
-                const int64_t i = base + q;
-                const c128 ci = form_entry(__ldg(a.z.ta_sup + i), __ldg(a.z.ta_sup_im + i), __ldg(a.z.b_sup + i), sg);
-                xnext = cfnma(y[q], ti[q * kp], cmul(ci, xnext));
-                v = xnext;
-            }
-            ti[q * kp] = v;                // x overwrites the consumed inverse pivot
-        }
-        ti[0] = xs;                        // interface row
+    mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
+    if (c.active) {
+        s3_body<M, true>(a, l, c, xs, xn);
     } else {
+        c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
 #pragma unroll
-        for (int q = 0; q < M; ++q) ti[q * kp] = cmk(0.0, 0.0);
+        for (int q = 0; q < M; ++q) ti[q * c.kp] = cmk(0.0, 0.0);
     }
     __syncthreads();
-    reduce_rows<M>(tinv, a, row0);
+    reduce_rows<M>(l.t0, a, c.row0);
 }
 
 // ---------------------------------------------------------------------------
 // K2 (refine): S3 + sum(beta x) + dd residual of the interior rows + the
-// correction's reduce (dd interface pieces, so the residual at interface rows
-// is formed exactly from the two blocks that own its terms)
+// correction's reduce.  The residual of an interface row has one term from
+// each of two blocks; both halves are kept in double-double and combined by
+// the next level, so it is formed as exactly as the interior residuals.
 // ---------------------------------------------------------------------------
-template <int M>
-__global__ void __launch_bounds__(L0_NT) k_l0_k2(L0Args a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    L0Smem *sm = reinterpret_cast<L0Smem *>(smem_raw);
-    const int kp = a.S.kp;
-    const int bpc = L0_NT / kp;
-    c128 *tinv = reinterpret_cast<c128 *>(smem_raw + 128);
-    c128 *tx = tinv + (size_t)bpc * M * kp;
-    const int b = threadIdx.x / kp, j = threadIdx.x % kp;
-    const int64_t n = a.L.n, P = a.L.P;
-    const int64_t row0 = (int64_t)blockIdx.x * bpc * M;
-    const int64_t row1 = min(row0 + (int64_t)bpc * M, n);
-    stage_tiles(&sm->bar, tinv, a.L.invd, nullptr, nullptr, row0, row1, kp);
-    const int64_t p = (int64_t)blockIdx.x * bpc + b;
-    const bool active = p < P;
-    const int64_t base = p * M;
-    const int cnt = active ? (int)min((int64_t)M, n - base) - 1 : -1;
-    const c128 sg = a.S.sigma[j];
-    const c128 *ti = tinv + (size_t)b * M * kp + j;
-    c128 *tc = tx + (size_t)b * M * kp + j;
-    c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
-    if (active) {
-        xs = a.X1[p * kp + j];
-        if (p + 1 < P) xn = a.X1[(p + 1) * kp + j];
-    }
-    mbar_wait(&sm->bar, 0);
-    c128 y[M];
-    if (active) {
-        y[0] = xs;
-#pragma unroll
-        for (int q = 1; q < M; ++q) {
-            y[q] = cmk(0.0, 0.0);
-            if (q <= cnt) {
-                const int64_t i = base + q;
-                const c128 ai = form_entry(__ldg(a.z.ta_sub + i), __ldg(a.z.ta_sub_im + i), __ldg(a.z.b_sub + i), sg);
-                y[q] = cmul(ti[q * kp], cfnma(a.rhs0[i], ai, y[q - 1]));
-            }
-        }
-        c128 xnext = xn;
-#pragma unroll
-        for (int q = M - 1; q >= 1; --q) {
-            c128 v = cmk(0.0, 0.0);
-            if (q <= cnt) {
-                const int64_t i = base + q;
-                const c128 ci = form_entry(__ldg(a.z.ta_sup + i), __ldg(a.z.ta_sup_im + i), __ldg(a.z.b_sup + i), sg);
-                xnext = cfnma(y[q], ti[q * kp], cmul(ci, xnext));
-                v = xnext;
-            }
-            tc[q * kp] = v;
-        }
-        tc[0] = xs;
-    } else {
-#pragma unroll
-        for (int q = 0; q < M; ++q) tc[q * kp] = cmk(0.0, 0.0);
-    }
-    __syncthreads();
-    reduce_rows<M>(tx, a, row0);
-    if (!active) return;
+template <int M, bool FULL>
+__device__ __forceinline__ void k2_solve(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
+                                         c128 xn, c128 (&y)[M]) {
+    const c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
+    c128 *tc = l.t1 + (size_t)c.lr0 * c.kp + c.j;
+    const RowView &rv = l.rv;
+    const int kp = c.kp;
+    y[0] = xs;
+    sweep_fwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, [&](int q) { return rv.rhs[c.lr0 + q]; });
+    sweep_bwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, xn, [&](int q, c128 x) { tc[q * kp] = x; });
+    tc[0] = xs;
+}
 
-    // residual r_q = d_q - a_q x_{q-1} - b_q x_q - c_q x_{q+1}, interior rows
+template <int M, bool FULL>
+__device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
+                                          c128 xn, c128 (&y)[M]) {
+    const c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
+    const c128 *tc = l.t1 + (size_t)c.lr0 * c.kp + c.j;
+    const RowView &rv = l.rv;
+    const int kp = c.kp, j = c.j;
+    const int cnt = FULL ? M - 1 : c.cnt;
+    // interior residuals r_q = d_q - a_q x_{q-1} - b_q x_q - c_q x_{q+1}
 #pragma unroll
     for (int q = 1; q < M; ++q) {
-        if (q <= cnt) {
-            const int64_t i = base + q;
-            const c128 d = a.rhs0[i];
-            const c128 xm = tc[(q - 1) * kp];
-            const c128 x0 = tc[q * kp];
+        if (FULL || q <= cnt) {
+            const int lr = c.lr0 + q;
+            const c128 d = rv.rhs[lr];
             const c128 xp = q < cnt ? tc[(q + 1) * kp] : xn;
             ddacc re = {d.x, 0.0}, im = {d.y, 0.0};
-            dot2_sub(re, im, form_entry(__ldg(a.z.ta_sub + i), __ldg(a.z.ta_sub_im + i), __ldg(a.z.b_sub + i), sg), xm);
-            dot2_sub(re, im, form_entry(__ldg(a.z.ta_dia + i), __ldg(a.z.ta_dia_im + i), __ldg(a.z.b_dia + i), sg), x0);
-            dot2_sub(re, im, form_entry(__ldg(a.z.ta_sup + i), __ldg(a.z.ta_sup_im + i), __ldg(a.z.b_sup + i), sg), xp);
+            dot2_sub(re, im, rv.sub(lr, c.sg), tc[(q - 1) * kp]);
+            dot2_sub(re, im, rv.dia(lr, c.sg), tc[q * kp]);
+            dot2_sub(re, im, rv.sup(lr, c.sg), xp);
             const c128 r = cmk(__dadd_rn(re.hi, re.lo), __dadd_rn(im.hi, im.lo));
-            a.rres_out[i * kp + j] = r;
+            a.rres_out[(c.base + q) * kp + j] = r;
             y[q] = r;
         }
     }
-    // interface pieces (double-double, combined by the next level)
+    // interface row: d_s - b_s x_s - c_s x_{s+1} (the -a_s x_{s-1} half comes from block p-1)
     ddacc p1re, p1im;
     {
-        const c128 d = a.rhs0[base];
+        const c128 d = rv.rhs[c.lr0];
         p1re = {d.x, 0.0};
         p1im = {d.y, 0.0};
-        dot2_sub(p1re, p1im, form_entry(__ldg(a.z.ta_dia + base), __ldg(a.z.ta_dia_im + base), __ldg(a.z.b_dia + base), sg), xs);
-        const c128 x1 = cnt >= 1 ? tc[kp] : xn;
-        dot2_sub(p1re, p1im, form_entry(__ldg(a.z.ta_sup + base), __ldg(a.z.ta_sup_im + base), __ldg(a.z.b_sup + base), sg), x1);
+        dot2_sub(p1re, p1im, rv.dia(c.lr0, c.sg), xs);
+        dot2_sub(p1re, p1im, rv.sup(c.lr0, c.sg), cnt >= 1 ? tc[kp] : xn);
     }
-    // correction reduce: S1 with rhs = r
+    // correction reduce: S1 with rhs = r, in place (r_q is read before y_q is written)
     y[0] = cmk(0.0, 0.0);
-#pragma unroll
-    for (int q = 1; q < M; ++q) {
-        if (q <= cnt) {
-            const int64_t i = base + q;
-            const c128 ai = form_entry(__ldg(a.z.ta_sub + i), __ldg(a.z.ta_sub_im + i), __ldg(a.z.b_sub + i), sg);
-            y[q] = cmul(ti[q * kp], cfnma(y[q], ai, y[q - 1]));
-        }
-    }
-    c128 ylast = y[0];
-#pragma unroll
-    for (int q = 1; q < M; ++q)
-        if (q == cnt) ylast = y[q];
-    c128 xnext = cmk(0.0, 0.0);
-#pragma unroll
-    for (int q = M - 1; q >= 1; --q) {
-        if (q <= cnt) {
-            const int64_t i = base + q;
-            const c128 ci = form_entry(__ldg(a.z.ta_sup + i), __ldg(a.z.ta_sup_im + i), __ldg(a.z.b_sup + i), sg);
-            xnext = cfnma(y[q], ti[q * kp], cmul(ci, xnext));
-            y[q] = xnext;
-        }
-    }
+    sweep_fwd<M, FULL>(y, ti, kp, rv, c.lr0, cnt, c.sg, [&](int q) { return y[q]; });
+    const c128 ylast = pick_last<M, FULL>(y, cnt);
+    sweep_bwd<M, FULL>(y, ti, kp, rv, c.lr0, cnt, c.sg, cmk(0.0, 0.0), [](int, c128) {});
     const c128 yfirst = cnt >= 1 ? y[1] : cmk(0.0, 0.0);
-    const c128 cs = form_entry(__ldg(a.z.ta_sup + base), __ldg(a.z.ta_sup_im + base), __ldg(a.z.b_sup + base), sg);
-    const c128 t1 = cneg(cmul(cs, yfirst));
+    const c128 t1 = cneg(cmul(rv.sup(c.lr0, c.sg), yfirst));
     ddacc_add(p1re, t1.x);
     ddacc_add(p1im, t1.y);
-    a.L.ypdd[p * kp + j] = cdd{{p1re.hi, p1re.lo}, {p1im.hi, p1im.lo}};
-    if (p + 1 < P) {
-        const int64_t s1 = base + M;
-        const c128 an = form_entry(__ldg(a.z.ta_sub + s1), __ldg(a.z.ta_sub_im + s1), __ldg(a.z.b_sub + s1), sg);
-        const c128 xl = cnt >= 1 ? tc[cnt * kp] : xs;
+    a.L.ypdd[c.p * kp + j] = cdd{{p1re.hi, p1re.lo}, {p1im.hi, p1im.lo}};
+    if (c.p + 1 < c.P) {
+        const c128 an = rv.sub(c.lr0 + M, c.sg);
         ddacc p2re = {0.0, 0.0}, p2im = {0.0, 0.0};
-        dot2_sub(p2re, p2im, an, xl);
+        dot2_sub(p2re, p2im, an, cnt >= 1 ? tc[cnt * kp] : xs);
         const c128 t2 = cneg(cmul(an, ylast));
         ddacc_add(p2re, t2.x);
         ddacc_add(p2im, t2.y);
-        a.L.lcdd[(p + 1) * kp + j] = cdd{{p2re.hi, p2re.lo}, {p2im.hi, p2im.lo}};
+        a.L.lcdd[(c.p + 1) * kp + j] = cdd{{p2re.hi, p2re.lo}, {p2im.hi, p2im.lo}};
     }
-    if (p == 0) a.L.lcdd[j] = cdd_zero();
+    if (c.p == 0) a.L.lcdd[j] = cdd_zero();
+}
+
+template <int M>
+__global__ void __launch_bounds__(L0_NT, 2) k_l0_k2(L0Args a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int flags = ST_RHS | ST_DIA | ST_TILE2;
+    const L0Layout l = carve(smem, a.S.kp, M, flags);
+    const Ctx c = make_ctx(a, M);
+    l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, flags & ~ST_TILE2);
+    c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
+    if (c.active) {
+        xs = a.X1[c.p * c.kp + c.j];
+        if (c.p + 1 < c.P) xn = a.X1[(c.p + 1) * c.kp + c.j];
+    }
+    mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
+    c128 y[M];
+    if (c.active) {
+        k2_solve<M, true>(a, l, c, xs, xn, y);
+    } else {
+        c128 *tc = l.t1 + (size_t)c.lr0 * c.kp + c.j;
+#pragma unroll
+        for (int q = 0; q < M; ++q) tc[q * c.kp] = cmk(0.0, 0.0);
+    }
+    __syncthreads();
+    reduce_rows<M>(l.t1, a, c.row0);
+    if (!c.active) return;
+    k2_refine<M, true>(a, l, c, xs, xn, y);
 }
 
 // ---------------------------------------------------------------------------
-// K3 (refine): correction solve with the stored residual, sum(beta dx) += acc
+// K3 (refine): correction solve from the stored residual, acc += sum(beta dx)
 // ---------------------------------------------------------------------------
+template <int M, bool FULL>
+__device__ __forceinline__ void k3_body(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
+                                        c128 xn) {
+    const c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
+    c128 *tr = l.t1 + (size_t)c.lr0 * c.kp + c.j;
+    const RowView &rv = l.rv;
+    const int kp = c.kp;
+    c128 y[M];
+    y[0] = xs;
+    sweep_fwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, [&](int q) { return tr[q * kp]; });
+    sweep_bwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, xn, [&](int q, c128 x) { tr[q * kp] = x; });
+    tr[0] = xs;
+}
+
 template <int M>
-__global__ void __launch_bounds__(L0_NT) k_l0_k3(L0Args a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    L0Smem *sm = reinterpret_cast<L0Smem *>(smem_raw);
-    const int kp = a.S.kp;
-    const int bpc = L0_NT / kp;
-    c128 *tinv = reinterpret_cast<c128 *>(smem_raw + 128);
-    c128 *tr = tinv + (size_t)bpc * M * kp;
-    const int b = threadIdx.x / kp, j = threadIdx.x % kp;
-    const int64_t n = a.L.n, P = a.L.P;
-    const int64_t row0 = (int64_t)blockIdx.x * bpc * M;
-    const int64_t row1 = min(row0 + (int64_t)bpc * M, n);
-    stage_tiles(&sm->bar, tinv, a.L.invd, tr, a.rres_in, row0, row1, kp);
-    const int64_t p = (int64_t)blockIdx.x * bpc + b;
-    const bool active = p < P;
-    const int64_t base = p * M;
-    const int cnt = active ? (int)min((int64_t)M, n - base) - 1 : -1;
-    const c128 sg = a.S.sigma[j];
-    const c128 *ti = tinv + (size_t)b * M * kp + j;
-    c128 *tc = tr + (size_t)b * M * kp + j;
+__global__ void __launch_bounds__(L0_NT, 4) k_l0_k3(L0Args a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int flags = ST_TILE2;
+    const L0Layout l = carve(smem, a.S.kp, M, flags);
+    const Ctx c = make_ctx(a, M);
+    l0_stage(smem, l, a, a.L.invd, a.rres_in, c.row0, flags);
     c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
-    if (active) {
-        xs = a.X1[p * kp + j];
-        if (p + 1 < P) xn = a.X1[(p + 1) * kp + j];
+    if (c.active) {
+        xs = a.X1[c.p * c.kp + c.j];
+        if (c.p + 1 < c.P) xn = a.X1[(c.p + 1) * c.kp + c.j];
     }
-    mbar_wait(&sm->bar, 0);
-    if (active) {
-        c128 y[M];
-        y[0] = xs;
-#pragma unroll
-        for (int q = 1; q < M; ++q) {
-            y[q] = cmk(0.0, 0.0);
-            if (q <= cnt) {
-                const int64_t i = base + q;
-                const c128 ai = form_entry(__ldg(a.z.ta_sub + i), __ldg(a.z.ta_sub_im + i), __ldg(a.z.b_sub + i), sg);
-                y[q] = cmul(ti[q * kp], cfnma(tc[q * kp], ai, y[q - 1]));
-            }
-        }
-        c128 xnext = xn;
-#pragma unroll
-        for (int q = M - 1; q >= 1; --q) {
-            c128 v = cmk(0.0, 0.0);
-            if (q <= cnt) {
-                const int64_t i = base + q;
-                const c128 ci = form_entry(__ldg(a.z.ta_sup + i), __ldg(a.z.ta_sup_im + i), __ldg(a.z.b_sup + i), sg);
-                xnext = cfnma(y[q], ti[q * kp], cmul(ci, xnext));
-                v = xnext;
-            }
-            tc[q * kp] = v;
-        }
-        tc[0] = xs;
+    mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
+    if (c.active) {
+        k3_body<M, true>(a, l, c, xs, xn);
     } else {
+        c128 *tr = l.t1 + (size_t)c.lr0 * c.kp + c.j;
 #pragma unroll
-        for (int q = 0; q < M; ++q) tc[q * kp] = cmk(0.0, 0.0);
+        for (int q = 0; q < M; ++q) tr[q * c.kp] = cmk(0.0, 0.0);
     }
     __syncthreads();
-    reduce_rows<M>(tr, a, row0);
+    reduce_rows<M>(l.t1, a, c.row0);
 }
 
 // ---------------------------------------------------------------------------
 template <typename K>
-static cudaError_t launch_l0(K kern, const L0Args &a, int tiles, cudaStream_t st) {
+static cudaError_t launch_l0(K kern, const L0Args &a, int flags, cudaStream_t st) {
     const int kp = a.S.kp;
     const int64_t rows = (int64_t)(L0_NT / kp) * TRI_M;
     const int64_t grid = (a.L.n + rows - 1) / rows;
-    const size_t smem = 128 + (size_t)tiles * rows * kp * sizeof(c128);
+    const size_t smem = l0_smem_bytes(kp, TRI_M, flags);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)grid, L0_NT, smem, st>>>(a);
@@ -444,36 +472,40 @@ static cudaError_t launch_l0(K kern, const L0Args &a, int tiles, cudaStream_t st
 }
 
 bool l0v2_supported(int kp) { return kp <= L0_NT; }
+int64_t l0_row_padding() { return (int64_t)L0_NT * TRI_M + 2 * L0_ROWPAD; }
 
 cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
                          cudaStream_t st) {
     L0Args a{};
     a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0;
-    return launch_l0(k_l0_s1<TRI_M>, a, 1, st);
+    return launch_l0(k_l0_s1<TRI_M>, a, ST_RHS, st);
 }
 
 cudaError_t l0_launch_s3acc(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
-                            const c128 *X1, double *acc, c128 *uout, cudaStream_t st) {
+                            const c128 *X1, double *acc, c128 *uout, int64_t nout, cudaStream_t st) {
     L0Args a{};
+    a.nout = nout;
     a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0; a.X1 = X1; a.acc = acc; a.uout = uout;
     a.acc_add = 0; a.final_out = uout != nullptr;
-    return launch_l0(k_l0_s3acc<TRI_M>, a, 1, st);
+    return launch_l0(k_l0_s3acc<TRI_M>, a, ST_RHS, st);
 }
 
 cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
-                         const c128 *X1, double *acc, c128 *rres, cudaStream_t st) {
+                         const c128 *X1, double *acc, c128 *rres, int64_t nout, cudaStream_t st) {
     L0Args a{};
+    a.nout = nout;
     a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0; a.X1 = X1; a.acc = acc; a.rres_out = rres;
     a.acc_add = 0; a.final_out = 0;
-    return launch_l0(k_l0_k2<TRI_M>, a, 2, st);
+    return launch_l0(k_l0_k2<TRI_M>, a, ST_RHS | ST_DIA | ST_TILE2, st);
 }
 
 cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *X1,
-                         const c128 *rres, double *acc, c128 *uout, cudaStream_t st) {
+                         const c128 *rres, double *acc, c128 *uout, int64_t nout, cudaStream_t st) {
     L0Args a{};
+    a.nout = nout;
     a.z = z; a.L = L; a.S = S; a.X1 = X1; a.rres_in = rres; a.acc = acc; a.uout = uout;
     a.acc_add = 1; a.final_out = uout != nullptr;
-    return launch_l0(k_l0_k3<TRI_M>, a, 2, st);
+    return launch_l0(k_l0_k3<TRI_M>, a, ST_TILE2, st);
 }
 
 }  // namespace rexi
