@@ -464,13 +464,16 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
         return rc;
     }
     plan->solver = solver;
-    plan->kp = solver == REXI_SOLVER_TRIDIAG ? pick_kp(d->k) : d->k;
+    plan->kp = pick_kp(d->k);
     if (solver == REXI_SOLVER_TRIDIAG && plan->kp > 256) {
         int rc = set_err(plan, REXI_ERR_UNSUPPORTED, "TRIDIAG solver supports at most 256 shifts per plan");
         rexi_plan_destroy(plan);
         return rc;
     }
-    plan->refine = d->refine < 0 ? 0 : std::min(d->refine, solver == REXI_SOLVER_TRIDIAG ? 1 : 4);
+    // auto (-1): the direct 1D solve is refined only on request (the Python layer
+    // decides by stiffness); COCG always gets one double-double refinement round
+    if (d->refine < 0) plan->refine = solver == REXI_SOLVER_TRIDIAG ? 0 : 1;
+    else plan->refine = std::min(d->refine, solver == REXI_SOLVER_TRIDIAG ? 1 : 4);
 
     cudaError_t e = cudaSetDevice(d->device);
     if (e != cudaSuccess) {

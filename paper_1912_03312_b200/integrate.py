@@ -223,11 +223,16 @@ def rexi_prepare(
     if sr_value is None:
         sr_value = _estimate_sr(sys)
     ratio, admissible = _admissibility(tau, sr_value, approx.domain_radius)
-    if refine is None:
-        refine = 1 if tau * float(sr_value) > AUTO_REFINE_STIFFNESS else 0
     dev = 0 if device is None else int(device)
 
     indptr, indices, a_re, a_im, b_re = shared_pattern(sys.A, sys.B)
+    if refine is None:
+        rows = np.repeat(np.arange(len(indptr) - 1), np.diff(indptr))
+        tridiagonal = len(indices) == 0 or int(np.max(np.abs(indices - rows))) <= 1
+        if tridiagonal and solver != "cocg":
+            refine = 1 if tau * float(sr_value) > AUTO_REFINE_STIFFNESS else 0
+        else:
+            refine = 1          # COCG: one double-double refinement round
     pieces = [c for c in np.array_split(np.arange(k), min(workers, k)) if len(c)]
     plans = []
     try:
