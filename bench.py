@@ -117,21 +117,27 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def kernel_bytes(name, n, k):
-    """Algorithmic HBM bytes per launch of the level-0 kernels:
-    16 B per (row, shift) for every per-shift complex array touched, plus the
-    shared per-row inputs: rhs 16 B, 6 coefficient arrays 48 B (A re/im, B of
-    the two off-diagonals), output 16 B or the dd partial 32 B."""
-    per_shift = {"s1_l0": 1, "s3_l0_acc": 1, "s3_l0_xacc": 2, "s3_l0_x": 2, "s1_l0_res": 2,
-                 "s3_l0_res_acc": 2, "residual": 2}
-    shared = {"s1_l0": 16 + 48, "s3_l0_acc": 16 + 48 + 32, "s3_l0_xacc": 16 + 48 + 32,
-              "s3_l0_x": 16 + 48, "s1_l0_res": 48, "s3_l0_res_acc": 48 + 32 + 32,
-              "residual": 16 + 72, "rhs": 16 + 16 + 24}
+def kernel_bytes(name, n, k, m=16):
+    """Algorithmic HBM bytes per launch of the level-0 kernels (DESIGN.md
+    "Roofline"): 16 B per (row, shift) for every per-shift complex array the
+    kernel must read or write (inverse pivots, stored residual), the shared
+    per-row inputs once (rhs 16 B, 8 B per A/B coefficient array), the
+    per-block interface values (16 or 32 B per (block, shift), blocks = n/m)
+    and the row outputs (rounded 16 B or the double-double partial 32 B)."""
+    kb = k * n / m
+    table = {
+        # per-shift complex arrays, shared row bytes, per-(block,shift) bytes
+        "l0_s1": (1, 16 + 48, 32),
+        "l0_s3acc": (1, 16 + 48 + 16, 32),
+        "l0_k2": (2, 16 + 72 + 32, 16 * 2 + 64),
+        "l0_k3": (2, 48 + 32 + 16, 32),
+    }
     if name == "rhs":
-        return shared["rhs"] * n
-    if name not in per_shift:
+        return (16 + 16 + 24) * n
+    if name not in table:
         return None
-    return per_shift[name] * 16 * n * k + shared[name] * n
+    per_shift, shared, per_block = table[name]
+    return int(per_shift * 16 * n * k + shared * n + per_block * kb)
 
 
 def load_traffic(name):

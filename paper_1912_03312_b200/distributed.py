@@ -75,6 +75,43 @@ def dd_combine_host(parts: np.ndarray) -> np.ndarray:
     return (rh + rl) + 1j * (ih + il)
 
 
+def shard_partial_host(terms: np.ndarray) -> np.ndarray:
+    """Double-double partial (4, n) of a shard's fp64 complex terms (k, n),
+    summed in ascending j with TwoSum -- host statement of what the level-0
+    kernels accumulate per shard (used by the CPU tests of the collective)."""
+    n = terms.shape[1]
+    out = np.zeros((4, n))
+    for comp, (hi_i, lo_i) in enumerate([(0, 1), (2, 3)]):
+        hi = np.zeros(n)
+        lo = np.zeros(n)
+        part = terms.real if comp == 0 else terms.imag
+        for t in part:
+            s = hi + t
+            bb = s - hi
+            e = (hi - (s - bb)) + (t - bb)
+            hi, lo = s, lo + e
+        out[hi_i], out[lo_i] = hi, lo
+    return out
+
+
+def allgather_partials(mine, world: int, group=None, out=None):
+    """All ranks' (4, n) float64 partials -> (world, 4, n), rank order.
+    NCCL: one all_gather_into_tensor over NVLink; other backends (gloo, used
+    by the CPU tests) fall back to all_gather of a tensor list."""
+    import torch
+    import torch.distributed as dist
+    if out is None:
+        out = torch.empty((world,) + tuple(mine.shape), dtype=mine.dtype, device=mine.device)
+    if world == 1:
+        out[0].copy_(mine)
+        return out
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out.view(-1), mine.contiguous().view(-1), group=group)
+    else:
+        dist.all_gather(list(out.unbind(0)), mine.contiguous(), group=group)
+    return out
+
+
 class ShardedStepper:
     """This rank's shard of one REXI step.  ``step(u, out)`` takes and writes
     device tensors (complex128, length n) on this rank's GPU."""
@@ -100,12 +137,8 @@ class ShardedStepper:
         self.stream = stream
 
     def step(self, u, out):
-        import torch.distributed as dist
         self.plan.step_partial(u.data_ptr(), self.mine.data_ptr())
-        if self.world > 1:
-            dist.all_gather_into_tensor(self.parts.view(-1), self.mine.view(-1), group=self.group)
-        else:
-            self.parts[0].copy_(self.mine)
+        allgather_partials(self.mine, self.world, self.group, out=self.parts)
         _native.combine_partials(self.parts.data_ptr(), self.world, self.n, out.data_ptr(),
                                  self.stream)
 
