@@ -4,26 +4,33 @@
 // solvers.py:108-115) and the K back-substitutions of rexi_step
 // (integrate.py:208-222).
 //
-// Layout: every per-shift vector is [row][kp] complex128 (shift index fastest)
-// so one warp = 32 shifts of one row: the shared CSR pattern and the A/B
-// values are read once per row for all shifts (broadcast) and every gather of
-// a neighbour's vector entries is a contiguous 512-B segment.  The shifted
-// entries tau*a - (1j*sigma)*b are formed on the fly with the reference's
-// rounding.
+// Layout: every per-shift vector is [row][kp_cur] complex128 with the shift
+// lane fastest: one warp = up to 32 shift lanes of one row (or 32/kp_cur rows
+// when fewer lanes are live), so the shared CSR pattern and A/B values are
+// read once per row for all shifts and every neighbour gather is one
+// contiguous segment.  Shifted entries tau*a - (1j*sigma)*b are formed on the
+// fly with the reference's rounding.
 //
-// Per iteration two kernels (two reductions -- the COCG recurrences need them):
-//   A: p = z + beta*p_old (own row, double-buffered), q = S p (neighbour p
-//      recomputed from the gathered z, p_old), mu = p^T q
-//   B: x += alpha p, r -= alpha q, z = D^{-1} r, rho' = r^T z, |r|^2
-// Per-shift dots are reduced per CTA in fixed order and finished by the last
-// CTA to arrive (deterministic, independent of how shifts are sharded), which
-// also computes alpha / beta, freezes converged shifts and flags breakdown.
-// Converged shifts are frozen (their lanes do no memory traffic).
-// Refinement: r = b - S x with error-free products (double-double), a
-// correction solve, x += dx.  The final step output is the beta-weighted
-// double-double sum over shifts.
+// Iteration = two kernels (COCG needs two reductions per iteration):
+//   spmv  : p = z + beta p_old (own row; double-buffered), q = S p with the
+//           neighbours' p recomputed from the gathered z, p_old; mu = p^T q.
+//           Rows are claimed in chunks from an atomic counter, so all SMs
+//           work on one narrow wavefront and the +-n neighbour rows of a 2D/3D
+//           stencil are L2 hits; the per-chunk partials are indexed by chunk,
+//           so the reduction order is fixed (deterministic).
+//   update: x += alpha p, r -= alpha q, z = D^-1 r, rho' = r^T z, |r|^2.
+// The last CTA of each kernel finishes the per-shift scalars (alpha, beta),
+// freezes converged shifts and flags breakdown / non-finite values.
+// Compaction: when at most half of the lanes are live, the live shifts are
+// repacked (ascending shift order) into a layout half as wide; frozen shifts'
+// x are written to the full-width solution first.  The work per iteration then
+// follows the number of live shifts instead of K.
+// Refinement: r = b - S x with error-free products (double-double), one
+// correction solve, and the step output sum_j beta_j (x_j + dx_j) in
+// double-double.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -33,8 +40,9 @@
 
 namespace rexi {
 
-constexpr int CG_NT = 256;           // threads per CTA (8 warps)
+constexpr int CG_NT = 256;            // threads per CTA (8 warps)
 constexpr int CG_WARPS = CG_NT / 32;
+constexpr int CG_CHUNK_PASSES = 8;    // row slots per chunk = passes * rows per CTA pass
 
 struct CgMat {
     int64_t n;
@@ -44,127 +52,105 @@ struct CgMat {
 };
 
 struct CgVec {
-    c128 *x, *r, *z, *p0, *p1, *q;         // [n][kp]
-    const c128 *bvec;                      // per-shift rhs [n][kp] or nullptr
+    c128 *x, *r, *z, *p0, *p1, *q;         // [n][kp] current (compacted) layout
+    const c128 *bvec;                      // per-shift rhs [n][kp_full] or nullptr
     const c128 *bshared;                   // shared rhs [n] or nullptr
 };
 
-struct CgScal {
-    double2 *rho, *mu, *alpha, *beta;      // [kp]
-    double *rnorm2, *bnorm2;               // [kp]
-    int *active;                           // [kp] 1 = iterating
-    int *iters;                            // [kp]
-    int *status;                           // [kp] 0 ok, 1 breakdown, 2 non-finite
+struct CgScal {                            // per lane of the current layout
+    double2 *rho, *alpha, *beta;
+    double *rnorm2, *bnorm2;
+    int *active, *iters, *status;
     int *nactive;                          // [1]
-    double2 *part_a;                       // [grid][kp] partials
-    double2 *part_b;                       // [grid][kp]
-    double *part_c;                        // [grid][kp]
-    unsigned int *counter;                 // [2]
+    double2 *part_a;                       // spmv partials [nchunks][kp]
+    double2 *part_b;                       // update partials [grid][kp]
+    double *part_c;                        // update partials [grid][kp]
+    unsigned int *ctr;                     // [8] claim / done counters (parity)
     double tol;
 };
 
 struct CgGeom {
-    int kp, kw, G, rpw;                    // lanes per group, groups per row, rows per warp
-    int k;                                 // real shifts (lanes >= k are padding)
+    int kp, kw, G, rpw;                    // lanes, lanes per warp group, groups, rows per warp
+    int64_t chunk_rows, nchunks;
+    const int *lane_shift;                 // [kp] shift index of each lane
 };
 
 __device__ __forceinline__ c128 cdiv_c(c128 a, c128 b) { return cmul(a, crcp(b)); }
 
-__device__ __forceinline__ void lane_geom(const CgGeom &g, int &j, int &roff, int64_t &item0,
-                                          int64_t &stride) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w = (int64_t)blockIdx.x * CG_WARPS + (threadIdx.x >> 5);
-    const int64_t W = (int64_t)gridDim.x * CG_WARPS;
-    const int grp = (int)(w % g.G);
-    j = grp * g.kw + (lane % g.kw);
-    roff = lane / g.kw;
-    item0 = w / g.G;
-    stride = W / g.G;
-}
-
-// shift index of thread u inside a CTA (same for every CTA)
-__device__ __forceinline__ int thread_shift(const CgGeom &g, int u) {
-    const int w = blockIdx.x * CG_WARPS + (u >> 5);   // global warp of thread u in this CTA
+// lane and row slot of this thread for one CTA pass
+__device__ __forceinline__ void cta_geom(const CgGeom &g, int &lane, int &slot, int &slots) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int grp = w % g.G;
-    return grp * g.kw + ((u & 31) % g.kw);
+    lane = grp * g.kw + (l % g.kw);
+    slot = (w / g.G) * g.rpw + l / g.kw;
+    slots = (CG_WARPS / g.G) * g.rpw;
 }
 
-// last-CTA-done: returns true in the single CTA that finishes last
-__device__ __forceinline__ bool last_block(unsigned int *counter) {
-    __shared__ bool is_last;
+// fixed-order CTA reduction: thread u's value summed into sm[lane(u)] in thread order
+template <typename T, typename Add>
+__device__ __forceinline__ void cta_sum(T v, const CgGeom &g, T *sm, T *out, Add add, T zero) {
+    sm[threadIdx.x] = v;
+    __syncthreads();
+    if (threadIdx.x < g.kp) {
+        T s = zero;
+        for (int u = 0; u < CG_NT; ++u) {
+            const int w = u >> 5, l = u & 31;
+            if ((w % g.G) * g.kw + (l % g.kw) == (int)threadIdx.x && (w / g.G) < CG_WARPS / g.G)
+                s = add(s, sm[u]);
+        }
+        out[threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ bool arrive_last(unsigned int *done, unsigned int total) {
+    __shared__ bool last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned int prev = atomicAdd(counter, 1u);
-        is_last = (prev == gridDim.x - 1);
-    }
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == total - 1;
     __syncthreads();
-    if (is_last) __threadfence();
-    return is_last;
+    if (last) __threadfence();
+    return last;
 }
 
 // ---------------------------------------------------------------------------
-// reduce helpers: each thread holds one complex / real partial for shift j;
-// write per-CTA partials part[cta][kp] summed in fixed thread order
+// init (full width, lane = shift): x = 0, r = b, z = D^-1 r, p_old = 0
 // ---------------------------------------------------------------------------
-__device__ void block_reduce_c(c128 v, const CgGeom &g, double2 *part, int kp) {
-    __shared__ double2 sm[CG_NT];
-    sm[threadIdx.x] = v;
-    __syncthreads();
-    for (int t = threadIdx.x; t < kp; t += CG_NT) {
-        double2 s = make_double2(0.0, 0.0);
-        for (int u = 0; u < CG_NT; ++u)
-            if (thread_shift(g, u) == t) s = cadd(s, sm[u]);
-        part[(size_t)blockIdx.x * kp + t] = s;
-    }
-    __syncthreads();
-}
-
-__device__ void block_reduce_r(double v, const CgGeom &g, double *part, int kp) {
-    __shared__ double sm[CG_NT];
-    sm[threadIdx.x] = v;
-    __syncthreads();
-    for (int t = threadIdx.x; t < kp; t += CG_NT) {
-        double s = 0.0;
-        for (int u = 0; u < CG_NT; ++u)
-            if (thread_shift(g, u) == t) s += sm[u];
-        part[(size_t)blockIdx.x * kp + t] = s;
-    }
-    __syncthreads();
-}
-
-// ---------------------------------------------------------------------------
-// init: x = 0, r = b, z = D^-1 r, p_old = 0; rho = r^T z, |b|^2
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
-    int j, roff;
-    int64_t item, stride;
-    lane_geom(g, j, roff, item, stride);
+__global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g,
+                                                    int kreal) {
+    __shared__ double2 smc[CG_NT];
+    __shared__ double smr[CG_NT];
+    __shared__ double2 outc[CG_NT];
+    __shared__ double outr[CG_NT];
+    int lane, slot, slots;
+    cta_geom(g, lane, slot, slots);
     const int kp = g.kp;
-    const c128 sg = S.sigma[j];
+    const c128 sg = S.sigma[lane];
     c128 rho = cmk(0.0, 0.0);
     double bn = 0.0;
-    for (int64_t it = item; it * g.rpw < M.n; it += stride) {
-        const int64_t i = it * g.rpw + roff;
-        if (i >= M.n) continue;
-        const c128 b = V.bshared ? V.bshared[i] : V.bvec[i * kp + j];
-        const c128 d = form_entry(M.dta[i], M.dta_im[i], M.db[i], sg);
-        const c128 z = cdiv_c(b, d);
-        V.x[i * kp + j] = cmk(0.0, 0.0);
-        V.r[i * kp + j] = b;
-        V.z[i * kp + j] = z;
-        V.p0[i * kp + j] = cmk(0.0, 0.0);
+    for (int64_t i = (int64_t)blockIdx.x * slots + slot; i < M.n; i += (int64_t)gridDim.x * slots) {
+        const size_t o = (size_t)i * kp + lane;
+        const c128 b = V.bshared ? V.bshared[i] : V.bvec[o];
+        const c128 z = cdiv_c(b, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
+        V.x[o] = cmk(0.0, 0.0);
+        V.r[o] = b;
+        V.z[o] = z;
+        V.p0[o] = cmk(0.0, 0.0);
         rho = cadd(rho, cmul(b, z));
         bn += cabs2(b);
     }
-    block_reduce_c(rho, g, Sc.part_a, kp);
-    block_reduce_r(bn, g, Sc.part_c, kp);
-    if (last_block(Sc.counter)) {
+    cta_sum<double2>(rho, g, smc, outc, [](double2 a, double2 b) { return cadd(a, b); }, make_double2(0, 0));
+    cta_sum<double>(bn, g, smr, outr, [](double a, double b) { return a + b; }, 0.0);
+    if (threadIdx.x < kp) {
+        Sc.part_b[(size_t)blockIdx.x * kp + threadIdx.x] = outc[threadIdx.x];
+        Sc.part_c[(size_t)blockIdx.x * kp + threadIdx.x] = outr[threadIdx.x];
+    }
+    if (arrive_last(Sc.ctr + 4, gridDim.x)) {
         for (int t = threadIdx.x; t < kp; t += CG_NT) {
             double2 s = make_double2(0.0, 0.0);
             double sb = 0.0;
             for (unsigned c = 0; c < gridDim.x; ++c) {
-                s = cadd(s, Sc.part_a[(size_t)c * kp + t]);
+                s = cadd(s, Sc.part_b[(size_t)c * kp + t]);
                 sb += Sc.part_c[(size_t)c * kp + t];
             }
             Sc.rho[t] = s;
@@ -173,106 +159,136 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
             Sc.beta[t] = make_double2(0.0, 0.0);
             Sc.iters[t] = 0;
             Sc.status[t] = 0;
-            Sc.active[t] = (t < g.k && sb > 0.0) ? 1 : 0;
+            Sc.active[t] = (g.lane_shift[t] < kreal && sb > 0.0) ? 1 : 0;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             int na = 0;
             for (int t = 0; t < kp; ++t) na += Sc.active[t];
             *Sc.nactive = na;
-            Sc.counter[0] = 0;
+            Sc.ctr[4] = 0;
+            Sc.ctr[0] = Sc.ctr[1] = Sc.ctr[2] = Sc.ctr[3] = 0;
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// A: p_new = z + beta p_old (own row); q = S p_new; mu = p^T q
+// spmv: p_new = z + beta p_old (own row), q = S p_new, mu = p^T q  -> alpha
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g,
                                                     int parity) {
+    __shared__ double2 smc[CG_NT];
+    __shared__ double2 outc[CG_NT];
+    __shared__ int64_t chunk_sh;
     if (*Sc.nactive == 0) return;
-    int j, roff;
-    int64_t item, stride;
-    lane_geom(g, j, roff, item, stride);
+    int lane, slot, slots;
+    cta_geom(g, lane, slot, slots);
     const int kp = g.kp;
-    const bool act = Sc.active[j] != 0;
-    const c128 sg = S.sigma[j];
-    const c128 beta = Sc.beta[j];
+    const bool act = Sc.active[lane] != 0;
+    const c128 sg = S.sigma[g.lane_shift[lane]];
+    const c128 beta = Sc.beta[lane];
     const c128 *pold = parity ? V.p1 : V.p0;
     c128 *pnew = parity ? V.p0 : V.p1;
-    c128 mu = cmk(0.0, 0.0);
-    for (int64_t it = item; it * g.rpw < M.n; it += stride) {
-        const int64_t i = it * g.rpw + roff;
-        if (i >= M.n || !act) continue;
-        c128 acc = cmk(0.0, 0.0);
-        c128 pi = cmk(0.0, 0.0);
-        const int32_t q0 = M.indptr[i], q1 = M.indptr[i + 1];
-        for (int32_t q = q0; q < q1; ++q) {
-            const int64_t c = M.indices[q];
-            const c128 pc = cadd(V.z[c * kp + j], cmul(beta, pold[c * kp + j]));
-            const c128 e = form_entry(M.ta[q], M.ta_im[q], M.b[q], sg);
-            acc = cadd(acc, cmul(e, pc));
-            if (c == i) pi = pc;
-        }
-        pnew[i * kp + j] = pi;
-        V.q[i * kp + j] = acc;
-        mu = cadd(mu, cmul(pi, acc));
-    }
-    block_reduce_c(mu, g, Sc.part_a, kp);
-    if (last_block(Sc.counter)) {
-        for (int t = threadIdx.x; t < kp; t += CG_NT) {
-            if (!Sc.active[t]) continue;
-            double2 s = make_double2(0.0, 0.0);
-            for (unsigned c = 0; c < gridDim.x; ++c) s = cadd(s, Sc.part_a[(size_t)c * kp + t]);
-            Sc.mu[t] = s;
-            const double2 rho = Sc.rho[t];
-            const double ms = cabs2(s);
-            if (!(ms > 0.0) || !isfinite(ms)) {
-                Sc.status[t] = isfinite(ms) ? 1 : 2;
-                Sc.active[t] = 0;
-                Sc.alpha[t] = make_double2(0.0, 0.0);
-            } else {
-                Sc.alpha[t] = cdiv_c(rho, s);
+    unsigned int *claim = Sc.ctr + (parity & 1);
+    unsigned int *done = Sc.ctr + 2 + (parity & 1);
+    for (;;) {
+        if (threadIdx.x == 0) chunk_sh = (int64_t)atomicAdd(claim, 1u);
+        __syncthreads();
+        const int64_t chunk = chunk_sh;
+        __syncthreads();
+        if (chunk >= g.nchunks) break;
+        c128 mu = cmk(0.0, 0.0);
+        if (act) {
+            const int64_t r0 = chunk * g.chunk_rows;
+            const int64_t r1 = min(r0 + g.chunk_rows, M.n);
+            for (int64_t i = r0 + slot; i < r1; i += slots) {
+                c128 acc = cmk(0.0, 0.0), pi = cmk(0.0, 0.0);
+                const int32_t q0 = M.indptr[i], q1 = M.indptr[i + 1];
+                for (int32_t q = q0; q < q1; ++q) {
+                    const int64_t c = M.indices[q];
+                    const size_t oc = (size_t)c * kp + lane;
+                    const c128 pc = cadd(V.z[oc], cmul(beta, pold[oc]));
+                    acc = cadd(acc, cmul(form_entry(M.ta[q], M.ta_im[q], M.b[q], sg), pc));
+                    if (c == i) pi = pc;
+                }
+                const size_t o = (size_t)i * kp + lane;
+                pnew[o] = pi;
+                V.q[o] = acc;
+                mu = cadd(mu, cmul(pi, acc));
             }
         }
-        __syncthreads();
-        if (threadIdx.x == 0) Sc.counter[0] = 0;
+        cta_sum<double2>(mu, g, smc, outc, [](double2 a, double2 b) { return cadd(a, b); }, make_double2(0, 0));
+        if (threadIdx.x < kp) Sc.part_a[(size_t)chunk * kp + threadIdx.x] = outc[threadIdx.x];
+        if (arrive_last(done, (unsigned)g.nchunks)) {
+            // fixed-order finish: thread t handles lane t % kp, chunks strided by CG_NT / kp
+            const int sub = CG_NT / kp > 0 ? CG_NT / kp : 1;
+            double2 s = make_double2(0.0, 0.0);
+            if (threadIdx.x < sub * kp) {
+                const int t = threadIdx.x % kp, sidx = threadIdx.x / kp;
+                for (int64_t c = sidx; c < g.nchunks; c += sub) s = cadd(s, Sc.part_a[(size_t)c * kp + t]);
+            }
+            smc[threadIdx.x] = s;
+            __syncthreads();
+            for (int t = threadIdx.x; t < kp; t += CG_NT) {
+                double2 m = make_double2(0.0, 0.0);
+                for (int sidx = 0; sidx < sub; ++sidx) m = cadd(m, smc[sidx * kp + t]);
+                if (Sc.active[t]) {
+                    const double ms = cabs2(m);
+                    if (!(ms > 0.0) || !isfinite(ms)) {
+                        Sc.status[t] = isfinite(ms) ? 1 : 2;
+                        Sc.active[t] = 0;
+                        Sc.alpha[t] = make_double2(0.0, 0.0);
+                    } else {
+                        Sc.alpha[t] = cdiv_c(Sc.rho[t], m);
+                    }
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) Sc.ctr[2 + ((parity + 1) & 1)] = 0, Sc.ctr[(parity + 1) & 1] = 0;
+            break;
+        }
     }
 }
 
 // ---------------------------------------------------------------------------
-// B: x += alpha p; r -= alpha q; z = D^-1 r; rho' = r^T z; |r|^2; freeze
+// update: x += alpha p; r -= alpha q; z = D^-1 r; rho' = r^T z; |r|^2 -> beta
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g,
                                                       int parity, int max_iters) {
+    __shared__ double2 smc[CG_NT];
+    __shared__ double smr[CG_NT];
+    __shared__ double2 outc[CG_NT];
+    __shared__ double outr[CG_NT];
     if (*Sc.nactive == 0) return;
-    int j, roff;
-    int64_t item, stride;
-    lane_geom(g, j, roff, item, stride);
+    int lane, slot, slots;
+    cta_geom(g, lane, slot, slots);
     const int kp = g.kp;
-    const bool act = Sc.active[j] != 0;
-    const c128 sg = S.sigma[j];
-    const c128 alpha = Sc.alpha[j];
+    const bool act = Sc.active[lane] != 0;
+    const c128 sg = S.sigma[g.lane_shift[lane]];
+    const c128 alpha = Sc.alpha[lane];
     const c128 *pnew = parity ? V.p0 : V.p1;
     c128 rho = cmk(0.0, 0.0);
     double rn = 0.0;
-    for (int64_t it = item; it * g.rpw < M.n; it += stride) {
-        const int64_t i = it * g.rpw + roff;
-        if (i >= M.n || !act) continue;
-        const size_t o = (size_t)i * kp + j;
-        const c128 p = pnew[o], q = V.q[o];
-        V.x[o] = cadd(V.x[o], cmul(alpha, p));
-        const c128 r = csub(V.r[o], cmul(alpha, q));
-        V.r[o] = r;
-        const c128 d = form_entry(M.dta[i], M.dta_im[i], M.db[i], sg);
-        const c128 z = cdiv_c(r, d);
-        V.z[o] = z;
-        rho = cadd(rho, cmul(r, z));
-        rn += cabs2(r);
+    if (act) {
+        for (int64_t i = (int64_t)blockIdx.x * slots + slot; i < M.n; i += (int64_t)gridDim.x * slots) {
+            const size_t o = (size_t)i * kp + lane;
+            const c128 p = pnew[o], q = V.q[o];
+            V.x[o] = cadd(V.x[o], cmul(alpha, p));
+            const c128 r = csub(V.r[o], cmul(alpha, q));
+            V.r[o] = r;
+            const c128 z = cdiv_c(r, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
+            V.z[o] = z;
+            rho = cadd(rho, cmul(r, z));
+            rn += cabs2(r);
+        }
     }
-    block_reduce_c(rho, g, Sc.part_b, kp);
-    block_reduce_r(rn, g, Sc.part_c, kp);
-    if (last_block(Sc.counter + 1)) {
+    cta_sum<double2>(rho, g, smc, outc, [](double2 a, double2 b) { return cadd(a, b); }, make_double2(0, 0));
+    cta_sum<double>(rn, g, smr, outr, [](double a, double b) { return a + b; }, 0.0);
+    if (threadIdx.x < kp) {
+        Sc.part_b[(size_t)blockIdx.x * kp + threadIdx.x] = outc[threadIdx.x];
+        Sc.part_c[(size_t)blockIdx.x * kp + threadIdx.x] = outr[threadIdx.x];
+    }
+    if (arrive_last(Sc.ctr + 5, gridDim.x)) {
         for (int t = threadIdx.x; t < kp; t += CG_NT) {
             if (!Sc.active[t]) continue;
             double2 s = make_double2(0.0, 0.0);
@@ -284,13 +300,12 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
             Sc.rnorm2[t] = sr;
             Sc.iters[t] += 1;
             const double2 rho_old = Sc.rho[t];
-            const double ro = cabs2(rho_old);
-            if (!isfinite(sr)) {
+            if (!isfinite(sr) || !isfinite(s.x) || !isfinite(s.y)) {
                 Sc.status[t] = 2;
                 Sc.active[t] = 0;
             } else if (sr <= Sc.tol * Sc.tol * Sc.bnorm2[t]) {
-                Sc.active[t] = 0;                              // converged: freeze
-            } else if (!(ro > 0.0)) {
+                Sc.active[t] = 0;                               // converged: freeze
+            } else if (!(cabs2(rho_old) > 0.0)) {
                 Sc.status[t] = 1;
                 Sc.active[t] = 0;
             } else if (Sc.iters[t] >= max_iters) {
@@ -306,35 +321,72 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
             int na = 0;
             for (int t = 0; t < kp; ++t) na += Sc.active[t];
             *Sc.nactive = na;
-            Sc.counter[1] = 0;
+            Sc.ctr[5] = 0;
         }
     }
 }
 
-// r_j = b - S_j x_j with error-free products, double-double sum, rounded once
-__global__ void __launch_bounds__(CG_NT) k_cg_residual(CgMat M, CgVec V, ShiftDev S, CgGeom g,
-                                                        c128 *out) {
-    int j, roff;
-    int64_t item, stride;
-    lane_geom(g, j, roff, item, stride);
-    const int kp = g.kp;
-    const c128 sg = S.sigma[j];
-    for (int64_t it = item; it * g.rpw < M.n; it += stride) {
-        const int64_t i = it * g.rpw + roff;
-        if (i >= M.n) continue;
-        const c128 b = V.bshared ? V.bshared[i] : V.bvec[i * kp + j];
-        ddacc re = {b.x, 0.0}, im = {b.y, 0.0};
-        for (int32_t q = M.indptr[i]; q < M.indptr[i + 1]; ++q) {
-            const c128 e = form_entry(M.ta[q], M.ta_im[q], M.b[q], sg);
-            const c128 x = V.x[(int64_t)M.indices[q] * kp + j];
-            dd p;
-            p = two_prod(e.x, x.x); ddacc_add(re, -p.hi); re.lo = __dsub_rn(re.lo, p.lo);
-            p = two_prod(e.y, x.y); ddacc_add(re, p.hi); re.lo = __dadd_rn(re.lo, p.lo);
-            p = two_prod(e.x, x.y); ddacc_add(im, -p.hi); im.lo = __dsub_rn(im.lo, p.lo);
-            p = two_prod(e.y, x.x); ddacc_add(im, -p.hi); im.lo = __dsub_rn(im.lo, p.lo);
-        }
-        out[i * kp + j] = cmk(__dadd_rn(re.hi, re.lo), __dadd_rn(im.hi, im.lo));
+// ---------------------------------------------------------------------------
+// compaction: dst[i][l'] = src[i][map[l']] (new width kp_new)
+// ---------------------------------------------------------------------------
+__global__ void k_cg_repack(const c128 *__restrict__ src, c128 *__restrict__ dst, int64_t n, int kp_old,
+                            int kp_new, const int *__restrict__ map) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * kp_new) return;
+    const int64_t i = t / kp_new;
+    const int l = (int)(t % kp_new);
+    dst[t] = src[i * kp_old + map[l]];
+}
+
+// x_out[i][lane_shift[l]] = x[i][l] for the lanes in mask
+__global__ void k_cg_scatter_x(const c128 *__restrict__ x, c128 *__restrict__ xout, int64_t n, int kp,
+                               int kp_full, const int *__restrict__ lane_shift,
+                               const int *__restrict__ mask) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * kp) return;
+    const int64_t i = t / kp;
+    const int l = (int)(t % kp);
+    if (mask[l]) xout[i * kp_full + lane_shift[l]] = x[t];
+}
+
+// scalars of the kept lanes, in place safe (map[l'] >= l')
+__global__ void k_cg_repack_scalars(CgScal Sc, int kp_new, const int *__restrict__ map) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int l = 0; l < kp_new; ++l) {
+        const int s = map[l];
+        Sc.rho[l] = Sc.rho[s];
+        Sc.alpha[l] = Sc.alpha[s];
+        Sc.beta[l] = Sc.beta[s];
+        Sc.rnorm2[l] = Sc.rnorm2[s];
+        Sc.bnorm2[l] = Sc.bnorm2[s];
+        Sc.active[l] = Sc.active[s];
+        Sc.iters[l] = Sc.iters[s];
+        Sc.status[l] = Sc.status[s];
     }
+}
+
+// r_j = b - S_j x_j with error-free products, double-double sum, rounded once
+// (full width: lane = shift)
+__global__ void __launch_bounds__(CG_NT) k_cg_residual(CgMat M, const c128 *__restrict__ bshared,
+                                                        const c128 *__restrict__ x, ShiftDev S, int kp,
+                                                        c128 *__restrict__ out) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= M.n * kp) return;
+    const int64_t i = t / kp;
+    const int j = (int)(t % kp);
+    const c128 sg = S.sigma[j];
+    const c128 b = bshared[i];
+    ddacc re = {b.x, 0.0}, im = {b.y, 0.0};
+    for (int32_t q = M.indptr[i]; q < M.indptr[i + 1]; ++q) {
+        const c128 e = form_entry(M.ta[q], M.ta_im[q], M.b[q], sg);
+        const c128 v = x[(int64_t)M.indices[q] * kp + j];
+        dd p;
+        p = two_prod(e.x, v.x); ddacc_add(re, -p.hi); re.lo = __dsub_rn(re.lo, p.lo);
+        p = two_prod(e.y, v.y); ddacc_add(re, p.hi); re.lo = __dadd_rn(re.lo, p.lo);
+        p = two_prod(e.x, v.y); ddacc_add(im, -p.hi); im.lo = __dsub_rn(im.lo, p.lo);
+        p = two_prod(e.y, v.x); ddacc_add(im, -p.hi); im.lo = __dsub_rn(im.lo, p.lo);
+    }
+    out[t] = cmk(__dadd_rn(re.hi, re.lo), __dadd_rn(im.hi, im.lo));
 }
 
 // rhs = 1j * (B @ u), CSR row order, no FMA (reference integrate.py:204)
@@ -351,7 +403,7 @@ __global__ void k_cg_rhs(CgMat M, const c128 *__restrict__ u, c128 *__restrict__
     rhs[i] = cmk(-si, sr);
 }
 
-// acc (dd, SoA 4n) (+)= sum_j beta_j (x1_j [+ x2_j]), fixed shift order
+// acc (dd, SoA 4n) = sum_j beta_j (x1_j [+ x2_j]), fixed shift order
 __global__ void k_cg_accum(int64_t n, int kp, int k, const c128 *__restrict__ beta,
                            const c128 *__restrict__ x1, const c128 *__restrict__ x2, double *acc,
                            c128 *uout) {
@@ -408,12 +460,17 @@ struct CocgImpl {
     CgMat M{};
     CgVec V{};
     CgScal Sc{};
-    CgGeom g{};
-    int grid = 0;
+    int kp_full = 0;
+    int sms = 148;
+    c128 *scratch = nullptr;   // repack staging [n][kp_full]
+    c128 *xout = nullptr;      // full-width solution [n][kp_full]
     c128 *rhs = nullptr;       // shared rhs [n]
-    c128 *xsave = nullptr;     // first-solve x [n][kp] (refinement)
-    c128 *res = nullptr;       // per-shift residual rhs [n][kp]
-    int *h_nactive = nullptr;  // pinned
+    c128 *xsave = nullptr;     // first-solve x [n][kp_full] (refinement)
+    c128 *res = nullptr;       // residual rhs [n][kp_full]
+    int *lane_shift = nullptr; // device [kp_full]
+    int *map = nullptr;        // device [kp_full]
+    int *mask = nullptr;       // device [kp_full]
+    int *h_buf = nullptr;      // pinned [2 + 2*kp_full]
 };
 
 static int alloc_(CocgState &cg, void **p, size_t bytes, std::string &err) {
@@ -441,6 +498,24 @@ static int alloc_(CocgState &cg, void **p, size_t bytes, std::string &err) {
         }                                                                 \
     } while (0)
 
+static CgGeom make_geom(const CocgImpl *im, int kp, int64_t n) {
+    CgGeom g{};
+    g.kp = kp;
+    g.kw = kp < 32 ? kp : 32;
+    g.G = kp / g.kw;
+    g.rpw = 32 / g.kw;
+    g.chunk_rows = (int64_t)(CG_WARPS / g.G) * g.rpw * CG_CHUNK_PASSES;
+    g.nchunks = (n + g.chunk_rows - 1) / g.chunk_rows;
+    g.lane_shift = im->lane_shift;
+    return g;
+}
+
+static int grid_for(const CocgImpl *im, const CgGeom &g, int64_t n) {
+    const int64_t slots = (CG_WARPS / g.G) * g.rpw;
+    const int64_t want = (n + slots - 1) / slots;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)im->sms * 8));
+}
+
 int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine, cudaStream_t st,
                 std::string &err) {
     CocgImpl *im = new CocgImpl();
@@ -454,7 +529,7 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     cg.shift_offset = d->shift_offset;
     const int64_t n = d->n, nnz = d->nnz;
     const int kp = S.kp;
-    // host: fl(tau*a) per nnz, diagonal positions
+    im->kp_full = kp;
     std::vector<double> ta(nnz), tai(nnz), bb(nnz), dta(n, 0.0), dtai(n, 0.0), db(n, 0.0);
     std::vector<char> hasdiag(n, 0);
     for (int64_t r = 0; r < n; ++r)
@@ -493,23 +568,9 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     CGK(cudaMemcpyAsync(dtai_, dtai.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
     CGK(cudaMemcpyAsync(db_, db.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
     im->M = CgMat{n, ip, ix, ta_, tai_, bb_, dta_, dtai_, db_};
-    // geometry
-    CgGeom &g = im->g;
-    g.kp = kp;
-    g.kw = kp < 32 ? kp : 32;
-    g.G = kp / g.kw;
-    g.rpw = 32 / g.kw;
-    g.k = d->k;
-    int dev = 0, sms = 148;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t items = ((n + g.rpw - 1) / g.rpw) * g.G;          // warp work items
-    int64_t want = (items + CG_WARPS - 1) / CG_WARPS;
-    int64_t cap = (int64_t)sms * 8;
-    im->grid = (int)std::max<int64_t>(1, std::min(want, cap));
-    // grid * CG_WARPS must be a multiple of G so every warp keeps one shift group
-    while ((im->grid * CG_WARPS) % g.G) ++im->grid;
-    // vectors
+    cudaDeviceGetAttribute(&im->sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t vb = sizeof(c128) * (size_t)n * kp;
     CGA(im->V.x, vb);
     CGA(im->V.r, vb);
@@ -517,14 +578,18 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     CGA(im->V.p0, vb);
     CGA(im->V.p1, vb);
     CGA(im->V.q, vb);
+    CGA(im->scratch, vb);
+    CGA(im->xout, vb);
     CGA(im->rhs, sizeof(c128) * n);
     if (refine > 0) {
         CGA(im->xsave, vb);
         CGA(im->res, vb);
     }
+    CGA(im->lane_shift, sizeof(int) * kp);
+    CGA(im->map, sizeof(int) * kp);
+    CGA(im->mask, sizeof(int) * kp);
     CgScal &Sc = im->Sc;
     CGA(Sc.rho, sizeof(double2) * kp);
-    CGA(Sc.mu, sizeof(double2) * kp);
     CGA(Sc.alpha, sizeof(double2) * kp);
     CGA(Sc.beta, sizeof(double2) * kp);
     CGA(Sc.rnorm2, sizeof(double) * kp);
@@ -533,97 +598,164 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     CGA(Sc.iters, sizeof(int) * kp);
     CGA(Sc.status, sizeof(int) * kp);
     CGA(Sc.nactive, sizeof(int));
-    CGA(Sc.part_a, sizeof(double2) * kp * im->grid);
-    CGA(Sc.part_b, sizeof(double2) * kp * im->grid);
-    CGA(Sc.part_c, sizeof(double) * kp * im->grid);
-    CGA(Sc.counter, sizeof(unsigned int) * 2);
-    CGK(cudaMemsetAsync(Sc.counter, 0, sizeof(unsigned int) * 2, st));
+    const CgGeom g1 = make_geom(im, 1, n);     // the most chunks any layout can have
+    CGA(Sc.part_a, sizeof(double2) * (size_t)kp * std::max<int64_t>(g1.nchunks, make_geom(im, kp, n).nchunks));
+    CGA(Sc.part_b, sizeof(double2) * (size_t)kp * im->sms * 8);
+    CGA(Sc.part_c, sizeof(double) * (size_t)kp * im->sms * 8);
+    CGA(Sc.ctr, sizeof(unsigned int) * 8);
+    CGK(cudaMemsetAsync(Sc.ctr, 0, sizeof(unsigned int) * 8, st));
     Sc.tol = cg.tol;
-    CGK(cudaMallocHost((void **)&im->h_nactive, sizeof(int)));
+    CGK(cudaMallocHost((void **)&im->h_buf, sizeof(int) * (2 + 2 * kp)));
     CGK(cudaStreamSynchronize(st));
     return REXI_OK;
 }
 
-// solve S_j x_j = b for all shifts (b shared or per shift); x in V.x
+// repack the live lanes into a layout of width kp_new (host decides the map)
+static int cg_repack(CocgImpl *im, int kp_old, int kp_new, const std::vector<int> &map,
+                     const std::vector<int> &drop_mask, std::vector<int> &lane_shift, int parity_live,
+                     cudaStream_t st, std::string &err) {
+    const int64_t n = im->M.n;
+    // 1) frozen lanes being dropped: x -> full-width solution
+    CGK(cudaMemcpyAsync(im->mask, drop_mask.data(), sizeof(int) * kp_old, cudaMemcpyHostToDevice, st));
+    const int64_t t_old = n * kp_old;
+    k_cg_scatter_x<<<(unsigned)((t_old + 255) / 256), 256, 0, st>>>(im->V.x, im->xout, n, kp_old, im->kp_full,
+                                                                   im->lane_shift, im->mask);
+    // 2) live vectors x, r, z, p(current) -> new width, through the scratch array
+    CGK(cudaMemcpyAsync(im->map, map.data(), sizeof(int) * kp_new, cudaMemcpyHostToDevice, st));
+    const int64_t t_new = n * kp_new;
+    c128 **vecs[4] = {&im->V.x, &im->V.r, &im->V.z, parity_live ? &im->V.p0 : &im->V.p1};
+    for (c128 **v : vecs) {
+        k_cg_repack<<<(unsigned)((t_new + 255) / 256), 256, 0, st>>>(*v, im->scratch, n, kp_old, kp_new, im->map);
+        std::swap(*v, im->scratch);
+    }
+    k_cg_repack_scalars<<<1, 32, 0, st>>>(im->Sc, kp_new, im->map);
+    std::vector<int> ls(kp_new);
+    for (int l = 0; l < kp_new; ++l) ls[l] = lane_shift[map[l]];
+    lane_shift = ls;
+    CGK(cudaMemcpyAsync(im->lane_shift, lane_shift.data(), sizeof(int) * kp_new, cudaMemcpyHostToDevice, st));
+    CGK(cudaGetLastError());
+    return REXI_OK;
+}
+
+// solve S_j x_j = b for all shifts (b shared or per shift); result in im->xout
 static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t st, int64_t *launches,
-                    std::string &err, int *iters_out) {
-    CgVec &V = im->V;
-    k_cg_init<<<im->grid, CG_NT, 0, st>>>(im->M, V, im->Sc, S, im->g);
+                    std::string &err, double tol) {
+    const int64_t n = cg.n;
+    int kp = im->kp_full;
+    std::vector<int> lane_shift(kp), valid(kp);
+    for (int l = 0; l < kp; ++l) {
+        lane_shift[l] = l;
+        valid[l] = l < cg.k;
+    }
+    CGK(cudaMemcpyAsync(im->lane_shift, lane_shift.data(), sizeof(int) * kp, cudaMemcpyHostToDevice, st));
+    im->Sc.tol = tol;
+    CgGeom g = make_geom(im, kp, n);
+    int grid = grid_for(im, g, n);
+    k_cg_init<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, cg.k);
     CGK(cudaGetLastError());
     ++*launches;
     int it = 0, parity = 0;
     const int check_every = 8;
     for (;;) {
         for (int s = 0; s < check_every; ++s) {
-            k_cg_spmv<<<im->grid, CG_NT, 0, st>>>(im->M, V, im->Sc, S, im->g, parity);
-            k_cg_update<<<im->grid, CG_NT, 0, st>>>(im->M, V, im->Sc, S, im->g, parity, cg.max_iters);
+            k_cg_spmv<<<(int)std::min<int64_t>(g.nchunks, (int64_t)im->sms * 8), CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
+            k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity, cg.max_iters);
             parity ^= 1;
             *launches += 2;
             ++it;
         }
         CGK(cudaGetLastError());
-        CGK(cudaMemcpyAsync(im->h_nactive, im->Sc.nactive, sizeof(int), cudaMemcpyDeviceToHost, st));
+        int *h_na = im->h_buf, *h_act = im->h_buf + 2;
+        CGK(cudaMemcpyAsync(h_na, im->Sc.nactive, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CGK(cudaMemcpyAsync(h_act, im->Sc.active, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
         CGK(cudaStreamSynchronize(st));
-        if (*im->h_nactive == 0 || it > cg.max_iters + check_every) break;
+        const int na = *h_na;
+        if (na == 0 || it > cg.max_iters + check_every) break;
+        // compaction: halve the layout while the live lanes fit
+        int kp_new = kp;
+        while (kp_new > 1 && na <= kp_new / 2) kp_new /= 2;
+        if (kp_new < kp) {
+            // live lanes keep ascending shift order; frozen valid lanes hand their
+            // x to the full-width solution; padding lanes (a copy of lane map[0],
+            // inactive, invalid) fill the new width
+            std::vector<int> map, drop(kp, 0);
+            for (int l = 0; l < kp; ++l) {
+                if (h_act[l]) map.push_back(l);
+                else if (valid[l]) drop[l] = 1;
+            }
+            const int live = (int)map.size();
+            for (int l = live; l < kp_new; ++l) map.push_back(map[0]);
+            // current p: the buffer the last spmv wrote (parity already toggled)
+            int rc = cg_repack(im, kp, kp_new, map, drop, lane_shift, parity ? 0 : 1, st, err);
+            if (rc) return rc;
+            std::vector<int> act(kp_new, 1);
+            valid.assign(kp_new, 1);
+            for (int l = live; l < kp_new; ++l) act[l] = valid[l] = 0;
+            CGK(cudaMemcpyAsync(im->Sc.active, act.data(), sizeof(int) * kp_new, cudaMemcpyHostToDevice, st));
+            kp = kp_new;
+            g = make_geom(im, kp, n);
+            grid = grid_for(im, g, n);
+        }
     }
-    // status / iteration statistics
-    const int kp = S.kp;
+    // statistics / failures (per current lane -> shift)
     std::vector<int> status(kp), iters(kp);
     CGK(cudaMemcpyAsync(status.data(), im->Sc.status, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
     CGK(cudaMemcpyAsync(iters.data(), im->Sc.iters, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
+    // remaining valid lanes' x -> full-width solution
+    CGK(cudaMemcpyAsync(im->mask, valid.data(), sizeof(int) * kp, cudaMemcpyHostToDevice, st));
+    k_cg_scatter_x<<<(unsigned)((n * kp + 255) / 256), 256, 0, st>>>(im->V.x, im->xout, n, kp, im->kp_full,
+                                                                    im->lane_shift, im->mask);
+    CGK(cudaGetLastError());
     CGK(cudaStreamSynchronize(st));
-    int mx = 0;
-    double mean = 0.0;
-    for (int j = 0; j < cg.k; ++j) {
-        mx = std::max(mx, iters[j]);
-        mean += iters[j];
-        if (iters_out) iters_out[j] += iters[j];
-        if (status[j]) {
-            char buf[256];
-            const char *why = status[j] == 1 ? "COCG breakdown (rho or p^T S p vanished)"
-                            : status[j] == 2 ? "non-finite values in COCG"
-                                             : "COCG did not converge within max_iters";
-            snprintf(buf, sizeof buf, "%s for shift j = %d after %d iterations", why,
-                     cg.shift_offset + j, iters[j]);
-            err = buf;
-            return status[j] == 3 ? REXI_ERR_NOCONV : REXI_ERR_BREAKDOWN;
-        }
+    for (int l = 0; l < kp; ++l) {
+        const int j = lane_shift[l];
+        if (j >= cg.k || !status[l]) continue;
+        char buf[256];
+        const char *why = status[l] == 1 ? "COCG breakdown (rho or p^T S p vanished)"
+                        : status[l] == 2 ? "non-finite values in COCG"
+                                         : "COCG did not converge within max_iters";
+        snprintf(buf, sizeof buf, "%s for shift j = %d after %d iterations", why, cg.shift_offset + j, iters[l]);
+        err = buf;
+        return status[l] == 3 ? REXI_ERR_NOCONV : REXI_ERR_BREAKDOWN;
     }
-    cg.last_iters_max = std::max(cg.last_iters_max, mx);
-    cg.last_iters_mean += mean / std::max(1, cg.k);
+    cg.last_iters_max = std::max(cg.last_iters_max, it);
+    cg.last_iters_mean += it;
     return REXI_OK;
 }
 
-// all shifts, x_j = S_j^{-1} rhs (refined); leaves x in V.x (+ xsave if refined)
+// all shifts, x_j = S_j^{-1} rhs (refined): result x1 (+ x2)
 static int cg_solve_refined(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t st,
-                            int64_t *launches, std::string &err) {
+                            int64_t *launches, std::string &err, const c128 **x1, const c128 **x2) {
     cg.last_iters_max = 0;
     cg.last_iters_mean = 0.0;
     im->V.bshared = im->rhs;
     im->V.bvec = nullptr;
-    im->Sc.tol = cg.tol;
-    int rc = cg_solve(cg, im, S, st, launches, err, nullptr);
+    // with refinement the first solve stops at tol*100 (the dd-residual
+    // correction supplies the remaining digits), the correction at 1e-4
+    const double tol1 = cg.refine > 0 ? std::min(1e-8, cg.tol * 100.0) : cg.tol;
+    int rc = cg_solve(cg, im, S, st, launches, err, tol1);
     if (rc) return rc;
+    *x1 = im->xout;
+    *x2 = nullptr;
+    if (cg.refine <= 0) return REXI_OK;
     const int64_t n = cg.n;
-    const int kp = S.kp;
+    const int kp = im->kp_full;
+    CGK(cudaMemcpyAsync(im->xsave, im->xout, sizeof(c128) * n * kp, cudaMemcpyDeviceToDevice, st));
     for (int r = 0; r < cg.refine; ++r) {
-        // true residual in double-double against the accumulated solution
-        if (r == 0) CGK(cudaMemcpyAsync(im->xsave, im->V.x, sizeof(c128) * n * kp, cudaMemcpyDeviceToDevice, st));
-        else CGK(cocg_axpy_inplace(im->xsave, im->V.x, n * kp, st));
-        CgVec Vr = im->V;
-        Vr.x = im->xsave;
-        k_cg_residual<<<im->grid, CG_NT, 0, st>>>(im->M, Vr, S, im->g, im->res);
+        if (r > 0) CGK(cocg_axpy_inplace(im->xsave, im->xout, n * kp, st));
+        k_cg_residual<<<(unsigned)((n * kp + CG_NT - 1) / CG_NT), CG_NT, 0, st>>>(im->M, im->rhs, im->xsave, S, kp,
+                                                                               im->res);
         CGK(cudaGetLastError());
         ++*launches;
         im->V.bshared = nullptr;
         im->V.bvec = im->res;
-        im->Sc.tol = std::max(1e-8, cg.tol);
-        rc = cg_solve(cg, im, S, st, launches, err, nullptr);
+        rc = cg_solve(cg, im, S, st, launches, err, 1e-4);
         im->V.bshared = im->rhs;
         im->V.bvec = nullptr;
-        im->Sc.tol = cg.tol;
         if (rc) return rc;
     }
+    *x1 = im->xsave;
+    *x2 = im->xout;
     return REXI_OK;
 }
 
@@ -634,12 +766,10 @@ int cocg_step(CocgState &cg, const ShiftDev &S, cudaStream_t st, const c128 *u, 
     k_cg_rhs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(im->M, u, im->rhs);
     CGK(cudaGetLastError());
     ++*launches;
-    int rc = cg_solve_refined(cg, im, S, st, launches, err);
+    const c128 *x1 = nullptr, *x2 = nullptr;
+    int rc = cg_solve_refined(cg, im, S, st, launches, err, &x1, &x2);
     if (rc) return rc;
-    // u1 = sum_j beta_j (x_j [+ dx_j])
-    const c128 *x1 = cg.refine > 0 ? im->xsave : im->V.x;
-    const c128 *x2 = cg.refine > 0 ? im->V.x : nullptr;
-    k_cg_accum<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, S.kp, cg.k, S.beta, x1, x2, acc, uout);
+    k_cg_accum<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, im->kp_full, cg.k, S.beta, x1, x2, acc, uout);
     CGK(cudaGetLastError());
     ++*launches;
     return REXI_OK;
@@ -652,12 +782,11 @@ int cocg_solve_all(CocgState &cg, const ShiftDev &S, cudaStream_t st, const c128
     CGK(cudaMemcpyAsync(im->rhs, rhs, sizeof(c128) * n,
                         rhs_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
     int64_t launches = 0;
-    int rc = cg_solve_refined(cg, im, S, st, &launches, err);
+    const c128 *x1 = nullptr, *x2 = nullptr;
+    int rc = cg_solve_refined(cg, im, S, st, &launches, err, &x1, &x2);
     if (rc) return rc;
-    const c128 *x1 = cg.refine > 0 ? im->xsave : im->V.x;
-    const c128 *x2 = cg.refine > 0 ? im->V.x : nullptr;
     const int64_t t = n * (int64_t)cg.k;
-    k_cg_transpose<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(x1, x2, n, S.kp, cg.k, x);
+    k_cg_transpose<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(x1, x2, n, im->kp_full, cg.k, x);
     CGK(cudaGetLastError());
     return REXI_OK;
 }
@@ -667,7 +796,7 @@ void cocg_destroy(CocgState &cg) {
     cg.allocs.clear();
     if (cg.impl) {
         CocgImpl *im = (CocgImpl *)cg.impl;
-        if (im->h_nactive) cudaFreeHost(im->h_nactive);
+        if (im->h_buf) cudaFreeHost(im->h_buf);
         delete im;
         cg.impl = nullptr;
     }
