@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -732,7 +733,10 @@ static int cg_solve_refined(CocgState &cg, CocgImpl *im, const ShiftDev &S, cuda
     im->V.bvec = nullptr;
     // with refinement the first solve stops at tol*100 (the dd-residual
     // correction supplies the remaining digits), the correction at 1e-4
-    const double tol1 = cg.refine > 0 ? std::min(1e-8, cg.tol * 100.0) : cg.tol;
+    double tol1 = cg.refine > 0 ? std::min(1e-8, cg.tol * 100.0) : cg.tol;
+    double tol2 = 1e-6;
+    if (const char *e = getenv("REXI_COCG_TOL1")) tol1 = atof(e);   // tuning knobs
+    if (const char *e = getenv("REXI_COCG_TOL2")) tol2 = atof(e);
     int rc = cg_solve(cg, im, S, st, launches, err, tol1);
     if (rc) return rc;
     *x1 = im->xout;
@@ -749,7 +753,7 @@ static int cg_solve_refined(CocgState &cg, CocgImpl *im, const ShiftDev &S, cuda
         ++*launches;
         im->V.bshared = nullptr;
         im->V.bvec = im->res;
-        rc = cg_solve(cg, im, S, st, launches, err, 1e-4);
+        rc = cg_solve(cg, im, S, st, launches, err, tol2);
         im->V.bshared = im->rhs;
         im->V.bvec = nullptr;
         if (rc) return rc;
