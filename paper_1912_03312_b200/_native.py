@@ -230,13 +230,13 @@ class NativePlan:
         raise_status(lib().rexi_plan_profile(self._h, 1 if enable else 0), self._err())
 
     def profile_report(self) -> dict:
-        """{kernel: (launches, total_ms)} since the last profile(True)."""
+        """{kernel: (launches, total_ms, algorithmic_bytes or 0)} since profile(True)."""
         buf = ctypes.create_string_buffer(1 << 16)
         raise_status(lib().rexi_plan_profile_report(self._h, buf, len(buf)), self._err())
         out = {}
         for line in buf.value.decode().splitlines():
-            name, cnt, ms = line.split()
-            out[name] = (int(cnt), float(ms))
+            name, cnt, ms, nbytes = line.split()
+            out[name] = (int(cnt), float(ms), float(nbytes))
         return out
 
     def close(self):

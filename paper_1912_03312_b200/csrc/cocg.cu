@@ -457,6 +457,13 @@ cudaError_t cocg_axpy_inplace(c128 *x, const c128 *y, int64_t n, cudaStream_t st
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+static inline void hook_begin(CocgState &cg, const char *name, double bytes) {
+    if (cg.hook) cg.hook->begin(name, bytes);
+}
+static inline void hook_end(CocgState &cg) {
+    if (cg.hook) cg.hook->end();
+}
+
 struct CocgImpl {
     CgMat M{};
     CgVec V{};
@@ -652,15 +659,23 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     im->Sc.tol = tol;
     CgGeom g = make_geom(im, kp, n);
     int grid = grid_for(im, g, n);
+    const double nnzb = 28.0 * (double)cg.nnz + 4.0 * (double)(n + 1);   // CSR pattern + 3 value arrays
+    hook_begin(cg, "cg_init", 96.0 * n * kp);
     k_cg_init<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, cg.k);
+    hook_end(cg);
     CGK(cudaGetLastError());
     ++*launches;
+    int live = cg.k;
     int it = 0, parity = 0;
     const int check_every = 8;
     for (;;) {
         for (int s = 0; s < check_every; ++s) {
+            hook_begin(cg, "cg_spmv", 64.0 * n * live + nnzb);
             k_cg_spmv<<<(int)std::min<int64_t>(g.nchunks, (int64_t)im->sms * 8), CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
+            hook_end(cg);
+            hook_begin(cg, "cg_update", 112.0 * n * live + 24.0 * n);
             k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity, cg.max_iters);
+            hook_end(cg);
             parity ^= 1;
             *launches += 2;
             ++it;
@@ -671,6 +686,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
         CGK(cudaMemcpyAsync(h_act, im->Sc.active, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
         CGK(cudaStreamSynchronize(st));
         const int na = *h_na;
+        live = na;
         if (na == 0 || it > cg.max_iters + check_every) break;
         // compaction: halve the layout while the live lanes fit
         int kp_new = kp;
@@ -747,8 +763,10 @@ static int cg_solve_refined(CocgState &cg, CocgImpl *im, const ShiftDev &S, cuda
     CGK(cudaMemcpyAsync(im->xsave, im->xout, sizeof(c128) * n * kp, cudaMemcpyDeviceToDevice, st));
     for (int r = 0; r < cg.refine; ++r) {
         if (r > 0) CGK(cocg_axpy_inplace(im->xsave, im->xout, n * kp, st));
+        hook_begin(cg, "cg_residual", 32.0 * n * cg.k + 28.0 * cg.nnz);
         k_cg_residual<<<(unsigned)((n * kp + CG_NT - 1) / CG_NT), CG_NT, 0, st>>>(im->M, im->rhs, im->xsave, S, kp,
                                                                                im->res);
+        hook_end(cg);
         CGK(cudaGetLastError());
         ++*launches;
         im->V.bshared = nullptr;
@@ -773,7 +791,9 @@ int cocg_step(CocgState &cg, const ShiftDev &S, cudaStream_t st, const c128 *u, 
     const c128 *x1 = nullptr, *x2 = nullptr;
     int rc = cg_solve_refined(cg, im, S, st, launches, err, &x1, &x2);
     if (rc) return rc;
+    hook_begin(cg, "cg_accum", (x2 ? 32.0 : 16.0) * n * cg.k + 32.0 * n);
     k_cg_accum<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, im->kp_full, cg.k, S.beta, x1, x2, acc, uout);
+    hook_end(cg);
     CGK(cudaGetLastError());
     ++*launches;
     return REXI_OK;

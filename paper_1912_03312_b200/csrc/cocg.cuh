@@ -9,7 +9,15 @@
 
 namespace rexi {
 
+// per-launch timing hook (implemented by the plan; begin/end bracket one launch)
+struct ProfHook {
+    virtual void begin(const char *name, double algorithmic_bytes) = 0;
+    virtual void end() = 0;
+    virtual ~ProfHook() {}
+};
+
 struct CocgState {
+    ProfHook *hook = nullptr;
     int64_t n = 0, nnz = 0;
     int k = 0;
     int refine = 0;

@@ -55,10 +55,19 @@ struct rexi_plan {
     int64_t launches = 0;
     // optional per-kernel CUDA-event profiling (rexi_plan_profile)
     bool prof = false;
-    struct Rec { const char *name; cudaEvent_t a, b; };
+    struct Rec { const char *name; cudaEvent_t a, b; double bytes; };
+    struct Acc { int64_t count = 0; double ms = 0.0, bytes = 0.0; };
     std::vector<Rec> pending;
     std::vector<cudaEvent_t> pool;
-    std::map<std::string, std::pair<int64_t, double>> prof_acc;
+    std::map<std::string, Acc> prof_acc;
+    struct Hook : rexi::ProfHook {
+        rexi_plan *p = nullptr;
+        cudaEvent_t a = nullptr;
+        const char *name = nullptr;
+        double bytes = 0.0;
+        void begin(const char *n, double b) override;
+        void end() override;
+    } hook;
 };
 
 namespace {
@@ -89,7 +98,7 @@ struct ProfScope {
         if (p->prof) {
             cudaEvent_t b = prof_event(p);
             cudaEventRecord(b, p->stream);
-            p->pending.push_back({name, a, b});
+            p->pending.push_back({name, a, b, 0.0});
         }
     }
 };
@@ -101,13 +110,33 @@ void prof_flush(rexi_plan *p) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, r.a, r.b);
         auto &acc = p->prof_acc[r.name];
-        acc.first += 1;
-        acc.second += ms;
+        acc.count += 1;
+        acc.ms += ms;
+        acc.bytes += r.bytes;
         p->pool.push_back(r.a);
         p->pool.push_back(r.b);
     }
     p->pending.clear();
 }
+
+}  // namespace
+
+void rexi_plan::Hook::begin(const char *n, double b) {
+    if (!p->prof) return;
+    name = n;
+    bytes = b;
+    a = prof_event(p);
+    cudaEventRecord(a, p->stream);
+}
+
+void rexi_plan::Hook::end() {
+    if (!p->prof) return;
+    cudaEvent_t b = prof_event(p);
+    cudaEventRecord(b, p->stream);
+    p->pending.push_back({name, a, b, bytes});
+}
+
+namespace {
 
 int set_err(rexi_plan *p, int code, const std::string &msg) {
     g_last_error = msg;
@@ -557,6 +586,8 @@ int rexi_plan_profile(rexi_plan *plan, int32_t enable) {
     prof_flush(plan);
     plan->prof = enable != 0;
     plan->prof_acc.clear();
+    plan->hook.p = plan;
+    plan->cg.hook = &plan->hook;
     return REXI_OK;
 }
 
@@ -566,8 +597,8 @@ int rexi_plan_profile_report(rexi_plan *plan, char *buf, int64_t len) {
     std::string s;
     char line[256];
     for (auto &kv : plan->prof_acc) {
-        snprintf(line, sizeof line, "%s %lld %.6f\n", kv.first.c_str(), (long long)kv.second.first,
-                 kv.second.second);
+        snprintf(line, sizeof line, "%s %lld %.6f %.0f\n", kv.first.c_str(), (long long)kv.second.count,
+                 kv.second.ms, kv.second.bytes);
         s += line;
     }
     if ((int64_t)s.size() + 1 > len) return set_err(plan, REXI_ERR_INVALID, "buffer too small");
