@@ -43,7 +43,6 @@ namespace rexi {
 
 constexpr int CG_NT = 256;            // threads per CTA (8 warps)
 constexpr int CG_WARPS = CG_NT / 32;
-constexpr int CG_CHUNK_PASSES = 8;    // row slots per chunk = passes * rows per CTA pass
 
 struct CgMat {
     int64_t n;
@@ -87,19 +86,31 @@ __device__ __forceinline__ void cta_geom(const CgGeom &g, int &lane, int &slot, 
     slots = (CG_WARPS / g.G) * g.rpw;
 }
 
-// fixed-order CTA reduction: thread u's value summed into sm[lane(u)] in thread order
-template <typename T, typename Add>
-__device__ __forceinline__ void cta_sum(T v, const CgGeom &g, T *sm, T *out, Add add, T zero) {
-    sm[threadIdx.x] = v;
+// faster fixed-order CTA reduction: lanes sharing a shift inside a warp
+// (rows-per-warp > 1) combine by a butterfly, then thread t < kp sums the
+// warps of its shift group in warp order
+__device__ __forceinline__ double warp_same_shift(double v, int kw) {
+    for (int off = kw; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+__device__ __forceinline__ void cta_sum2(double2 v, double r, const CgGeom &g, double2 *smc, double *smr,
+                                         double2 *outc, double *outr) {
+    v.x = warp_same_shift(v.x, g.kw);
+    v.y = warp_same_shift(v.y, g.kw);
+    r = warp_same_shift(r, g.kw);
+    smc[threadIdx.x] = v;
+    smr[threadIdx.x] = r;
     __syncthreads();
     if (threadIdx.x < g.kp) {
-        T s = zero;
-        for (int u = 0; u < CG_NT; ++u) {
-            const int w = u >> 5, l = u & 31;
-            if ((w % g.G) * g.kw + (l % g.kw) == (int)threadIdx.x && (w / g.G) < CG_WARPS / g.G)
-                s = add(s, sm[u]);
+        const int grp = threadIdx.x / g.kw, sl = threadIdx.x % g.kw;
+        double2 s = make_double2(0.0, 0.0);
+        double sr = 0.0;
+        for (int w = grp; w < CG_WARPS; w += g.G) {
+            s = cadd(s, smc[w * 32 + sl]);
+            sr += smr[w * 32 + sl];
         }
-        out[threadIdx.x] = s;
+        outc[threadIdx.x] = s;
+        outr[threadIdx.x] = sr;
     }
     __syncthreads();
 }
@@ -140,8 +151,7 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
         rho = cadd(rho, cmul(b, z));
         bn += cabs2(b);
     }
-    cta_sum<double2>(rho, g, smc, outc, [](double2 a, double2 b) { return cadd(a, b); }, make_double2(0, 0));
-    cta_sum<double>(bn, g, smr, outr, [](double a, double b) { return a + b; }, 0.0);
+    cta_sum2(rho, bn, g, smc, smr, outc, outr);
     if (threadIdx.x < kp) {
         Sc.part_b[(size_t)blockIdx.x * kp + threadIdx.x] = outc[threadIdx.x];
         Sc.part_c[(size_t)blockIdx.x * kp + threadIdx.x] = outr[threadIdx.x];
@@ -174,42 +184,45 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
 }
 
 // ---------------------------------------------------------------------------
-// spmv: p_new = z + beta p_old (own row), q = S p_new, mu = p^T q  -> alpha
+// spmv: p_new = z + beta p_old (own row), q = S p_new, mu = p^T q.
+// Work unit = (row chunk, shift group), claimed per warp from an atomic
+// counter (no CTA barriers); a unit's per-lane partial goes to
+// part_a[chunk][lane], and k_cg_spmv_finish sums them in chunk order.
 // ---------------------------------------------------------------------------
+template <bool CPLX>
 __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g,
                                                     int parity) {
-    __shared__ double2 smc[CG_NT];
-    __shared__ double2 outc[CG_NT];
-    __shared__ int64_t chunk_sh;
     if (*Sc.nactive == 0) return;
-    int lane, slot, slots;
-    cta_geom(g, lane, slot, slots);
+    const int l = threadIdx.x & 31;
     const int kp = g.kp;
-    const bool act = Sc.active[lane] != 0;
-    const c128 sg = S.sigma[g.lane_shift[lane]];
-    const c128 beta = Sc.beta[lane];
-    const c128 *pold = parity ? V.p1 : V.p0;
-    c128 *pnew = parity ? V.p0 : V.p1;
-    unsigned int *claim = Sc.ctr + (parity & 1);
-    unsigned int *done = Sc.ctr + 2 + (parity & 1);
+    const int sl = l % g.kw, roff = l / g.kw;
+    const c128 *__restrict__ pold = parity ? V.p1 : V.p0;
+    c128 *__restrict__ pnew = parity ? V.p0 : V.p1;
+    const c128 *__restrict__ zv = V.z;
+    const unsigned units = (unsigned)(g.nchunks * g.G);
     for (;;) {
-        if (threadIdx.x == 0) chunk_sh = (int64_t)atomicAdd(claim, 1u);
-        __syncthreads();
-        const int64_t chunk = chunk_sh;
-        __syncthreads();
-        if (chunk >= g.nchunks) break;
+        unsigned u = 0;
+        if (l == 0) u = atomicAdd(Sc.ctr, 1u);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= units) break;
+        const int64_t chunk = u / g.G;
+        const int lane = (int)(u % g.G) * g.kw + sl;
         c128 mu = cmk(0.0, 0.0);
-        if (act) {
+        if (Sc.active[lane]) {
+            const c128 sg = S.sigma[g.lane_shift[lane]];
+            const c128 beta = Sc.beta[lane];
             const int64_t r0 = chunk * g.chunk_rows;
             const int64_t r1 = min(r0 + g.chunk_rows, M.n);
-            for (int64_t i = r0 + slot; i < r1; i += slots) {
+            for (int64_t i = r0 + roff; i < r1; i += g.rpw) {
                 c128 acc = cmk(0.0, 0.0), pi = cmk(0.0, 0.0);
-                const int32_t q0 = M.indptr[i], q1 = M.indptr[i + 1];
+                const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
+#pragma unroll 4
                 for (int32_t q = q0; q < q1; ++q) {
-                    const int64_t c = M.indices[q];
+                    const int32_t c = __ldg(M.indices + q);
                     const size_t oc = (size_t)c * kp + lane;
-                    const c128 pc = cadd(V.z[oc], cmul(beta, pold[oc]));
-                    acc = cadd(acc, cmul(form_entry(M.ta[q], M.ta_im[q], M.b[q], sg), pc));
+                    const c128 pc = cadd(zv[oc], cmul(beta, pold[oc]));
+                    const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
+                    acc = cadd(acc, cmul(e, pc));
                     if (c == i) pi = pc;
                 }
                 const size_t o = (size_t)i * kp + lane;
@@ -218,37 +231,49 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, 
                 mu = cadd(mu, cmul(pi, acc));
             }
         }
-        cta_sum<double2>(mu, g, smc, outc, [](double2 a, double2 b) { return cadd(a, b); }, make_double2(0, 0));
-        if (threadIdx.x < kp) Sc.part_a[(size_t)chunk * kp + threadIdx.x] = outc[threadIdx.x];
-        if (arrive_last(done, (unsigned)g.nchunks)) {
-            // fixed-order finish: thread t handles lane t % kp, chunks strided by CG_NT / kp
-            const int sub = CG_NT / kp > 0 ? CG_NT / kp : 1;
-            double2 s = make_double2(0.0, 0.0);
-            if (threadIdx.x < sub * kp) {
-                const int t = threadIdx.x % kp, sidx = threadIdx.x / kp;
-                for (int64_t c = sidx; c < g.nchunks; c += sub) s = cadd(s, Sc.part_a[(size_t)c * kp + t]);
+        // lanes holding the same shift (rpw > 1): fixed butterfly
+        for (int off = g.kw; off < 32; off <<= 1) {
+            mu.x += __shfl_xor_sync(0xffffffffu, mu.x, off);
+            mu.y += __shfl_xor_sync(0xffffffffu, mu.y, off);
+        }
+        if (roff == 0) Sc.part_a[(size_t)chunk * kp + lane] = mu;
+    }
+}
+
+// alpha = rho / sum_chunks(mu), one CTA of CG_FIN threads, fixed order
+constexpr int CG_FIN = 1024;
+__global__ void __launch_bounds__(CG_FIN) k_cg_spmv_finish(CgScal Sc, CgGeom g) {
+    __shared__ double2 sm[CG_FIN];
+    if (*Sc.nactive == 0) return;
+    const int kp = g.kp;
+    const int sub = CG_FIN / kp;
+    const int t = threadIdx.x % kp, sidx = threadIdx.x / kp;
+    double2 s0 = make_double2(0.0, 0.0), s1 = s0;
+    if (sidx < sub) {
+        int64_t c = sidx;
+        for (; c + sub < g.nchunks; c += 2 * sub) {
+            s0 = cadd(s0, Sc.part_a[(size_t)c * kp + t]);
+            s1 = cadd(s1, Sc.part_a[(size_t)(c + sub) * kp + t]);
+        }
+        if (c < g.nchunks) s0 = cadd(s0, Sc.part_a[(size_t)c * kp + t]);
+    }
+    sm[threadIdx.x] = cadd(s0, s1);
+    __syncthreads();
+    if (threadIdx.x < kp) {
+        double2 m = make_double2(0.0, 0.0);
+        for (int q = 0; q < sub; ++q) m = cadd(m, sm[q * kp + threadIdx.x]);
+        if (Sc.active[threadIdx.x]) {
+            const double ms = cabs2(m);
+            if (!(ms > 0.0) || !isfinite(ms)) {
+                Sc.status[threadIdx.x] = isfinite(ms) ? 1 : 2;
+                Sc.active[threadIdx.x] = 0;
+                Sc.alpha[threadIdx.x] = make_double2(0.0, 0.0);
+            } else {
+                Sc.alpha[threadIdx.x] = cdiv_c(Sc.rho[threadIdx.x], m);
             }
-            smc[threadIdx.x] = s;
-            __syncthreads();
-            for (int t = threadIdx.x; t < kp; t += CG_NT) {
-                double2 m = make_double2(0.0, 0.0);
-                for (int sidx = 0; sidx < sub; ++sidx) m = cadd(m, smc[sidx * kp + t]);
-                if (Sc.active[t]) {
-                    const double ms = cabs2(m);
-                    if (!(ms > 0.0) || !isfinite(ms)) {
-                        Sc.status[t] = isfinite(ms) ? 1 : 2;
-                        Sc.active[t] = 0;
-                        Sc.alpha[t] = make_double2(0.0, 0.0);
-                    } else {
-                        Sc.alpha[t] = cdiv_c(Sc.rho[t], m);
-                    }
-                }
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) Sc.ctr[2 + ((parity + 1) & 1)] = 0, Sc.ctr[(parity + 1) & 1] = 0;
-            break;
         }
     }
+    if (threadIdx.x == 0) Sc.ctr[0] = 0;   // claim counter for the next spmv
 }
 
 // ---------------------------------------------------------------------------
@@ -271,7 +296,29 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
     c128 rho = cmk(0.0, 0.0);
     double rn = 0.0;
     if (act) {
-        for (int64_t i = (int64_t)blockIdx.x * slots + slot; i < M.n; i += (int64_t)gridDim.x * slots) {
+        const int64_t step = (int64_t)gridDim.x * slots;
+        int64_t i = (int64_t)blockIdx.x * slots + slot;
+        // two rows per trip: twice the loads in flight
+        for (; i + step < M.n; i += 2 * step) {
+            const size_t o0 = (size_t)i * kp + lane, o1 = (size_t)(i + step) * kp + lane;
+            const c128 p0 = pnew[o0], q0 = V.q[o0], x0 = V.x[o0], r0 = V.r[o0];
+            const c128 p1 = pnew[o1], q1 = V.q[o1], x1 = V.x[o1], r1 = V.r[o1];
+            const c128 d0 = form_entry(M.dta[i], M.dta_im[i], M.db[i], sg);
+            const c128 d1 = form_entry(M.dta[i + step], M.dta_im[i + step], M.db[i + step], sg);
+            V.x[o0] = cadd(x0, cmul(alpha, p0));
+            V.x[o1] = cadd(x1, cmul(alpha, p1));
+            const c128 ra = csub(r0, cmul(alpha, q0)), rb = csub(r1, cmul(alpha, q1));
+            V.r[o0] = ra;
+            V.r[o1] = rb;
+            const c128 za = cdiv_c(ra, d0), zb = cdiv_c(rb, d1);
+            V.z[o0] = za;
+            V.z[o1] = zb;
+            rho = cadd(rho, cmul(ra, za));
+            rho = cadd(rho, cmul(rb, zb));
+            rn += cabs2(ra);
+            rn += cabs2(rb);
+        }
+        if (i < M.n) {
             const size_t o = (size_t)i * kp + lane;
             const c128 p = pnew[o], q = V.q[o];
             V.x[o] = cadd(V.x[o], cmul(alpha, p));
@@ -283,8 +330,7 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
             rn += cabs2(r);
         }
     }
-    cta_sum<double2>(rho, g, smc, outc, [](double2 a, double2 b) { return cadd(a, b); }, make_double2(0, 0));
-    cta_sum<double>(rn, g, smr, outr, [](double a, double b) { return a + b; }, 0.0);
+    cta_sum2(rho, rn, g, smc, smr, outc, outr);
     if (threadIdx.x < kp) {
         Sc.part_b[(size_t)blockIdx.x * kp + threadIdx.x] = outc[threadIdx.x];
         Sc.part_c[(size_t)blockIdx.x * kp + threadIdx.x] = outr[threadIdx.x];
@@ -465,6 +511,7 @@ static inline void hook_end(CocgState &cg) {
 }
 
 struct CocgImpl {
+    bool cplx = false;         // A has an imaginary part
     CgMat M{};
     CgVec V{};
     CgScal Sc{};
@@ -512,8 +559,12 @@ static CgGeom make_geom(const CocgImpl *im, int kp, int64_t n) {
     g.kw = kp < 32 ? kp : 32;
     g.G = kp / g.kw;
     g.rpw = 32 / g.kw;
-    g.chunk_rows = (int64_t)(CG_WARPS / g.G) * g.rpw * CG_CHUNK_PASSES;
-    g.nchunks = (n + g.chunk_rows - 1) / g.chunk_rows;
+    // ~2 work units (row chunk x shift group) per resident warp, chunk a multiple of rpw
+    const int64_t target_units = (int64_t)im->sms * 8 * CG_WARPS * 2;
+    int64_t rows = std::max<int64_t>(1, (n * g.G + target_units - 1) / target_units);
+    rows = (rows + g.rpw - 1) / g.rpw * g.rpw;
+    g.chunk_rows = rows;
+    g.nchunks = (n + rows - 1) / rows;
     g.lane_shift = im->lane_shift;
     return g;
 }
@@ -544,6 +595,7 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
         for (int32_t q = d->indptr[r]; q < d->indptr[r + 1]; ++q) {
             ta[q] = d->tau * d->a_vals[q];
             tai[q] = d->a_imag ? d->tau * d->a_imag[q] : 0.0;
+            if (tai[q] != 0.0) im->cplx = true;
             bb[q] = d->b_vals[q];
             if (d->indices[q] == r) {
                 dta[r] = ta[q];
@@ -606,8 +658,9 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     CGA(Sc.iters, sizeof(int) * kp);
     CGA(Sc.status, sizeof(int) * kp);
     CGA(Sc.nactive, sizeof(int));
-    const CgGeom g1 = make_geom(im, 1, n);     // the most chunks any layout can have
-    CGA(Sc.part_a, sizeof(double2) * (size_t)kp * std::max<int64_t>(g1.nchunks, make_geom(im, kp, n).nchunks));
+    int64_t part_max = 1;                     // largest nchunks*kp over the layouts compaction can reach
+    for (int w = 1; w <= kp; w *= 2) part_max = std::max<int64_t>(part_max, make_geom(im, w, n).nchunks * w);
+    CGA(Sc.part_a, sizeof(double2) * (size_t)part_max);
     CGA(Sc.part_b, sizeof(double2) * (size_t)kp * im->sms * 8);
     CGA(Sc.part_c, sizeof(double) * (size_t)kp * im->sms * 8);
     CGA(Sc.ctr, sizeof(unsigned int) * 8);
@@ -671,13 +724,16 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     for (;;) {
         for (int s = 0; s < check_every; ++s) {
             hook_begin(cg, "cg_spmv", 64.0 * n * live + nnzb);
-            k_cg_spmv<<<(int)std::min<int64_t>(g.nchunks, (int64_t)im->sms * 8), CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
+            const int sgrid = (int)std::min<int64_t>((g.nchunks * g.G + CG_WARPS - 1) / CG_WARPS, (int64_t)im->sms * 8);
+            if (im->cplx) k_cg_spmv<true><<<sgrid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
+            else k_cg_spmv<false><<<sgrid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
+            k_cg_spmv_finish<<<1, CG_FIN, 0, st>>>(im->Sc, g);
             hook_end(cg);
             hook_begin(cg, "cg_update", 112.0 * n * live + 24.0 * n);
             k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity, cg.max_iters);
             hook_end(cg);
             parity ^= 1;
-            *launches += 2;
+            *launches += 3;
             ++it;
         }
         CGK(cudaGetLastError());
