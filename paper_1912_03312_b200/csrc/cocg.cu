@@ -185,35 +185,39 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
 
 // ---------------------------------------------------------------------------
 // spmv: p_new = z + beta p_old (own row), q = S p_new, mu = p^T q.
-// Work unit = (row chunk, shift group), claimed per warp from an atomic
-// counter (no CTA barriers); a unit's per-lane partial goes to
-// part_a[chunk][lane], and k_cg_spmv_finish sums them in chunk order.
+// Row chunks are claimed per CTA from an atomic counter (one coherent
+// wavefront of ~grid*chunk rows, so the +-n neighbour rows of the stencil are
+// L2 hits); the next claim is prefetched and the per-lane reduction buffer is
+// double-buffered, so a chunk costs one barrier.  part_a[chunk][lane] is
+// summed in chunk order by k_cg_spmv_finish (deterministic).
 // ---------------------------------------------------------------------------
 template <bool CPLX>
 __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g,
                                                     int parity) {
+    __shared__ double2 red[2][CG_NT];
+    __shared__ int64_t claim_q[2];
     if (*Sc.nactive == 0) return;
-    const int l = threadIdx.x & 31;
+    int lane, slot, slots;
+    cta_geom(g, lane, slot, slots);
     const int kp = g.kp;
-    const int sl = l % g.kw, roff = l / g.kw;
+    const bool act = Sc.active[lane] != 0;
+    const c128 sg = S.sigma[g.lane_shift[lane]];
+    const c128 beta = Sc.beta[lane];
     const c128 *__restrict__ pold = parity ? V.p1 : V.p0;
     c128 *__restrict__ pnew = parity ? V.p0 : V.p1;
     const c128 *__restrict__ zv = V.z;
-    const unsigned units = (unsigned)(g.nchunks * g.G);
+    if (threadIdx.x == 0) claim_q[0] = (int64_t)atomicAdd(Sc.ctr, 1u);
+    __syncthreads();
+    int buf = 0;
     for (;;) {
-        unsigned u = 0;
-        if (l == 0) u = atomicAdd(Sc.ctr, 1u);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (u >= units) break;
-        const int64_t chunk = u / g.G;
-        const int lane = (int)(u % g.G) * g.kw + sl;
+        const int64_t chunk = claim_q[buf];
+        if (chunk >= g.nchunks) break;
+        if (threadIdx.x == 0) claim_q[buf ^ 1] = (int64_t)atomicAdd(Sc.ctr, 1u);
         c128 mu = cmk(0.0, 0.0);
-        if (Sc.active[lane]) {
-            const c128 sg = S.sigma[g.lane_shift[lane]];
-            const c128 beta = Sc.beta[lane];
+        if (act) {
             const int64_t r0 = chunk * g.chunk_rows;
             const int64_t r1 = min(r0 + g.chunk_rows, M.n);
-            for (int64_t i = r0 + roff; i < r1; i += g.rpw) {
+            for (int64_t i = r0 + slot; i < r1; i += slots) {
                 c128 acc = cmk(0.0, 0.0), pi = cmk(0.0, 0.0);
                 const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
 #pragma unroll 4
@@ -231,12 +235,17 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, 
                 mu = cadd(mu, cmul(pi, acc));
             }
         }
-        // lanes holding the same shift (rpw > 1): fixed butterfly
-        for (int off = g.kw; off < 32; off <<= 1) {
-            mu.x += __shfl_xor_sync(0xffffffffu, mu.x, off);
-            mu.y += __shfl_xor_sync(0xffffffffu, mu.y, off);
+        mu.x = warp_same_shift(mu.x, g.kw);
+        mu.y = warp_same_shift(mu.y, g.kw);
+        red[buf][threadIdx.x] = mu;
+        __syncthreads();   // red[buf] complete, claim_q[buf^1] visible
+        if (threadIdx.x < kp) {
+            const int grp = threadIdx.x / g.kw, sl = threadIdx.x % g.kw;
+            double2 s = make_double2(0.0, 0.0);
+            for (int w = grp; w < CG_WARPS; w += g.G) s = cadd(s, red[buf][w * 32 + sl]);
+            Sc.part_a[(size_t)chunk * kp + threadIdx.x] = s;
         }
-        if (roff == 0) Sc.part_a[(size_t)chunk * kp + lane] = mu;
+        buf ^= 1;
     }
 }
 
@@ -559,12 +568,10 @@ static CgGeom make_geom(const CocgImpl *im, int kp, int64_t n) {
     g.kw = kp < 32 ? kp : 32;
     g.G = kp / g.kw;
     g.rpw = 32 / g.kw;
-    // ~2 work units (row chunk x shift group) per resident warp, chunk a multiple of rpw
-    const int64_t target_units = (int64_t)im->sms * 8 * CG_WARPS * 2;
-    int64_t rows = std::max<int64_t>(1, (n * g.G + target_units - 1) / target_units);
-    rows = (rows + g.rpw - 1) / g.rpw * g.rpw;
-    g.chunk_rows = rows;
-    g.nchunks = (n + rows - 1) / rows;
+    // a chunk = 8 CTA passes (32 rows at 64 lanes): the in-flight wavefront is
+    // ~grid*chunk rows, narrow enough for the stencil's +-n rows to stay in L2
+    g.chunk_rows = (int64_t)(CG_WARPS / g.G) * g.rpw * 8;
+    g.nchunks = (n + g.chunk_rows - 1) / g.chunk_rows;
     g.lane_shift = im->lane_shift;
     return g;
 }
@@ -724,7 +731,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     for (;;) {
         for (int s = 0; s < check_every; ++s) {
             hook_begin(cg, "cg_spmv", 64.0 * n * live + nnzb);
-            const int sgrid = (int)std::min<int64_t>((g.nchunks * g.G + CG_WARPS - 1) / CG_WARPS, (int64_t)im->sms * 8);
+            const int sgrid = (int)std::min<int64_t>(g.nchunks, (int64_t)im->sms * 8);
             if (im->cplx) k_cg_spmv<true><<<sgrid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
             else k_cg_spmv<false><<<sgrid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
             k_cg_spmv_finish<<<1, CG_FIN, 0, st>>>(im->Sc, g);

@@ -1,0 +1,38 @@
+"""Summarise ncu captures: python scripts/ncu_summary.py raw <rep>  |  launches <csv>"""
+import csv, collections, subprocess, sys
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "lts__t_sector_op_read_hit_rate.pct", "sm__warps_active.avg.per_cycle_active",
+            "launch__registers_per_thread", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "smsp__inst_executed.sum", "launch__grid_size"]
+    st = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")]
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")].split("(")[0]
+        t = float(r[hdr.index("gpu__time_duration.sum")]) * (1e-3 if units[hdr.index("gpu__time_duration.sum")] == "usecond" else 1.0)
+        rd = float(r[hdr.index("dram__bytes_read.sum")]); wr = float(r[hdr.index("dram__bytes_write.sum")])
+        print(f"{name}: " + " | ".join(f"{w.split('__')[-1]}={r[hdr.index(w)]} {units[hdr.index(w)]}" for w in want if w in hdr))
+        vals = sorted(((float(r[i]) if r[i] else 0.0, hdr[i][34:-23]) for i in st), reverse=True)[:5]
+        print("   stalls: " + ", ".join(f"{n}={v:.2f}" for v, n in vals))
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    for i, r in enumerate(rows):
+        if r and r[0] == "ID":
+            hdr = r; start = i + 1; break
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.OrderedDict()
+    for r in rows[start:]:
+        if len(r) <= vi: continue
+        v = float(r[vi].replace(",", "")); u = r[ui]
+        v = v / 1e6 if u == "nsecond" else (v / 1e3 if u == "usecond" else (v if u == "msecond" else v * 1e3))
+        a = agg.setdefault(r[ki].split("(")[0], [0, 0.0]); a[0] += 1; a[1] += v
+    tot = sum(t for _, t in agg.values())
+    for k, (c, t) in agg.items():
+        print(f"{k:28s} {c:6d} launches {t:10.3f} ms  ({100*t/tot:5.1f}%)  avg {1e3*t/c:9.1f} us")
+
+if __name__ == "__main__":
+    {"raw": raw, "launches": launches}[sys.argv[1]](sys.argv[2])
