@@ -43,6 +43,7 @@ namespace rexi {
 
 constexpr int CG_NT = 256;            // threads per CTA (8 warps)
 constexpr int CG_WARPS = CG_NT / 32;
+constexpr int CG_FIN = 1024;          // threads of the finish kernels
 
 struct CgMat {
     int64_t n;
@@ -250,7 +251,6 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, 
 }
 
 // alpha = rho / sum_chunks(mu), one CTA of CG_FIN threads, fixed order
-constexpr int CG_FIN = 1024;
 __global__ void __launch_bounds__(CG_FIN) k_cg_spmv_finish(CgScal Sc, CgGeom g) {
     __shared__ double2 sm[CG_FIN];
     if (*Sc.nactive == 0) return;
@@ -344,41 +344,60 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
         Sc.part_b[(size_t)blockIdx.x * kp + threadIdx.x] = outc[threadIdx.x];
         Sc.part_c[(size_t)blockIdx.x * kp + threadIdx.x] = outr[threadIdx.x];
     }
-    if (arrive_last(Sc.ctr + 5, gridDim.x)) {
-        for (int t = threadIdx.x; t < kp; t += CG_NT) {
-            if (!Sc.active[t]) continue;
-            double2 s = make_double2(0.0, 0.0);
-            double sr = 0.0;
-            for (unsigned c = 0; c < gridDim.x; ++c) {
-                s = cadd(s, Sc.part_b[(size_t)c * kp + t]);
-                sr += Sc.part_c[(size_t)c * kp + t];
-            }
-            Sc.rnorm2[t] = sr;
-            Sc.iters[t] += 1;
-            const double2 rho_old = Sc.rho[t];
-            if (!isfinite(sr) || !isfinite(s.x) || !isfinite(s.y)) {
-                Sc.status[t] = 2;
-                Sc.active[t] = 0;
-            } else if (sr <= Sc.tol * Sc.tol * Sc.bnorm2[t]) {
-                Sc.active[t] = 0;                               // converged: freeze
-            } else if (!(cabs2(rho_old) > 0.0)) {
-                Sc.status[t] = 1;
-                Sc.active[t] = 0;
-            } else if (Sc.iters[t] >= max_iters) {
-                Sc.status[t] = 3;
-                Sc.active[t] = 0;
-            } else {
-                Sc.beta[t] = cdiv_c(s, rho_old);
-                Sc.rho[t] = s;
-            }
+}
+
+// rho' and |r|^2 over the update CTAs (fixed order, parallel), then beta,
+// convergence freeze and failure flags; one CTA of CG_FIN threads
+__global__ void __launch_bounds__(CG_FIN) k_cg_update_finish(CgScal Sc, CgGeom g, int nparts, int max_iters) {
+    __shared__ double2 smc[CG_FIN];
+    __shared__ double smr[CG_FIN];
+    if (*Sc.nactive == 0) return;
+    const int kp = g.kp;
+    const int sub = CG_FIN / kp;
+    const int t = threadIdx.x % kp, sidx = threadIdx.x / kp;
+    double2 s = make_double2(0.0, 0.0);
+    double sr = 0.0;
+    if (sidx < sub)
+        for (int c = sidx; c < nparts; c += sub) {
+            s = cadd(s, Sc.part_b[(size_t)c * kp + t]);
+            sr += Sc.part_c[(size_t)c * kp + t];
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int na = 0;
-            for (int t = 0; t < kp; ++t) na += Sc.active[t];
-            *Sc.nactive = na;
-            Sc.ctr[5] = 0;
+    smc[threadIdx.x] = s;
+    smr[threadIdx.x] = sr;
+    __syncthreads();
+    if (threadIdx.x < kp && Sc.active[threadIdx.x]) {
+        const int l = threadIdx.x;
+        double2 rs = make_double2(0.0, 0.0);
+        double rr = 0.0;
+        for (int q = 0; q < sub; ++q) {
+            rs = cadd(rs, smc[q * kp + l]);
+            rr += smr[q * kp + l];
         }
+        Sc.rnorm2[l] = rr;
+        Sc.iters[l] += 1;
+        const double2 rho_old = Sc.rho[l];
+        if (!isfinite(rr) || !isfinite(rs.x) || !isfinite(rs.y)) {
+            Sc.status[l] = 2;
+            Sc.active[l] = 0;
+        } else if (rr <= Sc.tol * Sc.tol * Sc.bnorm2[l]) {
+            Sc.active[l] = 0;                               // converged: freeze
+        } else if (!(cabs2(rho_old) > 0.0)) {
+            Sc.status[l] = 1;
+            Sc.active[l] = 0;
+        } else if (Sc.iters[l] >= max_iters) {
+            Sc.status[l] = 3;
+            Sc.active[l] = 0;
+        } else {
+            Sc.beta[l] = cdiv_c(rs, rho_old);
+            Sc.rho[l] = rs;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int na = 0;
+        for (int l = threadIdx.x; l < kp; l += 32) na += Sc.active[l];
+        for (int off = 16; off > 0; off >>= 1) na += __shfl_xor_sync(0xffffffffu, na, off);
+        if (threadIdx.x == 0) *Sc.nactive = na;
     }
 }
 
@@ -738,9 +757,10 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             hook_end(cg);
             hook_begin(cg, "cg_update", 112.0 * n * live + 24.0 * n);
             k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity, cg.max_iters);
+            k_cg_update_finish<<<1, CG_FIN, 0, st>>>(im->Sc, g, grid, cg.max_iters);
             hook_end(cg);
             parity ^= 1;
-            *launches += 3;
+            *launches += 4;
             ++it;
         }
         CGK(cudaGetLastError());
