@@ -66,6 +66,7 @@ struct CgScal {                            // per lane of the current layout
     double2 *part_a;                       // spmv partials [nchunks][kp]
     double2 *part_b;                       // update partials [grid][kp]
     double *part_c;                        // update partials [grid][kp]
+    double2 *part_f;                       // spmv finish block partials [CG_FB][kp]
     unsigned int *ctr;                     // [8] claim / done counters (parity)
     double tol;
 };
@@ -250,39 +251,48 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, 
     }
 }
 
-// alpha = rho / sum_chunks(mu), one CTA of CG_FIN threads, fixed order
-__global__ void __launch_bounds__(CG_FIN) k_cg_spmv_finish(CgScal Sc, CgGeom g) {
-    __shared__ double2 sm[CG_FIN];
+// alpha = rho / sum_chunks(mu): CG_FB CTAs each sum a fixed contiguous range
+// of chunks (strided over the CTA's threads), the last CTA to arrive sums the
+// CG_FB block partials in block order -- fixed order, parallel over SMs
+constexpr int CG_FB = 64;
+__global__ void __launch_bounds__(CG_NT) k_cg_spmv_finish(CgScal Sc, CgGeom g) {
+    __shared__ double2 sm[CG_NT];
     if (*Sc.nactive == 0) return;
     const int kp = g.kp;
-    const int sub = CG_FIN / kp;
+    const int sub = CG_NT / kp > 0 ? CG_NT / kp : 1;
     const int t = threadIdx.x % kp, sidx = threadIdx.x / kp;
-    double2 s0 = make_double2(0.0, 0.0), s1 = s0;
-    if (sidx < sub) {
-        int64_t c = sidx;
-        for (; c + sub < g.nchunks; c += 2 * sub) {
-            s0 = cadd(s0, Sc.part_a[(size_t)c * kp + t]);
-            s1 = cadd(s1, Sc.part_a[(size_t)(c + sub) * kp + t]);
-        }
-        if (c < g.nchunks) s0 = cadd(s0, Sc.part_a[(size_t)c * kp + t]);
-    }
-    sm[threadIdx.x] = cadd(s0, s1);
+    const int64_t per = (g.nchunks + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = (int64_t)blockIdx.x * per, c1 = min(c0 + per, g.nchunks);
+    double2 s = make_double2(0.0, 0.0);
+    if (sidx < sub)
+        for (int64_t c = c0 + sidx; c < c1; c += sub) s = cadd(s, Sc.part_a[(size_t)c * kp + t]);
+    sm[threadIdx.x] = s;
     __syncthreads();
     if (threadIdx.x < kp) {
         double2 m = make_double2(0.0, 0.0);
         for (int q = 0; q < sub; ++q) m = cadd(m, sm[q * kp + threadIdx.x]);
-        if (Sc.active[threadIdx.x]) {
+        Sc.part_f[(size_t)blockIdx.x * kp + threadIdx.x] = m;
+    }
+    if (!arrive_last(Sc.ctr + 6, gridDim.x)) return;
+    for (int l = threadIdx.x; l < kp; l += CG_NT) {
+        double2 m = make_double2(0.0, 0.0);
+        for (unsigned blk = 0; blk < gridDim.x; ++blk) m = cadd(m, Sc.part_f[(size_t)blk * kp + l]);
+        if (Sc.active[l]) {
             const double ms = cabs2(m);
             if (!(ms > 0.0) || !isfinite(ms)) {
-                Sc.status[threadIdx.x] = isfinite(ms) ? 1 : 2;
-                Sc.active[threadIdx.x] = 0;
-                Sc.alpha[threadIdx.x] = make_double2(0.0, 0.0);
+                Sc.status[l] = isfinite(ms) ? 1 : 2;
+                Sc.active[l] = 0;
+                Sc.alpha[l] = make_double2(0.0, 0.0);
             } else {
-                Sc.alpha[threadIdx.x] = cdiv_c(Sc.rho[threadIdx.x], m);
+                Sc.alpha[l] = cdiv_c(Sc.rho[l], m);
             }
         }
     }
-    if (threadIdx.x == 0) Sc.ctr[0] = 0;   // claim counter for the next spmv
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Sc.ctr[0] = 0;   // claim counter for the next spmv
+        Sc.ctr[6] = 0;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -587,9 +597,12 @@ static CgGeom make_geom(const CocgImpl *im, int kp, int64_t n) {
     g.kw = kp < 32 ? kp : 32;
     g.G = kp / g.kw;
     g.rpw = 32 / g.kw;
-    // a chunk = 8 CTA passes (32 rows at 64 lanes): the in-flight wavefront is
-    // ~grid*chunk rows, narrow enough for the stencil's +-n rows to stay in L2
-    g.chunk_rows = (int64_t)(CG_WARPS / g.G) * g.rpw * 8;
+    // a chunk = up to 8 CTA passes (32 rows at 64 lanes): the in-flight
+    // wavefront is ~grid*chunk rows, narrow enough for the stencil's +-n rows to
+    // stay in L2; fewer passes when few lanes are live so every SM gets chunks
+    const int64_t pass_rows = (int64_t)(CG_WARPS / g.G) * g.rpw;
+    const int64_t passes = std::max<int64_t>(1, std::min<int64_t>(8, n / (pass_rows * 2 * im->sms * 8)));
+    g.chunk_rows = pass_rows * passes;
     g.nchunks = (n + g.chunk_rows - 1) / g.chunk_rows;
     g.lane_shift = im->lane_shift;
     return g;
@@ -689,6 +702,7 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     CGA(Sc.part_a, sizeof(double2) * (size_t)part_max);
     CGA(Sc.part_b, sizeof(double2) * (size_t)kp * im->sms * 8);
     CGA(Sc.part_c, sizeof(double) * (size_t)kp * im->sms * 8);
+    CGA(Sc.part_f, sizeof(double2) * (size_t)kp * CG_FB);
     CGA(Sc.ctr, sizeof(unsigned int) * 8);
     CGK(cudaMemsetAsync(Sc.ctr, 0, sizeof(unsigned int) * 8, st));
     Sc.tol = cg.tol;
@@ -753,7 +767,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             const int sgrid = (int)std::min<int64_t>(g.nchunks, (int64_t)im->sms * 8);
             if (im->cplx) k_cg_spmv<true><<<sgrid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
             else k_cg_spmv<false><<<sgrid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
-            k_cg_spmv_finish<<<1, CG_FIN, 0, st>>>(im->Sc, g);
+            k_cg_spmv_finish<<<(int)std::min<int64_t>(CG_FB, g.nchunks), CG_NT, 0, st>>>(im->Sc, g);
             hook_end(cg);
             hook_begin(cg, "cg_update", 112.0 * n * live + 24.0 * n);
             k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity, cg.max_iters);
