@@ -43,7 +43,6 @@ namespace rexi {
 
 constexpr int CG_NT = 256;            // threads per CTA (8 warps)
 constexpr int CG_WARPS = CG_NT / 32;
-constexpr int CG_FIN = 1024;          // threads of the finish kernels
 
 struct CgMat {
     int64_t n;
@@ -66,14 +65,16 @@ struct CgScal {                            // per lane of the current layout
     double2 *part_a;                       // spmv partials [nchunks][kp]
     double2 *part_b;                       // update partials [grid][kp]
     double *part_c;                        // update partials [grid][kp]
-    double2 *part_f;                       // spmv finish block partials [CG_FB][kp]
+    double2 *part_f;                       // finish range partials [CG_FB][kp]
+    double *part_g;                        // finish range partials [CG_FB][kp]
     unsigned int *ctr;                     // [8] claim / done counters (parity)
     double tol;
 };
 
 struct CgGeom {
     int kp, kw, G, rpw;                    // lanes, lanes per warp group, groups, rows per warp
-    int64_t chunk_rows, nchunks;
+    int slots, P, subs, cpc;               // row slots per pass, passes/claim, sub-blocks/claim, chunks/claim
+    int64_t nchunks, nclaims;              // 64-row chunks, claims
     const int *lane_shift;                 // [kp] shift index of each lane
 };
 
@@ -128,75 +129,84 @@ __device__ __forceinline__ bool arrive_last(unsigned int *done, unsigned int tot
 }
 
 // ---------------------------------------------------------------------------
-// init (full width, lane = shift): x = 0, r = b, z = D^-1 r, p_old = 0
+// Fixed reduction tree (independent of the lane layout, hence of K per GPU,
+// sharding and compaction): a thread owns one 8-row sub-block of one shift
+// and sums its rows in row order; a 64-row chunk sums its 8 sub-blocks in
+// order; the finish kernels sum chunks in chunk order (CG_FB fixed ranges,
+// then the ranges in order).  Every per-shift scalar is therefore computed by
+// the same operation sequence wherever the shift runs.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g,
-                                                    int kreal) {
-    __shared__ double2 smc[CG_NT];
-    __shared__ double smr[CG_NT];
-    __shared__ double2 outc[CG_NT];
-    __shared__ double outr[CG_NT];
+constexpr int CG_SB = 8;          // rows per sub-block
+constexpr int CG_CH = 8;          // sub-blocks per chunk
+constexpr int CG_SBP = 1024;      // shared sub-block partial slots (subs_per_claim * kp)
+
+// sub-block partials of a claim -> chunk partials part[chunk][lane]
+template <typename T, typename Add>
+__device__ __forceinline__ void chunk_partials(const T *sbp, const CgGeom &g, int64_t claim, T *part, Add add,
+                                               T zero) {
+    const int kp = g.kp;
+    for (int w = threadIdx.x; w < g.cpc * kp; w += CG_NT) {
+        const int cc = w / kp, l = w % kp;
+        const int64_t chunk = claim * g.cpc + cc;
+        if (chunk >= g.nchunks) continue;
+        T s = zero;
+        for (int b = 0; b < CG_CH; ++b) s = add(s, sbp[(cc * CG_CH + b) * kp + l]);
+        part[(size_t)chunk * kp + l] = s;
+    }
+}
+
+__device__ __forceinline__ double2 add_c(double2 a, double2 b) { return cadd(a, b); }
+__device__ __forceinline__ double add_r(double a, double b) { return a + b; }
+
+// ---------------------------------------------------------------------------
+// init (full width, lane = shift): x = 0, r = b, z = D^-1 r, p_old = 0;
+// partials of rho = r^T z and |b|^2
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
+    __shared__ double2 sbc[CG_SBP];
+    __shared__ double sbr[CG_SBP];
     int lane, slot, slots;
     cta_geom(g, lane, slot, slots);
     const int kp = g.kp;
     const c128 sg = S.sigma[lane];
-    c128 rho = cmk(0.0, 0.0);
-    double bn = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * slots + slot; i < M.n; i += (int64_t)gridDim.x * slots) {
-        const size_t o = (size_t)i * kp + lane;
-        const c128 b = V.bshared ? V.bshared[i] : V.bvec[o];
-        const c128 z = cdiv_c(b, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
-        V.x[o] = cmk(0.0, 0.0);
-        V.r[o] = b;
-        V.z[o] = z;
-        V.p0[o] = cmk(0.0, 0.0);
-        rho = cadd(rho, cmul(b, z));
-        bn += cabs2(b);
-    }
-    cta_sum2(rho, bn, g, smc, smr, outc, outr);
-    if (threadIdx.x < kp) {
-        Sc.part_b[(size_t)blockIdx.x * kp + threadIdx.x] = outc[threadIdx.x];
-        Sc.part_c[(size_t)blockIdx.x * kp + threadIdx.x] = outr[threadIdx.x];
-    }
-    if (arrive_last(Sc.ctr + 4, gridDim.x)) {
-        for (int t = threadIdx.x; t < kp; t += CG_NT) {
-            double2 s = make_double2(0.0, 0.0);
-            double sb = 0.0;
-            for (unsigned c = 0; c < gridDim.x; ++c) {
-                s = cadd(s, Sc.part_b[(size_t)c * kp + t]);
-                sb += Sc.part_c[(size_t)c * kp + t];
+    for (int64_t claim = blockIdx.x; claim < g.nclaims; claim += gridDim.x) {
+        for (int ps = 0; ps < g.P; ++ps) {
+            const int sbl = ps * slots + slot;
+            const int64_t r0 = (claim * g.subs + sbl) * CG_SB;
+            c128 rho = cmk(0.0, 0.0);
+            double bn = 0.0;
+            for (int64_t i = r0; i < min(r0 + CG_SB, M.n); ++i) {
+                const size_t o = (size_t)i * kp + lane;
+                const c128 b = V.bshared ? V.bshared[i] : V.bvec[o];
+                const c128 z = cdiv_c(b, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
+                V.x[o] = cmk(0.0, 0.0);
+                V.r[o] = b;
+                V.z[o] = z;
+                V.p0[o] = cmk(0.0, 0.0);
+                rho = cadd(rho, cmul(b, z));
+                bn += cabs2(b);
             }
-            Sc.rho[t] = s;
-            Sc.bnorm2[t] = sb;
-            Sc.rnorm2[t] = sb;
-            Sc.beta[t] = make_double2(0.0, 0.0);
-            Sc.iters[t] = 0;
-            Sc.status[t] = 0;
-            Sc.active[t] = (g.lane_shift[t] < kreal && sb > 0.0) ? 1 : 0;
+            sbc[sbl * kp + lane] = rho;
+            sbr[sbl * kp + lane] = bn;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int na = 0;
-            for (int t = 0; t < kp; ++t) na += Sc.active[t];
-            *Sc.nactive = na;
-            Sc.ctr[4] = 0;
-            Sc.ctr[0] = Sc.ctr[1] = Sc.ctr[2] = Sc.ctr[3] = 0;
-        }
+        chunk_partials<double2>(sbc, g, claim, Sc.part_b, add_c, make_double2(0.0, 0.0));
+        chunk_partials<double>(sbr, g, claim, Sc.part_c, add_r, 0.0);
+        __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
 // spmv: p_new = z + beta p_old (own row), q = S p_new, mu = p^T q.
-// Row chunks are claimed per CTA from an atomic counter (one coherent
-// wavefront of ~grid*chunk rows, so the +-n neighbour rows of the stencil are
-// L2 hits); the next claim is prefetched and the per-lane reduction buffer is
-// double-buffered, so a chunk costs one barrier.  part_a[chunk][lane] is
-// summed in chunk order by k_cg_spmv_finish (deterministic).
+// Claims (one or more 64-row chunks) are taken per CTA from an atomic counter:
+// all SMs work on one coherent wavefront, so the +-n neighbour rows of a 2D/3D
+// stencil are L2 hits.  The next claim is prefetched and the shared partials
+// are double-buffered: one barrier per claim.
 // ---------------------------------------------------------------------------
 template <bool CPLX>
 __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g,
                                                     int parity) {
-    __shared__ double2 red[2][CG_NT];
+    __shared__ double2 sbp[2][CG_SBP];
     __shared__ int64_t claim_q[2];
     if (*Sc.nactive == 0) return;
     int lane, slot, slots;
@@ -212,98 +222,49 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, 
     __syncthreads();
     int buf = 0;
     for (;;) {
-        const int64_t chunk = claim_q[buf];
-        if (chunk >= g.nchunks) break;
+        const int64_t claim = claim_q[buf];
+        if (claim >= g.nclaims) break;
         if (threadIdx.x == 0) claim_q[buf ^ 1] = (int64_t)atomicAdd(Sc.ctr, 1u);
-        c128 mu = cmk(0.0, 0.0);
-        if (act) {
-            const int64_t r0 = chunk * g.chunk_rows;
-            const int64_t r1 = min(r0 + g.chunk_rows, M.n);
-            for (int64_t i = r0 + slot; i < r1; i += slots) {
-                c128 acc = cmk(0.0, 0.0), pi = cmk(0.0, 0.0);
-                const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
+        for (int ps = 0; ps < g.P; ++ps) {
+            const int sbl = ps * slots + slot;
+            const int64_t r0 = (claim * g.subs + sbl) * CG_SB;
+            c128 mu = cmk(0.0, 0.0);
+            if (act) {
+                const int64_t r1 = min(r0 + CG_SB, M.n);
+                for (int64_t i = r0; i < r1; ++i) {
+                    c128 acc = cmk(0.0, 0.0), pi = cmk(0.0, 0.0);
+                    const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
 #pragma unroll 4
-                for (int32_t q = q0; q < q1; ++q) {
-                    const int32_t c = __ldg(M.indices + q);
-                    const size_t oc = (size_t)c * kp + lane;
-                    const c128 pc = cadd(zv[oc], cmul(beta, pold[oc]));
-                    const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
-                    acc = cadd(acc, cmul(e, pc));
-                    if (c == i) pi = pc;
+                    for (int32_t q = q0; q < q1; ++q) {
+                        const int32_t c = __ldg(M.indices + q);
+                        const size_t oc = (size_t)c * kp + lane;
+                        const c128 pc = cadd(zv[oc], cmul(beta, pold[oc]));
+                        const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
+                        acc = cadd(acc, cmul(e, pc));
+                        if (c == i) pi = pc;
+                    }
+                    const size_t o = (size_t)i * kp + lane;
+                    pnew[o] = pi;
+                    V.q[o] = acc;
+                    mu = cadd(mu, cmul(pi, acc));
                 }
-                const size_t o = (size_t)i * kp + lane;
-                pnew[o] = pi;
-                V.q[o] = acc;
-                mu = cadd(mu, cmul(pi, acc));
             }
+            sbp[buf][sbl * kp + lane] = mu;
         }
-        mu.x = warp_same_shift(mu.x, g.kw);
-        mu.y = warp_same_shift(mu.y, g.kw);
-        red[buf][threadIdx.x] = mu;
-        __syncthreads();   // red[buf] complete, claim_q[buf^1] visible
-        if (threadIdx.x < kp) {
-            const int grp = threadIdx.x / g.kw, sl = threadIdx.x % g.kw;
-            double2 s = make_double2(0.0, 0.0);
-            for (int w = grp; w < CG_WARPS; w += g.G) s = cadd(s, red[buf][w * 32 + sl]);
-            Sc.part_a[(size_t)chunk * kp + threadIdx.x] = s;
-        }
+        __syncthreads();   // sub-block partials complete, claim_q[buf^1] visible
+        chunk_partials<double2>(sbp[buf], g, claim, Sc.part_a, add_c, make_double2(0.0, 0.0));
         buf ^= 1;
     }
 }
 
-// alpha = rho / sum_chunks(mu): CG_FB CTAs each sum a fixed contiguous range
-// of chunks (strided over the CTA's threads), the last CTA to arrive sums the
-// CG_FB block partials in block order -- fixed order, parallel over SMs
-constexpr int CG_FB = 64;
-__global__ void __launch_bounds__(CG_NT) k_cg_spmv_finish(CgScal Sc, CgGeom g) {
-    __shared__ double2 sm[CG_NT];
-    if (*Sc.nactive == 0) return;
-    const int kp = g.kp;
-    const int sub = CG_NT / kp > 0 ? CG_NT / kp : 1;
-    const int t = threadIdx.x % kp, sidx = threadIdx.x / kp;
-    const int64_t per = (g.nchunks + gridDim.x - 1) / gridDim.x;
-    const int64_t c0 = (int64_t)blockIdx.x * per, c1 = min(c0 + per, g.nchunks);
-    double2 s = make_double2(0.0, 0.0);
-    if (sidx < sub)
-        for (int64_t c = c0 + sidx; c < c1; c += sub) s = cadd(s, Sc.part_a[(size_t)c * kp + t]);
-    sm[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x < kp) {
-        double2 m = make_double2(0.0, 0.0);
-        for (int q = 0; q < sub; ++q) m = cadd(m, sm[q * kp + threadIdx.x]);
-        Sc.part_f[(size_t)blockIdx.x * kp + threadIdx.x] = m;
-    }
-    if (!arrive_last(Sc.ctr + 6, gridDim.x)) return;
-    for (int l = threadIdx.x; l < kp; l += CG_NT) {
-        double2 m = make_double2(0.0, 0.0);
-        for (unsigned blk = 0; blk < gridDim.x; ++blk) m = cadd(m, Sc.part_f[(size_t)blk * kp + l]);
-        if (Sc.active[l]) {
-            const double ms = cabs2(m);
-            if (!(ms > 0.0) || !isfinite(ms)) {
-                Sc.status[l] = isfinite(ms) ? 1 : 2;
-                Sc.active[l] = 0;
-                Sc.alpha[l] = make_double2(0.0, 0.0);
-            } else {
-                Sc.alpha[l] = cdiv_c(Sc.rho[l], m);
-            }
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        Sc.ctr[0] = 0;   // claim counter for the next spmv
-        Sc.ctr[6] = 0;
-    }
-}
-
 // ---------------------------------------------------------------------------
-// update: x += alpha p; r -= alpha q; z = D^-1 r; rho' = r^T z; |r|^2 -> beta
+// update: x += alpha p; r -= alpha q; z = D^-1 r; partials of rho' = r^T z, |r|^2
+// (claims statically strided over CTAs: pointwise, no locality to exploit)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g,
-                                                      int parity, int max_iters) {
-    __shared__ double2 smc[CG_NT];
-    __shared__ double smr[CG_NT];
-    __shared__ double2 outc[CG_NT];
-    __shared__ double outr[CG_NT];
+                                                      int parity) {
+    __shared__ double2 sbc[CG_SBP];
+    __shared__ double sbr[CG_SBP];
     if (*Sc.nactive == 0) return;
     int lane, slot, slots;
     cta_geom(g, lane, slot, slots);
@@ -311,103 +272,124 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
     const bool act = Sc.active[lane] != 0;
     const c128 sg = S.sigma[g.lane_shift[lane]];
     const c128 alpha = Sc.alpha[lane];
-    const c128 *pnew = parity ? V.p0 : V.p1;
-    c128 rho = cmk(0.0, 0.0);
-    double rn = 0.0;
-    if (act) {
-        const int64_t step = (int64_t)gridDim.x * slots;
-        int64_t i = (int64_t)blockIdx.x * slots + slot;
-        // two rows per trip: twice the loads in flight
-        for (; i + step < M.n; i += 2 * step) {
-            const size_t o0 = (size_t)i * kp + lane, o1 = (size_t)(i + step) * kp + lane;
-            const c128 p0 = pnew[o0], q0 = V.q[o0], x0 = V.x[o0], r0 = V.r[o0];
-            const c128 p1 = pnew[o1], q1 = V.q[o1], x1 = V.x[o1], r1 = V.r[o1];
-            const c128 d0 = form_entry(M.dta[i], M.dta_im[i], M.db[i], sg);
-            const c128 d1 = form_entry(M.dta[i + step], M.dta_im[i + step], M.db[i + step], sg);
-            V.x[o0] = cadd(x0, cmul(alpha, p0));
-            V.x[o1] = cadd(x1, cmul(alpha, p1));
-            const c128 ra = csub(r0, cmul(alpha, q0)), rb = csub(r1, cmul(alpha, q1));
-            V.r[o0] = ra;
-            V.r[o1] = rb;
-            const c128 za = cdiv_c(ra, d0), zb = cdiv_c(rb, d1);
-            V.z[o0] = za;
-            V.z[o1] = zb;
-            rho = cadd(rho, cmul(ra, za));
-            rho = cadd(rho, cmul(rb, zb));
-            rn += cabs2(ra);
-            rn += cabs2(rb);
+    const c128 *__restrict__ pnew = parity ? V.p0 : V.p1;
+    for (int64_t claim = blockIdx.x; claim < g.nclaims; claim += gridDim.x) {
+        for (int ps = 0; ps < g.P; ++ps) {
+            const int sbl = ps * slots + slot;
+            const int64_t r0 = (claim * g.subs + sbl) * CG_SB;
+            c128 rho = cmk(0.0, 0.0);
+            double rn = 0.0;
+            if (act) {
+                const int64_t r1 = min(r0 + CG_SB, M.n);
+#pragma unroll 2
+                for (int64_t i = r0; i < r1; ++i) {
+                    const size_t o = (size_t)i * kp + lane;
+                    const c128 p = pnew[o], q = V.q[o];
+                    V.x[o] = cadd(V.x[o], cmul(alpha, p));
+                    const c128 r = csub(V.r[o], cmul(alpha, q));
+                    V.r[o] = r;
+                    const c128 z = cdiv_c(r, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
+                    V.z[o] = z;
+                    rho = cadd(rho, cmul(r, z));
+                    rn += cabs2(r);
+                }
+            }
+            sbc[sbl * kp + lane] = rho;
+            sbr[sbl * kp + lane] = rn;
         }
-        if (i < M.n) {
-            const size_t o = (size_t)i * kp + lane;
-            const c128 p = pnew[o], q = V.q[o];
-            V.x[o] = cadd(V.x[o], cmul(alpha, p));
-            const c128 r = csub(V.r[o], cmul(alpha, q));
-            V.r[o] = r;
-            const c128 z = cdiv_c(r, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
-            V.z[o] = z;
-            rho = cadd(rho, cmul(r, z));
-            rn += cabs2(r);
-        }
-    }
-    cta_sum2(rho, rn, g, smc, smr, outc, outr);
-    if (threadIdx.x < kp) {
-        Sc.part_b[(size_t)blockIdx.x * kp + threadIdx.x] = outc[threadIdx.x];
-        Sc.part_c[(size_t)blockIdx.x * kp + threadIdx.x] = outr[threadIdx.x];
+        __syncthreads();
+        chunk_partials<double2>(sbc, g, claim, Sc.part_b, add_c, make_double2(0.0, 0.0));
+        chunk_partials<double>(sbr, g, claim, Sc.part_c, add_r, 0.0);
+        __syncthreads();
     }
 }
 
-// rho' and |r|^2 over the update CTAs (fixed order, parallel), then beta,
-// convergence freeze and failure flags; one CTA of CG_FIN threads
-__global__ void __launch_bounds__(CG_FIN) k_cg_update_finish(CgScal Sc, CgGeom g, int nparts, int max_iters) {
-    __shared__ double2 smc[CG_FIN];
-    __shared__ double smr[CG_FIN];
-    if (*Sc.nactive == 0) return;
+// ---------------------------------------------------------------------------
+// finish kernels: CG_FB CTAs sum fixed contiguous chunk ranges (sequential per
+// lane), the last CTA to arrive sums the CG_FB range partials in order and
+// updates the per-shift scalars.
+//   MODE 0 (after init):   rho, |b|^2 -> rho, bnorm2, active
+//   MODE 1 (after spmv):   mu -> alpha (breakdown / non-finite -> status)
+//   MODE 2 (after update): rho', |r|^2 -> freeze / beta / rho, nactive
+// ---------------------------------------------------------------------------
+constexpr int CG_FB = 64;
+template <int MODE>
+__global__ void __launch_bounds__(CG_NT) k_cg_finish(CgScal Sc, CgGeom g, int kreal, int max_iters) {
+    if (MODE != 0 && *Sc.nactive == 0) return;
     const int kp = g.kp;
-    const int sub = CG_FIN / kp;
-    const int t = threadIdx.x % kp, sidx = threadIdx.x / kp;
-    double2 s = make_double2(0.0, 0.0);
-    double sr = 0.0;
-    if (sidx < sub)
-        for (int c = sidx; c < nparts; c += sub) {
-            s = cadd(s, Sc.part_b[(size_t)c * kp + t]);
-            sr += Sc.part_c[(size_t)c * kp + t];
+    const double2 *pa = MODE == 1 ? Sc.part_a : Sc.part_b;
+    const int64_t per = (g.nchunks + CG_FB - 1) / CG_FB;
+    const int64_t c0 = (int64_t)blockIdx.x * per, c1 = min(c0 + per, g.nchunks);
+    for (int l = threadIdx.x; l < kp; l += CG_NT) {
+        double2 s = make_double2(0.0, 0.0);
+        double sr = 0.0;
+        for (int64_t c = c0; c < c1; ++c) {
+            s = cadd(s, pa[(size_t)c * kp + l]);
+            if (MODE != 1) sr += Sc.part_c[(size_t)c * kp + l];
         }
-    smc[threadIdx.x] = s;
-    smr[threadIdx.x] = sr;
-    __syncthreads();
-    if (threadIdx.x < kp && Sc.active[threadIdx.x]) {
-        const int l = threadIdx.x;
-        double2 rs = make_double2(0.0, 0.0);
-        double rr = 0.0;
-        for (int q = 0; q < sub; ++q) {
-            rs = cadd(rs, smc[q * kp + l]);
-            rr += smr[q * kp + l];
+        Sc.part_f[(size_t)blockIdx.x * kp + l] = s;
+        if (MODE != 1) Sc.part_g[(size_t)blockIdx.x * kp + l] = sr;
+    }
+    if (!arrive_last(Sc.ctr + 6, gridDim.x)) return;
+    for (int l = threadIdx.x; l < kp; l += CG_NT) {
+        double2 s = make_double2(0.0, 0.0);
+        double sr = 0.0;
+        for (unsigned blk = 0; blk < gridDim.x; ++blk) {
+            s = cadd(s, Sc.part_f[(size_t)blk * kp + l]);
+            if (MODE != 1) sr += Sc.part_g[(size_t)blk * kp + l];
         }
-        Sc.rnorm2[l] = rr;
-        Sc.iters[l] += 1;
-        const double2 rho_old = Sc.rho[l];
-        if (!isfinite(rr) || !isfinite(rs.x) || !isfinite(rs.y)) {
-            Sc.status[l] = 2;
-            Sc.active[l] = 0;
-        } else if (rr <= Sc.tol * Sc.tol * Sc.bnorm2[l]) {
-            Sc.active[l] = 0;                               // converged: freeze
-        } else if (!(cabs2(rho_old) > 0.0)) {
-            Sc.status[l] = 1;
-            Sc.active[l] = 0;
-        } else if (Sc.iters[l] >= max_iters) {
-            Sc.status[l] = 3;
-            Sc.active[l] = 0;
-        } else {
-            Sc.beta[l] = cdiv_c(rs, rho_old);
-            Sc.rho[l] = rs;
+        if (MODE == 0) {
+            Sc.rho[l] = s;
+            Sc.bnorm2[l] = sr;
+            Sc.rnorm2[l] = sr;
+            Sc.beta[l] = make_double2(0.0, 0.0);
+            Sc.iters[l] = 0;
+            Sc.status[l] = 0;
+            Sc.active[l] = (g.lane_shift[l] < kreal && sr > 0.0) ? 1 : 0;
+        } else if (MODE == 1) {
+            if (Sc.active[l]) {
+                const double ms = cabs2(s);
+                if (!(ms > 0.0) || !isfinite(ms)) {
+                    Sc.status[l] = isfinite(ms) ? 1 : 2;
+                    Sc.active[l] = 0;
+                    Sc.alpha[l] = make_double2(0.0, 0.0);
+                } else {
+                    Sc.alpha[l] = cdiv_c(Sc.rho[l], s);
+                }
+            }
+        } else if (Sc.active[l]) {
+            Sc.rnorm2[l] = sr;
+            Sc.iters[l] += 1;
+            const double2 rho_old = Sc.rho[l];
+            if (!isfinite(sr) || !isfinite(s.x) || !isfinite(s.y)) {
+                Sc.status[l] = 2;
+                Sc.active[l] = 0;
+            } else if (sr <= Sc.tol * Sc.tol * Sc.bnorm2[l]) {
+                Sc.active[l] = 0;                               // converged: freeze
+            } else if (!(cabs2(rho_old) > 0.0)) {
+                Sc.status[l] = 1;
+                Sc.active[l] = 0;
+            } else if (Sc.iters[l] >= max_iters) {
+                Sc.status[l] = 3;
+                Sc.active[l] = 0;
+            } else {
+                Sc.beta[l] = cdiv_c(s, rho_old);
+                Sc.rho[l] = s;
+            }
         }
     }
     __syncthreads();
     if (threadIdx.x < 32) {
-        int na = 0;
-        for (int l = threadIdx.x; l < kp; l += 32) na += Sc.active[l];
-        for (int off = 16; off > 0; off >>= 1) na += __shfl_xor_sync(0xffffffffu, na, off);
-        if (threadIdx.x == 0) *Sc.nactive = na;
+        if (MODE != 1) {
+            int na = 0;
+            for (int l = threadIdx.x; l < kp; l += 32) na += Sc.active[l];
+            for (int off = 16; off > 0; off >>= 1) na += __shfl_xor_sync(0xffffffffu, na, off);
+            if (threadIdx.x == 0) *Sc.nactive = na;
+        }
+        if (threadIdx.x == 0) {
+            Sc.ctr[6] = 0;
+            if (MODE == 1) Sc.ctr[0] = 0;   // spmv claim counter
+        }
     }
 }
 
@@ -597,21 +579,18 @@ static CgGeom make_geom(const CocgImpl *im, int kp, int64_t n) {
     g.kw = kp < 32 ? kp : 32;
     g.G = kp / g.kw;
     g.rpw = 32 / g.kw;
-    // a chunk = up to 8 CTA passes (32 rows at 64 lanes): the in-flight
-    // wavefront is ~grid*chunk rows, narrow enough for the stencil's +-n rows to
-    // stay in L2; fewer passes when few lanes are live so every SM gets chunks
-    const int64_t pass_rows = (int64_t)(CG_WARPS / g.G) * g.rpw;
-    const int64_t passes = std::max<int64_t>(1, std::min<int64_t>(8, n / (pass_rows * 2 * im->sms * 8)));
-    g.chunk_rows = pass_rows * passes;
-    g.nchunks = (n + g.chunk_rows - 1) / g.chunk_rows;
+    g.slots = (CG_WARPS / g.G) * g.rpw;                 // sub-blocks per CTA pass
+    g.P = g.slots >= CG_CH ? 1 : CG_CH / g.slots;       // passes per claim
+    g.subs = g.slots * g.P;                             // sub-blocks per claim (multiple of CG_CH)
+    g.cpc = g.subs / CG_CH;                             // chunks per claim
+    g.nchunks = (n + CG_SB * CG_CH - 1) / (CG_SB * CG_CH);
+    g.nclaims = (g.nchunks + g.cpc - 1) / g.cpc;
     g.lane_shift = im->lane_shift;
     return g;
 }
 
-static int grid_for(const CocgImpl *im, const CgGeom &g, int64_t n) {
-    const int64_t slots = (CG_WARPS / g.G) * g.rpw;
-    const int64_t want = (n + slots - 1) / slots;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)im->sms * 8));
+static int grid_for(const CocgImpl *im, const CgGeom &g, int64_t) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g.nclaims, (int64_t)im->sms * 8));
 }
 
 int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine, cudaStream_t st,
@@ -700,9 +679,10 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     int64_t part_max = 1;                     // largest nchunks*kp over the layouts compaction can reach
     for (int w = 1; w <= kp; w *= 2) part_max = std::max<int64_t>(part_max, make_geom(im, w, n).nchunks * w);
     CGA(Sc.part_a, sizeof(double2) * (size_t)part_max);
-    CGA(Sc.part_b, sizeof(double2) * (size_t)kp * im->sms * 8);
-    CGA(Sc.part_c, sizeof(double) * (size_t)kp * im->sms * 8);
+    CGA(Sc.part_b, sizeof(double2) * (size_t)part_max);
+    CGA(Sc.part_c, sizeof(double) * (size_t)part_max);
     CGA(Sc.part_f, sizeof(double2) * (size_t)kp * CG_FB);
+    CGA(Sc.part_g, sizeof(double) * (size_t)kp * CG_FB);
     CGA(Sc.ctr, sizeof(unsigned int) * 8);
     CGK(cudaMemsetAsync(Sc.ctr, 0, sizeof(unsigned int) * 8, st));
     Sc.tol = cg.tol;
@@ -754,24 +734,24 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     int grid = grid_for(im, g, n);
     const double nnzb = 28.0 * (double)cg.nnz + 4.0 * (double)(n + 1);   // CSR pattern + 3 value arrays
     hook_begin(cg, "cg_init", 96.0 * n * kp);
-    k_cg_init<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, cg.k);
+    k_cg_init<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+    k_cg_finish<0><<<CG_FB, CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
     hook_end(cg);
     CGK(cudaGetLastError());
-    ++*launches;
+    *launches += 2;
     int live = cg.k;
     int it = 0, parity = 0;
     const int check_every = 8;
     for (;;) {
         for (int s = 0; s < check_every; ++s) {
             hook_begin(cg, "cg_spmv", 64.0 * n * live + nnzb);
-            const int sgrid = (int)std::min<int64_t>(g.nchunks, (int64_t)im->sms * 8);
-            if (im->cplx) k_cg_spmv<true><<<sgrid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
-            else k_cg_spmv<false><<<sgrid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
-            k_cg_spmv_finish<<<(int)std::min<int64_t>(CG_FB, g.nchunks), CG_NT, 0, st>>>(im->Sc, g);
+            if (im->cplx) k_cg_spmv<true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
+            else k_cg_spmv<false><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
+            k_cg_finish<1><<<CG_FB, CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             hook_begin(cg, "cg_update", 112.0 * n * live + 24.0 * n);
-            k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity, cg.max_iters);
-            k_cg_update_finish<<<1, CG_FIN, 0, st>>>(im->Sc, g, grid, cg.max_iters);
+            k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
+            k_cg_finish<2><<<CG_FB, CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             parity ^= 1;
             *launches += 4;
