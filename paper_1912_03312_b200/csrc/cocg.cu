@@ -130,13 +130,13 @@ __device__ __forceinline__ bool arrive_last(unsigned int *done, unsigned int tot
 
 // ---------------------------------------------------------------------------
 // Fixed reduction tree (independent of the lane layout, hence of K per GPU,
-// sharding and compaction): a thread owns one 8-row sub-block of one shift
-// and sums its rows in row order; a 64-row chunk sums its 8 sub-blocks in
-// order; the finish kernels sum chunks in chunk order (CG_FB fixed ranges,
-// then the ranges in order).  Every per-shift scalar is therefore computed by
+// sharding and compaction): a thread owns one 4-row sub-block of one shift
+// and sums its rows in row order; a 32-row chunk sums its 8 sub-blocks in
+// order; the finish kernels sum ranges of CG_RANGE chunks in chunk order,
+// then the ranges in order.  Every per-shift scalar is therefore computed by
 // the same operation sequence wherever the shift runs.
 // ---------------------------------------------------------------------------
-constexpr int CG_SB = 8;          // rows per sub-block
+constexpr int CG_SB = 4;          // rows per sub-block
 constexpr int CG_CH = 8;          // sub-blocks per chunk
 constexpr int CG_SBP = 1024;      // shared sub-block partial slots (subs_per_claim * kp)
 
@@ -305,39 +305,63 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
 }
 
 // ---------------------------------------------------------------------------
-// finish kernels: CG_FB CTAs sum fixed contiguous chunk ranges (sequential per
-// lane), the last CTA to arrive sums the CG_FB range partials in order and
-// updates the per-shift scalars.
+// finish kernels: one thread per (range of CG_RANGE chunks, lane) sums its
+// range in chunk order (loads batched, adds in order); the last CTA to arrive
+// sums the ranges in order per lane and updates the per-shift scalars.
 //   MODE 0 (after init):   rho, |b|^2 -> rho, bnorm2, active
 //   MODE 1 (after spmv):   mu -> alpha (breakdown / non-finite -> status)
 //   MODE 2 (after update): rho', |r|^2 -> freeze / beta / rho, nactive
 // ---------------------------------------------------------------------------
-constexpr int CG_FB = 64;
+constexpr int CG_RANGE = 64;
+
+template <bool REAL>
+__device__ __forceinline__ void sum_range(const double2 *pa, const double *pc, int64_t c0, int64_t c1, int kp,
+                                          int l, double2 &s, double &sr) {
+    int64_t c = c0;
+    for (; c + 8 <= c1; c += 8) {
+        double2 v[8];
+        double w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            v[u] = pa[(size_t)(c + u) * kp + l];
+            if (REAL) w[u] = pc[(size_t)(c + u) * kp + l];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            s = cadd(s, v[u]);
+            if (REAL) sr += w[u];
+        }
+    }
+    for (; c < c1; ++c) {
+        s = cadd(s, pa[(size_t)c * kp + l]);
+        if (REAL) sr += pc[(size_t)c * kp + l];
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(CG_NT) k_cg_finish(CgScal Sc, CgGeom g, int kreal, int max_iters) {
     if (MODE != 0 && *Sc.nactive == 0) return;
     const int kp = g.kp;
+    const int64_t nranges = (g.nchunks + CG_RANGE - 1) / CG_RANGE;
     const double2 *pa = MODE == 1 ? Sc.part_a : Sc.part_b;
-    const int64_t per = (g.nchunks + CG_FB - 1) / CG_FB;
-    const int64_t c0 = (int64_t)blockIdx.x * per, c1 = min(c0 + per, g.nchunks);
-    for (int l = threadIdx.x; l < kp; l += CG_NT) {
+    const int64_t t = (int64_t)blockIdx.x * CG_NT + threadIdx.x;
+    if (t < nranges * kp) {
+        const int64_t r = t / kp;
+        const int l = (int)(t % kp);
         double2 s = make_double2(0.0, 0.0);
         double sr = 0.0;
-        for (int64_t c = c0; c < c1; ++c) {
-            s = cadd(s, pa[(size_t)c * kp + l]);
-            if (MODE != 1) sr += Sc.part_c[(size_t)c * kp + l];
-        }
-        Sc.part_f[(size_t)blockIdx.x * kp + l] = s;
-        if (MODE != 1) Sc.part_g[(size_t)blockIdx.x * kp + l] = sr;
+        const int64_t c0 = r * CG_RANGE, c1 = min(c0 + CG_RANGE, g.nchunks);
+        if (MODE == 1) sum_range<false>(pa, Sc.part_c, c0, c1, kp, l, s, sr);
+        else sum_range<true>(pa, Sc.part_c, c0, c1, kp, l, s, sr);
+        Sc.part_f[(size_t)r * kp + l] = s;
+        if (MODE != 1) Sc.part_g[(size_t)r * kp + l] = sr;
     }
     if (!arrive_last(Sc.ctr + 6, gridDim.x)) return;
     for (int l = threadIdx.x; l < kp; l += CG_NT) {
         double2 s = make_double2(0.0, 0.0);
         double sr = 0.0;
-        for (unsigned blk = 0; blk < gridDim.x; ++blk) {
-            s = cadd(s, Sc.part_f[(size_t)blk * kp + l]);
-            if (MODE != 1) sr += Sc.part_g[(size_t)blk * kp + l];
-        }
+        if (MODE == 1) sum_range<false>(Sc.part_f, Sc.part_g, 0, nranges, kp, l, s, sr);
+        else sum_range<true>(Sc.part_f, Sc.part_g, 0, nranges, kp, l, s, sr);
         if (MODE == 0) {
             Sc.rho[l] = s;
             Sc.bnorm2[l] = sr;
@@ -391,6 +415,11 @@ __global__ void __launch_bounds__(CG_NT) k_cg_finish(CgScal Sc, CgGeom g, int kr
             if (MODE == 1) Sc.ctr[0] = 0;   // spmv claim counter
         }
     }
+}
+
+static inline int finish_grid(const CgGeom &g) {
+    const int64_t nranges = (g.nchunks + CG_RANGE - 1) / CG_RANGE;
+    return (int)std::max<int64_t>(1, (nranges * g.kp + CG_NT - 1) / CG_NT);
 }
 
 // ---------------------------------------------------------------------------
@@ -681,8 +710,9 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     CGA(Sc.part_a, sizeof(double2) * (size_t)part_max);
     CGA(Sc.part_b, sizeof(double2) * (size_t)part_max);
     CGA(Sc.part_c, sizeof(double) * (size_t)part_max);
-    CGA(Sc.part_f, sizeof(double2) * (size_t)kp * CG_FB);
-    CGA(Sc.part_g, sizeof(double) * (size_t)kp * CG_FB);
+    const int64_t nranges_max = (make_geom(im, kp, n).nchunks + CG_RANGE - 1) / CG_RANGE;
+    CGA(Sc.part_f, sizeof(double2) * (size_t)kp * nranges_max);
+    CGA(Sc.part_g, sizeof(double) * (size_t)kp * nranges_max);
     CGA(Sc.ctr, sizeof(unsigned int) * 8);
     CGK(cudaMemsetAsync(Sc.ctr, 0, sizeof(unsigned int) * 8, st));
     Sc.tol = cg.tol;
@@ -735,7 +765,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     const double nnzb = 28.0 * (double)cg.nnz + 4.0 * (double)(n + 1);   // CSR pattern + 3 value arrays
     hook_begin(cg, "cg_init", 96.0 * n * kp);
     k_cg_init<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
-    k_cg_finish<0><<<CG_FB, CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
+    k_cg_finish<0><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
     hook_end(cg);
     CGK(cudaGetLastError());
     *launches += 2;
@@ -747,11 +777,11 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             hook_begin(cg, "cg_spmv", 64.0 * n * live + nnzb);
             if (im->cplx) k_cg_spmv<true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
             else k_cg_spmv<false><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
-            k_cg_finish<1><<<CG_FB, CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
+            k_cg_finish<1><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             hook_begin(cg, "cg_update", 112.0 * n * live + 24.0 * n);
             k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
-            k_cg_finish<2><<<CG_FB, CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
+            k_cg_finish<2><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             parity ^= 1;
             *launches += 4;
