@@ -65,8 +65,8 @@ struct CgScal {                            // per lane of the current layout
     double2 *part_a;                       // spmv partials [nchunks][kp]
     double2 *part_b;                       // update partials [grid][kp]
     double *part_c;                        // update partials [grid][kp]
-    double2 *part_f;                       // finish range partials [CG_FB][kp]
-    double *part_g;                        // finish range partials [CG_FB][kp]
+    double2 *part_f, *part_f2;             // finish level partials [nranges][kp] (ping-pong)
+    double *part_g, *part_g2;
     unsigned int *ctr;                     // [8] claim / done counters (parity)
     double tol;
 };
@@ -131,7 +131,8 @@ __device__ __forceinline__ bool arrive_last(unsigned int *done, unsigned int tot
 // ---------------------------------------------------------------------------
 // Fixed reduction tree (independent of the lane layout, hence of K per GPU,
 // sharding and compaction): a thread owns one 4-row sub-block of one shift
-// and sums its rows in row order; a 32-row chunk sums its 8 sub-blocks in
+// (rows b, b+8, b+16, b+24 of a 32-row chunk, so a warp's row slots touch
+// consecutive rows at every step) and sums its rows in order; a 32-row chunk sums its 8 sub-blocks in
 // order; the finish kernels sum ranges of CG_RANGE chunks in chunk order,
 // then the ranges in order.  Every per-shift scalar is therefore computed by
 // the same operation sequence wherever the shift runs.
@@ -172,10 +173,11 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
     for (int64_t claim = blockIdx.x; claim < g.nclaims; claim += gridDim.x) {
         for (int ps = 0; ps < g.P; ++ps) {
             const int sbl = ps * slots + slot;
-            const int64_t r0 = (claim * g.subs + sbl) * CG_SB;
+            const int64_t gsb = claim * g.subs + sbl;   // sub-block b of chunk c: rows c*32 + b + 8k
+            const int64_t r0 = (gsb / CG_CH) * (CG_SB * CG_CH) + gsb % CG_CH;
             c128 rho = cmk(0.0, 0.0);
             double bn = 0.0;
-            for (int64_t i = r0; i < min(r0 + CG_SB, M.n); ++i) {
+            for (int64_t i = r0; i < min(r0 + CG_SB * CG_CH, M.n); i += CG_CH) {
                 const size_t o = (size_t)i * kp + lane;
                 const c128 b = V.bshared ? V.bshared[i] : V.bvec[o];
                 const c128 z = cdiv_c(b, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
@@ -227,11 +229,12 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, 
         if (threadIdx.x == 0) claim_q[buf ^ 1] = (int64_t)atomicAdd(Sc.ctr, 1u);
         for (int ps = 0; ps < g.P; ++ps) {
             const int sbl = ps * slots + slot;
-            const int64_t r0 = (claim * g.subs + sbl) * CG_SB;
+            const int64_t gsb = claim * g.subs + sbl;   // sub-block b of chunk c: rows c*32 + b + 8k
+            const int64_t r0 = (gsb / CG_CH) * (CG_SB * CG_CH) + gsb % CG_CH;
             c128 mu = cmk(0.0, 0.0);
             if (act) {
-                const int64_t r1 = min(r0 + CG_SB, M.n);
-                for (int64_t i = r0; i < r1; ++i) {
+                const int64_t r1 = min(r0 + CG_SB * CG_CH, M.n);
+                for (int64_t i = r0; i < r1; i += CG_CH) {
                     c128 acc = cmk(0.0, 0.0), pi = cmk(0.0, 0.0);
                     const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
 #pragma unroll 4
@@ -276,13 +279,14 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
     for (int64_t claim = blockIdx.x; claim < g.nclaims; claim += gridDim.x) {
         for (int ps = 0; ps < g.P; ++ps) {
             const int sbl = ps * slots + slot;
-            const int64_t r0 = (claim * g.subs + sbl) * CG_SB;
+            const int64_t gsb = claim * g.subs + sbl;   // sub-block b of chunk c: rows c*32 + b + 8k
+            const int64_t r0 = (gsb / CG_CH) * (CG_SB * CG_CH) + gsb % CG_CH;
             c128 rho = cmk(0.0, 0.0);
             double rn = 0.0;
             if (act) {
-                const int64_t r1 = min(r0 + CG_SB, M.n);
+                const int64_t r1 = min(r0 + CG_SB * CG_CH, M.n);
 #pragma unroll 2
-                for (int64_t i = r0; i < r1; ++i) {
+                for (int64_t i = r0; i < r1; i += CG_CH) {
                     const size_t o = (size_t)i * kp + lane;
                     const c128 p = pnew[o], q = V.q[o];
                     V.x[o] = cadd(V.x[o], cmul(alpha, p));
@@ -357,11 +361,32 @@ __global__ void __launch_bounds__(CG_NT) k_cg_finish(CgScal Sc, CgGeom g, int kr
         if (MODE != 1) Sc.part_g[(size_t)r * kp + l] = sr;
     }
     if (!arrive_last(Sc.ctr + 6, gridDim.x)) return;
+    // fixed fan-in-CG_RANGE levels inside the last CTA (ping-pong part_f/part_f2)
+    double2 *src = Sc.part_f, *dst = Sc.part_f2;
+    double *srcr = Sc.part_g, *dstr = Sc.part_g2;
+    int64_t n1 = nranges;
+    while (n1 > 1) {
+        const int64_t n2 = (n1 + CG_RANGE - 1) / CG_RANGE;
+        for (int64_t w = threadIdx.x; w < n2 * kp; w += CG_NT) {
+            const int64_t r = w / kp;
+            const int l = (int)(w % kp);
+            double2 s = make_double2(0.0, 0.0);
+            double sr = 0.0;
+            const int64_t c0 = r * CG_RANGE, c1 = min(c0 + CG_RANGE, n1);
+            if (MODE == 1) sum_range<false>(src, srcr, c0, c1, kp, l, s, sr);
+            else sum_range<true>(src, srcr, c0, c1, kp, l, s, sr);
+            dst[(size_t)r * kp + l] = s;
+            if (MODE != 1) dstr[(size_t)r * kp + l] = sr;
+        }
+        __threadfence_block();
+        __syncthreads();
+        double2 *tc = src; src = dst; dst = tc;
+        double *tr = srcr; srcr = dstr; dstr = tr;
+        n1 = n2;
+    }
     for (int l = threadIdx.x; l < kp; l += CG_NT) {
-        double2 s = make_double2(0.0, 0.0);
-        double sr = 0.0;
-        if (MODE == 1) sum_range<false>(Sc.part_f, Sc.part_g, 0, nranges, kp, l, s, sr);
-        else sum_range<true>(Sc.part_f, Sc.part_g, 0, nranges, kp, l, s, sr);
+        const double2 s = src[l];
+        const double sr = MODE != 1 ? srcr[l] : 0.0;
         if (MODE == 0) {
             Sc.rho[l] = s;
             Sc.bnorm2[l] = sr;
@@ -713,6 +738,8 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     const int64_t nranges_max = (make_geom(im, kp, n).nchunks + CG_RANGE - 1) / CG_RANGE;
     CGA(Sc.part_f, sizeof(double2) * (size_t)kp * nranges_max);
     CGA(Sc.part_g, sizeof(double) * (size_t)kp * nranges_max);
+    CGA(Sc.part_f2, sizeof(double2) * (size_t)kp * nranges_max);
+    CGA(Sc.part_g2, sizeof(double) * (size_t)kp * nranges_max);
     CGA(Sc.ctr, sizeof(unsigned int) * 8);
     CGK(cudaMemsetAsync(Sc.ctr, 0, sizeof(unsigned int) * 8, st));
     Sc.tol = cg.tol;
