@@ -68,7 +68,7 @@ struct CgScal {                            // per lane of the current layout
     double2 *part_f, *part_f2;             // finish level partials [nranges][kp] (ping-pong)
     double *part_g, *part_g2;
     unsigned int *ctr;                     // [8] claim / done counters (parity)
-    double tol;
+    double *tolsq;                         // [kp] squared relative residual target per lane
 };
 
 struct CgGeom {
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(CG_NT) k_cg_finish(CgScal Sc, CgGeom g, int kr
             if (!isfinite(sr) || !isfinite(s.x) || !isfinite(s.y)) {
                 Sc.status[l] = 2;
                 Sc.active[l] = 0;
-            } else if (sr <= Sc.tol * Sc.tol * Sc.bnorm2[l]) {
+            } else if (sr <= Sc.tolsq[l] * Sc.bnorm2[l]) {
                 Sc.active[l] = 0;                               // converged: freeze
             } else if (!(cabs2(rho_old) > 0.0)) {
                 Sc.status[l] = 1;
@@ -483,6 +483,7 @@ __global__ void k_cg_repack_scalars(CgScal Sc, int kp_new, const int *__restrict
         Sc.active[l] = Sc.active[s];
         Sc.iters[l] = Sc.iters[s];
         Sc.status[l] = Sc.status[s];
+        Sc.tolsq[l] = Sc.tolsq[s];
     }
 }
 
@@ -586,6 +587,7 @@ static inline void hook_end(CocgState &cg) {
 
 struct CocgImpl {
     bool cplx = false;         // A has an imaginary part
+    std::vector<double> wts;   // per shift: mean|beta| / |beta_j| (tolerance weights)
     CgMat M{};
     CgVec V{};
     CgScal Sc{};
@@ -661,6 +663,18 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     const int64_t n = d->n, nnz = d->nnz;
     const int kp = S.kp;
     im->kp_full = kp;
+    {
+        double mean = 0.0;
+        for (int j = 0; j < d->k; ++j) mean += std::hypot(d->weights[j].re, d->weights[j].im);
+        mean /= std::max(1, d->k);
+        im->wts.assign(kp, 1.0);
+        for (int j = 0; j < d->k; ++j) {
+            const double b = std::hypot(d->weights[j].re, d->weights[j].im);
+            im->wts[j] = b > 0.0 ? mean / b : 1e30;
+        }
+        if (const char *e = getenv("REXI_COCG_WEIGHTED"))
+            if (atoi(e) == 0) std::fill(im->wts.begin(), im->wts.end(), 1.0);
+    }
     std::vector<double> ta(nnz), tai(nnz), bb(nnz), dta(n, 0.0), dtai(n, 0.0), db(n, 0.0);
     std::vector<char> hasdiag(n, 0);
     for (int64_t r = 0; r < n; ++r)
@@ -742,7 +756,7 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     CGA(Sc.part_g2, sizeof(double) * (size_t)kp * nranges_max);
     CGA(Sc.ctr, sizeof(unsigned int) * 8);
     CGK(cudaMemsetAsync(Sc.ctr, 0, sizeof(unsigned int) * 8, st));
-    Sc.tol = cg.tol;
+    CGA(Sc.tolsq, sizeof(double) * kp);
     CGK(cudaMallocHost((void **)&im->h_buf, sizeof(int) * (2 + 2 * kp)));
     CGK(cudaStreamSynchronize(st));
     return REXI_OK;
@@ -777,7 +791,7 @@ static int cg_repack(CocgImpl *im, int kp_old, int kp_new, const std::vector<int
 
 // solve S_j x_j = b for all shifts (b shared or per shift); result in im->xout
 static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t st, int64_t *launches,
-                    std::string &err, double tol) {
+                    std::string &err, double tol, double cap) {
     const int64_t n = cg.n;
     int kp = im->kp_full;
     std::vector<int> lane_shift(kp), valid(kp);
@@ -786,7 +800,17 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
         valid[l] = l < cg.k;
     }
     CGK(cudaMemcpyAsync(im->lane_shift, lane_shift.data(), sizeof(int) * kp, cudaMemcpyHostToDevice, st));
-    im->Sc.tol = tol;
+    {
+        // weighted per-shift targets: shift j's error enters u1 scaled by |beta_j|,
+        // so tol_j = min(cap, tol * mean|beta| / |beta_j|) keeps sum_j |beta_j| e_j
+        // at the uniform-tol budget while small-weight shifts stop early
+        std::vector<double> tsq(kp);
+        for (int l = 0; l < kp; ++l) {
+            const double t = std::min(cap, tol * im->wts[l]);
+            tsq[l] = t * t;
+        }
+        CGK(cudaMemcpyAsync(im->Sc.tolsq, tsq.data(), sizeof(double) * kp, cudaMemcpyHostToDevice, st));
+    }
     CgGeom g = make_geom(im, kp, n);
     int grid = grid_for(im, g, n);
     const double nnzb = 28.0 * (double)cg.nnz + 4.0 * (double)(n + 1);   // CSR pattern + 3 value arrays
@@ -883,11 +907,14 @@ static int cg_solve_refined(CocgState &cg, CocgImpl *im, const ShiftDev &S, cuda
     im->V.bvec = nullptr;
     // with refinement the first solve stops at tol*100 (the dd-residual
     // correction supplies the remaining digits), the correction at 1e-4
+    // targets: first solve min(1e-8, 1e-10 w_j), correction min(1e-4, 1e-6 w_j):
+    // every shift ends at a true relative residual <= 1e-12 (cap1 * cap2)
     double tol1 = cg.refine > 0 ? std::min(1e-8, cg.tol * 100.0) : cg.tol;
     double tol2 = 1e-6;
+    double cap1 = cg.refine > 0 ? 1e-8 : cg.tol, cap2 = 1e-4;
     if (const char *e = getenv("REXI_COCG_TOL1")) tol1 = atof(e);   // tuning knobs
     if (const char *e = getenv("REXI_COCG_TOL2")) tol2 = atof(e);
-    int rc = cg_solve(cg, im, S, st, launches, err, tol1);
+    int rc = cg_solve(cg, im, S, st, launches, err, tol1, std::max(tol1, cap1));
     if (rc) return rc;
     *x1 = im->xout;
     *x2 = nullptr;
@@ -905,7 +932,7 @@ static int cg_solve_refined(CocgState &cg, CocgImpl *im, const ShiftDev &S, cuda
         ++*launches;
         im->V.bshared = nullptr;
         im->V.bvec = im->res;
-        rc = cg_solve(cg, im, S, st, launches, err, tol2);
+        rc = cg_solve(cg, im, S, st, launches, err, tol2, std::max(tol2, cap2));
         im->V.bshared = im->rhs;
         im->V.bvec = nullptr;
         if (rc) return rc;
