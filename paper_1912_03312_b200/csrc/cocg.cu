@@ -914,6 +914,8 @@ static int cg_solve_refined(CocgState &cg, CocgImpl *im, const ShiftDev &S, cuda
     double cap1 = cg.refine > 0 ? 1e-8 : cg.tol, cap2 = 1e-4;
     if (const char *e = getenv("REXI_COCG_TOL1")) tol1 = atof(e);   // tuning knobs
     if (const char *e = getenv("REXI_COCG_TOL2")) tol2 = atof(e);
+    if (const char *e = getenv("REXI_COCG_CAP1")) cap1 = atof(e);
+    if (const char *e = getenv("REXI_COCG_CAP2")) cap2 = atof(e);
     int rc = cg_solve(cg, im, S, st, launches, err, tol1, std::max(tol1, cap1));
     if (rc) return rc;
     *x1 = im->xout;
