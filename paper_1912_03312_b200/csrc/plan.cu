@@ -60,6 +60,8 @@ struct rexi_plan {
     std::vector<Rec> pending;
     std::vector<cudaEvent_t> pool;
     std::map<std::string, Acc> prof_acc;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};   // 1D step replay (ubuf[g] -> ubuf[g^1])
+    int64_t graph_kernels = 0;
     struct Hook : rexi::ProfHook {
         rexi_plan *p = nullptr;
         cudaEvent_t a = nullptr;
@@ -447,6 +449,8 @@ int rexi_plan_destroy(rexi_plan *plan) {
     for (void *p : plan->allocs) cudaFree(p);
     cocg_destroy(plan->cg);
     for (auto &r : plan->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto &g : plan->graph)
+        if (g) cudaGraphExecDestroy(g);
     for (auto e : plan->pool) cudaEventDestroy(e);
     if (plan->own_stream && plan->stream) cudaStreamDestroy(plan->stream);
     delete plan;
@@ -641,6 +645,35 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     }
     if (stats) CK(cudaEventRecord(ev[0], st));
     int cur = (src == plan->ubuf[0]) ? 0 : 1;
+    if (n_steps > 0 && plan->solver == REXI_SOLVER_TRIDIAG && !plan->prof) {
+        // the 1D step is a fixed kernel sequence: replay it as a CUDA graph
+        // (two graphs, ping-ponging between the plan's state buffers)
+        if (src != plan->ubuf[0] && src != plan->ubuf[1]) {
+            CK(cudaMemcpyAsync(plan->ubuf[0], src, sizeof(c128) * n, cudaMemcpyDeviceToDevice, st));
+            cur = 0;
+        }
+        for (int g = 0; g < 2; ++g) {
+            if (plan->graph[g]) continue;
+            cudaGraph_t graph = nullptr;
+            const int64_t l0 = plan->launches;
+            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            int rc = tri_step(plan, plan->ubuf[g], plan->ubuf[g ^ 1]);
+            cudaError_t ce = cudaStreamEndCapture(st, &graph);
+            if (rc) return rc;
+            if (ce != cudaSuccess) return cuda_err(plan, ce, "cudaStreamEndCapture");
+            CK(cudaGraphInstantiate(&plan->graph[g], graph, 0));
+            cudaGraphDestroy(graph);
+            plan->graph_kernels = plan->launches - l0;
+            plan->launches = l0;
+        }
+        for (int s = 0; s < n_steps; ++s) {
+            CK(cudaGraphLaunch(plan->graph[cur], st));
+            plan->launches += plan->graph_kernels;
+            cur ^= 1;
+        }
+        src = plan->ubuf[cur];
+        n_steps = -n_steps;    // steps done; restored below
+    }
     for (int s = 0; s < n_steps; ++s) {
         c128 *dst;
         bool last = s == n_steps - 1;
@@ -656,6 +689,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
         src = dst;
         cur = (src == plan->ubuf[0]) ? 0 : 1;
     }
+    if (n_steps < 0) n_steps = -n_steps;
     if (stats) CK(cudaEventRecord(ev[1], st));
     if (n_steps == 0) {
         if (mem == REXI_MEM_HOST) {
