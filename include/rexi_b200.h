@@ -85,6 +85,10 @@ typedef struct rexi_desc {
     double tol;                /* COCG relative residual target (0 -> 1e-12)      */
     int32_t max_iters;         /* COCG iteration cap per solve (0 -> 20000)       */
     void *stream;              /* cudaStream_t to run on, or NULL (plan-owned)    */
+    double weight_ref;         /* COCG: reference |beta| for the per-shift tolerance
+                                  weights (mean |beta| over ALL K shifts, so a shard
+                                  converges exactly as in the unsharded run); 0 ->
+                                  the mean over this plan's shifts                 */
 } rexi_desc;
 
 typedef struct rexi_stats {

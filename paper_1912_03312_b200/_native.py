@@ -58,6 +58,7 @@ class RexiDesc(ctypes.Structure):
         ("tol", ctypes.c_double),
         ("max_iters", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
+        ("weight_ref", ctypes.c_double),
     ]
 
 
@@ -151,7 +152,7 @@ class NativePlan:
 
     def __init__(self, indptr, indices, a_vals, b_vals, shifts, weights, tau, *, a_imag=None,
                  device=0, solver=SOLVER_AUTO, refine=-1, tol=0.0, max_iters=0, shift_offset=0,
-                 stream=None):
+                 stream=None, weight_ref=0.0):
         L = lib()
         self._keep = [np.ascontiguousarray(indptr, dtype=np.int32),
                       np.ascontiguousarray(indices, dtype=np.int32),
@@ -182,6 +183,7 @@ class NativePlan:
         d.tol = float(tol)
         d.max_iters = int(max_iters)
         d.stream = stream
+        d.weight_ref = float(weight_ref)
         self.n = int(d.n)
         self.k = int(d.k)
         self.device = int(device)

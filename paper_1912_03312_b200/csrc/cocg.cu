@@ -667,6 +667,7 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
         double mean = 0.0;
         for (int j = 0; j < d->k; ++j) mean += std::hypot(d->weights[j].re, d->weights[j].im);
         mean /= std::max(1, d->k);
+        if (d->weight_ref > 0.0) mean = d->weight_ref;   // global reference (sharded runs)
         im->wts.assign(kp, 1.0);
         for (int j = 0; j < d->k; ++j) {
             const double b = std::hypot(d->weights[j].re, d->weights[j].im);

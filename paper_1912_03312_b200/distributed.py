@@ -130,7 +130,7 @@ class ShardedStepper:
         self.plan = _native.NativePlan(indptr, indices, a_re, b_re, shifts[idx], weights[idx], tau,
                                        a_imag=a_im, device=device, solver=solver, refine=refine,
                                        shift_offset=idx[0] if idx else 0, stream=stream, tol=tol,
-                                       max_iters=max_iters)
+                                       max_iters=max_iters, weight_ref=float(np.mean(np.abs(weights))))
         dev = torch.device("cuda", device)
         self.parts = torch.empty((world, 4, self.n), dtype=torch.float64, device=dev)
         self.mine = torch.empty((4, self.n), dtype=torch.float64, device=dev)

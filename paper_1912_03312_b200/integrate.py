@@ -242,7 +242,7 @@ def rexi_prepare(
                     indptr, indices, a_re, b_re, shifts[idx], weights[idx], tau, a_imag=a_im,
                     device=dev, solver=_SOLVERS[solver], refine=int(refine),
                     tol=float(tol or 0.0), max_iters=int(max_iters or 0),
-                    shift_offset=int(idx[0])))
+                    shift_offset=int(idx[0]), weight_ref=float(np.mean(np.abs(weights)))))
             except SolverError as exc:
                 m = re.search(r"j = (\d+)", str(exc))
                 j = int(m.group(1)) if m else int(idx[0])
