@@ -148,8 +148,11 @@ def assemble_p1(mesh: StructuredMesh, potential) -> SystemMatrices:
         # potential element matrices: vol h^d sum_q w_q V(x_q) lam_a lam_b
         vq = np.empty((cell_lo.shape[0], len(wq)))
         for q in range(len(wq)):
-            xq = mesh.lo + h * (cell_lo + lam[q] @ t.astype(float))
-            vq[:, q] = potential(xq)
+            off = lam[q] @ t.astype(float)                 # quadrature point, in cell units
+            if hasattr(potential, "on_cells"):
+                vq[:, q] = potential.on_cells(mesh, off)   # separable fast path
+            else:
+                vq[:, q] = potential(mesh.lo + h * (cell_lo + off))
         coef = wq[:, None, None] * lam[:, :, None] * lam[:, None, :]   # (nq, d+1, d+1)
         pot_e = (vq @ coef.reshape(len(wq), -1)) * (vol * h ** d)
         pot_e = pot_e.reshape((m,) * d + (d + 1, d + 1))
@@ -358,20 +361,38 @@ def config4_potential(seed: int = 3312, grid_m: int = 2048):
     a = rng.uniform(0.0, 1.0, 64)
     phi = rng.uniform(0.0, 2.0 * math.pi, 64)
 
-    def f(x):
-        out = np.zeros(x.shape[0])
-        for j in range(64):
-            out += a[j] * np.cos(2.0 * math.pi * (pq[j, 0] * x[:, 0] + pq[j, 1] * x[:, 1]) + phi[j])
-        return out
+    c = a * np.exp(1j * phi)
 
+    class FourierPotential:
+        """V = 1e3 F / max|F|; on_cells() evaluates all cells at one offset as
+        Re(X diag(c) Y^T) with X[i,m] = exp(2 pi i p_m x_i), Y[j,m] likewise
+        (each mode factorises per axis)."""
+
+        def __init__(self):
+            self.scale = 1.0
+
+        def f(self, x):
+            arg = 2.0 * math.pi * (np.outer(x[:, 0], pq[:, 0]) + np.outer(x[:, 1], pq[:, 1])) + phi
+            return np.cos(arg) @ a
+
+        def f_grid(self, xs, ys):
+            X = np.exp(2j * math.pi * np.outer(xs, pq[:, 0]))
+            Y = np.exp(2j * math.pi * np.outer(ys, pq[:, 1]))
+            return ((X * c) @ Y.T).real                    # [i, j]
+
+        def __call__(self, x):
+            return self.scale * self.f(x)
+
+        def on_cells(self, mesh, off):
+            m, h = mesh.m, mesh.h
+            xs = mesh.lo[0] + h * (np.arange(m) + off[0])
+            ys = mesh.lo[1] + h * (np.arange(m) + off[1])
+            return self.scale * self.f_grid(xs, ys).ravel()
+
+    v = FourierPotential()
     g = np.linspace(0.0, 1.0, grid_m + 1)
-    fmax = 0.0
-    for row in range(0, grid_m + 1, 256):
-        xs = np.stack(np.meshgrid(g[row:row + 256], g, indexing="ij"), axis=-1).reshape(-1, 2)
-        fmax = max(fmax, float(np.max(np.abs(f(xs)))))
-
-    def v(x):
-        return 1e3 * f(x) / fmax
+    fmax = float(np.max(np.abs(v.f_grid(g, g))))
+    v.scale = 1e3 / fmax
     return v
 
 
