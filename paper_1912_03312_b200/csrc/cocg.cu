@@ -52,7 +52,7 @@ struct CgMat {
 };
 
 struct CgVec {
-    c128 *x, *r, *z, *p0, *p1, *q;         // [n][kp] current (compacted) layout
+    c128 *x, *r, *z, *p, *q;               // [n][kp] current (compacted) layout
     const c128 *bvec;                      // per-shift rhs [n][kp_full] or nullptr
     const c128 *bshared;                   // shared rhs [n] or nullptr
 };
@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
                 V.x[o] = cmk(0.0, 0.0);
                 V.r[o] = b;
                 V.z[o] = z;
-                V.p0[o] = cmk(0.0, 0.0);
+                V.p[o] = cmk(0.0, 0.0);
+                V.q[o] = cmk(0.0, 0.0);
                 rho = cadd(rho, cmul(b, z));
                 bn += cabs2(b);
             }
@@ -199,26 +200,29 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
 }
 
 // ---------------------------------------------------------------------------
-// spmv: p_new = z + beta p_old (own row), q = S p_new, mu = p^T q.
-// Claims (one or more 64-row chunks) are taken per CTA from an atomic counter:
+// spmv: w = S z (only z is gathered), then pointwise p <- z + beta p and
+// q <- w + beta q (q = S p by linearity: S(z + beta p_old) = S z + beta q_old),
+// mu = p^T q.  Gathering one vector instead of two halves the neighbour
+// traffic through L2 (the bottleneck of the two-vector form).
+// Claims (one or more 32-row chunks) are taken per CTA from an atomic counter:
 // all SMs work on one coherent wavefront, so the +-n neighbour rows of a 2D/3D
 // stencil are L2 hits.  The next claim is prefetched and the shared partials
-// are double-buffered: one barrier per claim.
+// are double-buffered: one barrier per claim.  Element offsets fit in 32 bits
+// (n * kp < 2^31 is checked at plan creation).
 // ---------------------------------------------------------------------------
 template <bool CPLX>
-__global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g,
-                                                    int parity) {
+__global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
     __shared__ double2 sbp[2][CG_SBP];
     __shared__ int64_t claim_q[2];
     if (*Sc.nactive == 0) return;
     int lane, slot, slots;
     cta_geom(g, lane, slot, slots);
-    const int kp = g.kp;
+    const uint32_t kp = (uint32_t)g.kp;
     const bool act = Sc.active[lane] != 0;
     const c128 sg = S.sigma[g.lane_shift[lane]];
     const c128 beta = Sc.beta[lane];
-    const c128 *__restrict__ pold = parity ? V.p1 : V.p0;
-    c128 *__restrict__ pnew = parity ? V.p0 : V.p1;
+    c128 *__restrict__ pv = V.p;
+    c128 *__restrict__ qv = V.q;
     const c128 *__restrict__ zv = V.z;
     if (threadIdx.x == 0) claim_q[0] = (int64_t)atomicAdd(Sc.ctr, 1u);
     __syncthreads();
@@ -235,21 +239,20 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, 
             if (act) {
                 const int64_t r1 = min(r0 + CG_SB * CG_CH, M.n);
                 for (int64_t i = r0; i < r1; i += CG_CH) {
-                    c128 acc = cmk(0.0, 0.0), pi = cmk(0.0, 0.0);
+                    c128 acc = cmk(0.0, 0.0);
                     const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
 #pragma unroll 4
                     for (int32_t q = q0; q < q1; ++q) {
-                        const int32_t c = __ldg(M.indices + q);
-                        const size_t oc = (size_t)c * kp + lane;
-                        const c128 pc = cadd(zv[oc], cmul(beta, pold[oc]));
+                        const uint32_t c = (uint32_t)__ldg(M.indices + q);
                         const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
-                        acc = cadd(acc, cmul(e, pc));
-                        if (c == i) pi = pc;
+                        acc = cadd(acc, cmul(e, zv[c * kp + lane]));
                     }
-                    const size_t o = (size_t)i * kp + lane;
-                    pnew[o] = pi;
-                    V.q[o] = acc;
-                    mu = cadd(mu, cmul(pi, acc));
+                    const uint32_t o = (uint32_t)i * kp + lane;
+                    const c128 pi = cadd(zv[o], cmul(beta, pv[o]));
+                    const c128 qi = cadd(acc, cmul(beta, qv[o]));
+                    pv[o] = pi;
+                    qv[o] = qi;
+                    mu = cadd(mu, cmul(pi, qi));
                 }
             }
             sbp[buf][sbl * kp + lane] = mu;
@@ -264,8 +267,7 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, 
 // update: x += alpha p; r -= alpha q; z = D^-1 r; partials of rho' = r^T z, |r|^2
 // (claims statically strided over CTAs: pointwise, no locality to exploit)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g,
-                                                      int parity) {
+__global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
     __shared__ double2 sbc[CG_SBP];
     __shared__ double sbr[CG_SBP];
     if (*Sc.nactive == 0) return;
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
     const bool act = Sc.active[lane] != 0;
     const c128 sg = S.sigma[g.lane_shift[lane]];
     const c128 alpha = Sc.alpha[lane];
-    const c128 *__restrict__ pnew = parity ? V.p0 : V.p1;
+    const c128 *__restrict__ pnew = V.p;
     for (int64_t claim = blockIdx.x; claim < g.nclaims; claim += gridDim.x) {
         for (int ps = 0; ps < g.P; ++ps) {
             const int sbl = ps * slots + slot;
@@ -718,12 +720,15 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&im->sms, cudaDevAttrMultiProcessorCount, dev);
+    if ((double)n * kp >= 2147483647.0) {
+        err = "COCG plan too large for 32-bit element offsets (n * k_pad >= 2^31); split the shifts";
+        return REXI_ERR_UNSUPPORTED;
+    }
     const size_t vb = sizeof(c128) * (size_t)n * kp;
     CGA(im->V.x, vb);
     CGA(im->V.r, vb);
     CGA(im->V.z, vb);
-    CGA(im->V.p0, vb);
-    CGA(im->V.p1, vb);
+    CGA(im->V.p, vb);
     CGA(im->V.q, vb);
     CGA(im->scratch, vb);
     CGA(im->xout, vb);
@@ -765,7 +770,7 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
 
 // repack the live lanes into a layout of width kp_new (host decides the map)
 static int cg_repack(CocgImpl *im, int kp_old, int kp_new, const std::vector<int> &map,
-                     const std::vector<int> &drop_mask, std::vector<int> &lane_shift, int parity_live,
+                     const std::vector<int> &drop_mask, std::vector<int> &lane_shift,
                      cudaStream_t st, std::string &err) {
     const int64_t n = im->M.n;
     // 1) frozen lanes being dropped: x -> full-width solution
@@ -776,7 +781,7 @@ static int cg_repack(CocgImpl *im, int kp_old, int kp_new, const std::vector<int
     // 2) live vectors x, r, z, p(current) -> new width, through the scratch array
     CGK(cudaMemcpyAsync(im->map, map.data(), sizeof(int) * kp_new, cudaMemcpyHostToDevice, st));
     const int64_t t_new = n * kp_new;
-    c128 **vecs[4] = {&im->V.x, &im->V.r, &im->V.z, parity_live ? &im->V.p0 : &im->V.p1};
+    c128 **vecs[5] = {&im->V.x, &im->V.r, &im->V.z, &im->V.p, &im->V.q};
     for (c128 **v : vecs) {
         k_cg_repack<<<(unsigned)((t_new + 255) / 256), 256, 0, st>>>(*v, im->scratch, n, kp_old, kp_new, im->map);
         std::swap(*v, im->scratch);
@@ -822,20 +827,19 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     CGK(cudaGetLastError());
     *launches += 2;
     int live = cg.k;
-    int it = 0, parity = 0;
+    int it = 0;
     const int check_every = 8;
     for (;;) {
         for (int s = 0; s < check_every; ++s) {
-            hook_begin(cg, "cg_spmv", 64.0 * n * live + nnzb);
-            if (im->cplx) k_cg_spmv<true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
-            else k_cg_spmv<false><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
+            hook_begin(cg, "cg_spmv", 80.0 * n * live + nnzb);
+            if (im->cplx) k_cg_spmv<true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+            else k_cg_spmv<false><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
             k_cg_finish<1><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             hook_begin(cg, "cg_update", 112.0 * n * live + 24.0 * n);
-            k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g, parity);
+            k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
             k_cg_finish<2><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
-            parity ^= 1;
             *launches += 4;
             ++it;
         }
@@ -861,8 +865,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             }
             const int live = (int)map.size();
             for (int l = live; l < kp_new; ++l) map.push_back(map[0]);
-            // current p: the buffer the last spmv wrote (parity already toggled)
-            int rc = cg_repack(im, kp, kp_new, map, drop, lane_shift, parity ? 0 : 1, st, err);
+            int rc = cg_repack(im, kp, kp_new, map, drop, lane_shift, st, err);
             if (rc) return rc;
             std::vector<int> act(kp_new, 1);
             valid.assign(kp_new, 1);
