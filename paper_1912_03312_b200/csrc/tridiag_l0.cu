@@ -338,50 +338,55 @@ __device__ __forceinline__ void k2_solve(const L0Args &a, const L0Layout &l, con
 template <int M, bool FULL>
 __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
                                           c128 xn, c128 (&y)[M]) {
+    static_assert(FULL, "level 0 is padded to full blocks");
     const c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
-    const c128 *tc = l.t1 + (size_t)c.lr0 * c.kp + c.j;
+    c128 *tc = l.t1 + (size_t)c.lr0 * c.kp + c.j;
     const RowView &rv = l.rv;
     const int kp = c.kp, j = c.j;
-    const int cnt = FULL ? M - 1 : c.cnt;
-    // interior residuals r_q = d_q - a_q x_{q-1} - b_q x_q - c_q x_{q+1}
-#pragma unroll
-    for (int q = 1; q < M; ++q) {
-        if (FULL || q <= cnt) {
-            const int lr = c.lr0 + q;
-            const c128 d = rv.rhs[lr];
-            const c128 xp = q < cnt ? tc[(q + 1) * kp] : xn;
-            ddacc re = {d.x, 0.0}, im = {d.y, 0.0};
-            dot2_sub(re, im, rv.sub(lr, c.sg), tc[(q - 1) * kp]);
-            dot2_sub(re, im, rv.dia(lr, c.sg), tc[q * kp]);
-            dot2_sub(re, im, rv.sup(lr, c.sg), xp);
-            const c128 r = cmk(__dadd_rn(re.hi, re.lo), __dadd_rn(im.hi, im.lo));
-            a.rres_out[(c.base + q) * kp + j] = r;
-            y[q] = r;
-        }
-    }
-    // interface row: d_s - b_s x_s - c_s x_{s+1} (the -a_s x_{s-1} half comes from block p-1)
-    ddacc p1re, p1im;
+    constexpr int cnt = M - 1;
+    // interface row s: d_s - b_s x_s - c_s x_{s+1} (the -a_s x_{s-1} half comes
+    // from block p-1) and this block's half of the next interface row; taken
+    // before the residual loop recycles the x slots
+    ddacc p1re, p1im, p2re = {0.0, 0.0}, p2im = {0.0, 0.0};
     {
         const c128 d = rv.rhs[c.lr0];
         p1re = {d.x, 0.0};
         p1im = {d.y, 0.0};
         dot2_sub(p1re, p1im, rv.dia(c.lr0, c.sg), xs);
-        dot2_sub(p1re, p1im, rv.sup(c.lr0, c.sg), cnt >= 1 ? tc[kp] : xn);
+        dot2_sub(p1re, p1im, rv.sup(c.lr0, c.sg), tc[kp]);
     }
-    // correction reduce: S1 with rhs = r, in place (r_q is read before y_q is written)
+    const bool has_next = c.p + 1 < c.P;
+    const c128 an = rv.sub(c.lr0 + M, c.sg);
+    if (has_next) dot2_sub(p2re, p2im, an, tc[cnt * kp]);
+    // interior residuals r_q = d_q - a_q x_{q-1} - b_q x_q - c_q x_{q+1}, error-free
+    // products; r_q goes to slot q-1 (x_{q-1} is dead once r_q is formed) -- a
+    // rolled loop keeps the kernel's code and register footprint small
+    c128 xm = tc[0], x0 = tc[kp];
+#pragma unroll 1
+    for (int q = 1; q < M; ++q) {
+        const int lr = c.lr0 + q;
+        const c128 xp = q < cnt ? tc[(q + 1) * kp] : xn;
+        const c128 d = rv.rhs[lr];
+        ddacc re = {d.x, 0.0}, im = {d.y, 0.0};
+        dot2_sub(re, im, rv.sub(lr, c.sg), xm);
+        dot2_sub(re, im, rv.dia(lr, c.sg), x0);
+        dot2_sub(re, im, rv.sup(lr, c.sg), xp);
+        const c128 r = cmk(__dadd_rn(re.hi, re.lo), __dadd_rn(im.hi, im.lo));
+        a.rres_out[(c.base + q) * kp + j] = r;
+        tc[(q - 1) * kp] = r;
+        xm = x0;
+        x0 = xp;
+    }
+    // correction reduce: S1 with rhs = r
     y[0] = cmk(0.0, 0.0);
-    sweep_fwd<M, FULL>(y, ti, kp, rv, c.lr0, cnt, c.sg, [&](int q) { return y[q]; });
-    const c128 ylast = pick_last<M, FULL>(y, cnt);
+    sweep_fwd<M, FULL>(y, ti, kp, rv, c.lr0, cnt, c.sg, [&](int q) { return tc[(q - 1) * kp]; });
+    const c128 ylast = y[M - 1];
     sweep_bwd<M, FULL>(y, ti, kp, rv, c.lr0, cnt, c.sg, cmk(0.0, 0.0), [](int, c128) {});
-    const c128 yfirst = cnt >= 1 ? y[1] : cmk(0.0, 0.0);
-    const c128 t1 = cneg(cmul(rv.sup(c.lr0, c.sg), yfirst));
+    const c128 t1 = cneg(cmul(rv.sup(c.lr0, c.sg), y[1]));
     ddacc_add(p1re, t1.x);
     ddacc_add(p1im, t1.y);
     a.L.ypdd[c.p * kp + j] = cdd{{p1re.hi, p1re.lo}, {p1im.hi, p1im.lo}};
-    if (c.p + 1 < c.P) {
-        const c128 an = rv.sub(c.lr0 + M, c.sg);
-        ddacc p2re = {0.0, 0.0}, p2im = {0.0, 0.0};
-        dot2_sub(p2re, p2im, an, cnt >= 1 ? tc[cnt * kp] : xs);
+    if (has_next) {
         const c128 t2 = cneg(cmul(an, ylast));
         ddacc_add(p2re, t2.x);
         ddacc_add(p2im, t2.y);
