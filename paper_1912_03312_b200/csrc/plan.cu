@@ -227,12 +227,17 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
     }
     T.z = L0Dev{dz[0], dz[1], dz[2], dz[3], dz[4], dz[5], dz[6], dz[7], dz[8], dz[2], dz[5], dz[8]};
 
+    // symmetric pencil (the FEM case): reduced levels keep only sup
+    bool sym = true;
+    for (int64_t r = 0; r + 1 < n && sym; ++r)
+        sym = a_sup[r] == a_sub[r + 1] && ai_sup[r] == ai_sub[r + 1] && b_sup[r] == b_sub[r + 1];
     // levels
     const int kp = plan->kp;
     int64_t nl = n0;
     for (;;) {
         LevelDev L{};
         L.n = nl;
+        L.sym = sym ? 1 : 0;
         if (!T.lv.empty() && nl <= TOP_MAX) {
             L.top = 1;
             L.P = 0;
@@ -244,7 +249,7 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
         DALLOC(L.invd, rows);
         DALLOC(L.X, rows);
         if (!T.lv.empty()) {
-            DALLOC(L.sub, rows);
+            if (!sym) DALLOC(L.sub, rows);
             DALLOC(L.dia, rows);
             DALLOC(L.sup, rows);
         }

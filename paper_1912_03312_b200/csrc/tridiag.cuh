@@ -41,6 +41,7 @@ struct LevelDev {
     int64_t n;        // rows of this level
     int64_t P;        // blocks (= rows of the next level)
     int top;          // 1: solved directly
+    int sym;          // 1: symmetric pencil -> reduced levels store sup only
     c128 *sub, *dia, *sup;          // explicit coefficients, levels >= 1
     c128 *invd;                     // inverse pivots of interior rows
     c128 *ypart, *lc;               // S1 outputs: next-level rhs = ypart + lc  [P][kp]
@@ -60,6 +61,9 @@ template <bool L0>
 __device__ __forceinline__ c128 co_sub(const L0Dev &z, const LevelDev &L, const ShiftDev &S,
                                        int64_t i, int j, c128 sg) {
     if constexpr (L0) return form_entry(__ldg(z.ta_sub + i), __ldg(z.ta_sub_im + i), __ldg(z.b_sub + i), sg);
+    // reduced levels of a symmetric pencil are complex symmetric: sub_i := sup_{i-1}
+    // (one array, used consistently by the factorisation and the sweeps)
+    else if (L.sym) return i > 0 ? L.sup[(i - 1) * S.kp + j] : cmk(0.0, 0.0);
     else return L.sub[i * S.kp + j];
 }
 template <bool L0>

@@ -222,7 +222,7 @@ __global__ void k_top_solve(LevelDev L, ShiftDev S, const c128 *__restrict__ rin
     for (int64_t i = 0; i < n; ++i) {
         c128 d = rdd_a ? cdd_round(cdd_add(rdd_a[i * kp + j], rdd_b[i * kp + j]))
                        : cadd(rin_a[i * kp + j], rin_b[i * kp + j]);
-        c128 ai = L.sub[i * kp + j];
+        c128 ai = L.sym ? (i > 0 ? L.sup[(i - 1) * kp + j] : cmk(0.0, 0.0)) : L.sub[i * kp + j];
         yp = cmul(L.invd[i * kp + j], cfnma(d, ai, yp));
         L.X[i * kp + j] = yp;
     }
@@ -330,7 +330,7 @@ __global__ void k_assemble(L0Dev z, LevelDev L, LevelDev N, ShiftDev S) {
     }
     dv = csub(dv, cmul(cs, L.phiF[p * kp + j]));
     if (p + 1 < L.P) uv = cneg(cmul(cs, L.psiF[p * kp + j]));
-    N.sub[p * kp + j] = lv;
+    if (!N.sym) N.sub[p * kp + j] = lv;
     N.dia[p * kp + j] = dv;
     N.sup[p * kp + j] = uv;
 }
@@ -344,7 +344,10 @@ __global__ void k_top_factor(LevelDev L, ShiftDev S, unsigned long long *pmin,
     c128 ivp = cmk(0.0, 0.0);
     for (int64_t i = 0; i < L.n; ++i) {
         c128 delta = L.dia[i * kp + j];
-        if (i > 0) delta = csub(delta, cmul(L.sub[i * kp + j], cmul(L.sup[(i - 1) * kp + j], ivp)));
+        if (i > 0) {
+            const c128 ai = L.sym ? L.sup[(i - 1) * kp + j] : L.sub[i * kp + j];
+            delta = csub(delta, cmul(ai, cmul(L.sup[(i - 1) * kp + j], ivp)));
+        }
         pivot_stats(delta, mn, mx);
         ivp = crcp(delta);
         L.invd[i * kp + j] = ivp;

@@ -396,7 +396,7 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
 }
 
 template <int M>
-__global__ void __launch_bounds__(L0_NT, 2) k_l0_k2(L0Args a) {
+__global__ void __launch_bounds__(L0_NT, 3) k_l0_k2(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int flags = ST_RHS | ST_DIA | ST_TILE2;
     const L0Layout l = carve(smem, a.S.kp, M, flags);
