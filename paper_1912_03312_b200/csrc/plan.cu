@@ -350,9 +350,13 @@ int tri_mid(rexi_plan *plan, bool dd) {
     TriState &T = plan->tri;
     const size_t nl = T.lv.size();
     cudaStream_t st = plan->stream;
+    const bool tma = T.lv[0].sym && l0v2_supported(plan->kp);
     for (size_t l = 1; l + 1 < nl; ++l) {
         ProfScope ps(plan, "s1_lv");
-        if (l == 1 && dd) CK(tri_launch_lv_dd(T.lv[1], plan->S, 1, T.lv[0].ypdd, T.lv[0].lcdd, nullptr, st));
+        const bool d = l == 1 && dd;
+        if (tma) CK(lv_launch_tma(T.lv[l], plan->S, 1, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
+                                  d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, nullptr, st));
+        else if (d) CK(tri_launch_lv_dd(T.lv[1], plan->S, 1, T.lv[0].ypdd, T.lv[0].lcdd, nullptr, st));
         else CK(tri_launch_s1(T.z, T.lv[l], plan->S, (int)l, nullptr, nullptr, T.lv[l - 1].ypart,
                               T.lv[l - 1].lc, st));
     }
@@ -363,7 +367,10 @@ int tri_mid(rexi_plan *plan, bool dd) {
     }
     for (size_t l = nl - 1; l-- > 1;) {
         ProfScope ps(plan, "s3_lv");
-        if (l == 1 && dd) CK(tri_launch_lv_dd(T.lv[1], plan->S, 3, T.lv[0].ypdd, T.lv[0].lcdd, T.lv[2].X, st));
+        const bool d = l == 1 && dd;
+        if (tma) CK(lv_launch_tma(T.lv[l], plan->S, 3, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
+                                  d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, T.lv[l + 1].X, st));
+        else if (d) CK(tri_launch_lv_dd(T.lv[1], plan->S, 3, T.lv[0].ypdd, T.lv[0].lcdd, T.lv[2].X, st));
         else CK(tri_launch_s3(T.z, T.lv[l], plan->S, (int)l, nullptr, nullptr, T.lv[l - 1].ypart,
                               T.lv[l - 1].lc, T.lv[l + 1].X, TRI_OUT_X, nullptr, 0, nullptr, st));
     }

@@ -464,6 +464,150 @@ __global__ void __launch_bounds__(L0_NT, 4) k_l0_k3(L0Args a) {
 }
 
 // ---------------------------------------------------------------------------
+// Levels >= 1 (explicit reduced coefficients, symmetric pencils): TMA-staged
+// invd and sup tiles (sub_q := sup_{q-1}); the block's rhs goes straight into
+// the sweep registers.  PHASE 1 -> reduced rhs of the next level, PHASE 3 -> X.
+// ---------------------------------------------------------------------------
+#ifndef LV_MINB
+#define LV_MINB 3
+#endif
+struct LvArgs {
+    LevelDev L;
+    ShiftDev S;
+    const c128 *rin_a, *rin_b;   // previous level ypart / lc
+    const cdd *rdd_a, *rdd_b;    // or their double-double versions (correction pass)
+    const c128 *Xnext;
+};
+
+struct LvPtrs {
+    const c128 *inv, *sup;          // staged tiles (+ lane offset)
+    const c128 *ra, *rb;
+    const cdd *da, *db;
+    const c128 *Xn;
+    c128 *ypart, *lc, *X;
+};
+
+template <bool DD>
+__device__ __forceinline__ c128 lv_rhs(const LvPtrs &q, int64_t i, int j, int kp) {
+    if constexpr (DD) return cdd_round(cdd_add(q.da[i * kp + j], q.db[i * kp + j]));
+    else return cadd(q.ra[i * kp + j], q.rb[i * kp + j]);
+}
+
+template <int M, int PHASE, bool DD, bool FULL>
+__device__ __forceinline__ void lv_body(const LvPtrs &t, int lr0, int kp, int j, int64_t p, int64_t P,
+                                        int64_t base, int cnt) {
+    c128 y[M];
+#pragma unroll
+    for (int q = 1; q < M; ++q)
+        if (FULL || q <= cnt) y[q] = lv_rhs<DD>(t, base + q, j, kp);
+    c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
+    if (PHASE == 3) {
+        xs = t.Xn[p * kp + j];
+        if (p + 1 < P) xn = t.Xn[(p + 1) * kp + j];
+    }
+    y[0] = xs;
+#pragma unroll
+    for (int q = 1; q < M; ++q) {
+        if (FULL || q <= cnt) {
+            const c128 aq = t.sup[(lr0 + q - 1) * kp];            // sub_q = sup_{q-1}
+            y[q] = cmul(t.inv[(lr0 + q) * kp], cfnma(y[q], aq, y[q - 1]));
+        }
+    }
+    c128 ylast = y[0];
+    if (FULL) ylast = y[M - 1];
+    else {
+#pragma unroll
+        for (int q = 1; q < M; ++q)
+            if (q == cnt) ylast = y[q];
+    }
+    c128 xnext = xn;
+#pragma unroll
+    for (int q = M - 1; q >= 1; --q) {
+        if (FULL || q <= cnt) {
+            xnext = cfnma(y[q], t.inv[(lr0 + q) * kp], cmul(t.sup[(lr0 + q) * kp], xnext));
+            y[q] = xnext;
+        }
+    }
+    if constexpr (PHASE == 1) {
+        const c128 yfirst = cnt >= 1 ? y[1] : cmk(0.0, 0.0);
+        const c128 ds = lv_rhs<DD>(t, base, j, kp);
+        t.ypart[p * kp + j] = cfnma(ds, t.sup[lr0 * kp], yfirst);
+        if (p + 1 < P) t.lc[(p + 1) * kp + j] = cneg(cmul(t.sup[(lr0 + M - 1) * kp], ylast));
+        if (p == 0) t.lc[j] = cmk(0.0, 0.0);
+    } else {
+        t.X[base * kp + j] = xs;
+#pragma unroll
+        for (int q = 1; q < M; ++q)
+            if (FULL || q <= cnt) t.X[(base + q) * kp + j] = y[q];
+    }
+}
+
+template <int M, int PHASE, bool DD>
+__global__ void __launch_bounds__(L0_NT, LV_MINB) k_lv_tma(const __grid_constant__ LvArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    const int kp = a.S.kp;
+    const int bpc = L0_NT / kp;
+    const int T = bpc * M;
+    c128 *tinv = reinterpret_cast<c128 *>(smem + 128);
+    c128 *tsup = tinv + (size_t)T * kp;
+    const int b = threadIdx.x / kp, j = threadIdx.x % kp;
+    const int64_t n = a.L.n, P = a.L.P;
+    const int64_t row0 = (int64_t)blockIdx.x * T;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int64_t row1 = min(row0 + (int64_t)T, n);
+        const uint32_t tb = (uint32_t)((row1 - row0) * kp * sizeof(c128));
+        mbar_expect_tx(bar, 2 * tb);
+        bulk_g2s(tinv, a.L.invd + row0 * kp, tb, bar);
+        bulk_g2s(tsup, a.L.sup + row0 * kp, tb, bar);
+    }
+    const int64_t p = (int64_t)blockIdx.x * bpc + b;
+    const bool active = p < P;
+    const int64_t base = p * M;
+    const int cnt = active ? (int)min((int64_t)M, n - base) - 1 : -1;
+    mbar_wait(bar, 0);
+    if (!active) return;
+    LvPtrs t;
+    t.inv = tinv + j; t.sup = tsup + j;
+    t.ra = a.rin_a; t.rb = a.rin_b; t.da = a.rdd_a; t.db = a.rdd_b; t.Xn = a.Xnext;
+    t.ypart = a.L.ypart; t.lc = a.L.lc; t.X = a.L.X;
+    if (cnt == M - 1) lv_body<M, PHASE, DD, true>(t, b * M, kp, j, p, P, base, cnt);
+    else lv_body<M, PHASE, DD, false>(t, b * M, kp, j, p, P, base, cnt);
+}
+
+cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,
+                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st) {
+    LvArgs a{};
+    a.L = L; a.S = S; a.rin_a = rin_a; a.rin_b = rin_b; a.rdd_a = rdd_a; a.rdd_b = rdd_b; a.Xnext = Xnext;
+    const int kp = S.kp;
+    const int64_t rows = (int64_t)(L0_NT / kp) * TRI_M;
+    const int64_t grid = (L.n + rows - 1) / rows;
+    const size_t smem = 128 + 2 * (size_t)rows * kp * sizeof(c128);
+    cudaError_t e;
+#define LV_LAUNCH(PH, DDV)                                                                              \
+    do {                                                                                                \
+        auto kern = k_lv_tma<TRI_M, PH, DDV>;                                                            \
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+        if (e != cudaSuccess) return e;                                                                 \
+        kern<<<(unsigned)grid, L0_NT, smem, st>>>(a);                                                   \
+    } while (0)
+    if (phase == 1) {
+        if (rdd_a) LV_LAUNCH(1, true);
+        else LV_LAUNCH(1, false);
+    } else {
+        if (rdd_a) LV_LAUNCH(3, true);
+        else LV_LAUNCH(3, false);
+    }
+#undef LV_LAUNCH
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 template <typename K>
 static cudaError_t launch_l0(K kern, const L0Args &a, int flags, cudaStream_t st) {
     const int kp = a.S.kp;

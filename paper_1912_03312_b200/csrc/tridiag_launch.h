@@ -30,6 +30,10 @@ cudaError_t tri_launch_lv_dd(const LevelDev &L, const ShiftDev &S, int phase, co
 cudaError_t tri_launch_top_solve_dd(const LevelDev &L, const ShiftDev &S, const cdd *rdd_a,
                                     const cdd *rdd_b, cudaStream_t st);
 
+// TMA-fed kernel for levels >= 1 of symmetric pencils (tridiag_l0.cu)
+cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,
+                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st);
+
 // TMA-fed level-0 kernels (tridiag_l0.cu)
 bool l0v2_supported(int kp);
 int64_t l0_row_padding();

@@ -26,4 +26,11 @@ for which in sys.argv[1:] or ["1", "2"]:
         nst = 20
         t = time.time(); out = rexi_run(stp, ud, nst); torch.cuda.synchronize(); dt = (time.time()-t)/nst
         print(f"  device-resident: {dt*1e3:.3f} ms/step  ({1/dt:.1f} steps/s)", flush=True)
+        if os.environ.get("PROBE_PROF"):
+            stp.plans[0].profile(True)
+            rexi_run(stp, ud, nst); torch.cuda.synchronize()
+            rep = stp.plans[0].profile_report(); stp.plans[0].profile(False)
+            tot = sum(v[1] for v in rep.values())
+            for k, v in sorted(rep.items(), key=lambda kv: -kv[1][1]):
+                print(f"    {k:12s} n={v[0]:5d} {v[1]/nst:.4f} ms/step {100*v[1]/tot:5.1f}%")
         stp.close()
