@@ -23,6 +23,15 @@
  *   rexi_plan_solve    <- factorizations[j].solve(b)  solvers.py:76-80
  *   rexi_plan_destroy  <- RexiStepper.close()   integrate.py:131-140
  *
+ * and, for the prepare/comparison paths around the step,
+ * a pencil object holding (A, B) on one GPU:
+ *
+ *   rexi_pencil_create           <- factorize(sys.B)         solvers.py:108-115
+ *   rexi_pencil_solve_b          <- factorize(sys.B).solve   solvers.py:76-80
+ *   rexi_pencil_spectral_radius  <- spectral_radius_estimate spatial.py:314-344
+ *   rexi_pencil_cheb_step        <- chebyshev_step / _run    integrate.py:333-377
+ *   rexi_pencil_destroy
+ *
  * Conventions: plain pointers and sizes only.  Complex values are
  * interleaved (re, im) doubles, layout-compatible with numpy complex128.
  * Every call returns a rexi_status; on failure rexi_plan_last_error() (or
@@ -147,6 +156,38 @@ int rexi_plan_destroy(rexi_plan *plan);
 const char *rexi_plan_last_error(const rexi_plan *plan);
 const char *rexi_last_error(void);
 int rexi_device_count(int32_t *count);
+
+/* ---- pencil (A, B): B-solves, spectral radius, Chebyshev stepping ---- */
+typedef struct rexi_pencil rexi_pencil;
+
+/* Uses n, nnz, indptr, indices, a_vals, a_imag, b_vals, device, stream and
+ * tol / max_iters (CG on B: relative residual target, 0 -> 1e-14; iteration
+ * cap, 0 -> 1000) of the descriptor; k, shifts, weights, tau are ignored.
+ * B must be symmetric positive definite (the reference's mass matrix);
+ * REXI_ERR_SINGULAR if a diagonal entry of B is not positive. */
+int rexi_pencil_create(const rexi_desc *desc, rexi_pencil **out);
+
+/* x = B^-1 rhs (Jacobi-preconditioned CG); mem applies to rhs and x. */
+int rexi_pencil_solve_b(rexi_pencil *pencil, const rexi_c128 *rhs, rexi_c128 *x, int32_t mem,
+                        int32_t *iterations);
+
+/* Power iteration on B^-1 A from the host start vector v0 (normalised on
+ * the device), Rayleigh quotient |v^H A v / v^H B v|, stop when two
+ * successive quotients agree to tol relative (spatial.py:314-344).
+ * iterations / converged as in SpectralRadiusEstimate (spatial.py:296-311). */
+int rexi_pencil_spectral_radius(rexi_pencil *pencil, const rexi_c128 *v0, double tol, int32_t max_iters,
+                                double *value, int32_t *iterations, int32_t *converged);
+
+/* n_steps Chebyshev steps u <- p(tau M) u by the Clenshaw recurrence with
+ * coefficients coeffs[0..degree] and scale = -tau/R (integrate.py:333-356):
+ * b_k = a_k u + 2 scale B^-1 A b_{k+1} - b_{k+2}, out = a_0 u + scale B^-1 A b_1 - b_2.
+ * mem applies to u_in / u_out; stats: device time, CG iterations (max and
+ * mean per B-solve), launches. */
+int rexi_pencil_cheb_step(rexi_pencil *pencil, const rexi_c128 *coeffs, int32_t degree, double scale,
+                          const rexi_c128 *u_in, rexi_c128 *u_out, int32_t n_steps, int32_t mem,
+                          rexi_stats *stats);
+const char *rexi_pencil_last_error(const rexi_pencil *pencil);
+int rexi_pencil_destroy(rexi_pencil *pencil);
 int32_t rexi_abi_version(void);
 
 #ifdef __cplusplus

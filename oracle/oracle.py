@@ -178,3 +178,48 @@ def rel_l2(x, y):
     y = np.asarray(y)
     d = np.linalg.norm(y)
     return float(np.linalg.norm(x - y) / (d if d > 0 else 1.0))
+
+
+# ---------------------------------------------------------------------------
+# prepare/comparison paths, numpy/scipy restatements
+# ---------------------------------------------------------------------------
+
+def _b_solver(B):
+    from scipy.sparse.linalg import splu
+    return splu(B.tocsc().astype(complex)).solve
+
+
+def power_iteration(sysm, tol=1e-6, max_iters=500, seed=0):
+    """Restates ``spectral_radius_estimate`` (reference spatial.py:314-344):
+    power iteration on B^-1 A from default_rng(seed).standard_normal(n),
+    Rayleigh quotient |v^H A v / v^H B v|, relative-change stop.  B^-1 by a
+    sparse LU (the reference's banded/dense LU).  Returns (value, its, conv)."""
+    solve_b = _b_solver(sysm.B)
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(sysm.n_dof).astype(complex)
+    v /= np.linalg.norm(v)
+    prev = None
+    rq = 0.0
+    it = 0
+    for it in range(1, max_iters + 1):
+        av = sysm.A @ v
+        rq = abs(np.vdot(v, av) / np.vdot(v, sysm.B @ v))
+        if prev is not None and abs(rq - prev) <= tol * max(rq, 1e-300):
+            return float(rq), it, True
+        prev = rq
+        w = solve_b(av)
+        v = w / np.linalg.norm(w)
+    return float(rq), it, False
+
+
+def clenshaw_step(sysm, coeffs, tau, radius, u):
+    """Restates ``chebyshev_step`` (reference integrate.py:333-356): Clenshaw
+    backward recurrence for sum a_k T_k(-(tau/R) B^-1 A) u."""
+    solve_b = _b_solver(sysm.B)
+    s = -(tau / radius)
+    u = np.asarray(u, dtype=complex)
+    b1 = np.zeros_like(u)
+    b2 = np.zeros_like(u)
+    for k in range(len(coeffs) - 1, 0, -1):
+        b1, b2 = coeffs[k] * u + 2.0 * s * solve_b(sysm.A @ b1) - b2, b1
+    return coeffs[0] * u + s * solve_b(sysm.A @ b1) - b2

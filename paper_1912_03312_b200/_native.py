@@ -33,7 +33,9 @@ EXPORTED = (
     "rexi_plan_create", "rexi_plan_step", "rexi_plan_step_partial", "rexi_combine_partials",
     "rexi_plan_solve", "rexi_plan_info", "rexi_plan_destroy", "rexi_plan_last_error",
     "rexi_last_error", "rexi_device_count", "rexi_abi_version", "rexi_plan_profile",
-    "rexi_plan_profile_report",
+    "rexi_plan_profile_report", "rexi_pencil_create", "rexi_pencil_solve_b",
+    "rexi_pencil_spectral_radius", "rexi_pencil_cheb_step", "rexi_pencil_last_error",
+    "rexi_pencil_destroy",
 )
 
 
@@ -117,6 +119,16 @@ def lib():
     L.rexi_abi_version.restype = ctypes.c_int32
     L.rexi_plan_profile.argtypes = [vp, ctypes.c_int32]
     L.rexi_plan_profile_report.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    L.rexi_pencil_create.argtypes = [ctypes.POINTER(RexiDesc), ctypes.POINTER(vp)]
+    L.rexi_pencil_solve_b.argtypes = [vp, vp, vp, ctypes.c_int32, i32p]
+    L.rexi_pencil_spectral_radius.argtypes = [vp, vp, ctypes.c_double, ctypes.c_int32,
+                                              ctypes.POINTER(ctypes.c_double), i32p, i32p]
+    L.rexi_pencil_cheb_step.argtypes = [vp, vp, ctypes.c_int32, ctypes.c_double, vp, vp,
+                                        ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(RexiStats)]
+    L.rexi_pencil_last_error.argtypes = [vp]
+    L.rexi_pencil_last_error.restype = ctypes.c_char_p
+    L.rexi_pencil_destroy.argtypes = [vp]
     if L.rexi_abi_version() != ABI_VERSION:
         raise DeviceError("native library ABI version mismatch")
     _lib = L
@@ -244,6 +256,90 @@ class NativePlan:
     def close(self):
         if getattr(self, "_h", None):
             lib().rexi_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NativePencil:
+    """Owns one ``rexi_pencil``: the pencil (A, B) on one device, for B-solves,
+    the spectral-radius power iteration and Chebyshev stepping."""
+
+    def __init__(self, indptr, indices, a_vals, b_vals, *, a_imag=None, device=0, tol=0.0,
+                 max_iters=0, stream=None):
+        L = lib()
+        self._keep = [np.ascontiguousarray(indptr, dtype=np.int32),
+                      np.ascontiguousarray(indices, dtype=np.int32),
+                      np.ascontiguousarray(a_vals, dtype=np.float64),
+                      np.ascontiguousarray(b_vals, dtype=np.float64)]
+        if a_imag is not None:
+            self._keep.append(np.ascontiguousarray(a_imag, dtype=np.float64))
+        ip, ix, av, bv = self._keep[:4]
+        d = RexiDesc()
+        d.abi_version = ABI_VERSION
+        d.n = len(ip) - 1
+        d.nnz = len(ix)
+        d.indptr = ip.ctypes.data
+        d.indices = ix.ctypes.data
+        d.a_vals = av.ctypes.data
+        d.a_imag = self._keep[4].ctypes.data if a_imag is not None else None
+        d.b_vals = bv.ctypes.data
+        d.device = int(device)
+        d.tol = float(tol)
+        d.max_iters = int(max_iters)
+        d.stream = stream
+        self.n = int(d.n)
+        self.device = int(device)
+        h = ctypes.c_void_p(None)
+        rc = L.rexi_pencil_create(ctypes.byref(d), ctypes.byref(h))
+        if rc != REXI_OK:
+            raise_status(rc, L.rexi_last_error().decode())
+        self._h = h
+
+    def _err(self) -> str:
+        return lib().rexi_pencil_last_error(self._h).decode()
+
+    def solve_b(self, rhs: np.ndarray):
+        rhs = np.ascontiguousarray(rhs, dtype=np.complex128)
+        x = np.empty_like(rhs)
+        it = ctypes.c_int32(0)
+        rc = lib().rexi_pencil_solve_b(self._h, _ptr(rhs), _ptr(x), MEM_HOST, ctypes.byref(it))
+        raise_status(rc, self._err())
+        return x, int(it.value)
+
+    def spectral_radius(self, v0: np.ndarray, tol: float, max_iters: int):
+        v0 = np.ascontiguousarray(v0, dtype=np.complex128)
+        val = ctypes.c_double(0.0)
+        it = ctypes.c_int32(0)
+        conv = ctypes.c_int32(0)
+        rc = lib().rexi_pencil_spectral_radius(self._h, _ptr(v0), float(tol), int(max_iters),
+                                               ctypes.byref(val), ctypes.byref(it), ctypes.byref(conv))
+        raise_status(rc, self._err())
+        return float(val.value), int(it.value), bool(conv.value)
+
+    def cheb_step(self, coeffs, scale: float, u_ptr, out_ptr, n_steps: int, mem: int,
+                  stats: RexiStats | None = None):
+        c = np.ascontiguousarray(coeffs, dtype=np.complex128)
+        rc = lib().rexi_pencil_cheb_step(self._h, _ptr(c), len(c) - 1, float(scale),
+                                         ctypes.c_void_p(u_ptr), ctypes.c_void_p(out_ptr),
+                                         int(n_steps), int(mem),
+                                         ctypes.byref(stats) if stats is not None else None)
+        raise_status(rc, self._err())
+
+    def cheb_step_host(self, coeffs, scale: float, u: np.ndarray, n_steps: int = 1,
+                       stats: RexiStats | None = None) -> np.ndarray:
+        u = np.ascontiguousarray(u, dtype=np.complex128)
+        out = np.empty_like(u)
+        self.cheb_step(coeffs, scale, u.ctypes.data, out.ctypes.data, n_steps, MEM_HOST, stats)
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().rexi_pencil_destroy(self._h)
             self._h = None
 
     def __del__(self):

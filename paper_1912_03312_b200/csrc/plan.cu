@@ -32,6 +32,10 @@ struct TriState {
 
 }  // namespace
 
+namespace rexi {
+void set_global_error(const std::string &msg) { g_last_error = msg; }
+}  // namespace rexi
+
 struct rexi_plan {
     int device = 0;
     int solver = REXI_SOLVER_AUTO;

@@ -21,6 +21,9 @@ namespace rexi {
 constexpr int L0_NT = 128;      // threads per CTA
 constexpr int L0_ROWPAD = 2;    // extra staged rows (next interface row + 16-B rounding)
 
+#ifndef K2_MINB
+#define K2_MINB 3
+#endif
 struct L0Args {
     L0Dev z;
     LevelDev L;
@@ -396,7 +399,7 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
 }
 
 template <int M>
-__global__ void __launch_bounds__(L0_NT, 3) k_l0_k2(L0Args a) {
+__global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int flags = ST_RHS | ST_DIA | ST_TILE2;
     const L0Layout l = carve(smem, a.S.kp, M, flags);

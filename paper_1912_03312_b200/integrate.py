@@ -161,26 +161,6 @@ class RexiStepper:
         raise IndexError(j)
 
 
-def _estimate_sr(sysm) -> float:
-    """Power iteration on B^-1 A (the reference algorithm, spatial.py:314-344),
-    host-side prepare utility; only used when ``sr_value`` is not given."""
-    from scipy.sparse.linalg import splu
-    solve_b = splu(sysm.B.tocsc().astype(complex)).solve
-    rng = np.random.default_rng(0)
-    v = rng.standard_normal(sysm.n_dof).astype(complex)
-    v /= np.linalg.norm(v)
-    rq_prev, rq = None, 0.0
-    for _ in range(500):
-        av = sysm.A @ v
-        rq = abs(np.vdot(v, av) / np.vdot(v, sysm.B @ v))
-        if rq_prev is not None and abs(rq - rq_prev) <= 1e-6 * max(rq, 1e-300):
-            break
-        rq_prev = rq
-        w = solve_b(av)
-        v = w / np.linalg.norm(w)
-    return float(rq)
-
-
 _SOLVERS = {"auto": _native.SOLVER_AUTO, "tridiag": _native.SOLVER_TRIDIAG,
             "cocg": _native.SOLVER_COCG}
 
@@ -221,7 +201,8 @@ def rexi_prepare(
     if solver not in _SOLVERS:
         raise ValueError(f"unknown solver {solver!r}")
     if sr_value is None:
-        sr_value = _estimate_sr(sys)
+        from .spectral import spectral_radius_estimate
+        sr_value = spectral_radius_estimate(sys, device=0 if device is None else int(device))
     ratio, admissible = _admissibility(tau, sr_value, approx.domain_radius)
     dev = 0 if device is None else int(device)
 

@@ -32,7 +32,26 @@ def load_golden(name):
 
 
 def golden_names():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+    """REXI golden cases (the cheb_* files hold the 8(f) rows)."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if not os.path.basename(p).startswith("cheb_"))
+
+
+def cheb_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "cheb_*.npz")))
+
+
+def load_cheb(name):
+    """(npz, SystemMatrices) of a spectral-radius / Chebyshev golden case
+    (reference spectral_radius_estimate + chebyshev_run, make_golden.py --cheb)."""
+    from scipy.sparse import csr_matrix
+    from paper_1912_03312_b200.types import SystemMatrices
+    d = np.load(os.path.join(GOLDEN, name + ".npz"))
+
+    def csr(p):
+        return csr_matrix((d[p + "_data"], d[p + "_indices"], d[p + "_indptr"]),
+                          shape=tuple(d[p + "_shape"]))
+    return d, SystemMatrices(csr("A"), csr("B"), int(d["A_shape"][0]))
 
 
 @pytest.fixture(scope="session")

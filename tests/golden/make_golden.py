@@ -107,6 +107,51 @@ def run_ref(name, sysm, approx, tau, u0, n_steps, sr, workers=1, extra=None):
     print(f"golden {name}: n={sysm.n_dof} K={approx.K} steps={n_steps}")
 
 
+def run_ref_cheb(name, sysm, u0, n_steps, degree=26, radius=10.0):
+    """Reference spectral_radius_estimate + chebyshev_prepare/chebyshev_run
+    (spatial.py:314-344, integrate.py:257-377) on one system."""
+    from rexiprop.integrate import chebyshev_coeffs, chebyshev_prepare, chebyshev_run
+    est = spectral_radius_estimate(sysm)
+    tau = 0.9 * radius / (1.05 * float(est))
+    stp = chebyshev_prepare(sysm, tau, degree=degree, radius=radius, sr_value=float(est))
+    seen = []
+    chebyshev_run(stp, sysm, u0, n_steps, observer=lambda k, t, u: seen.append(u.copy()))
+    cc = chebyshev_coeffs(radius, degree)
+    out = {"tau": np.float64(tau), "radius": np.float64(radius), "degree": np.int64(degree),
+           "u0": np.asarray(u0, complex), "steps": np.stack(seen), "coeffs": cc.coeffs,
+           "sup_error": np.float64(cc.sup_error), "sr": np.float64(float(est)),
+           "sr_iterations": np.int64(est.iterations), "sr_converged": np.bool_(est.converged),
+           "admissibility_ratio": np.float64(stp.admissibility_ratio)}
+    out.update(csr_arrays("A", sysm.A))
+    out.update(csr_arrays("B", sysm.B))
+    np.savez_compressed(os.path.join(HERE, f"cheb_{name}.npz"), **out)
+    print(f"golden cheb_{name}: n={sysm.n_dof} sr={float(est):.6e} its={est.iterations} "
+          f"conv={est.converged} steps={n_steps}")
+
+
+def cheb_main():
+    """Golden vectors of the 8(f) rows: spectral radius + Chebyshev stepper."""
+    consts = PhysicalConstants()
+    mesh = build_mesh(-12.0, 12.0, 64)
+    sysm = assemble_system(mesh, PotentialSpec(kind="step", v_max=1.0, c_barr=2.0), consts)
+    u0 = project_initial(mesh, WavePacketParams(r_bar=-4.0, p_bar=2.0, sigma=1.0), consts, sysm.B)
+    run_ref_cheb("fem_p2", sysm, u0, 3)
+    c1 = fixtures.config1()
+    run_ref_cheb("cfg1", c1.system, c1.u0, 3)
+    c3 = fixtures.config3(m=16)
+    run_ref_cheb("p1_2d_m16", c3.system, c3.u0, 2)
+    c5 = fixtures.config5(m=8)
+    run_ref_cheb("p1_3d_m8", c5.system, c5.u0, 2)
+    from scipy.sparse import csr_matrix
+    rng = np.random.default_rng(13)
+    n = 24
+    m0 = rng.standard_normal((n, n))
+    r0 = rng.standard_normal((n, n))
+    sysn = SystemMatrices(A=csr_matrix(0.5 * (m0 + m0.T)), B=csr_matrix(r0 @ r0.T + n * np.eye(n)),
+                          n_dof=n)
+    run_ref_cheb("pencil", sysn, rng.standard_normal(n) + 1j * rng.standard_normal(n), 2)
+
+
 def main():
     sets = write_poles()
     flag = sets[16]
@@ -157,4 +202,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--cheb" in sys.argv:
+        cheb_main()
+    else:
+        main()

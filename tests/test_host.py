@@ -240,3 +240,13 @@ def test_create_rejects_bad_descriptor_without_gpu():
     with pytest.raises(ValueError):
         _native.NativePlan(np.array([0, 1], np.int32), np.array([0], np.int32), np.array([1.0]),
                            np.array([1.0]), np.array([1 + 1j]), np.array([1 + 0j]), tau=-1.0)
+
+
+def test_pencil_create_rejects_bad_descriptor_without_gpu():
+    from paper_1912_03312_b200 import _native
+    with pytest.raises(ValueError, match="column index"):
+        _native.NativePencil(np.array([0, 1], np.int32), np.array([3], np.int32), np.array([1.0]),
+                             np.array([1.0]))
+    with pytest.raises(ValueError, match="nnz"):
+        _native.NativePencil(np.array([0, 2], np.int32), np.array([0], np.int32), np.array([1.0]),
+                             np.array([1.0]))
