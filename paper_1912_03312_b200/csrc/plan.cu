@@ -354,11 +354,14 @@ int tri_mid(rexi_plan *plan, bool dd) {
     TriState &T = plan->tri;
     const size_t nl = T.lv.size();
     cudaStream_t st = plan->stream;
-    const bool tma = T.lv[0].sym && l0v2_supported(plan->kp);
+    // TMA-staged kernel for the levels that fill the GPU; the few-CTA upper
+    // levels are latency-bound and keep the plain kernel
+    const bool tma_ok = T.lv[0].sym && l0v2_supported(plan->kp);
+    auto use_tma = [&](size_t l) { return tma_ok && lv_tma_ctas(T.lv[l].n, plan->kp) >= 148; };
     for (size_t l = 1; l + 1 < nl; ++l) {
         ProfScope ps(plan, "s1_lv");
         const bool d = l == 1 && dd;
-        if (tma) CK(lv_launch_tma(T.lv[l], plan->S, 1, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
+        if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 1, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
                                   d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, nullptr, st));
         else if (d) CK(tri_launch_lv_dd(T.lv[1], plan->S, 1, T.lv[0].ypdd, T.lv[0].lcdd, nullptr, st));
         else CK(tri_launch_s1(T.z, T.lv[l], plan->S, (int)l, nullptr, nullptr, T.lv[l - 1].ypart,
@@ -372,7 +375,7 @@ int tri_mid(rexi_plan *plan, bool dd) {
     for (size_t l = nl - 1; l-- > 1;) {
         ProfScope ps(plan, "s3_lv");
         const bool d = l == 1 && dd;
-        if (tma) CK(lv_launch_tma(T.lv[l], plan->S, 3, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
+        if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 3, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
                                   d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, T.lv[l + 1].X, st));
         else if (d) CK(tri_launch_lv_dd(T.lv[1], plan->S, 3, T.lv[0].ypdd, T.lv[0].lcdd, T.lv[2].X, st));
         else CK(tri_launch_s3(T.z, T.lv[l], plan->S, (int)l, nullptr, nullptr, T.lv[l - 1].ypart,

@@ -31,6 +31,10 @@ cudaError_t tri_launch_top_solve_dd(const LevelDev &L, const ShiftDev &S, const 
                                     const cdd *rdd_b, cudaStream_t st);
 
 // TMA-fed kernel for levels >= 1 of symmetric pencils (tridiag_l0.cu)
+inline int64_t lv_tma_ctas(int64_t n, int kp) {   // grid of lv_launch_tma
+    const int64_t rows = (int64_t)(128 / kp) * TRI_M;
+    return (n + rows - 1) / rows;
+}
 cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,
                           const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st);
 
