@@ -141,6 +141,18 @@ def device_count() -> int:
     return int(c.value) if rc == 0 else 0
 
 
+def host_empty(shape, dtype=np.complex128) -> np.ndarray:
+    """Host output buffer in page-locked memory (torch's caching pinned-host
+    allocator, so repeated steps reuse the block), so the device->host copy
+    of a step result runs at full link speed; plain numpy if torch is absent."""
+    try:
+        import torch
+        tdt = {np.dtype(np.complex128): torch.complex128, np.dtype(np.float64): torch.float64}[np.dtype(dtype)]
+        return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+    except Exception:
+        return np.empty(shape, dtype=dtype)
+
+
 def _ptr(a: np.ndarray):
     return ctypes.c_void_p(a.ctypes.data)
 
@@ -214,7 +226,7 @@ class NativePlan:
 
     def step_host(self, u: np.ndarray, n_steps: int = 1, stats: RexiStats | None = None) -> np.ndarray:
         u = np.ascontiguousarray(u, dtype=np.complex128)
-        out = np.empty_like(u)
+        out = host_empty(u.shape)
         rc = lib().rexi_plan_step(self._h, _ptr(u), _ptr(out), int(n_steps), MEM_HOST,
                                   ctypes.byref(stats) if stats is not None else None)
         raise_status(rc, self._err())
@@ -333,7 +345,7 @@ class NativePencil:
     def cheb_step_host(self, coeffs, scale: float, u: np.ndarray, n_steps: int = 1,
                        stats: RexiStats | None = None) -> np.ndarray:
         u = np.ascontiguousarray(u, dtype=np.complex128)
-        out = np.empty_like(u)
+        out = host_empty(u.shape)
         self.cheb_step(coeffs, scale, u.ctypes.data, out.ctypes.data, n_steps, MEM_HOST, stats)
         return out
 

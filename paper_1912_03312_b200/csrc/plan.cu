@@ -354,10 +354,10 @@ int tri_mid(rexi_plan *plan, bool dd) {
     TriState &T = plan->tri;
     const size_t nl = T.lv.size();
     cudaStream_t st = plan->stream;
-    // TMA-staged kernel for the levels that fill the GPU; the few-CTA upper
-    // levels are latency-bound and keep the plain kernel
+    // TMA-staged kernel at every reduced level of a symmetric pencil (measured
+    // faster than the plain kernel even for the few-CTA upper levels)
     const bool tma_ok = T.lv[0].sym && l0v2_supported(plan->kp);
-    auto use_tma = [&](size_t l) { return tma_ok && lv_tma_ctas(T.lv[l].n, plan->kp) >= 148; };
+    auto use_tma = [&](size_t) { return tma_ok; };
     for (size_t l = 1; l + 1 < nl; ++l) {
         ProfScope ps(plan, "s1_lv");
         const bool d = l == 1 && dd;

@@ -28,7 +28,7 @@ def launches(path):
     for r in rows[start:]:
         if len(r) <= vi: continue
         v = float(r[vi].replace(",", "")); u = r[ui]
-        v = v / 1e6 if u == "nsecond" else (v / 1e3 if u == "usecond" else (v if u == "msecond" else v * 1e3))
+        v = v / 1e6 if u in ("nsecond", "ns") else (v / 1e3 if u in ("usecond", "us") else (v if u in ("msecond", "ms") else v * 1e3))
         a = agg.setdefault(r[ki].split("(")[0], [0, 0.0]); a[0] += 1; a[1] += v
     tot = sum(t for _, t in agg.values())
     for k, (c, t) in agg.items():
