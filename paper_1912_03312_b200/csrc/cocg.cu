@@ -30,11 +30,15 @@
 // double-double.
 #include <cuda_runtime.h>
 
+#include <chrono>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <string>
 #include <vector>
 
 #include "cocg.cuh"
@@ -583,6 +587,16 @@ cudaError_t cocg_axpy_inplace(c128 *x, const c128 *y, int64_t n, cudaStream_t st
 static inline void hook_begin(CocgState &cg, const char *name, double bytes) {
     if (cg.hook) cg.hook->begin(name, bytes);
 }
+// REXI_COCG_TRACE: profile names carry the layout width ("cg_spmv@16")
+static const char *width_name(const char *base, int kp) {
+    static const bool trace = getenv("REXI_COCG_TRACE") != nullptr;
+    if (!trace) return base;
+    static std::map<std::string, std::string> names;
+    std::string key = std::string(base) + "@" + std::to_string(kp);
+    auto it = names.find(key);
+    if (it == names.end()) it = names.emplace(key, key).first;
+    return it->second.c_str();
+}
 static inline void hook_end(CocgState &cg) {
     if (cg.hook) cg.hook->end();
 }
@@ -829,14 +843,26 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     int live = cg.k;
     int it = 0;
     const int check_every = 8;
+    // REXI_COCG_TRACE=1: iterations and host time spent at each layout width
+    static const bool trace = getenv("REXI_COCG_TRACE") != nullptr;
+    auto tr_t0 = std::chrono::steady_clock::now();
+    int tr_it0 = 0;
+    auto trace_phase = [&](int width, int live_now) {
+        if (!trace) return;
+        const auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[cocg] width %3d  iters %5d..%5d  live at end %3d  %.3f ms\n", width, tr_it0, it,
+                live_now, std::chrono::duration<double, std::milli>(t1 - tr_t0).count());
+        tr_t0 = t1;
+        tr_it0 = it;
+    };
     for (;;) {
         for (int s = 0; s < check_every; ++s) {
-            hook_begin(cg, "cg_spmv", 80.0 * n * live + nnzb);
+            hook_begin(cg, width_name("cg_spmv", kp), 80.0 * n * live + nnzb);
             if (im->cplx) k_cg_spmv<true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
             else k_cg_spmv<false><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
             k_cg_finish<1><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
-            hook_begin(cg, "cg_update", 112.0 * n * live + 24.0 * n);
+            hook_begin(cg, width_name("cg_update", kp), 112.0 * n * live + 24.0 * n);
             k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
             k_cg_finish<2><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
@@ -850,11 +876,15 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
         CGK(cudaStreamSynchronize(st));
         const int na = *h_na;
         live = na;
-        if (na == 0 || it > cg.max_iters + check_every) break;
+        if (na == 0 || it > cg.max_iters + check_every) {
+            trace_phase(kp, na);
+            break;
+        }
         // compaction: halve the layout while the live lanes fit
         int kp_new = kp;
         while (kp_new > 1 && na <= kp_new / 2) kp_new /= 2;
         if (kp_new < kp) {
+            trace_phase(kp, na);
             // live lanes keep ascending shift order; frozen valid lanes hand their
             // x to the full-width solution; padding lanes (a copy of lane map[0],
             // inactive, invalid) fill the new width
