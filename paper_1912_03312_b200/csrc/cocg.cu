@@ -214,8 +214,15 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
 // are double-buffered: one barrier per claim.  Element offsets fit in 32 bits
 // (n * kp < 2^31 is checked at plan creation).
 // ---------------------------------------------------------------------------
+#ifndef CG_SPMV_UNROLL
+#define CG_SPMV_UNROLL 4
+#endif
+#ifndef CG_SPMV_MINB
+#define CG_SPMV_MINB 1
+#endif
+constexpr int kSpmvUnroll = CG_SPMV_UNROLL;
 template <bool CPLX>
-__global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
+__global__ void __launch_bounds__(CG_NT, CG_SPMV_MINB) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
     __shared__ double2 sbp[2][CG_SBP];
     __shared__ int64_t claim_q[2];
     if (*Sc.nactive == 0) return;
@@ -245,7 +252,7 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, 
                 for (int64_t i = r0; i < r1; i += CG_CH) {
                     c128 acc = cmk(0.0, 0.0);
                     const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
-#pragma unroll 4
+#pragma unroll kSpmvUnroll
                     for (int32_t q = q0; q < q1; ++q) {
                         const uint32_t c = (uint32_t)__ldg(M.indices + q);
                         const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
@@ -262,6 +269,160 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, 
             sbp[buf][sbl * kp + lane] = mu;
         }
         __syncthreads();   // sub-block partials complete, claim_q[buf^1] visible
+        chunk_partials<double2>(sbp[buf], g, claim, Sc.part_a, add_c, make_double2(0.0, 0.0));
+        buf ^= 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// spmv with the claim's CSR slice staged in shared memory (wide layouts).
+// Thread 0 bulk-copies (cp.async.bulk, one mbarrier per buffer) the indptr,
+// indices and value slices of the NEXT claim while the CTA computes the
+// current one, so the per-entry index/value reads are shared-memory
+// broadcasts and only the z gathers go to L2/HBM.  Same rows, same order of
+// operations as k_cg_spmv -> bitwise identical results.
+// ---------------------------------------------------------------------------
+constexpr int CG_ST_ROWS = 2 * CG_SB * CG_CH + 8;   // indptr slots per buffer (claims of <= 2 chunks)
+constexpr int CG_ST_NNZ = 512;                      // entries per buffer
+#ifndef CG_STB
+#define CG_STB 8                                    // z gathers in flight per thread
+#endif
+
+struct StLayout {
+    uint64_t *bar;      // [2]
+    int *meta;          // [2][4]: indptr base, index base, value base
+    int *ip, *ix;       // [2][CG_ST_ROWS], [2][CG_ST_NNZ + 8]
+    double *ta, *tb, *ti;   // [2][CG_ST_NNZ + 8] each (ti only for complex A)
+};
+
+__host__ __device__ inline size_t st_smem_bytes(bool cplx) {
+    return 128 + 2 * CG_ST_ROWS * 4 + 2 * (CG_ST_NNZ + 8) * 4 + (cplx ? 3 : 2) * 2 * (CG_ST_NNZ + 8) * 8;
+}
+
+__device__ __forceinline__ StLayout st_carve(unsigned char *smem, bool cplx) {
+    StLayout L;
+    L.bar = reinterpret_cast<uint64_t *>(smem);
+    L.meta = reinterpret_cast<int *>(smem + 16);
+    unsigned char *p = smem + 128;
+    L.ip = reinterpret_cast<int *>(p);
+    p += 2 * CG_ST_ROWS * 4;
+    L.ix = reinterpret_cast<int *>(p);
+    p += 2 * (CG_ST_NNZ + 8) * 4;
+    L.ta = reinterpret_cast<double *>(p);
+    p += 2 * (CG_ST_NNZ + 8) * 8;
+    L.tb = reinterpret_cast<double *>(p);
+    p += 2 * (CG_ST_NNZ + 8) * 8;
+    L.ti = cplx ? reinterpret_cast<double *>(p) : nullptr;
+    return L;
+}
+
+// thread 0: stage claim `claim` into buffer `b` (arrays padded by >= 32 B)
+template <bool CPLX>
+__device__ __forceinline__ void st_issue(const StLayout &L, int b, int64_t claim, const CgMat &M, const CgGeom &g) {
+    const int64_t rows = (int64_t)g.cpc * CG_SB * CG_CH;
+    const int64_t R0 = claim * rows, R1 = min(R0 + rows, M.n);
+    const int64_t ipb = R0 & ~3ll, ipe = (R1 + 1 + 3) & ~3ll;
+    const int32_t Q0 = __ldg(M.indptr + R0), Q1 = __ldg(M.indptr + R1);
+    const int64_t xb = Q0 & ~3, xe = (Q1 + 3) & ~3;
+    const int64_t vb = Q0 & ~1, ve = (Q1 + 1) & ~1;
+    L.meta[b * 4 + 0] = (int)ipb;
+    L.meta[b * 4 + 1] = (int)xb;
+    L.meta[b * 4 + 2] = (int)vb;
+    const uint32_t bip = (uint32_t)((ipe - ipb) * 4), bix = (uint32_t)((xe - xb) * 4), bv = (uint32_t)((ve - vb) * 8);
+    mbar_expect_tx(L.bar + b, bip + bix + bv * (CPLX ? 3 : 2));
+    bulk_g2s(L.ip + b * CG_ST_ROWS, M.indptr + ipb, bip, L.bar + b);
+    if (bix) bulk_g2s(L.ix + b * (CG_ST_NNZ + 8), M.indices + xb, bix, L.bar + b);
+    if (bv) {
+        bulk_g2s(L.ta + b * (CG_ST_NNZ + 8), M.ta + vb, bv, L.bar + b);
+        bulk_g2s(L.tb + b * (CG_ST_NNZ + 8), M.b + vb, bv, L.bar + b);
+        if (CPLX) bulk_g2s(L.ti + b * (CG_ST_NNZ + 8), M.ta_im + vb, bv, L.bar + b);
+    }
+}
+
+template <bool CPLX>
+__global__ void __launch_bounds__(CG_NT) k_cg_spmv_st(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
+    __shared__ double2 sbp[2][CG_SBP];
+    __shared__ int64_t claim_q[2];
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (*Sc.nactive == 0) return;
+    const StLayout L = st_carve(smem, CPLX);
+    int lane, slot, slots;
+    cta_geom(g, lane, slot, slots);
+    const uint32_t kp = (uint32_t)g.kp;
+    const bool act = Sc.active[lane] != 0;
+    const c128 sg = S.sigma[g.lane_shift[lane]];
+    const c128 beta = Sc.beta[lane];
+    c128 *__restrict__ pv = V.p;
+    c128 *__restrict__ qv = V.q;
+    const c128 *__restrict__ zv = V.z;
+    if (threadIdx.x == 0) {
+        mbar_init(L.bar, 1);
+        mbar_init(L.bar + 1, 1);
+        fence_mbar_init();
+        const int64_t c0 = (int64_t)atomicAdd(Sc.ctr, 1u);
+        claim_q[0] = c0;
+        if (c0 < g.nclaims) st_issue<CPLX>(L, 0, c0, M, g);
+    }
+    __syncthreads();
+    int buf = 0;
+    uint32_t ph0 = 0, ph1 = 0;
+    for (;;) {
+        const int64_t claim = claim_q[buf];
+        if (claim >= g.nclaims) break;
+        if (threadIdx.x == 0) {
+            const int64_t cn = (int64_t)atomicAdd(Sc.ctr, 1u);
+            claim_q[buf ^ 1] = cn;
+            if (cn < g.nclaims) st_issue<CPLX>(L, buf ^ 1, cn, M, g);
+        }
+        mbar_wait(L.bar + buf, buf ? ph1 : ph0);
+        if (buf) ph1 ^= 1u; else ph0 ^= 1u;
+        const int *ip = L.ip + buf * CG_ST_ROWS;
+        const int *ix = L.ix + buf * (CG_ST_NNZ + 8);
+        const double *sta = L.ta + buf * (CG_ST_NNZ + 8);
+        const double *stb = L.tb + buf * (CG_ST_NNZ + 8);
+        const double *sti = CPLX ? L.ti + buf * (CG_ST_NNZ + 8) : nullptr;
+        const int ipb = L.meta[buf * 4 + 0], xb = L.meta[buf * 4 + 1], vb = L.meta[buf * 4 + 2];
+        for (int ps = 0; ps < g.P; ++ps) {
+            const int sbl = ps * slots + slot;
+            const int64_t gsb = claim * g.subs + sbl;   // sub-block b of chunk c: rows c*32 + b + 8k
+            const int64_t r0 = (gsb / CG_CH) * (CG_SB * CG_CH) + gsb % CG_CH;
+            c128 mu = cmk(0.0, 0.0);
+            if (act) {
+                const int64_t r1 = min(r0 + CG_SB * CG_CH, M.n);
+                for (int64_t i = r0; i < r1; i += CG_CH) {
+                    c128 acc = cmk(0.0, 0.0);
+                    const int li = (int)(i - ipb);
+                    const int32_t q0 = ip[li], q1 = ip[li + 1];
+                    // batches of CG_STB entries: all gathers of a batch in flight
+                    // before the (ascending-q) accumulation
+                    for (int32_t qb = q0; qb < q1; qb += CG_STB) {
+                        c128 zz[CG_STB];
+                        uint32_t cc[CG_STB];
+#pragma unroll
+                        for (int k = 0; k < CG_STB; ++k) cc[k] = qb + k < q1 ? (uint32_t)ix[qb + k - xb] : 0u;
+#pragma unroll
+                        for (int k = 0; k < CG_STB; ++k)
+                            zz[k] = qb + k < q1 ? zv[cc[k] * kp + lane] : cmk(0.0, 0.0);
+#pragma unroll
+                        for (int k = 0; k < CG_STB; ++k) {
+                            if (qb + k < q1) {
+                                const int qv = qb + k;
+                                const c128 e = form_entry(sta[qv - vb], CPLX ? sti[qv - vb] : 0.0, stb[qv - vb], sg);
+                                acc = cadd(acc, cmul(e, zz[k]));
+                            }
+                        }
+                    }
+                    const uint32_t o = (uint32_t)i * kp + lane;
+                    const c128 pi = cadd(zv[o], cmul(beta, pv[o]));
+                    const c128 qi = cadd(acc, cmul(beta, qv[o]));
+                    pv[o] = pi;
+                    qv[o] = qi;
+                    mu = cadd(mu, cmul(pi, qi));
+                }
+            }
+            sbp[buf][sbl * kp + lane] = mu;
+        }
+        __syncthreads();   // sub-block partials complete, claim_q[buf^1] visible, buffer buf free
         chunk_partials<double2>(sbp[buf], g, claim, Sc.part_a, add_c, make_double2(0.0, 0.0));
         buf ^= 1;
     }
@@ -618,6 +779,7 @@ struct CocgImpl {
     int *map = nullptr;        // device [kp_full]
     int *mask = nullptr;       // device [kp_full]
     int *h_buf = nullptr;      // pinned [2 + 2*kp_full]
+    bool stage_ok[3] = {false, false, false};   // [cpc]: every claim's CSR slice fits the staging buffers
 };
 
 static int alloc_(CocgState &cg, void **p, size_t bytes, std::string &err) {
@@ -714,11 +876,27 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
         }
     int32_t *ip, *ix;
     double *dta_, *dtai_, *db_, *ta_, *tai_, *bb_;
-    CGA(ip, sizeof(int32_t) * (n + 1));
-    CGA(ix, sizeof(int32_t) * nnz);
-    CGA(ta_, sizeof(double) * nnz);
-    CGA(tai_, sizeof(double) * nnz);
-    CGA(bb_, sizeof(double) * nnz);
+    // +32 B of zeroed padding: the staged spmv bulk-copies 16-B aligned supersets
+    CGA(ip, sizeof(int32_t) * (n + 1) + 32);
+    CGA(ix, sizeof(int32_t) * nnz + 32);
+    CGA(ta_, sizeof(double) * nnz + 32);
+    CGA(tai_, sizeof(double) * nnz + 32);
+    CGA(bb_, sizeof(double) * nnz + 32);
+    CGK(cudaMemsetAsync(ip, 0, sizeof(int32_t) * (n + 1) + 32, st));
+    CGK(cudaMemsetAsync(ix, 0, sizeof(int32_t) * nnz + 32, st));
+    CGK(cudaMemsetAsync(ta_, 0, sizeof(double) * nnz + 32, st));
+    CGK(cudaMemsetAsync(tai_, 0, sizeof(double) * nnz + 32, st));
+    CGK(cudaMemsetAsync(bb_, 0, sizeof(double) * nnz + 32, st));
+    for (int cpc = 1; cpc <= 2; ++cpc) {
+        const int64_t rows = (int64_t)cpc * CG_SB * CG_CH;
+        bool ok = !getenv("REXI_COCG_NOSTAGE");
+        for (int64_t r0 = 0; ok && r0 < n; r0 += rows) {
+            const int64_t r1 = std::min<int64_t>(r0 + rows, n);
+            const int64_t q0 = d->indptr[r0], q1 = d->indptr[r1];
+            if (((q1 + 3) & ~3ll) - (q0 & ~3ll) > CG_ST_NNZ) ok = false;
+        }
+        im->stage_ok[cpc] = ok;
+    }
     CGA(dta_, sizeof(double) * n);
     CGA(dtai_, sizeof(double) * n);
     CGA(db_, sizeof(double) * n);
@@ -858,8 +1036,23 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     for (;;) {
         for (int s = 0; s < check_every; ++s) {
             hook_begin(cg, width_name("cg_spmv", kp), 80.0 * n * live + nnzb);
-            if (im->cplx) k_cg_spmv<true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
-            else k_cg_spmv<false><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+            if (g.cpc <= 2 && im->stage_ok[g.cpc]) {
+                const size_t sm = st_smem_bytes(im->cplx);
+                static bool attr_set = false;
+                if (!attr_set) {
+                    CGK(cudaFuncSetAttribute(k_cg_spmv_st<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)st_smem_bytes(true)));
+                    CGK(cudaFuncSetAttribute(k_cg_spmv_st<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)st_smem_bytes(false)));
+                    attr_set = true;
+                }
+                if (im->cplx) k_cg_spmv_st<true><<<grid, CG_NT, sm, st>>>(im->M, im->V, im->Sc, S, g);
+                else k_cg_spmv_st<false><<<grid, CG_NT, sm, st>>>(im->M, im->V, im->Sc, S, g);
+            } else if (im->cplx) {
+                k_cg_spmv<true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+            } else {
+                k_cg_spmv<false><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+            }
             k_cg_finish<1><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             hook_begin(cg, width_name("cg_update", kp), 112.0 * n * live + 24.0 * n);
