@@ -121,6 +121,8 @@ typedef struct rexi_info {
     int64_t device_bytes;      /* HBM held by the plan                            */
     double prepare_ms;         /* device time of rexi_plan_create                 */
     double min_pivot_ratio;    /* TRIDIAG: min over shifts of min|d|/max|d|       */
+    int32_t persistent;        /* >0: small 1D plan, all steps of a call run in ONE
+                                  launch of a thread-block cluster of this many CTAs */
 } rexi_info;
 
 int rexi_plan_create(const rexi_desc *desc, rexi_plan **out);

@@ -88,6 +88,7 @@ class RexiInfo(ctypes.Structure):
         ("device_bytes", ctypes.c_int64),
         ("prepare_ms", ctypes.c_double),
         ("min_pivot_ratio", ctypes.c_double),
+        ("persistent", ctypes.c_int32),
     ]
 
 

@@ -65,6 +65,8 @@ struct rexi_plan {
     std::vector<cudaEvent_t> pool;
     std::map<std::string, Acc> prof_acc;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};   // 1D step replay (ubuf[g] -> ubuf[g^1])
+    int persist_cs = 0;                               // >0: small 1D plan, all steps in one cluster launch
+    c128 *pbuf[2] = {nullptr, nullptr};               // its state ping-pong
     int64_t graph_kernels = 0;
     struct Hook : rexi::ProfHook {
         rexi_plan *p = nullptr;
@@ -414,6 +416,26 @@ int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
     return REXI_OK;
 }
 
+// small unrefined 1D plans run every step of a call in ONE cluster launch
+// (tridiag_persist.cu); REXI_PERSIST=0 disables it
+int persist_setup(rexi_plan *plan) {
+    TriState &T = plan->tri;
+    const size_t nl = T.lv.size();
+    if (const char *e = getenv("REXI_PERSIST"))
+        if (atoi(e) == 0) return REXI_OK;
+    if (plan->refine > 0 || nl < 2 || nl > (size_t)PS_MAXLV || plan->kp > 128 ||
+        !l0v2_supported(plan->kp) || T.lv[nl - 2].P != 1)
+        return REXI_OK;
+    // the level-0 slices must fit in the shared memory of one cluster
+    const int cs = persist_cluster_size(T.lv.data(), (int)nl, plan->kp);
+    if (cs <= 0) return REXI_OK;
+    int rc = dalloc(plan, &plan->pbuf[0], (size_t)plan->n);
+    if (!rc) rc = dalloc(plan, &plan->pbuf[1], (size_t)plan->n);
+    if (rc) return rc;
+    plan->persist_cs = cs;
+    return REXI_OK;
+}
+
 // one step from device u -> (uout rounded) or (T.acc partial when uout == nullptr)
 int tri_step(rexi_plan *plan, const c128 *u, c128 *uout) {
     TriState &T = plan->tri;
@@ -570,6 +592,7 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
         if (!rc) {
             if (solver == REXI_SOLVER_TRIDIAG) {
                 rc = tri_create(plan, d);
+                if (!rc) rc = persist_setup(plan);
             } else {
                 rc = dalloc(plan, &plan->tri.acc, (size_t)4 * d->n);
                 if (!rc) rc = cocg_create(plan->cg, d, plan->S, plan->refine, plan->stream, plan->err);
@@ -639,6 +662,7 @@ int rexi_plan_info(const rexi_plan *plan, rexi_info *info) {
     info->device_bytes = plan->bytes + plan->cg.bytes;
     info->prepare_ms = plan->prepare_ms;
     info->min_pivot_ratio = plan->min_pivot_ratio;
+    info->persistent = plan->persist_cs;
     return REXI_OK;
 }
 
@@ -664,7 +688,14 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     }
     if (stats) CK(cudaEventRecord(ev[0], st));
     int cur = (src == plan->ubuf[0]) ? 0 : 1;
-    if (n_steps > 0 && plan->solver == REXI_SOLVER_TRIDIAG && !plan->prof) {
+    if (n_steps > 0 && plan->persist_cs > 0 && !plan->prof) {
+        TriState &T = plan->tri;
+        CK(persist_launch(T.z, T.lv.data(), (int)T.lv.size(), plan->S, n, src, plan->pbuf[0], plan->pbuf[1],
+                          nullptr, n_steps, plan->persist_cs, st));
+        plan->launches += 1;
+        src = plan->pbuf[(n_steps - 1) & 1];
+        n_steps = -n_steps;    // steps done; restored below
+    } else if (n_steps > 0 && plan->solver == REXI_SOLVER_TRIDIAG && !plan->prof) {
         // the 1D step is a fixed kernel sequence: replay it as a CUDA graph
         // (two graphs, ping-ponging between the plan's state buffers)
         if (src != plan->ubuf[0] && src != plan->ubuf[1]) {

@@ -31,6 +31,13 @@ cudaError_t tri_launch_top_solve_dd(const LevelDev &L, const ShiftDev &S, const 
                                     const cdd *rdd_b, cudaStream_t st);
 
 // TMA-fed kernel for levels >= 1 of symmetric pencils (tridiag_l0.cu)
+// one-launch multi-step loop for small 1D plans (tridiag_persist.cu)
+constexpr int PS_MAXLV = 8;
+int persist_cluster_size(const LevelDev *lv, int nl, int kp);
+cudaError_t persist_launch(const L0Dev &z, const LevelDev *lv, int nl, const ShiftDev &S, int64_t n,
+                           const c128 *u_in, c128 *ua, c128 *ub, c128 *snaps, int n_steps, int csize,
+                           cudaStream_t st);
+
 inline int64_t lv_tma_ctas(int64_t n, int kp) {   // grid of lv_launch_tma
     const int64_t rows = (int64_t)(128 / kp) * TRI_M;
     return (n + rows - 1) / rows;
