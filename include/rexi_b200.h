@@ -14,6 +14,7 @@
  *                         (shifted-operator formation integrate.py:171,
  *                          factorize + zgbtrf   solvers.py:42-69,108-115)
  *   rexi_plan_step     <- rexi_step / rexi_run  integrate.py:193-245
+ *   rexi_plan_run      <- rexi_run with an observer (every state kept)
  *                         (rhs integrate.py:203-206, K solves :208-222 via
  *                          zgbtrs solvers.py:76-80, Kahan reduce :59-68,224)
  *   rexi_plan_step_partial + rexi_combine_partials
@@ -131,6 +132,14 @@ int rexi_plan_create(const rexi_desc *desc, rexi_plan **out);
  * host (pinned or pageable) or device pointers.  u_in == u_out is allowed. */
 int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out,
                    int32_t n_steps, int32_t mem, rexi_stats *stats);
+
+/* n_steps steps from u_in, writing the state after EVERY step into snaps
+ * (n_steps * n complex, step-major): the on-device snapshots behind
+ * rexi_run's observer (integrate.py:229-245, harness.py:220-225,330-336).
+ * Small 1D plans run all steps in one launch; others chain device steps
+ * without a host round trip.  mem applies to u_in and snaps. */
+int rexi_plan_run(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *snaps, int32_t n_steps, int32_t mem,
+                  rexi_stats *stats);
 
 /* One step for this plan's shard of shifts, leaving the double-double
  * partial sum sum_{j in shard} beta_j x_j in partial (device, 4*n doubles:

@@ -33,7 +33,7 @@ EXPORTED = (
     "rexi_plan_create", "rexi_plan_step", "rexi_plan_step_partial", "rexi_combine_partials",
     "rexi_plan_solve", "rexi_plan_info", "rexi_plan_destroy", "rexi_plan_last_error",
     "rexi_last_error", "rexi_device_count", "rexi_abi_version", "rexi_plan_profile",
-    "rexi_plan_profile_report", "rexi_pencil_create", "rexi_pencil_solve_b",
+    "rexi_plan_profile_report", "rexi_plan_run", "rexi_pencil_create", "rexi_pencil_solve_b",
     "rexi_pencil_spectral_radius", "rexi_pencil_cheb_step", "rexi_pencil_last_error",
     "rexi_pencil_destroy",
 )
@@ -109,6 +109,7 @@ def lib():
     L.rexi_plan_create.argtypes = [ctypes.POINTER(RexiDesc), ctypes.POINTER(vp)]
     L.rexi_plan_step.argtypes = [vp, vp, vp, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(RexiStats)]
     L.rexi_plan_step_partial.argtypes = [vp, vp, vp, ctypes.POINTER(RexiStats)]
+    L.rexi_plan_run.argtypes = [vp, vp, vp, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(RexiStats)]
     L.rexi_combine_partials.argtypes = [vp, ctypes.c_int32, ctypes.c_int64, vp, vp]
     L.rexi_plan_solve.argtypes = [vp, vp, vp, ctypes.c_int32]
     L.rexi_plan_info.argtypes = [vp, ctypes.POINTER(RexiInfo)]
@@ -239,6 +240,15 @@ class NativePlan:
                                   int(n_steps), MEM_DEVICE,
                                   ctypes.byref(stats) if stats is not None else None)
         raise_status(rc, self._err())
+
+    def run_host(self, u: np.ndarray, n_steps: int, stats: RexiStats | None = None) -> np.ndarray:
+        """States after each of n_steps steps, shape (n_steps, n) (fresh pinned buffer)."""
+        u = np.ascontiguousarray(u, dtype=np.complex128)
+        out = host_empty((int(n_steps), self.n))
+        rc = lib().rexi_plan_run(self._h, _ptr(u), _ptr(out), int(n_steps), MEM_HOST,
+                                 ctypes.byref(stats) if stats is not None else None)
+        raise_status(rc, self._err())
+        return out
 
     def step_partial(self, u_ptr: int, partial_ptr: int, stats: RexiStats | None = None):
         rc = lib().rexi_plan_step_partial(self._h, ctypes.c_void_p(u_ptr), ctypes.c_void_p(partial_ptr),

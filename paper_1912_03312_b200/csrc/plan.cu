@@ -772,6 +772,67 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     return REXI_OK;
 }
 
+int rexi_plan_run(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *snaps, int32_t n_steps, int32_t mem,
+                  rexi_stats *stats) {
+    if (!plan) return set_err(nullptr, REXI_ERR_INVALID, "null plan");
+    if (!u_in || !snaps) return set_err(plan, REXI_ERR_INVALID, "null argument");
+    if (n_steps < 0) return set_err(plan, REXI_ERR_INVALID, "n_steps must be >= 0");
+    if (n_steps == 0) return REXI_OK;
+    CK(cudaSetDevice(plan->device));
+    const int64_t n = plan->n;
+    cudaStream_t st = plan->stream;
+    plan->launches = 0;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    CK(cudaEventCreate(&ev[0]));
+    CK(cudaEventCreate(&ev[1]));
+    c128 *dsnap = (c128 *)snaps, *tmp = nullptr;
+    if (mem == REXI_MEM_HOST) {
+        CK(cudaMallocAsync((void **)&tmp, sizeof(c128) * n * (size_t)n_steps, st));
+        dsnap = tmp;
+    }
+    const c128 *src = (const c128 *)u_in;
+    if (mem == REXI_MEM_HOST) {
+        CK(cudaMemcpyAsync(plan->ubuf[0], u_in, sizeof(c128) * n, cudaMemcpyHostToDevice, st));
+        src = plan->ubuf[0];
+    }
+    CK(cudaEventRecord(ev[0], st));
+    int rc = REXI_OK;
+    if (plan->persist_cs > 0 && !plan->prof) {
+        TriState &T = plan->tri;
+        CK(persist_launch(T.z, T.lv.data(), (int)T.lv.size(), plan->S, n, src, plan->pbuf[0], plan->pbuf[1], dsnap,
+                          n_steps, plan->persist_cs, st));
+        plan->launches += 1;
+    } else {
+        for (int s = 0; s < n_steps && !rc; ++s)
+            rc = plan_step_device(plan, s == 0 ? src : dsnap + (size_t)(s - 1) * n, dsnap + (size_t)s * n);
+    }
+    CK(cudaEventRecord(ev[1], st));
+    if (!rc && mem == REXI_MEM_HOST)
+        CK(cudaMemcpyAsync(snaps, dsnap, sizeof(c128) * n * (size_t)n_steps, cudaMemcpyDeviceToHost, st));
+    if (tmp) cudaFreeAsync(tmp, st);
+    CK(cudaStreamSynchronize(st));
+    prof_flush(plan);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[0], ev[1]);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    if (rc) {
+        if (rc == REXI_ERR_NOCONV || rc == REXI_ERR_BREAKDOWN) return set_err(plan, rc, plan->err);
+        return rc;
+    }
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->t_local_ms = ms;
+        stats->steps = n_steps;
+        stats->launches = plan->launches;
+        stats->iters_max = plan->cg.last_iters_max;
+        stats->iters_mean = plan->cg.last_iters_mean;
+        stats->refine_rounds = plan->refine;
+        stats->bad_shift = -1;
+    }
+    return REXI_OK;
+}
+
 int rexi_plan_step_partial(rexi_plan *plan, const rexi_c128 *u_in, double *partial,
                            rexi_stats *stats) {
     if (!plan) return set_err(nullptr, REXI_ERR_INVALID, "null plan");

@@ -41,6 +41,8 @@ SAFETY_FACTOR = 1.05
 # tau * sr(M) above which 1D solves get one round of double-double residual
 # refinement by default.
 AUTO_REFINE_STIFFNESS = 5e3
+# rexi_run with an observer keeps at most this many bytes of states per chunk
+RUN_CHUNK_BYTES = 256 << 20
 
 Observer = Callable[[int, float, np.ndarray], None]
 
@@ -336,6 +338,23 @@ def rexi_run(stepper: RexiStepper, u0, n_steps: int, observer: Observer | None =
         return u
     if observer is None:
         return _run_native(stepper, u, n_steps)
+    if len(stepper.plans) == 1 and not _is_torch(u):
+        # every state is produced on the device (rexi_plan_run: one launch for
+        # small 1D plans), copied back in chunks, and handed to the observer
+        # in order; each state is its own array, as in the reference loop
+        n = stepper.plans[0].n
+        chunk = max(1, min(n_steps, RUN_CHUNK_BYTES // (16 * max(n, 1))))
+        k = 0
+        while k < n_steps:
+            c = min(chunk, n_steps - k)
+            t0 = time.perf_counter()
+            states = stepper.plans[0].run_host(u, c)
+            stepper.timers["local"] += time.perf_counter() - t0
+            for s in range(c):
+                k += 1
+                observer(k, k * stepper.tau, states[s])
+            u = states[c - 1]
+        return u
     for k in range(1, n_steps + 1):
         u = rexi_step(stepper, u)
         observer(k, k * stepper.tau, u)

@@ -71,3 +71,25 @@ def test_persistent_in_place_device_call():
     p.step_device(ut.data_ptr(), ut.data_ptr(), 3)
     assert np.array_equal(ut.cpu().numpy(), ref)
     stp.close()
+
+
+@pytest.mark.parametrize("name,refine", [("cfg1_k32", 0), ("cfg1_k32", 1), ("p1_2d_m16", None), ("fem_p2", None)])
+def test_observer_states_equal_step_loop(name, refine):
+    """rexi_run(observer) produces every state on the device (rexi_plan_run);
+    the observer sees exactly the states of a rexi_step loop, each its own array."""
+    from paper_1912_03312_b200 import rexi_prepare, rexi_run, rexi_step
+    d, sysm, ap = load_golden(name)
+    stp = rexi_prepare(sysm, ap, float(d["tau"]), sr_value=float(d["sr"]), override_admissibility=True,
+                       refine=refine)
+    nst = 5
+    seen = []
+    final = rexi_run(stp, d["u0"], nst, observer=lambda k, t, u: seen.append((k, t, u)))
+    assert [k for k, _, _ in seen] == list(range(1, nst + 1))
+    assert all(abs(t - k * float(d["tau"])) < 1e-15 for k, t, _ in seen)
+    u = d["u0"]
+    for k in range(nst):
+        u = rexi_step(stp, u)
+        assert np.array_equal(seen[k][2], u), k
+    assert np.array_equal(final, u)
+    assert len({id(s[2]) for s in seen}) == nst
+    stp.close()
