@@ -269,7 +269,10 @@ __device__ __forceinline__ void s1_body(const L0Args &a, const L0Layout &l, cons
 }
 
 template <int M>
-__global__ void __launch_bounds__(L0_NT, 3) k_l0_s1(L0Args a) {
+#ifndef S1_MINB
+#define S1_MINB 3
+#endif
+__global__ void __launch_bounds__(L0_NT, S1_MINB) k_l0_s1(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const L0Layout l = carve(smem, a.S.kp, M, ST_RHS);
     const Ctx c = make_ctx(a, M);
@@ -297,7 +300,10 @@ __device__ __forceinline__ void s3_body(const L0Args &a, const L0Layout &l, cons
 }
 
 template <int M>
-__global__ void __launch_bounds__(L0_NT, 4) k_l0_s3acc(L0Args a) {
+#ifndef S3_MINB
+#define S3_MINB 4
+#endif
+__global__ void __launch_bounds__(L0_NT, S3_MINB) k_l0_s3acc(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const L0Layout l = carve(smem, a.S.kp, M, ST_RHS);
     const Ctx c = make_ctx(a, M);
@@ -426,44 +432,45 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
 }
 
 // ---------------------------------------------------------------------------
-// K3 (refine): correction solve from the stored residual, acc += sum(beta dx)
+// K3 (refine): correction solve from the stored residual, acc += sum(beta dx).
+// Only the inverse pivots are staged (one 32-KB tile); the residual rows go
+// straight into the sweep registers (loads issued before the mbarrier wait,
+// so they overlap the bulk copy) and dx overwrites the consumed pivots for
+// the lane sum -- half the shared memory of a two-tile CTA, so more CTAs
+// (sweep chains) per SM.
 // ---------------------------------------------------------------------------
-template <int M, bool FULL>
-__device__ __forceinline__ void k3_body(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
-                                        c128 xn) {
-    const c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
-    c128 *tr = l.t1 + (size_t)c.lr0 * c.kp + c.j;
-    const RowView &rv = l.rv;
+#ifndef K3_MINB
+#define K3_MINB 5
+#endif
+template <int M>
+__global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const L0Layout l = carve(smem, a.S.kp, M, 0);
+    const Ctx c = make_ctx(a, M);
+    l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, 0);
     const int kp = c.kp;
     c128 y[M];
-    y[0] = xs;
-    sweep_fwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, [&](int q) { return tr[q * kp]; });
-    sweep_bwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, xn, [&](int q, c128 x) { tr[q * kp] = x; });
-    tr[0] = xs;
-}
-
-template <int M>
-__global__ void __launch_bounds__(L0_NT, 4) k_l0_k3(L0Args a) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int flags = ST_TILE2;
-    const L0Layout l = carve(smem, a.S.kp, M, flags);
-    const Ctx c = make_ctx(a, M);
-    l0_stage(smem, l, a, a.L.invd, a.rres_in, c.row0, flags);
     c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
     if (c.active) {
-        xs = a.X1[c.p * c.kp + c.j];
-        if (c.p + 1 < c.P) xn = a.X1[(c.p + 1) * c.kp + c.j];
+        xs = a.X1[c.p * kp + c.j];
+        if (c.p + 1 < c.P) xn = a.X1[(c.p + 1) * kp + c.j];
+#pragma unroll
+        for (int q = 1; q < M; ++q) y[q] = a.rres_in[(c.base + q) * kp + c.j];
     }
     mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
+    c128 *ti = l.t0 + (size_t)c.lr0 * kp + c.j;
     if (c.active) {
-        k3_body<M, true>(a, l, c, xs, xn);
+        const RowView &rv = l.rv;
+        y[0] = xs;
+        sweep_fwd<M, true>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, [&](int q) { return y[q]; });
+        sweep_bwd<M, true>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, xn, [&](int q, c128 x) { ti[q * kp] = x; });
+        ti[0] = xs;
     } else {
-        c128 *tr = l.t1 + (size_t)c.lr0 * c.kp + c.j;
 #pragma unroll
-        for (int q = 0; q < M; ++q) tr[q * c.kp] = cmk(0.0, 0.0);
+        for (int q = 0; q < M; ++q) ti[q * kp] = cmk(0.0, 0.0);
     }
     __syncthreads();
-    reduce_rows<M>(l.t1, a, c.row0);
+    reduce_rows<M>(l.t0, a, c.row0);
 }
 
 // ---------------------------------------------------------------------------
@@ -657,7 +664,7 @@ cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
     a.nout = nout;
     a.z = z; a.L = L; a.S = S; a.X1 = X1; a.rres_in = rres; a.acc = acc; a.uout = uout;
     a.acc_add = 1; a.final_out = uout != nullptr;
-    return launch_l0(k_l0_k3<TRI_M>, a, ST_TILE2, st);
+    return launch_l0(k_l0_k3<TRI_M>, a, 0, st);
 }
 
 }  // namespace rexi
