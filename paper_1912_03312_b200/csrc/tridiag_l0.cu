@@ -270,7 +270,7 @@ __device__ __forceinline__ void s1_body(const L0Args &a, const L0Layout &l, cons
 
 template <int M>
 #ifndef S1_MINB
-#define S1_MINB 3
+#define S1_MINB 4
 #endif
 __global__ void __launch_bounds__(L0_NT, S1_MINB) k_l0_s1(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -301,7 +301,7 @@ __device__ __forceinline__ void s3_body(const L0Args &a, const L0Layout &l, cons
 
 template <int M>
 #ifndef S3_MINB
-#define S3_MINB 4
+#define S3_MINB 5
 #endif
 __global__ void __launch_bounds__(L0_NT, S3_MINB) k_l0_s3acc(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
