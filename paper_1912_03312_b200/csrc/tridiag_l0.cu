@@ -21,6 +21,10 @@ namespace rexi {
 constexpr int L0_NT = 128;      // threads per CTA
 constexpr int L0_ROWPAD = 2;    // extra staged rows (next interface row + 16-B rounding)
 
+#ifndef K2_RES_UNROLL
+#define K2_RES_UNROLL 3
+#endif
+constexpr int K2_UNROLL = K2_RES_UNROLL;
 #ifndef K2_MINB
 #define K2_MINB 3
 #endif
@@ -371,7 +375,7 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
     // products; r_q goes to slot q-1 (x_{q-1} is dead once r_q is formed) -- a
     // rolled loop keeps the kernel's code and register footprint small
     c128 xm = tc[0], x0 = tc[kp];
-#pragma unroll 1
+#pragma unroll K2_UNROLL
     for (int q = 1; q < M; ++q) {
         const int lr = c.lr0 + q;
         const c128 xp = q < cnt ? tc[(q + 1) * kp] : xn;
