@@ -198,6 +198,34 @@ int rexi_pencil_cheb_step(rexi_pencil *pencil, const rexi_c128 *coeffs, int32_t 
                           const rexi_c128 *u_in, rexi_c128 *u_out, int32_t n_steps, int32_t mem,
                           rexi_stats *stats);
 const char *rexi_pencil_last_error(const rexi_pencil *pencil);
+
+/* ---- P1 assembly on a structured Kuhn mesh ----
+ * Builds A = 0.5 K + M_V and B = M on the interior nodes of an m^d-cell grid
+ * (d = 1, 2, 3; d! simplices per cell) directly in device memory, in the
+ * builder's host assembly order (fixtures.py assemble_p1, restating the
+ * reference's COO assembly spatial.py:193-223 for P1).  The caller supplies
+ * the stencil/contribution table (host) and the element potential matrices
+ * pot_e (device, [n_templates][m^d][(d+1)^2]); indptr (n_int+1), indices,
+ * a_vals, b_vals (nnz = sum over offsets of prod_k (m-1-|o_k|)) are device
+ * buffers the caller allocates. */
+typedef struct rexi_p1_desc {
+    int32_t d, m;                   /* dimension, cells per axis                     */
+    int32_t n_templates;            /* simplices per cell (d!)                      */
+    int32_t n_off;                  /* stencil offsets, sorted by column delta       */
+    const int32_t *offsets;         /* host [n_off][d]                              */
+    int32_t n_contrib;              /* element contributions, grouped by offset     */
+    const int32_t *contrib_start;   /* host [n_off + 1]                             */
+    const int32_t *contrib_t;       /* host [n_contrib] template index              */
+    const int32_t *contrib_a;       /* host [n_contrib] local row (vertex a)        */
+    const int32_t *contrib_b;       /* host [n_contrib] local column (vertex b)     */
+    const int32_t *contrib_va;      /* host [n_contrib][d] vertex a offset in cells */
+    const double *contrib_stiff;    /* host [n_contrib] K_e[a][b] (scaled by h)     */
+    const double *contrib_mass;     /* host [n_contrib] M_e[a][b]                   */
+    int32_t device;
+    void *stream;
+} rexi_p1_desc;
+int rexi_assemble_p1(const rexi_p1_desc *desc, const double *pot_e, int32_t *indptr, int32_t *indices,
+                     double *a_vals, double *b_vals);
 int rexi_pencil_destroy(rexi_pencil *pencil);
 int32_t rexi_abi_version(void);
 

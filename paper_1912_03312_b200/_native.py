@@ -35,7 +35,7 @@ EXPORTED = (
     "rexi_last_error", "rexi_device_count", "rexi_abi_version", "rexi_plan_profile",
     "rexi_plan_profile_report", "rexi_plan_run", "rexi_pencil_create", "rexi_pencil_solve_b",
     "rexi_pencil_spectral_radius", "rexi_pencil_cheb_step", "rexi_pencil_last_error",
-    "rexi_pencil_destroy",
+    "rexi_pencil_destroy", "rexi_assemble_p1",
 )
 
 
@@ -61,6 +61,17 @@ class RexiDesc(ctypes.Structure):
         ("max_iters", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
         ("weight_ref", ctypes.c_double),
+    ]
+
+
+class RexiP1Desc(ctypes.Structure):
+    _fields_ = [
+        ("d", ctypes.c_int32), ("m", ctypes.c_int32), ("n_templates", ctypes.c_int32),
+        ("n_off", ctypes.c_int32), ("offsets", ctypes.c_void_p), ("n_contrib", ctypes.c_int32),
+        ("contrib_start", ctypes.c_void_p), ("contrib_t", ctypes.c_void_p),
+        ("contrib_a", ctypes.c_void_p), ("contrib_b", ctypes.c_void_p),
+        ("contrib_va", ctypes.c_void_p), ("contrib_stiff", ctypes.c_void_p),
+        ("contrib_mass", ctypes.c_void_p), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
     ]
 
 
@@ -131,6 +142,7 @@ def lib():
     L.rexi_pencil_last_error.argtypes = [vp]
     L.rexi_pencil_last_error.restype = ctypes.c_char_p
     L.rexi_pencil_destroy.argtypes = [vp]
+    L.rexi_assemble_p1.argtypes = [ctypes.POINTER(RexiP1Desc), vp, vp, vp, vp, vp]
     if L.rexi_abi_version() != ABI_VERSION:
         raise DeviceError("native library ABI version mismatch")
     _lib = L

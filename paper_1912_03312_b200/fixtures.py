@@ -119,7 +119,27 @@ class StructuredMesh:
         return np.stack([g.ravel() for g in grids], axis=1)
 
 
+def _use_device() -> bool:
+    if os.environ.get("REXI_FIXTURE_HOST"):
+        return False
+    try:
+        import torch
+        from . import _native
+        return torch.cuda.is_available() and os.path.exists(_native.LIB_PATH)
+    except Exception:
+        return False
+
+
 def assemble_p1(mesh: StructuredMesh, potential) -> SystemMatrices:
+    """The pencil on the GPU when one is available (assembly.assemble_p1_device,
+    SURVEY 8(f)4), else on the host (assemble_p1_host)."""
+    if mesh.d > 1 and _use_device():
+        from .assembly import assemble_p1_device
+        return assemble_p1_device(mesh, potential)
+    return assemble_p1_host(mesh, potential)
+
+
+def assemble_p1_host(mesh: StructuredMesh, potential) -> SystemMatrices:
     """A = 0.5*K + M_V, B = M on interior nodes, CSR with sorted columns.
 
     ``potential(x)`` takes points (n, d) and returns V (n,).  Stencil
@@ -291,13 +311,41 @@ class Config:
     mesh: StructuredMesh
 
 
-def _harmonic(center, coef):
-    c = np.asarray(center, dtype=float)
+def _cell_axis(mesh, k, off, dev):
+    """Coordinates lo_k + h (i + off_k) of the cells along axis k (device),
+    in the host formula's operation order."""
+    import torch
+    i = torch.arange(mesh.m, dtype=torch.float64, device=dev)
+    return mesh.lo[k] + mesh.h * (i + float(off[k]))
 
-    def v(x):
-        dx = x - c
-        return coef * np.sum(dx * dx, axis=1)
-    return v
+
+class _Harmonic:
+    """V = coef |x - c|^2; device_on_cells evaluates all cells at one
+    quadrature offset on the GPU (same operation order as __call__)."""
+
+    def __init__(self, center, coef):
+        self.c = np.asarray(center, dtype=float)
+        self.coef = coef
+
+    def __call__(self, x):
+        dx = x - self.c
+        return self.coef * np.sum(dx * dx, axis=1)
+
+    def device_on_cells(self, mesh, off, dev):
+        import torch
+        d = mesh.d
+        s = None
+        for k in range(d):
+            dx = _cell_axis(mesh, k, off, dev) - float(self.c[k])
+            shape = [1] * d
+            shape[k] = mesh.m
+            term = (dx * dx).reshape(shape)
+            s = term if s is None else s + term
+        return (self.coef * s).reshape(-1)
+
+
+def _harmonic(center, coef):
+    return _Harmonic(center, coef)
 
 
 def config1(m: int = 1024, k: int = 32) -> Config:
@@ -321,10 +369,19 @@ def config2_potential(seed: int = 1912):
     kw = rng.uniform(-1.5, 1.5)
     modes = np.arange(1, 17)
 
-    def v(x):
-        arg = 2.0 * math.pi * np.outer(x[:, 0] + 200.0, modes) / 400.0 + phi
-        return np.cos(arg) @ a
-    return v, center, std, kw, float(np.sum(a))
+    class Fourier1D:
+        def __call__(self, x):
+            arg = 2.0 * math.pi * np.outer(x[:, 0] + 200.0, modes) / 400.0 + phi
+            return np.cos(arg) @ a
+
+        def device_on_cells(self, mesh, off, dev):
+            import torch
+            x = _cell_axis(mesh, 0, off, dev)
+            md = torch.from_numpy(modes.astype(float)).to(dev)
+            arg = 2.0 * math.pi * torch.outer(x + 200.0, md) / 400.0 + torch.from_numpy(phi).to(dev)
+            return torch.cos(arg) @ torch.from_numpy(a).to(dev)
+
+    return Fourier1D(), center, std, kw, float(np.sum(a))
 
 
 def config2(m: int = 2 ** 20 - 1, k: int = 64, sr: float | None = None) -> Config:
@@ -388,6 +445,16 @@ def config4_potential(seed: int = 3312, grid_m: int = 2048):
             xs = mesh.lo[0] + h * (np.arange(m) + off[0])
             ys = mesh.lo[1] + h * (np.arange(m) + off[1])
             return self.scale * self.f_grid(xs, ys).ravel()
+
+        def device_on_cells(self, mesh, off, dev):
+            import torch
+            xs, ys = _cell_axis(mesh, 0, off, dev), _cell_axis(mesh, 1, off, dev)
+            p = torch.from_numpy(pq[:, 0].astype(float)).to(dev)
+            q = torch.from_numpy(pq[:, 1].astype(float)).to(dev)
+            X = torch.exp(2j * math.pi * torch.outer(xs, p).to(torch.complex128))
+            Y = torch.exp(2j * math.pi * torch.outer(ys, q).to(torch.complex128))
+            cc = torch.from_numpy(c).to(dev)
+            return self.scale * ((X * cc) @ Y.T).real.reshape(-1)
 
     v = FourierPotential()
     g = np.linspace(0.0, 1.0, grid_m + 1)

@@ -152,6 +152,18 @@ def cheb_main():
     run_ref_cheb("pencil", sysn, rng.standard_normal(n) + 1j * rng.standard_normal(n), 2)
 
 
+def harness_main():
+    """The reference harness's default tunneling experiment (harness.py:68-90,
+    205-213): 1D P2, 4000 elements, step barrier, flagship K=16 poles, dt=5e-5;
+    a few REXI steps through the reference (the P2 pencil is pentadiagonal)."""
+    from rexiprop.harness import ExperimentConfig, _build_experiment
+    cfg = ExperimentConfig()
+    mesh, consts, system, u0 = _build_experiment(cfg)
+    flag = faber_cf(JoukowskiMap(10.0))
+    sr = float(spectral_radius_estimate(system))
+    run_ref("harness_p2", system, flag, cfg.dt, u0, 3, sr)
+
+
 def main():
     sets = write_poles()
     flag = sets[16]
@@ -204,5 +216,7 @@ def main():
 if __name__ == "__main__":
     if "--cheb" in sys.argv:
         cheb_main()
+    elif "--harness" in sys.argv:
+        harness_main()
     else:
         main()
