@@ -107,6 +107,11 @@ def allgather_partials(mine, world: int, group=None, out=None):
         return out
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out.view(-1), mine.contiguous().view(-1), group=group)
+    elif mine.is_cuda:
+        # gloo gathers host tensors only (functional multi-rank checks)
+        parts = [torch.empty(tuple(mine.shape), dtype=mine.dtype) for _ in range(world)]
+        dist.all_gather(parts, mine.detach().cpu(), group=group)
+        out.copy_(torch.stack(parts))
     else:
         dist.all_gather(list(out.unbind(0)), mine.contiguous(), group=group)
     return out
