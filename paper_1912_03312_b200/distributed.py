@@ -117,6 +117,43 @@ def allgather_partials(mine, world: int, group=None, out=None):
     return out
 
 
+def exchange_segments(mine, send, recv, world: int, seg: int, group=None):
+    """All-to-all of row segments of the (4, n) partials: afterwards
+    recv[g] = rows [r*seg, (r+1)*seg) of rank g's partial (r = this rank),
+    zero-padded past n.  NCCL: one all_to_all_single; gloo (functional
+    checks): host tensors."""
+    import torch
+    import torch.distributed as dist
+    n = mine.shape[1]
+    npad = seg * world
+    src = mine
+    if npad != n:
+        src = torch.zeros((4, npad), dtype=mine.dtype, device=mine.device)
+        src[:, :n] = mine
+    send.copy_(src.view(4, world, seg).transpose(0, 1))
+    if dist.get_backend(group) == "nccl":
+        dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
+        return
+    # gloo has no all_to_all: gather every rank's segments, keep this rank's
+    rank = dist.get_rank(group)
+    allp = [torch.empty(tuple(send.shape), dtype=send.dtype) for _ in range(world)]
+    dist.all_gather(allp, send.detach().cpu(), group=group)
+    recv.copy_(torch.stack([allp[g][rank] for g in range(world)]))
+
+
+def gather_segments(useg, uall, world: int, group=None):
+    """All-gather of the rounded complex128 segments into uall (world*seg)."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(torch.view_as_real(uall).view(-1), torch.view_as_real(useg).view(-1),
+                                    group=group)
+    else:
+        parts = [torch.empty(useg.shape, dtype=useg.dtype) for _ in range(world)]
+        dist.all_gather(parts, useg.detach().cpu(), group=group)
+        uall.copy_(torch.cat(parts))
+
+
 class ShardedStepper:
     """This rank's shard of one REXI step.  ``step(u, out)`` takes and writes
     device tensors (complex128, length n) on this rank's GPU."""
@@ -140,12 +177,30 @@ class ShardedStepper:
         self.parts = torch.empty((world, 4, self.n), dtype=torch.float64, device=dev)
         self.mine = torch.empty((4, self.n), dtype=torch.float64, device=dev)
         self.stream = stream
+        # segmented exchange buffers: row segments of seg rows per rank
+        self.seg = -(-self.n // world)
+        npad = self.seg * world
+        self.send = torch.zeros((world, 4, self.seg), dtype=torch.float64, device=dev)
+        self.recv = torch.empty((world, 4, self.seg), dtype=torch.float64, device=dev)
+        self.useg = torch.empty(self.seg, dtype=torch.complex128, device=dev)
+        self.uall = torch.empty(npad, dtype=torch.complex128, device=dev)
 
     def step(self, u, out):
+        """u1 = sum over all shards of beta_j x_j.  Each rank computes its
+        shard's double-double partial; an all-to-all hands rank r the row
+        segment r of every partial; rank r combines it in rank order (the
+        same per-row double-double operations as combining everything
+        everywhere) and rounds; an all-gather assembles u1.  Per rank and step
+        that moves 48 B/row instead of (world-1) x 32 B/row."""
         self.plan.step_partial(u.data_ptr(), self.mine.data_ptr())
-        allgather_partials(self.mine, self.world, self.group, out=self.parts)
-        _native.combine_partials(self.parts.data_ptr(), self.world, self.n, out.data_ptr(),
+        if self.world == 1:
+            _native.combine_partials(self.mine.data_ptr(), 1, self.n, out.data_ptr(), self.stream)
+            return
+        exchange_segments(self.mine, self.send, self.recv, self.world, self.seg, self.group)
+        _native.combine_partials(self.recv.data_ptr(), self.world, self.seg, self.useg.data_ptr(),
                                  self.stream)
+        gather_segments(self.useg, self.uall, self.world, self.group)
+        out.copy_(self.uall[:self.n])
 
     def close(self):
         self.plan.close()
