@@ -411,7 +411,16 @@ def main():
                 cpu = cpu_baseline(cfg)
             except Exception as exc:  # the baseline must not kill the bench line
                 cpu = {"error": str(exc)}
-        step_bytes = 80 * n + 32 * k * n
+        # algorithmic bytes of one step: the kernels' own counts where the
+        # profile carries them (COCG: live shifts per iteration), else SURVEY
+        # 8(d)'s closed form for the direct 1D step
+        kshard_ = len(sh.shards[rank]) if world > 1 else k
+        prof_bytes = 0.0
+        for kname, (cnt_, _t, b_) in prof.items():
+            kb = kernel_bytes(kname, n, kshard_) if b_ <= 0 else None
+            prof_bytes += b_ if b_ > 0 else (kb or 0) * cnt_
+        step_bytes = prof_bytes / args.steps if prof_bytes > 0 else 80 * n + 32 * k * n
+        prof_ms = sum(v[1] for v in prof.values())
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -428,6 +437,13 @@ def main():
             "kernels": {kname: {"launches": c, "total_ms": t, "GBps": (bt / (t / 1e3) / 1e9 if bt else None)}
                         for kname, (c, t, bt) in prof.items()},
             "step_algorithmic_GBps": step_bytes / (ms / args.steps / 1e3) / 1e9,
+            "step_roofline": {
+                "algorithmic_bytes_per_step": step_bytes,
+                "achieved_GBps": step_bytes / (ms / args.steps / 1e3) / 1e9,
+                "frac": step_bytes / (ms / args.steps / 1e3) / 1e9 / peak,
+                "kernel_time_frac": (prof_ms / ms) if prof_ms and not persistent else None,
+                "note": "whole step (all kernels, launch gaps and host polls included) against the "
+                        "measured HBM peak"},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
