@@ -72,6 +72,7 @@ struct CgScal {                            // per lane of the current layout
     double2 *part_f, *part_f2;             // finish level partials [nranges][kp] (ping-pong)
     double *part_g, *part_g2;
     unsigned int *ctr;                     // [8] claim / done counters (parity)
+    unsigned int *gctr;                    // [CG_GCTR] finish-tree group counters
     double *tolsq;                         // [kp] squared relative residual target per lane
 };
 
@@ -221,7 +222,10 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
 #define CG_SPMV_MINB 1
 #endif
 constexpr int kSpmvUnroll = CG_SPMV_UNROLL;
-template <bool CPLX>
+#ifndef CG_GB
+#define CG_GB 8   // z gathers in flight per thread (global-CSR spmv)
+#endif
+template <bool CPLX, bool BATCH>
 __global__ void __launch_bounds__(CG_NT, CG_SPMV_MINB) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
     __shared__ double2 sbp[2][CG_SBP];
     __shared__ int64_t claim_q[2];
@@ -252,11 +256,33 @@ __global__ void __launch_bounds__(CG_NT, CG_SPMV_MINB) k_cg_spmv(CgMat M, CgVec 
                 for (int64_t i = r0; i < r1; i += CG_CH) {
                     c128 acc = cmk(0.0, 0.0);
                     const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
+                    if (BATCH) {
+                        // batches of CG_GB entries: indices, then all z gathers of the
+                        // batch in flight, then the ascending-q accumulation
+                        for (int32_t qb = q0; qb < q1; qb += CG_GB) {
+                            uint32_t cc[CG_GB];
+                            c128 zz[CG_GB];
+    #pragma unroll
+                            for (int k = 0; k < CG_GB; ++k) cc[k] = qb + k < q1 ? (uint32_t)__ldg(M.indices + qb + k) : 0u;
+    #pragma unroll
+                            for (int k = 0; k < CG_GB; ++k) zz[k] = qb + k < q1 ? zv[cc[k] * kp + lane] : cmk(0.0, 0.0);
+    #pragma unroll
+                            for (int k = 0; k < CG_GB; ++k) {
+                                if (qb + k < q1) {
+                                    const int32_t q = qb + k;
+                                    const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0,
+                                                              __ldg(M.b + q), sg);
+                                    acc = cadd(acc, cmul(e, zz[k]));
+                                }
+                            }
+                        }
+                    } else {
 #pragma unroll kSpmvUnroll
-                    for (int32_t q = q0; q < q1; ++q) {
-                        const uint32_t c = (uint32_t)__ldg(M.indices + q);
-                        const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
-                        acc = cadd(acc, cmul(e, zv[c * kp + lane]));
+                        for (int32_t q = q0; q < q1; ++q) {
+                            const uint32_t c = (uint32_t)__ldg(M.indices + q);
+                            const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
+                            acc = cadd(acc, cmul(e, zv[c * kp + lane]));
+                        }
                     }
                     const uint32_t o = (uint32_t)i * kp + lane;
                     const c128 pi = cadd(zv[o], cmul(beta, pv[o]));
@@ -509,51 +535,107 @@ __device__ __forceinline__ void sum_range(const double2 *pa, const double *pc, i
     }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(CG_NT) k_cg_finish(CgScal Sc, CgGeom g, int kreal, int max_iters) {
-    if (MODE != 0 && *Sc.nactive == 0) return;
-    const int kp = g.kp;
-    const int64_t nranges = (g.nchunks + CG_RANGE - 1) / CG_RANGE;
-    const double2 *pa = MODE == 1 ? Sc.part_a : Sc.part_b;
-    const int64_t t = (int64_t)blockIdx.x * CG_NT + threadIdx.x;
-    if (t < nranges * kp) {
-        const int64_t r = t / kp;
-        const int l = (int)(t % kp);
-        double2 s = make_double2(0.0, 0.0);
-        double sr = 0.0;
-        const int64_t c0 = r * CG_RANGE, c1 = min(c0 + CG_RANGE, g.nchunks);
-        if (MODE == 1) sum_range<false>(pa, Sc.part_c, c0, c1, kp, l, s, sr);
-        else sum_range<true>(pa, Sc.part_c, c0, c1, kp, l, s, sr);
-        Sc.part_f[(size_t)r * kp + l] = s;
-        if (MODE != 1) Sc.part_g[(size_t)r * kp + l] = sr;
+// The tree: level-1 value r = ordered sum of chunk partials [64r, 64r+64),
+// level-(k+1) value g = ordered sum of level-k values [64g, 64g+64), until
+// one value per lane remains.  Every CTA stages the partials it sums into
+// shared memory with coalesced loads and one thread per (value, lane) adds
+// them in order (sum_range's order); the last CTA to finish the 64 inputs of
+// a group (atomic counter per group and lane group) computes that group's
+// value, so the levels run on many CTAs; the CTA holding a lane group's
+// final value applies the per-shift scalar updates.
+constexpr int CG_GCTR = 4096;
+constexpr int CG_FL_NT = 256;
+constexpr int CG_FL_MAXV = 2048;   // staged values per CTA
+
+__device__ __forceinline__ bool arrive_count(unsigned int *ctr, unsigned int add, unsigned int total) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ctr, add) + add == total;
+    __syncthreads();
+    if (last) __threadfence();
+    return last;
+}
+
+// ordered sums of nv groups (of up to CG_RANGE consecutive values each, starting
+// at value index v0 of src) for LG lanes starting at l0: dst[(g0+v)*kp + l0 + l]
+template <bool REAL>
+__device__ __forceinline__ void fl_sum_groups(const double2 *src, const double *srcr, int64_t v0, int64_t nsrc,
+                                             int nv, int kp, int l0, int LG, double2 *dst, double *dstr,
+                                             int64_t g0, double2 *smv, double *smr) {
+    const int64_t vend = min(v0 + (int64_t)nv * CG_RANGE, nsrc);
+    const int cnt = (int)(vend - v0);
+    for (int e = threadIdx.x; e < cnt * LG; e += CG_FL_NT) {
+        const int64_t v = v0 + e / LG;
+        const int l = l0 + e % LG;
+        smv[e] = __ldcg(src + v * kp + l);
+        if (REAL) smr[e] = __ldcg(srcr + v * kp + l);
     }
-    if (!arrive_last(Sc.ctr + 6, gridDim.x)) return;
-    // fixed fan-in-CG_RANGE levels inside the last CTA (ping-pong part_f/part_f2)
-    double2 *src = Sc.part_f, *dst = Sc.part_f2;
-    double *srcr = Sc.part_g, *dstr = Sc.part_g2;
-    int64_t n1 = nranges;
-    while (n1 > 1) {
-        const int64_t n2 = (n1 + CG_RANGE - 1) / CG_RANGE;
-        for (int64_t w = threadIdx.x; w < n2 * kp; w += CG_NT) {
-            const int64_t r = w / kp;
-            const int l = (int)(w % kp);
-            double2 s = make_double2(0.0, 0.0);
-            double sr = 0.0;
-            const int64_t c0 = r * CG_RANGE, c1 = min(c0 + CG_RANGE, n1);
-            if (MODE == 1) sum_range<false>(src, srcr, c0, c1, kp, l, s, sr);
-            else sum_range<true>(src, srcr, c0, c1, kp, l, s, sr);
-            dst[(size_t)r * kp + l] = s;
-            if (MODE != 1) dstr[(size_t)r * kp + l] = sr;
+    __syncthreads();
+    if (threadIdx.x < nv * LG) {
+        const int gi = threadIdx.x / LG, l = threadIdx.x % LG;
+        const int c0 = gi * CG_RANGE, c1 = min(c0 + CG_RANGE, cnt);
+        if (c0 < cnt) {
+            double2 acc = make_double2(0.0, 0.0);
+            double accr = 0.0;
+            for (int c = c0; c < c1; ++c) {
+                acc = cadd(acc, smv[c * LG + l]);
+                if (REAL) accr += smr[c * LG + l];
+            }
+            dst[(g0 + gi) * kp + l0 + l] = acc;
+            if (REAL) dstr[(g0 + gi) * kp + l0 + l] = accr;
         }
-        __threadfence_block();
-        __syncthreads();
-        double2 *tc = src; src = dst; dst = tc;
-        double *tr = srcr; srcr = dstr; dstr = tr;
-        n1 = n2;
     }
-    for (int l = threadIdx.x; l < kp; l += CG_NT) {
-        const double2 s = src[l];
-        const double sr = MODE != 1 ? srcr[l] : 0.0;
+    __syncthreads();
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(CG_FL_NT) k_cg_finish(CgScal Sc, CgGeom g, int kreal, int max_iters) {
+    extern __shared__ __align__(16) unsigned char fl_smem[];
+    if (MODE != 0 && *Sc.nactive == 0) return;
+    constexpr bool REAL = MODE != 1;
+    double2 *smv = reinterpret_cast<double2 *>(fl_smem);
+    double *smr = reinterpret_cast<double *>(smv + CG_FL_MAXV);
+    const int kp = g.kp;
+    const int LG = kp < 32 ? kp : 32;            // lanes per CTA
+    const int nlg = kp / LG;
+    const int TR = max(1, CG_FL_NT / (LG * CG_RANGE));   // level-1 values per CTA (divides 64)
+    const int lg = blockIdx.x % nlg, rt = blockIdx.x / nlg;
+    const int l0 = lg * LG;
+    const double2 *pa = MODE == 1 ? Sc.part_a : Sc.part_b;
+    const int64_t n1 = (g.nchunks + CG_RANGE - 1) / CG_RANGE;
+    // level 1: TR ranges of chunk partials
+    const int64_t r0 = (int64_t)rt * TR;
+    const int nv = (int)min((int64_t)TR, n1 - r0);
+    fl_sum_groups<REAL>(pa, Sc.part_c, r0 * CG_RANGE, g.nchunks, nv, kp, l0, LG, Sc.part_f, Sc.part_g, r0, smv, smr);
+    // upper levels: the last arriver of each group of 64 computes its value
+    const double2 *src = Sc.part_f;
+    const double *srcr = Sc.part_g;
+    double2 *dst = Sc.part_f2;
+    double *dstr = Sc.part_g2;
+    int64_t ncur = n1, grp = r0 / CG_RANGE, coff = 0;
+    unsigned int add = (unsigned int)nv;
+    while (ncur > 1) {
+        const int64_t nnext = (ncur + CG_RANGE - 1) / CG_RANGE;
+        const unsigned int total = (unsigned int)min((int64_t)CG_RANGE, ncur - grp * CG_RANGE);
+        unsigned int *ctr = Sc.gctr + coff + grp * nlg + lg;
+        if (!arrive_count(ctr, add, total)) return;
+        if (threadIdx.x == 0) *ctr = 0;
+        fl_sum_groups<REAL>(src, srcr, grp * CG_RANGE, ncur, 1, kp, l0, LG, dst, dstr, grp, smv, smr);
+        coff += nnext * nlg;
+        src = dst;
+        srcr = dstr;
+        dst += nnext * kp;
+        dstr += nnext * kp;
+        ncur = nnext;
+        grp /= CG_RANGE;
+        add = 1;
+    }
+    // this CTA holds its lane group's final values (src[l]); scalar updates
+    for (int ll = threadIdx.x; ll < LG; ll += CG_FL_NT) {
+        const int l = l0 + ll;
+        const double2 s = __ldcg(src + l);
+        const double sr = MODE != 1 ? __ldcg(srcr + l) : 0.0;
         if (MODE == 0) {
             Sc.rho[l] = s;
             Sc.bnorm2[l] = sr;
@@ -594,25 +676,30 @@ __global__ void __launch_bounds__(CG_NT) k_cg_finish(CgScal Sc, CgGeom g, int kr
             }
         }
     }
-    __syncthreads();
+    // the last lane group to finish counts the live lanes and resets the claim counter
+    if (!arrive_count(Sc.gctr + CG_GCTR - 1, 1u, (unsigned int)nlg)) return;
     if (threadIdx.x < 32) {
         if (MODE != 1) {
             int na = 0;
-            for (int l = threadIdx.x; l < kp; l += 32) na += Sc.active[l];
+            for (int l = threadIdx.x; l < kp; l += 32) na += __ldcg(Sc.active + l);
             for (int off = 16; off > 0; off >>= 1) na += __shfl_xor_sync(0xffffffffu, na, off);
             if (threadIdx.x == 0) *Sc.nactive = na;
         }
         if (threadIdx.x == 0) {
-            Sc.ctr[6] = 0;
+            Sc.gctr[CG_GCTR - 1] = 0;
             if (MODE == 1) Sc.ctr[0] = 0;   // spmv claim counter
         }
     }
 }
 
 static inline int finish_grid(const CgGeom &g) {
-    const int64_t nranges = (g.nchunks + CG_RANGE - 1) / CG_RANGE;
-    return (int)std::max<int64_t>(1, (nranges * g.kp + CG_NT - 1) / CG_NT);
+    const int64_t n1 = (g.nchunks + CG_RANGE - 1) / CG_RANGE;
+    const int LG = g.kp < 32 ? g.kp : 32;
+    const int TR = std::max(1, CG_FL_NT / (LG * CG_RANGE));
+    return (int)(((n1 + TR - 1) / TR) * (g.kp / LG));
 }
+
+static inline size_t finish_smem(int mode) { return (size_t)CG_FL_MAXV * (sizeof(double2) + (mode != 1 ? 8 : 0)); }
 
 // ---------------------------------------------------------------------------
 // compaction: dst[i][l'] = src[i][map[l']] (new width kp_new)
@@ -954,6 +1041,14 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     CGA(Sc.part_g2, sizeof(double) * (size_t)kp * nranges_max);
     CGA(Sc.ctr, sizeof(unsigned int) * 8);
     CGK(cudaMemsetAsync(Sc.ctr, 0, sizeof(unsigned int) * 8, st));
+    CGA(Sc.gctr, sizeof(unsigned int) * CG_GCTR);
+    CGK(cudaMemsetAsync(Sc.gctr, 0, sizeof(unsigned int) * CG_GCTR, st));
+    for (int mode = 0; mode < 3; ++mode) {
+        cudaError_t fe = mode == 0 ? cudaFuncSetAttribute(k_cg_finish<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)finish_smem(0))
+                       : mode == 1 ? cudaFuncSetAttribute(k_cg_finish<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)finish_smem(1))
+                                   : cudaFuncSetAttribute(k_cg_finish<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)finish_smem(2));
+        CGK(fe);
+    }
     CGA(Sc.tolsq, sizeof(double) * kp);
     CGK(cudaMallocHost((void **)&im->h_buf, sizeof(int) * (2 + 2 * kp)));
     CGK(cudaStreamSynchronize(st));
@@ -1014,7 +1109,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     const double nnzb = 28.0 * (double)cg.nnz + 4.0 * (double)(n + 1);   // CSR pattern + 3 value arrays
     hook_begin(cg, "cg_init", 96.0 * n * kp);
     k_cg_init<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
-    k_cg_finish<0><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
+    k_cg_finish<0><<<finish_grid(g), CG_FL_NT, finish_smem(0), st>>>(im->Sc, g, cg.k, cg.max_iters);
     hook_end(cg);
     CGK(cudaGetLastError());
     *launches += 2;
@@ -1048,16 +1143,18 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
                 }
                 if (im->cplx) k_cg_spmv_st<true><<<grid, CG_NT, sm, st>>>(im->M, im->V, im->Sc, S, g);
                 else k_cg_spmv_st<false><<<grid, CG_NT, sm, st>>>(im->M, im->V, im->Sc, S, g);
-            } else if (im->cplx) {
-                k_cg_spmv<true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+            } else if (g.kp == 1) {   // one lane: batched gathers (measured faster only here)
+                if (im->cplx) k_cg_spmv<true, true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+                else k_cg_spmv<false, true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
             } else {
-                k_cg_spmv<false><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+                if (im->cplx) k_cg_spmv<true, false><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+                else k_cg_spmv<false, false><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
             }
-            k_cg_finish<1><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
+            k_cg_finish<1><<<finish_grid(g), CG_FL_NT, finish_smem(1), st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             hook_begin(cg, width_name("cg_update", kp), 112.0 * n * live + 24.0 * n);
             k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
-            k_cg_finish<2><<<finish_grid(g), CG_NT, 0, st>>>(im->Sc, g, cg.k, cg.max_iters);
+            k_cg_finish<2><<<finish_grid(g), CG_FL_NT, finish_smem(2), st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             *launches += 4;
             ++it;
