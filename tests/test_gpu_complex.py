@@ -1,0 +1,63 @@
+"""GPU: complex A (absorbing potential, A = 0.5 K + M_V with Im V < 0) through
+both solvers.  The reference only assembles real A (spatial.py:193-223), so
+the check is against a scipy LU evaluation of the same pole sum
+(integrate.py:171,203-213) and between the two independent GPU solvers."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _complex_system(n_cells=400):
+    from scipy.sparse import csr_matrix, diags
+    from paper_1912_03312_b200.fixtures import StructuredMesh, _harmonic, assemble_p1_host
+    from paper_1912_03312_b200.types import SystemMatrices
+    mesh = StructuredMesh(1, n_cells, np.array([-10.0]), 20.0 / n_cells)
+    s = assemble_p1_host(mesh, _harmonic([0.0], 0.5))
+    x = mesh.interior_coords()[:, 0]
+    absorb = -0.5j * np.clip((np.abs(x) - 7.0) / 3.0, 0.0, None) ** 2   # absorbing layer near the ends
+    A = (s.A + diags(absorb * np.asarray(s.B.diagonal()))).tocsr().astype(complex)
+    return SystemMatrices(A=csr_matrix(A), B=s.B, n_dof=s.n_dof), mesh
+
+
+def _scipy_step(sysm, approx, tau, u):
+    from scipy.sparse.linalg import splu
+    rhs = 1j * (sysm.B @ u)
+    out = np.zeros_like(u)
+    for s, w in zip(approx.shifts, approx.weights):
+        S = (tau * sysm.A - (1j * s) * sysm.B).tocsc()
+        out += w * splu(S).solve(rhs)
+    return out
+
+
+@pytest.mark.parametrize("solver", ["tridiag", "cocg"])
+def test_complex_potential_matches_scipy(flagship, solver):
+    from paper_1912_03312_b200 import rexi_prepare, rexi_step
+    sysm, mesh = _complex_system()
+    x = mesh.interior_coords()[:, 0]
+    u0 = np.exp(-(x + 2.0) ** 2) * np.exp(2j * x)
+    tau = 0.01
+    stp = rexi_prepare(sysm, flagship, tau, sr_value=2.0e4, override_admissibility=True, solver=solver)
+    u1 = rexi_step(stp, u0)
+    ref = _scipy_step(sysm, flagship, tau, u0)
+    assert np.linalg.norm(u1 - ref) <= 1e-8 * np.linalg.norm(ref)
+    stp.close()
+
+
+def test_complex_potential_solvers_agree(flagship):
+    from paper_1912_03312_b200 import rexi_prepare, rexi_run
+    sysm, mesh = _complex_system()
+    x = mesh.interior_coords()[:, 0]
+    u0 = np.exp(-(x + 2.0) ** 2) * np.exp(2j * x)
+    outs = []
+    for solver in ("tridiag", "cocg"):
+        stp = rexi_prepare(sysm, flagship, 0.01, sr_value=2.0e4, override_admissibility=True, solver=solver,
+                           refine=1)
+        outs.append(rexi_run(stp, u0, 3))
+        stp.close()
+    assert np.linalg.norm(outs[0] - outs[1]) <= 1e-9 * np.linalg.norm(outs[1])
+    # absorption: the B-norm decreases
+    B = sysm.B
+    n0 = np.sqrt(np.real(np.vdot(u0, B @ u0)))
+    n3 = np.sqrt(np.real(np.vdot(outs[0], B @ outs[0])))
+    assert n3 <= n0 * (1 + 1e-9)
