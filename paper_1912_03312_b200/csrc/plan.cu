@@ -8,6 +8,7 @@
 #include <cmath>
 #include <map>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -688,6 +689,18 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     }
     if (stats) CK(cudaEventRecord(ev[0], st));
     int cur = (src == plan->ubuf[0]) ? 0 : 1;
+    // zero-copy output: when u_out is page-locked host memory, the last step's
+    // final kernel writes u1 straight into it over PCIe (overlapped with the
+    // kernel) instead of a separate device-to-host copy afterwards
+    c128 *zc_out = nullptr;
+    if (mem == REXI_MEM_HOST && n_steps > 0 && !(plan->persist_cs > 0 && !plan->prof) &&
+        !getenv("REXI_NO_ZEROCOPY")) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, u_out) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+            zc_out = (c128 *)pa.devicePointer;
+        else
+            cudaGetLastError();
+    }
     if (n_steps > 0 && plan->persist_cs > 0 && !plan->prof) {
         TriState &T = plan->tri;
         CK(persist_launch(T.z, T.lv.data(), (int)T.lv.size(), plan->S, n, src, plan->pbuf[0], plan->pbuf[1],
@@ -716,18 +729,24 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
             plan->graph_kernels = plan->launches - l0;
             plan->launches = l0;
         }
-        for (int s = 0; s < n_steps; ++s) {
+        const int graph_steps = zc_out ? n_steps - 1 : n_steps;
+        for (int s = 0; s < graph_steps; ++s) {
             CK(cudaGraphLaunch(plan->graph[cur], st));
             plan->launches += plan->graph_kernels;
             cur ^= 1;
         }
         src = plan->ubuf[cur];
+        if (zc_out) {   // last step straight into the page-locked output
+            int rc = plan_step_device(plan, src, zc_out);
+            if (rc) return rc;
+        }
         n_steps = -n_steps;    // steps done; restored below
     }
     for (int s = 0; s < n_steps; ++s) {
         c128 *dst;
         bool last = s == n_steps - 1;
         if (last && mem == REXI_MEM_DEVICE) dst = (c128 *)u_out;
+        else if (last && zc_out) dst = zc_out;
         else dst = plan->ubuf[src == plan->ubuf[0] ? 1 : 0];
         if (dst == src) dst = plan->ubuf[cur ^ 1];   // in-place device call
         int rc = plan_step_device(plan, src, dst);
@@ -748,7 +767,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
             CK(cudaMemcpyAsync(u_out, u_in, sizeof(c128) * n, cudaMemcpyDeviceToDevice, st));
         }
     } else if (mem == REXI_MEM_HOST) {
-        CK(cudaMemcpyAsync(u_out, src, sizeof(c128) * n, cudaMemcpyDeviceToHost, st));
+        if (!zc_out) CK(cudaMemcpyAsync(u_out, src, sizeof(c128) * n, cudaMemcpyDeviceToHost, st));
     } else if ((const void *)src != (const void *)u_out) {
         CK(cudaMemcpyAsync(u_out, src, sizeof(c128) * n, cudaMemcpyDeviceToDevice, st));
     }
