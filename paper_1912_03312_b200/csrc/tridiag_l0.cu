@@ -220,10 +220,20 @@ __device__ __forceinline__ void reduce_rows(const c128 *tile, const L0Args &a, i
 // acc -= e*x, error-free (Dot2 style) into complex double-double accumulators
 __device__ __forceinline__ void dot2_sub(ddacc &re, ddacc &im, c128 e, c128 x) {
     dd p;
+#ifdef K2_MIXED
+    // experiment: exact products only for the real part of the entry (tau*A
+    // dominated on stiff pencils); the small -Re(sigma) b products go into the
+    // low word with one FMA each
+    p = two_prod(e.x, x.x); ddacc_add(re, -p.hi); re.lo = __dsub_rn(re.lo, p.lo);
+    re.lo = __fma_rn(e.y, x.y, re.lo);
+    p = two_prod(e.x, x.y); ddacc_add(im, -p.hi); im.lo = __dsub_rn(im.lo, p.lo);
+    im.lo = __fma_rn(-e.y, x.x, im.lo);
+#else
     p = two_prod(e.x, x.x); ddacc_add(re, -p.hi); re.lo = __dsub_rn(re.lo, p.lo);
     p = two_prod(e.y, x.y); ddacc_add(re, p.hi); re.lo = __dadd_rn(re.lo, p.lo);
     p = two_prod(e.x, x.y); ddacc_add(im, -p.hi); im.lo = __dsub_rn(im.lo, p.lo);
     p = two_prod(e.y, x.x); ddacc_add(im, -p.hi); im.lo = __dsub_rn(im.lo, p.lo);
+#endif
 }
 
 struct Ctx {
