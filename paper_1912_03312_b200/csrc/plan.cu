@@ -29,6 +29,7 @@ struct TriState {
     L0Dev z{};
     c128 *rhs0 = nullptr, *rres = nullptr;
     double *acc = nullptr;
+    bool complex_a = false;       // A has an imaginary part: K2 keeps every residual product error-free
 };
 
 }  // namespace
@@ -205,6 +206,7 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
         for (int32_t q = d->indptr[r]; q < d->indptr[r + 1]; ++q) {
             int64_t c = d->indices[q];
             double av = d->a_vals[q], ai = d->a_imag ? d->a_imag[q] : 0.0, bv = d->b_vals[q];
+            if (ai != 0.0) T.complex_a = true;
             if (c == r - 1) { a_sub[r] = av; ai_sub[r] = ai; b_sub[r] = bv; }
             else if (c == r) { a_dia[r] = av; ai_dia[r] = ai; b_dia[r] = bv; }
             else if (c == r + 1) { a_sup[r] = av; ai_sup[r] = ai; b_sup[r] = bv; }
@@ -408,7 +410,7 @@ int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
     }
     {
         ProfScope ps(plan, "l0_k2");
-        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres, T.n, st));
+        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres, T.n, T.complex_a, st));
     }
     rc = tri_mid(plan, true);
     if (rc) return rc;
