@@ -542,6 +542,9 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
     }
     plan->solver = solver;
     plan->kp = pick_kp(d->k);
+    // 1D: at least two lanes -- with one lane a level-0 CTA spans 2048 rows and
+    // K2's staged row arrays exceed shared memory (the padding lane has beta = 0)
+    if (solver == REXI_SOLVER_TRIDIAG && plan->kp < 2) plan->kp = 2;
     if (solver == REXI_SOLVER_TRIDIAG && plan->kp > 256) {
         int rc = set_err(plan, REXI_ERR_UNSUPPORTED, "TRIDIAG solver supports at most 256 shifts per plan");
         rexi_plan_destroy(plan);
