@@ -355,19 +355,10 @@ int tri_chain(rexi_plan *plan, const c128 *rst, int out_mode, int acc_add, c128 
 
 // levels 1..top (S1 up, top solve, S3 down); level-1 rhs from level 0's
 // ypart/lc, or from its double-double pieces in the correction pass
-// level-0 S1 defers its interface term to the level-1 S1 (L0Fix) when level 1
-// runs the TMA kernel -- a level-0 tile then needs no neighbour state
-bool defer_ds(const rexi_plan *plan) {
-    static const bool off = getenv("REXI_NO_DEFER") != nullptr;   // debug knob
-    const TriState &T = plan->tri;
-    return !off && T.lv.size() >= 3 && T.lv[0].sym && l0v2_supported(plan->kp);
-}
-
-int tri_mid(rexi_plan *plan, bool dd, const c128 *u) {
+int tri_mid(rexi_plan *plan, bool dd) {
     TriState &T = plan->tri;
     const size_t nl = T.lv.size();
     cudaStream_t st = plan->stream;
-    const bool fix = !dd && defer_ds(plan);
     // TMA-staged kernel at every reduced level of a symmetric pencil (measured
     // faster than the plain kernel even for the few-CTA upper levels)
     const bool tma_ok = T.lv[0].sym && l0v2_supported(plan->kp);
@@ -376,8 +367,7 @@ int tri_mid(rexi_plan *plan, bool dd, const c128 *u) {
         ProfScope ps(plan, "s1_lv");
         const bool d = l == 1 && dd;
         if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 1, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
-                                  d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, nullptr, st,
-                                  (fix && l == 1) ? &T.z : nullptr, u, T.n, T.rhs0));
+                                  d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, nullptr, st));
         else if (d) CK(tri_launch_lv_dd(T.lv[1], plan->S, 1, T.lv[0].ypdd, T.lv[0].lcdd, nullptr, st));
         else CK(tri_launch_s1(T.z, T.lv[l], plan->S, (int)l, nullptr, nullptr, T.lv[l - 1].ypart,
                               T.lv[l - 1].lc, st));
@@ -409,9 +399,9 @@ int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
     }
     {
         ProfScope ps(plan, "l0_s1");
-        CK(l0_launch_s1(T.z, T.lv[0], plan->S, T.rhs0, st, defer_ds(plan)));
+        CK(l0_launch_s1(T.z, T.lv[0], plan->S, T.rhs0, st));
     }
-    int rc = tri_mid(plan, false, u);
+    int rc = tri_mid(plan, false);
     if (rc) return rc;
     if (plan->refine <= 0) {
         ProfScope ps(plan, "l0_s3acc");
@@ -422,7 +412,7 @@ int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
         ProfScope ps(plan, "l0_k2");
         CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres, T.n, T.complex_a, st));
     }
-    rc = tri_mid(plan, true, u);
+    rc = tri_mid(plan, true);
     if (rc) return rc;
     ProfScope ps(plan, "l0_k3");
     CK(l0_launch_k3(T.z, T.lv[0], plan->S, T.lv[1].X, T.rres, T.acc, uout, T.n, st));

@@ -41,7 +41,6 @@ struct L0Args {
     int64_t nout;         // real n (level 0 is padded to a multiple of M)
     int acc_add;
     int final_out;
-    int defer_ds;         // S1: store yfirst, the level-1 S1 adds the interface term
 };
 
 // shared-memory view of the staged per-row inputs (local row index)
@@ -284,8 +283,7 @@ __device__ __forceinline__ void s1_body(const L0Args &a, const L0Layout &l, cons
     sweep_bwd<M, FULL>(y, ti, c.kp, rv, c.lr0, c.cnt, c.sg, cmk(0.0, 0.0), [](int, c128) {});
     const c128 yfirst = c.cnt >= 1 ? y[1] : cmk(0.0, 0.0);
     const int kp = c.kp, j = c.j;
-    // deferred interface term: the level-1 S1 completes it (L0Fix)
-    a.L.ypart[c.p * kp + j] = a.defer_ds ? yfirst : cfnma(rv.rhs[c.lr0], rv.sup(c.lr0, c.sg), yfirst);
+    a.L.ypart[c.p * kp + j] = cfnma(rv.rhs[c.lr0], rv.sup(c.lr0, c.sg), yfirst);
     if (c.p + 1 < c.P) a.L.lc[(c.p + 1) * kp + j] = cneg(cmul(rv.sub(c.lr0 + M, c.sg), ylast));
     if (c.p == 0) a.L.lc[j] = cmk(0.0, 0.0);
 }
@@ -503,63 +501,12 @@ __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
 #ifndef LV_MINB
 #define LV_MINB 3
 #endif
-// Deferred interface term of the level-0 S1 (L0Fix): level-0 S1 stores
-// yfirst in ypart and the level-1 S1 completes ypart = cfnma(ds, cs, yfirst)
-// with ds = rhs at the block's interface row (formed here from u, as k_rhs
-// does) and cs the interface row's sup entry -- the same operation on the same
-// values as the undeferred S1, so results are bitwise unchanged.  It lets a
-// level-0 tile run S1 without the neighbouring tile's state (fused K3 + S1).
-struct L0Fix {
-    L0Dev z;
-    const c128 *u;      // state the rhs iBu is formed from
-    int64_t n;          // real rows
-    c128 *rhs0;         // interface rows of rhs0 are written here (lane 0)
-    c128 *ypart;        // level-0 ypart: raw in, completed out
-};
-
-__device__ __forceinline__ c128 rhs_at_row(const L0Fix &f, int64_t i) {
-    if (i >= f.n) return cmk(0.0, 0.0);
-    double sr = 0.0, si = 0.0;
-    if (i > 0) {
-        const double b = __ldg(f.z.b_sub + i);
-        const c128 x = f.u[i - 1];
-        sr = __dadd_rn(sr, __dmul_rn(b, x.x));
-        si = __dadd_rn(si, __dmul_rn(b, x.y));
-    }
-    {
-        const double b = __ldg(f.z.b_dia + i);
-        const c128 x = f.u[i];
-        sr = __dadd_rn(sr, __dmul_rn(b, x.x));
-        si = __dadd_rn(si, __dmul_rn(b, x.y));
-    }
-    if (i + 1 < f.n) {
-        const double b = __ldg(f.z.b_sup + i);
-        const c128 x = f.u[i + 1];
-        sr = __dadd_rn(sr, __dmul_rn(b, x.x));
-        si = __dadd_rn(si, __dmul_rn(b, x.y));
-    }
-    return cmk(-si, sr);
-}
-
-// complete ypart of level-0 block p (= level-1 row p) for lane j
-__device__ __forceinline__ c128 fix_ypart(const L0Fix &f, int64_t p, int j, int kp, c128 sg) {
-    const int64_t r = p * TRI_M;
-    const c128 ds = rhs_at_row(f, r);
-    const c128 cs = form_entry(__ldg(f.z.ta_sup + r), __ldg(f.z.ta_sup_im + r), __ldg(f.z.b_sup + r), sg);
-    const c128 y = cfnma(ds, cs, f.ypart[p * kp + j]);
-    f.ypart[p * kp + j] = y;
-    if (j == 0) f.rhs0[r] = ds;
-    return y;
-}
-
 struct LvArgs {
     LevelDev L;
     ShiftDev S;
     const c128 *rin_a, *rin_b;   // previous level ypart / lc
     const cdd *rdd_a, *rdd_b;    // or their double-double versions (correction pass)
     const c128 *Xnext;
-    L0Fix fx;                    // level 1, S1: complete the deferred level-0 ypart
-    int fix;
 };
 
 struct LvPtrs {
@@ -568,14 +515,11 @@ struct LvPtrs {
     const cdd *da, *db;
     const c128 *Xn;
     c128 *ypart, *lc, *X;
-    const L0Fix *fx;                // non-null: complete level-0 ypart while reading it
-    c128 sg;
 };
 
 template <bool DD>
 __device__ __forceinline__ c128 lv_rhs(const LvPtrs &q, int64_t i, int j, int kp) {
     if constexpr (DD) return cdd_round(cdd_add(q.da[i * kp + j], q.db[i * kp + j]));
-    else if (q.fx) return cadd(fix_ypart(*q.fx, i, j, kp, q.sg), q.rb[i * kp + j]);
     else return cadd(q.ra[i * kp + j], q.rb[i * kp + j]);
 }
 
@@ -662,21 +606,14 @@ __global__ void __launch_bounds__(L0_NT, LV_MINB) k_lv_tma(const __grid_constant
     t.inv = tinv + j; t.sup = tsup + j;
     t.ra = a.rin_a; t.rb = a.rin_b; t.da = a.rdd_a; t.db = a.rdd_b; t.Xn = a.Xnext;
     t.ypart = a.L.ypart; t.lc = a.L.lc; t.X = a.L.X;
-    t.fx = (PHASE == 1 && !DD && a.fix) ? &a.fx : nullptr;
-    t.sg = a.S.sigma[j];
     if (cnt == M - 1) lv_body<M, PHASE, DD, true>(t, b * M, kp, j, p, P, base, cnt);
     else lv_body<M, PHASE, DD, false>(t, b * M, kp, j, p, P, base, cnt);
 }
 
 cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,
-                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st,
-                          const L0Dev *fz, const c128 *fu, int64_t fn, c128 *frhs0) {
+                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st) {
     LvArgs a{};
     a.L = L; a.S = S; a.rin_a = rin_a; a.rin_b = rin_b; a.rdd_a = rdd_a; a.rdd_b = rdd_b; a.Xnext = Xnext;
-    if (fz) {
-        a.fix = 1;
-        a.fx = L0Fix{*fz, fu, fn, frhs0, const_cast<c128 *>(rin_a)};
-    }
     const int kp = S.kp;
     const int64_t rows = (int64_t)(L0_NT / kp) * TRI_M;
     const int64_t grid = (L.n + rows - 1) / rows;
@@ -717,9 +654,9 @@ bool l0v2_supported(int kp) { return kp <= L0_NT; }
 int64_t l0_row_padding() { return (int64_t)L0_NT * TRI_M + 2 * L0_ROWPAD; }
 
 cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
-                         cudaStream_t st, bool defer_ds) {
+                         cudaStream_t st) {
     L0Args a{};
-    a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0; a.defer_ds = defer_ds ? 1 : 0;
+    a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0;
     return launch_l0(k_l0_s1<TRI_M>, a, ST_RHS, st);
 }
 

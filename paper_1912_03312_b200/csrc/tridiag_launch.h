@@ -43,15 +43,13 @@ inline int64_t lv_tma_ctas(int64_t n, int kp) {   // grid of lv_launch_tma
     return (n + rows - 1) / rows;
 }
 cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,
-                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st,
-                          const L0Dev *fz = nullptr, const c128 *fu = nullptr, int64_t fn = 0,
-                          c128 *frhs0 = nullptr);
+                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st);
 
 // TMA-fed level-0 kernels (tridiag_l0.cu)
 bool l0v2_supported(int kp);
 int64_t l0_row_padding();
 cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
-                         cudaStream_t st, bool defer_ds = false);
+                         cudaStream_t st);
 cudaError_t l0_launch_s3acc(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
                             const c128 *X1, double *acc, c128 *uout, int64_t nout, cudaStream_t st);
 cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
