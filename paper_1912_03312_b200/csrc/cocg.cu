@@ -455,6 +455,114 @@ __global__ void __launch_bounds__(CG_NT) k_cg_spmv_st(CgMat M, CgVec V, CgScal S
 }
 
 // ---------------------------------------------------------------------------
+// Width 1 (one live shift, the tail of a solve): one thread per row, a warp
+// per 32-row chunk.  The sub-block partial (rows b, b+8, b+16, b+24 summed
+// in that order from 0) and the chunk partial (sub-blocks 0..7 in order) are
+// formed with shuffles in the same order as the general kernels, so the
+// results are bitwise identical to them -- with 4x the threads in flight.
+// ---------------------------------------------------------------------------
+constexpr int CG1_NT = 256;
+
+__device__ __forceinline__ double2 shfl_c(double2 v, int src) {
+    return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+// chunk partial of a warp's 32 per-row terms (lane = row in chunk)
+__device__ __forceinline__ double2 chunk_sum_c(double2 t) {
+    const int l = threadIdx.x & 31;
+    const double2 t1 = shfl_c(t, (l + 8) & 31), t2 = shfl_c(t, (l + 16) & 31), t3 = shfl_c(t, (l + 24) & 31);
+    const double2 mu = cadd(cadd(cadd(cadd(make_double2(0.0, 0.0), t), t1), t2), t3);   // lanes 0..7
+    double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int b = 0; b < CG_CH; ++b) s = cadd(s, shfl_c(mu, b));
+    return s;
+}
+__device__ __forceinline__ double chunk_sum_r(double t) {
+    const int l = threadIdx.x & 31;
+    const double t1 = __shfl_sync(0xffffffffu, t, (l + 8) & 31), t2 = __shfl_sync(0xffffffffu, t, (l + 16) & 31),
+                 t3 = __shfl_sync(0xffffffffu, t, (l + 24) & 31);
+    const double mu = (((0.0 + t) + t1) + t2) + t3;
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < CG_CH; ++b) s = s + __shfl_sync(0xffffffffu, mu, b);
+    return s;
+}
+
+template <bool CPLX>
+__global__ void __launch_bounds__(CG1_NT) k_cg_spmv1(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
+    if (*Sc.nactive == 0) return;
+    const bool act = Sc.active[0] != 0;
+    const c128 sg = S.sigma[g.lane_shift[0]];
+    const c128 beta = Sc.beta[0];
+    c128 *__restrict__ pv = V.p;
+    c128 *__restrict__ qv = V.q;
+    const c128 *__restrict__ zv = V.z;
+    const int l = threadIdx.x & 31;
+    const int64_t wstride = (int64_t)gridDim.x * (CG1_NT / 32);
+    for (int64_t c = (int64_t)blockIdx.x * (CG1_NT / 32) + (threadIdx.x >> 5); c < g.nchunks; c += wstride) {
+        const int64_t i = c * (CG_SB * CG_CH) + l;
+        c128 term = cmk(0.0, 0.0);
+        if (act && i < M.n) {
+            c128 acc = cmk(0.0, 0.0);
+            const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
+            for (int32_t qb = q0; qb < q1; qb += CG_GB) {
+                uint32_t cc[CG_GB];
+                c128 zz[CG_GB];
+#pragma unroll
+                for (int k = 0; k < CG_GB; ++k) cc[k] = qb + k < q1 ? (uint32_t)__ldg(M.indices + qb + k) : 0u;
+#pragma unroll
+                for (int k = 0; k < CG_GB; ++k) zz[k] = qb + k < q1 ? zv[cc[k]] : cmk(0.0, 0.0);
+#pragma unroll
+                for (int k = 0; k < CG_GB; ++k) {
+                    if (qb + k < q1) {
+                        const int32_t q = qb + k;
+                        const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
+                        acc = cadd(acc, cmul(e, zz[k]));
+                    }
+                }
+            }
+            const c128 pi = cadd(zv[i], cmul(beta, pv[i]));
+            const c128 qi = cadd(acc, cmul(beta, qv[i]));
+            pv[i] = pi;
+            qv[i] = qi;
+            term = cmul(pi, qi);
+        }
+        const double2 s = chunk_sum_c(term);
+        if (l == 0) Sc.part_a[c] = s;
+    }
+}
+
+__global__ void __launch_bounds__(CG1_NT) k_cg_update1(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
+    if (*Sc.nactive == 0) return;
+    const bool act = Sc.active[0] != 0;
+    const c128 sg = S.sigma[g.lane_shift[0]];
+    const c128 alpha = Sc.alpha[0];
+    const int l = threadIdx.x & 31;
+    const int64_t wstride = (int64_t)gridDim.x * (CG1_NT / 32);
+    for (int64_t c = (int64_t)blockIdx.x * (CG1_NT / 32) + (threadIdx.x >> 5); c < g.nchunks; c += wstride) {
+        const int64_t i = c * (CG_SB * CG_CH) + l;
+        c128 trho = cmk(0.0, 0.0);
+        double trn = 0.0;
+        if (act && i < M.n) {
+            const c128 p = V.p[i], q = V.q[i];
+            V.x[i] = cadd(V.x[i], cmul(alpha, p));
+            const c128 r = csub(V.r[i], cmul(alpha, q));
+            V.r[i] = r;
+            const c128 z = cdiv_c(r, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
+            V.z[i] = z;
+            trho = cmul(r, z);
+            trn = cabs2(r);
+        }
+        const double2 s = chunk_sum_c(trho);
+        const double sr = chunk_sum_r(trn);
+        if (l == 0) {
+            Sc.part_b[c] = s;
+            Sc.part_c[c] = sr;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // update: x += alpha p; r -= alpha q; z = D^-1 r; partials of rho' = r^T z, |r|^2
 // (claims statically strided over CTAs: pointwise, no locality to exploit)
 // ---------------------------------------------------------------------------
@@ -1143,6 +1251,13 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
                 }
                 if (im->cplx) k_cg_spmv_st<true><<<grid, CG_NT, sm, st>>>(im->M, im->V, im->Sc, S, g);
                 else k_cg_spmv_st<false><<<grid, CG_NT, sm, st>>>(im->M, im->V, im->Sc, S, g);
+            } else if (g.kp == 1 && cg.nnz > (int64_t)CG_GB * n) {
+                // one lane, rows longer than one gather batch (3D stencils): a thread
+                // per row.  Shorter rows (2D) keep the 4-rows-per-thread batched kernel,
+                // measured faster there (209 vs 224 us at 4M rows).
+                const int g1 = (int)std::min<int64_t>((g.nchunks + 7) / 8, (int64_t)im->sms * 16);
+                if (im->cplx) k_cg_spmv1<true><<<g1, CG1_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+                else k_cg_spmv1<false><<<g1, CG1_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
             } else if (g.kp == 1) {   // one lane: batched gathers (measured faster only here)
                 if (im->cplx) k_cg_spmv<true, true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
                 else k_cg_spmv<false, true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
@@ -1153,7 +1268,12 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             k_cg_finish<1><<<finish_grid(g), CG_FL_NT, finish_smem(1), st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             hook_begin(cg, width_name("cg_update", kp), 112.0 * n * live + 24.0 * n);
-            k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+            if (g.kp == 1) {
+                const int g1 = (int)std::min<int64_t>((g.nchunks + 7) / 8, (int64_t)im->sms * 16);
+                k_cg_update1<<<g1, CG1_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+            } else {
+                k_cg_update<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
+            }
             k_cg_finish<2><<<finish_grid(g), CG_FL_NT, finish_smem(2), st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             *launches += 4;
