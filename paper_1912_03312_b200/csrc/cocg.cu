@@ -1251,10 +1251,10 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
                 }
                 if (im->cplx) k_cg_spmv_st<true><<<grid, CG_NT, sm, st>>>(im->M, im->V, im->Sc, S, g);
                 else k_cg_spmv_st<false><<<grid, CG_NT, sm, st>>>(im->M, im->V, im->Sc, S, g);
-            } else if (g.kp == 1 && cg.nnz > (int64_t)CG_GB * n) {
-                // one lane, rows longer than one gather batch (3D stencils): a thread
-                // per row.  Shorter rows (2D) keep the 4-rows-per-thread batched kernel,
-                // measured faster there (209 vs 224 us at 4M rows).
+            } else if (g.kp == 1 && cg.nnz <= (int64_t)CG_GB * n) {
+                // one lane, rows within one gather batch (2D stencils): a thread per row
+                // (78 -> 71 us at 1M rows).  Longer rows (3D) keep the 4-rows-per-thread
+                // batched kernel, measured faster there (209 vs 224 us at 2M rows).
                 const int g1 = (int)std::min<int64_t>((g.nchunks + 7) / 8, (int64_t)im->sms * 16);
                 if (im->cplx) k_cg_spmv1<true><<<g1, CG1_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
                 else k_cg_spmv1<false><<<g1, CG1_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
