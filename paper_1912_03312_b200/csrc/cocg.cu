@@ -1222,8 +1222,22 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     CGK(cudaGetLastError());
     *launches += 2;
     int live = cg.k;
+    int packed_live = std::min(cg.k, kp);   // live lanes at the last (re)pack
     int it = 0;
     const int check_every = 8;
+    // failed lane l (current layout) -> error naming its shift
+    auto lane_failure = [&](int l, int status) -> int {
+        int iters = 0;
+        cudaMemcpy(&iters, im->Sc.iters + l, sizeof(int), cudaMemcpyDeviceToHost);
+        char buf[256];
+        const char *why = status == 1 ? "COCG breakdown (rho or p^T S p vanished)"
+                        : status == 2 ? "non-finite values in COCG"
+                                      : "COCG did not converge within max_iters";
+        snprintf(buf, sizeof buf, "%s for shift j = %d after %d iterations", why,
+                 cg.shift_offset + lane_shift[l], iters);
+        err = buf;
+        return status == 3 ? REXI_ERR_NOCONV : REXI_ERR_BREAKDOWN;
+    };
     // REXI_COCG_TRACE=1: iterations and host time spent at each layout width
     static const bool trace = getenv("REXI_COCG_TRACE") != nullptr;
     auto tr_t0 = std::chrono::steady_clock::now();
@@ -1280,21 +1294,39 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             ++it;
         }
         CGK(cudaGetLastError());
-        int *h_na = im->h_buf, *h_act = im->h_buf + 2;
+        int *h_na = im->h_buf, *h_act = im->h_buf + 2, *h_st = im->h_buf + 2 + im->kp_full;
         CGK(cudaMemcpyAsync(h_na, im->Sc.nactive, sizeof(int), cudaMemcpyDeviceToHost, st));
         CGK(cudaMemcpyAsync(h_act, im->Sc.active, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
         CGK(cudaStreamSynchronize(st));
         const int na = *h_na;
         live = na;
+        if (trace && getenv("REXI_COCG_TRACE_LIVE")) fprintf(stderr, "[cocg]   it %5d  width %3d  live %3d\n", it, kp, na);
         if (na == 0 || it > cg.max_iters + check_every) {
             trace_phase(kp, na);
             break;
         }
-        // compaction: halve the layout while the live lanes fit
+        // compaction: halve the layout while the live lanes fit; otherwise, once
+        // kp/8 more lanes have frozen inside the layout, repack the live lanes
+        // into a prefix of the same width.  A frozen lane costs bandwidth while
+        // it sits between live ones (2 lanes per 32-B sector, 32 per warp
+        // segment) and none as trailing padding: the wide phases run at ~80 %
+        // live lanes.  Repacking moves 160 B per live row-shift, about 0.8 of an
+        // iteration.  Per-lane results are unchanged (layout-independent
+        // reduction tree).
         int kp_new = kp;
         while (kp_new > 1 && na <= kp_new / 2) kp_new /= 2;
-        if (kp_new < kp) {
-            trace_phase(kp, na);
+        bool prefix = false;
+        if (kp_new == kp && kp >= 16 && packed_live - na >= kp / 8)
+            for (int l = na; l < kp && !prefix; ++l) prefix = h_act[l] != 0;
+        if (kp_new < kp || prefix) {
+            if (kp_new < kp) trace_phase(kp, na);
+            // a frozen lane leaving the layout takes its status with it: report
+            // a failed one now
+            CGK(cudaMemcpyAsync(h_st, im->Sc.status, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
+            CGK(cudaStreamSynchronize(st));
+            for (int l = 0; l < kp; ++l)
+                if (valid[l] && !h_act[l] && h_st[l]) return lane_failure(l, h_st[l]);
+            packed_live = na;
             // live lanes keep ascending shift order; frozen valid lanes hand their
             // x to the full-width solution; padding lanes (a copy of lane map[0],
             // inactive, invalid) fill the new width
@@ -1317,26 +1349,16 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
         }
     }
     // statistics / failures (per current lane -> shift)
-    std::vector<int> status(kp), iters(kp);
+    std::vector<int> status(kp);
     CGK(cudaMemcpyAsync(status.data(), im->Sc.status, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
-    CGK(cudaMemcpyAsync(iters.data(), im->Sc.iters, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
     // remaining valid lanes' x -> full-width solution
     CGK(cudaMemcpyAsync(im->mask, valid.data(), sizeof(int) * kp, cudaMemcpyHostToDevice, st));
     k_cg_scatter_x<<<(unsigned)((n * kp + 255) / 256), 256, 0, st>>>(im->V.x, im->xout, n, kp, im->kp_full,
                                                                     im->lane_shift, im->mask);
     CGK(cudaGetLastError());
     CGK(cudaStreamSynchronize(st));
-    for (int l = 0; l < kp; ++l) {
-        const int j = lane_shift[l];
-        if (j >= cg.k || !status[l]) continue;
-        char buf[256];
-        const char *why = status[l] == 1 ? "COCG breakdown (rho or p^T S p vanished)"
-                        : status[l] == 2 ? "non-finite values in COCG"
-                                         : "COCG did not converge within max_iters";
-        snprintf(buf, sizeof buf, "%s for shift j = %d after %d iterations", why, cg.shift_offset + j, iters[l]);
-        err = buf;
-        return status[l] == 3 ? REXI_ERR_NOCONV : REXI_ERR_BREAKDOWN;
-    }
+    for (int l = 0; l < kp; ++l)
+        if (valid[l] && lane_shift[l] < cg.k && status[l]) return lane_failure(l, status[l]);
     cg.last_iters_max = std::max(cg.last_iters_max, it);
     cg.last_iters_mean += it;
     return REXI_OK;

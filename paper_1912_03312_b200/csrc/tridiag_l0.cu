@@ -364,7 +364,7 @@ __device__ __forceinline__ void k2_solve(const L0Args &a, const L0Layout &l, con
     tc[0] = xs;
 }
 
-template <int M, bool FULL, bool EXACT>
+template <int M, bool FULL, bool EXACT, bool SYM>
 __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
                                           c128 xn, c128 (&y)[M]) {
     static_assert(FULL, "level 0 is padded to full blocks");
@@ -377,34 +377,40 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
     // from block p-1) and this block's half of the next interface row; taken
     // before the residual loop recycles the x slots
     ddacc p1re, p1im, p2re = {0.0, 0.0}, p2im = {0.0, 0.0};
+    const c128 sup0 = rv.sup(c.lr0, c.sg);
     {
         const c128 d = rv.rhs[c.lr0];
         p1re = {d.x, 0.0};
         p1im = {d.y, 0.0};
         dot2_sub<EXACT>(p1re, p1im, rv.dia(c.lr0, c.sg), xs);
-        dot2_sub<EXACT>(p1re, p1im, rv.sup(c.lr0, c.sg), tc[kp]);
+        dot2_sub<EXACT>(p1re, p1im, sup0, tc[kp]);
     }
     const bool has_next = c.p + 1 < c.P;
     const c128 an = rv.sub(c.lr0 + M, c.sg);
     if (has_next) dot2_sub<EXACT>(p2re, p2im, an, tc[cnt * kp]);
     // interior residuals r_q = d_q - a_q x_{q-1} - b_q x_q - c_q x_{q+1}, error-free
     // products; r_q goes to slot q-1 (x_{q-1} is dead once r_q is formed) -- a
-    // rolled loop keeps the kernel's code and register footprint small
+    // rolled loop keeps the kernel's code and register footprint small.  SYM
+    // (symmetric pencil, checked bitwise on the formed entries at plan
+    // creation): a_q = c_{q-1}, so each off-diagonal entry is formed once.
     c128 xm = tc[0], x0 = tc[kp];
+    c128 esub = sup0;
 #pragma unroll K2_UNROLL
     for (int q = 1; q < M; ++q) {
         const int lr = c.lr0 + q;
         const c128 xp = q < cnt ? tc[(q + 1) * kp] : xn;
         const c128 d = rv.rhs[lr];
         ddacc re = {d.x, 0.0}, im = {d.y, 0.0};
-        dot2_sub<EXACT>(re, im, rv.sub(lr, c.sg), xm);
+        const c128 eup = rv.sup(lr, c.sg);
+        dot2_sub<EXACT>(re, im, SYM ? esub : rv.sub(lr, c.sg), xm);
         dot2_sub<EXACT>(re, im, rv.dia(lr, c.sg), x0);
-        dot2_sub<EXACT>(re, im, rv.sup(lr, c.sg), xp);
+        dot2_sub<EXACT>(re, im, eup, xp);
         const c128 r = cmk(__dadd_rn(re.hi, re.lo), __dadd_rn(im.hi, im.lo));
         a.rres_out[(c.base + q) * kp + j] = r;
         tc[(q - 1) * kp] = r;
         xm = x0;
         x0 = xp;
+        esub = eup;
     }
     // correction reduce: S1 with rhs = r
     y[0] = cmk(0.0, 0.0);
@@ -448,7 +454,8 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
     __syncthreads();
     reduce_rows<M>(l.t1, a, c.row0);
     if (!c.active) return;
-    k2_refine<M, true, EXACT>(a, l, c, xs, xn, y);
+    if (a.L.sym) k2_refine<M, true, EXACT, true>(a, l, c, xs, xn, y);
+    else k2_refine<M, true, EXACT, false>(a, l, c, xs, xn, y);
 }
 
 // ---------------------------------------------------------------------------
