@@ -366,7 +366,10 @@ __device__ __forceinline__ void st_issue(const StLayout &L, int b, int64_t claim
 }
 
 template <bool CPLX>
-__global__ void __launch_bounds__(CG_NT) k_cg_spmv_st(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
+#ifndef CG_ST_MINB
+#define CG_ST_MINB 3   // 80 registers: 3 CTAs/SM (swept: scripts/tune_spmv_minb.sh)
+#endif
+__global__ void __launch_bounds__(CG_NT, CG_ST_MINB) k_cg_spmv_st(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
     __shared__ double2 sbp[2][CG_SBP];
     __shared__ int64_t claim_q[2];
     extern __shared__ __align__(128) unsigned char smem[];
