@@ -700,6 +700,51 @@ __device__ __forceinline__ void fl_sum_groups(const double2 *src, const double *
     __syncthreads();
 }
 
+// per-shift scalar update of lane l from its final reduced value(s)
+template <int MODE>
+__device__ __forceinline__ void finish_lane(CgScal &Sc, const CgGeom &g, int l, double2 s, double sr, int kreal,
+                                            int max_iters) {
+    if (MODE == 0) {
+        Sc.rho[l] = s;
+        Sc.bnorm2[l] = sr;
+        Sc.rnorm2[l] = sr;
+        Sc.beta[l] = make_double2(0.0, 0.0);
+        Sc.iters[l] = 0;
+        Sc.status[l] = 0;
+        Sc.active[l] = (g.lane_shift[l] < kreal && sr > 0.0) ? 1 : 0;
+    } else if (MODE == 1) {
+        if (Sc.active[l]) {
+            const double ms = cabs2(s);
+            if (!(ms > 0.0) || !isfinite(ms)) {
+                Sc.status[l] = isfinite(ms) ? 1 : 2;
+                Sc.active[l] = 0;
+                Sc.alpha[l] = make_double2(0.0, 0.0);
+            } else {
+                Sc.alpha[l] = cdiv_c(Sc.rho[l], s);
+            }
+        }
+    } else if (Sc.active[l]) {
+        Sc.rnorm2[l] = sr;
+        Sc.iters[l] += 1;
+        const double2 rho_old = Sc.rho[l];
+        if (!isfinite(sr) || !isfinite(s.x) || !isfinite(s.y)) {
+            Sc.status[l] = 2;
+            Sc.active[l] = 0;
+        } else if (sr <= Sc.tolsq[l] * Sc.bnorm2[l]) {
+            Sc.active[l] = 0;                               // converged: freeze
+        } else if (!(cabs2(rho_old) > 0.0)) {
+            Sc.status[l] = 1;
+            Sc.active[l] = 0;
+        } else if (Sc.iters[l] >= max_iters) {
+            Sc.status[l] = 3;
+            Sc.active[l] = 0;
+        } else {
+            Sc.beta[l] = cdiv_c(s, rho_old);
+            Sc.rho[l] = s;
+        }
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(CG_FL_NT) k_cg_finish(CgScal Sc, CgGeom g, int kreal, int max_iters) {
     extern __shared__ __align__(16) unsigned char fl_smem[];
@@ -745,47 +790,7 @@ __global__ void __launch_bounds__(CG_FL_NT) k_cg_finish(CgScal Sc, CgGeom g, int
     // this CTA holds its lane group's final values (src[l]); scalar updates
     for (int ll = threadIdx.x; ll < LG; ll += CG_FL_NT) {
         const int l = l0 + ll;
-        const double2 s = __ldcg(src + l);
-        const double sr = MODE != 1 ? __ldcg(srcr + l) : 0.0;
-        if (MODE == 0) {
-            Sc.rho[l] = s;
-            Sc.bnorm2[l] = sr;
-            Sc.rnorm2[l] = sr;
-            Sc.beta[l] = make_double2(0.0, 0.0);
-            Sc.iters[l] = 0;
-            Sc.status[l] = 0;
-            Sc.active[l] = (g.lane_shift[l] < kreal && sr > 0.0) ? 1 : 0;
-        } else if (MODE == 1) {
-            if (Sc.active[l]) {
-                const double ms = cabs2(s);
-                if (!(ms > 0.0) || !isfinite(ms)) {
-                    Sc.status[l] = isfinite(ms) ? 1 : 2;
-                    Sc.active[l] = 0;
-                    Sc.alpha[l] = make_double2(0.0, 0.0);
-                } else {
-                    Sc.alpha[l] = cdiv_c(Sc.rho[l], s);
-                }
-            }
-        } else if (Sc.active[l]) {
-            Sc.rnorm2[l] = sr;
-            Sc.iters[l] += 1;
-            const double2 rho_old = Sc.rho[l];
-            if (!isfinite(sr) || !isfinite(s.x) || !isfinite(s.y)) {
-                Sc.status[l] = 2;
-                Sc.active[l] = 0;
-            } else if (sr <= Sc.tolsq[l] * Sc.bnorm2[l]) {
-                Sc.active[l] = 0;                               // converged: freeze
-            } else if (!(cabs2(rho_old) > 0.0)) {
-                Sc.status[l] = 1;
-                Sc.active[l] = 0;
-            } else if (Sc.iters[l] >= max_iters) {
-                Sc.status[l] = 3;
-                Sc.active[l] = 0;
-            } else {
-                Sc.beta[l] = cdiv_c(s, rho_old);
-                Sc.rho[l] = s;
-            }
-        }
+        finish_lane<MODE>(Sc, g, l, __ldcg(src + l), MODE != 1 ? __ldcg(srcr + l) : 0.0, kreal, max_iters);
     }
     // the last lane group to finish counts the live lanes and resets the claim counter
     if (!arrive_count(Sc.gctr + CG_GCTR - 1, 1u, (unsigned int)nlg)) return;
@@ -1319,7 +1324,8 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
         int kp_new = kp;
         while (kp_new > 1 && na <= kp_new / 2) kp_new /= 2;
         bool prefix = false;
-        if (kp_new == kp && kp >= 16 && packed_live - na >= kp / 8)
+        static const bool no_prefix = getenv("REXI_COCG_NOPREFIX") != nullptr;   // A/B switch
+        if (!no_prefix && kp_new == kp && kp >= 16 && packed_live - na >= kp / 8)
             for (int l = na; l < kp && !prefix; ++l) prefix = h_act[l] != 0;
         if (kp_new < kp || prefix) {
             if (kp_new < kp) trace_phase(kp, na);

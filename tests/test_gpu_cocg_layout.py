@@ -1,0 +1,41 @@
+"""GPU: COCG layout changes must not change the answer.  Repacking the live
+lanes into a prefix of the same width (cocg.cu cg_solve) is bitwise
+identical to the halving-only compaction (layout-independent reduction
+tree), on 2D and 3D pencils, plain and refined."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+_PROBE = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_1912_03312_b200 import fixtures, rexi_prepare, rexi_run
+c, m, refine, steps = (int(a) for a in sys.argv[1:5])
+cfg = fixtures.build_config(c, m=m)
+stp = rexi_prepare(cfg.system, cfg.approx, cfg.tau, sr_value=cfg.sr, override_admissibility=True, refine=refine)
+out = rexi_run(stp, cfg.u0, steps)
+np.save(sys.argv[5], out)
+"""
+
+
+def _run(c, m, refine, steps, env_extra, tmp_path, tag):
+    env = dict(os.environ, **env_extra)
+    path = str(tmp_path / f"cocg_{c}_{m}_{refine}_{tag}.npy")
+    subprocess.run([sys.executable, "-c", _PROBE % ROOT, str(c), str(m), str(refine), str(steps), path],
+                   check=True, env=env, cwd=ROOT)
+    return np.load(path)
+
+
+@pytest.mark.parametrize("c,m,refine", [(3, 64, 1), (3, 64, 0), (5, 12, 1), (4, 48, 1)])
+def test_prefix_repack_bitwise(c, m, refine, tmp_path):
+    repacked = _run(c, m, refine, 2, {}, tmp_path, "prefix")
+    plain = _run(c, m, refine, 2, {"REXI_COCG_NOPREFIX": "1"}, tmp_path, "plain")
+    assert np.all(np.isfinite(plain))
+    assert np.array_equal(repacked, plain)
