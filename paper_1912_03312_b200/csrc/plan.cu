@@ -394,12 +394,8 @@ int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
     TriState &T = plan->tri;
     cudaStream_t st = plan->stream;
     {
-        ProfScope ps(plan, "rhs");
-        CK(tri_launch_rhs(T.z, T.n, u, T.rhs0, st));
-    }
-    {
-        ProfScope ps(plan, "l0_s1");
-        CK(l0_launch_s1(T.z, T.lv[0], plan->S, T.rhs0, st));
+        ProfScope ps(plan, "l0_s1");   // rhs = iBu formed inside (no separate rhs kernel)
+        CK(l0_launch_s1(T.z, T.lv[0], plan->S, u, T.rhs0, T.n, st));
     }
     int rc = tri_mid(plan, false);
     if (rc) return rc;
@@ -685,8 +681,31 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
         CK(cudaEventCreate(&ev[0]));
         CK(cudaEventCreate(&ev[1]));
     }
+    // zero-copy output: when u_out is page-locked host memory, the last step's
+    // final kernel writes u1 straight into it over PCIe (overlapped with the
+    // kernel) instead of a separate device-to-host copy afterwards
+    auto mapped = [](const void *p) -> c128 * {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+            return (c128 *)pa.devicePointer;
+        cudaGetLastError();
+        return nullptr;
+    };
+    c128 *zc_out = nullptr;
+    const bool zc_ok = mem == REXI_MEM_HOST && n_steps > 0 && !(plan->persist_cs > 0 && !plan->prof) &&
+                       !getenv("REXI_NO_ZEROCOPY");
+    if (zc_ok) zc_out = mapped(u_out);
+    // zero-copy input: a one-step host call of a TMA-path 1D plan reads u from
+    // page-locked host memory inside the level-0 S1 kernel (which forms rhs =
+    // iBu itself), so the host->device transfer overlaps that kernel's HBM
+    // traffic instead of preceding it
+    const c128 *zc_in = nullptr;
+    if (zc_ok && zc_out && n_steps == 1 && plan->solver == REXI_SOLVER_TRIDIAG && l0v2_supported(plan->kp))
+        zc_in = mapped(u_in);
     const c128 *src;
-    if (mem == REXI_MEM_HOST) {
+    if (zc_in) {
+        src = zc_in;
+    } else if (mem == REXI_MEM_HOST) {
         CK(cudaMemcpyAsync(plan->ubuf[0], u_in, sizeof(c128) * n, cudaMemcpyHostToDevice, st));
         src = plan->ubuf[0];
     } else {
@@ -694,18 +713,6 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     }
     if (stats) CK(cudaEventRecord(ev[0], st));
     int cur = (src == plan->ubuf[0]) ? 0 : 1;
-    // zero-copy output: when u_out is page-locked host memory, the last step's
-    // final kernel writes u1 straight into it over PCIe (overlapped with the
-    // kernel) instead of a separate device-to-host copy afterwards
-    c128 *zc_out = nullptr;
-    if (mem == REXI_MEM_HOST && n_steps > 0 && !(plan->persist_cs > 0 && !plan->prof) &&
-        !getenv("REXI_NO_ZEROCOPY")) {
-        cudaPointerAttributes pa{};
-        if (cudaPointerGetAttributes(&pa, u_out) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
-            zc_out = (c128 *)pa.devicePointer;
-        else
-            cudaGetLastError();
-    }
     if (n_steps > 0 && plan->persist_cs > 0 && !plan->prof) {
         TriState &T = plan->tri;
         CK(persist_launch(T.z, T.lv.data(), (int)T.lv.size(), plan->S, n, src, plan->pbuf[0], plan->pbuf[1],
@@ -716,7 +723,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     } else if (n_steps > 0 && plan->solver == REXI_SOLVER_TRIDIAG && !plan->prof) {
         // the 1D step is a fixed kernel sequence: replay it as a CUDA graph
         // (two graphs, ping-ponging between the plan's state buffers)
-        if (src != plan->ubuf[0] && src != plan->ubuf[1]) {
+        if (src != plan->ubuf[0] && src != plan->ubuf[1] && !zc_in) {
             CK(cudaMemcpyAsync(plan->ubuf[0], src, sizeof(c128) * n, cudaMemcpyDeviceToDevice, st));
             cur = 0;
         }
@@ -740,7 +747,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
             plan->launches += plan->graph_kernels;
             cur ^= 1;
         }
-        src = plan->ubuf[cur];
+        if (!(zc_in && graph_steps == 0)) src = plan->ubuf[cur];
         if (zc_out) {   // last step straight into the page-locked output
             int rc = plan_step_device(plan, src, zc_out);
             if (rc) return rc;

@@ -41,6 +41,8 @@ struct L0Args {
     int64_t nout;         // real n (level 0 is padded to a multiple of M)
     int acc_add;
     int final_out;
+    const c128 *u;        // S1: state u (device or mapped page-locked host memory)
+    c128 *rhs_out;        // S1: rhs = iBu of the CTA's rows -> rhs0 for K2 / S3ACC
 };
 
 // shared-memory view of the staged per-row inputs (local row index)
@@ -54,7 +56,7 @@ struct RowView {
     __device__ __forceinline__ c128 sup(int lr, c128 sg) const { return form_entry(ur[lr], ui[lr], ub[lr], sg); }
 };
 
-enum { ST_RHS = 1, ST_DIA = 2, ST_TILE2 = 4 };
+enum { ST_RHS = 1, ST_DIA = 2, ST_TILE2 = 4, ST_BDIA = 8 };
 
 struct L0Layout {
     int kp, T, Tp;
@@ -86,6 +88,7 @@ __device__ __forceinline__ L0Layout carve(unsigned char *smem, int kp, int M, in
     r.ur = d; d += l.Tp; r.ui = d; d += l.Tp; r.ub = d; d += l.Tp;
     r.dr = r.di = r.db = nullptr;
     if (flags & ST_DIA) { r.dr = d; d += l.Tp; r.di = d; d += l.Tp; r.db = d; d += l.Tp; }
+    else if (flags & ST_BDIA) { r.db = d; d += l.Tp; }
     return l;
 }
 
@@ -93,7 +96,7 @@ __host__ __device__ inline size_t l0_smem_bytes(int kp, int M, int flags) {
     size_t T = (size_t)(L0_NT / kp) * M, Tp = T + L0_ROWPAD;
     size_t b = 128 + T * kp * 16 * ((flags & ST_TILE2) ? 2 : 1);
     if (flags & ST_RHS) b += Tp * 16;
-    b += Tp * 8 * ((flags & ST_DIA) ? 9 : 6);
+    b += Tp * 8 * ((flags & ST_DIA) ? 9 : (flags & ST_BDIA) ? 7 : 6);
     return b;
 }
 
@@ -112,7 +115,7 @@ __device__ __forceinline__ void l0_stage(unsigned char *smem, const L0Layout &l,
         const uint32_t tb = (uint32_t)((row1 - row0) * l.kp * sizeof(c128));
         const uint32_t rb8 = (uint32_t)(l.Tp * 8), rb16 = (uint32_t)(l.Tp * 16);
         uint32_t total = tb * ((flags & ST_TILE2) ? 2 : 1) + ((flags & ST_RHS) ? rb16 : 0) +
-                         rb8 * ((flags & ST_DIA) ? 9 : 6);
+                         rb8 * ((flags & ST_DIA) ? 9 : (flags & ST_BDIA) ? 7 : 6);
         mbar_expect_tx(bar, total);
         bulk_g2s(l.t0, g_t0 + row0 * l.kp, tb, bar);
         if (flags & ST_TILE2) bulk_g2s(l.t1, g_t1 + row0 * l.kp, tb, bar);
@@ -126,6 +129,8 @@ __device__ __forceinline__ void l0_stage(unsigned char *smem, const L0Layout &l,
         if (flags & ST_DIA) {
             bulk_g2s((void *)l.rv.dr, a.z.ta_dia + row0, rb8, bar);
             bulk_g2s((void *)l.rv.di, a.z.ta_dia_im + row0, rb8, bar);
+            bulk_g2s((void *)l.rv.db, a.z.b_dia + row0, rb8, bar);
+        } else if (flags & ST_BDIA) {
             bulk_g2s((void *)l.rv.db, a.z.b_dia + row0, rb8, bar);
         }
     }
@@ -288,16 +293,61 @@ __device__ __forceinline__ void s1_body(const L0Args &a, const L0Layout &l, cons
     if (c.p == 0) a.L.lc[j] = cmk(0.0, 0.0);
 }
 
+// S1 with the rhs formed in the kernel: rhs_i = 1j * (B u)_i for the CTA's
+// rows, in k_rhs's order (CSR row order, unfused products: bitwise equal), from
+// u read directly -- device memory, or page-locked host memory mapped into the
+// device address space, which makes the host->device transfer of a host-buffer
+// step part of this kernel instead of a separate copy in front of it.  The rhs
+// rows go to rhs0 for K2 / S3ACC (padding rows stay zero).
 template <int M>
 #ifndef S1_MINB
 #define S1_MINB 4
 #endif
 __global__ void __launch_bounds__(L0_NT, S1_MINB) k_l0_s1(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const L0Layout l = carve(smem, a.S.kp, M, ST_RHS);
+    constexpr int FL = ST_RHS | ST_BDIA;
+    const L0Layout l = carve(smem, a.S.kp, M, FL);
     const Ctx c = make_ctx(a, M);
-    l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, ST_RHS);
+    l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, FL & ~ST_RHS);
+    // u rows row0-1 .. row0+T (loads in flight under the bulk copies)
+    c128 *su = reinterpret_cast<c128 *>(smem + ((l0_smem_bytes(a.S.kp, M, FL) + 15) & ~(size_t)15));   // T+2 slots after the carve
+    const int64_t n = a.nout;
+    for (int t = threadIdx.x; t < l.T + 2; t += L0_NT) {
+        const int64_t i = c.row0 - 1 + t;
+        su[t] = (i >= 0 && i < n) ? a.u[i] : cmk(0.0, 0.0);
+    }
     mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
+    __syncthreads();
+    c128 *rhs = const_cast<c128 *>(l.rv.rhs);
+    for (int t = threadIdx.x; t < l.T; t += L0_NT) {
+        const int64_t i = c.row0 + t;
+        c128 v = cmk(0.0, 0.0);
+        if (i < n) {
+            double sr = 0.0, si = 0.0;
+            if (i > 0) {
+                const double b = l.rv.sb[t];
+                const c128 x = su[t];
+                sr = __dadd_rn(sr, __dmul_rn(b, x.x));
+                si = __dadd_rn(si, __dmul_rn(b, x.y));
+            }
+            {
+                const double b = l.rv.db[t];
+                const c128 x = su[t + 1];
+                sr = __dadd_rn(sr, __dmul_rn(b, x.x));
+                si = __dadd_rn(si, __dmul_rn(b, x.y));
+            }
+            if (i + 1 < n) {
+                const double b = l.rv.ub[t];
+                const c128 x = su[t + 2];
+                sr = __dadd_rn(sr, __dmul_rn(b, x.x));
+                si = __dadd_rn(si, __dmul_rn(b, x.y));
+            }
+            v = cmk(-si, sr);
+            a.rhs_out[i] = v;
+        }
+        rhs[t] = v;
+    }
+    __syncthreads();
     if (!c.active) return;
     s1_body<M, true>(a, l, c);
 }
@@ -660,11 +710,21 @@ static cudaError_t launch_l0(K kern, const L0Args &a, int flags, cudaStream_t st
 bool l0v2_supported(int kp) { return kp <= L0_NT; }
 int64_t l0_row_padding() { return (int64_t)L0_NT * TRI_M + 2 * L0_ROWPAD; }
 
-cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
-                         cudaStream_t st) {
+cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *u, c128 *rhs0,
+                         int64_t nout, cudaStream_t st) {
     L0Args a{};
-    a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0;
-    return launch_l0(k_l0_s1<TRI_M>, a, ST_RHS, st);
+    a.z = z; a.L = L; a.S = S; a.u = u; a.rhs_out = rhs0; a.nout = nout;
+    // + T+2 u rows after the staged rhs rows
+    const size_t extra = 16 + ((size_t)(L0_NT / S.kp) * TRI_M + 2) * sizeof(c128);
+    const int kp = S.kp;
+    const int64_t rows = (int64_t)(L0_NT / kp) * TRI_M;
+    const int64_t grid = (L.n + rows - 1) / rows;
+    const size_t smem = l0_smem_bytes(kp, TRI_M, ST_RHS | ST_BDIA) + extra;
+    auto kern = k_l0_s1<TRI_M>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)grid, L0_NT, smem, st>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t l0_launch_s3acc(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,

@@ -48,8 +48,8 @@ cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const
 // TMA-fed level-0 kernels (tridiag_l0.cu)
 bool l0v2_supported(int kp);
 int64_t l0_row_padding();
-cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
-                         cudaStream_t st);
+cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *u, c128 *rhs0,
+                         int64_t nout, cudaStream_t st);
 cudaError_t l0_launch_s3acc(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
                             const c128 *X1, double *acc, c128 *uout, int64_t nout, cudaStream_t st);
 cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,

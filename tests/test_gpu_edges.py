@@ -91,3 +91,30 @@ def test_pageable_and_pinned_outputs_agree():
     assert rc == 0
     assert np.array_equal(pinned, pageable)
     stp.close()
+
+
+@pytest.mark.parametrize("n,refine", [(5000, 1), (5000, 0), (20_001, 1)])
+def test_pinned_input_zero_copy_agrees(n, refine):
+    """one-step host call with page-locked input AND output: u is read over
+    the link inside the level-0 S1 kernel (zero-copy input) -- bitwise equal
+    to a pageable input (staged copy) and to the device-resident path"""
+    import torch
+    from paper_1912_03312_b200 import _native, rexi_prepare
+    sysm, ap = _system(n), _approx(16)
+    u = np.exp(1j * np.arange(n) * 0.01) * (1 + 0.1 * np.cos(np.arange(n)))
+    stp = rexi_prepare(sysm, ap, 1e-3, sr_value=1.0, override_admissibility=True, refine=refine)
+    p = stp.plans[0]
+    u_pin = _native.host_empty(u.shape)
+    u_pin[:] = u
+    zc = p.step_host(u_pin, 1)                       # pinned in, pinned out: zero-copy both ways
+    staged = p.step_host(u.copy(), 1)                # pageable in
+    ud = torch.from_numpy(u).cuda()
+    out = torch.empty_like(ud)
+    p.step_device(ud.data_ptr(), out.data_ptr(), 1)
+    assert np.array_equal(zc, staged)
+    assert np.array_equal(zc, out.cpu().numpy())
+    ref = _scipy_step(sysm, ap, 1e-3, u)
+    assert np.linalg.norm(zc - ref) <= 1e-8 * np.linalg.norm(ref)
+    two = p.step_host(u_pin, 2)                      # multi-step call (staged input, graphs)
+    assert np.array_equal(two, p.step_host(zc, 1))
+    stp.close()
