@@ -355,7 +355,9 @@ def main():
         stp.close()
         e2e = {"value": ke / dt, "unit": UNIT, "h2d_bytes_per_step": 16 * n,
                "d2h_bytes_per_step": 16 * n, "api": "paper_1912_03312_b200.rexi_step(numpy)",
-               "timing": "host wall clock around synchronous calls"}
+               "timing": "host wall clock around synchronous calls",
+               "transfer": "page-locked numpy buffers: the state crosses PCIe every step, read inside the "
+                           "first kernel (1D) or copied in (COCG), and written by the last kernel"}
     else:
         # multi-GPU public API (distributed.ShardedStepper): every rank holds the
         # state on the host (pinned), copies it in, steps its shard (all-gather
