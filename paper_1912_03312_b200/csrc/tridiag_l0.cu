@@ -41,6 +41,7 @@ struct L0Args {
     int64_t nout;         // real n (level 0 is padded to a multiple of M)
     int acc_add;
     int final_out;
+    int64_t pf_dist;      // K2: L2-prefetch the tile of CTA blockIdx.x + pf_dist
     const c128 *u;        // S1: state u (device or mapped page-locked host memory)
     c128 *rhs_out;        // S1: rhs = iBu of the CTA's rows -> rhs0 for K2 / S3ACC
 };
@@ -487,6 +488,26 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
     const L0Layout l = carve(smem, a.S.kp, M, flags);
     const Ctx c = make_ctx(a, M);
     l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, flags & ~ST_TILE2);
+#ifndef K2_PF
+#define K2_PF 1
+#endif
+    // K2 is latency-bound (FP64 dependency chains at 3 CTAs/SM): a CTA's
+    // start waits ~1.5 us for its bulk copies.  Warm L2 with the tile of the
+    // CTA that will take this slot about one residency-wave later.
+    if (K2_PF && threadIdx.x == 0 && a.pf_dist > 0) {
+        const int64_t nb = (int64_t)blockIdx.x + a.pf_dist;
+        const int64_t r0 = nb * l.T;
+        if (r0 < a.L.n) {
+            const int64_t r1 = min(r0 + (int64_t)l.T, a.L.n);
+            bulk_prefetch_l2(a.L.invd + r0 * l.kp, (uint32_t)((r1 - r0) * l.kp * sizeof(c128)));
+            const uint32_t rb8 = (uint32_t)(l.Tp * 8);
+            bulk_prefetch_l2(a.rhs0 + r0, (uint32_t)(l.Tp * 16));
+            const double *rows[9] = {a.z.ta_sub, a.z.ta_sub_im, a.z.b_sub, a.z.ta_sup, a.z.ta_sup_im,
+                                     a.z.b_sup, a.z.ta_dia, a.z.ta_dia_im, a.z.b_dia};
+#pragma unroll
+            for (int q = 0; q < 9; ++q) bulk_prefetch_l2(rows[q] + r0, rb8);
+        }
+    }
     c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
     if (c.active) {
         xs = a.X1[c.p * c.kp + c.j];
@@ -743,6 +764,13 @@ cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
     a.nout = nout;
     a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0; a.X1 = X1; a.acc = acc; a.rres_out = rres;
     a.acc_add = 0; a.final_out = 0;
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        a.pf_dist = (int64_t)sms * K2_MINB;   // one residency wave ahead
+        if (const char *e = getenv("REXI_K2_PF")) a.pf_dist = (int64_t)(atof(e) * sms * K2_MINB);
+    }
     if (exact_residual) return launch_l0(k_l0_k2<TRI_M, true>, a, ST_RHS | ST_DIA | ST_TILE2, st);
     return launch_l0(k_l0_k2<TRI_M, false>, a, ST_RHS | ST_DIA | ST_TILE2, st);
 }
