@@ -23,6 +23,19 @@ __device__ __forceinline__ c128 crcp(c128 d) {
 }
 __device__ __forceinline__ double cabs2(c128 a) { return fma(a.x, a.x, a.y * a.y); }
 
+// complex64 helpers (the level-0 correction solve of the refined 1D step)
+typedef float2 c64;
+__device__ __forceinline__ c64 c64mk(float r, float i) { return make_float2(r, i); }
+__device__ __forceinline__ c64 to_c64(c128 a) { return make_float2(__double2float_rn(a.x), __double2float_rn(a.y)); }
+__device__ __forceinline__ c128 to_c128(c64 a) { return make_double2((double)a.x, (double)a.y); }
+__device__ __forceinline__ c64 fmul(c64 a, c64 b) {
+    return c64mk(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a - b*c
+__device__ __forceinline__ c64 ffnma(c64 a, c64 b, c64 c) {
+    return c64mk(fmaf(-b.x, c.x, fmaf(b.y, c.y, a.x)), fmaf(-b.x, c.y, fmaf(-b.y, c.x, a.y)));
+}
+
 // Shifted-operator entry with the reference's rounding (integrate.py:171):
 // tau*A - (1j*sigma)*B  ->  re = fl(fl(tau*a) + fl(Im(sigma)*b)),  im = -fl(Re(sigma)*b)
 // ta = fl(tau*a) is precomputed on the host side of the plan; no FMA contraction here.

@@ -28,6 +28,8 @@ struct TriState {
     std::vector<LevelDev> lv;     // device pointers, one per level (last = top)
     L0Dev z{};
     c128 *rhs0 = nullptr, *rres = nullptr;
+    c64 *inv32 = nullptr;         // refinement, TMA path: level-0 inverse pivots as complex64
+    c64 *rres32 = nullptr;        // refinement, TMA path: complex64 residual (aliases rres)
     double *acc = nullptr;
     bool complex_a = false;       // A has an imaginary part: K2 keeps every residual product error-free
 };
@@ -320,6 +322,13 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
         }
     }
     plan->min_pivot_ratio = worst;
+    if (plan->refine > 0 && l0v2_supported(kp)) {
+        // the level-0 correction solve (K3) runs in complex64 (tridiag_l0.cu)
+        DALLOC(T.inv32, (size_t)n0 * kp);
+        CK(launch_to_c64(T.lv[0].invd, T.inv32, n0 * kp, plan->stream));
+        T.rres32 = reinterpret_cast<c64 *>(T.rres);
+        CK(cudaStreamSynchronize(plan->stream));
+    }
     return REXI_OK;
 }
 
@@ -406,12 +415,12 @@ int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
     }
     {
         ProfScope ps(plan, "l0_k2");
-        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres, T.n, T.complex_a, st));
+        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres32, T.n, T.complex_a, st));
     }
     rc = tri_mid(plan, true);
     if (rc) return rc;
     ProfScope ps(plan, "l0_k3");
-    CK(l0_launch_k3(T.z, T.lv[0], plan->S, T.lv[1].X, T.rres, T.acc, uout, T.n, st));
+    CK(l0_launch_k3(T.z, T.lv[0], plan->S, T.lv[1].X, T.inv32, T.rres32, T.acc, uout, T.n, st));
     return REXI_OK;
 }
 

@@ -34,8 +34,9 @@ struct L0Args {
     ShiftDev S;
     const c128 *rhs0;     // [n (+pad)]
     const c128 *X1;       // next-level solution [P][kp]
-    const c128 *rres_in;  // K3
-    c128 *rres_out;       // K2
+    const c64 *rres_in;   // K3: interior residuals, complex64
+    c64 *rres_out;        // K2
+    const c64 *inv32;     // K3: level-0 inverse pivots rounded to complex64
     double *acc;          // dd partial SoA 4*nout
     c128 *uout;
     int64_t nout;         // real n (level 0 is padded to a multiple of M)
@@ -57,7 +58,7 @@ struct RowView {
     __device__ __forceinline__ c128 sup(int lr, c128 sg) const { return form_entry(ur[lr], ui[lr], ub[lr], sg); }
 };
 
-enum { ST_RHS = 1, ST_DIA = 2, ST_TILE2 = 4, ST_BDIA = 8 };
+enum { ST_RHS = 1, ST_DIA = 2, ST_TILE2 = 4, ST_BDIA = 8, ST_T32 = 16 };   // ST_T32: t0 holds complex64
 
 struct L0Layout {
     int kp, T, Tp;
@@ -72,7 +73,7 @@ __device__ __forceinline__ L0Layout carve(unsigned char *smem, int kp, int M, in
     l.Tp = l.T + L0_ROWPAD;
     unsigned char *p = smem + 128;
     l.t0 = reinterpret_cast<c128 *>(p);
-    p += (size_t)l.T * kp * sizeof(c128);
+    p += (size_t)l.T * kp * ((flags & ST_T32) ? sizeof(c64) : sizeof(c128));
     l.t1 = nullptr;
     if (flags & ST_TILE2) {
         l.t1 = reinterpret_cast<c128 *>(p);
@@ -95,7 +96,7 @@ __device__ __forceinline__ L0Layout carve(unsigned char *smem, int kp, int M, in
 
 __host__ __device__ inline size_t l0_smem_bytes(int kp, int M, int flags) {
     size_t T = (size_t)(L0_NT / kp) * M, Tp = T + L0_ROWPAD;
-    size_t b = 128 + T * kp * 16 * ((flags & ST_TILE2) ? 2 : 1);
+    size_t b = 128 + T * kp * ((flags & ST_T32) ? 8 : 16) + ((flags & ST_TILE2) ? T * kp * 16 : 0);
     if (flags & ST_RHS) b += Tp * 16;
     b += Tp * 8 * ((flags & ST_DIA) ? 9 : (flags & ST_BDIA) ? 7 : 6);
     return b;
@@ -103,7 +104,7 @@ __host__ __device__ inline size_t l0_smem_bytes(int kp, int M, int flags) {
 
 // one thread: init the mbarrier, then issue every bulk copy of this CTA
 __device__ __forceinline__ void l0_stage(unsigned char *smem, const L0Layout &l, const L0Args &a,
-                                         const c128 *g_t0, const c128 *g_t1, int64_t row0, int flags) {
+                                         const void *g_t0, const c128 *g_t1, int64_t row0, int flags) {
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
@@ -113,12 +114,14 @@ __device__ __forceinline__ void l0_stage(unsigned char *smem, const L0Layout &l,
     if (threadIdx.x == 0) {
         const int64_t n = a.L.n;
         const int64_t row1 = min(row0 + (int64_t)l.T, n);
+        const size_t esz = (flags & ST_T32) ? sizeof(c64) : sizeof(c128);
         const uint32_t tb = (uint32_t)((row1 - row0) * l.kp * sizeof(c128));
+        const uint32_t tb0 = (uint32_t)((row1 - row0) * l.kp * esz);
         const uint32_t rb8 = (uint32_t)(l.Tp * 8), rb16 = (uint32_t)(l.Tp * 16);
-        uint32_t total = tb * ((flags & ST_TILE2) ? 2 : 1) + ((flags & ST_RHS) ? rb16 : 0) +
+        uint32_t total = tb0 + ((flags & ST_TILE2) ? tb : 0) + ((flags & ST_RHS) ? rb16 : 0) +
                          rb8 * ((flags & ST_DIA) ? 9 : (flags & ST_BDIA) ? 7 : 6);
         mbar_expect_tx(bar, total);
-        bulk_g2s(l.t0, g_t0 + row0 * l.kp, tb, bar);
+        bulk_g2s(l.t0, reinterpret_cast<const unsigned char *>(g_t0) + (size_t)row0 * l.kp * esz, tb0, bar);
         if (flags & ST_TILE2) bulk_g2s(l.t1, g_t1 + row0 * l.kp, tb, bar);
         if (flags & ST_RHS) bulk_g2s((void *)l.rv.rhs, a.rhs0 + row0, rb16, bar);
         bulk_g2s((void *)l.rv.sr, a.z.ta_sub + row0, rb8, bar);
@@ -180,8 +183,11 @@ __device__ __forceinline__ c128 pick_last(const c128 (&y)[M], int cnt) {
 
 // beta-weighted sum over the kp lanes of every tile row (fixed order, fp64
 // products accumulated with error-free TwoSum, lanes combined in dd)
-template <int M>
-__device__ __forceinline__ void reduce_rows(const c128 *tile, const L0Args &a, int64_t row0) {
+__device__ __forceinline__ c128 tile_c128(c128 v) { return v; }
+__device__ __forceinline__ c128 tile_c128(c64 v) { return to_c128(v); }
+
+template <int M, typename TT = c128>
+__device__ __forceinline__ void reduce_rows(const TT *tile, const L0Args &a, int64_t row0) {
     const int kp = a.S.kp;
     const int rows = (L0_NT / kp) * M;
     const int tpr = L0_NT / rows > 0 ? L0_NT / rows : 1;
@@ -191,7 +197,7 @@ __device__ __forceinline__ void reduce_rows(const c128 *tile, const L0Args &a, i
         ddacc re = {0.0, 0.0}, im = {0.0, 0.0};
         for (int jj = sub; jj < kp; jj += tpr) {
             const c128 b = a.S.beta[jj];
-            const c128 x = tile[r * kp + jj];
+            const c128 x = tile_c128(tile[r * kp + jj]);
             ddacc_add(re, fma(b.x, x.x, -b.y * x.y));
             ddacc_add(im, fma(b.x, x.y, b.y * x.x));
         }
@@ -456,9 +462,12 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
         dot2_sub<EXACT>(re, im, SYM ? esub : rv.sub(lr, c.sg), xm);
         dot2_sub<EXACT>(re, im, rv.dia(lr, c.sg), x0);
         dot2_sub<EXACT>(re, im, eup, xp);
-        const c128 r = cmk(__dadd_rn(re.hi, re.lo), __dadd_rn(im.hi, im.lo));
-        a.rres_out[(c.base + q) * kp + j] = r;
-        tc[(q - 1) * kp] = r;
+        // the correction is solved to ~1e-5 relative (it only has to shrink an
+        // error that is already ~1e-13 of x): its rhs is stored as complex64,
+        // and the correction's S1 here uses the same rounded values as K3's S3
+        const c64 r32 = to_c64(cmk(__dadd_rn(re.hi, re.lo), __dadd_rn(im.hi, im.lo)));
+        a.rres_out[(c.base + q) * kp + j] = r32;
+        tc[(q - 1) * kp] = to_c128(r32);
         xm = x0;
         x0 = xp;
         esub = eup;
@@ -531,23 +540,26 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
 
 // ---------------------------------------------------------------------------
 // K3 (refine): correction solve from the stored residual, acc += sum(beta dx).
-// Only the inverse pivots are staged (one 32-KB tile); the residual rows go
-// straight into the sweep registers (loads issued before the mbarrier wait,
-// so they overlap the bulk copy) and dx overwrites the consumed pivots for
-// the lane sum -- half the shared memory of a two-tile CTA, so more CTAs
-// (sweep chains) per SM.
+// The correction only has to shrink an error that is already ~1e-13 of x, so
+// its level-0 part runs in complex64: the inverse pivots are staged from their
+// complex64 copy (one 16-KB tile), the complex64 residual rows go straight
+// into the sweep registers (loads issued before the mbarrier wait, so they
+// overlap the bulk copy), entries are formed with the reference's fp64
+// rounding and then rounded, and dx (complex64) overwrites the consumed
+// pivots for the lane sum, which is accumulated in double-double as before.
+// Half the bytes of an fp64 correction (16 instead of 32 per row-shift).
 // ---------------------------------------------------------------------------
 #ifndef K3_MINB
-#define K3_MINB 5
+#define K3_MINB 8   // 93 -> 64 registers: 8 CTAs/SM (swept: scripts/tune_k3.sh)
 #endif
 template <int M>
 __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const L0Layout l = carve(smem, a.S.kp, M, 0);
+    const L0Layout l = carve(smem, a.S.kp, M, ST_T32);
     const Ctx c = make_ctx(a, M);
-    l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, 0);
+    l0_stage(smem, l, a, a.inv32, nullptr, c.row0, ST_T32);
     const int kp = c.kp;
-    c128 y[M];
+    c64 y[M];
     c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
     if (c.active) {
         xs = a.X1[c.p * kp + c.j];
@@ -556,19 +568,26 @@ __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
         for (int q = 1; q < M; ++q) y[q] = a.rres_in[(c.base + q) * kp + c.j];
     }
     mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
-    c128 *ti = l.t0 + (size_t)c.lr0 * kp + c.j;
+    c64 *ti = reinterpret_cast<c64 *>(l.t0) + (size_t)c.lr0 * kp + c.j;
     if (c.active) {
         const RowView &rv = l.rv;
-        y[0] = xs;
-        sweep_fwd<M, true>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, [&](int q) { return y[q]; });
-        sweep_bwd<M, true>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, xn, [&](int q, c128 x) { ti[q * kp] = x; });
-        ti[0] = xs;
+        y[0] = to_c64(xs);
+#pragma unroll
+        for (int q = 1; q < M; ++q)
+            y[q] = fmul(ti[q * kp], ffnma(y[q], to_c64(rv.sub(c.lr0 + q, c.sg)), y[q - 1]));
+        c64 xnext = to_c64(xn);
+#pragma unroll
+        for (int q = M - 1; q >= 1; --q) {
+            xnext = ffnma(y[q], ti[q * kp], fmul(to_c64(rv.sup(c.lr0 + q, c.sg)), xnext));
+            ti[q * kp] = xnext;
+        }
+        ti[0] = to_c64(xs);
     } else {
 #pragma unroll
-        for (int q = 0; q < M; ++q) ti[q * kp] = cmk(0.0, 0.0);
+        for (int q = 0; q < M; ++q) ti[q * kp] = c64mk(0.f, 0.f);
     }
     __syncthreads();
-    reduce_rows<M>(l.t0, a, c.row0);
+    reduce_rows<M, c64>(reinterpret_cast<const c64 *>(l.t0), a, c.row0);
 }
 
 // ---------------------------------------------------------------------------
@@ -728,6 +747,16 @@ static cudaError_t launch_l0(K kern, const L0Args &a, int flags, cudaStream_t st
     return cudaGetLastError();
 }
 
+__global__ void k_to_c64(const c128 *__restrict__ src, c64 *__restrict__ dst, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = to_c64(src[i]);
+}
+
+cudaError_t launch_to_c64(const c128 *src, c64 *dst, int64_t n, cudaStream_t st) {
+    k_to_c64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, dst, n);
+    return cudaGetLastError();
+}
+
 bool l0v2_supported(int kp) { return kp <= L0_NT; }
 int64_t l0_row_padding() { return (int64_t)L0_NT * TRI_M + 2 * L0_ROWPAD; }
 
@@ -758,7 +787,7 @@ cudaError_t l0_launch_s3acc(const L0Dev &z, const LevelDev &L, const ShiftDev &S
 }
 
 cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
-                         const c128 *X1, double *acc, c128 *rres, int64_t nout, bool exact_residual,
+                         const c128 *X1, double *acc, c64 *rres, int64_t nout, bool exact_residual,
                          cudaStream_t st) {
     L0Args a{};
     a.nout = nout;
@@ -776,12 +805,13 @@ cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
 }
 
 cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *X1,
-                         const c128 *rres, double *acc, c128 *uout, int64_t nout, cudaStream_t st) {
+                         const c64 *inv32, const c64 *rres, double *acc, c128 *uout, int64_t nout,
+                         cudaStream_t st) {
     L0Args a{};
     a.nout = nout;
-    a.z = z; a.L = L; a.S = S; a.X1 = X1; a.rres_in = rres; a.acc = acc; a.uout = uout;
+    a.z = z; a.L = L; a.S = S; a.X1 = X1; a.inv32 = inv32; a.rres_in = rres; a.acc = acc; a.uout = uout;
     a.acc_add = 1; a.final_out = uout != nullptr;
-    return launch_l0(k_l0_k3<TRI_M>, a, 0, st);
+    return launch_l0(k_l0_k3<TRI_M>, a, ST_T32, st);
 }
 
 }  // namespace rexi

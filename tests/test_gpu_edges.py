@@ -113,8 +113,16 @@ def test_pinned_input_zero_copy_agrees(n, refine):
     p.step_device(ud.data_ptr(), out.data_ptr(), 1)
     assert np.array_equal(zc, staged)
     assert np.array_equal(zc, out.cpu().numpy())
-    ref = _scipy_step(sysm, ap, 1e-3, u)
-    assert np.linalg.norm(zc - ref) <= 1e-8 * np.linalg.norm(ref)
+    # accuracy against the truth oracle (double-double refined solves): the
+    # flagship pole weights reach 1.7e7, so fp64 direct solves (scipy, the
+    # reference, refine=0) sit 2e-8..2e-7 from truth here; the refined step
+    # reaches ~1e-10, the unrefined one must stay within 10x the reference's
+    # own distance
+    from oracle.oracle import OraclePlan, rel_l2
+    orc = OraclePlan(sysm, ap, 1e-3)
+    truth = orc.step(u, "truth")
+    floor = rel_l2(orc.step(u, "reference"), truth)
+    assert rel_l2(zc, truth) <= (1e-9 if refine else 10 * floor + 1e-9)
     two = p.step_host(u_pin, 2)                      # multi-step call (staged input, graphs)
     assert np.array_equal(two, p.step_host(zc, 1))
     stp.close()
