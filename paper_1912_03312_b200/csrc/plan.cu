@@ -701,16 +701,20 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
         return nullptr;
     };
     c128 *zc_out = nullptr;
-    const bool zc_ok = mem == REXI_MEM_HOST && n_steps > 0 && !(plan->persist_cs > 0 && !plan->prof) &&
-                       !getenv("REXI_NO_ZEROCOPY");
+    const bool persist = n_steps > 0 && plan->persist_cs > 0 && !plan->prof;
+    const bool zc_ok = mem == REXI_MEM_HOST && n_steps > 0 && !getenv("REXI_NO_ZEROCOPY");
     if (zc_ok) zc_out = mapped(u_out);
     // zero-copy input: a one-step host call of a TMA-path 1D plan reads u from
     // page-locked host memory inside the level-0 S1 kernel (which forms rhs =
     // iBu itself), so the host->device transfer overlaps that kernel's HBM
     // traffic instead of preceding it
     const c128 *zc_in = nullptr;
-    if (zc_ok && zc_out && n_steps == 1 && plan->solver == REXI_SOLVER_TRIDIAG && l0v2_supported(plan->kp))
+    if (zc_ok && zc_out && (persist || (n_steps == 1 && plan->solver == REXI_SOLVER_TRIDIAG &&
+                                        l0v2_supported(plan->kp))))
         zc_in = mapped(u_in);
+    // the persistent loop reads its input once and writes its last state
+    // once: both straight over the link when the host buffers are page-locked
+    if (persist && !zc_in) zc_out = nullptr;
     const c128 *src;
     if (zc_in) {
         src = zc_in;
@@ -725,7 +729,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     if (n_steps > 0 && plan->persist_cs > 0 && !plan->prof) {
         TriState &T = plan->tri;
         CK(persist_launch(T.z, T.lv.data(), (int)T.lv.size(), plan->S, n, src, plan->pbuf[0], plan->pbuf[1],
-                          nullptr, n_steps, plan->persist_cs, st));
+                          nullptr, n_steps, plan->persist_cs, st, zc_out));
         plan->launches += 1;
         src = plan->pbuf[(n_steps - 1) & 1];
         n_steps = -n_steps;    // steps done; restored below

@@ -36,7 +36,7 @@ constexpr int PS_MAXLV = 8;
 int persist_cluster_size(const LevelDev *lv, int nl, int kp);
 cudaError_t persist_launch(const L0Dev &z, const LevelDev *lv, int nl, const ShiftDev &S, int64_t n,
                            const c128 *u_in, c128 *ua, c128 *ub, c128 *snaps, int n_steps, int csize,
-                           cudaStream_t st);
+                           cudaStream_t st, c128 *final_out = nullptr);
 
 inline int64_t lv_tma_ctas(int64_t n, int kp) {   // grid of lv_launch_tma
     const int64_t rows = (int64_t)(128 / kp) * TRI_M;

@@ -51,6 +51,7 @@ struct PersistArgs {
     const c128 *u_in;
     c128 *ua, *ub;          // state ping-pong [n]
     c128 *snaps;            // optional [n_steps][n]: state after every step
+    c128 *final_out;        // optional: the last state also goes here (mapped page-locked host output)
     int n_steps;
     unsigned long long *tstamp;   // optional (REXI_PERSIST_TRACE): %globaltimer per phase, steps 0-2
 };
@@ -434,6 +435,7 @@ __global__ void __launch_bounds__(PS_NT) k_persist(const __grid_constant__ Persi
                     const c128 v = row_sum(sl.tile + (size_t)r * kp, a.S, tpr);
                     un[row] = v;
                     if (a.snaps) a.snaps[(int64_t)step * a.n + row] = v;
+                    if (a.final_out && step == a.n_steps - 1) a.final_out[row] = v;
                 }
             }
         }
@@ -483,7 +485,7 @@ int persist_cluster_size(const LevelDev *lv, int nl, int kp) {
 
 cudaError_t persist_launch(const L0Dev &z, const LevelDev *lv, int nl, const ShiftDev &S, int64_t n,
                            const c128 *u_in, c128 *ua, c128 *ub, c128 *snaps, int n_steps, int csize,
-                           cudaStream_t st) {
+                           cudaStream_t st, c128 *final_out) {
     if (nl < 2 || nl > PS_MAXLV) return cudaErrorInvalidValue;
     PersistArgs a{};
     a.z = z;
@@ -496,6 +498,7 @@ cudaError_t persist_launch(const L0Dev &z, const LevelDev *lv, int nl, const Shi
     a.ua = ua;
     a.ub = ub;
     a.snaps = snaps;
+    a.final_out = final_out;
     a.n_steps = n_steps;
     static unsigned long long *tbuf = nullptr;
     const bool trace = getenv("REXI_PERSIST_TRACE") != nullptr;
@@ -503,6 +506,7 @@ cudaError_t persist_launch(const L0Dev &z, const LevelDev *lv, int nl, const Shi
     if (trace) cudaMemsetAsync(tbuf, 0, 64 * sizeof(unsigned long long), st);
     a.tstamp = trace ? tbuf : nullptr;
     const size_t sm = persist_smem_bytes(lv, nl, S.kp, csize);
+    // (set on every launch: persist_cluster_size probes other sizes on the same function)
     cudaFuncSetAttribute(k_persist, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(k_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaLaunchConfig_t cfg = {};

@@ -93,3 +93,26 @@ def test_observer_states_equal_step_loop(name, refine):
     assert np.array_equal(final, u)
     assert len({id(s[2]) for s in seen}) == nst
     stp.close()
+
+
+@pytest.mark.parametrize("steps", [1, 3])
+def test_persistent_pinned_buffers_zero_copy(steps):
+    """page-locked input and output: the persistent loop reads u and writes
+    its last state over the link (no staging copies) -- bitwise equal to
+    pageable buffers and to device-resident stepping"""
+    import torch
+    from paper_1912_03312_b200 import _native, rexi_prepare
+    d, sysm, ap = load_golden("cfg1_k32")
+    stp = rexi_prepare(sysm, ap, float(d["tau"]), sr_value=float(d["sr"]), override_admissibility=True)
+    p = stp.plans[0]
+    assert p.info.persistent >= 4
+    u_pin = _native.host_empty(d["u0"].shape)
+    u_pin[:] = d["u0"]
+    zc = p.step_host(u_pin, steps)
+    staged = p.step_host(np.array(d["u0"]), steps)
+    ud = torch.from_numpy(np.array(d["u0"])).cuda()
+    out = torch.empty_like(ud)
+    p.step_device(ud.data_ptr(), out.data_ptr(), steps)
+    assert np.array_equal(zc, staged)
+    assert np.array_equal(zc, out.cpu().numpy())
+    stp.close()
