@@ -119,7 +119,8 @@ __device__ __forceinline__ c128 rhs_row(double bs, double bd, double bu, const c
 // level-0 block b of the slice (tridiag_l0.cu sweeps on a full block), all
 // operands from shared memory; PHASE 1 -> ypart/lc, PHASE 3 -> tile rows
 template <int PHASE>
-__device__ __forceinline__ void l0_block(const PersistArgs &a, const Slice &sl, int R, int64_t pb0, int b, int j) {
+__device__ __forceinline__ void l0_block(const PersistArgs &a, const Slice &sl, int R, int64_t pb0, int b, int j,
+                                         c128 *yp_out = nullptr, c128 *lc_out = nullptr) {
     constexpr int M = TRI_M;
     const LevelDev &L = a.lv[0];
     const int kp = a.S.kp;
@@ -148,9 +149,10 @@ __device__ __forceinline__ void l0_block(const PersistArgs &a, const Slice &sl, 
         y[q] = xnext;
     }
     if (PHASE == 1) {
-        L.ypart[p * kp + j] = cfnma(sl.rhs[lr0], zentry(sl.zd, R1, 2, lr0, sg), y[1]);
-        if (p + 1 < P) L.lc[(p + 1) * kp + j] = cneg(cmul(zentry(sl.zd, R1, 0, lr0 + M, sg), ylast));
-        if (p == 0) L.lc[j] = cmk(0.0, 0.0);
+        // straight into the level CTA's shared memory (distributed shared memory)
+        yp_out[p * kp + j] = cfnma(sl.rhs[lr0], zentry(sl.zd, R1, 2, lr0, sg), y[1]);
+        if (p + 1 < P) lc_out[(p + 1) * kp + j] = cneg(cmul(zentry(sl.zd, R1, 0, lr0 + M, sg), ylast));
+        if (p == 0) lc_out[j] = cmk(0.0, 0.0);
     } else {
         c128 *tc = sl.tile + (size_t)lr0 * kp + j;
         tc[0] = xs;
@@ -330,14 +332,11 @@ __global__ void __launch_bounds__(PS_NT) k_persist(const __grid_constant__ Persi
     const int R = bc * TRI_M, R1 = R + 1;
     const int64_t r0 = pb0 * TRI_M;
     const Slice sl = carve_slice(smem, bc, kp);
-    c128 *stage_yp = nullptr, *stage_lc = nullptr;
     if (level_cta) {
-        // resident: every reduced level's operands; views = offsets into ps_smem
-        int off = 0;
-        stage_yp = psm() + off;
-        off += (int)(P0 * kp);
-        stage_lc = psm() + off;
-        off += (int)(P0 * kp);
+        // resident: level 0's S1 outputs (written by the slices through
+        // distributed shared memory) at offsets 0 and P0*kp, then every
+        // reduced level's operands; views = offsets into ps_smem
+        int off = 2 * (int)(P0 * kp);
         for (int l = 1; l < nl; ++l) {
             const LevelDev &L = a.lv[l];
             const int ne = (int)(L.n * kp);
@@ -387,6 +386,10 @@ __global__ void __launch_bounds__(PS_NT) k_persist(const __grid_constant__ Persi
         __syncthreads();
     }
     const int tpr = max(1, 128 / ((128 / kp) * TRI_M));   // reduce_rows' threads per row (L0_NT = 128)
+    // the level CTA's staging arrays (offset 0 and P0*kp of its dynamic shared
+    // memory), as seen from this CTA: the slices' S1 writes them directly
+    c128 *rem_yp = cl.map_shared_rank(psm(), 0);
+    c128 *rem_lc = rem_yp + P0 * kp;
     const c128 *u = a.u_in;
     for (int step = 0; step < a.n_steps; ++step) {
         int ts = 0;
@@ -397,17 +400,13 @@ __global__ void __launch_bounds__(PS_NT) k_persist(const __grid_constant__ Persi
             for (int r = threadIdx.x; r <= nb * TRI_M; r += PS_NT)
                 sl.rhs[r] = rhs_row(sl.zd[2 * R1 + r], sl.zd[5 * R1 + r], sl.zd[8 * R1 + r], u, a.n, r0 + r);
             __syncthreads();
-            for (int it = threadIdx.x; it < nb * kp; it += PS_NT) l0_block<1>(a, sl, R, pb0, it / kp, it % kp);
+            for (int it = threadIdx.x; it < nb * kp; it += PS_NT)
+                l0_block<1>(a, sl, R, pb0, it / kp, it % kp, rem_yp, rem_lc);
         }
         cl.sync();
         stamp(a, step, ts);
         // M (level CTA): every reduced level, S1 up, top, S3 down
         if (level_cta) {
-            for (int64_t e = threadIdx.x; e < P0 * kp; e += PS_NT) {
-                stage_yp[e] = a.lv[0].ypart[e];
-                stage_lc[e] = a.lv[0].lc[e];
-            }
-            __syncthreads();
             stamp(a, step, ts);
             for (int l = 1; l <= nl - 2; ++l) {
                 for (int t = threadIdx.x; t < views[l].P * kp; t += PS_NT) lv_block<1>(views[l], t / kp, t % kp, kp);
