@@ -372,7 +372,10 @@ int tri_mid(rexi_plan *plan, bool dd) {
     // faster than the plain kernel even for the few-CTA upper levels)
     const bool tma_ok = T.lv[0].sym && l0v2_supported(plan->kp);
     auto use_tma = [&](size_t) { return tma_ok; };
-    for (size_t l = 1; l + 1 < nl; ++l) {
+    // levels >= lc (one wave of <= 16 CTAs each) run as one cluster launch
+    int ccs = 0;
+    const int lc = tma_ok && !(nl == 2 && dd) ? lv_chain_start(T.lv.data(), (int)nl, plan->kp, &ccs) : 0;
+    for (size_t l = 1; l + 1 < nl && (lc == 0 || (int)l < lc); ++l) {
         ProfScope ps(plan, "s1_lv");
         const bool d = l == 1 && dd;
         if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 1, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
@@ -381,12 +384,15 @@ int tri_mid(rexi_plan *plan, bool dd) {
         else CK(tri_launch_s1(T.z, T.lv[l], plan->S, (int)l, nullptr, nullptr, T.lv[l - 1].ypart,
                               T.lv[l - 1].lc, st));
     }
-    {
+    if (lc > 0) {
+        ProfScope ps(plan, "lv_chain");
+        CK(lv_launch_chain(T.lv.data(), (int)nl, lc, ccs, plan->S, st));
+    } else {
         ProfScope ps(plan, "top");
         if (nl == 2 && dd) CK(tri_launch_top_solve_dd(T.lv[1], plan->S, T.lv[0].ypdd, T.lv[0].lcdd, st));
         else CK(tri_launch_top_solve(T.lv[nl - 1], plan->S, T.lv[nl - 2].ypart, T.lv[nl - 2].lc, st));
     }
-    for (size_t l = nl - 1; l-- > 1;) {
+    for (size_t l = lc > 0 ? (size_t)lc : nl - 1; l-- > 1;) {
         ProfScope ps(plan, "s3_lv");
         const bool d = l == 1 && dd;
         if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 3, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
@@ -882,10 +888,13 @@ int rexi_plan_step_partial(rexi_plan *plan, const rexi_c128 *u_in, double *parti
     if (!plan) return set_err(nullptr, REXI_ERR_INVALID, "null plan");
     CK(cudaSetDevice(plan->device));
     plan->launches = 0;
+    // the step accumulates its double-double partial straight into the
+    // caller's buffer (same SoA layout as the plan's accumulator)
+    double *const acc_saved = plan->tri.acc;
+    plan->tri.acc = partial;
     int rc = plan_step_device(plan, (const c128 *)u_in, nullptr);
+    plan->tri.acc = acc_saved;
     if (rc) return rc == REXI_ERR_NOCONV || rc == REXI_ERR_BREAKDOWN ? set_err(plan, rc, plan->err) : rc;
-    CK(cudaMemcpyAsync(partial, plan->tri.acc, sizeof(double) * 4 * plan->n, cudaMemcpyDeviceToDevice,
-                       plan->stream));
     CK(cudaStreamSynchronize(plan->stream));
     prof_flush(plan);
     if (stats) {

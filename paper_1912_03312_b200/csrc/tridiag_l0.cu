@@ -13,8 +13,15 @@
 // refine = 0:  S1 (reduce) ... levels >= 1 ... S3ACC (solve + beta-sum)
 // refine = 1:  S1 ... K2 (solve + beta-sum + dd residual + correction reduce)
 //              ... levels >= 1 (correction) ... K3 (correction solve + sum)
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+
 #include "tridiag.cuh"
 #include "tridiag_launch.h"
+
+namespace cgr = cooperative_groups;
 
 namespace rexi {
 
@@ -705,6 +712,147 @@ __global__ void __launch_bounds__(L0_NT, LV_MINB) k_lv_tma(const __grid_constant
     t.ypart = a.L.ypart; t.lc = a.L.lc; t.X = a.L.X;
     if (cnt == M - 1) lv_body<M, PHASE, DD, true>(t, b * M, kp, j, p, P, base, cnt);
     else lv_body<M, PHASE, DD, false>(t, b * M, kp, j, p, P, base, cnt);
+}
+
+// ---------------------------------------------------------------------------
+// The small reduced levels in ONE thread-block-cluster launch: S1 up levels
+// l0..nl-2, the top solve, S3 down levels nl-2..l0, separated by cluster
+// barriers instead of kernel boundaries.  Each cluster CTA plays the role of
+// k_lv_tma's CTAs for a level (virtual CTAs rank, rank + CS, ...): the same
+// TMA-staged invd/sup tiles and the same lv_body, so results are bitwise
+// identical to the per-level launches; the top solve repeats k_top_solve.
+// Level data written by one CTA and read by another (ypart/lc, X) are plain
+// global stores/loads ordered by the cluster barrier (release/acquire).
+// ---------------------------------------------------------------------------
+constexpr int CH_MAXLV = 8;
+constexpr int CH_MAXCS = 16;
+
+struct ChainArgs {
+    LevelDev lv[CH_MAXLV];
+    ShiftDev S;
+    int l0, nl;
+};
+
+template <int M, int PHASE>
+__device__ __forceinline__ void chain_level(const LevelDev &L, const LevelDev &Lp, const c128 *Xnext, const ShiftDev &S,
+                                            c128 *tinv, c128 *tsup, uint64_t *bar, uint32_t &phase,
+                                            unsigned rank, unsigned cs) {
+    const int kp = S.kp;
+    const int bpc = L0_NT / kp;
+    const int T = bpc * M;
+    const int b = threadIdx.x / kp, j = threadIdx.x % kp;
+    const int64_t n = L.n, P = L.P;
+    const int64_t G = (n + T - 1) / T;
+    for (int64_t vb = rank; vb < G; vb += cs) {
+        const int64_t row0 = vb * T;
+        if (threadIdx.x == 0) {
+            const int64_t row1 = min(row0 + (int64_t)T, n);
+            const uint32_t tb = (uint32_t)((row1 - row0) * kp * sizeof(c128));
+            mbar_expect_tx(bar, 2 * tb);
+            bulk_g2s(tinv, L.invd + row0 * kp, tb, bar);
+            bulk_g2s(tsup, L.sup + row0 * kp, tb, bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        const int64_t p = vb * bpc + b;
+        if (p < P) {
+            const int64_t base = p * M;
+            const int cnt = (int)min((int64_t)M, n - base) - 1;
+            LvPtrs t;
+            t.inv = tinv + j; t.sup = tsup + j;
+            t.ra = Lp.ypart; t.rb = Lp.lc; t.da = nullptr; t.db = nullptr; t.Xn = Xnext;
+            t.ypart = L.ypart; t.lc = L.lc; t.X = L.X;
+            if (cnt == M - 1) lv_body<M, PHASE, false, true>(t, b * M, kp, j, p, P, base, cnt);
+            else lv_body<M, PHASE, false, false>(t, b * M, kp, j, p, P, base, cnt);
+        }
+        __syncthreads();   // tiles free for the next virtual CTA
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(L0_NT, 1) k_lv_chain(const __grid_constant__ ChainArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    const int kp = a.S.kp;
+    const int T = (L0_NT / kp) * M;
+    c128 *tinv = reinterpret_cast<c128 *>(smem + 128);
+    c128 *tsup = tinv + (size_t)T * kp;
+    auto cl = cgr::this_cluster();
+    const unsigned rank = cl.block_rank(), cs = cl.num_blocks();
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    const LevelDev *lv = a.lv;
+    for (int l = a.l0; l + 1 < a.nl; ++l) {
+        chain_level<M, 1>(lv[l], lv[l - 1], nullptr, a.S, tinv, tsup, bar, phase, rank, cs);
+        cl.sync();
+    }
+    if (rank == 0 && (int)threadIdx.x < kp) {   // k_top_solve's order
+        const LevelDev &Tl = lv[a.nl - 1], &Tp = lv[a.nl - 2];
+        const int j = threadIdx.x;
+        c128 yp = cmk(0.0, 0.0);
+        for (int64_t i = 0; i < Tl.n; ++i) {
+            const c128 d = cadd(Tp.ypart[i * kp + j], Tp.lc[i * kp + j]);
+            const c128 ai = i > 0 ? Tl.sup[(i - 1) * kp + j] : cmk(0.0, 0.0);
+            yp = cmul(Tl.invd[i * kp + j], cfnma(d, ai, yp));
+            Tl.X[i * kp + j] = yp;
+        }
+        c128 xnext = cmk(0.0, 0.0);
+        for (int64_t i = Tl.n - 1; i >= 0; --i) {
+            const c128 xi = cfnma(Tl.X[i * kp + j], Tl.invd[i * kp + j], cmul(Tl.sup[i * kp + j], xnext));
+            Tl.X[i * kp + j] = xi;
+            xnext = xi;
+        }
+    }
+    cl.sync();
+    for (int l = a.nl - 2; l >= a.l0; --l) {
+        chain_level<M, 3>(lv[l], lv[l - 1], lv[l + 1].X, a.S, tinv, tsup, bar, phase, rank, cs);
+        if (l > a.l0) cl.sync();
+    }
+}
+
+// first chained level (0: the plan does not use the chain) and the cluster
+// size: levels >= 2 whose k_lv_tma grid fits one wave of <= 16 CTAs
+int lv_chain_start(const LevelDev *lv, int nl, int kp, int *cs) {
+    if (getenv("REXI_NO_CHAIN") || nl > CH_MAXLV || nl < 4 || !lv[0].sym || kp > L0_NT) return 0;
+    for (int l = 2; l + 1 < nl; ++l) {
+        const int64_t g = lv_tma_ctas(lv[l].n, kp);
+        if (g <= CH_MAXCS) {
+            *cs = (int)std::max<int64_t>(1, g);
+            return l;
+        }
+    }
+    return 0;
+}
+
+cudaError_t lv_launch_chain(const LevelDev *lv, int nl, int l0, int cs, const ShiftDev &S, cudaStream_t st) {
+    ChainArgs a{};
+    for (int l = 0; l < nl; ++l) a.lv[l] = lv[l];
+    a.S = S;
+    a.l0 = l0;
+    a.nl = nl;
+    const int64_t rows = (int64_t)(L0_NT / S.kp) * TRI_M;
+    const size_t smem = 128 + 2 * (size_t)rows * S.kp * sizeof(c128);
+    auto kern = k_lv_chain<TRI_M>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(L0_NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,

@@ -45,6 +45,11 @@ inline int64_t lv_tma_ctas(int64_t n, int kp) {   // grid of lv_launch_tma
 cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,
                           const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st);
 
+// levels l0..top..l0 in one cluster launch (tridiag_l0.cu); lv_chain_start
+// returns the first chained level (0: none) and the cluster size
+int lv_chain_start(const LevelDev *lv, int nl, int kp, int *cs);
+cudaError_t lv_launch_chain(const LevelDev *lv, int nl, int l0, int cs, const ShiftDev &S, cudaStream_t st);
+
 // TMA-fed level-0 kernels (tridiag_l0.cu)
 bool l0v2_supported(int kp);
 int64_t l0_row_padding();
