@@ -51,6 +51,7 @@ struct L0Args {
     int final_out;
     int64_t pf_dist;      // K2: L2-prefetch the tile of CTA blockIdx.x + pf_dist
     const c128 *u;        // S1: state u (device or mapped page-locked host memory)
+    int u_bulk;           // S1: u is 16-B aligned -> staged by one bulk copy
     c128 *rhs_out;        // S1: rhs = iBu of the CTA's rows -> rhs0 for K2 / S3ACC
 };
 
@@ -322,15 +323,37 @@ __global__ void __launch_bounds__(L0_NT, S1_MINB) k_l0_s1(L0Args a) {
     constexpr int FL = ST_RHS | ST_BDIA;
     const L0Layout l = carve(smem, a.S.kp, M, FL);
     const Ctx c = make_ctx(a, M);
+    uint64_t *bar_u = reinterpret_cast<uint64_t *>(smem) + 1;
+    if (threadIdx.x == 0 && a.u_bulk) mbar_init(bar_u, 1);   // fenced with l0_stage's barrier init
     l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, FL & ~ST_RHS);
-    // u rows row0-1 .. row0+T (loads in flight under the bulk copies)
+    // u rows row0-1 .. row0+T, slots outside [0, n) zero
     c128 *su = reinterpret_cast<c128 *>(smem + ((l0_smem_bytes(a.S.kp, M, FL) + 15) & ~(size_t)15));   // T+2 slots after the carve
     const int64_t n = a.nout;
-    for (int t = threadIdx.x; t < l.T + 2; t += L0_NT) {
-        const int64_t i = c.row0 - 1 + t;
-        su[t] = (i >= 0 && i < n) ? a.u[i] : cmk(0.0, 0.0);
+    const int64_t i0 = max(c.row0 - 1, (int64_t)0), i1 = min(c.row0 + (int64_t)l.T + 1, n);
+    if (a.u_bulk) {
+        // one bulk copy (also from mapped page-locked host memory: larger link
+        // transactions than per-thread loads)
+        if (threadIdx.x == 0) {
+            if (i1 > i0) {
+                const uint32_t ub = (uint32_t)((i1 - i0) * sizeof(c128));
+                mbar_expect_tx(bar_u, ub);
+                bulk_g2s(su + (i0 - (c.row0 - 1)), a.u + i0, ub, bar_u);
+            } else {
+                mbar_arrive(bar_u);
+            }
+        }
+        for (int t = threadIdx.x; t < l.T + 2; t += L0_NT) {
+            const int64_t i = c.row0 - 1 + t;
+            if (i < i0 || i >= i1) su[t] = cmk(0.0, 0.0);
+        }
+    } else {
+        for (int t = threadIdx.x; t < l.T + 2; t += L0_NT) {
+            const int64_t i = c.row0 - 1 + t;
+            su[t] = (i >= 0 && i < n) ? a.u[i] : cmk(0.0, 0.0);
+        }
     }
     mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
+    if (a.u_bulk) mbar_wait(bar_u, 0);
     __syncthreads();
     c128 *rhs = const_cast<c128 *>(l.rv.rhs);
     for (int t = threadIdx.x; t < l.T; t += L0_NT) {
@@ -912,6 +935,7 @@ cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
                          int64_t nout, cudaStream_t st) {
     L0Args a{};
     a.z = z; a.L = L; a.S = S; a.u = u; a.rhs_out = rhs0; a.nout = nout;
+    a.u_bulk = ((uintptr_t)u & 15) == 0 && !getenv("REXI_S1_NO_BULK");
     // + T+2 u rows after the staged rhs rows
     const size_t extra = 16 + ((size_t)(L0_NT / S.kp) * TRI_M + 2) * sizeof(c128);
     const int kp = S.kp;
