@@ -143,12 +143,17 @@ int rexi_plan_run(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *snaps, int3
 
 /* One step for this plan's shard of shifts, leaving the double-double
  * partial sum sum_{j in shard} beta_j x_j in partial (device, 4*n doubles:
- * re_hi[n], re_lo[n], im_hi[n], im_lo[n]).  u_in is a device pointer. */
+ * re_hi[n], re_lo[n], im_hi[n], im_lo[n]).  u_in is a device pointer.
+ * On a caller-provided stream (desc.stream) a 1D plan's call is
+ * stream-ordered: it returns once the step is enqueued, so the caller's
+ * collective on that stream follows without a host round trip.  Otherwise
+ * (own stream, COCG) it returns after the step completes. */
 int rexi_plan_step_partial(rexi_plan *plan, const rexi_c128 *u_in, double *partial,
                            rexi_stats *stats);
 
 /* out = round(sum_{g=0}^{G-1} partials[g]) in fixed g order (device pointers,
- * partials laid out as G consecutive 4*n blocks).  stream may be NULL. */
+ * partials laid out as G consecutive 4*n blocks).  stream NULL: the legacy
+ * stream, returns when done; otherwise stream-ordered on that stream. */
 int rexi_combine_partials(const double *partials, int32_t g, int64_t n, rexi_c128 *out,
                           void *stream);
 

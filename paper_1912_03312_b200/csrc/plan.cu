@@ -895,7 +895,10 @@ int rexi_plan_step_partial(rexi_plan *plan, const rexi_c128 *u_in, double *parti
     int rc = plan_step_device(plan, (const c128 *)u_in, nullptr);
     plan->tri.acc = acc_saved;
     if (rc) return rc == REXI_ERR_NOCONV || rc == REXI_ERR_BREAKDOWN ? set_err(plan, rc, plan->err) : rc;
-    CK(cudaStreamSynchronize(plan->stream));
+    // stream-ordered on a caller's stream (1D: nothing to check on the host;
+    // COCG has synchronised for its convergence checks already)
+    if (plan->own_stream || plan->prof || plan->solver != REXI_SOLVER_TRIDIAG) CK(cudaStreamSynchronize(plan->stream));
+    else CK(cudaGetLastError());
     prof_flush(plan);
     if (stats) {
         memset(stats, 0, sizeof *stats);
@@ -912,7 +915,7 @@ int rexi_plan_step_partial(rexi_plan *plan, const rexi_c128 *u_in, double *parti
 int rexi_combine_partials(const double *partials, int32_t g, int64_t n, rexi_c128 *out, void *stream) {
     rexi_plan *plan = nullptr;
     CK(launch_combine(partials, g, n, (c128 *)out, (cudaStream_t)stream));
-    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    if (!stream) CK(cudaStreamSynchronize((cudaStream_t)stream));
     return REXI_OK;
 }
 
