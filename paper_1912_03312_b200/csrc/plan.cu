@@ -72,6 +72,9 @@ struct rexi_plan {
     int persist_cs = 0;                               // >0: small 1D plan, all steps in one cluster launch
     c128 *pbuf[2] = {nullptr, nullptr};               // its state ping-pong
     int64_t graph_kernels = 0;
+    // 1D shard step (rexi_plan_step_partial) replays, keyed by (u_in, partial)
+    struct PartGraph { const void *u, *part; cudaGraphExec_t exec; int64_t kernels; };
+    std::vector<PartGraph> part_graphs;
     struct Hook : rexi::ProfHook {
         rexi_plan *p = nullptr;
         cudaEvent_t a = nullptr;
@@ -506,6 +509,7 @@ int rexi_plan_destroy(rexi_plan *plan) {
     for (auto &r : plan->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto &g : plan->graph)
         if (g) cudaGraphExecDestroy(g);
+    for (auto &g : plan->part_graphs) cudaGraphExecDestroy(g.exec);
     for (auto e : plan->pool) cudaEventDestroy(e);
     if (plan->own_stream && plan->stream) cudaStreamDestroy(plan->stream);
     delete plan;
@@ -892,8 +896,51 @@ int rexi_plan_step_partial(rexi_plan *plan, const rexi_c128 *u_in, double *parti
     // caller's buffer (same SoA layout as the plan's accumulator)
     double *const acc_saved = plan->tri.acc;
     plan->tri.acc = partial;
-    int rc = plan_step_device(plan, (const c128 *)u_in, nullptr);
-    plan->tri.acc = acc_saved;
+    int rc = REXI_OK;
+    if (plan->solver == REXI_SOLVER_TRIDIAG && !plan->prof && !getenv("REXI_NO_GRAPH")) {
+        // the 1D step is a fixed kernel sequence: capture it once per
+        // (u_in, partial) pair and replay (a sharded run alternates two)
+        cudaStream_t st = plan->stream;
+        auto it = std::find_if(plan->part_graphs.begin(), plan->part_graphs.end(),
+                               [&](const rexi_plan::PartGraph &g) { return g.u == u_in && g.part == partial; });
+        if (it == plan->part_graphs.end()) {
+            if (plan->part_graphs.size() >= 4) {
+                cudaGraphExecDestroy(plan->part_graphs.front().exec);
+                plan->part_graphs.erase(plan->part_graphs.begin());
+            }
+            cudaGraph_t graph = nullptr;
+            const int64_t l0 = plan->launches;
+            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            rc = tri_step(plan, (const c128 *)u_in, nullptr);
+            cudaError_t ce = cudaStreamEndCapture(st, &graph);
+            if (rc) {
+                plan->tri.acc = acc_saved;
+                if (graph) cudaGraphDestroy(graph);
+                return rc;
+            }
+            if (ce != cudaSuccess) {
+                plan->tri.acc = acc_saved;
+                return cuda_err(plan, ce, "cudaStreamEndCapture");
+            }
+            rexi_plan::PartGraph g{u_in, partial, nullptr, plan->launches - l0};
+            cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ie != cudaSuccess) {
+                plan->tri.acc = acc_saved;
+                return cuda_err(plan, ie, "cudaGraphInstantiate");
+            }
+            plan->launches = l0;
+            plan->part_graphs.push_back(g);
+            it = plan->part_graphs.end() - 1;
+        }
+        const cudaError_t le = cudaGraphLaunch(it->exec, st);
+        plan->launches += it->kernels;
+        plan->tri.acc = acc_saved;
+        if (le != cudaSuccess) return cuda_err(plan, le, "cudaGraphLaunch");
+    } else {
+        rc = plan_step_device(plan, (const c128 *)u_in, nullptr);
+        plan->tri.acc = acc_saved;
+    }
     if (rc) return rc == REXI_ERR_NOCONV || rc == REXI_ERR_BREAKDOWN ? set_err(plan, rc, plan->err) : rc;
     // stream-ordered on a caller's stream (1D: nothing to check on the host;
     // COCG has synchronised for its convergence checks already)

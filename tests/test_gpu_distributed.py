@@ -64,3 +64,29 @@ def test_sharded_step_equals_single_plan(name):
         p.join(timeout=60)
     for _, u in outs:
         assert np.array_equal(u, single)
+
+
+def test_partial_step_graph_cache_many_buffers():
+    """rexi_plan_step_partial replays a captured graph per (u, partial)
+    buffer pair (at most 4 kept): six distinct input buffers, each result
+    equal bit for bit to the plan's own step"""
+    import torch
+    from paper_1912_03312_b200 import _native, fixtures
+    from paper_1912_03312_b200._pattern import shared_pattern
+    cfg = fixtures.config2(m=20_000, k=16)
+    ip, ix, ar, ai, br = shared_pattern(cfg.system.A, cfg.system.B)
+    s = torch.cuda.Stream()
+    p = _native.NativePlan(ip, ix, ar, br, cfg.approx.shifts, cfg.approx.weights, cfg.tau, a_imag=ai,
+                           device=0, refine=1, stream=s.cuda_stream)
+    n = cfg.system.n_dof
+    part = torch.empty((4, n), dtype=torch.float64, device="cuda")
+    for q in range(6):
+        u = torch.from_numpy(cfg.u0 * np.exp(0.3j * q)).cuda()
+        ref = torch.empty_like(u)
+        p.step_device(u.data_ptr(), ref.data_ptr(), 1)
+        for _ in range(2):                       # capture, then replay
+            p.step_partial(u.data_ptr(), part.data_ptr())
+            out = torch.empty_like(u)
+            _native.combine_partials(part.data_ptr(), 1, n, out.data_ptr(), s.cuda_stream)
+            s.synchronize()
+            assert torch.equal(out, ref), q
