@@ -30,6 +30,7 @@ struct TriState {
     c128 *rhs0 = nullptr, *rres = nullptr;
     c64 *inv32 = nullptr;         // refinement, TMA path: level-0 inverse pivots as complex64
     c64 *rres32 = nullptr;        // refinement, TMA path: complex64 residual (aliases rres)
+    float *r32[6] = {};           // refinement, TMA path: level-0 sub/sup row data rounded to float
     double *acc = nullptr;
     bool complex_a = false;       // A has an imaginary part: K2 keeps every residual product error-free
 };
@@ -329,6 +330,12 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
         // the level-0 correction solve (K3) runs in complex64 (tridiag_l0.cu)
         DALLOC(T.inv32, (size_t)n0 * kp);
         CK(launch_to_c64(T.lv[0].invd, T.inv32, n0 * kp, plan->stream));
+        const double *src32[6] = {T.z.ta_sub, T.z.ta_sub_im, T.z.b_sub, T.z.ta_sup, T.z.ta_sup_im, T.z.b_sup};
+        const int64_t nrow = n0 + l0_row_padding();
+        for (int q = 0; q < 6; ++q) {
+            DALLOC(T.r32[q], (size_t)nrow);
+            CK(launch_to_f32(src32[q], T.r32[q], nrow, plan->stream));
+        }
         T.rres32 = reinterpret_cast<c64 *>(T.rres);
         CK(cudaStreamSynchronize(plan->stream));
     }
@@ -429,7 +436,7 @@ int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
     rc = tri_mid(plan, true);
     if (rc) return rc;
     ProfScope ps(plan, "l0_k3");
-    CK(l0_launch_k3(T.z, T.lv[0], plan->S, T.lv[1].X, T.inv32, T.rres32, T.acc, uout, T.n, st));
+    CK(l0_launch_k3(T.z, T.lv[0], plan->S, T.lv[1].X, T.inv32, T.r32, T.rres32, T.acc, uout, T.n, st));
     return REXI_OK;
 }
 

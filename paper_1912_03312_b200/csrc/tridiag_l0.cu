@@ -44,6 +44,7 @@ struct L0Args {
     const c64 *rres_in;   // K3: interior residuals, complex64
     c64 *rres_out;        // K2
     const c64 *inv32;     // K3: level-0 inverse pivots rounded to complex64
+    const float *r32[6];  // K3: fl(tau a) sub/im/b, sup/im/b rounded to float
     double *acc;          // dd partial SoA 4*nout
     c128 *uout;
     int64_t nout;         // real n (level 0 is padded to a multiple of M)
@@ -582,13 +583,37 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
 #ifndef K3_MINB
 #define K3_MINB 8   // 93 -> 64 registers: 8 CTAs/SM (swept: scripts/tune_k3.sh)
 #endif
+// K3's shared memory: mbarrier | complex64 pivot tile T*kp | 6 float row
+// arrays (sub: tau a, tau a_im, b; sup: same) of Tp4 = T + 2 rounded to 4
+__host__ __device__ inline int k3_tp4(int T) { return (T + 2 + 3) & ~3; }
+__host__ __device__ inline size_t k3_smem_bytes(int kp, int M) {
+    const int T = (L0_NT / kp) * M;
+    return 128 + (size_t)T * kp * sizeof(c64) + 6 * (size_t)k3_tp4(T) * sizeof(float);
+}
+
 template <int M>
 __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const L0Layout l = carve(smem, a.S.kp, M, ST_T32);
+    const int kp = a.S.kp;
+    const int T = (L0_NT / kp) * M, Tp4 = k3_tp4(T);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    c64 *tile = reinterpret_cast<c64 *>(smem + 128);
+    float *rows = reinterpret_cast<float *>(tile + (size_t)T * kp);
     const Ctx c = make_ctx(a, M);
-    l0_stage(smem, l, a, a.inv32, nullptr, c.row0, ST_T32);
-    const int kp = c.kp;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int64_t row1 = min(c.row0 + (int64_t)T, a.L.n);
+        const uint32_t tb = (uint32_t)((row1 - c.row0) * kp * sizeof(c64));
+        const uint32_t rb = (uint32_t)(Tp4 * sizeof(float));
+        mbar_expect_tx(bar, tb + 6 * rb);
+        bulk_g2s(tile, a.inv32 + c.row0 * kp, tb, bar);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) bulk_g2s(rows + q * Tp4, a.r32[q] + c.row0, rb, bar);
+    }
     c64 y[M];
     c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
     if (c.active) {
@@ -597,18 +622,27 @@ __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
 #pragma unroll
         for (int q = 1; q < M; ++q) y[q] = a.rres_in[(c.base + q) * kp + c.j];
     }
-    mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
-    c64 *ti = reinterpret_cast<c64 *>(l.t0) + (size_t)c.lr0 * kp + c.j;
+    mbar_wait(bar, 0);
+    c64 *ti = tile + (size_t)c.lr0 * kp + c.j;
     if (c.active) {
-        const RowView &rv = l.rv;
+        // entries formed in fp32 from fp32 copies of fl(tau a) and b: the
+        // correction only needs ~1e-5 relative accuracy
+        const c64 sg = to_c64(c.sg);
+        const float *sr = rows, *si = rows + Tp4, *sb = rows + 2 * Tp4;
+        const float *ur = rows + 3 * Tp4, *ui = rows + 4 * Tp4, *ub = rows + 5 * Tp4;
         y[0] = to_c64(xs);
 #pragma unroll
-        for (int q = 1; q < M; ++q)
-            y[q] = fmul(ti[q * kp], ffnma(y[q], to_c64(rv.sub(c.lr0 + q, c.sg)), y[q - 1]));
+        for (int q = 1; q < M; ++q) {
+            const int lr = c.lr0 + q;
+            const c64 e = c64mk(fmaf(sg.y, sb[lr], sr[lr]), fmaf(-sg.x, sb[lr], si[lr]));
+            y[q] = fmul(ti[q * kp], ffnma(y[q], e, y[q - 1]));
+        }
         c64 xnext = to_c64(xn);
 #pragma unroll
         for (int q = M - 1; q >= 1; --q) {
-            xnext = ffnma(y[q], ti[q * kp], fmul(to_c64(rv.sup(c.lr0 + q, c.sg)), xnext));
+            const int lr = c.lr0 + q;
+            const c64 e = c64mk(fmaf(sg.y, ub[lr], ur[lr]), fmaf(-sg.x, ub[lr], ui[lr]));
+            xnext = ffnma(y[q], ti[q * kp], fmul(e, xnext));
             ti[q * kp] = xnext;
         }
         ti[0] = to_c64(xs);
@@ -617,7 +651,7 @@ __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
         for (int q = 0; q < M; ++q) ti[q * kp] = c64mk(0.f, 0.f);
     }
     __syncthreads();
-    reduce_rows<M, c64>(reinterpret_cast<const c64 *>(l.t0), a, c.row0);
+    reduce_rows<M, c64>(tile, a, c.row0);
 }
 
 // ---------------------------------------------------------------------------
@@ -923,6 +957,16 @@ __global__ void k_to_c64(const c128 *__restrict__ src, c64 *__restrict__ dst, in
     if (i < n) dst[i] = to_c64(src[i]);
 }
 
+__global__ void k_to_f32(const double *__restrict__ src, float *__restrict__ dst, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = __double2float_rn(src[i]);
+}
+
+cudaError_t launch_to_f32(const double *src, float *dst, int64_t n, cudaStream_t st) {
+    k_to_f32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, dst, n);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_to_c64(const c128 *src, c64 *dst, int64_t n, cudaStream_t st) {
     k_to_c64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, dst, n);
     return cudaGetLastError();
@@ -977,13 +1021,22 @@ cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
 }
 
 cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *X1,
-                         const c64 *inv32, const c64 *rres, double *acc, c128 *uout, int64_t nout,
-                         cudaStream_t st) {
+                         const c64 *inv32, const float *const *r32, const c64 *rres, double *acc, c128 *uout,
+                         int64_t nout, cudaStream_t st) {
     L0Args a{};
     a.nout = nout;
     a.z = z; a.L = L; a.S = S; a.X1 = X1; a.inv32 = inv32; a.rres_in = rres; a.acc = acc; a.uout = uout;
+    for (int q = 0; q < 6; ++q) a.r32[q] = r32[q];
     a.acc_add = 1; a.final_out = uout != nullptr;
-    return launch_l0(k_l0_k3<TRI_M>, a, ST_T32, st);
+    const int kp = S.kp;
+    const int64_t rows = (int64_t)(L0_NT / kp) * TRI_M;
+    const int64_t grid = (L.n + rows - 1) / rows;
+    const size_t smem = k3_smem_bytes(kp, TRI_M);
+    auto kern = k_l0_k3<TRI_M>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)grid, L0_NT, smem, st>>>(a);
+    return cudaGetLastError();
 }
 
 }  // namespace rexi

@@ -61,8 +61,9 @@ cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
                          const c128 *X1, double *acc, c64 *rres, int64_t nout, bool exact_residual,
                          cudaStream_t st);
 cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *X1,
-                         const c64 *inv32, const c64 *rres, double *acc, c128 *uout, int64_t nout,
-                         cudaStream_t st);
+                         const c64 *inv32, const float *const *r32, const c64 *rres, double *acc, c128 *uout,
+                         int64_t nout, cudaStream_t st);
 cudaError_t launch_to_c64(const c128 *src, c64 *dst, int64_t n, cudaStream_t st);
+cudaError_t launch_to_f32(const double *src, float *dst, int64_t n, cudaStream_t st);
 
 }  // namespace rexi
