@@ -62,12 +62,21 @@ struct RowView {
     const double *sr, *si, *sb;   // sub  : fl(tau a), fl(tau a_im), b
     const double *dr, *di, *db;   // diag
     const double *ur, *ui, *ub;   // sup
+    const float *f[6];            // ST_R32: sub (tau a, tau a_im, b), sup (same) rounded to float
     __device__ __forceinline__ c128 sub(int lr, c128 sg) const { return form_entry(sr[lr], si[lr], sb[lr], sg); }
+    // complex64 entries for the level-0 correction solve (fp32 formation)
+    __device__ __forceinline__ c64 sub32(int lr, c64 sg) const {
+        return c64mk(fmaf(sg.y, f[2][lr], f[0][lr]), fmaf(-sg.x, f[2][lr], f[1][lr]));
+    }
+    __device__ __forceinline__ c64 sup32(int lr, c64 sg) const {
+        return c64mk(fmaf(sg.y, f[5][lr], f[3][lr]), fmaf(-sg.x, f[5][lr], f[4][lr]));
+    }
     __device__ __forceinline__ c128 dia(int lr, c128 sg) const { return form_entry(dr[lr], di[lr], db[lr], sg); }
     __device__ __forceinline__ c128 sup(int lr, c128 sg) const { return form_entry(ur[lr], ui[lr], ub[lr], sg); }
 };
 
-enum { ST_RHS = 1, ST_DIA = 2, ST_TILE2 = 4, ST_BDIA = 8, ST_T32 = 16 };   // ST_T32: t0 holds complex64
+enum { ST_RHS = 1, ST_DIA = 2, ST_TILE2 = 4, ST_BDIA = 8, ST_T32 = 16, ST_R32 = 32 };
+// ST_T32: t0 holds complex64; ST_R32: + float copies of the sub/sup row data
 
 struct L0Layout {
     int kp, T, Tp;
@@ -100,6 +109,11 @@ __device__ __forceinline__ L0Layout carve(unsigned char *smem, int kp, int M, in
     r.dr = r.di = r.db = nullptr;
     if (flags & ST_DIA) { r.dr = d; d += l.Tp; r.di = d; d += l.Tp; r.db = d; d += l.Tp; }
     else if (flags & ST_BDIA) { r.db = d; d += l.Tp; }
+    if (flags & ST_R32) {
+        float *f = reinterpret_cast<float *>(d);
+        const int tp4 = (l.Tp + 3) & ~3;
+        for (int q = 0; q < 6; ++q) r.f[q] = f + q * tp4;
+    }
     return l;
 }
 
@@ -108,6 +122,7 @@ __host__ __device__ inline size_t l0_smem_bytes(int kp, int M, int flags) {
     size_t b = 128 + T * kp * ((flags & ST_T32) ? 8 : 16) + ((flags & ST_TILE2) ? T * kp * 16 : 0);
     if (flags & ST_RHS) b += Tp * 16;
     b += Tp * 8 * ((flags & ST_DIA) ? 9 : (flags & ST_BDIA) ? 7 : 6);
+    if (flags & ST_R32) b += 6 * ((Tp + 3) & ~(size_t)3) * sizeof(float);
     return b;
 }
 
@@ -127,8 +142,9 @@ __device__ __forceinline__ void l0_stage(unsigned char *smem, const L0Layout &l,
         const uint32_t tb = (uint32_t)((row1 - row0) * l.kp * sizeof(c128));
         const uint32_t tb0 = (uint32_t)((row1 - row0) * l.kp * esz);
         const uint32_t rb8 = (uint32_t)(l.Tp * 8), rb16 = (uint32_t)(l.Tp * 16);
+        const uint32_t rb4 = (uint32_t)(((l.Tp + 3) & ~3) * sizeof(float));
         uint32_t total = tb0 + ((flags & ST_TILE2) ? tb : 0) + ((flags & ST_RHS) ? rb16 : 0) +
-                         rb8 * ((flags & ST_DIA) ? 9 : (flags & ST_BDIA) ? 7 : 6);
+                         rb8 * ((flags & ST_DIA) ? 9 : (flags & ST_BDIA) ? 7 : 6) + ((flags & ST_R32) ? 6 * rb4 : 0);
         mbar_expect_tx(bar, total);
         bulk_g2s(l.t0, reinterpret_cast<const unsigned char *>(g_t0) + (size_t)row0 * l.kp * esz, tb0, bar);
         if (flags & ST_TILE2) bulk_g2s(l.t1, g_t1 + row0 * l.kp, tb, bar);
@@ -146,6 +162,8 @@ __device__ __forceinline__ void l0_stage(unsigned char *smem, const L0Layout &l,
         } else if (flags & ST_BDIA) {
             bulk_g2s((void *)l.rv.db, a.z.b_dia + row0, rb8, bar);
         }
+        if (flags & ST_R32)
+            for (int q = 0; q < 6; ++q) bulk_g2s((void *)l.rv.f[q], a.r32[q] + row0, rb4, bar);
     }
 }
 
@@ -498,22 +516,37 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
         // and the correction's S1 here uses the same rounded values as K3's S3
         const c64 r32 = to_c64(cmk(__dadd_rn(re.hi, re.lo), __dadd_rn(im.hi, im.lo)));
         a.rres_out[(c.base + q) * kp + j] = r32;
-        tc[(q - 1) * kp] = to_c128(r32);
+        *reinterpret_cast<c64 *>(tc + (q - 1) * kp) = r32;
         xm = x0;
         x0 = xp;
         esub = eup;
     }
-    // correction reduce: S1 with rhs = r
-    y[0] = cmk(0.0, 0.0);
-    sweep_fwd<M, FULL>(y, ti, kp, rv, c.lr0, cnt, c.sg, [&](int q) { return tc[(q - 1) * kp]; });
-    const c128 ylast = y[M - 1];
-    sweep_bwd<M, FULL>(y, ti, kp, rv, c.lr0, cnt, c.sg, cmk(0.0, 0.0), [](int, c128) {});
-    const c128 t1 = cneg(cmul(rv.sup(c.lr0, c.sg), y[1]));
+    // correction reduce: S1 with rhs = r, in complex64 like K3's correction
+    // S3 (pivots rounded from the staged fp64 tile, entries formed in fp32)
+    (void)y;
+    const c64 sg32 = to_c64(c.sg);
+    c64 yf[M];
+    yf[0] = c64mk(0.f, 0.f);
+#pragma unroll
+    for (int q = 1; q < M; ++q) {
+        const c64 rq = *reinterpret_cast<const c64 *>(tc + (q - 1) * kp);
+        yf[q] = fmul(to_c64(ti[q * kp]), ffnma(rq, rv.sub32(c.lr0 + q, sg32), yf[q - 1]));
+    }
+    const c64 ylast = yf[M - 1];
+    c64 xnext = c64mk(0.f, 0.f);
+#pragma unroll
+    for (int q = M - 1; q >= 1; --q) {
+        xnext = ffnma(yf[q], to_c64(ti[q * kp]), fmul(rv.sup32(c.lr0 + q, sg32), xnext));
+        yf[q] = xnext;
+    }
+    const c64 m1 = fmul(rv.sup32(c.lr0, sg32), yf[1]);
+    const c128 t1 = cmk(-(double)m1.x, -(double)m1.y);
     ddacc_add(p1re, t1.x);
     ddacc_add(p1im, t1.y);
     a.L.ypdd[c.p * kp + j] = cdd{{p1re.hi, p1re.lo}, {p1im.hi, p1im.lo}};
     if (has_next) {
-        const c128 t2 = cneg(cmul(an, ylast));
+        const c64 m2 = fmul(rv.sub32(c.lr0 + M, sg32), ylast);
+        const c128 t2 = cmk(-(double)m2.x, -(double)m2.y);
         ddacc_add(p2re, t2.x);
         ddacc_add(p2im, t2.y);
         a.L.lcdd[(c.p + 1) * kp + j] = cdd{{p2re.hi, p2re.lo}, {p2im.hi, p2im.lo}};
@@ -524,7 +557,7 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
 template <int M, bool EXACT>
 __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int flags = ST_RHS | ST_DIA | ST_TILE2;
+    const int flags = ST_RHS | ST_DIA | ST_TILE2 | ST_R32;
     const L0Layout l = carve(smem, a.S.kp, M, flags);
     const Ctx c = make_ctx(a, M);
     l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, flags & ~ST_TILE2);
@@ -1003,8 +1036,8 @@ cudaError_t l0_launch_s3acc(const L0Dev &z, const LevelDev &L, const ShiftDev &S
 }
 
 cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
-                         const c128 *X1, double *acc, c64 *rres, int64_t nout, bool exact_residual,
-                         cudaStream_t st) {
+                         const c128 *X1, double *acc, c64 *rres, const float *const *r32, int64_t nout,
+                         bool exact_residual, cudaStream_t st) {
     L0Args a{};
     a.nout = nout;
     a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0; a.X1 = X1; a.acc = acc; a.rres_out = rres;
@@ -1016,8 +1049,9 @@ cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
         a.pf_dist = (int64_t)sms * K2_MINB;   // one residency wave ahead
         if (const char *e = getenv("REXI_K2_PF")) a.pf_dist = (int64_t)(atof(e) * sms * K2_MINB);
     }
-    if (exact_residual) return launch_l0(k_l0_k2<TRI_M, true>, a, ST_RHS | ST_DIA | ST_TILE2, st);
-    return launch_l0(k_l0_k2<TRI_M, false>, a, ST_RHS | ST_DIA | ST_TILE2, st);
+    for (int q = 0; q < 6; ++q) a.r32[q] = r32[q];
+    if (exact_residual) return launch_l0(k_l0_k2<TRI_M, true>, a, ST_RHS | ST_DIA | ST_TILE2 | ST_R32, st);
+    return launch_l0(k_l0_k2<TRI_M, false>, a, ST_RHS | ST_DIA | ST_TILE2 | ST_R32, st);
 }
 
 cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *X1,
