@@ -29,7 +29,7 @@ constexpr int L0_NT = 128;      // threads per CTA
 constexpr int L0_ROWPAD = 2;    // extra staged rows (next interface row + 16-B rounding)
 
 #ifndef K2_RES_UNROLL
-#define K2_RES_UNROLL 3
+#define K2_RES_UNROLL 5   // swept: scripts/tune_k2u.sh (3: +1.2 %, 15: +15 %)
 #endif
 constexpr int K2_UNROLL = K2_RES_UNROLL;
 #ifndef K2_MINB
