@@ -452,14 +452,38 @@ static size_t persist_smem_bytes(const LevelDev *lv, int nl, int kp, int cs) {
     return a > b ? a : b;
 }
 
+// k_persist's dynamic shared-memory attribute as last set on this device
+// (setting it costs ~1 us, a visible share of a ~20 us small-plan call)
+// (per device; plans are created and stepped on their own device)
+constexpr int PS_MAXDEV = 64;
+static size_t g_persist_smem_attr[PS_MAXDEV] = {};
+static bool g_persist_cluster_attr[PS_MAXDEV] = {};
+
+static cudaError_t persist_set_smem(size_t sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= PS_MAXDEV) {
+        cudaFuncSetAttribute(k_persist, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        return cudaFuncSetAttribute(k_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    }
+    if (!g_persist_cluster_attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(k_persist, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        g_persist_cluster_attr[dev] = true;
+    }
+    if (sm == g_persist_smem_attr[dev]) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e == cudaSuccess) g_persist_smem_attr[dev] = sm;
+    return e;
+}
+
 // largest cluster this plan can run as (0: cannot run -- the slice must fit
 // in shared memory and the cluster must be schedulable)
 int persist_cluster_size(const LevelDev *lv, int nl, int kp) {
-    cudaFuncSetAttribute(k_persist, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     for (int cs : {16, 8, 4}) {
         const size_t sm = persist_smem_bytes(lv, nl, kp, cs);
         if (sm > 200 * 1024) continue;
-        cudaFuncSetAttribute(k_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        persist_set_smem(sm);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(cs);
         cfg.blockDim = dim3(PS_NT);
@@ -505,9 +529,10 @@ cudaError_t persist_launch(const L0Dev &z, const LevelDev *lv, int nl, const Shi
     if (trace) cudaMemsetAsync(tbuf, 0, 64 * sizeof(unsigned long long), st);
     a.tstamp = trace ? tbuf : nullptr;
     const size_t sm = persist_smem_bytes(lv, nl, S.kp, csize);
-    // (set on every launch: persist_cluster_size probes other sizes on the same function)
-    cudaFuncSetAttribute(k_persist, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(k_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    {
+        cudaError_t e = persist_set_smem(sm);
+        if (e != cudaSuccess) return e;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csize);
     cfg.blockDim = dim3(PS_NT);
