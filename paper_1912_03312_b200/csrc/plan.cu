@@ -389,7 +389,8 @@ int tri_mid(rexi_plan *plan, bool dd) {
         ProfScope ps(plan, "s1_lv");
         const bool d = l == 1 && dd;
         if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 1, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
-                                  d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, nullptr, st));
+                                  d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, nullptr, st,
+                                  d ? T.lv[1].X : nullptr));
         else if (d) CK(tri_launch_lv_dd(T.lv[1], plan->S, 1, T.lv[0].ypdd, T.lv[0].lcdd, nullptr, st));
         else CK(tri_launch_s1(T.z, T.lv[l], plan->S, (int)l, nullptr, nullptr, T.lv[l - 1].ypart,
                               T.lv[l - 1].lc, st));
@@ -406,7 +407,8 @@ int tri_mid(rexi_plan *plan, bool dd) {
         ProfScope ps(plan, "s3_lv");
         const bool d = l == 1 && dd;
         if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 3, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
-                                  d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, T.lv[l + 1].X, st));
+                                  d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, T.lv[l + 1].X, st,
+                                  d ? T.lv[1].X : nullptr));
         else if (d) CK(tri_launch_lv_dd(T.lv[1], plan->S, 3, T.lv[0].ypdd, T.lv[0].lcdd, T.lv[2].X, st));
         else CK(tri_launch_s3(T.z, T.lv[l], plan->S, (int)l, nullptr, nullptr, T.lv[l - 1].ypart,
                               T.lv[l - 1].lc, T.lv[l + 1].X, TRI_OUT_X, nullptr, 0, nullptr, st));

@@ -701,6 +701,7 @@ struct LvArgs {
     const c128 *rin_a, *rin_b;   // previous level ypart / lc
     const cdd *rdd_a, *rdd_b;    // or their double-double versions (correction pass)
     const c128 *Xnext;
+    c128 *rw;                    // SRC 1, PHASE 1: the rounded rhs rows, reused by the level's S3
 };
 
 struct LvPtrs {
@@ -709,21 +710,32 @@ struct LvPtrs {
     const cdd *da, *db;
     const c128 *Xn;
     c128 *ypart, *lc, *X;
+    c128 *rw;
 };
 
-template <bool DD>
+// rhs of a reduced level: SRC 0 = ypart + lc, 1 = round(ypdd + lcdd) (the
+// correction pass's double-double halves), 2 = the rounded rhs SRC 1 stored
+enum { LV_SRC_PLAIN = 0, LV_SRC_DD = 1, LV_SRC_STORED = 2 };
+template <int SRC>
 __device__ __forceinline__ c128 lv_rhs(const LvPtrs &q, int64_t i, int j, int kp) {
-    if constexpr (DD) return cdd_round(cdd_add(q.da[i * kp + j], q.db[i * kp + j]));
+    if constexpr (SRC == LV_SRC_DD) return cdd_round(cdd_add(q.da[i * kp + j], q.db[i * kp + j]));
+    else if constexpr (SRC == LV_SRC_STORED) return q.ra[i * kp + j];
     else return cadd(q.ra[i * kp + j], q.rb[i * kp + j]);
 }
 
-template <int M, int PHASE, bool DD, bool FULL>
+template <int M, int PHASE, int SRC, bool FULL>
 __device__ __forceinline__ void lv_body(const LvPtrs &t, int lr0, int kp, int j, int64_t p, int64_t P,
                                         int64_t base, int cnt) {
     c128 y[M];
 #pragma unroll
     for (int q = 1; q < M; ++q)
-        if (FULL || q <= cnt) y[q] = lv_rhs<DD>(t, base + q, j, kp);
+        if (FULL || q <= cnt) y[q] = lv_rhs<SRC>(t, base + q, j, kp);
+    if (SRC == LV_SRC_DD && PHASE == 1 && t.rw) {
+        // the combined, rounded rhs for this level's S3 (16 instead of 64 B re-read)
+#pragma unroll
+        for (int q = 1; q < M; ++q)
+            if (FULL || q <= cnt) t.rw[(base + q) * kp + j] = y[q];
+    }
     c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
     if (PHASE == 3) {
         xs = t.Xn[p * kp + j];
@@ -754,7 +766,7 @@ __device__ __forceinline__ void lv_body(const LvPtrs &t, int lr0, int kp, int j,
     }
     if constexpr (PHASE == 1) {
         const c128 yfirst = cnt >= 1 ? y[1] : cmk(0.0, 0.0);
-        const c128 ds = lv_rhs<DD>(t, base, j, kp);
+        const c128 ds = lv_rhs<SRC>(t, base, j, kp);
         t.ypart[p * kp + j] = cfnma(ds, t.sup[lr0 * kp], yfirst);
         if (p + 1 < P) t.lc[(p + 1) * kp + j] = cneg(cmul(t.sup[(lr0 + M - 1) * kp], ylast));
         if (p == 0) t.lc[j] = cmk(0.0, 0.0);
@@ -766,7 +778,7 @@ __device__ __forceinline__ void lv_body(const LvPtrs &t, int lr0, int kp, int j,
     }
 }
 
-template <int M, int PHASE, bool DD>
+template <int M, int PHASE, int SRC>
 __global__ void __launch_bounds__(L0_NT, LV_MINB) k_lv_tma(const __grid_constant__ LvArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
@@ -799,9 +811,9 @@ __global__ void __launch_bounds__(L0_NT, LV_MINB) k_lv_tma(const __grid_constant
     LvPtrs t;
     t.inv = tinv + j; t.sup = tsup + j;
     t.ra = a.rin_a; t.rb = a.rin_b; t.da = a.rdd_a; t.db = a.rdd_b; t.Xn = a.Xnext;
-    t.ypart = a.L.ypart; t.lc = a.L.lc; t.X = a.L.X;
-    if (cnt == M - 1) lv_body<M, PHASE, DD, true>(t, b * M, kp, j, p, P, base, cnt);
-    else lv_body<M, PHASE, DD, false>(t, b * M, kp, j, p, P, base, cnt);
+    t.ypart = a.L.ypart; t.lc = a.L.lc; t.X = a.L.X; t.rw = a.rw;
+    if (cnt == M - 1) lv_body<M, PHASE, SRC, true>(t, b * M, kp, j, p, P, base, cnt);
+    else lv_body<M, PHASE, SRC, false>(t, b * M, kp, j, p, P, base, cnt);
 }
 
 // ---------------------------------------------------------------------------
@@ -851,9 +863,9 @@ __device__ __forceinline__ void chain_level(const LevelDev &L, const LevelDev &L
             LvPtrs t;
             t.inv = tinv + j; t.sup = tsup + j;
             t.ra = Lp.ypart; t.rb = Lp.lc; t.da = nullptr; t.db = nullptr; t.Xn = Xnext;
-            t.ypart = L.ypart; t.lc = L.lc; t.X = L.X;
-            if (cnt == M - 1) lv_body<M, PHASE, false, true>(t, b * M, kp, j, p, P, base, cnt);
-            else lv_body<M, PHASE, false, false>(t, b * M, kp, j, p, P, base, cnt);
+            t.ypart = L.ypart; t.lc = L.lc; t.X = L.X; t.rw = nullptr;
+            if (cnt == M - 1) lv_body<M, PHASE, LV_SRC_PLAIN, true>(t, b * M, kp, j, p, P, base, cnt);
+            else lv_body<M, PHASE, LV_SRC_PLAIN, false>(t, b * M, kp, j, p, P, base, cnt);
         }
         __syncthreads();   // tiles free for the next virtual CTA
     }
@@ -946,7 +958,7 @@ cudaError_t lv_launch_chain(const LevelDev *lv, int nl, int l0, int cs, const Sh
 }
 
 cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,
-                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st) {
+                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st, c128 *rw) {
     LvArgs a{};
     a.L = L; a.S = S; a.rin_a = rin_a; a.rin_b = rin_b; a.rdd_a = rdd_a; a.rdd_b = rdd_b; a.Xnext = Xnext;
     const int kp = S.kp;
@@ -954,19 +966,23 @@ cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const
     const int64_t grid = (L.n + rows - 1) / rows;
     const size_t smem = 128 + 2 * (size_t)rows * kp * sizeof(c128);
     cudaError_t e;
-#define LV_LAUNCH(PH, DDV)                                                                              \
+#define LV_LAUNCH(PH, SRCV)                                                                             \
     do {                                                                                                \
-        auto kern = k_lv_tma<TRI_M, PH, DDV>;                                                            \
+        auto kern = k_lv_tma<TRI_M, PH, SRCV>;                                                           \
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
         if (e != cudaSuccess) return e;                                                                 \
         kern<<<(unsigned)grid, L0_NT, smem, st>>>(a);                                                   \
     } while (0)
     if (phase == 1) {
-        if (rdd_a) LV_LAUNCH(1, true);
-        else LV_LAUNCH(1, false);
+        a.rw = rdd_a ? rw : nullptr;
+        if (rdd_a) LV_LAUNCH(1, LV_SRC_DD);
+        else LV_LAUNCH(1, LV_SRC_PLAIN);
+    } else if (rdd_a && rw) {   // the rhs the S1 pass stored
+        a.rin_a = rw;
+        LV_LAUNCH(3, LV_SRC_STORED);
     } else {
-        if (rdd_a) LV_LAUNCH(3, true);
-        else LV_LAUNCH(3, false);
+        if (rdd_a) LV_LAUNCH(3, LV_SRC_DD);
+        else LV_LAUNCH(3, LV_SRC_PLAIN);
     }
 #undef LV_LAUNCH
     return cudaGetLastError();

@@ -42,8 +42,11 @@ inline int64_t lv_tma_ctas(int64_t n, int kp) {   // grid of lv_launch_tma
     const int64_t rows = (int64_t)(128 / kp) * TRI_M;
     return (n + rows - 1) / rows;
 }
+// rw (correction pass, dd rhs): phase 1 stores the rounded rhs rows there,
+// phase 3 reads them back instead of re-combining the double-double halves
 cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,
-                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st);
+                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st,
+                          c128 *rw = nullptr);
 
 // levels l0..top..l0 in one cluster launch (tridiag_l0.cu); lv_chain_start
 // returns the first chained level (0: none) and the cluster size
