@@ -70,6 +70,11 @@ struct rexi_plan {
     std::vector<cudaEvent_t> pool;
     std::map<std::string, Acc> prof_acc;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};   // 1D step replay (ubuf[g] -> ubuf[g^1])
+    // the same step with its input/output kernels re-pointed per call at
+    // page-locked host buffers (the last step of a host call)
+    cudaGraph_t zc_src[2] = {nullptr, nullptr};
+    cudaGraphExec_t zc_exec[2] = {nullptr, nullptr};
+    cudaGraphNode_t zc_in_node[2] = {nullptr, nullptr}, zc_out_node[2] = {nullptr, nullptr};
     int persist_cs = 0;                               // >0: small 1D plan, all steps in one cluster launch
     c128 *pbuf[2] = {nullptr, nullptr};               // its state ping-pong
     int64_t graph_kernels = 0;
@@ -518,6 +523,10 @@ int rexi_plan_destroy(rexi_plan *plan) {
     for (auto &r : plan->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto &g : plan->graph)
         if (g) cudaGraphExecDestroy(g);
+    for (int g = 0; g < 2; ++g) {
+        if (plan->zc_exec[g]) cudaGraphExecDestroy(plan->zc_exec[g]);
+        if (plan->zc_src[g]) cudaGraphDestroy(plan->zc_src[g]);
+    }
     for (auto &g : plan->part_graphs) cudaGraphExecDestroy(g.exec);
     for (auto e : plan->pool) cudaEventDestroy(e);
     if (plan->own_stream && plan->stream) cudaStreamDestroy(plan->stream);
@@ -769,7 +778,23 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
             if (rc) return rc;
             if (ce != cudaSuccess) return cuda_err(plan, ce, "cudaStreamEndCapture");
             CK(cudaGraphInstantiate(&plan->graph[g], graph, 0));
-            cudaGraphDestroy(graph);
+            // a second instance whose S1 / output kernels get re-pointed per
+            // host call (the source graph stays alive for the node handles)
+            size_t nn = 0;
+            CK(cudaGraphGetNodes(graph, nullptr, &nn));
+            std::vector<cudaGraphNode_t> nodes(nn);
+            CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+            for (cudaGraphNode_t nd : nodes) {
+                const int role = l0_graph_role(nd);
+                if (role == 1) plan->zc_in_node[g] = nd;
+                if (role == 2) plan->zc_out_node[g] = nd;
+            }
+            if (plan->zc_in_node[g] && plan->zc_out_node[g]) {
+                CK(cudaGraphInstantiate(&plan->zc_exec[g], graph, 0));
+                plan->zc_src[g] = graph;
+            } else {
+                cudaGraphDestroy(graph);
+            }
             plan->graph_kernels = plan->launches - l0;
             plan->launches = l0;
         }
@@ -780,7 +805,14 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
             cur ^= 1;
         }
         if (!(zc_in && graph_steps == 0)) src = plan->ubuf[cur];
-        if (zc_out) {   // last step straight into the page-locked output
+        if (zc_out && plan->zc_exec[cur] && !getenv("REXI_NO_ZC_GRAPH")) {
+            // last step straight into the page-locked output: the captured
+            // step with its S1 (input) and output kernels re-pointed
+            CK(l0_graph_patch(plan->zc_exec[cur], plan->zc_in_node[cur], 1, src, nullptr));
+            CK(l0_graph_patch(plan->zc_exec[cur], plan->zc_out_node[cur], 2, nullptr, zc_out));
+            CK(cudaGraphLaunch(plan->zc_exec[cur], st));
+            plan->launches += plan->graph_kernels;
+        } else if (zc_out) {   // last step straight into the page-locked output
             int rc = plan_step_device(plan, src, zc_out);
             if (rc) return rc;
         }

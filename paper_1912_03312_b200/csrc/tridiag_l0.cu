@@ -1021,6 +1021,39 @@ cudaError_t launch_to_c64(const c128 *src, c64 *dst, int64_t n, cudaStream_t st)
     return cudaGetLastError();
 }
 
+// Graph patching for host-buffer steps (plan.cu): find the level-0 kernel
+// nodes of a captured step that read u (S1) and write the rounded output
+// (K3, or S3ACC without refinement), and re-point them at other buffers.
+int l0_graph_role(cudaGraphNode_t node) {
+    cudaGraphNodeType ty;
+    if (cudaGraphNodeGetType(node, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) return 0;
+    cudaKernelNodeParams p{};
+    if (cudaGraphKernelNodeGetParams(node, &p) != cudaSuccess) return 0;
+    if (p.func == (void *)k_l0_s1<TRI_M>) return 1;
+    if (p.func == (void *)k_l0_k3<TRI_M> || p.func == (void *)k_l0_s3acc<TRI_M>) {
+        const L0Args *a = reinterpret_cast<const L0Args *>(p.kernelParams[0]);
+        return a->final_out ? 2 : 0;
+    }
+    return 0;
+}
+
+cudaError_t l0_graph_patch(cudaGraphExec_t exec, cudaGraphNode_t node, int role, const c128 *u, c128 *uout) {
+    cudaKernelNodeParams p{};
+    cudaError_t e = cudaGraphKernelNodeGetParams(node, &p);
+    if (e != cudaSuccess) return e;
+    L0Args a = *reinterpret_cast<const L0Args *>(p.kernelParams[0]);
+    if (role == 1) {
+        a.u = u;
+        a.u_bulk = ((uintptr_t)u & 15) == 0 && !getenv("REXI_S1_NO_BULK");
+    } else {
+        a.uout = uout;
+    }
+    void *args[1] = {&a};
+    p.kernelParams = args;
+    p.extra = nullptr;
+    return cudaGraphExecKernelNodeSetParams(exec, node, &p);
+}
+
 bool l0v2_supported(int kp) { return kp <= L0_NT; }
 int64_t l0_row_padding() { return (int64_t)L0_NT * TRI_M + 2 * L0_ROWPAD; }
 

@@ -53,6 +53,11 @@ cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const
 int lv_chain_start(const LevelDev *lv, int nl, int kp, int *cs);
 cudaError_t lv_launch_chain(const LevelDev *lv, int nl, int l0, int cs, const ShiftDev &S, cudaStream_t st);
 
+// captured-step graph nodes (role 1: S1 reads u; role 2: the kernel that
+// writes the rounded output) and their re-pointing (tridiag_l0.cu)
+int l0_graph_role(cudaGraphNode_t node);
+cudaError_t l0_graph_patch(cudaGraphExec_t exec, cudaGraphNode_t node, int role, const c128 *u, c128 *uout);
+
 // TMA-fed level-0 kernels (tridiag_l0.cu)
 bool l0v2_supported(int kp);
 int64_t l0_row_padding();
