@@ -188,7 +188,7 @@ __device__ __forceinline__ c128 lvv_sub(const LvView &V, int i, int j, int kp) {
 
 // reduced level block (k_lv_tma's lv_body / k_block with RHS_LV, same order)
 template <int PHASE>
-__device__ __forceinline__ void lv_block(const LvView &V, int p, int j, int kp) {
+__device__ __forceinline__ void lv_block(const LvView V, int p, int j, int kp) {   // by value: offsets in registers
     constexpr int M = TRI_M;
     c128 *sm = psm();
     const int n = V.n, P = V.P, base = p * M;
@@ -240,7 +240,7 @@ __device__ __forceinline__ void lv_block(const LvView &V, int p, int j, int kp) 
 
 // k_top_solve for one lane (the top level's rows solved sequentially); the
 // top's solution stays in shared memory (or global when the top is level 1)
-__device__ __forceinline__ void top_solve(const LvView &T, int j, int kp) {
+__device__ __forceinline__ void top_solve(const LvView T, int j, int kp) {
     c128 *sm = psm();
     c128 *X = T.X >= 0 ? sm + T.X : T.Xg;
     c128 yp = cmk(0.0, 0.0);
