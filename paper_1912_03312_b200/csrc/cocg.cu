@@ -38,6 +38,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -48,11 +49,27 @@ namespace rexi {
 constexpr int CG_NT = 256;            // threads per CTA (8 warps)
 constexpr int CG_WARPS = CG_NT / 32;
 
+// Stencil classes (narrow layouts): rows whose column offsets (col - row) and
+// B values equal those of a class share one table entry, so the narrow
+// spmv streams only fl(tau a) (and fl(tau a_im)) per entry plus a 1-byte
+// class id per row instead of index + a + b -- the matrix dominates the
+// bytes of an iteration once few shifts are live.  The entries are formed
+// from the same doubles in the same order: results are bitwise identical.
+constexpr int CG_CLS_MAX = 64;        // classes (id 255: a row without one)
+constexpr int CG_CLS_MAXNNZ = 32;     // entries per class row
+struct CgClass {
+    int nnz;
+    int off[CG_CLS_MAXNNZ];
+    double b[CG_CLS_MAXNNZ];
+};
+
 struct CgMat {
     int64_t n;
     const int32_t *indptr, *indices;
     const double *ta, *ta_im, *b;          // per nnz: fl(tau a), fl(tau a_im), b
     const double *dta, *dta_im, *db;       // per row: the diagonal entry's values
+    const uint8_t *cls;                    // per row: stencil class or 255 (nullptr: none)
+    const CgClass *classes;
 };
 
 struct CgVec {
@@ -84,6 +101,78 @@ struct CgGeom {
 };
 
 __device__ __forceinline__ c128 cdiv_c(c128 a, c128 b) { return cmul(a, crcp(b)); }
+
+#ifndef CG_GB
+#define CG_GB 8   // z gathers in flight per thread (global-CSR spmv)
+#endif
+
+// (S z)_i for one lane, ascending CSR order, z gathers batched CG_GB at a
+// time; a classed row takes its columns and B values from the class table
+#ifndef CG_SPMV_UNROLL
+#define CG_SPMV_UNROLL 4
+#endif
+constexpr int kSpmvUnroll = CG_SPMV_UNROLL;
+template <bool CPLX, bool BATCH>
+__device__ __forceinline__ c128 row_sz(const CgMat &M, int64_t i, const c128 *__restrict__ zv, uint32_t kp,
+                                       int lane, c128 sg) {
+    c128 acc = cmk(0.0, 0.0);
+    const int32_t q0 = __ldg(M.indptr + i);
+    const int cl = M.cls ? (int)__ldg(M.cls + i) : 255;
+    if (cl != 255) {
+        const CgClass &C = M.classes[cl];
+        const int nz = C.nnz;
+        if (!BATCH) {
+#pragma unroll kSpmvUnroll
+            for (int k = 0; k < nz; ++k) {
+                const c128 e = form_entry(__ldg(M.ta + q0 + k), CPLX ? __ldg(M.ta_im + q0 + k) : 0.0, C.b[k], sg);
+                acc = cadd(acc, cmul(e, zv[(uint32_t)(i + C.off[k]) * kp + lane]));
+            }
+            return acc;
+        }
+        for (int kb = 0; kb < nz; kb += CG_GB) {
+            c128 zz[CG_GB];
+#pragma unroll
+            for (int k = 0; k < CG_GB; ++k)
+                zz[k] = kb + k < nz ? zv[(uint32_t)(i + C.off[kb + k]) * kp + lane] : cmk(0.0, 0.0);
+#pragma unroll
+            for (int k = 0; k < CG_GB; ++k) {
+                if (kb + k < nz) {
+                    const int32_t q = q0 + kb + k;
+                    const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, C.b[kb + k], sg);
+                    acc = cadd(acc, cmul(e, zz[k]));
+                }
+            }
+        }
+        return acc;
+    }
+    const int32_t q1 = __ldg(M.indptr + i + 1);
+    if (!BATCH) {
+#pragma unroll kSpmvUnroll
+        for (int32_t q = q0; q < q1; ++q) {
+            const uint32_t c = (uint32_t)__ldg(M.indices + q);
+            const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
+            acc = cadd(acc, cmul(e, zv[c * kp + lane]));
+        }
+        return acc;
+    }
+    for (int32_t qb = q0; qb < q1; qb += CG_GB) {
+        uint32_t cc[CG_GB];
+        c128 zz[CG_GB];
+#pragma unroll
+        for (int k = 0; k < CG_GB; ++k) cc[k] = qb + k < q1 ? (uint32_t)__ldg(M.indices + qb + k) : 0u;
+#pragma unroll
+        for (int k = 0; k < CG_GB; ++k) zz[k] = qb + k < q1 ? zv[cc[k] * kp + lane] : cmk(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < CG_GB; ++k) {
+            if (qb + k < q1) {
+                const int32_t q = qb + k;
+                const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
+                acc = cadd(acc, cmul(e, zz[k]));
+            }
+        }
+    }
+    return acc;
+}
 
 // lane and row slot of this thread for one CTA pass
 __device__ __forceinline__ void cta_geom(const CgGeom &g, int &lane, int &slot, int &slots) {
@@ -215,15 +304,8 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
 // are double-buffered: one barrier per claim.  Element offsets fit in 32 bits
 // (n * kp < 2^31 is checked at plan creation).
 // ---------------------------------------------------------------------------
-#ifndef CG_SPMV_UNROLL
-#define CG_SPMV_UNROLL 4
-#endif
 #ifndef CG_SPMV_MINB
 #define CG_SPMV_MINB 1
-#endif
-constexpr int kSpmvUnroll = CG_SPMV_UNROLL;
-#ifndef CG_GB
-#define CG_GB 8   // z gathers in flight per thread (global-CSR spmv)
 #endif
 template <bool CPLX, bool BATCH>
 __global__ void __launch_bounds__(CG_NT, CG_SPMV_MINB) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
@@ -254,36 +336,7 @@ __global__ void __launch_bounds__(CG_NT, CG_SPMV_MINB) k_cg_spmv(CgMat M, CgVec 
             if (act) {
                 const int64_t r1 = min(r0 + CG_SB * CG_CH, M.n);
                 for (int64_t i = r0; i < r1; i += CG_CH) {
-                    c128 acc = cmk(0.0, 0.0);
-                    const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
-                    if (BATCH) {
-                        // batches of CG_GB entries: indices, then all z gathers of the
-                        // batch in flight, then the ascending-q accumulation
-                        for (int32_t qb = q0; qb < q1; qb += CG_GB) {
-                            uint32_t cc[CG_GB];
-                            c128 zz[CG_GB];
-    #pragma unroll
-                            for (int k = 0; k < CG_GB; ++k) cc[k] = qb + k < q1 ? (uint32_t)__ldg(M.indices + qb + k) : 0u;
-    #pragma unroll
-                            for (int k = 0; k < CG_GB; ++k) zz[k] = qb + k < q1 ? zv[cc[k] * kp + lane] : cmk(0.0, 0.0);
-    #pragma unroll
-                            for (int k = 0; k < CG_GB; ++k) {
-                                if (qb + k < q1) {
-                                    const int32_t q = qb + k;
-                                    const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0,
-                                                              __ldg(M.b + q), sg);
-                                    acc = cadd(acc, cmul(e, zz[k]));
-                                }
-                            }
-                        }
-                    } else {
-#pragma unroll kSpmvUnroll
-                        for (int32_t q = q0; q < q1; ++q) {
-                            const uint32_t c = (uint32_t)__ldg(M.indices + q);
-                            const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
-                            acc = cadd(acc, cmul(e, zv[c * kp + lane]));
-                        }
-                    }
+                    const c128 acc = row_sz<CPLX, BATCH>(M, i, zv, kp, lane, sg);
                     const uint32_t o = (uint32_t)i * kp + lane;
                     const c128 pi = cadd(zv[o], cmul(beta, pv[o]));
                     const c128 qi = cadd(acc, cmul(beta, qv[o]));
@@ -506,24 +559,7 @@ __global__ void __launch_bounds__(CG1_NT) k_cg_spmv1(CgMat M, CgVec V, CgScal Sc
         const int64_t i = c * (CG_SB * CG_CH) + l;
         c128 term = cmk(0.0, 0.0);
         if (act && i < M.n) {
-            c128 acc = cmk(0.0, 0.0);
-            const int32_t q0 = __ldg(M.indptr + i), q1 = __ldg(M.indptr + i + 1);
-            for (int32_t qb = q0; qb < q1; qb += CG_GB) {
-                uint32_t cc[CG_GB];
-                c128 zz[CG_GB];
-#pragma unroll
-                for (int k = 0; k < CG_GB; ++k) cc[k] = qb + k < q1 ? (uint32_t)__ldg(M.indices + qb + k) : 0u;
-#pragma unroll
-                for (int k = 0; k < CG_GB; ++k) zz[k] = qb + k < q1 ? zv[cc[k]] : cmk(0.0, 0.0);
-#pragma unroll
-                for (int k = 0; k < CG_GB; ++k) {
-                    if (qb + k < q1) {
-                        const int32_t q = qb + k;
-                        const c128 e = form_entry(__ldg(M.ta + q), CPLX ? __ldg(M.ta_im + q) : 0.0, __ldg(M.b + q), sg);
-                        acc = cadd(acc, cmul(e, zz[k]));
-                    }
-                }
-            }
+            const c128 acc = row_sz<CPLX, true>(M, i, zv, 1u, 0, sg);
             const c128 pi = cadd(zv[i], cmul(beta, pv[i]));
             const c128 qi = cadd(acc, cmul(beta, qv[i]));
             pv[i] = pi;
@@ -1111,7 +1147,73 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     CGK(cudaMemcpyAsync(dta_, dta.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
     CGK(cudaMemcpyAsync(dtai_, dtai.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
     CGK(cudaMemcpyAsync(db_, db.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
-    im->M = CgMat{n, ip, ix, ta_, tai_, bb_, dta_, dtai_, db_};
+    im->M = CgMat{n, ip, ix, ta_, tai_, bb_, dta_, dtai_, db_, nullptr, nullptr};
+    {
+        // stencil classes for the narrow-layout spmv (see CgClass)
+        std::vector<uint8_t> cls((size_t)n, 255);
+        std::vector<CgClass> classes;
+        int64_t classed = 0;
+        if (!getenv("REXI_COCG_NOCLS")) {
+            std::unordered_map<std::string, int> ids;
+            int prev = -1;
+            std::string key;
+            auto matches = [&](int id, int64_t r, int32_t q0, int nz) {
+                const CgClass &C = classes[id];
+                if (C.nnz != nz) return false;
+                for (int k = 0; k < nz; ++k)
+                    if ((int64_t)d->indices[q0 + k] - r != C.off[k] || memcmp(&bb[q0 + k], &C.b[k], sizeof(double)))
+                        return false;
+                return true;
+            };
+            for (int64_t r = 0; r < n; ++r) {
+                const int32_t q0 = d->indptr[r], q1 = d->indptr[r + 1];
+                const int nz = q1 - q0;
+                if (nz <= 0 || nz > CG_CLS_MAXNNZ) continue;
+                if (prev >= 0 && matches(prev, r, q0, nz)) {
+                    cls[r] = (uint8_t)prev;
+                    ++classed;
+                    continue;
+                }
+                key.assign(reinterpret_cast<const char *>(&nz), sizeof nz);
+                for (int k = 0; k < nz; ++k) {
+                    const int32_t off = (int32_t)((int64_t)d->indices[q0 + k] - r);
+                    key.append(reinterpret_cast<const char *>(&off), sizeof off);
+                    key.append(reinterpret_cast<const char *>(&bb[q0 + k]), sizeof(double));
+                }
+                auto it = ids.find(key);
+                int id;
+                if (it != ids.end()) {
+                    id = it->second;
+                } else if ((int)classes.size() < CG_CLS_MAX) {
+                    CgClass C{};
+                    C.nnz = nz;
+                    for (int k = 0; k < nz; ++k) {
+                        C.off[k] = (int32_t)((int64_t)d->indices[q0 + k] - r);
+                        C.b[k] = bb[q0 + k];
+                    }
+                    id = (int)classes.size();
+                    classes.push_back(C);
+                    ids.emplace(key, id);
+                } else {
+                    prev = -1;
+                    continue;
+                }
+                cls[r] = (uint8_t)id;
+                prev = id;
+                ++classed;
+            }
+        }
+        if (classed * 2 >= n) {   // worth a table: most rows share few stencils
+            uint8_t *cls_;
+            CgClass *cl_;
+            CGA(cls_, (size_t)n);
+            CGA(cl_, sizeof(CgClass) * classes.size());
+            CGK(cudaMemcpyAsync(cls_, cls.data(), (size_t)n, cudaMemcpyHostToDevice, st));
+            CGK(cudaMemcpyAsync(cl_, classes.data(), sizeof(CgClass) * classes.size(), cudaMemcpyHostToDevice, st));
+            im->M.cls = cls_;
+            im->M.classes = cl_;
+        }
+    }
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&im->sms, cudaDevAttrMultiProcessorCount, dev);

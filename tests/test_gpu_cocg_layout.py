@@ -1,7 +1,9 @@
-"""GPU: COCG layout changes must not change the answer.  Repacking the live
-lanes into a prefix of the same width (cocg.cu cg_solve) is bitwise
-identical to the halving-only compaction (layout-independent reduction
-tree), on 2D and 3D pencils, plain and refined."""
+"""GPU: COCG layout and format changes must not change the answer.
+Repacking the live lanes into a prefix of the same width (cocg.cu cg_solve)
+is bitwise identical to the halving-only compaction (layout-independent
+reduction tree), and the narrow-layout spmv over stencil classes (CgClass:
+columns and B values from a per-class table) is bitwise identical to plain
+CSR, on 2D and 3D pencils, plain and refined."""
 import os
 import subprocess
 import sys
@@ -39,3 +41,11 @@ def test_prefix_repack_bitwise(c, m, refine, tmp_path):
     plain = _run(c, m, refine, 2, {"REXI_COCG_NOPREFIX": "1"}, tmp_path, "plain")
     assert np.all(np.isfinite(plain))
     assert np.array_equal(repacked, plain)
+
+
+@pytest.mark.parametrize("c,m,refine", [(3, 64, 1), (5, 12, 1), (4, 48, 0)])
+def test_stencil_classes_bitwise(c, m, refine, tmp_path):
+    classed = _run(c, m, refine, 2, {}, tmp_path, "cls")
+    plain = _run(c, m, refine, 2, {"REXI_COCG_NOCLS": "1"}, tmp_path, "nocls")
+    assert np.all(np.isfinite(plain))
+    assert np.array_equal(classed, plain)
