@@ -31,6 +31,7 @@ struct TriState {
     c64 *inv32 = nullptr;         // refinement, TMA path: level-0 inverse pivots as complex64
     c64 *rres32 = nullptr;        // refinement, TMA path: complex64 residual (aliases rres)
     float *r32[6] = {};           // refinement, TMA path: level-0 sub/sup row data rounded to float
+    c64 *l1_inv32 = nullptr, *l1_sup32 = nullptr, *l1_rw32 = nullptr;   // correction pass, level 1 (complex64)
     double *acc = nullptr;
     bool complex_a = false;       // A has an imaginary part: K2 keeps every residual product error-free
 };
@@ -341,6 +342,15 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
             DALLOC(T.r32[q], (size_t)nrow);
             CK(launch_to_f32(src32[q], T.r32[q], nrow, plan->stream));
         }
+        if (T.lv.size() >= 3 && T.lv[0].sym && !getenv("REXI_L1_FP64")) {
+            // the correction pass's level 1 in complex64 (level 1 is not the top)
+            const size_t e1 = (size_t)T.lv[1].n * kp;
+            DALLOC(T.l1_inv32, e1);
+            DALLOC(T.l1_sup32, e1);
+            DALLOC(T.l1_rw32, e1);
+            CK(launch_to_c64(T.lv[1].invd, T.l1_inv32, (int64_t)e1, plan->stream));
+            CK(launch_to_c64(T.lv[1].sup, T.l1_sup32, (int64_t)e1, plan->stream));
+        }
         T.rres32 = reinterpret_cast<c64 *>(T.rres);
         CK(cudaStreamSynchronize(plan->stream));
     }
@@ -393,7 +403,9 @@ int tri_mid(rexi_plan *plan, bool dd) {
     for (size_t l = 1; l + 1 < nl && (lc == 0 || (int)l < lc); ++l) {
         ProfScope ps(plan, "s1_lv");
         const bool d = l == 1 && dd;
-        if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 1, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
+        if (d && T.l1_inv32) CK(lv32_launch(T.lv[1], plan->S, 1, T.l1_inv32, T.l1_sup32, T.lv[0].ypdd, T.lv[0].lcdd,
+                                            T.l1_rw32, nullptr, st));
+        else if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 1, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
                                   d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, nullptr, st,
                                   d ? T.lv[1].X : nullptr));
         else if (d) CK(tri_launch_lv_dd(T.lv[1], plan->S, 1, T.lv[0].ypdd, T.lv[0].lcdd, nullptr, st));
@@ -411,7 +423,9 @@ int tri_mid(rexi_plan *plan, bool dd) {
     for (size_t l = lc > 0 ? (size_t)lc : nl - 1; l-- > 1;) {
         ProfScope ps(plan, "s3_lv");
         const bool d = l == 1 && dd;
-        if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 3, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
+        if (d && T.l1_inv32) CK(lv32_launch(T.lv[1], plan->S, 3, T.l1_inv32, T.l1_sup32, nullptr, nullptr,
+                                            T.l1_rw32, T.lv[2].X, st));
+        else if (use_tma(l)) CK(lv_launch_tma(T.lv[l], plan->S, 3, d ? nullptr : T.lv[l - 1].ypart, d ? nullptr : T.lv[l - 1].lc,
                                   d ? T.lv[0].ypdd : nullptr, d ? T.lv[0].lcdd : nullptr, T.lv[l + 1].X, st,
                                   d ? T.lv[1].X : nullptr));
         else if (d) CK(tri_launch_lv_dd(T.lv[1], plan->S, 3, T.lv[0].ypdd, T.lv[0].lcdd, T.lv[2].X, st));

@@ -817,6 +817,127 @@ __global__ void __launch_bounds__(L0_NT, LV_MINB) k_lv_tma(const __grid_constant
 }
 
 // ---------------------------------------------------------------------------
+// Level 1 of the correction pass in complex64 (like the level-0 correction):
+// complex64 copies of the level's inverse pivots and couplings, the rhs
+// combined from the double-double halves and rounded, stored (complex64) for
+// the level's S3; the level-2 rhs and the level-1 solution stay complex128.
+// ---------------------------------------------------------------------------
+struct Lv32Args {
+    LevelDev L;
+    ShiftDev S;
+    const c64 *inv32, *sup32;    // level 1, [n][kp]
+    const cdd *rdd_a, *rdd_b;    // PHASE 1: the double-double rhs halves
+    c64 *rw;                     // PHASE 1 writes, PHASE 3 reads: the rounded rhs rows
+    const c128 *Xnext;           // PHASE 3: level-2 solution
+};
+
+template <int M, int PHASE>
+__global__ void __launch_bounds__(L0_NT, LV_MINB) k_lv32(const __grid_constant__ Lv32Args a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    const int kp = a.S.kp;
+    const int bpc = L0_NT / kp;
+    const int T = bpc * M;
+    c64 *tinv = reinterpret_cast<c64 *>(smem + 128);
+    c64 *tsup = tinv + (size_t)T * kp;
+    const int b = threadIdx.x / kp, j = threadIdx.x % kp;
+    const int64_t n = a.L.n, P = a.L.P;
+    const int64_t row0 = (int64_t)blockIdx.x * T;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int64_t row1 = min(row0 + (int64_t)T, n);
+        const uint32_t tb = (uint32_t)((row1 - row0) * kp * sizeof(c64));
+        mbar_expect_tx(bar, 2 * tb);
+        bulk_g2s(tinv, a.inv32 + row0 * kp, tb, bar);
+        bulk_g2s(tsup, a.sup32 + row0 * kp, tb, bar);
+    }
+    const int64_t p = (int64_t)blockIdx.x * bpc + b;
+    const bool active = p < P;
+    const int64_t base = p * M;
+    const int cnt = active ? (int)min((int64_t)M, n - base) - 1 : -1;
+    c64 y[M];
+    c128 xs = cmk(0.0, 0.0), xn = cmk(0.0, 0.0);
+    if (active) {
+#pragma unroll
+        for (int q = 1; q < M; ++q) {
+            if (q <= cnt) {
+                if (PHASE == 1) {
+                    const int64_t e = (base + q) * kp + j;
+                    y[q] = to_c64(cdd_round(cdd_add(a.rdd_a[e], a.rdd_b[e])));
+                    a.rw[e] = y[q];
+                } else {
+                    y[q] = a.rw[(base + q) * kp + j];
+                }
+            }
+        }
+        if (PHASE == 3) {
+            xs = a.Xnext[p * kp + j];
+            if (p + 1 < P) xn = a.Xnext[(p + 1) * kp + j];
+        }
+    }
+    mbar_wait(bar, 0);
+    if (!active) return;
+    const c64 *ti = tinv + (size_t)b * M * kp + j;
+    const c64 *ts = tsup + (size_t)b * M * kp + j;
+    y[0] = to_c64(xs);
+#pragma unroll
+    for (int q = 1; q < M; ++q)
+        if (q <= cnt) y[q] = fmul(ti[q * kp], ffnma(y[q], ts[(q - 1) * kp], y[q - 1]));   // sub_q = sup_{q-1}
+    c64 ylast = y[0];
+#pragma unroll
+    for (int q = 1; q < M; ++q)
+        if (q == cnt) ylast = y[q];
+    c64 xnext = to_c64(xn);
+#pragma unroll
+    for (int q = M - 1; q >= 1; --q) {
+        if (q <= cnt) {
+            xnext = ffnma(y[q], ti[q * kp], fmul(ts[q * kp], xnext));
+            y[q] = xnext;
+        }
+    }
+    if (PHASE == 1) {
+        const c64 yfirst = cnt >= 1 ? y[1] : c64mk(0.f, 0.f);
+        const c64 ds = to_c64(cdd_round(cdd_add(a.rdd_a[base * kp + j], a.rdd_b[base * kp + j])));
+        a.L.ypart[p * kp + j] = to_c128(ffnma(ds, ts[0], yfirst));
+        if (p + 1 < P) {
+            const c64 m = fmul(ts[(M - 1) * kp], ylast);
+            a.L.lc[(p + 1) * kp + j] = cmk(-(double)m.x, -(double)m.y);
+        }
+        if (p == 0) a.L.lc[j] = cmk(0.0, 0.0);
+    } else {
+        a.L.X[base * kp + j] = xs;
+#pragma unroll
+        for (int q = 1; q < M; ++q)
+            if (q <= cnt) a.L.X[(base + q) * kp + j] = to_c128(y[q]);
+    }
+}
+
+cudaError_t lv32_launch(const LevelDev &L, const ShiftDev &S, int phase, const c64 *inv32, const c64 *sup32,
+                        const cdd *rdd_a, const cdd *rdd_b, c64 *rw, const c128 *Xnext, cudaStream_t st) {
+    Lv32Args a{};
+    a.L = L; a.S = S; a.inv32 = inv32; a.sup32 = sup32; a.rdd_a = rdd_a; a.rdd_b = rdd_b; a.rw = rw; a.Xnext = Xnext;
+    const int kp = S.kp;
+    const int64_t rows = (int64_t)(L0_NT / kp) * TRI_M;
+    const int64_t grid = (L.n + rows - 1) / rows;
+    const size_t smem = 128 + 2 * (size_t)rows * kp * sizeof(c64);
+    cudaError_t e;
+    if (phase == 1) {
+        e = cudaFuncSetAttribute(k_lv32<TRI_M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_lv32<TRI_M, 1><<<(unsigned)grid, L0_NT, smem, st>>>(a);
+    } else {
+        e = cudaFuncSetAttribute(k_lv32<TRI_M, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_lv32<TRI_M, 3><<<(unsigned)grid, L0_NT, smem, st>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // The small reduced levels in ONE thread-block-cluster launch: S1 up levels
 // l0..nl-2, the top solve, S3 down levels nl-2..l0, separated by cluster
 // barriers instead of kernel boundaries.  Each cluster CTA plays the role of

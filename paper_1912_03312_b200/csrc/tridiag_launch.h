@@ -48,6 +48,10 @@ cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const
                           const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st,
                           c128 *rw = nullptr);
 
+// level 1 of the refinement's correction pass in complex64 (tridiag_l0.cu)
+cudaError_t lv32_launch(const LevelDev &L, const ShiftDev &S, int phase, const c64 *inv32, const c64 *sup32,
+                        const cdd *rdd_a, const cdd *rdd_b, c64 *rw, const c128 *Xnext, cudaStream_t st);
+
 // levels l0..top..l0 in one cluster launch (tridiag_l0.cu); lv_chain_start
 // returns the first chained level (0: none) and the cluster size
 int lv_chain_start(const LevelDev *lv, int nl, int kp, int *cs);
