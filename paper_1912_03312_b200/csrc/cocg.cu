@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
 // (n * kp < 2^31 is checked at plan creation).
 // ---------------------------------------------------------------------------
 #ifndef CG_SPMV_MINB
-#define CG_SPMV_MINB 1
+#define CG_SPMV_MINB 3   // <= 85 registers: 3 CTAs/SM (the stencil-class path adds registers)
 #endif
 template <bool CPLX, bool BATCH>
 __global__ void __launch_bounds__(CG_NT, CG_SPMV_MINB) k_cg_spmv(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
