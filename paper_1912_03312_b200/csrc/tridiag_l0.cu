@@ -335,7 +335,7 @@ __device__ __forceinline__ void s1_body(const L0Args &a, const L0Layout &l, cons
 // rows go to rhs0 for K2 / S3ACC (padding rows stay zero).
 template <int M>
 #ifndef S1_MINB
-#define S1_MINB 4
+#define S1_MINB 4   // 128 registers + 60 B spills, 7 % faster than 3 CTAs/SM without (scripts/tune_l0minb.sh)
 #endif
 __global__ void __launch_bounds__(L0_NT, S1_MINB) k_l0_s1(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
 // Half the bytes of an fp64 correction (16 instead of 32 per row-shift).
 // ---------------------------------------------------------------------------
 #ifndef K3_MINB
-#define K3_MINB 8   // 93 -> 64 registers: 8 CTAs/SM (swept: scripts/tune_k3.sh)
+#define K3_MINB 7   // 72 registers, no spills (8: 64 + spills, equal time; scripts/tune_l0minb.sh)
 #endif
 // K3's shared memory: mbarrier | complex64 pivot tile T*kp | 6 float row
 // arrays (sub: tau a, tau a_im, b; sup: same) of Tp4 = T + 2 rounded to 4
@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
 // the sweep registers.  PHASE 1 -> reduced rhs of the next level, PHASE 3 -> X.
 // ---------------------------------------------------------------------------
 #ifndef LV_MINB
-#define LV_MINB 3
+#define LV_MINB 2   // 212 registers, no spills (3: 168 + 116-196 B spills, 1 % slower; scripts/tune_lv.sh)
 #endif
 struct LvArgs {
     LevelDev L;
