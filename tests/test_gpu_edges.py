@@ -126,3 +126,30 @@ def test_pinned_input_zero_copy_agrees(n, refine):
     two = p.step_host(u_pin, 2)                      # multi-step call (staged input, graphs)
     assert np.array_equal(two, p.step_host(zc, 1))
     stp.close()
+
+
+@pytest.mark.parametrize("k,refine", [(128, 1), (128, 0), (256, 1), (256, 0)])
+def test_wide_shift_counts_vs_truth(k, refine):
+    """K = 128 (the widest level-0 tile, 16 rows per CTA) and K = 256 (k_pad
+    beyond the TMA path: the general level kernels) against the truth
+    oracle: within 10x of the fp64 reference's own distance unrefined,
+    and <= 1e-9 refined"""
+    from paper_1912_03312_b200 import fixtures, rexi_prepare, rexi_step
+    from paper_1912_03312_b200.types import PartialFractionApproximation
+    from oracle.oracle import OraclePlan, rel_l2
+    p = fixtures.load_poles(128)
+    sh, w = np.asarray(p.shifts), np.asarray(p.weights)
+    if k == 256:   # a second, distinct copy of the pole set (the test is the solver, not the approximation)
+        sh, w = np.concatenate([sh, sh + 0.37j]), np.concatenate([w, 0.5 * w])
+    ap = PartialFractionApproximation(sh, w, p.domain_radius, 0.0)
+    n = 3000
+    sysm = _system(n)
+    u = np.exp(1j * np.arange(n) * 0.01) * (1 + 0.1 * np.cos(np.arange(n)))
+    stp = rexi_prepare(sysm, ap, 1e-3, sr_value=1.0, override_admissibility=True, refine=refine)
+    assert stp.stats["k_pad"] == k
+    u1 = rexi_step(stp, u)
+    stp.close()
+    orc = OraclePlan(sysm, ap, 1e-3)
+    truth = orc.step(u, "truth")
+    floor = rel_l2(orc.step(u, "reference"), truth)
+    assert rel_l2(u1, truth) <= (1e-9 if refine else 10 * floor + 1e-9), (rel_l2(u1, truth), floor)
