@@ -213,7 +213,10 @@ __device__ __forceinline__ c128 pick_last(const c128 (&y)[M], int cnt) {
 __device__ __forceinline__ c128 tile_c128(c128 v) { return v; }
 __device__ __forceinline__ c128 tile_c128(c64 v) { return to_c128(v); }
 
-template <int M, typename TT = c128>
+// DD = false (K3's correction sum): the terms beta_j dx_j are ~|x| * 1e-6 at
+// most, so a plain fp64 FMA chain per row (error ~1e-20 of |x|) replaces the
+// per-term TwoSum; the row total still enters the dd partial exactly.
+template <int M, typename TT = c128, bool DD = true>
 __device__ __forceinline__ void reduce_rows(const TT *tile, const L0Args &a, int64_t row0) {
     const int kp = a.S.kp;
     const int rows = (L0_NT / kp) * M;
@@ -221,14 +224,28 @@ __device__ __forceinline__ void reduce_rows(const TT *tile, const L0Args &a, int
     const int sub = threadIdx.x % tpr;
     const int64_t n = a.nout;
     for (int r = threadIdx.x / tpr; r < rows; r += L0_NT / tpr) {
-        ddacc re = {0.0, 0.0}, im = {0.0, 0.0};
-        for (int jj = sub; jj < kp; jj += tpr) {
-            const c128 b = a.S.beta[jj];
-            const c128 x = tile_c128(tile[r * kp + jj]);
-            ddacc_add(re, fma(b.x, x.x, -b.y * x.y));
-            ddacc_add(im, fma(b.x, x.y, b.y * x.x));
+        dd sre, sim;
+        if constexpr (DD) {
+            ddacc re = {0.0, 0.0}, im = {0.0, 0.0};
+            for (int jj = sub; jj < kp; jj += tpr) {
+                const c128 b = a.S.beta[jj];
+                const c128 x = tile_c128(tile[r * kp + jj]);
+                ddacc_add(re, fma(b.x, x.x, -b.y * x.y));
+                ddacc_add(im, fma(b.x, x.y, b.y * x.x));
+            }
+            sre = fast_two_sum(re.hi, re.lo);
+            sim = fast_two_sum(im.hi, im.lo);
+        } else {
+            double re = 0.0, im = 0.0;
+            for (int jj = sub; jj < kp; jj += tpr) {
+                const c128 b = a.S.beta[jj];
+                const c128 x = tile_c128(tile[r * kp + jj]);
+                re = fma(b.x, x.x, fma(-b.y, x.y, re));
+                im = fma(b.x, x.y, fma(b.y, x.x, im));
+            }
+            sre = dd{re, 0.0};
+            sim = dd{im, 0.0};
         }
-        dd sre = fast_two_sum(re.hi, re.lo), sim = fast_two_sum(im.hi, im.lo);
         for (int off = tpr >> 1; off > 0; off >>= 1) {
             dd ore, oim;
             ore.hi = __shfl_down_sync(0xffffffffu, sre.hi, off, tpr);
@@ -684,7 +701,7 @@ __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
         for (int q = 0; q < M; ++q) ti[q * kp] = c64mk(0.f, 0.f);
     }
     __syncthreads();
-    reduce_rows<M, c64>(tile, a, c.row0);
+    reduce_rows<M, c64, false>(tile, a, c.row0);
 }
 
 // ---------------------------------------------------------------------------
