@@ -452,7 +452,7 @@ int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
     }
     {
         ProfScope ps(plan, "l0_k2");
-        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres32, T.r32, T.n, T.complex_a, st));
+        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres32, T.inv32, T.r32, T.n, T.complex_a, st));
     }
     rc = tri_mid(plan, true);
     if (rc) return rc;

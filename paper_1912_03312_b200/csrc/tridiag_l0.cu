@@ -32,8 +32,11 @@ constexpr int L0_ROWPAD = 2;    // extra staged rows (next interface row + 16-B 
 #define K2_RES_UNROLL 5   // swept: scripts/tune_k2u.sh (3: +1.2 %, 15: +15 %)
 #endif
 constexpr int K2_UNROLL = K2_RES_UNROLL;
+#ifndef K2_ONE_TILE
+#define K2_ONE_TILE 1   // x overwrites the pivot tile; the correction reads complex64 pivots from HBM
+#endif
 #ifndef K2_MINB
-#define K2_MINB 3
+#define K2_MINB 4
 #endif
 struct L0Args {
     L0Dev z;
@@ -476,9 +479,9 @@ __global__ void __launch_bounds__(L0_NT, S3_MINB) k_l0_s3acc(L0Args a) {
 // ---------------------------------------------------------------------------
 template <int M, bool FULL>
 __device__ __forceinline__ void k2_solve(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
-                                         c128 xn, c128 (&y)[M]) {
+                                         c128 xn, c128 (&y)[M], c128 *xt) {
     const c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
-    c128 *tc = l.t1 + (size_t)c.lr0 * c.kp + c.j;
+    c128 *tc = xt + (size_t)c.lr0 * c.kp + c.j;   // may alias ti: slot q is read before x_q overwrites it
     const RowView &rv = l.rv;
     const int kp = c.kp;
     y[0] = xs;
@@ -489,10 +492,10 @@ __device__ __forceinline__ void k2_solve(const L0Args &a, const L0Layout &l, con
 
 template <int M, bool FULL, bool EXACT, bool SYM>
 __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
-                                          c128 xn, c128 (&y)[M]) {
+                                          c128 xn, c128 (&y)[M], c128 *xt) {
     static_assert(FULL, "level 0 is padded to full blocks");
     const c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
-    c128 *tc = l.t1 + (size_t)c.lr0 * c.kp + c.j;
+    c128 *tc = xt + (size_t)c.lr0 * c.kp + c.j;
     const RowView &rv = l.rv;
     const int kp = c.kp, j = c.j;
     constexpr int cnt = M - 1;
@@ -538,22 +541,27 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
         x0 = xp;
         esub = eup;
     }
-    // correction reduce: S1 with rhs = r, in complex64 like K3's correction
-    // S3 (pivots rounded from the staged fp64 tile, entries formed in fp32)
+    // correction reduce: S1 with rhs = r, in complex64 with K3's pivots
+    // (K2_ONE_TILE: the complex64 pivot copy in HBM, as K3 reads it; else
+    // rounded from the staged fp64 tile -- the same values), entries formed
+    // in fp32
     (void)y;
+    (void)ti;
     const c64 sg32 = to_c64(c.sg);
+    const c64 *iv32 = a.inv32 + c.base * kp + j;
+    auto piv = [&](int q) -> c64 { return K2_ONE_TILE ? __ldg(iv32 + q * kp) : to_c64(ti[q * kp]); };
     c64 yf[M];
     yf[0] = c64mk(0.f, 0.f);
 #pragma unroll
     for (int q = 1; q < M; ++q) {
         const c64 rq = *reinterpret_cast<const c64 *>(tc + (q - 1) * kp);
-        yf[q] = fmul(to_c64(ti[q * kp]), ffnma(rq, rv.sub32(c.lr0 + q, sg32), yf[q - 1]));
+        yf[q] = fmul(piv(q), ffnma(rq, rv.sub32(c.lr0 + q, sg32), yf[q - 1]));
     }
     const c64 ylast = yf[M - 1];
     c64 xnext = c64mk(0.f, 0.f);
 #pragma unroll
     for (int q = M - 1; q >= 1; --q) {
-        xnext = ffnma(yf[q], to_c64(ti[q * kp]), fmul(rv.sup32(c.lr0 + q, sg32), xnext));
+        xnext = ffnma(yf[q], piv(q), fmul(rv.sup32(c.lr0 + q, sg32), xnext));
         yf[q] = xnext;
     }
     const c64 m1 = fmul(rv.sup32(c.lr0, sg32), yf[1]);
@@ -571,11 +579,13 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
     if (c.p == 0) a.L.lcdd[j] = cdd_zero();
 }
 
+constexpr int K2_FLAGS = K2_ONE_TILE ? (ST_RHS | ST_DIA | ST_R32) : (ST_RHS | ST_DIA | ST_TILE2 | ST_R32);
 template <int M, bool EXACT>
 __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int flags = ST_RHS | ST_DIA | ST_TILE2 | ST_R32;
+    constexpr int flags = K2_FLAGS;
     const L0Layout l = carve(smem, a.S.kp, M, flags);
+    c128 *const xt = K2_ONE_TILE ? l.t0 : l.t1;
     const Ctx c = make_ctx(a, M);
     l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, flags & ~ST_TILE2);
 #ifndef K2_PF
@@ -606,17 +616,17 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
     mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
     c128 y[M];
     if (c.active) {
-        k2_solve<M, true>(a, l, c, xs, xn, y);
+        k2_solve<M, true>(a, l, c, xs, xn, y, xt);
     } else {
-        c128 *tc = l.t1 + (size_t)c.lr0 * c.kp + c.j;
+        c128 *tc = xt + (size_t)c.lr0 * c.kp + c.j;
 #pragma unroll
         for (int q = 0; q < M; ++q) tc[q * c.kp] = cmk(0.0, 0.0);
     }
     __syncthreads();
-    reduce_rows<M>(l.t1, a, c.row0);
+    reduce_rows<M>(xt, a, c.row0);
     if (!c.active) return;
-    if (a.L.sym) k2_refine<M, true, EXACT, true>(a, l, c, xs, xn, y);
-    else k2_refine<M, true, EXACT, false>(a, l, c, xs, xn, y);
+    if (a.L.sym) k2_refine<M, true, EXACT, true>(a, l, c, xs, xn, y, xt);
+    else k2_refine<M, true, EXACT, false>(a, l, c, xs, xn, y, xt);
 }
 
 // ---------------------------------------------------------------------------
@@ -1223,11 +1233,11 @@ cudaError_t l0_launch_s3acc(const L0Dev &z, const LevelDev &L, const ShiftDev &S
 }
 
 cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
-                         const c128 *X1, double *acc, c64 *rres, const float *const *r32, int64_t nout,
-                         bool exact_residual, cudaStream_t st) {
+                         const c128 *X1, double *acc, c64 *rres, const c64 *inv32, const float *const *r32,
+                         int64_t nout, bool exact_residual, cudaStream_t st) {
     L0Args a{};
     a.nout = nout;
-    a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0; a.X1 = X1; a.acc = acc; a.rres_out = rres;
+    a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0; a.X1 = X1; a.acc = acc; a.rres_out = rres; a.inv32 = inv32;
     a.acc_add = 0; a.final_out = 0;
     {
         int dev = 0, sms = 148;
@@ -1237,8 +1247,8 @@ cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
         if (const char *e = getenv("REXI_K2_PF")) a.pf_dist = (int64_t)(atof(e) * sms * K2_MINB);
     }
     for (int q = 0; q < 6; ++q) a.r32[q] = r32[q];
-    if (exact_residual) return launch_l0(k_l0_k2<TRI_M, true>, a, ST_RHS | ST_DIA | ST_TILE2 | ST_R32, st);
-    return launch_l0(k_l0_k2<TRI_M, false>, a, ST_RHS | ST_DIA | ST_TILE2 | ST_R32, st);
+    if (exact_residual) return launch_l0(k_l0_k2<TRI_M, true>, a, K2_FLAGS, st);
+    return launch_l0(k_l0_k2<TRI_M, false>, a, K2_FLAGS, st);
 }
 
 cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *X1,
