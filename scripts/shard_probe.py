@@ -27,4 +27,14 @@ for world in (1, 2, 4, 8):
         p.step_partial(u.data_ptr(), part.data_ptr())
     torch.cuda.synchronize(); dt = (time.perf_counter() - t) / steps
     print(f"cfg{c} world {world}: shard K={k} {dt*1e3:.3f} ms/step (speedup vs world 1 at equal exchange: see first line)", flush=True)
+    if os.environ.get("SHARD_PROF"):
+        # per-kernel device time of the same steps (CUDA events around each launch)
+        p.profile(True)
+        for _ in range(steps):
+            p.step_partial(u.data_ptr(), part.data_ptr())
+        torch.cuda.synchronize()
+        rep = p.profile_report()
+        p.profile(False)
+        print("   " + ", ".join(f"{kn}: {v[1] / steps * 1e3:.1f} us x{v[0] // steps}" for kn, v in
+                                 sorted(rep.items(), key=lambda kv: -kv[1][1])), flush=True)
     p.close() if hasattr(p, "close") else None
