@@ -148,6 +148,16 @@ def l2_note(n, k):
             "small config, reported as such")
 
 
+def fp64_peak():
+    """Measured FP64 issue peak (profiles/r01_fp64_peak.json, written by
+    scripts/micro/dfma_peak.cu on a B200 of this pool)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
 def load_traffic(name):
     """ncu evidence for a kernel (profiles/ncu_traffic.json, from one
     `ncu --set full` capture): DRAM bytes per launch and FP64-pipe use."""
@@ -418,6 +428,21 @@ def main():
             # the double-double kernels are FP64-issue bound, not HBM bound
             roof["fp64_pipe_pct"] = ev["fp64_pipe_pct"]
             roof["ncu_capture"] = ev.get("capture")
+        fp = fp64_peak()
+        if ev.get("fp64_inst_per_row_shift") and fp and not name.startswith("cg"):
+            # t_roof = max(B_alg / HBM peak, F_alg / FP64 peak); FP64
+            # work as thread-level DADD/DMUL/DFMA instructions (ncu counts of one
+            # cfg 2 launch, per row-shift) against the measured DFMA issue rate
+            inst = ev["fp64_inst_per_row_shift"] * n * kshard
+            t_hbm = b / (peak * 1e9) * 1e3 if b else 0.0
+            t_fp = inst / fp["dfma_per_s"] * 1e3
+            roof["fp64"] = {"inst_per_launch": inst, "achieved_inst_per_s": inst / (avg_ms / 1e3),
+                            "peak_inst_per_s": fp["dfma_per_s"], "frac": (inst / (avg_ms / 1e3)) / fp["dfma_per_s"],
+                            "peak_source": "profiles/r01_fp64_peak.json (scripts/micro/dfma_peak.cu)",
+                            "count_source": ev.get("fp64_inst_src")}
+            roof["t_roof_ms"] = max(t_hbm, t_fp)
+            roof["t_roof_bound"] = "fp64" if t_fp > t_hbm else "hbm"
+            roof["t_roof_frac"] = max(t_hbm, t_fp) / avg_ms
 
     if rank == 0:
         cpu = None
