@@ -219,40 +219,25 @@ __device__ __forceinline__ c128 pick_last(const c128 (&y)[M], int cnt) {
 __device__ __forceinline__ c128 tile_c128(c128 v) { return v; }
 __device__ __forceinline__ c128 tile_c128(c64 v) { return to_c128(v); }
 
-// DD = false (K3's correction sum): the terms beta_j dx_j are ~|x| * 1e-6 at
-// most, so a plain fp64 FMA chain per row (error ~1e-20 of |x|) replaces the
-// per-term TwoSum; the row total still enters the dd partial exactly.
-template <int M, typename TT = c128, bool DD = true>
+template <int M, typename TT = c128>
 __device__ __forceinline__ void reduce_rows(const TT *tile, const L0Args &a, int64_t row0) {
     const int kp = a.S.kp;
-    const int rows = (L0_NT >> lg2(kp)) * M;
-    const int tpr = kp >= M ? kp / M : 1;   // L0_NT / rows
-    const int ltpr = lg2(tpr);
-    const int sub = threadIdx.x & (tpr - 1);
+    const int rows = (L0_NT / kp) * M;
+    const int tpr = L0_NT / rows > 0 ? L0_NT / rows : 1;
+    const int sub = threadIdx.x % tpr;
     const int64_t n = a.nout;
-    for (int r = threadIdx.x >> ltpr; r < rows; r += L0_NT >> ltpr) {
-        dd sre, sim;
-        if constexpr (DD) {
-            ddacc re = {0.0, 0.0}, im = {0.0, 0.0};
-            for (int jj = sub; jj < kp; jj += tpr) {
-                const c128 b = a.S.beta[jj];
-                const c128 x = tile_c128(tile[r * kp + jj]);
-                ddacc_add(re, fma(b.x, x.x, -b.y * x.y));
-                ddacc_add(im, fma(b.x, x.y, b.y * x.x));
-            }
-            sre = fast_two_sum(re.hi, re.lo);
-            sim = fast_two_sum(im.hi, im.lo);
-        } else {
-            double re = 0.0, im = 0.0;
-            for (int jj = sub; jj < kp; jj += tpr) {
-                const c128 b = a.S.beta[jj];
-                const c128 x = tile_c128(tile[r * kp + jj]);
-                re = fma(b.x, x.x, fma(-b.y, x.y, re));
-                im = fma(b.x, x.y, fma(b.y, x.x, im));
-            }
-            sre = dd{re, 0.0};
-            sim = dd{im, 0.0};
+    for (int r = threadIdx.x / tpr; r < rows; r += L0_NT / tpr) {
+        // the dd accumulation keeps the rounded row sum independent of how
+        // the lanes are grouped (k_pad, sharding): a plain fp64 chain here
+        // broke the bitwise sharded-vs-single equality of the refined path
+        ddacc re = {0.0, 0.0}, im = {0.0, 0.0};
+        for (int jj = sub; jj < kp; jj += tpr) {
+            const c128 b = a.S.beta[jj];
+            const c128 x = tile_c128(tile[r * kp + jj]);
+            ddacc_add(re, fma(b.x, x.x, -b.y * x.y));
+            ddacc_add(im, fma(b.x, x.y, b.y * x.x));
         }
+        dd sre = fast_two_sum(re.hi, re.lo), sim = fast_two_sum(im.hi, im.lo);
         for (int off = tpr >> 1; off > 0; off >>= 1) {
             dd ore, oim;
             ore.hi = __shfl_down_sync(0xffffffffu, sre.hi, off, tpr);
@@ -648,6 +633,9 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
 // pivots for the lane sum, which is accumulated in double-double as before.
 // Half the bytes of an fp64 correction (16 instead of 32 per row-shift).
 // ---------------------------------------------------------------------------
+#ifndef K3_DIV
+#define K3_DIV 1   // scripts/tune_k3div.sh: equal within noise
+#endif
 #ifndef K3_MINB
 #define K3_MINB 7   // 72 registers, no spills (8: 64 + spills, equal time; scripts/tune_l0minb.sh)
 #endif
@@ -667,7 +655,7 @@ __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
     c64 *tile = reinterpret_cast<c64 *>(smem + 128);
     float *rows = reinterpret_cast<float *>(tile + (size_t)T * kp);
-    const Ctx c = make_ctx(a, M);
+    const Ctx c = make_ctx<K3_DIV>(a, M);
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
@@ -719,7 +707,7 @@ __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
         for (int q = 0; q < M; ++q) ti[q * kp] = c64mk(0.f, 0.f);
     }
     __syncthreads();
-    reduce_rows<M, c64, false>(tile, a, c.row0);
+    reduce_rows<M, c64>(tile, a, c.row0);
 }
 
 // ---------------------------------------------------------------------------
