@@ -1,4 +1,4 @@
-"""Summarise ncu captures: python scripts/ncu_summary.py raw <rep>  |  launches <csv>"""
+"""Summarise ncu captures: python scripts/ncu_summary.py raw <rep>  |  launches <csv> [first last n]"""
 import csv, collections, subprocess, sys
 
 def raw(rep):
@@ -18,21 +18,34 @@ def raw(rep):
         vals = sorted(((float(r[i]) if r[i] else 0.0, hdr[i][34:-23]) for i in st), reverse=True)[:5]
         print("   stalls: " + ", ".join(f"{n}={v:.2f}" for v, n in vals))
 
-def launches(path):
+def launches(path, first=None, last=None, nlast=1):
+    """Per-kernel totals of a launch list; optionally only the launches from
+    the first one whose name contains `first` through the `nlast`-th one whose
+    name contains `last` (e.g. the device-resident steps of a run)."""
     rows = list(csv.reader(open(path)))
     for i, r in enumerate(rows):
         if r and r[0] == "ID":
             hdr = r; start = i + 1; break
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     agg = collections.OrderedDict()
+    on, seen = first is None, 0
     for r in rows[start:]:
         if len(r) <= vi: continue
+        name = r[ki].split("(")[0]
+        if not on and first in name: on = True
+        if not on: continue
         v = float(r[vi].replace(",", "")); u = r[ui]
         v = v / 1e6 if u in ("nsecond", "ns") else (v / 1e3 if u in ("usecond", "us") else (v if u in ("msecond", "ms") else v * 1e3))
-        a = agg.setdefault(r[ki].split("(")[0], [0, 0.0]); a[0] += 1; a[1] += v
+        a = agg.setdefault(name, [0, 0.0]); a[0] += 1; a[1] += v
+        if last is not None and last in name:
+            seen += 1
+            if seen >= nlast: break
     tot = sum(t for _, t in agg.values())
     for k, (c, t) in agg.items():
         print(f"{k:28s} {c:6d} launches {t:10.3f} ms  ({100*t/tot:5.1f}%)  avg {1e3*t/c:9.1f} us")
 
 if __name__ == "__main__":
-    {"raw": raw, "launches": launches}[sys.argv[1]](sys.argv[2])
+    if sys.argv[1] == "launches" and len(sys.argv) > 3:
+        launches(sys.argv[2], sys.argv[3], sys.argv[4], int(sys.argv[5]))
+    else:
+        {"raw": raw, "launches": launches}[sys.argv[1]](sys.argv[2])
