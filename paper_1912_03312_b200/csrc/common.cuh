@@ -90,6 +90,17 @@ __device__ __forceinline__ cdd cdd_fma(cdd acc, c128 w, c128 x) {
 __device__ __forceinline__ cdd cdd_add(cdd a, cdd b) {
     return {dd_add(a.re, b.re), dd_add(a.im, b.im)};
 }
+// a complex double-double stored as (fp64 hi, fp32 lo): 24 instead of 32 B.
+// The refined 1D step keeps the correction's interface halves in it: they
+// only need to cancel to ~1e-13 of hi and then be accurate to ~1e-5.  The
+// pair is renormalised first (the accumulators' low words also carry whole
+// small products), so rounding lo to fp32 costs ~2^-77 of |hi|.
+struct cdh { double hr, hi; float lr, li; };
+__device__ __forceinline__ cdh cdh_pack(cdd a) {
+    const dd r = two_sum(a.re.hi, a.re.lo), i = two_sum(a.im.hi, a.im.lo);
+    return {r.hi, i.hi, __double2float_rn(r.lo), __double2float_rn(i.lo)};
+}
+__device__ __forceinline__ cdd cdh_unpack(cdh h) { return {{h.hr, (double)h.lr}, {h.hi, (double)h.li}}; }
 __device__ __forceinline__ c128 cdd_round(cdd a) {
     return cmk(__dadd_rn(a.re.hi, a.re.lo), __dadd_rn(a.im.hi, a.im.lo));
 }

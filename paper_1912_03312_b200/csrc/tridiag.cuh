@@ -47,7 +47,7 @@ struct LevelDev {
     c128 *ypart, *lc;               // S1 outputs: next-level rhs = ypart + lc  [P][kp]
     c128 *X;                        // solution  [n][kp]
     c128 *phiF, *phiL, *psiF, *psiL;// factor tips [P][kp]
-    cdd *ypdd, *lcdd;               // refinement (level 0): dd reduced rhs of the correction
+    cdh *ypdd, *lcdd;               // refinement (level 0): dd reduced rhs of the correction (fp64 hi, fp32 lo)
 };
 
 struct ShiftDev {

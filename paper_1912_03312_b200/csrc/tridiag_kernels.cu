@@ -14,7 +14,7 @@ struct BlkArgs {
     const c128 *rhs0;                 // RHS_L0: shared rhs [n]
     const c128 *rin_a, *rin_b;        // RHS_LV: previous level ypart / lc [n][kp]
     const c128 *rst;                  // RHS_ST: stored per-shift rhs [n][kp]
-    const cdd *rdd_a, *rdd_b;         // RHS_LVDD: previous level dd ypart / lc
+    const cdh *rdd_a, *rdd_b;         // RHS_LVDD: previous level dd ypart / lc
     const c128 *Xnext;                // S3: next-level solution [P][kp]
     double *acc;                      // dd partial, SoA 4*n
     c128 *uout;                       // rounded output (final_out)
@@ -27,7 +27,7 @@ __device__ __forceinline__ c128 rhs_at(const BlkArgs &a, int64_t i, int j) {
     const int kp = a.S.kp;
     if constexpr (RHS == RHS_L0) return a.rhs0[i];
     else if constexpr (RHS == RHS_LV) return cadd(a.rin_a[i * kp + j], a.rin_b[i * kp + j]);
-    else if constexpr (RHS == RHS_LVDD) return cdd_round(cdd_add(a.rdd_a[i * kp + j], a.rdd_b[i * kp + j]));
+    else if constexpr (RHS == RHS_LVDD) return cdd_round(cdd_add(cdh_unpack(a.rdd_a[i * kp + j]), cdh_unpack(a.rdd_b[i * kp + j])));
     else return a.rst[i * kp + j];
 }
 
@@ -212,15 +212,15 @@ __global__ void k_residual(L0Dev z, LevelDev L, ShiftDev S, const c128 *__restri
 // Top level: direct solve, one thread per shift
 // ---------------------------------------------------------------------------
 __global__ void k_top_solve(LevelDev L, ShiftDev S, const c128 *__restrict__ rin_a,
-                            const c128 *__restrict__ rin_b, const cdd *__restrict__ rdd_a,
-                            const cdd *__restrict__ rdd_b) {
+                            const c128 *__restrict__ rin_b, const cdh *__restrict__ rdd_a,
+                            const cdh *__restrict__ rdd_b) {
     const int kp = S.kp;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= kp) return;
     const int64_t n = L.n;
     c128 yp = cmk(0.0, 0.0);
     for (int64_t i = 0; i < n; ++i) {
-        c128 d = rdd_a ? cdd_round(cdd_add(rdd_a[i * kp + j], rdd_b[i * kp + j]))
+        c128 d = rdd_a ? cdd_round(cdd_add(cdh_unpack(rdd_a[i * kp + j]), cdh_unpack(rdd_b[i * kp + j])))
                        : cadd(rin_a[i * kp + j], rin_b[i * kp + j]);
         c128 ai = L.sym ? (i > 0 ? L.sup[(i - 1) * kp + j] : cmk(0.0, 0.0)) : L.sub[i * kp + j];
         yp = cmul(L.invd[i * kp + j], cfnma(d, ai, yp));
@@ -447,14 +447,14 @@ cudaError_t tri_launch_top_solve(const LevelDev &L, const ShiftDev &S, const c12
     return cudaGetLastError();
 }
 
-cudaError_t tri_launch_top_solve_dd(const LevelDev &L, const ShiftDev &S, const cdd *rdd_a,
-                                    const cdd *rdd_b, cudaStream_t st) {
+cudaError_t tri_launch_top_solve_dd(const LevelDev &L, const ShiftDev &S, const cdh *rdd_a,
+                                    const cdh *rdd_b, cudaStream_t st) {
     k_top_solve<<<(S.kp + 63) / 64, 64, 0, st>>>(L, S, nullptr, nullptr, rdd_a, rdd_b);
     return cudaGetLastError();
 }
 
-cudaError_t tri_launch_lv_dd(const LevelDev &L, const ShiftDev &S, int phase, const cdd *rdd_a,
-                             const cdd *rdd_b, const c128 *Xnext, cudaStream_t st) {
+cudaError_t tri_launch_lv_dd(const LevelDev &L, const ShiftDev &S, int phase, const cdh *rdd_a,
+                             const cdh *rdd_b, const c128 *Xnext, cudaStream_t st) {
     BlkArgs a{};
     a.L = L; a.S = S; a.rdd_a = rdd_a; a.rdd_b = rdd_b; a.Xnext = Xnext;
     if (phase == 1) return launch_block<false, RHS_LVDD, 1, false, false>(a, st);

@@ -561,15 +561,15 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
     const c128 t1 = cmk(-(double)m1.x, -(double)m1.y);
     ddacc_add(p1re, t1.x);
     ddacc_add(p1im, t1.y);
-    a.L.ypdd[c.p * kp + j] = cdd{{p1re.hi, p1re.lo}, {p1im.hi, p1im.lo}};
+    a.L.ypdd[c.p * kp + j] = cdh_pack(cdd{{p1re.hi, p1re.lo}, {p1im.hi, p1im.lo}});
     if (has_next) {
         const c64 m2 = fmul(rv.sub32(c.lr0 + M, sg32), ylast);
         const c128 t2 = cmk(-(double)m2.x, -(double)m2.y);
         ddacc_add(p2re, t2.x);
         ddacc_add(p2im, t2.y);
-        a.L.lcdd[(c.p + 1) * kp + j] = cdd{{p2re.hi, p2re.lo}, {p2im.hi, p2im.lo}};
+        a.L.lcdd[(c.p + 1) * kp + j] = cdh_pack(cdd{{p2re.hi, p2re.lo}, {p2im.hi, p2im.lo}});
     }
-    if (c.p == 0) a.L.lcdd[j] = cdd_zero();
+    if (c.p == 0) a.L.lcdd[j] = cdh_pack(cdd_zero());
 }
 
 constexpr int K2_FLAGS = K2_ONE_TILE ? (ST_RHS | ST_DIA | ST_R32) : (ST_RHS | ST_DIA | ST_TILE2 | ST_R32);
@@ -722,7 +722,7 @@ struct LvArgs {
     LevelDev L;
     ShiftDev S;
     const c128 *rin_a, *rin_b;   // previous level ypart / lc
-    const cdd *rdd_a, *rdd_b;    // or their double-double versions (correction pass)
+    const cdh *rdd_a, *rdd_b;    // or their double-double versions (correction pass)
     const c128 *Xnext;
     c128 *rw;                    // SRC 1, PHASE 1: the rounded rhs rows, reused by the level's S3
 };
@@ -730,7 +730,7 @@ struct LvArgs {
 struct LvPtrs {
     const c128 *inv, *sup;          // staged tiles (+ lane offset)
     const c128 *ra, *rb;
-    const cdd *da, *db;
+    const cdh *da, *db;
     const c128 *Xn;
     c128 *ypart, *lc, *X;
     c128 *rw;
@@ -741,7 +741,7 @@ struct LvPtrs {
 enum { LV_SRC_PLAIN = 0, LV_SRC_DD = 1, LV_SRC_STORED = 2 };
 template <int SRC>
 __device__ __forceinline__ c128 lv_rhs(const LvPtrs &q, int64_t i, int j, int kp) {
-    if constexpr (SRC == LV_SRC_DD) return cdd_round(cdd_add(q.da[i * kp + j], q.db[i * kp + j]));
+    if constexpr (SRC == LV_SRC_DD) return cdd_round(cdd_add(cdh_unpack(q.da[i * kp + j]), cdh_unpack(q.db[i * kp + j])));
     else if constexpr (SRC == LV_SRC_STORED) return q.ra[i * kp + j];
     else return cadd(q.ra[i * kp + j], q.rb[i * kp + j]);
 }
@@ -849,7 +849,7 @@ struct Lv32Args {
     LevelDev L;
     ShiftDev S;
     const c64 *inv32, *sup32;    // level 1, [n][kp]
-    const cdd *rdd_a, *rdd_b;    // PHASE 1: the double-double rhs halves
+    const cdh *rdd_a, *rdd_b;    // PHASE 1: the double-double rhs halves
     c64 *rw;                     // PHASE 1 writes, PHASE 3 reads: the rounded rhs rows
     const c128 *Xnext;           // PHASE 3: level-2 solution
 };
@@ -890,7 +890,7 @@ __global__ void __launch_bounds__(L0_NT, LV_MINB) k_lv32(const __grid_constant__
             if (q <= cnt) {
                 if (PHASE == 1) {
                     const int64_t e = (base + q) * kp + j;
-                    y[q] = to_c64(cdd_round(cdd_add(a.rdd_a[e], a.rdd_b[e])));
+                    y[q] = to_c64(cdd_round(cdd_add(cdh_unpack(a.rdd_a[e]), cdh_unpack(a.rdd_b[e]))));
                     a.rw[e] = y[q];
                 } else {
                     y[q] = a.rw[(base + q) * kp + j];
@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(L0_NT, LV_MINB) k_lv32(const __grid_constant__
     }
     if (PHASE == 1) {
         const c64 yfirst = cnt >= 1 ? y[1] : c64mk(0.f, 0.f);
-        const c64 ds = to_c64(cdd_round(cdd_add(a.rdd_a[base * kp + j], a.rdd_b[base * kp + j])));
+        const c64 ds = to_c64(cdd_round(cdd_add(cdh_unpack(a.rdd_a[base * kp + j]), cdh_unpack(a.rdd_b[base * kp + j]))));
         a.L.ypart[p * kp + j] = to_c128(ffnma(ds, ts[0], yfirst));
         if (p + 1 < P) {
             const c64 m = fmul(ts[(M - 1) * kp], ylast);
@@ -940,7 +940,7 @@ __global__ void __launch_bounds__(L0_NT, LV_MINB) k_lv32(const __grid_constant__
 }
 
 cudaError_t lv32_launch(const LevelDev &L, const ShiftDev &S, int phase, const c64 *inv32, const c64 *sup32,
-                        const cdd *rdd_a, const cdd *rdd_b, c64 *rw, const c128 *Xnext, cudaStream_t st) {
+                        const cdh *rdd_a, const cdh *rdd_b, c64 *rw, const c128 *Xnext, cudaStream_t st) {
     Lv32Args a{};
     a.L = L; a.S = S; a.inv32 = inv32; a.sup32 = sup32; a.rdd_a = rdd_a; a.rdd_b = rdd_b; a.rw = rw; a.Xnext = Xnext;
     const int kp = S.kp;
@@ -1102,7 +1102,7 @@ cudaError_t lv_launch_chain(const LevelDev *lv, int nl, int l0, int cs, const Sh
 }
 
 cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,
-                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st, c128 *rw) {
+                          const cdh *rdd_a, const cdh *rdd_b, const c128 *Xnext, cudaStream_t st, c128 *rw) {
     LvArgs a{};
     a.L = L; a.S = S; a.rin_a = rin_a; a.rin_b = rin_b; a.rdd_a = rdd_a; a.rdd_b = rdd_b; a.Xnext = Xnext;
     const int kp = S.kp;

@@ -25,10 +25,10 @@ cudaError_t tri_launch_transpose(const c128 *X, int64_t n, int kp, int k, c128 *
 cudaError_t launch_combine(const double *parts, int g, int64_t n, c128 *out, cudaStream_t st);
 
 // levels >= 1 reading the double-double reduced rhs of the correction pass
-cudaError_t tri_launch_lv_dd(const LevelDev &L, const ShiftDev &S, int phase, const cdd *rdd_a,
-                             const cdd *rdd_b, const c128 *Xnext, cudaStream_t st);
-cudaError_t tri_launch_top_solve_dd(const LevelDev &L, const ShiftDev &S, const cdd *rdd_a,
-                                    const cdd *rdd_b, cudaStream_t st);
+cudaError_t tri_launch_lv_dd(const LevelDev &L, const ShiftDev &S, int phase, const cdh *rdd_a,
+                             const cdh *rdd_b, const c128 *Xnext, cudaStream_t st);
+cudaError_t tri_launch_top_solve_dd(const LevelDev &L, const ShiftDev &S, const cdh *rdd_a,
+                                    const cdh *rdd_b, cudaStream_t st);
 
 // TMA-fed kernel for levels >= 1 of symmetric pencils (tridiag_l0.cu)
 // one-launch multi-step loop for small 1D plans (tridiag_persist.cu)
@@ -45,12 +45,12 @@ inline int64_t lv_tma_ctas(int64_t n, int kp) {   // grid of lv_launch_tma
 // rw (correction pass, dd rhs): phase 1 stores the rounded rhs rows there,
 // phase 3 reads them back instead of re-combining the double-double halves
 cudaError_t lv_launch_tma(const LevelDev &L, const ShiftDev &S, int phase, const c128 *rin_a, const c128 *rin_b,
-                          const cdd *rdd_a, const cdd *rdd_b, const c128 *Xnext, cudaStream_t st,
+                          const cdh *rdd_a, const cdh *rdd_b, const c128 *Xnext, cudaStream_t st,
                           c128 *rw = nullptr);
 
 // level 1 of the refinement's correction pass in complex64 (tridiag_l0.cu)
 cudaError_t lv32_launch(const LevelDev &L, const ShiftDev &S, int phase, const c64 *inv32, const c64 *sup32,
-                        const cdd *rdd_a, const cdd *rdd_b, c64 *rw, const c128 *Xnext, cudaStream_t st);
+                        const cdh *rdd_a, const cdh *rdd_b, c64 *rw, const c128 *Xnext, cudaStream_t st);
 
 // levels l0..top..l0 in one cluster launch (tridiag_l0.cu); lv_chain_start
 // returns the first chained level (0: none) and the cluster size
