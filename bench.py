@@ -129,7 +129,7 @@ def kernel_bytes(name, n, k, m=16):
         # per-shift complex arrays, shared row bytes, per-(block,shift) bytes
         "l0_s1": (1, 16 + 48, 32),
         "l0_s3acc": (1, 16 + 48 + 16, 32),
-        "l0_k2": (2, 16 + 72 + 32, 16 * 2 + 64),       # pivots in (16 B), complex64 residual out and pivots in (8 + 8 B)
+        "l0_k2": (2, 16 + 72 + 32, 16 * 2 + 48),       # pivots in (16 B), complex64 residual out and pivots in (8 + 8 B); interface halves 2 x 24 B
         "l0_k3": (1, 48 + 32 + 16, 32),                # complex64 pivots + residual in (8 + 8 B)
     }
     if name == "rhs":
