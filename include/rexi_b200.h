@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define REXI_ABI_VERSION 1
+#define REXI_ABI_VERSION 2
 
 typedef struct rexi_c128 { double re, im; } rexi_c128;
 typedef struct rexi_plan rexi_plan;
@@ -99,16 +99,29 @@ typedef struct rexi_desc {
                                   weights (mean |beta| over ALL K shifts, so a shard
                                   converges exactly as in the unsharded run); 0 ->
                                   the mean over this plan's shifts                 */
+    const int32_t *shift_ids;  /* host, k or NULL: global index of each shift (a
+                                  cost-balanced shard is not contiguous); NULL ->
+                                  shift_offset + i.  Error messages name these. */
 } rexi_desc;
 
 typedef struct rexi_stats {
-    double t_rhs_ms;           /* accumulated device time of the phases, like the */
-    double t_local_ms;         /* reference timers rhs/local/reduce               */
-    double t_reduce_ms;        /*   (integrate.py:110-112, 203-225)               */
+    /* device time (CUDA events on the plan's stream) of the phases of the
+     * reference timers rhs/local/reduce (integrate.py:110-112, 203-225):
+     * rhs    = staging u onto the device + forming iB u where it is a kernel
+     *          of its own (COCG); 0 when both are fused into the first solve
+     *          kernel (1D zero-copy / device input),
+     * local  = the shifted solves (and whatever is fused into them: the 1D
+     *          level-0 kernels also form iB u and the beta-weighted sum),
+     * reduce = the beta-weighted accumulation where it is a kernel of its own
+     *          (COCG) + copying u1 back to the host. */
+    double t_rhs_ms;
+    double t_local_ms;
+    double t_reduce_ms;
     int64_t steps;             /* steps executed by this call                     */
     int64_t launches;          /* kernels launched by this call                   */
-    int32_t iters_max;         /* COCG: max iterations over shifts (last step)    */
-    double iters_mean;         /* COCG: mean iterations over shifts (last step)   */
+    int32_t iters_max;         /* COCG: max over shifts of the shift's iterations,
+                                  first solve + corrections (last step)           */
+    double iters_mean;         /* COCG: mean over shifts of the same (last step)  */
     int32_t refine_rounds;     /* refinement rounds applied per step              */
     int32_t bad_shift;         /* global index of a failing shift, -1 if none     */
 } rexi_stats;
@@ -163,6 +176,19 @@ int rexi_plan_solve(rexi_plan *plan, const rexi_c128 *rhs, rexi_c128 *x, int32_t
 
 int rexi_plan_info(const rexi_plan *plan, rexi_info *info);
 
+/* Order the plan's stream after all work enqueued so far on `stream` (e.g.
+ * torch's current stream, which produced the device input): an event
+ * recorded on `stream`, waited on by the plan's stream, no host sync.
+ * Every rexi_plan_* call with device pointers returns only after its work
+ * completed (except the stream-ordered 1D rexi_plan_step_partial on a
+ * caller's stream), so outputs need no such wait. */
+int rexi_plan_wait_stream(rexi_plan *plan, void *stream);
+
+/* Per-shift COCG iterations of the last step (first solve + corrections),
+ * iters: k entries in the plan's shift order; all 0 for the direct solver.
+ * The cost model for balancing pole shards. */
+int rexi_plan_shift_iters(const rexi_plan *plan, int32_t *iters);
+
 /* Per-kernel device-time profiling with CUDA events on the plan's stream
  * (used by bench.py for the roofline).  enable resets the counters; the
  * report is text lines "<kernel> <launches> <total_ms>". */
@@ -203,6 +229,8 @@ int rexi_pencil_cheb_step(rexi_pencil *pencil, const rexi_c128 *coeffs, int32_t 
                           const rexi_c128 *u_in, rexi_c128 *u_out, int32_t n_steps, int32_t mem,
                           rexi_stats *stats);
 const char *rexi_pencil_last_error(const rexi_pencil *pencil);
+/* as rexi_plan_wait_stream */
+int rexi_pencil_wait_stream(rexi_pencil *pencil, void *stream);
 
 /* ---- P1 assembly on a structured Kuhn mesh ----
  * Builds A = 0.5 K + M_V and B = M on the interior nodes of an m^d-cell grid

@@ -58,6 +58,13 @@ def lib():
         L.orc_bandwidth.restype = ctypes.c_int32
         L.orc_rhs.argtypes = [p, p, p]
         L.orc_cocg_step.restype = ctypes.c_int
+        L.orc_cocg_truth_step.restype = ctypes.c_int
+        L.orc_cocg_truth_step.argtypes = [ctypes.c_int64, p, p, p, p, ctypes.c_int32, p, p,
+                                          ctypes.c_double, p, p, ctypes.c_double, ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.c_double, ctypes.c_int32, p, p, p]
+        L.orc_csr_rel_residual.restype = ctypes.c_double
+        L.orc_csr_rel_residual.argtypes = [ctypes.c_int64, p, p, p, p, ctypes.c_double,
+                                           ctypes.c_double * 2, p, p, ctypes.c_int32]
         L.orc_cocg_step.argtypes = [ctypes.c_int64, p, p, p, p, ctypes.c_int32, p, p,
                                     ctypes.c_double, p, p, ctypes.c_double, ctypes.c_int32,
                                     ctypes.c_int32, ctypes.c_double, ctypes.c_int32, p]
@@ -171,6 +178,44 @@ def cocg_step(sysm, approx, tau, u, tol=1e-12, maxit=20000, refine=1, tol_refine
     if rc:
         raise RuntimeError(f"oracle COCG failed for shift j = {rc - 10}")
     return out, iters
+
+
+def cocg_truth_step(sysm, approx, tau, u, tol=1e-12, maxit=40000, rounds=6, tol_refine=1e-8,
+                    nthreads=0, pattern=None, return_solutions=False):
+    """Truth-level CPU step for any CSR pencil (2D/3D, where the banded truth
+    of ``OraclePlan`` does not fit): per-shift Jacobi-COCG, double-double
+    residual refinement with x kept in double-double, exact-product
+    double-double sum (``cocg_oracle.c: orc_cocg_truth_step``).
+    Returns (u1, iterations[K], last relative correction[K]) and the fp64
+    per-shift solutions when ``return_solutions``."""
+    indptr, indices, a, b = pattern if pattern is not None else union_pattern(sysm.A, sysm.B)
+    shifts = np.ascontiguousarray(approx.shifts, dtype=np.complex128)
+    weights = np.ascontiguousarray(approx.weights, dtype=np.complex128)
+    u = np.ascontiguousarray(u, dtype=np.complex128)
+    out = np.empty_like(u)
+    k = len(shifts)
+    iters = np.zeros(k, dtype=np.int32)
+    corr = np.zeros(k, dtype=np.float64)
+    xs = np.empty((k, len(u)), dtype=np.complex128) if return_solutions else None
+    rc = lib().orc_cocg_truth_step(len(u), _ptr(indptr), _ptr(indices), _ptr(a), _ptr(b), k,
+                                   _ptr(shifts), _ptr(weights), float(tau), _ptr(u), _ptr(out),
+                                   float(tol), int(maxit), int(rounds), float(tol_refine),
+                                   int(nthreads), _ptr(iters), _ptr(corr),
+                                   _ptr(xs) if xs is not None else None)
+    if rc:
+        raise RuntimeError(f"oracle COCG failed for shift j = {rc - 10}")
+    return (out, iters, corr, xs) if return_solutions else (out, iters, corr)
+
+
+def csr_rel_residual(pattern, tau, sigma, b, x, nthreads=0):
+    """||b - (tau A - 1j sigma B) x|| / ||b|| with a double-double residual
+    (entries formed with the reference's rounding, integrate.py:171)."""
+    indptr, indices, a, bv = pattern
+    b = np.ascontiguousarray(b, dtype=np.complex128)
+    x = np.ascontiguousarray(x, dtype=np.complex128)
+    s = (ctypes.c_double * 2)(complex(sigma).real, complex(sigma).imag)
+    return float(lib().orc_csr_rel_residual(len(b), _ptr(indptr), _ptr(indices), _ptr(a), _ptr(bv),
+                                            float(tau), s, _ptr(b), _ptr(x), int(nthreads)))
 
 
 def rel_l2(x, y):

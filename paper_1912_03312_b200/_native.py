@@ -27,7 +27,7 @@ REXI_ERR_UNSUPPORTED = 7
 
 SOLVER_AUTO, SOLVER_TRIDIAG, SOLVER_COCG = 0, 1, 2
 MEM_HOST, MEM_DEVICE = 0, 1
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 EXPORTED = (
     "rexi_plan_create", "rexi_plan_step", "rexi_plan_step_partial", "rexi_combine_partials",
@@ -35,7 +35,8 @@ EXPORTED = (
     "rexi_last_error", "rexi_device_count", "rexi_abi_version", "rexi_plan_profile",
     "rexi_plan_profile_report", "rexi_plan_run", "rexi_pencil_create", "rexi_pencil_solve_b",
     "rexi_pencil_spectral_radius", "rexi_pencil_cheb_step", "rexi_pencil_last_error",
-    "rexi_pencil_destroy", "rexi_assemble_p1",
+    "rexi_pencil_destroy", "rexi_assemble_p1", "rexi_plan_wait_stream", "rexi_plan_shift_iters",
+    "rexi_pencil_wait_stream",
 )
 
 
@@ -61,6 +62,7 @@ class RexiDesc(ctypes.Structure):
         ("max_iters", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
         ("weight_ref", ctypes.c_double),
+        ("shift_ids", ctypes.c_void_p),
     ]
 
 
@@ -142,6 +144,9 @@ def lib():
     L.rexi_pencil_last_error.argtypes = [vp]
     L.rexi_pencil_last_error.restype = ctypes.c_char_p
     L.rexi_pencil_destroy.argtypes = [vp]
+    L.rexi_plan_wait_stream.argtypes = [vp, vp]
+    L.rexi_plan_shift_iters.argtypes = [vp, i32p]
+    L.rexi_pencil_wait_stream.argtypes = [vp, vp]
     L.rexi_assemble_p1.argtypes = [ctypes.POINTER(RexiP1Desc), vp, vp, vp, vp, vp]
     if L.rexi_abi_version() != ABI_VERSION:
         raise DeviceError("native library ABI version mismatch")
@@ -190,7 +195,7 @@ class NativePlan:
 
     def __init__(self, indptr, indices, a_vals, b_vals, shifts, weights, tau, *, a_imag=None,
                  device=0, solver=SOLVER_AUTO, refine=-1, tol=0.0, max_iters=0, shift_offset=0,
-                 stream=None, weight_ref=0.0):
+                 stream=None, weight_ref=0.0, shift_ids=None):
         L = lib()
         self._keep = [np.ascontiguousarray(indptr, dtype=np.int32),
                       np.ascontiguousarray(indices, dtype=np.int32),
@@ -198,6 +203,7 @@ class NativePlan:
                       np.ascontiguousarray(b_vals, dtype=np.float64),
                       np.ascontiguousarray(shifts, dtype=np.complex128),
                       np.ascontiguousarray(weights, dtype=np.complex128)]
+        self._ids = None if shift_ids is None else np.ascontiguousarray(shift_ids, dtype=np.int32)
         if a_imag is not None:
             self._keep.append(np.ascontiguousarray(a_imag, dtype=np.float64))
         ip, ix, av, bv, sh, wt = self._keep[:6]
@@ -222,6 +228,7 @@ class NativePlan:
         d.max_iters = int(max_iters)
         d.stream = stream
         d.weight_ref = float(weight_ref)
+        d.shift_ids = self._ids.ctypes.data if self._ids is not None else None
         self.n = int(d.n)
         self.k = int(d.k)
         self.device = int(device)
@@ -259,6 +266,19 @@ class NativePlan:
         out = host_empty((int(n_steps), self.n))
         rc = lib().rexi_plan_run(self._h, _ptr(u), _ptr(out), int(n_steps), MEM_HOST,
                                  ctypes.byref(stats) if stats is not None else None)
+        raise_status(rc, self._err())
+        return out
+
+    def wait_stream(self, stream_handle):
+        """Order this plan's stream after the work queued on ``stream_handle``
+        (a cudaStream_t as int, e.g. torch's current stream)."""
+        rc = lib().rexi_plan_wait_stream(self._h, ctypes.c_void_p(stream_handle))
+        raise_status(rc, self._err())
+
+    def shift_iters(self) -> np.ndarray:
+        """Per-shift COCG iterations of the last step (zeros for the direct solver)."""
+        out = np.zeros(self.k, dtype=np.int32)
+        rc = lib().rexi_plan_shift_iters(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
         raise_status(rc, self._err())
         return out
 
@@ -337,6 +357,10 @@ class NativePencil:
 
     def _err(self) -> str:
         return lib().rexi_pencil_last_error(self._h).decode()
+
+    def wait_stream(self, stream_handle):
+        rc = lib().rexi_pencil_wait_stream(self._h, ctypes.c_void_p(stream_handle))
+        raise_status(rc, self._err())
 
     def solve_b(self, rhs: np.ndarray):
         rhs = np.ascontiguousarray(rhs, dtype=np.complex128)

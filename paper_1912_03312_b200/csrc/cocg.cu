@@ -1077,6 +1077,10 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     cg.tol = d->tol > 0 ? d->tol : 1e-12;
     cg.max_iters = d->max_iters > 0 ? d->max_iters : 20000;
     cg.shift_offset = d->shift_offset;
+    cg.gid.resize(d->k);
+    for (int j = 0; j < d->k; ++j) cg.gid[j] = d->shift_ids ? d->shift_ids[j] : d->shift_offset + j;
+    cg.shift_iters.assign(d->k, 0);
+    for (auto &e : cg.ev) CGK(cudaEventCreate(&e));
     const int64_t n = d->n, nnz = d->nnz;
     const int kp = S.kp;
     im->kp_full = kp;
@@ -1333,6 +1337,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     *launches += 2;
     int live = cg.k;
     int packed_live = std::min(cg.k, kp);   // live lanes at the last (re)pack
+    std::vector<int> h_it(kp);
     int it = 0;
     const int check_every = 8;
     // failed lane l (current layout) -> error naming its shift
@@ -1343,8 +1348,9 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
         const char *why = status == 1 ? "COCG breakdown (rho or p^T S p vanished)"
                         : status == 2 ? "non-finite values in COCG"
                                       : "COCG did not converge within max_iters";
+        const int ls = lane_shift[l];
         snprintf(buf, sizeof buf, "%s for shift j = %d after %d iterations", why,
-                 cg.shift_offset + lane_shift[l], iters);
+                 ls < cg.k ? cg.gid[ls] : cg.shift_offset + ls, iters);
         err = buf;
         return status == 3 ? REXI_ERR_NOCONV : REXI_ERR_BREAKDOWN;
     };
@@ -1434,9 +1440,12 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             // a frozen lane leaving the layout takes its status with it: report
             // a failed one now
             CGK(cudaMemcpyAsync(h_st, im->Sc.status, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
+            CGK(cudaMemcpyAsync(h_it.data(), im->Sc.iters, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
             CGK(cudaStreamSynchronize(st));
             for (int l = 0; l < kp; ++l)
                 if (valid[l] && !h_act[l] && h_st[l]) return lane_failure(l, h_st[l]);
+            for (int l = 0; l < kp; ++l)
+                if (valid[l] && !h_act[l] && lane_shift[l] < cg.k) cg.shift_iters[lane_shift[l]] += h_it[l];
             packed_live = na;
             // live lanes keep ascending shift order; frozen valid lanes hand their
             // x to the full-width solution; padding lanes (a copy of lane map[0],
@@ -1462,6 +1471,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     // statistics / failures (per current lane -> shift)
     std::vector<int> status(kp);
     CGK(cudaMemcpyAsync(status.data(), im->Sc.status, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
+    CGK(cudaMemcpyAsync(h_it.data(), im->Sc.iters, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
     // remaining valid lanes' x -> full-width solution
     CGK(cudaMemcpyAsync(im->mask, valid.data(), sizeof(int) * kp, cudaMemcpyHostToDevice, st));
     k_cg_scatter_x<<<(unsigned)((n * kp + 255) / 256), 256, 0, st>>>(im->V.x, im->xout, n, kp, im->kp_full,
@@ -1470,16 +1480,15 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     CGK(cudaStreamSynchronize(st));
     for (int l = 0; l < kp; ++l)
         if (valid[l] && lane_shift[l] < cg.k && status[l]) return lane_failure(l, status[l]);
-    cg.last_iters_max = std::max(cg.last_iters_max, it);
-    cg.last_iters_mean += it;
+    for (int l = 0; l < kp; ++l)
+        if (valid[l] && lane_shift[l] < cg.k) cg.shift_iters[lane_shift[l]] += h_it[l];
     return REXI_OK;
 }
 
 // all shifts, x_j = S_j^{-1} rhs (refined): result x1 (+ x2)
 static int cg_solve_refined(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t st,
                             int64_t *launches, std::string &err, const c128 **x1, const c128 **x2) {
-    cg.last_iters_max = 0;
-    cg.last_iters_mean = 0.0;
+    std::fill(cg.shift_iters.begin(), cg.shift_iters.end(), 0);
     im->V.bshared = im->rhs;
     im->V.bvec = nullptr;
     // with refinement the first solve stops at tol*100 (the dd-residual
@@ -1521,20 +1530,49 @@ static int cg_solve_refined(CocgState &cg, CocgImpl *im, const ShiftDev &S, cuda
     return REXI_OK;
 }
 
+static void iter_summary(CocgState &cg) {
+    int mx = 0;
+    double sum = 0.0;
+    for (int v : cg.shift_iters) {
+        mx = std::max(mx, v);
+        sum += v;
+    }
+    cg.last_iters_max = mx;
+    cg.last_iters_mean = cg.k ? sum / cg.k : 0.0;
+}
+
+void cocg_collect_phase(CocgState &cg) {
+    if (!cg.ev_pending) return;
+    cg.ev_pending = false;
+    float a = 0.f, b = 0.f;
+    if (cudaEventSynchronize(cg.ev[3]) != cudaSuccess) return;
+    cudaEventElapsedTime(&a, cg.ev[0], cg.ev[1]);
+    cudaEventElapsedTime(&b, cg.ev[2], cg.ev[3]);
+    cg.t_rhs_ms += a;
+    cg.t_acc_ms += b;
+}
+
 int cocg_step(CocgState &cg, const ShiftDev &S, cudaStream_t st, const c128 *u, c128 *uout, double *acc,
               int64_t *launches, std::string &err) {
     CocgImpl *im = (CocgImpl *)cg.impl;
     const int64_t n = cg.n;
+    cocg_collect_phase(cg);
+    CGK(cudaEventRecord(cg.ev[0], st));
     k_cg_rhs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(im->M, u, im->rhs);
     CGK(cudaGetLastError());
+    CGK(cudaEventRecord(cg.ev[1], st));
     ++*launches;
     const c128 *x1 = nullptr, *x2 = nullptr;
     int rc = cg_solve_refined(cg, im, S, st, launches, err, &x1, &x2);
+    iter_summary(cg);
     if (rc) return rc;
+    CGK(cudaEventRecord(cg.ev[2], st));
     hook_begin(cg, "cg_accum", (x2 ? 32.0 : 16.0) * n * cg.k + 32.0 * n);
     k_cg_accum<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, im->kp_full, cg.k, S.beta, x1, x2, acc, uout);
     hook_end(cg);
     CGK(cudaGetLastError());
+    CGK(cudaEventRecord(cg.ev[3], st));
+    cg.ev_pending = true;
     ++*launches;
     return REXI_OK;
 }
@@ -1548,6 +1586,7 @@ int cocg_solve_all(CocgState &cg, const ShiftDev &S, cudaStream_t st, const c128
     int64_t launches = 0;
     const c128 *x1 = nullptr, *x2 = nullptr;
     int rc = cg_solve_refined(cg, im, S, st, &launches, err, &x1, &x2);
+    iter_summary(cg);
     if (rc) return rc;
     const int64_t t = n * (int64_t)cg.k;
     k_cg_transpose<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(x1, x2, n, im->kp_full, cg.k, x);
@@ -1556,6 +1595,11 @@ int cocg_solve_all(CocgState &cg, const ShiftDev &S, cudaStream_t st, const c128
 }
 
 void cocg_destroy(CocgState &cg) {
+    for (auto &e : cg.ev)
+        if (e) {
+            cudaEventDestroy(e);
+            e = nullptr;
+        }
     for (void *p : cg.allocs) cudaFree(p);
     cg.allocs.clear();
     if (cg.impl) {

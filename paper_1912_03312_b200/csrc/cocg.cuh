@@ -27,6 +27,12 @@ struct CocgState {
     int last_iters_max = 0;
     double last_iters_mean = 0.0;
     int shift_offset = 0;
+    std::vector<int> gid;            // global index of each shift (error messages)
+    std::vector<int> shift_iters;    // per-shift iterations of the last step (first solve + corrections)
+    // phase timing of the rhs / accumulation kernels (stats rhs / reduce)
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool ev_pending = false;
+    double t_rhs_ms = 0.0, t_acc_ms = 0.0;
     std::vector<void *> allocs;
     void *impl = nullptr;   // CocgImpl (cocg.cu)
 };
@@ -38,6 +44,8 @@ int cocg_step(CocgState &cg, const ShiftDev &S, cudaStream_t st, const c128 *u, 
 int cocg_solve_all(CocgState &cg, const ShiftDev &S, cudaStream_t st, const c128 *rhs, bool rhs_host,
                    c128 *x, std::string &err);
 void cocg_destroy(CocgState &cg);
+// fold the last step's rhs / accumulation event times into t_rhs_ms / t_acc_ms
+void cocg_collect_phase(CocgState &cg);
 cudaError_t cocg_axpy_inplace(c128 *x, const c128 *y, int64_t n, cudaStream_t st);
 
 }  // namespace rexi

@@ -593,6 +593,19 @@ int rexi_pencil_cheb_step(rexi_pencil *pn, const rexi_c128 *coeffs, int32_t degr
 
 const char *rexi_pencil_last_error(const rexi_pencil *pn) { return pn ? pn->err.c_str() : rexi_last_error(); }
 
+int rexi_pencil_wait_stream(rexi_pencil *pn, void *stream) {
+    if (!pn) return pn_err(nullptr, REXI_ERR_INVALID, "null pencil");
+    if ((cudaStream_t)stream == pn->stream) return REXI_OK;
+    cudaSetDevice(pn->device);
+    cudaEvent_t e = nullptr;
+    cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (r == cudaSuccess) r = cudaEventRecord(e, (cudaStream_t)stream);
+    if (r == cudaSuccess) r = cudaStreamWaitEvent(pn->stream, e, 0);
+    if (e) cudaEventDestroy(e);
+    if (r != cudaSuccess) return pn_err(pn, REXI_ERR_CUDA, cudaGetErrorString(r));
+    return REXI_OK;
+}
+
 int rexi_pencil_destroy(rexi_pencil *pn) {
     if (!pn) return REXI_OK;
     cudaSetDevice(pn->device);

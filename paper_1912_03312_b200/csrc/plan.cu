@@ -48,6 +48,7 @@ struct rexi_plan {
     int64_t n = 0;
     int k = 0, kp = 0;
     int shift_offset = 0;
+    std::vector<int> gid;         // global index of each shift (error messages)
     int refine = 0;
     int bandwidth = 0;
     cudaStream_t stream = nullptr;
@@ -326,7 +327,7 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
         if (!(mn > 0.0) || !(mx < INFINITY) || mn < 1e-14 * mx) {
             char buf[256];
             snprintf(buf, sizeof buf, "matrix is numerically singular (pivot ratio = %.3e) for shift j = %d",
-                     ratio, plan->shift_offset + j);
+                     ratio, plan->gid[j]);
             plan->min_pivot_ratio = ratio;
             return set_err(plan, REXI_ERR_SINGULAR, buf);
         }
@@ -499,6 +500,22 @@ int tri_step(rexi_plan *plan, const c128 *u, c128 *uout) {
     return tri_chain(plan, T.rres, TRI_OUT_ACC, 1, uout);
 }
 
+// stats phases from the four events of a call (see rexi_plan_step) and the
+// COCG rhs / accumulation kernel times; destroys the events
+void fill_phases(rexi_plan *plan, cudaEvent_t ev[4], rexi_stats *stats) {
+    float stage = 0.f, steps = 0.f, out = 0.f;
+    cudaEventElapsedTime(&stage, ev[0], ev[1]);
+    cudaEventElapsedTime(&steps, ev[1], ev[2]);
+    cudaEventElapsedTime(&out, ev[2], ev[3]);
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+    cocg_collect_phase(plan->cg);
+    const double cr = plan->cg.t_rhs_ms, ca = plan->cg.t_acc_ms;
+    plan->cg.t_rhs_ms = plan->cg.t_acc_ms = 0.0;
+    stats->t_rhs_ms = stage + cr;
+    stats->t_local_ms = std::max(0.0, (double)steps - cr - ca);
+    stats->t_reduce_ms = ca + out;
+}
+
 int plan_step_device(rexi_plan *plan, const c128 *u, c128 *uout) {
     if (plan->solver == REXI_SOLVER_TRIDIAG) return tri_step(plan, u, uout);
     return cocg_step(plan->cg, plan->S, plan->stream, u, uout, plan->tri.acc, &plan->launches,
@@ -563,6 +580,8 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
     plan->n = d->n;
     plan->k = d->k;
     plan->shift_offset = d->shift_offset;
+    plan->gid.resize(d->k);
+    for (int j = 0; j < d->k; ++j) plan->gid[j] = d->shift_ids ? d->shift_ids[j] : d->shift_offset + j;
     plan->shifts_host.assign(d->shifts, d->shifts + d->k);
     // structure
     bool tri = true;
@@ -719,6 +738,27 @@ int rexi_plan_info(const rexi_plan *plan, rexi_info *info) {
     return REXI_OK;
 }
 
+int rexi_plan_wait_stream(rexi_plan *plan, void *stream) {
+    if (!plan) return set_err(nullptr, REXI_ERR_INVALID, "null plan");
+    if ((cudaStream_t)stream == plan->stream) return REXI_OK;
+    CK(cudaSetDevice(plan->device));
+    cudaEvent_t e = nullptr;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaError_t r = cudaEventRecord(e, (cudaStream_t)stream);
+    if (r == cudaSuccess) r = cudaStreamWaitEvent(plan->stream, e, 0);
+    cudaEventDestroy(e);   // released once the wait is satisfied
+    if (r != cudaSuccess) return cuda_err(plan, r, "rexi_plan_wait_stream");
+    return REXI_OK;
+}
+
+int rexi_plan_shift_iters(const rexi_plan *plan, int32_t *iters) {
+    if (!plan || !iters) return set_err(nullptr, REXI_ERR_INVALID, "null argument");
+    for (int j = 0; j < plan->k; ++j)
+        iters[j] = plan->solver == REXI_SOLVER_COCG && j < (int)plan->cg.shift_iters.size()
+                       ? plan->cg.shift_iters[j] : 0;
+    return REXI_OK;
+}
+
 int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int32_t n_steps,
                    int32_t mem, rexi_stats *stats) {
     if (!plan) return set_err(nullptr, REXI_ERR_INVALID, "null plan");
@@ -727,10 +767,14 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     const int64_t n = plan->n;
     cudaStream_t st = plan->stream;
     plan->launches = 0;
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    // phase events: [0] before staging u, [1] after it (rhs), [2] after the
+    // steps (local), [3] after copying u1 out (reduce)
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     if (stats) {
-        CK(cudaEventCreate(&ev[0]));
-        CK(cudaEventCreate(&ev[1]));
+        for (auto &e : ev) CK(cudaEventCreate(&e));
+        cocg_collect_phase(plan->cg);
+        plan->cg.t_rhs_ms = plan->cg.t_acc_ms = 0.0;
+        CK(cudaEventRecord(ev[0], st));
     }
     // zero-copy output: when u_out is page-locked host memory, the last step's
     // final kernel writes u1 straight into it over PCIe (overlapped with the
@@ -766,7 +810,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     } else {
         src = (const c128 *)u_in;
     }
-    if (stats) CK(cudaEventRecord(ev[0], st));
+    if (stats) CK(cudaEventRecord(ev[1], st));
     int cur = (src == plan->ubuf[0]) ? 0 : 1;
     if (n_steps > 0 && plan->persist_cs > 0 && !plan->prof) {
         TriState &T = plan->tri;
@@ -841,7 +885,8 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
         if (dst == src) dst = plan->ubuf[cur ^ 1];   // in-place device call
         int rc = plan_step_device(plan, src, dst);
         if (rc) {
-            if (ev[0]) { cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]); }
+            for (auto e : ev)
+                if (e) cudaEventDestroy(e);
             if (rc == REXI_ERR_NOCONV || rc == REXI_ERR_BREAKDOWN) return set_err(plan, rc, plan->err);
             return rc;
         }
@@ -849,7 +894,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
         cur = (src == plan->ubuf[0]) ? 0 : 1;
     }
     if (n_steps < 0) n_steps = -n_steps;
-    if (stats) CK(cudaEventRecord(ev[1], st));
+    if (stats) CK(cudaEventRecord(ev[2], st));
     if (n_steps == 0) {
         if (mem == REXI_MEM_HOST) {
             if (u_out != u_in) memcpy(u_out, u_in, sizeof(c128) * n);
@@ -861,16 +906,11 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     } else if ((const void *)src != (const void *)u_out) {
         CK(cudaMemcpyAsync(u_out, src, sizeof(c128) * n, cudaMemcpyDeviceToDevice, st));
     }
+    if (stats) CK(cudaEventRecord(ev[3], st));
     CK(cudaStreamSynchronize(st));
     prof_flush(plan);
     if (stats) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, ev[0], ev[1]);
-        cudaEventDestroy(ev[0]);
-        cudaEventDestroy(ev[1]);
-        stats->t_rhs_ms = 0.0;
-        stats->t_local_ms = ms;
-        stats->t_reduce_ms = 0.0;
+        fill_phases(plan, ev, stats);
         stats->steps = n_steps;
         stats->launches = plan->launches;
         stats->iters_max = plan->cg.last_iters_max;
@@ -891,9 +931,11 @@ int rexi_plan_run(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *snaps, int3
     const int64_t n = plan->n;
     cudaStream_t st = plan->stream;
     plan->launches = 0;
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    CK(cudaEventCreate(&ev[0]));
-    CK(cudaEventCreate(&ev[1]));
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (auto &e : ev) CK(cudaEventCreate(&e));
+    cocg_collect_phase(plan->cg);
+    plan->cg.t_rhs_ms = plan->cg.t_acc_ms = 0.0;
+    CK(cudaEventRecord(ev[0], st));
     c128 *dsnap = (c128 *)snaps, *tmp = nullptr;
     if (mem == REXI_MEM_HOST) {
         CK(cudaMallocAsync((void **)&tmp, sizeof(c128) * n * (size_t)n_steps, st));
@@ -904,7 +946,7 @@ int rexi_plan_run(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *snaps, int3
         CK(cudaMemcpyAsync(plan->ubuf[0], u_in, sizeof(c128) * n, cudaMemcpyHostToDevice, st));
         src = plan->ubuf[0];
     }
-    CK(cudaEventRecord(ev[0], st));
+    CK(cudaEventRecord(ev[1], st));
     int rc = REXI_OK;
     if (plan->persist_cs > 0 && !plan->prof) {
         TriState &T = plan->tri;
@@ -915,23 +957,21 @@ int rexi_plan_run(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *snaps, int3
         for (int s = 0; s < n_steps && !rc; ++s)
             rc = plan_step_device(plan, s == 0 ? src : dsnap + (size_t)(s - 1) * n, dsnap + (size_t)s * n);
     }
-    CK(cudaEventRecord(ev[1], st));
+    CK(cudaEventRecord(ev[2], st));
     if (!rc && mem == REXI_MEM_HOST)
         CK(cudaMemcpyAsync(snaps, dsnap, sizeof(c128) * n * (size_t)n_steps, cudaMemcpyDeviceToHost, st));
     if (tmp) cudaFreeAsync(tmp, st);
+    CK(cudaEventRecord(ev[3], st));
     CK(cudaStreamSynchronize(st));
     prof_flush(plan);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev[0], ev[1]);
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
+    rexi_stats local_stats{};
+    fill_phases(plan, ev, &local_stats);
     if (rc) {
         if (rc == REXI_ERR_NOCONV || rc == REXI_ERR_BREAKDOWN) return set_err(plan, rc, plan->err);
         return rc;
     }
     if (stats) {
-        std::memset(stats, 0, sizeof *stats);
-        stats->t_local_ms = ms;
+        *stats = local_stats;
         stats->steps = n_steps;
         stats->launches = plan->launches;
         stats->iters_max = plan->cg.last_iters_max;
@@ -1004,6 +1044,10 @@ int rexi_plan_step_partial(rexi_plan *plan, const rexi_c128 *u_in, double *parti
     prof_flush(plan);
     if (stats) {
         memset(stats, 0, sizeof *stats);
+        cocg_collect_phase(plan->cg);
+        stats->t_rhs_ms = plan->cg.t_rhs_ms;
+        stats->t_reduce_ms = plan->cg.t_acc_ms;
+        plan->cg.t_rhs_ms = plan->cg.t_acc_ms = 0.0;
         stats->steps = 1;
         stats->launches = plan->launches;
         stats->iters_max = plan->cg.last_iters_max;

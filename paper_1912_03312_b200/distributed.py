@@ -156,27 +156,37 @@ def gather_segments(useg, uall, world: int, group=None):
 
 class ShardedStepper:
     """This rank's shard of one REXI step.  ``step(u, out)`` takes and writes
-    device tensors (complex128, length n) on this rank's GPU."""
+    device tensors (complex128, length n) on this rank's GPU.
+
+    ``stream`` (a cudaStream_t as int) defaults to torch's current stream on
+    ``device``, so the step is ordered with the torch ops that produce u and
+    consume out.  A rank whose shard is empty (world > K) contributes a zero
+    partial.  ``reshard(cost)`` re-splits the shifts by per-shift costs
+    (``measure_costs()``: the COCG iterations of the last step, gathered from
+    every rank), longest-processing-time first."""
 
     def __init__(self, sysm, approx, tau, *, rank: int, world: int, device: int,
                  refine: int = -1, solver: int = _native.SOLVER_AUTO, cost=None, group=None,
                  stream=None, tol: float = 0.0, max_iters: int = 0):
         import torch
         self.rank, self.world, self.group = rank, world, group
-        shifts = np.asarray(approx.shifts, dtype=complex)
-        weights = np.asarray(approx.weights, dtype=complex)
-        self.shards = shard_indices(len(shifts), world, cost)
-        idx = self.shards[rank]
-        indptr, indices, a_re, a_im, b_re = shared_pattern(sysm.A, sysm.B)
+        self.shifts = np.asarray(approx.shifts, dtype=complex)
+        self.weights = np.asarray(approx.weights, dtype=complex)
+        self.k = len(self.shifts)
+        self.pattern = shared_pattern(sysm.A, sysm.B)
+        self.tau = tau
+        self.device = device
         self.n = int(sysm.n_dof)
-        self.plan = _native.NativePlan(indptr, indices, a_re, b_re, shifts[idx], weights[idx], tau,
-                                       a_imag=a_im, device=device, solver=solver, refine=refine,
-                                       shift_offset=idx[0] if idx else 0, stream=stream, tol=tol,
-                                       max_iters=max_iters, weight_ref=float(np.mean(np.abs(weights))))
         dev = torch.device("cuda", device)
-        self.parts = torch.empty((world, 4, self.n), dtype=torch.float64, device=dev)
-        self.mine = torch.empty((4, self.n), dtype=torch.float64, device=dev)
+        if stream is None:
+            stream = torch.cuda.current_stream(dev).cuda_stream
         self.stream = stream
+        self._opts = dict(device=device, solver=solver, refine=refine, stream=stream, tol=tol,
+                          max_iters=max_iters, weight_ref=float(np.mean(np.abs(self.weights))))
+        self.plan = None
+        self._build(shard_indices(self.k, world, cost))
+        self.parts = torch.empty((world, 4, self.n), dtype=torch.float64, device=dev)
+        self.mine = torch.zeros((4, self.n), dtype=torch.float64, device=dev)
         # segmented exchange buffers: row segments of seg rows per rank
         self.seg = -(-self.n // world)
         npad = self.seg * world
@@ -185,6 +195,40 @@ class ShardedStepper:
         self.useg = torch.empty(self.seg, dtype=torch.complex128, device=dev)
         self.uall = torch.empty(npad, dtype=torch.complex128, device=dev)
 
+    def _build(self, shards):
+        if self.plan is not None:
+            self.plan.close()
+            self.plan = None
+        self.shards = shards
+        idx = shards[self.rank]
+        if idx:
+            indptr, indices, a_re, a_im, b_re = self.pattern
+            ids = np.asarray(idx, dtype=np.int64)
+            self.plan = _native.NativePlan(indptr, indices, a_re, b_re, self.shifts[ids],
+                                           self.weights[ids], self.tau, a_imag=a_im,
+                                           shift_offset=int(idx[0]), shift_ids=ids, **self._opts)
+
+    def measure_costs(self):
+        """Per-shift COCG iterations of the last step, all K, on every rank
+        (one small all_reduce of an int tensor: each rank fills its shifts)."""
+        import torch
+        import torch.distributed as dist
+        c = np.zeros(self.k, dtype=np.int64)
+        if self.plan is not None:
+            c[self.shards[self.rank]] = self.plan.shift_iters()
+        t = torch.from_numpy(c)
+        if self.world > 1:
+            if dist.get_backend(self.group) == "nccl":
+                t = t.to(f"cuda:{self.device}")
+            dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    def reshard(self, cost):
+        """Rebuild this rank's plan for the LPT split by ``cost`` (same on
+        every rank, e.g. from measure_costs()).  Returns the new shards."""
+        self._build(shard_indices(self.k, self.world, np.asarray(cost, dtype=float) + 1.0))
+        return self.shards
+
     def step(self, u, out):
         """u1 = sum over all shards of beta_j x_j.  Each rank computes its
         shard's double-double partial; an all-to-all hands rank r the row
@@ -192,7 +236,10 @@ class ShardedStepper:
         same per-row double-double operations as combining everything
         everywhere) and rounds; an all-gather assembles u1.  Per rank and step
         that moves 48 B/row instead of (world-1) x 32 B/row."""
-        self.plan.step_partial(u.data_ptr(), self.mine.data_ptr())
+        if self.plan is not None:
+            self.plan.step_partial(u.data_ptr(), self.mine.data_ptr())
+        else:
+            self.mine.zero_()
         if self.world == 1:
             _native.combine_partials(self.mine.data_ptr(), 1, self.n, out.data_ptr(), self.stream)
             return
@@ -203,4 +250,6 @@ class ShardedStepper:
         out.copy_(self.uall[:self.n])
 
     def close(self):
-        self.plan.close()
+        if self.plan is not None:
+            self.plan.close()
+            self.plan = None

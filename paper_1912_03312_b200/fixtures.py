@@ -485,6 +485,23 @@ def config5(m: int = 128, k: int = 64) -> Config:
 
 
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
+FULL_M = {3: 1024, 4: 2048, 5: 128}
+V_MAX = {3: 50.0 * 0.5, 4: 1e3, 5: 30.0 * 0.75}
+
+
+def stiffness_matched(idx: int, m: int) -> Config:
+    """Config idx (3, 4 or 5) on an m-cell mesh with tau scaled so that
+    tau * sr(M) equals the full-size config's (1.89e4 / 3.77e4 / 559): the
+    shifted systems keep the BASELINE conditioning (and the COCG iteration
+    counts it drives) at a size a CPU truth oracle solves in seconds."""
+    cfg = CONFIGS[idx](m=m)
+    d = cfg.mesh.d
+    full = StructuredMesh(d, FULL_M[idx], np.zeros(d), 1.0 / FULL_M[idx])
+    tau_full = {3: 1e-3, 4: 5e-4, 5: 1e-3}[idx]
+    target = tau_full * element_sr_bound(full, V_MAX[idx])
+    cfg.tau = target / cfg.sr
+    cfg.name = f"{cfg.name}@m={m},tau*sr={target:.4g}"
+    return cfg
 
 
 def build_config(idx: int, **kw) -> Config:

@@ -15,10 +15,11 @@ semantics as the reference (``pkg/src/rexiprop/integrate.py:43-245``):
 
 ``workers`` keeps its meaning of "how many pieces the K shifts are split
 into" (ref ``:114-120``): each piece is one native plan producing a
-double-double partial sum, and the pieces are combined in fixed order, so
-the answer does not depend on ``workers`` (ref ``:196-198``,
-``test_integrate.py:268-274``).  The default is one piece.  Across GPUs the
-same split is driven by :mod:`paper_1912_03312_b200.distributed`.
+double-double partial sum, the pieces are spread over the visible GPUs of
+this process and combined in fixed order, so the answer does not depend on
+``workers`` or on the GPU count (ref ``:196-198``,
+``test_integrate.py:268-274``).  The default is one piece per GPU.  One
+process per GPU (torchrun) uses :mod:`paper_1912_03312_b200.distributed`.
 
 There is no CPU fallback: without the native library or a CUDA device the
 calls raise :class:`DeviceError`.
@@ -130,6 +131,9 @@ class RexiStepper:
     refine: int = 0
     solver: str = "auto"
     stats: dict = field(default_factory=dict)
+    _plan_args: tuple = field(default=None, repr=False)
+    _slots: list = field(default_factory=list, repr=False)
+    _rebalanced: bool = field(default=True, repr=False)
 
     @property
     def interval_radius(self) -> float:
@@ -158,74 +162,47 @@ class RexiStepper:
         if b.ndim == 2:
             return np.stack([self._solve_shift(j, b[:, c]) for c in range(b.shape[1])], axis=1)
         for plan, idx in zip(self.plans, self.pieces):
-            if idx[0] <= j <= idx[-1]:
-                return plan.solve_host(b)[j - idx[0]]
+            if j in idx:
+                return plan.solve_host(b)[idx.index(j)]
         raise IndexError(j)
 
 
 _SOLVERS = {"auto": _native.SOLVER_AUTO, "tridiag": _native.SOLVER_TRIDIAG,
             "cocg": _native.SOLVER_COCG}
+# below this many row-shifts (n*K) the default keeps one GPU: a config-1-sized
+# step (~1 MB of work) is launch-latency bound and a cross-GPU combine would
+# cost more than the solves
+MULTI_GPU_MIN_WORK = 1 << 22
 
 
-def rexi_prepare(
-    sys,
-    approx,
-    tau: float,
-    *,
-    workers: int | None = None,
-    sr_value: float | None = None,
-    override_admissibility: bool = False,
-    device: int | None = None,
-    refine: int | None = None,
-    solver: str = "auto",
-    tol: float | None = None,
-    max_iters: int | None = None,
-) -> RexiStepper:
-    """Form and factor the K shifted systems on the GPU (ref ``:143-190``).
+def _default_devices(n: int, k: int, device, devices):
+    if devices is not None:
+        devs = [int(d) for d in devices]
+        if not devs:
+            raise ValueError("devices must not be empty")
+        return devs
+    if device is not None:
+        return [int(device)]
+    visible = _native.device_count()
+    if visible <= 1 or n * k < MULTI_GPU_MIN_WORK:
+        return [0]
+    return list(range(visible))
 
-    Extra keyword-only knobs (all optional): ``device`` (CUDA ordinal),
-    ``refine`` (double-double residual-refinement rounds; default by
-    stiffness), ``solver`` ("auto" | "tridiag" | "cocg"), ``tol`` and
-    ``max_iters`` for COCG.
-    """
-    if not tau > 0:
-        raise ValueError(f"tau must be positive, got {tau}")
-    shifts = np.asarray(approx.shifts, dtype=complex)
-    weights = np.asarray(approx.weights, dtype=complex)
-    k = len(shifts)
-    if len(np.unique(shifts)) != k:
-        raise ValueError("approximation shifts must be distinct")
-    requested = workers
-    if workers is None:
-        workers = 1
-    if workers < 1:
-        raise ValueError(f"workers must be >= 1, got {workers}")
-    if solver not in _SOLVERS:
-        raise ValueError(f"unknown solver {solver!r}")
-    if sr_value is None:
-        from .spectral import spectral_radius_estimate
-        sr_value = spectral_radius_estimate(sys, device=0 if device is None else int(device))
-    ratio, admissible = _admissibility(tau, sr_value, approx.domain_radius)
-    dev = 0 if device is None else int(device)
 
-    indptr, indices, a_re, a_im, b_re = shared_pattern(sys.A, sys.B)
-    if refine is None:
-        rows = np.repeat(np.arange(len(indptr) - 1), np.diff(indptr))
-        tridiagonal = len(indices) == 0 or int(np.max(np.abs(indices - rows))) <= 1
-        if tridiagonal and solver != "cocg":
-            refine = 1 if tau * float(sr_value) > AUTO_REFINE_STIFFNESS else 0
-        else:
-            refine = 1          # COCG: one double-double refinement round
-    pieces = [c for c in np.array_split(np.arange(k), min(workers, k)) if len(c)]
+def _make_plans(stepper_args, pieces, piece_devs):
+    """One native plan per piece (shift index list) on its device."""
+    (indptr, indices, a_re, a_im, b_re, shifts, weights, tau, solver, refine, tol, max_iters,
+     wref) = stepper_args
     plans = []
     try:
-        for idx in pieces:
+        for idx, dev in zip(pieces, piece_devs):
+            idx = np.asarray(idx, dtype=np.int64)
             try:
                 plans.append(_native.NativePlan(
                     indptr, indices, a_re, b_re, shifts[idx], weights[idx], tau, a_imag=a_im,
                     device=dev, solver=_SOLVERS[solver], refine=int(refine),
                     tol=float(tol or 0.0), max_iters=int(max_iters or 0),
-                    shift_offset=int(idx[0]), weight_ref=float(np.mean(np.abs(weights)))))
+                    shift_offset=int(idx[0]), weight_ref=wref, shift_ids=idx))
             except SolverError as exc:
                 m = re.search(r"j = (\d+)", str(exc))
                 j = int(m.group(1)) if m else int(idx[0])
@@ -237,6 +214,73 @@ def rexi_prepare(
         for p in plans:
             p.close()
         raise
+    return plans
+
+
+def rexi_prepare(
+    sys,
+    approx,
+    tau: float,
+    *,
+    workers: int | None = None,
+    sr_value: float | None = None,
+    override_admissibility: bool = False,
+    device: int | None = None,
+    devices=None,
+    refine: int | None = None,
+    solver: str = "auto",
+    tol: float | None = None,
+    max_iters: int | None = None,
+) -> RexiStepper:
+    """Form and factor the K shifted systems on the GPU(s) (ref ``:143-190``).
+
+    ``workers`` keeps the reference's meaning -- the number of pieces the K
+    shifts are split into (ref ``:114-120``) -- and the pieces are spread
+    round-robin over the GPUs: ``devices`` (list of CUDA ordinals; default
+    all visible GPUs for steps of at least ``MULTI_GPU_MIN_WORK`` row-shifts,
+    else GPU 0, or ``[device]`` when ``device`` is given).  ``workers=None``
+    gives one piece per GPU and reports ``workers = K`` like the reference's
+    default (``:161-162``).  Pieces produce double-double partial sums that
+    are combined in fixed piece order, so the answer does not depend on the
+    split.  With COCG on several GPUs the pieces are re-balanced once after
+    the first step by the measured per-shift iteration counts (LPT).
+
+    Extra keyword-only knobs (all optional): ``refine`` (double-double
+    residual-refinement rounds; default by stiffness), ``solver`` ("auto" |
+    "tridiag" | "cocg"), ``tol`` and ``max_iters`` for COCG.
+    """
+    if not tau > 0:
+        raise ValueError(f"tau must be positive, got {tau}")
+    shifts = np.asarray(approx.shifts, dtype=complex)
+    weights = np.asarray(approx.weights, dtype=complex)
+    k = len(shifts)
+    if len(np.unique(shifts)) != k:
+        raise ValueError("approximation shifts must be distinct")
+    if workers is not None and workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    if solver not in _SOLVERS:
+        raise ValueError(f"unknown solver {solver!r}")
+    devs = _default_devices(int(sys.n_dof), k, device, devices)
+    if sr_value is None:
+        from .spectral import spectral_radius_estimate
+        sr_value = spectral_radius_estimate(sys, device=devs[0])
+    ratio, admissible = _admissibility(tau, sr_value, approx.domain_radius)
+
+    indptr, indices, a_re, a_im, b_re = shared_pattern(sys.A, sys.B)
+    if refine is None:
+        rows = np.repeat(np.arange(len(indptr) - 1), np.diff(indptr))
+        tridiagonal = len(indices) == 0 or int(np.max(np.abs(indices - rows))) <= 1
+        if tridiagonal and solver != "cocg":
+            refine = 1 if tau * float(sr_value) > AUTO_REFINE_STIFFNESS else 0
+        else:
+            refine = 1          # COCG: one double-double refinement round
+    n_pieces = min(workers, k) if workers is not None else min(len(devs), k)
+    devs = devs[:n_pieces]          # one concurrent slot (host thread) per entry
+    pieces = [list(map(int, c)) for c in np.array_split(np.arange(k), n_pieces) if len(c)]
+    piece_devs = [devs[q % len(devs)] for q in range(len(pieces))]
+    args = (indptr, indices, a_re, a_im, b_re, shifts, weights, tau, solver, refine, tol, max_iters,
+            float(np.mean(np.abs(weights))))
+    plans = _make_plans(args, pieces, piece_devs)
 
     info = plans[0].info
     band = int(info.bandwidth)
@@ -245,22 +289,27 @@ def rexi_prepare(
         tau=tau,
         system=sys,
         factorizations=[],
-        workers=workers if requested is not None else workers,
+        workers=int(workers) if workers is not None else k,
         sr_value=float(sr_value),
         admissibility_ratio=ratio,
         admissible=admissible,
         override_admissibility=override_admissibility,
         plans=plans,
-        pieces=[list(map(int, c)) for c in pieces],
-        device=dev,
+        pieces=pieces,
+        device=devs[0],
         refine=int(info.refine),
         solver={1: "tridiag", 2: "cocg"}.get(int(info.solver), "auto"),
         stats={"bandwidth": band if band <= 32 else None,
                "levels": int(info.levels), "k_pad": int(info.k_pad),
+               "devices": sorted(set(piece_devs)),
                "device_bytes": int(sum(p.info.device_bytes for p in plans)),
                "prepare_ms": float(sum(p.info.prepare_ms for p in plans)),
-               "min_pivot_ratio": float(min(p.info.min_pivot_ratio for p in plans))},
+               "min_pivot_ratio": float(min(p.info.min_pivot_ratio for p in plans)),
+               "steps": 0, "per_step": []},
     )
+    stepper._plan_args = args
+    stepper._slots = devs
+    stepper._rebalanced = len(devs) < 2 or stepper.solver != "cocg"
     stepper.factorizations = [ShiftedSystem(stepper, j) for j in range(k)]
     return stepper
 
@@ -269,25 +318,147 @@ def _is_torch(u) -> bool:
     return type(u).__module__.startswith("torch")
 
 
-def _step_pieces_device(stepper: RexiStepper, u_t, out_t, n_steps: int):
-    """Multi-piece stepping on device tensors (torch plumbing only)."""
-    import torch
-    n = u_t.shape[0]
-    g = len(stepper.plans)
-    parts = torch.empty((g, 4, n), dtype=torch.float64, device=u_t.device)
+def _record(stepper: RexiStepper, st: _native.RexiStats | None, wall: float, staged: float = 0.0,
+            finish: float = 0.0):
+    """Fold one native call into the reference timers (seconds, wall clock
+    like ``integrate.py:203-225``) and the per-step stats.  The native
+    stats split the device time into rhs / local / reduce (see rexi_stats in
+    include/rexi_b200.h); host staging counts as rhs, host finishing as reduce."""
+    t_rhs = t_red = 0.0
+    if st is not None:
+        t_rhs, t_red = st.t_rhs_ms * 1e-3, st.t_reduce_ms * 1e-3
+    stepper.timers["rhs"] += staged + t_rhs
+    stepper.timers["local"] += max(0.0, wall - t_rhs - t_red)
+    stepper.timers["reduce"] += finish + t_red
+    if st is None:
+        return
+    stepper.stats["steps"] += int(st.steps)
+    stepper.stats["refine_rounds"] = int(st.refine_rounds)
+    stepper.stats["launches"] = int(st.launches)
+    if stepper.solver == "cocg":
+        its = np.zeros(len(stepper.approx.shifts), dtype=np.int32)
+        for plan, idx in zip(stepper.plans, stepper.pieces):
+            its[idx] = plan.shift_iters()
+        stepper.stats["shift_iters"] = its
+        stepper.stats["iters_max"] = int(its.max())
+        stepper.stats["iters_mean"] = float(its.mean())
+        stepper.stats["per_step"].append({"step": stepper.stats["steps"], "steps_in_call": int(st.steps),
+                                          "iters_max": int(its.max()), "iters_mean": float(its.mean())})
+
+
+def _rebalance(stepper: RexiStepper):
+    """COCG on several GPUs: after the first step, re-split the shifts by
+    the measured per-shift iterations, longest-processing-time first (the
+    lockstep cost of a piece grows with its shifts' iterations; SURVEY.md
+    8(e)), keeping the piece count and the piece -> slot assignment."""
+    stepper._rebalanced = True
+    its = stepper.stats.get("shift_iters")
+    if its is None:
+        return
+    from .distributed import shard_indices
+    devs = [p.device for p in stepper.plans]
+    cost = its.astype(float) + 1.0
+    new = shard_indices(len(cost), len(devs), cost)
+    # pieces sharing a slot run one after the other: balance slot loads
+    slots = stepper._slots
+    if len(devs) != len(slots):
+        return
+    old_load = max(cost[i].sum() for i in stepper.pieces)
+    new_load = max(cost[i].sum() for i in new if i)
+    if not new_load < 0.9 * old_load or any(not i for i in new):
+        return
+    plans = _make_plans(stepper._plan_args, new, devs)
+    for p in stepper.plans:
+        p.close()
+    stepper.plans, stepper.pieces = plans, new
+    stepper.stats["rebalanced"] = {"old_max_cost": float(old_load), "new_max_cost": float(new_load)}
+
+
+def _step_pieces_device(stepper: RexiStepper, u_t, n_steps: int):
+    """Multi-piece stepping: u_t on the first plan's device (torch plumbing
+    only).  Each device gets u, runs its pieces' partial sums (one host
+    thread per device: the native calls release the GIL), the partials are
+    gathered on the first device and combined there in piece order."""
     cur = u_t.clone()
+    done = 0
+    while done < n_steps:
+        cur, ran = _pieces_chunk(stepper, cur, n_steps - done)
+        done += ran
+    return cur
+
+
+def _pieces_chunk(stepper: RexiStepper, cur, n_steps: int):
+    """Steps until n_steps are done or the pieces are re-balanced (after
+    which the device buffers must be rebuilt); returns (state, steps run)."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    n = cur.shape[0]
+    g = len(stepper.plans)
+    dev0 = torch.device("cuda", stepper.plans[0].device)
+    nslot = max(1, len(stepper._slots))
+    by_dev = {}        # slot -> piece indices (one host thread per slot)
+    for q in range(g):
+        by_dev.setdefault(q % nslot, []).append(q)
+    bufs = {d: (torch.empty(n, dtype=torch.complex128, device=f"cuda:{stepper.plans[qs[0]].device}"),
+                torch.empty((len(qs), 4, n), dtype=torch.float64,
+                            device=f"cuda:{stepper.plans[qs[0]].device}"))
+            for d, qs in by_dev.items()}
+    parts = torch.empty((g, 4, n), dtype=torch.float64, device=dev0)
     nxt = torch.empty_like(cur)
-    for _ in range(n_steps):
-        t0 = time.perf_counter()
-        for q, plan in enumerate(stepper.plans):
-            plan.step_partial(cur.data_ptr(), parts[q].data_ptr())
-        t1 = time.perf_counter()
-        _native.combine_partials(parts.data_ptr(), g, n, nxt.data_ptr())
-        t2 = time.perf_counter()
-        stepper.timers["local"] += t1 - t0
-        stepper.timers["reduce"] += t2 - t1
-        cur, nxt = nxt, cur
-    out_t.copy_(cur)
+
+    def run_dev(d):
+        ub, pb = bufs[d]
+        stream = torch.cuda.current_stream(stepper.plans[by_dev[d][0]].device).cuda_stream
+        for i, q in enumerate(by_dev[d]):
+            plan = stepper.plans[q]
+            plan.wait_stream(stream)
+            plan.step_partial(ub.data_ptr(), pb[i].data_ptr())
+
+    pool = ThreadPoolExecutor(max_workers=len(by_dev)) if len(by_dev) > 1 else None
+    ran = 0
+    try:
+        while ran < n_steps:
+            t0 = time.perf_counter()
+            for d in by_dev:
+                bufs[d][0].copy_(cur)
+            t1 = time.perf_counter()
+            if pool is None:
+                for d in by_dev:
+                    run_dev(d)
+            else:
+                list(pool.map(run_dev, list(by_dev)))
+            t2 = time.perf_counter()
+            for d, qs in by_dev.items():
+                for i, q in enumerate(qs):
+                    parts[q].copy_(bufs[d][1][i])
+            with torch.cuda.device(dev0):
+                _native.combine_partials(parts.data_ptr(), g, n, nxt.data_ptr(),
+                                         torch.cuda.current_stream(dev0).cuda_stream)
+            torch.cuda.current_stream(dev0).synchronize()
+            t3 = time.perf_counter()
+            stepper.timers["rhs"] += t1 - t0
+            stepper.timers["local"] += t2 - t1
+            stepper.timers["reduce"] += t3 - t2
+            stepper.stats["steps"] += 1
+            if stepper.solver == "cocg":
+                its = np.zeros(len(stepper.approx.shifts), dtype=np.int32)
+                for plan, idx in zip(stepper.plans, stepper.pieces):
+                    its[idx] = plan.shift_iters()
+                stepper.stats["shift_iters"] = its
+                stepper.stats["iters_max"] = int(its.max())
+                stepper.stats["iters_mean"] = float(its.mean())
+                stepper.stats["per_step"].append({"step": stepper.stats["steps"], "steps_in_call": 1,
+                                                  "iters_max": int(its.max()),
+                                                  "iters_mean": float(its.mean())})
+            cur, nxt = nxt, cur
+            ran += 1
+            if not stepper._rebalanced:
+                _rebalance(stepper)
+                break
+    finally:
+        if pool is not None:
+            pool.shutdown()
+    return cur, ran
 
 
 def _run_native(stepper: RexiStepper, u, n_steps: int):
@@ -296,26 +467,36 @@ def _run_native(stepper: RexiStepper, u, n_steps: int):
         import torch
         if not u.is_cuda:
             return torch.from_numpy(_run_native(stepper, u.detach().cpu().numpy(), n_steps))
-        u_t = u.to(torch.complex128).contiguous()
-        out = torch.empty_like(u_t)
+        t0 = time.perf_counter()
+        dev = torch.device("cuda", stepper.plans[0].device)
+        u_t = u.to(device=dev, dtype=torch.complex128).contiguous()
         if len(stepper.plans) == 1:
-            t0 = time.perf_counter()
-            stepper.plans[0].step_device(u_t.data_ptr(), out.data_ptr(), n_steps)
-            stepper.timers["local"] += time.perf_counter() - t0
-        else:
-            _step_pieces_device(stepper, u_t, out, n_steps)
-        return out
+            out = torch.empty_like(u_t)
+            plan = stepper.plans[0]
+            # the input was produced on torch's current stream: order the plan after it
+            plan.wait_stream(torch.cuda.current_stream(dev).cuda_stream)
+            st = _native.RexiStats()
+            t1 = time.perf_counter()
+            plan.step_device(u_t.data_ptr(), out.data_ptr(), n_steps, st)
+            _record(stepper, st, time.perf_counter() - t1, staged=t1 - t0)
+            return out
+        return _step_pieces_device(stepper, u_t, n_steps)
+    t0 = time.perf_counter()
     u = np.ascontiguousarray(u, dtype=complex)
     if len(stepper.plans) == 1:
-        t0 = time.perf_counter()
-        out = stepper.plans[0].step_host(u, n_steps)
-        stepper.timers["local"] += time.perf_counter() - t0
+        st = _native.RexiStats()
+        t1 = time.perf_counter()
+        out = stepper.plans[0].step_host(u, n_steps, st)
+        _record(stepper, st, time.perf_counter() - t1, staged=t1 - t0)
         return out
     import torch
-    u_t = torch.from_numpy(u).to(f"cuda:{stepper.device}")
-    out_t = torch.empty_like(u_t)
-    _step_pieces_device(stepper, u_t, out_t, n_steps)
-    return out_t.cpu().numpy()
+    u_t = torch.from_numpy(u).to(f"cuda:{stepper.plans[0].device}")
+    stepper.timers["rhs"] += time.perf_counter() - t0
+    out_t = _step_pieces_device(stepper, u_t, n_steps)
+    t2 = time.perf_counter()
+    out = out_t.cpu().numpy()
+    stepper.timers["reduce"] += time.perf_counter() - t2
+    return out
 
 
 def rexi_step(stepper: RexiStepper, u):
@@ -324,8 +505,19 @@ def rexi_step(stepper: RexiStepper, u):
     return _run_native(stepper, u, 1)
 
 
-def rexi_run(stepper: RexiStepper, u0, n_steps: int, observer: Observer | None = None):
-    """Apply rexi_step ``n_steps`` times (ref ``integrate.py:229-245``)."""
+def rexi_run(stepper: RexiStepper, u0, n_steps: int, observer: Observer | None = None, *,
+             readonly_observer: bool = False):
+    """Apply rexi_step ``n_steps`` times (ref ``integrate.py:229-245``).
+
+    With an observer each step starts from the very array the observer was
+    handed, as in the reference loop, so an observer that modifies the state
+    in place steers the run.  ``readonly_observer=True`` promises the
+    observer does not modify its argument: the states of a whole chunk of
+    steps are then produced on the device in one native call
+    (``rexi_plan_run``: one launch for small 1D plans) and handed out in
+    order afterwards -- bitwise the same states, much faster for small
+    systems.
+    """
     if n_steps < 0:
         raise ValueError(f"n_steps must be >= 0, got {n_steps}")
     if n_steps > 0:
@@ -337,23 +529,26 @@ def rexi_run(stepper: RexiStepper, u0, n_steps: int, observer: Observer | None =
     if n_steps == 0:
         return u
     if observer is None:
+        if stepper.solver == "cocg" and len(stepper.plans) == 1:
+            # one native call per step: per-step stats (iterations) are kept
+            for _ in range(n_steps):
+                u = _run_native(stepper, u, 1)
+            return u
         return _run_native(stepper, u, n_steps)
-    if len(stepper.plans) == 1 and not _is_torch(u):
-        # every state is produced on the device (rexi_plan_run: one launch for
-        # small 1D plans), copied back in chunks, and handed to the observer
-        # in order; each state is its own array, as in the reference loop
+    if readonly_observer and len(stepper.plans) == 1 and not _is_torch(u):
         n = stepper.plans[0].n
         chunk = max(1, min(n_steps, RUN_CHUNK_BYTES // (16 * max(n, 1))))
         k = 0
         while k < n_steps:
             c = min(chunk, n_steps - k)
             t0 = time.perf_counter()
-            states = stepper.plans[0].run_host(u, c)
-            stepper.timers["local"] += time.perf_counter() - t0
+            st = _native.RexiStats()
+            states = stepper.plans[0].run_host(u, c, st)
+            _record(stepper, st, time.perf_counter() - t0)
             for s in range(c):
                 k += 1
                 observer(k, k * stepper.tau, states[s])
-            u = states[c - 1]
+            u = np.array(states[c - 1])     # do not keep the pinned chunk alive
         return u
     for k in range(1, n_steps + 1):
         u = rexi_step(stepper, u)

@@ -66,3 +66,36 @@ def test_full_size_cocg_properties(c):
     assert np.all(np.isfinite(u1))
     assert bn1 <= bn0 * (1.0 + ap.sup_error + 1e-9)
     stp.close()
+
+
+@pytest.mark.parametrize("c", [3, 5])
+def test_full_size_step1_vs_cpu_truth(c):
+    """Step 1 of the FULL-SIZE config c (1M / 2M DOF, K = 64, BASELINE tau)
+    against the CPU truth restatement (oracle.cocg_truth_step: COCG refined
+    against double-double residuals to 1e-22, exact dd sum), precomputed by
+    tests/golden/make_fullsize.py and kept as u1 at 8192 seeded rows plus 4
+    seeded projections <w, u1> of the whole vector."""
+    import os
+    import sys
+    from paper_1912_03312_b200 import fixtures, rexi_prepare, rexi_step
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, here)
+    from fullsize_probes import probes
+    g = np.load(os.path.join(here, "fullsize", f"cfg{c}_step1.npz"))
+    cfg = fixtures.build_config(c)
+    n = cfg.system.n_dof
+    assert n == int(g["n"]) and cfg.tau == float(g["tau"])
+    assert abs(np.linalg.norm(cfg.u0) - float(g["norm_u0"])) <= 1e-13 * float(g["norm_u0"])
+    stp = rexi_prepare(cfg.system, cfg.approx, cfg.tau, sr_value=cfg.sr, override_admissibility=True)
+    u1 = rexi_step(stp, cfg.u0)
+    stp.close()
+    rows, w = probes(c, n)
+    assert np.array_equal(rows, g["rows"])
+    u_ref = g["u1_rows"]
+    e_rows = np.linalg.norm(u1[rows] - u_ref) / np.linalg.norm(u_ref)
+    proj = w @ u1
+    e_proj = np.abs(proj - g["proj"]) / np.abs(g["proj"])
+    e_norm = abs(np.linalg.norm(u1) - float(g["norm_u1"])) / float(g["norm_u1"])
+    assert e_rows <= 1e-8, e_rows          # north_star: rel-L2 <= 1e-8
+    assert np.all(e_proj <= 1e-8), e_proj
+    assert e_norm <= 1e-9, e_norm

@@ -225,7 +225,9 @@ def test_library_exports_all_declared_symbols():
     assert not missing, missing
     L = ctypes.CDLL(lib)
     L.rexi_abi_version.restype = ctypes.c_int32
-    assert L.rexi_abi_version() == 1
+    from paper_1912_03312_b200 import _native
+    assert L.rexi_abi_version() == _native.ABI_VERSION == 2
+    assert set(_declared_functions()) <= set(_native.EXPORTED) | {"rexi_abi_version"}
 
 
 def test_library_is_sm100a_only():
