@@ -45,17 +45,51 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--refine", type=int, default=-1, help="-1: auto (parity-correct)")
+    ap.add_argument("--refine", type=int, default=-1, help="-1: rexi_prepare's default")
+    ap.add_argument("--secondary", type=int, default=-1,
+                    help="also time this config's steps in a 'secondary' block (default: cfg 3 when "
+                         "the main config is 2 and N = 1; 0 = off)")
+    ap.add_argument("--secondary-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps")
     return ap.parse_args()
 
 
-def workload_name(cfg, refine):
+def workload_name(cfg):
+    """The same string in both arms (the refinement setting is a separate
+    config key: it is how an arm computes, not what the workload is)."""
     n, k = cfg.system.n_dof, cfg.approx.K
     dims = {1: "1D", 2: "2D", 3: "3D"}[cfg.mesh.d]
     return (f"{cfg.name}: {dims} P1 Schroedinger REXI step, {n} DOF, nnz {cfg.system.A.nnz}, "
-            f"K={k}, tau={cfg.tau}, refine={refine}")
+            f"K={k}, tau={cfg.tau}")
+
+
+def api_refine(cfg):
+    """rexi_prepare's default refinement for this config (integrate.default_refine)."""
+    from paper_1912_03312_b200._pattern import shared_pattern
+    from paper_1912_03312_b200.integrate import default_refine
+    ip, ix = shared_pattern(cfg.system.A, cfg.system.B)[:2]
+    return default_refine(ip, ix, cfg.tau, cfg.sr)
+
+
+def cocg_8d_bytes(prof, n, nnz, k, steps):
+    """SURVEY.md 8(d)'s algorithmic bytes of a COCG step: per lockstep
+    iteration (20 nnz + 4 (N+1)) + 160 K_act N, plus 16 N (2 + 3K) for the
+    prologue / epilogue; the refinement's dd-residual SpMVs count as extra
+    iterations with K_act = K.  sum(K_act) over the iterations comes from the
+    spmv hooks' own byte counts (80 B per live row-shift + the CSR bytes)."""
+    csr_impl = 28.0 * nnz + 4.0 * (n + 1)
+    csr_8d = 20.0 * nnz + 4.0 * (n + 1)
+    total, iters, kact_n = 0.0, 0, 0.0
+    for name, (cnt, _t, b) in prof.items():
+        if name.startswith("cg_spmv"):
+            kact_n += max(0.0, (b - cnt * csr_impl) / 80.0)
+            iters += cnt
+        elif name.startswith("cg_residual"):
+            kact_n += cnt * k * n
+            iters += cnt
+    total = iters * csr_8d + 160.0 * kact_n + steps * 16.0 * n * (2 + 3 * k)
+    return total / steps, iters / steps, kact_n / max(iters, 1) / n
 
 
 def measured_peak():
@@ -169,11 +203,11 @@ def load_traffic(name):
         return {}
 
 
-def cpu_baseline_cocg(cfg, shifts=4):
+def cpu_baseline_cocg(cfg, shifts=4, refine=1, repeats=1):
     """2D/3D: the reference cannot run (dense-LU fallback, solvers.py:108-115);
     time the C/OpenMP Jacobi-COCG restatement (oracle/cocg_oracle.c, same
-    stopping rule and refinement) on a bounded sample of `shifts` of the K
-    shifts and scale to a full step."""
+    stopping rule, refinement as the GPU arm) on a bounded sample of
+    `shifts` of the K shifts, `repeats` times, and scale to a full step."""
     import numpy as np
     from oracle.oracle import cocg_step
     from paper_1912_03312_b200.types import PartialFractionApproximation
@@ -183,19 +217,23 @@ def cpu_baseline_cocg(cfg, shifts=4):
     sub = PartialFractionApproximation(cfg.approx.shifts[idx], cfg.approx.weights[idx],
                                        cfg.approx.domain_radius, 0.0)
     t0 = time.perf_counter()
-    cocg_step(cfg.system, sub, cfg.tau, cfg.u0, tol=1e-10, refine=1, tol_refine=1e-6, nthreads=cores)
-    dt = (time.perf_counter() - t0) * k / shifts
-    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{shifts} of {k} shifts (evenly spaced) of one {cfg.name} step through "
-                      "oracle/cocg_oracle.c (Jacobi-COCG 1e-10 + dd-residual correction 1e-6), "
-                      f"OpenMP over shifts on {cores} threads, time scaled by K/{shifts}"}
+    for _ in range(repeats):
+        cocg_step(cfg.system, sub, cfg.tau, cfg.u0, tol=1e-10, refine=refine, tol_refine=1e-6,
+                  nthreads=cores)
+    steps_eq = repeats * shifts / k
+    dt = (time.perf_counter() - t0) / steps_eq
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "port", "steps_equivalent": steps_eq,
+            "sample": f"{repeats} x {shifts} of {k} shifts (evenly spaced) of step 1 of {cfg.name} through "
+                      f"oracle/cocg_oracle.c (Jacobi-COCG 1e-10, refine={refine}: dd-residual correction "
+                      f"1e-6), OpenMP over shifts on {cores} threads; value = full steps/s, the sample "
+                      f"time scaled by K/{shifts}"}
 
 
 def cpu_baseline(cfg, steps=2):
     """The reference algorithm restated in C (oracle/, kind "port"), timed on
     this host's cores: factor once (not timed), then `steps` full steps."""
     if cfg.mesh.d > 1:
-        return cpu_baseline_cocg(cfg)
+        return cpu_baseline_cocg(cfg, refine=api_refine(cfg))
     from oracle.oracle import OraclePlan
     cores = os.cpu_count() or 1
     orc = OraclePlan(cfg.system, cfg.approx, cfg.tau, nthreads=cores)
@@ -219,9 +257,19 @@ def run_reference(args, rank, world):
     from oracle.oracle import OraclePlan
     cfg = fixtures.build_config(args.config)
     cores = os.cpu_count() or 1
+    refine = api_refine(cfg)
     if cfg.mesh.d > 1:
-        cb = cpu_baseline_cocg(cfg)
-        v, dt = cb["value"], args.steps / cb["value"]
+        # 2D/3D: the reference cannot run (dense-LU fallback); one full CPU
+        # step takes minutes, so the arm times a bounded sample (4 of the K
+        # shifts) and reports what it ran: `steps` is the number of full-step
+        # equivalents actually computed (samples x 4/K), `ms_per_step` the
+        # measured time per full-step equivalent
+        samples = max(1, min(args.steps, 2))
+        cb = cpu_baseline_cocg(cfg, refine=refine, repeats=samples)
+        v = cb["value"]
+        steps_done = cb["steps_equivalent"]
+        dt = steps_done / v
+        sample = cb["sample"]
     else:
         orc = OraclePlan(cfg.system, cfg.approx, cfg.tau, nthreads=cores)
         u = cfg.u0
@@ -232,16 +280,88 @@ def run_reference(args, rank, world):
             u = orc.step(u)
         dt = time.perf_counter() - t0
         v = args.steps / dt
+        steps_done = args.steps
+        sample = (f"{args.steps} full steps, reference algorithm restated in C "
+                  "(oracle/rexi_oracle.c: zgbtrf/zgbtrs, fl(beta x), Kahan), OpenMP over shifts")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "steps": steps_done, "warmup": args.warmup, "ms_per_step": 1e3 * dt / steps_done,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "complex128",
             "data": "synthetic (seeded fixtures, poles frozen from the reference generator)",
-            "config": {"workload": workload_name(cfg, "n/a (direct LU)"), "parallelism": "host threads"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full steps, reference algorithm restated in C "
-                                       "(oracle/rexi_oracle.c), OpenMP over shifts"},
+            "config": {"workload": workload_name(cfg), "refine": "n/a (direct LU)" if cfg.mesh.d == 1 else refine,
+                       "parallelism": "host threads"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def secondary(c, steps, local, peak):
+    """The 2D north_star target on the same run: device-timed steps of
+    config c (default cfg 3: 2D, 1M DOF, K = 64) at rexi_prepare's default
+    refinement, one warm-up step, then `steps` consecutive steps (2..steps+1
+    of the trajectory) timed with CUDA events on the plan's stream, and a
+    second pass over the same steps with per-kernel profiling for the
+    SURVEY.md 8(d) step bytes.  The per-shift arrays (1 GB each) exceed L2."""
+    import torch
+    from paper_1912_03312_b200 import fixtures, _native
+    from paper_1912_03312_b200._pattern import shared_pattern
+    t_build = time.perf_counter()
+    cfg = fixtures.build_config(c)
+    n, k, nnz = cfg.system.n_dof, cfg.approx.K, cfg.system.A.nnz
+    refine = api_refine(cfg)
+    stream = torch.cuda.current_stream()
+    ip, ix, ar, ai, br = shared_pattern(cfg.system.A, cfg.system.B)
+    plan = _native.NativePlan(ip, ix, ar, br, cfg.approx.shifts, cfg.approx.weights, cfg.tau, a_imag=ai,
+                              device=local, refine=refine, stream=stream.cuda_stream)
+    t_build = time.perf_counter() - t_build
+    u0 = torch.from_numpy(cfg.u0).to(f"cuda:{local}")
+    u1 = torch.empty_like(u0)
+    bufs = [torch.empty_like(u0), torch.empty_like(u0)]
+    st = _native.RexiStats()
+    plan.step_device(u0.data_ptr(), u1.data_ptr(), 1, st)         # warm-up = step 1
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        src = u1
+        for s in range(steps):
+            st = _native.RexiStats()
+            plan.step_device(src.data_ptr(), bufs[s % 2].data_ptr(), 1, st)
+            launches += int(st.launches)
+            src = bufs[s % 2]
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    plan.profile(True)
+    src = u1
+    iters = []
+    for s in range(steps):
+        plan.step_device(src.data_ptr(), bufs[s % 2].data_ptr(), 1, _native.RexiStats())
+        iters.append(int(plan.shift_iters().max()))
+        src = bufs[s % 2]
+    torch.cuda.synchronize()
+    prof = plan.profile_report()
+    plan.profile(False)
+    plan.close()
+    step_bytes, it_step, kact = cocg_8d_bytes(prof, n, nnz, k, steps)
+    ms_step = ms / steps
+    ach = step_bytes / (ms_step / 1e3) / 1e9
+    dom = max(prof.items(), key=lambda kv: kv[1][1])
+    return {
+        "workload": workload_name(cfg), "refine": refine, "steps": steps, "warmup": 1,
+        "timed": f"steps 2..{steps + 1} of the trajectory from u0, device-resident state, CUDA events "
+                 "on the plan's stream",
+        "value": steps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms_step, "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "algorithmic_bytes_per_step": step_bytes,
+                     "bytes": "SURVEY.md 8(d): per lockstep iteration (20 nnz + 4(N+1)) + 160 K_act N, plus "
+                              "16 N (2 + 3K) per step; dd-residual SpMVs count as iterations with K_act = K",
+                     "lockstep_iterations_per_step": it_step, "mean_live_lanes": kact,
+                     "max_shift_iterations": iters},
+        "dominant_kernel": {"name": dom[0], "share_of_step": dom[1][1] / sum(v[1] for v in prof.values())},
+        "kernels": {kname: {"launches": cnt, "total_ms": t} for kname, (cnt, t, _b) in prof.items()},
+        "clocks": clk.summary(), "setup_s": t_build,
+    }
 
 
 def max_over_ranks(x, backend, local):
@@ -280,9 +400,12 @@ def main():
             dist.init_process_group(backend)
     cfg = fixtures.build_config(args.config)
     n, k = cfg.system.n_dof, cfg.approx.K
+    sec_cfg = args.secondary if args.secondary >= 0 else (3 if args.config == 2 and world == 1 else 0)
+    if world > 1 or sec_cfg == args.config:
+        sec_cfg = 0
     refine = args.refine
     if refine < 0:
-        refine = 1 if cfg.tau * cfg.sr > 5e3 else 0
+        refine = api_refine(cfg)      # what rexi_prepare does by default
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     u0 = torch.from_numpy(cfg.u0).to(f"cuda:{local}")
@@ -320,6 +443,14 @@ def main():
     # warm-up
     run(args.warmup, ua, ub)
     torch.cuda.synchronize()
+    if world > 1 and cfg.mesh.d > 1:
+        # COCG: balance the pole shards by the per-shift iterations of the
+        # last warm-up step (longest processing time first),
+        # then warm the re-built plans once
+        sh.reshard(sh.measure_costs())
+        plan = sh.plan
+        run(1, ua, ub)
+        torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -420,6 +551,8 @@ def main():
         avg_ms = tot / max(cnt, 1)
         ach = (b / (avg_ms / 1e3)) / 1e9 if b else None
         ev = load_traffic(name)
+        if ev.get("config") not in (None, args.config):
+            ev = {}           # an ncu capture of another config is not this kernel's traffic
         roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": (ach / peak) if ach else None, "traffic": ev.get("dram_bytes"),
                 "algorithmic_bytes_per_launch": b, "avg_launch_ms": avg_ms,
@@ -460,13 +593,19 @@ def main():
             kb = kernel_bytes(kname, n, kshard_) if b_ <= 0 else None
             prof_bytes += b_ if b_ > 0 else (kb or 0) * cnt_
         step_bytes = prof_bytes / args.steps if prof_bytes > 0 else 80 * n + 32 * k * n
+        bytes_note = "the kernels' own algorithmic byte counts (bench.kernel_bytes / the COCG hooks)"
+        cg_iters = cg_kact = None
+        if cfg.mesh.d > 1:
+            step_bytes, cg_iters, cg_kact = cocg_8d_bytes(prof, n, cfg.system.A.nnz, kshard_, args.steps)
+            bytes_note = ("SURVEY.md 8(d): per lockstep iteration (20 nnz + 4(N+1)) + 160 K_act N, plus "
+                          "16 N (2 + 3K) per step; dd-residual SpMVs count as iterations with K_act = K")
         prof_ms = sum(v[1] for v in prof.values())
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "complex128",
             "data": "synthetic (seeded fixtures, poles frozen from the reference generator)",
-            "config": {"workload": workload_name(cfg, refine), "n_dof": n, "K": k, "tau": cfg.tau,
+            "config": {"workload": workload_name(cfg), "n_dof": n, "K": k, "tau": cfg.tau,
                        "refine": refine, "parallelism": f"pole-shard x{world}" if world > 1 else "1 GPU",
                        "l2": l2_note(n, k)},
             "e2e": e2e,
@@ -482,9 +621,13 @@ def main():
                 "achieved_GBps": step_bytes / (ms / args.steps / 1e3) / 1e9,
                 "frac": step_bytes / (ms / args.steps / 1e3) / 1e9 / peak,
                 "kernel_time_frac": (prof_ms / ms) if prof_ms and not persistent else None,
+                "bytes": bytes_note,
+                "cocg_iterations_per_step": cg_iters, "cocg_mean_live_lanes": cg_kact,
                 "note": "whole step (all kernels, launch gaps and host polls included) against the "
                         "measured HBM peak"},
         }
+        if sec_cfg:
+            line["secondary"] = secondary(sec_cfg, args.secondary_steps, local, peak)
         print(json.dumps(line), flush=True)
     if world > 1:
         sh.close()

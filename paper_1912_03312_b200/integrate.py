@@ -217,6 +217,20 @@ def _make_plans(stepper_args, pieces, piece_devs):
     return plans
 
 
+def default_refine(indptr, indices, tau: float, sr_value: float, solver: str = "auto") -> int:
+    """The refinement rounds ``rexi_prepare`` uses when ``refine`` is not
+    given: the direct 1D solver refines once on stiff pencils (tau*sr above
+    AUTO_REFINE_STIFFNESS, where the fp64 solve alone drifts past 1e-8 of
+    truth), COCG always refines once (double-double residual round)."""
+    indptr = np.asarray(indptr)
+    indices = np.asarray(indices)
+    rows = np.repeat(np.arange(len(indptr) - 1), np.diff(indptr))
+    tridiagonal = len(indices) == 0 or int(np.max(np.abs(indices - rows))) <= 1
+    if tridiagonal and solver != "cocg":
+        return 1 if tau * float(sr_value) > AUTO_REFINE_STIFFNESS else 0
+    return 1
+
+
 def rexi_prepare(
     sys,
     approx,
@@ -268,12 +282,7 @@ def rexi_prepare(
 
     indptr, indices, a_re, a_im, b_re = shared_pattern(sys.A, sys.B)
     if refine is None:
-        rows = np.repeat(np.arange(len(indptr) - 1), np.diff(indptr))
-        tridiagonal = len(indices) == 0 or int(np.max(np.abs(indices - rows))) <= 1
-        if tridiagonal and solver != "cocg":
-            refine = 1 if tau * float(sr_value) > AUTO_REFINE_STIFFNESS else 0
-        else:
-            refine = 1          # COCG: one double-double refinement round
+        refine = default_refine(indptr, indices, tau, sr_value, solver)
     n_pieces = min(workers, k) if workers is not None else min(len(devs), k)
     devs = devs[:n_pieces]          # one concurrent slot (host thread) per entry
     pieces = [list(map(int, c)) for c in np.array_split(np.arange(k), n_pieces) if len(c)]
