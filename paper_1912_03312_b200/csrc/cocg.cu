@@ -18,7 +18,8 @@
 //           work on one narrow wavefront and the +-n neighbour rows of a 2D/3D
 //           stencil are L2 hits; the per-chunk partials are indexed by chunk,
 //           so the reduction order is fixed (deterministic).
-//   update: x += alpha p, r -= alpha q, z = D^-1 r, rho' = r^T z, |r|^2.
+//   update: x += alpha p, z -= alpha D^-1 q (the preconditioned residual; r =
+//           D z is formed for rho' = r^T z and |r|^2 only).
 // The last CTA of each kernel finishes the per-shift scalars (alpha, beta),
 // freezes converged shifts and flags breakdown / non-finite values.
 // Compaction: when at most half of the lanes are live, the live shifts are
@@ -73,7 +74,8 @@ struct CgMat {
 };
 
 struct CgVec {
-    c128 *x, *r, *z, *p, *q;               // [n][kp] current (compacted) layout
+    c128 *x, *z, *p, *q;                   // [n][kp] current (compacted) layout; the residual
+                                           // is kept preconditioned only (r = D z, see k_cg_update)
     const c128 *bvec;                      // per-shift rhs [n][kp_full] or nullptr
     const c128 *bshared;                   // shared rhs [n] or nullptr
 };
@@ -254,7 +256,7 @@ __device__ __forceinline__ double2 add_c(double2 a, double2 b) { return cadd(a, 
 __device__ __forceinline__ double add_r(double a, double b) { return a + b; }
 
 // ---------------------------------------------------------------------------
-// init (full width, lane = shift): x = 0, r = b, z = D^-1 r, p_old = 0;
+// init (full width, lane = shift): x = 0, z = D^-1 b, p_old = 0;
 // partials of rho = r^T z and |b|^2
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
@@ -276,7 +278,6 @@ __global__ void __launch_bounds__(CG_NT) k_cg_init(CgMat M, CgVec V, CgScal Sc, 
                 const c128 b = V.bshared ? V.bshared[i] : V.bvec[o];
                 const c128 z = cdiv_c(b, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
                 V.x[o] = cmk(0.0, 0.0);
-                V.r[o] = b;
                 V.z[o] = z;
                 V.p[o] = cmk(0.0, 0.0);
                 V.q[o] = cmk(0.0, 0.0);
@@ -585,10 +586,10 @@ __global__ void __launch_bounds__(CG1_NT) k_cg_update1(CgMat M, CgVec V, CgScal 
         if (act && i < M.n) {
             const c128 p = V.p[i], q = V.q[i];
             V.x[i] = cadd(V.x[i], cmul(alpha, p));
-            const c128 r = csub(V.r[i], cmul(alpha, q));
-            V.r[i] = r;
-            const c128 z = cdiv_c(r, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
+            const c128 d = form_entry(M.dta[i], M.dta_im[i], M.db[i], sg);
+            const c128 z = csub(V.z[i], cmul(alpha, cdiv_c(q, d)));
             V.z[i] = z;
+            const c128 r = cmul(d, z);
             trho = cmul(r, z);
             trn = cabs2(r);
         }
@@ -602,7 +603,8 @@ __global__ void __launch_bounds__(CG1_NT) k_cg_update1(CgMat M, CgVec V, CgScal 
 }
 
 // ---------------------------------------------------------------------------
-// update: x += alpha p; r -= alpha q; z = D^-1 r; partials of rho' = r^T z, |r|^2
+// update: x += alpha p; z -= alpha D^-1 q; partials of rho' = r^T z, |r|^2 with
+// r = D z (96 B per live row-shift: x, z read + written, p, q read)
 // (claims statically strided over CTAs: pointwise, no locality to exploit)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
@@ -630,10 +632,13 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
                     const size_t o = (size_t)i * kp + lane;
                     const c128 p = pnew[o], q = V.q[o];
                     V.x[o] = cadd(V.x[o], cmul(alpha, p));
-                    const c128 r = csub(V.r[o], cmul(alpha, q));
-                    V.r[o] = r;
-                    const c128 z = cdiv_c(r, form_entry(M.dta[i], M.dta_im[i], M.db[i], sg));
+                    // preconditioned residual recurrence z <- z - alpha D^-1 q;
+                    // r = D z is formed for the dots only (16 B per row-shift
+                    // less than storing r and z)
+                    const c128 d = form_entry(M.dta[i], M.dta_im[i], M.db[i], sg);
+                    const c128 z = csub(V.z[o], cmul(alpha, cdiv_c(q, d)));
                     V.z[o] = z;
+                    const c128 r = cmul(d, z);
                     rho = cadd(rho, cmul(r, z));
                     rn += cabs2(r);
                 }
@@ -1227,7 +1232,6 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     }
     const size_t vb = sizeof(c128) * (size_t)n * kp;
     CGA(im->V.x, vb);
-    CGA(im->V.r, vb);
     CGA(im->V.z, vb);
     CGA(im->V.p, vb);
     CGA(im->V.q, vb);
@@ -1290,7 +1294,7 @@ static int cg_repack(CocgImpl *im, int kp_old, int kp_new, const std::vector<int
     // 2) live vectors x, r, z, p(current) -> new width, through the scratch array
     CGK(cudaMemcpyAsync(im->map, map.data(), sizeof(int) * kp_new, cudaMemcpyHostToDevice, st));
     const int64_t t_new = n * kp_new;
-    c128 **vecs[5] = {&im->V.x, &im->V.r, &im->V.z, &im->V.p, &im->V.q};
+    c128 **vecs[4] = {&im->V.x, &im->V.z, &im->V.p, &im->V.q};
     for (c128 **v : vecs) {
         k_cg_repack<<<(unsigned)((t_new + 255) / 256), 256, 0, st>>>(*v, im->scratch, n, kp_old, kp_new, im->map);
         std::swap(*v, im->scratch);
@@ -1329,7 +1333,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     CgGeom g = make_geom(im, kp, n);
     int grid = grid_for(im, g, n);
     const double nnzb = 28.0 * (double)cg.nnz + 4.0 * (double)(n + 1);   // CSR pattern + 3 value arrays
-    hook_begin(cg, "cg_init", 96.0 * n * kp);
+    hook_begin(cg, "cg_init", 80.0 * n * kp);
     k_cg_init<<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
     k_cg_finish<0><<<finish_grid(g), CG_FL_NT, finish_smem(0), st>>>(im->Sc, g, cg.k, cg.max_iters);
     hook_end(cg);
@@ -1397,7 +1401,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             }
             k_cg_finish<1><<<finish_grid(g), CG_FL_NT, finish_smem(1), st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
-            hook_begin(cg, width_name("cg_update", kp), 112.0 * n * live + 24.0 * n);
+            hook_begin(cg, width_name("cg_update", kp), 96.0 * n * live + 24.0 * n);
             if (g.kp == 1) {
                 const int g1 = (int)std::min<int64_t>((g.nchunks + 7) / 8, (int64_t)im->sms * 16);
                 k_cg_update1<<<g1, CG1_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
@@ -1426,7 +1430,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
         // into a prefix of the same width.  A frozen lane costs bandwidth while
         // it sits between live ones (2 lanes per 32-B sector, 32 per warp
         // segment) and none as trailing padding: the wide phases run at ~80 %
-        // live lanes.  Repacking moves 160 B per live row-shift, about 0.8 of an
+        // live lanes.  Repacking moves 128 B per live row-shift, about 0.7 of an
         // iteration.  Per-lane results are unchanged (layout-independent
         // reduction tree).
         int kp_new = kp;
