@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define REXI_ABI_VERSION 2
+#define REXI_ABI_VERSION 3
 
 typedef struct rexi_c128 { double re, im; } rexi_c128;
 typedef struct rexi_plan rexi_plan;
@@ -137,6 +137,11 @@ typedef struct rexi_info {
     double min_pivot_ratio;    /* TRIDIAG: min over shifts of min|d|/max|d|       */
     int32_t persistent;        /* >0: small 1D plan, all steps of a call run in ONE
                                   launch of a thread-block cluster of this many CTAs */
+    double screen_pivot_ratio; /* bandwidth <= 32: min over shifts of min|U_ii| /
+                                  max|U_ii| of the partially pivoted band LU -- the
+                                  reference's singularity screen (solvers.py:52-69),
+                                  recomputed on the device at plan creation; 1 when
+                                  the band is wider (the reference's dense LU) */
 } rexi_info;
 
 int rexi_plan_create(const rexi_desc *desc, rexi_plan **out);

@@ -57,6 +57,7 @@ def lib():
         L.orc_bandwidth.argtypes = [p]
         L.orc_bandwidth.restype = ctypes.c_int32
         L.orc_rhs.argtypes = [p, p, p]
+        L.orc_screen.argtypes = [p, p, p, p]
         L.orc_cocg_step.restype = ctypes.c_int
         L.orc_cocg_truth_step.restype = ctypes.c_int
         L.orc_cocg_truth_step.argtypes = [ctypes.c_int64, p, p, p, p, ctypes.c_int32, p, p,
@@ -155,6 +156,15 @@ class OraclePlan:
         x = np.empty(self.n, dtype=np.complex128)
         lib().orc_solve(self._p, int(j), _ptr(b), _ptr(x))
         return x
+
+    def screen(self):
+        """Per shift (min|U_ii|, max|U_ii|, info) of the partially pivoted band
+        LU -- the data of the reference's singularity screen (solvers.py:52-69)."""
+        umin = np.zeros(self.k)
+        umax = np.zeros(self.k)
+        info = np.zeros(self.k, dtype=np.int32)
+        lib().orc_screen(self._p, _ptr(umin), _ptr(umax), _ptr(info))
+        return umin, umax, info
 
     def rel_residual(self, j, rhs, x):
         rhs = np.ascontiguousarray(rhs, dtype=np.complex128)

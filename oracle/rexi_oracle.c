@@ -105,6 +105,8 @@ typedef struct {
     int32_t *ipiv;                  /* k * n */
     int32_t nthreads;
     int32_t bad_shift;              /* index of the singular shift, -1 if none */
+    double *umin, *umax;            /* per shift: extremes of |U_ii| (solvers.py:59-69) */
+    int32_t *uinfo;                 /* per shift: zgbtf2 info */
     char msg[256];
 } orc_plan;
 
@@ -225,6 +227,9 @@ orc_plan *orc_create(int64_t n, int64_t nnz, const int32_t *indptr, const int32_
     p->kl = kl; p->ku = ku; p->ldab = 2 * kl + ku + 1;
     p->ab = calloc((size_t)k * p->ldab * n, sizeof(c128));
     p->ipiv = calloc((size_t)k * n, sizeof(int32_t));
+    p->umin = calloc((size_t)(k ? k : 1), sizeof(double));
+    p->umax = calloc((size_t)(k ? k : 1), sizeof(double));
+    p->uinfo = calloc((size_t)(k ? k : 1), sizeof(int32_t));
     if (!p->ab || !p->ipiv) { *status = 7; snprintf(p->msg, sizeof p->msg, "out of memory"); return p; }
     int bad = -1;
     #pragma omp parallel for schedule(dynamic) num_threads(p->nthreads)
@@ -238,14 +243,17 @@ orc_plan *orc_create(int64_t n, int64_t nnz, const int32_t *indptr, const int32_
             }
         int info = gbtf2(p, j);
         int singular = info > 0;
+        double umin = INFINITY, umax = 0.0;
+        for (int64_t c = 0; c < n; ++c) {
+            c128 u = AB(p, j, kv, c);
+            double v = hypot(u.re, u.im);
+            if (v < umin) umin = v;
+            if (v > umax) umax = v;
+        }
+        p->umin[j] = umin;
+        p->umax[j] = umax;
+        p->uinfo[j] = info;
         if (!singular && n > 0) {
-            double umin = INFINITY, umax = 0.0;
-            for (int64_t c = 0; c < n; ++c) {
-                c128 u = AB(p, j, kv, c);
-                double v = hypot(u.re, u.im);
-                if (v < umin) umin = v;
-                if (v > umax) umax = v;
-            }
             if (!(umin > 0.0) || umin < 1e-14 * umax) singular = 1;
         }
         if (singular) {
@@ -265,7 +273,8 @@ int32_t orc_bandwidth(const orc_plan *p) { return p->kl + p->ku + 1; }
 void orc_destroy(orc_plan *p) {
     if (!p) return;
     free(p->indptr); free(p->indices); free(p->a); free(p->b);
-    free(p->shifts); free(p->weights); free(p->ab); free(p->ipiv); free(p);
+    free(p->shifts); free(p->weights); free(p->ab); free(p->ipiv);
+    free(p->umin); free(p->umax); free(p->uinfo); free(p);
 }
 
 /* rhs = 1j * (B @ u) */
@@ -395,6 +404,16 @@ double orc_rel_residual(const orc_plan *p, int32_t j, const c128 *rhs, const c12
     }
     free(res); free(zero);
     return nb > 0 ? sqrt(nr / nb) : sqrt(nr);
+}
+
+/* per-shift singularity screen data of the band LU (tests): extremes of |U_ii|
+ * and zgbtf2's info, as the reference's BandedFactorization sees them */
+void orc_screen(const orc_plan *p, double *umin, double *umax, int32_t *info) {
+    for (int j = 0; j < p->k; ++j) {
+        umin[j] = p->umin[j];
+        umax[j] = p->umax[j];
+        info[j] = p->uinfo[j];
+    }
 }
 
 /* rhs helper exported for tests */

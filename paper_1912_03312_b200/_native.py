@@ -27,7 +27,7 @@ REXI_ERR_UNSUPPORTED = 7
 
 SOLVER_AUTO, SOLVER_TRIDIAG, SOLVER_COCG = 0, 1, 2
 MEM_HOST, MEM_DEVICE = 0, 1
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 EXPORTED = (
     "rexi_plan_create", "rexi_plan_step", "rexi_plan_step_partial", "rexi_combine_partials",
@@ -102,6 +102,7 @@ class RexiInfo(ctypes.Structure):
         ("prepare_ms", ctypes.c_double),
         ("min_pivot_ratio", ctypes.c_double),
         ("persistent", ctypes.c_int32),
+        ("screen_pivot_ratio", ctypes.c_double),
     ]
 
 

@@ -15,6 +15,7 @@
 
 #include "../../include/rexi_b200.h"
 #include "cocg.cuh"
+#include "screen.cuh"
 #include "tridiag_launch.h"
 
 using namespace rexi;
@@ -62,6 +63,7 @@ struct rexi_plan {
     CocgState cg;
     double prepare_ms = 0.0;
     double min_pivot_ratio = 1.0;
+    double screen_ratio = 1.0;    // min over shifts of min|U_ii| / max|U_ii| (pivoted band LU)
     std::vector<rexi_c128> shifts_host;
     int64_t launches = 0;
     // optional per-kernel CUDA-event profiling (rexi_plan_profile)
@@ -324,9 +326,12 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
         double ratio = mx > 0 ? mn / mx : 0.0;
         if (std::isinf(mn)) ratio = 1.0;  // no pivots at all (cannot happen: top level has >= 1 row)
         worst = std::min(worst, ratio);
-        if (!(mn > 0.0) || !(mx < INFINITY) || mn < 1e-14 * mx) {
+        // the reference's verdict (pivoted zgbtrf screen) ran before this
+        // factorization (rexi_plan_create); here only a no-pivot breakdown
+        // the direct solver cannot run through is an error
+        if (!(mn > 0.0) || !(mx < INFINITY)) {
             char buf[256];
-            snprintf(buf, sizeof buf, "matrix is numerically singular (pivot ratio = %.3e) for shift j = %d",
+            snprintf(buf, sizeof buf, "no-pivot block factorization broke down (pivot ratio = %.3e) [shift j = %d]",
                      ratio, plan->gid[j]);
             plan->min_pivot_ratio = ratio;
             return set_err(plan, REXI_ERR_SINGULAR, buf);
@@ -661,6 +666,28 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
         }
         if (!rc) rc = dalloc(plan, &plan->ubuf[0], (size_t)d->n);
         if (!rc) rc = dalloc(plan, &plan->ubuf[1], (size_t)d->n);
+        if (!rc && plan->bandwidth <= 32 && !getenv("REXI_NO_SCREEN")) {
+            // the reference's singularity screen: it factors every shifted system
+            // with partially pivoted zgbtrf when kl + ku + 1 <= 32 (solvers.py:25,
+            // 108-115) and rejects the first shift j whose factor has a zero
+            // pivot or min|U_ii| < 1e-14 max|U_ii| (solvers.py:52-69).  Same
+            // algorithm on the device (screen.cu), same order, same messages.
+            std::vector<rexi::ScreenResult> scr;
+            std::string serr;
+            rc = rexi::band_screen(d, kl, ku, plan->S.sigma, plan->stream, scr, serr);
+            if (rc) {
+                set_err(plan, rc, serr);
+            } else {
+                for (int j = 0; j < d->k; ++j) {
+                    const std::string v = rexi::screen_verdict(scr[j], d->n);
+                    plan->screen_ratio = std::min(plan->screen_ratio, scr[j].umax > 0 ? scr[j].umin / scr[j].umax : 0.0);
+                    if (!v.empty()) {
+                        rc = set_err(plan, REXI_ERR_SINGULAR, v + " [shift j = " + std::to_string(plan->gid[j]) + "]");
+                        break;
+                    }
+                }
+            }
+        }
         if (!rc) {
             if (solver == REXI_SOLVER_TRIDIAG) {
                 rc = tri_create(plan, d);
@@ -735,6 +762,7 @@ int rexi_plan_info(const rexi_plan *plan, rexi_info *info) {
     info->prepare_ms = plan->prepare_ms;
     info->min_pivot_ratio = plan->min_pivot_ratio;
     info->persistent = plan->persist_cs;
+    info->screen_pivot_ratio = plan->screen_ratio;
     return REXI_OK;
 }
 

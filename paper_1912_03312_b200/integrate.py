@@ -204,11 +204,14 @@ def _make_plans(stepper_args, pieces, piece_devs):
                     tol=float(tol or 0.0), max_iters=int(max_iters or 0),
                     shift_offset=int(idx[0]), weight_ref=wref, shift_ids=idx))
             except SolverError as exc:
+                # the native message is the reference's factorize() message
+                # (solvers.py:52-69) tagged "[shift j = N]" with the global index
                 m = re.search(r"j = (\d+)", str(exc))
                 j = int(m.group(1)) if m else int(idx[0])
+                inner = re.sub(r"\s*\[shift j = \d+\]$", "", str(exc))
                 raise SolverError(
                     f"shifted system j = {j} (sigma = {shifts[j]}) is singular: the "
-                    f"shift coincides with an eigenvalue of tau*M ({exc})"
+                    f"shift coincides with an eigenvalue of tau*M ({inner})"
                 ) from exc
     except BaseException:
         for p in plans:

@@ -226,7 +226,7 @@ def test_library_exports_all_declared_symbols():
     L = ctypes.CDLL(lib)
     L.rexi_abi_version.restype = ctypes.c_int32
     from paper_1912_03312_b200 import _native
-    assert L.rexi_abi_version() == _native.ABI_VERSION == 2
+    assert L.rexi_abi_version() == _native.ABI_VERSION == 3
     assert set(_declared_functions()) <= set(_native.EXPORTED) | {"rexi_abi_version"}
 
 
