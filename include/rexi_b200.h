@@ -68,9 +68,12 @@ typedef enum rexi_status {
 } rexi_status;
 
 typedef enum rexi_solver {
-    REXI_SOLVER_AUTO = 0,      /* tridiagonal pattern -> TRIDIAG, else COCG      */
+    REXI_SOLVER_AUTO = 0,      /* tridiagonal -> TRIDIAG, half band 2..4 -> BAND,
+                                  else COCG                                      */
     REXI_SOLVER_TRIDIAG = 1,   /* batched partitioned direct solve (1D P1)       */
-    REXI_SOLVER_COCG = 2       /* lockstep Jacobi-COCG over shifts (2D/3D, any)  */
+    REXI_SOLVER_COCG = 2,      /* lockstep Jacobi-COCG over shifts (2D/3D, any)  */
+    REXI_SOLVER_BAND = 3       /* partitioned band LU, half bandwidth 2..4 (the
+                                  reference's P2 1D pencils, bandwidth 5)        */
 } rexi_solver;
 
 typedef enum rexi_mem { REXI_MEM_HOST = 0, REXI_MEM_DEVICE = 1 } rexi_mem;

@@ -25,7 +25,7 @@ REXI_ERR_CUDA = 5
 REXI_ERR_NOMEM = 6
 REXI_ERR_UNSUPPORTED = 7
 
-SOLVER_AUTO, SOLVER_TRIDIAG, SOLVER_COCG = 0, 1, 2
+SOLVER_AUTO, SOLVER_TRIDIAG, SOLVER_COCG, SOLVER_BAND = 0, 1, 2, 3
 MEM_HOST, MEM_DEVICE = 0, 1
 ABI_VERSION = 3
 

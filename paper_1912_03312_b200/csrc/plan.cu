@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/rexi_b200.h"
+#include "band.cuh"
 #include "cocg.cuh"
 #include "screen.cuh"
 #include "tridiag_launch.h"
@@ -61,6 +62,7 @@ struct rexi_plan {
     c128 *ubuf[2] = {nullptr, nullptr};
     TriState tri;
     CocgState cg;
+    BandState band;
     double prepare_ms = 0.0;
     double min_pivot_ratio = 1.0;
     double screen_ratio = 1.0;    // min over shifts of min|U_ii| / max|U_ii| (pivoted band LU)
@@ -523,6 +525,8 @@ void fill_phases(rexi_plan *plan, cudaEvent_t ev[4], rexi_stats *stats) {
 
 int plan_step_device(rexi_plan *plan, const c128 *u, c128 *uout) {
     if (plan->solver == REXI_SOLVER_TRIDIAG) return tri_step(plan, u, uout);
+    if (plan->solver == REXI_SOLVER_BAND)
+        return band_step(plan->band, plan->S, plan->stream, u, uout, plan->tri.acc, &plan->launches, plan->err);
     return cocg_step(plan->cg, plan->S, plan->stream, u, uout, plan->tri.acc, &plan->launches,
                      plan->err);
 }
@@ -556,6 +560,7 @@ int rexi_plan_destroy(rexi_plan *plan) {
     if (plan->stream) cudaStreamSynchronize(plan->stream);
     for (void *p : plan->allocs) cudaFree(p);
     cocg_destroy(plan->cg);
+    band_destroy(plan->band);
     for (auto &r : plan->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto &g : plan->graph)
         if (g) cudaGraphExecDestroy(g);
@@ -605,7 +610,16 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
     tri = kl <= 1 && ku <= 1;
     plan->bandwidth = kl + ku + 1;
     int solver = d->solver;
-    if (solver == REXI_SOLVER_AUTO) solver = tri ? REXI_SOLVER_TRIDIAG : REXI_SOLVER_COCG;
+    const int hb = std::max(kl, ku);
+    const bool banded = hb >= BAND_MIN && hb <= BAND_MAX;
+    // tridiagonal -> the partitioned 1D solver; half bandwidth 2..4 (the
+    // reference's P2 pencils) -> the partitioned band LU; wider -> COCG
+    if (solver == REXI_SOLVER_AUTO) solver = tri ? REXI_SOLVER_TRIDIAG : banded ? REXI_SOLVER_BAND : REXI_SOLVER_COCG;
+    if (solver == REXI_SOLVER_BAND && !banded) {
+        int rc = set_err(plan, REXI_ERR_UNSUPPORTED, "BAND solver needs a half bandwidth of 2..4");
+        rexi_plan_destroy(plan);
+        return rc;
+    }
     if (solver == REXI_SOLVER_TRIDIAG && !tri) {
         int rc = set_err(plan, REXI_ERR_UNSUPPORTED, "TRIDIAG solver needs a tridiagonal pattern");
         rexi_plan_destroy(plan);
@@ -623,8 +637,9 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
     }
     // auto (-1): the direct 1D solve is refined only on request (the Python layer
     // decides by stiffness); COCG always gets one double-double refinement round
-    if (d->refine < 0) plan->refine = solver == REXI_SOLVER_TRIDIAG ? 0 : 1;
-    else plan->refine = std::min(d->refine, solver == REXI_SOLVER_TRIDIAG ? 1 : 4);
+    const bool direct = solver == REXI_SOLVER_TRIDIAG || solver == REXI_SOLVER_BAND;
+    if (d->refine < 0) plan->refine = direct ? 0 : 1;
+    else plan->refine = std::min(d->refine, direct ? 1 : 4);
 
     cudaError_t e = cudaSetDevice(d->device);
     if (e != cudaSuccess) {
@@ -692,6 +707,12 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
             if (solver == REXI_SOLVER_TRIDIAG) {
                 rc = tri_create(plan, d);
                 if (!rc) rc = persist_setup(plan);
+            } else if (solver == REXI_SOLVER_BAND) {
+                rc = dalloc(plan, &plan->tri.acc, (size_t)4 * d->n);
+                if (!rc) rc = band_create(plan->band, d, std::max(hb, BAND_MIN), plan->S, plan->kp, plan->refine,
+                                          plan->stream, plan->err);
+                if (rc) set_err(plan, rc, plan->err);
+                else plan->min_pivot_ratio = plan->band.min_pivot_ratio;
             } else {
                 rc = dalloc(plan, &plan->tri.acc, (size_t)4 * d->n);
                 if (!rc) rc = cocg_create(plan->cg, d, plan->S, plan->refine, plan->stream, plan->err);
@@ -733,6 +754,7 @@ int rexi_plan_profile(rexi_plan *plan, int32_t enable) {
     plan->prof_acc.clear();
     plan->hook.p = plan;
     plan->cg.hook = &plan->hook;
+    plan->band.hook = plan->prof ? &plan->hook : nullptr;
     return REXI_OK;
 }
 
@@ -758,7 +780,7 @@ int rexi_plan_info(const rexi_plan *plan, rexi_info *info) {
     info->k_pad = plan->kp;
     info->levels = (int32_t)plan->tri.lv.size();
     info->refine = plan->refine;
-    info->device_bytes = plan->bytes + plan->cg.bytes;
+    info->device_bytes = plan->bytes + plan->cg.bytes + plan->band.bytes;
     info->prepare_ms = plan->prepare_ms;
     info->min_pivot_ratio = plan->min_pivot_ratio;
     info->persistent = plan->persist_cs;
@@ -847,8 +869,9 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
         plan->launches += 1;
         src = plan->pbuf[(n_steps - 1) & 1];
         n_steps = -n_steps;    // steps done; restored below
-    } else if (n_steps > 0 && plan->solver == REXI_SOLVER_TRIDIAG && !plan->prof) {
-        // the 1D step is a fixed kernel sequence: replay it as a CUDA graph
+    } else if (n_steps > 0 && (plan->solver == REXI_SOLVER_TRIDIAG || plan->solver == REXI_SOLVER_BAND) &&
+               !plan->prof) {
+        // a direct step is a fixed kernel sequence: replay it as a CUDA graph
         // (two graphs, ping-ponging between the plan's state buffers)
         if (src != plan->ubuf[0] && src != plan->ubuf[1] && !zc_in) {
             CK(cudaMemcpyAsync(plan->ubuf[0], src, sizeof(c128) * n, cudaMemcpyDeviceToDevice, st));
@@ -859,7 +882,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
             cudaGraph_t graph = nullptr;
             const int64_t l0 = plan->launches;
             CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-            int rc = tri_step(plan, plan->ubuf[g], plan->ubuf[g ^ 1]);
+            int rc = plan_step_device(plan, plan->ubuf[g], plan->ubuf[g ^ 1]);
             cudaError_t ce = cudaStreamEndCapture(st, &graph);
             if (rc) return rc;
             if (ce != cudaSuccess) return cuda_err(plan, ce, "cudaStreamEndCapture");
@@ -1124,6 +1147,14 @@ int rexi_plan_solve(rexi_plan *plan, const rexi_c128 *rhs, rexi_c128 *x, int32_t
             CK(cudaFreeAsync(x0, st));
         }
         CK(tri_launch_transpose(T.lv[0].X, n, plan->kp, plan->k, xd, st));
+    } else if (plan->solver == REXI_SOLVER_BAND) {
+        c128 *rd = (c128 *)rhs;
+        if (mem == REXI_MEM_HOST) {
+            CK(cudaMemcpyAsync(plan->ubuf[0], rhs, sizeof(c128) * n, cudaMemcpyHostToDevice, st));
+            rd = plan->ubuf[0];
+        }
+        int rc = band_solve_all(plan->band, plan->S, st, rd, xd, plan->err);
+        if (rc) return set_err(plan, rc, plan->err);
     } else {
         int rc = cocg_solve_all(plan->cg, plan->S, st, (const c128 *)rhs, mem == REXI_MEM_HOST, xd, plan->err);
         if (rc) return set_err(plan, rc, plan->err);

@@ -168,7 +168,7 @@ class RexiStepper:
 
 
 _SOLVERS = {"auto": _native.SOLVER_AUTO, "tridiag": _native.SOLVER_TRIDIAG,
-            "cocg": _native.SOLVER_COCG}
+            "cocg": _native.SOLVER_COCG, "band": _native.SOLVER_BAND}
 # below this many row-shifts (n*K) the default keeps one GPU: a config-1-sized
 # step (~1 MB of work) is launch-latency bound and a cross-GPU combine would
 # cost more than the solves
@@ -222,14 +222,17 @@ def _make_plans(stepper_args, pieces, piece_devs):
 
 def default_refine(indptr, indices, tau: float, sr_value: float, solver: str = "auto") -> int:
     """The refinement rounds ``rexi_prepare`` uses when ``refine`` is not
-    given: the direct 1D solver refines once on stiff pencils (tau*sr above
-    AUTO_REFINE_STIFFNESS, where the fp64 solve alone drifts past 1e-8 of
-    truth), COCG always refines once (double-double residual round)."""
+    given: the direct solvers (1D tridiagonal, and the band LU for half
+    bandwidths 2..4, the reference's P2 pencils) refine once on stiff pencils
+    (tau*sr above AUTO_REFINE_STIFFNESS, where the fp64 solve alone drifts
+    past 1e-8 of truth), COCG always refines once (double-double residual
+    round)."""
     indptr = np.asarray(indptr)
     indices = np.asarray(indices)
     rows = np.repeat(np.arange(len(indptr) - 1), np.diff(indptr))
-    tridiagonal = len(indices) == 0 or int(np.max(np.abs(indices - rows))) <= 1
-    if tridiagonal and solver != "cocg":
+    half_band = 0 if len(indices) == 0 else int(np.max(np.abs(indices - rows)))
+    direct = half_band <= 1 or (2 <= half_band <= 4 and solver != "tridiag")
+    if direct and solver != "cocg":
         return 1 if tau * float(sr_value) > AUTO_REFINE_STIFFNESS else 0
     return 1
 
@@ -264,7 +267,7 @@ def rexi_prepare(
 
     Extra keyword-only knobs (all optional): ``refine`` (double-double
     residual-refinement rounds; default by stiffness), ``solver`` ("auto" |
-    "tridiag" | "cocg"), ``tol`` and ``max_iters`` for COCG.
+    "tridiag" | "band" | "cocg"), ``tol`` and ``max_iters`` for COCG.
     """
     if not tau > 0:
         raise ValueError(f"tau must be positive, got {tau}")
@@ -310,7 +313,7 @@ def rexi_prepare(
         pieces=pieces,
         device=devs[0],
         refine=int(info.refine),
-        solver={1: "tridiag", 2: "cocg"}.get(int(info.solver), "auto"),
+        solver={1: "tridiag", 2: "cocg", 3: "band"}.get(int(info.solver), "auto"),
         stats={"bandwidth": band if band <= 32 else None,
                "levels": int(info.levels), "k_pad": int(info.k_pad),
                "devices": sorted(set(piece_devs)),
