@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -58,6 +59,7 @@ struct BandImpl {
     c128 *rhs = nullptr;           // shared rhs [npad]
     c128 *X1 = nullptr, *X2 = nullptr, *res = nullptr;   // [npad][kp]
     double *pstat = nullptr;       // [2*kp] pivot |.| min / max per lane (prepare)
+    bool staged = false;           // shared-memory staged step kernels (M = 64, small P)
 };
 
 template <int B>
@@ -77,18 +79,36 @@ __device__ __forceinline__ c128 crecip_c(c128 b) {
     return cmk(r / den, -1.0 / den);
 }
 
+// factor access: the interior factors in HBM ([row][coef][kp], read-only
+// path) or staged in shared memory ([row][2B+1][lg], lo | up | dinv)
+template <int B>
+struct GlobalF {
+    const c128 *__restrict__ lo;
+    const c128 *__restrict__ up;
+    const c128 *__restrict__ dinv;
+    int kp, lane;
+    __device__ __forceinline__ c128 l(int64_t r, int q) const { return __ldg(lo + ((size_t)r * B + q) * kp + lane); }
+    __device__ __forceinline__ c128 u(int64_t r, int q) const { return __ldg(up + ((size_t)r * B + q) * kp + lane); }
+    __device__ __forceinline__ c128 d(int64_t r) const { return __ldg(dinv + (size_t)r * kp + lane); }
+};
+template <int B>
+struct SmemF {
+    const c128 *f;
+    int64_t r0;
+    int lg, ll;
+    __device__ __forceinline__ c128 l(int64_t r, int q) const { return f[((r - r0) * (2 * B + 1) + q) * lg + ll]; }
+    __device__ __forceinline__ c128 u(int64_t r, int q) const {
+        return f[((r - r0) * (2 * B + 1) + B + q) * lg + ll];
+    }
+    __device__ __forceinline__ c128 d(int64_t r) const { return f[((r - r0) * (2 * B + 1) + 2 * B) * lg + ll]; }
+};
+
 // interior solve of rows [r0, r1) for one lane: forward with the unit lower
-// factor (y' into the scratch Yt), backward with the upper factor (y handed
-// to out(r, y)).  The factors are read through the read-only path and the
-// scratch is written and read at disjoint rows of distinct arrays, so the
-// loads of the next rows are issued ahead of the dependent chain.
-template <int B, typename Rhs, typename Out>
-__device__ __forceinline__ void interior_solve(const BandDev &D, c128 *__restrict__ Yt, int64_t r0, int64_t r1,
-                                               int lane, Rhs rhs, Out out) {
-    const int kp = D.kp;
-    const c128 *__restrict__ lo = D.lo;
-    const c128 *__restrict__ up = D.up;
-    const c128 *__restrict__ dinv = D.dinv;
+// factor (y' into the scratch Yt(r)), backward with the upper factor (y handed
+// to out(r, y)).  The loads of the next rows are independent of the dependent
+// chain and go out ahead of it.
+template <int B, typename F, typename Yt, typename Rhs, typename Out>
+__device__ __forceinline__ void interior_solve_f(const F &f, Yt yt, int64_t r0, int64_t r1, Rhs rhs, Out out) {
     c128 w[B];
 #pragma unroll
     for (int q = 0; q < B; ++q) w[q] = cmk(0.0, 0.0);
@@ -96,25 +116,33 @@ __device__ __forceinline__ void interior_solve(const BandDev &D, c128 *__restric
     for (int64_t r = r0; r < r1; ++r) {
         c128 v = rhs(r);
 #pragma unroll
-        for (int q = 0; q < B; ++q) v = cfnma(v, __ldg(lo + ((size_t)r * B + q) * kp + lane), w[q]);
+        for (int q = 0; q < B; ++q) v = cfnma(v, f.l(r, q), w[q]);
 #pragma unroll
         for (int q = B - 1; q > 0; --q) w[q] = w[q - 1];
         w[0] = v;
-        Yt[(size_t)r * kp + lane] = v;
+        yt(r) = v;
     }
 #pragma unroll
     for (int q = 0; q < B; ++q) w[q] = cmk(0.0, 0.0);
 #pragma unroll 4
     for (int64_t r = r1 - 1; r >= r0; --r) {
-        c128 v = Yt[(size_t)r * kp + lane];
+        c128 v = yt(r);
 #pragma unroll
-        for (int q = 0; q < B; ++q) v = cfnma(v, __ldg(up + ((size_t)r * B + q) * kp + lane), w[q]);
-        v = cmul(__ldg(dinv + (size_t)r * kp + lane), v);
+        for (int q = 0; q < B; ++q) v = cfnma(v, f.u(r, q), w[q]);
+        v = cmul(f.d(r), v);
 #pragma unroll
         for (int q = B - 1; q > 0; --q) w[q] = w[q - 1];
         w[0] = v;
         out(r, v);
     }
+}
+
+template <int B, typename Rhs, typename Out>
+__device__ __forceinline__ void interior_solve(const BandDev &D, c128 *__restrict__ Yt, int64_t r0, int64_t r1,
+                                               int lane, Rhs rhs, Out out) {
+    const GlobalF<B> f{D.lo, D.up, D.dinv, D.kp, lane};
+    const int kp = D.kp;
+    interior_solve_f<B>(f, [&](int64_t r) -> c128 & { return Yt[(size_t)r * kp + lane]; }, r0, r1, rhs, out);
 }
 
 __device__ __forceinline__ bool thread_block_lane(const BandDev &D, int &p, int &lane) {
@@ -597,6 +625,228 @@ __global__ void k_band_accum(int64_t n, int kp, int k, const c128 *__restrict__ 
     }
 }
 
+// ---- shared-memory staged step kernels (P small: the reference's P2 sizes) --
+// One CTA per (block, group of BLG lanes): all threads copy the block's factor
+// rows and rhs into shared memory (independent coalesced loads, ~one memory
+// latency), then one thread per lane runs the dependent sweeps out of shared
+// memory instead of paying an HBM/L2 round trip every few rows.
+constexpr int BLG = 16;
+constexpr int BST_NT = 256;
+
+template <int B>
+__host__ __device__ inline size_t band_st_smem(int M, int lg) {
+    return (size_t)M * lg * sizeof(c128) * (2 * B + 3);   // factors + rhs + sweep scratch
+}
+
+template <int B>
+__device__ __forceinline__ void band_stage(const BandDev &D, const c128 *rsh, const c128 *rps, int64_t r0,
+                                           int64_t r1, int lane0, int lg, c128 *f, c128 *rb) {
+    const int m = (int)(r1 - r0);
+    const int kp = D.kp;
+    const int nf = m * (2 * B + 1) * lg;
+    for (int idx = threadIdx.x; idx < nf; idx += blockDim.x) {
+        const int l = idx % lg, cr = idx / lg;
+        const int co = cr % (2 * B + 1), rr = cr / (2 * B + 1);
+        const int64_t r = r0 + rr;
+        const int lane = lane0 + l;
+        c128 v;
+        if (co < B) v = __ldg(D.lo + ((size_t)r * B + co) * kp + lane);
+        else if (co < 2 * B) v = __ldg(D.up + ((size_t)r * B + co - B) * kp + lane);
+        else v = __ldg(D.dinv + (size_t)r * kp + lane);
+        f[idx] = v;
+    }
+    if (rsh) {
+        for (int idx = threadIdx.x; idx < m; idx += blockDim.x) rb[idx] = __ldg(rsh + r0 + idx);
+    } else {
+        for (int idx = threadIdx.x; idx < m * lg; idx += blockDim.x)
+            rb[idx] = __ldg(rps + (size_t)(r0 + idx / lg) * kp + lane0 + idx % lg);
+    }
+    __syncthreads();
+}
+
+template <int B>
+__global__ void __launch_bounds__(BST_NT) k_band_s1_st(BandDev D, ShiftDev S, const c128 *__restrict__ rsh,
+                                                       const c128 *__restrict__ rps) {
+    extern __shared__ __align__(16) unsigned char bsm[];
+    const int p = blockIdx.x, lane0 = blockIdx.y * BLG;
+    const int kp = D.kp, M = D.M;
+    const int lg = min(BLG, kp - lane0);
+    const int64_t r0 = blk_i0(p, M, B), r1 = (int64_t)(p + 1) * M;
+    const int m = (int)(r1 - r0);
+    c128 *f = reinterpret_cast<c128 *>(bsm);
+    c128 *rb = f + (size_t)M * (2 * B + 1) * lg;
+    c128 *yt = rb + (size_t)M * lg;
+    band_stage<B>(D, rsh, rps, r0, r1, lane0, lg, f, rb);
+    const int ll = threadIdx.x;
+    if (ll >= lg) return;
+    const int lane = lane0 + ll;
+    const c128 sg = S.sigma[lane];
+    const SmemF<B> fa{f, r0, lg, ll};
+    c128 yf[B], yl[B];
+    interior_solve_f<B>(
+        fa, [&](int64_t r) -> c128 & { return yt[(size_t)(r - r0) * lg + ll]; }, r0, r1,
+        [&](int64_t r) { return rsh ? rb[r - r0] : rb[(size_t)(r - r0) * lg + ll]; },
+        [&](int64_t r, c128 y) {
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                if (r == r0 + i) yf[i] = y;
+                if (r == r1 - B + i) yl[i] = y;
+            }
+        });
+    (void)m;
+    c128 *gc = D.gcon + (size_t)p * 2 * B * kp;
+    if (p >= 1) {
+        c128 gg[B][B], gp[B][B], gcur[B][B];
+        couplings<B>(D, p, sg, gg, gp, gcur);
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            c128 s = cmk(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < B; ++j) s = cadd(s, cmul(gcur[i][j], yf[j]));
+            gc[(size_t)i * kp + lane] = s;
+        }
+    }
+    if (p + 1 < D.P) {
+        c128 gg[B][B], gp[B][B], gcur[B][B];
+        couplings<B>(D, p + 1, sg, gg, gp, gcur);
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            c128 s = cmk(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < B; ++j) s = cadd(s, cmul(gp[i][j], yl[j]));
+            gc[(size_t)(B + i) * kp + lane] = s;
+        }
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(BST_NT) k_band_s3_st(BandDev D, ShiftDev S, const c128 *__restrict__ rsh,
+                                                       const c128 *__restrict__ rps, c128 *Xout) {
+    extern __shared__ __align__(16) unsigned char bsm[];
+    const int p = blockIdx.x, lane0 = blockIdx.y * BLG;
+    const int kp = D.kp, M = D.M;
+    const int lg = min(BLG, kp - lane0);
+    const int64_t r0 = blk_i0(p, M, B), r1 = (int64_t)(p + 1) * M;
+    c128 *f = reinterpret_cast<c128 *>(bsm);
+    c128 *rb = f + (size_t)M * (2 * B + 1) * lg;
+    c128 *yt = rb + (size_t)M * lg;
+    band_stage<B>(D, rsh, rps, r0, r1, lane0, lg, f, rb);
+    const int ll = threadIdx.x;
+    if (ll >= lg) return;
+    const int lane = lane0 + ll;
+    const c128 sg = S.sigma[lane];
+    c128 xa[B], xb[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+        xa[i] = p >= 1 ? D.xg[((size_t)p * B + i) * kp + lane] : cmk(0.0, 0.0);
+        xb[i] = p + 1 < D.P ? D.xg[((size_t)(p + 1) * B + i) * kp + lane] : cmk(0.0, 0.0);
+    }
+    const int64_t ga = (int64_t)p * M, gb = (int64_t)(p + 1) * M;
+    const SmemF<B> fa{f, r0, lg, ll};
+    interior_solve_f<B>(
+        fa, [&](int64_t r) -> c128 & { return yt[(size_t)(r - r0) * lg + ll]; }, r0, r1,
+        [&](int64_t r) {
+            c128 v = rsh ? rb[r - r0] : rb[(size_t)(r - r0) * lg + ll];
+            if (p >= 1 && r < r0 + B) {
+#pragma unroll
+                for (int i = 0; i < B; ++i) {
+                    const int64_t dd = ga + i - r;
+                    if (dd >= -B) v = cfnma(v, ent<B>(D, r, (int)dd, sg), xa[i]);
+                }
+            }
+            if (p + 1 < D.P && r >= r1 - B) {
+#pragma unroll
+                for (int i = 0; i < B; ++i) {
+                    const int64_t dd = gb + i - r;
+                    if (dd <= B) v = cfnma(v, ent<B>(D, r, (int)dd, sg), xb[i]);
+                }
+            }
+            return v;
+        },
+        [&](int64_t r, c128 y) { Xout[(size_t)r * kp + lane] = y; });
+    if (p >= 1)
+#pragma unroll
+        for (int i = 0; i < B; ++i) Xout[(size_t)(ga + i) * kp + lane] = xa[i];
+}
+
+// interface system with one CTA per shift: the CTA stages the shift's block
+// LU pieces and reduced-rhs pieces in shared memory, thread 0 runs the chain
+template <int B>
+__host__ __device__ inline size_t band_red_smem(int P) {
+    return (size_t)(P > 1 ? P : 1) * (3 * B * B + 3 * B) * sizeof(c128);
+}
+
+template <int B>
+__global__ void __launch_bounds__(64) k_band_red_st(BandDev D, const c128 *__restrict__ rsh,
+                                                    const c128 *__restrict__ rps) {
+    extern __shared__ __align__(16) unsigned char bsm[];
+    const int lane = blockIdx.x;
+    const int kp = D.kp, M = D.M, P = D.P;
+    constexpr int W = 3 * B * B + 3 * B;   // per block: L, Dinv, U, g_in (rhs - gprev - gcur)
+    c128 *sm = reinterpret_cast<c128 *>(bsm);
+    for (int idx = threadIdx.x; idx < (P - 1) * W; idx += blockDim.x) {
+        const int p = 1 + idx / W, e = idx % W;
+        c128 v;
+        if (e < B * B) v = __ldg(D.rl + ((size_t)p * B * B + e) * kp + lane);
+        else if (e < 2 * B * B) v = __ldg(D.rdi + ((size_t)p * B * B + e - B * B) * kp + lane);
+        else if (e < 3 * B * B) v = __ldg(D.ru + ((size_t)p * B * B + e - 2 * B * B) * kp + lane);
+        else {
+            const int i = (e - 3 * B * B) % B, which = (e - 3 * B * B) / B;
+            if (which == 0) v = rhs_at<B>(D, rsh, rps, (int64_t)p * M + i, lane);
+            else if (which == 1) v = __ldg(D.gcon + ((size_t)(p - 1) * 2 * B + B + i) * kp + lane);
+            else v = __ldg(D.gcon + ((size_t)p * 2 * B + i) * kp + lane);
+        }
+        sm[idx] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    c128 h[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) h[i] = cmk(0.0, 0.0);
+    for (int p = 1; p < P; ++p) {
+        const c128 *b = sm + (size_t)(p - 1) * W;
+        c128 g[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) g[i] = csub(csub(b[3 * B * B + i], b[3 * B * B + B + i]), b[3 * B * B + 2 * B + i]);
+        if (p >= 2) {
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+                for (int j = 0; j < B; ++j) g[i] = cfnma(g[i], b[i * B + j], h[j]);
+        }
+        c128 *hs = const_cast<c128 *>(b) + 3 * B * B;    // keep h_p where g_in was
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            h[i] = g[i];
+            hs[i] = g[i];
+        }
+    }
+    c128 x[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) x[i] = cmk(0.0, 0.0);
+    for (int p = P - 1; p >= 1; --p) {
+        const c128 *b = sm + (size_t)(p - 1) * W;
+        c128 v[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) v[i] = b[3 * B * B + i];
+        if (p + 1 < P) {
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], b[2 * B * B + i * B + j], x[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            c128 t = cmk(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < B; ++j) t = cadd(t, cmul(b[B * B + i * B + j], v[j]));
+            x[i] = t;
+        }
+#pragma unroll
+        for (int i = 0; i < B; ++i) D.xg[((size_t)p * B + i) * kp + lane] = x[i];
+    }
+}
+
 int launch_nt(int kp) { return std::max(128, kp); }
 int launch_grid(const BandDev &D) {
     const int per = launch_nt(D.kp) / D.kp;
@@ -609,14 +859,19 @@ cudaError_t solve_chain(BandImpl *im, const ShiftDev &S, cudaStream_t st, const 
     BandDev &D = im->D;
     const int nt = launch_nt(D.kp), grid = launch_grid(D);
     const double lane_rows = (double)D.npad * kreal;
+    const dim3 sgrid(D.P, (D.kp + BLG - 1) / BLG);
+    const size_t ssm = band_st_smem<B>(D.M, std::min(BLG, D.kp)), rsm = band_red_smem<B>(D.P);
     if (hook) hook->begin("band_s1", 16.0 * lane_rows * ((2 * B + 1) + 2) + (rps ? 16.0 * lane_rows : 16.0 * D.npad));
-    k_band_s1<B><<<grid, nt, 0, st>>>(D, S, rsh, rps);
+    if (im->staged) k_band_s1_st<B><<<sgrid, BST_NT, ssm, st>>>(D, S, rsh, rps);
+    else k_band_s1<B><<<grid, nt, 0, st>>>(D, S, rsh, rps);
     if (hook) hook->end();
     if (hook) hook->begin("band_red", 0.0);
-    k_band_red<B><<<(D.kp + 31) / 32, 32, 0, st>>>(D, rsh, rps);
+    if (im->staged && D.P > 1) k_band_red_st<B><<<D.kp, 64, rsm, st>>>(D, rsh, rps);
+    else k_band_red<B><<<(D.kp + 31) / 32, 32, 0, st>>>(D, rsh, rps);
     if (hook) hook->end();
     if (hook) hook->begin("band_s3", 16.0 * lane_rows * ((2 * B + 1) + 2) + (rps ? 16.0 * lane_rows : 16.0 * D.npad));
-    k_band_s3<B><<<grid, nt, 0, st>>>(D, S, rsh, rps, Xout);
+    if (im->staged) k_band_s3_st<B><<<sgrid, BST_NT, ssm, st>>>(D, S, rsh, rps, Xout);
+    else k_band_s3<B><<<grid, nt, 0, st>>>(D, S, rsh, rps, Xout);
     if (hook) hook->end();
     *launches += 3;
     return cudaGetLastError();
@@ -660,6 +915,15 @@ static int band_create_t(BandState &bs, BandImpl *im, const rexi_desc *d, const 
     int M = 16;
     while ((double)M * M < (double)n && M < 2048) M *= 2;
     M = std::max(M, 4 * B);
+    // the reference's P2 sizes: blocks of 64 rows whose factors fit shared
+    // memory, and an interface chain whose pieces fit one CTA's shared memory
+    constexpr int MST = 64;
+    const int64_t pst = (n + MST - 1) / MST;
+    if (!getenv("REXI_BAND_NOSTAGE") && band_red_smem<B>((int)std::min<int64_t>(pst, 1 << 20)) <= 200 * 1024 &&
+        band_st_smem<B>(MST, std::min(BLG, kp)) <= 200 * 1024) {
+        M = MST;
+        im->staged = true;
+    }
     const int P = (int)((n + M - 1) / M);
     const int64_t npad = (int64_t)P * M;
     bs.B = B;
@@ -718,6 +982,14 @@ static int band_create_t(BandState &bs, BandImpl *im, const rexi_desc *d, const 
         std::vector<double> init(2 * kp, 0.0);
         for (int l = 0; l < kp; ++l) init[l] = INFINITY;
         BK(cudaMemcpyAsync(im->pstat, init.data(), sizeof(double) * 2 * kp, cudaMemcpyHostToDevice, st));
+    }
+    if (im->staged) {
+        BK(cudaFuncSetAttribute(k_band_s1_st<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)band_st_smem<B>(M, std::min(BLG, kp))));
+        BK(cudaFuncSetAttribute(k_band_s3_st<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)band_st_smem<B>(M, std::min(BLG, kp))));
+        BK(cudaFuncSetAttribute(k_band_red_st<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)band_red_smem<B>(P)));
     }
     k_band_factor<B><<<launch_grid(D), launch_nt(kp), 0, st>>>(D, S, im->pstat);
     BK(cudaGetLastError());
