@@ -116,7 +116,11 @@ typedef struct rexi_stats {
      * local  = the shifted solves (and whatever is fused into them: the 1D
      *          level-0 kernels also form iB u and the beta-weighted sum),
      * reduce = the beta-weighted accumulation where it is a kernel of its own
-     *          (COCG) + copying u1 back to the host. */
+     *          (COCG) + copying u1 back to the host.
+     * A one-step call of a direct solver (TRIDIAG / BAND) fuses rhs and sum
+     * into its kernels and is not event-timed (four timed events cost ~17 us,
+     * a third of a config-1 step): t_local_ms is the host time of the call,
+     * t_rhs_ms = t_reduce_ms = 0. */
     double t_rhs_ms;
     double t_local_ms;
     double t_reduce_ms;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <map>
 #include <cstdio>
@@ -66,6 +67,7 @@ struct rexi_plan {
     double prepare_ms = 0.0;
     double min_pivot_ratio = 1.0;
     double screen_ratio = 1.0;    // min over shifts of min|U_ii| / max|U_ii| (pivoted band LU)
+    cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // rexi_stats phases, reused per call
     std::vector<rexi_c128> shifts_host;
     int64_t launches = 0;
     // optional per-kernel CUDA-event profiling (rexi_plan_profile)
@@ -514,7 +516,7 @@ void fill_phases(rexi_plan *plan, cudaEvent_t ev[4], rexi_stats *stats) {
     cudaEventElapsedTime(&stage, ev[0], ev[1]);
     cudaEventElapsedTime(&steps, ev[1], ev[2]);
     cudaEventElapsedTime(&out, ev[2], ev[3]);
-    for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+    (void)0;   // the events are the plan's (phase_ev), reused by every call
     cocg_collect_phase(plan->cg);
     const double cr = plan->cg.t_rhs_ms, ca = plan->cg.t_acc_ms;
     plan->cg.t_rhs_ms = plan->cg.t_acc_ms = 0.0;
@@ -561,6 +563,8 @@ int rexi_plan_destroy(rexi_plan *plan) {
     for (void *p : plan->allocs) cudaFree(p);
     cocg_destroy(plan->cg);
     band_destroy(plan->band);
+    for (auto &e : plan->phase_ev)
+        if (e) cudaEventDestroy(e);
     for (auto &r : plan->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto &g : plan->graph)
         if (g) cudaGraphExecDestroy(g);
@@ -819,9 +823,15 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     plan->launches = 0;
     // phase events: [0] before staging u, [1] after it (rhs), [2] after the
     // steps (local), [3] after copying u1 out (reduce)
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (stats) {
-        for (auto &e : ev) CK(cudaEventCreate(&e));
+    // A one-step call of a direct solver fuses the rhs into its first kernel
+    // and the sum into its last: its phases are all "local", timed on the
+    // host (four timed events cost ~17 us per call, a third of a cfg-1 step)
+    const bool phase_ev = stats && !(n_steps <= 1 && plan->solver != REXI_SOLVER_COCG);
+    const auto host_t0 = std::chrono::steady_clock::now();
+    cudaEvent_t *ev = plan->phase_ev;
+    if (phase_ev) {
+        for (int i = 0; i < 4; ++i)
+            if (!ev[i]) CK(cudaEventCreate(&ev[i]));
         cocg_collect_phase(plan->cg);
         plan->cg.t_rhs_ms = plan->cg.t_acc_ms = 0.0;
         CK(cudaEventRecord(ev[0], st));
@@ -860,7 +870,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     } else {
         src = (const c128 *)u_in;
     }
-    if (stats) CK(cudaEventRecord(ev[1], st));
+    if (phase_ev) CK(cudaEventRecord(ev[1], st));
     int cur = (src == plan->ubuf[0]) ? 0 : 1;
     if (n_steps > 0 && plan->persist_cs > 0 && !plan->prof) {
         TriState &T = plan->tri;
@@ -936,8 +946,6 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
         if (dst == src) dst = plan->ubuf[cur ^ 1];   // in-place device call
         int rc = plan_step_device(plan, src, dst);
         if (rc) {
-            for (auto e : ev)
-                if (e) cudaEventDestroy(e);
             if (rc == REXI_ERR_NOCONV || rc == REXI_ERR_BREAKDOWN) return set_err(plan, rc, plan->err);
             return rc;
         }
@@ -945,7 +953,7 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
         cur = (src == plan->ubuf[0]) ? 0 : 1;
     }
     if (n_steps < 0) n_steps = -n_steps;
-    if (stats) CK(cudaEventRecord(ev[2], st));
+    if (phase_ev) CK(cudaEventRecord(ev[2], st));
     if (n_steps == 0) {
         if (mem == REXI_MEM_HOST) {
             if (u_out != u_in) memcpy(u_out, u_in, sizeof(c128) * n);
@@ -957,11 +965,17 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     } else if ((const void *)src != (const void *)u_out) {
         CK(cudaMemcpyAsync(u_out, src, sizeof(c128) * n, cudaMemcpyDeviceToDevice, st));
     }
-    if (stats) CK(cudaEventRecord(ev[3], st));
+    if (phase_ev) CK(cudaEventRecord(ev[3], st));
     CK(cudaStreamSynchronize(st));
     prof_flush(plan);
     if (stats) {
-        fill_phases(plan, ev, stats);
+        if (phase_ev) {
+            fill_phases(plan, ev, stats);
+        } else {
+            stats->t_rhs_ms = stats->t_reduce_ms = 0.0;
+            stats->t_local_ms =
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+        }
         stats->steps = n_steps;
         stats->launches = plan->launches;
         stats->iters_max = plan->cg.last_iters_max;
@@ -982,8 +996,9 @@ int rexi_plan_run(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *snaps, int3
     const int64_t n = plan->n;
     cudaStream_t st = plan->stream;
     plan->launches = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    for (auto &e : ev) CK(cudaEventCreate(&e));
+    cudaEvent_t *ev = plan->phase_ev;
+    for (int i = 0; i < 4; ++i)
+        if (!ev[i]) CK(cudaEventCreate(&ev[i]));
     cocg_collect_phase(plan->cg);
     plan->cg.t_rhs_ms = plan->cg.t_acc_ms = 0.0;
     CK(cudaEventRecord(ev[0], st));

@@ -493,7 +493,8 @@ def _run_native(stepper: RexiStepper, u, n_steps: int):
             st = _native.RexiStats()
             t1 = time.perf_counter()
             plan.step_device(u_t.data_ptr(), out.data_ptr(), n_steps, st)
-            _record(stepper, st, time.perf_counter() - t1, staged=t1 - t0)
+            t2 = time.perf_counter()
+            _record(stepper, st, t2 - t1, staged=t1 - t0, finish=time.perf_counter() - t2)
             return out
         return _step_pieces_device(stepper, u_t, n_steps)
     t0 = time.perf_counter()
@@ -502,7 +503,10 @@ def _run_native(stepper: RexiStepper, u, n_steps: int):
         st = _native.RexiStats()
         t1 = time.perf_counter()
         out = stepper.plans[0].step_host(u, n_steps, st)
-        _record(stepper, st, time.perf_counter() - t1, staged=t1 - t0)
+        t2 = time.perf_counter()
+        # a fused direct step reports its device time as local only; the
+        # host-side staging / finishing around it count as rhs / reduce
+        _record(stepper, st, t2 - t1, staged=t1 - t0, finish=time.perf_counter() - t2)
         return out
     import torch
     u_t = torch.from_numpy(u).to(f"cuda:{stepper.plans[0].device}")
