@@ -167,7 +167,7 @@ class ShardedStepper:
 
     def __init__(self, sysm, approx, tau, *, rank: int, world: int, device: int,
                  refine: int = -1, solver: int = _native.SOLVER_AUTO, cost=None, group=None,
-                 stream=None, tol: float = 0.0, max_iters: int = 0):
+                 stream=None, tol: float = 0.0, max_iters: int = 0, exchange: str = "auto"):
         import torch
         self.rank, self.world, self.group = rank, world, group
         self.shifts = np.asarray(approx.shifts, dtype=complex)
@@ -185,6 +185,19 @@ class ShardedStepper:
                           max_iters=max_iters, weight_ref=float(np.mean(np.abs(self.weights))))
         self.plan = None
         self._build(shard_indices(self.k, world, cost))
+        # exchange of the partials: "allgather" = ONE collective per step (all
+        # ranks' (hi, lo) partials, then the rank-order combine of the whole
+        # vector everywhere; (world-1) x 32 B/row per rank), "segmented" = an
+        # all-to-all of row segments + an all-gather of the rounded segments
+        # (48 B/row per rank).  auto: one collective where a step is long
+        # (COCG, >= 0.1 s: the extra bytes cost microseconds), segmented for
+        # the direct solvers (a 1D step is ~0.2-1.6 ms per rank)
+        if exchange not in ("auto", "allgather", "segmented"):
+            raise ValueError(f"unknown exchange {exchange!r}")
+        if exchange == "auto":
+            iterative = self.plan is not None and int(self.plan.info.solver) == _native.SOLVER_COCG
+            exchange = "allgather" if iterative or world == 1 else "segmented"
+        self.exchange = exchange
         self.parts = torch.empty((world, 4, self.n), dtype=torch.float64, device=dev)
         self.mine = torch.zeros((4, self.n), dtype=torch.float64, device=dev)
         # segmented exchange buffers: row segments of seg rows per rank
@@ -231,17 +244,23 @@ class ShardedStepper:
 
     def step(self, u, out):
         """u1 = sum over all shards of beta_j x_j.  Each rank computes its
-        shard's double-double partial; an all-to-all hands rank r the row
-        segment r of every partial; rank r combines it in rank order (the
-        same per-row double-double operations as combining everything
-        everywhere) and rounds; an all-gather assembles u1.  Per rank and step
-        that moves 48 B/row instead of (world-1) x 32 B/row."""
+        shard's double-double partial.  exchange "allgather": one all-gather
+        of the partials and the rank-order combine on every rank (one
+        collective per step).  exchange "segmented": an all-to-all hands rank
+        r the row segment r of every partial; rank r combines it in rank order
+        (the same per-row double-double operations as combining everything
+        everywhere) and rounds; an all-gather assembles u1 -- 48 B/row per
+        rank instead of (world-1) x 32 B/row.  Both give the same bits."""
         if self.plan is not None:
             self.plan.step_partial(u.data_ptr(), self.mine.data_ptr())
         else:
             self.mine.zero_()
         if self.world == 1:
             _native.combine_partials(self.mine.data_ptr(), 1, self.n, out.data_ptr(), self.stream)
+            return
+        if self.exchange == "allgather":
+            allgather_partials(self.mine, self.world, self.group, out=self.parts)
+            _native.combine_partials(self.parts.data_ptr(), self.world, self.n, out.data_ptr(), self.stream)
             return
         exchange_segments(self.mine, self.send, self.recv, self.world, self.seg, self.group)
         _native.combine_partials(self.recv.data_ptr(), self.world, self.seg, self.useg.data_ptr(),

@@ -18,7 +18,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, q):
+def _worker(rank, world, port, name, q, exchange="auto"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     import torch
@@ -31,7 +31,8 @@ def _worker(rank, world, port, name, q):
     try:
         d, sysm, ap = load_golden(name)
         torch.cuda.set_device(0)
-        sh = ShardedStepper(sysm, ap, float(d["tau"]), rank=rank, world=world, device=0, refine=1)
+        sh = ShardedStepper(sysm, ap, float(d["tau"]), rank=rank, world=world, device=0, refine=1,
+                            exchange=exchange)
         u = torch.from_numpy(d["u0"]).cuda()
         out = torch.empty_like(u)
         sh.step(u, out)
@@ -42,8 +43,12 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["cfg1_k32", "p1_2d_m16"])
-def test_sharded_step_equals_single_plan(name):
+@pytest.mark.parametrize("exchange", ["segmented", "allgather"])
+@pytest.mark.parametrize("name", ["cfg1_k32", "p1_2d_m16", "fem_p2"])
+def test_sharded_step_equals_single_plan(name, exchange):
+    """both exchanges (one all-gather collective, or all-to-all + all-gather of
+    segments) give the single plan's bits, on the direct 1D, COCG and band
+    paths"""
     import torch.multiprocessing as mp
     from conftest import load_golden
     from paper_1912_03312_b200 import rexi_prepare, rexi_step
@@ -56,7 +61,7 @@ def test_sharded_step_equals_single_plan(name):
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     outs = [q.get(timeout=300) for _ in range(world)]
