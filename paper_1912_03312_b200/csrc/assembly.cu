@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/rexi_b200.h"
+#include "common.cuh"
 
 namespace rexi {
 void set_global_error(const std::string &msg);
@@ -147,6 +148,7 @@ extern "C" int rexi_assemble_p1(const rexi_p1_desc *desc, const double *pot_e, i
     const unsigned grid = (unsigned)std::min<int64_t>((n_int + 255) / 256, 65535);
     int *counts = nullptr;
     if (e == cudaSuccess) e = cudaMallocAsync((void **)&counts, sizeof(int) * (n_int + 1), st);
+    if (e == cudaSuccess) e = rexi_poison(counts, sizeof(int) * (n_int + 1), st);
     if (e == cudaSuccess) {
         k_p1_count<<<grid, 256, 0, st>>>(n_int, counts);
         e = cudaGetLastError();

@@ -890,6 +890,7 @@ cudaError_t solve_chain(BandImpl *im, const ShiftDev &S, cudaStream_t st, const 
 
 static int balloc(BandState &bs, void **p, size_t bytes, std::string &err) {
     cudaError_t e = cudaMalloc(p, bytes < 16 ? 16 : bytes);
+    if (e == cudaSuccess) e = rexi_poison(*p, bytes < 16 ? 16 : bytes);
     if (e != cudaSuccess) {
         err = std::string("cudaMalloc failed: ") + cudaGetErrorString(e);
         return e == cudaErrorMemoryAllocation ? REXI_ERR_NOMEM : REXI_ERR_CUDA;

@@ -1028,6 +1028,7 @@ struct CocgImpl {
 
 static int alloc_(CocgState &cg, void **p, size_t bytes, std::string &err) {
     cudaError_t e = cudaMalloc(p, bytes < 16 ? 16 : bytes);
+    if (e == cudaSuccess) e = rexi_poison(*p, bytes < 16 ? 16 : bytes);
     if (e != cudaSuccess) {
         err = std::string("cudaMalloc failed: ") + cudaGetErrorString(e);
         return e == cudaErrorMemoryAllocation ? REXI_ERR_NOMEM : REXI_ERR_CUDA;
@@ -1370,6 +1371,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
         tr_t0 = t1;
         tr_it0 = it;
     };
+    static const bool batch_all = getenv("REXI_COCG_BATCH") != nullptr;   // A/B switch
     for (;;) {
         for (int s = 0; s < check_every; ++s) {
             hook_begin(cg, width_name("cg_spmv", kp), 80.0 * n * live + nnzb);
@@ -1392,7 +1394,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
                 const int g1 = (int)std::min<int64_t>((g.nchunks + 7) / 8, (int64_t)im->sms * 16);
                 if (im->cplx) k_cg_spmv1<true><<<g1, CG1_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
                 else k_cg_spmv1<false><<<g1, CG1_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
-            } else if (g.kp == 1) {   // one lane: batched gathers (measured faster only here)
+            } else if (g.kp == 1 || batch_all) {   // batched gathers (measured faster only at one lane)
                 if (im->cplx) k_cg_spmv<true, true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
                 else k_cg_spmv<false, true><<<grid, CG_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
             } else {

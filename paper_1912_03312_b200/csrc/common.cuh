@@ -5,6 +5,19 @@
 
 typedef double2 c128;   // (x = re, y = im), layout-compatible with numpy complex128
 
+// REXI_POISON=1 (test hygiene, tests/test_gpu_hygiene.py): every device
+// allocation is filled with 0xFF bytes (NaN doubles, -1 integers) before use,
+// so a kernel that reads memory nothing wrote first changes the results
+// instead of silently reading the zeros a fresh allocation usually holds
+// (the stand-in for compute-sanitizer initcheck, closed on this pool).
+#include <cstdlib>
+inline cudaError_t rexi_poison(void *p, size_t bytes, cudaStream_t st = 0) {
+    static const bool on = std::getenv("REXI_POISON") != nullptr;
+    if (!on || !p || !bytes) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(p, 0xFF, bytes, st);
+    return e == cudaSuccess ? cudaStreamSynchronize(st) : e;
+}
+
 __device__ __forceinline__ c128 cmk(double r, double i) { return make_double2(r, i); }
 __device__ __forceinline__ c128 cadd(c128 a, c128 b) { return cmk(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ c128 csub(c128 a, c128 b) { return cmk(a.x - b.x, a.y - b.y); }

@@ -347,6 +347,7 @@ template <typename T>
 int pn_alloc(rexi_pencil *pn, T **ptr, size_t count) {
     void *d = nullptr;
     cudaError_t e = cudaMalloc(&d, count * sizeof(T) + 16);
+    if (e == cudaSuccess) e = rexi_poison(d, count * sizeof(T) + 16);
     if (e != cudaSuccess) return pn_cuda(pn, e, "cudaMalloc");
     pn->allocs.push_back(d);
     *ptr = reinterpret_cast<T *>(d);

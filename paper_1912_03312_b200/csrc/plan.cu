@@ -192,6 +192,8 @@ int dalloc(rexi_plan *plan, T **ptr, size_t count) {
     size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
     cudaError_t e = cudaMalloc(&v, bytes);
     if (e != cudaSuccess) return cuda_err(plan, e, "cudaMalloc");
+    e = rexi_poison(v, bytes);
+    if (e != cudaSuccess) return cuda_err(plan, e, "poison");
     plan->allocs.push_back(v);
     plan->bytes += (int64_t)bytes;
     *ptr = (T *)v;
@@ -1005,6 +1007,7 @@ int rexi_plan_run(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *snaps, int3
     c128 *dsnap = (c128 *)snaps, *tmp = nullptr;
     if (mem == REXI_MEM_HOST) {
         CK(cudaMallocAsync((void **)&tmp, sizeof(c128) * n * (size_t)n_steps, st));
+        CK(rexi_poison(tmp, sizeof(c128) * n * (size_t)n_steps, st));
         dsnap = tmp;
     }
     const c128 *src = (const c128 *)u_in;

@@ -186,6 +186,10 @@ int band_screen(const rexi_desc *d, int kl, int ku, const c128 *sigma_dev, cudaS
     SCK(cudaMalloc(&dmin, sizeof(double) * k));
     SCK(cudaMalloc(&dmax, sizeof(double) * k));
     SCK(cudaMalloc(&dinfo, sizeof(long long) * k));
+    SCK(rexi_poison(dband, sizeof(double) * band.size()));
+    SCK(rexi_poison(dmin, sizeof(double) * k));
+    SCK(rexi_poison(dmax, sizeof(double) * k));
+    SCK(rexi_poison(dinfo, sizeof(long long) * k));
     SCK(cudaMemcpyAsync(dband, band.data(), sizeof(double) * band.size(), cudaMemcpyHostToDevice, st));
     const int grid = (k + 31) / 32;
     if (kl == 1 && ku == 1)
