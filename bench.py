@@ -55,12 +55,39 @@ def parse():
     return ap.parse_args()
 
 
+def acceptance_config():
+    """--config 6: the reference's own acceptance workload (tests/golden/
+    acceptance_p2.npz, made by tests/golden/make_acceptance.py from the
+    reference: test_acceptance.py:60-65,95-121) -- the 7,999-DOF P2
+    tunneling system (pentadiagonal), the flagship K = 16 poles, dt = 2e-4."""
+    import numpy as np
+    from scipy.sparse import csr_matrix
+    from paper_1912_03312_b200 import fixtures
+    from paper_1912_03312_b200.types import PartialFractionApproximation, SystemMatrices
+    d = np.load(os.path.join(ROOT, "tests", "golden", "acceptance_p2.npz"))
+
+    def csr(p):
+        return csr_matrix((d[p + "_data"], d[p + "_indices"], d[p + "_indptr"]), shape=tuple(d[p + "_shape"]))
+    sysm = SystemMatrices(csr("A"), csr("B"), int(d["A_shape"][0]))
+    ap = PartialFractionApproximation(d["shifts"], d["weights"], float(d["R1"]), 0.0)
+    mesh = fixtures.StructuredMesh(1, 4000, np.array([-120.0]), 240.0 / 4000)
+    return fixtures.Config(name="acceptance_p2 (reference test_acceptance.py workload, P2)", system=sysm,
+                           u0=d["u0"], approx=ap, tau=float(d["tau"]), n_steps=1000, sr=float(d["sr"]),
+                           mesh=mesh)
+
+
+def build_cfg(idx):
+    from paper_1912_03312_b200 import fixtures
+    return acceptance_config() if idx == 6 else fixtures.build_config(idx)
+
+
 def workload_name(cfg):
     """The same string in both arms (the refinement setting is a separate
     config key: it is how an arm computes, not what the workload is)."""
     n, k = cfg.system.n_dof, cfg.approx.K
     dims = {1: "1D", 2: "2D", 3: "3D"}[cfg.mesh.d]
-    return (f"{cfg.name}: {dims} P1 Schroedinger REXI step, {n} DOF, nnz {cfg.system.A.nnz}, "
+    fem = "P2" if cfg.name.startswith("acceptance") else "P1"
+    return (f"{cfg.name}: {dims} {fem} Schroedinger REXI step, {n} DOF, nnz {cfg.system.A.nnz}, "
             f"K={k}, tau={cfg.tau}")
 
 
@@ -255,7 +282,7 @@ def run_reference(args, rank, world):
         return
     from paper_1912_03312_b200 import fixtures
     from oracle.oracle import OraclePlan
-    cfg = fixtures.build_config(args.config)
+    cfg = build_cfg(args.config)
     cores = os.cpu_count() or 1
     refine = api_refine(cfg)
     if cfg.mesh.d > 1:
@@ -398,7 +425,7 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    cfg = fixtures.build_config(args.config)
+    cfg = build_cfg(args.config)
     n, k = cfg.system.n_dof, cfg.approx.K
     sec_cfg = args.secondary if args.secondary >= 0 else (3 if args.config == 2 and world == 1 else 0)
     if world > 1 or sec_cfg == args.config:

@@ -769,23 +769,32 @@ __global__ void __launch_bounds__(BST_NT) k_band_s3_st(BandDev D, ShiftDev S, co
         for (int i = 0; i < B; ++i) Xout[(size_t)(ga + i) * kp + lane] = xa[i];
 }
 
-// interface system with one CTA per shift: the CTA stages the shift's block
-// LU pieces and reduced-rhs pieces in shared memory, thread 0 runs the chain
+// interface system, a CTA per RLG shifts: all threads stage the shifts' block
+// LU pieces and reduced-rhs pieces in shared memory (RLG-lane runs of each
+// (block, coefficient) row are contiguous), then one thread per shift runs the
+// forward / backward chain out of shared memory; h goes to its own array so
+// the next block's loads are not ordered behind this block's stores
+constexpr int RLG = 4;
 template <int B>
 __host__ __device__ inline size_t band_red_smem(int P) {
-    return (size_t)(P > 1 ? P : 1) * (3 * B * B + 3 * B) * sizeof(c128);
+    const size_t np = (size_t)(P > 1 ? P - 1 : 1);
+    return np * RLG * sizeof(c128) * (3 * B * B + 3 * B + B);
 }
 
 template <int B>
-__global__ void __launch_bounds__(64) k_band_red_st(BandDev D, const c128 *__restrict__ rsh,
-                                                    const c128 *__restrict__ rps) {
+__global__ void __launch_bounds__(256) k_band_red_st(BandDev D, const c128 *__restrict__ rsh,
+                                                     const c128 *__restrict__ rps) {
     extern __shared__ __align__(16) unsigned char bsm[];
-    const int lane = blockIdx.x;
+    const int lane0 = blockIdx.x * RLG;
     const int kp = D.kp, M = D.M, P = D.P;
-    constexpr int W = 3 * B * B + 3 * B;   // per block: L, Dinv, U, g_in (rhs - gprev - gcur)
-    c128 *sm = reinterpret_cast<c128 *>(bsm);
-    for (int idx = threadIdx.x; idx < (P - 1) * W; idx += blockDim.x) {
-        const int p = 1 + idx / W, e = idx % W;
+    const int lg = min(RLG, kp - lane0);
+    constexpr int W = 3 * B * B + 3 * B;   // per block: L, Dinv, U, (rhs, gprev, gcur)
+    c128 *sm = reinterpret_cast<c128 *>(bsm);                 // [P-1][W][RLG]
+    c128 *hsm = sm + (size_t)(P - 1) * W * RLG;               // [P-1][B][RLG]
+    for (int idx = threadIdx.x; idx < (P - 1) * W * lg; idx += blockDim.x) {
+        const int l = idx % lg, pe = idx / lg;
+        const int p = 1 + pe / W, e = pe % W;
+        const int lane = lane0 + l;
         c128 v;
         if (e < B * B) v = __ldg(D.rl + ((size_t)p * B * B + e) * kp + lane);
         else if (e < 2 * B * B) v = __ldg(D.rdi + ((size_t)p * B * B + e - B * B) * kp + lane);
@@ -796,50 +805,52 @@ __global__ void __launch_bounds__(64) k_band_red_st(BandDev D, const c128 *__res
             else if (which == 1) v = __ldg(D.gcon + ((size_t)(p - 1) * 2 * B + B + i) * kp + lane);
             else v = __ldg(D.gcon + ((size_t)p * 2 * B + i) * kp + lane);
         }
-        sm[idx] = v;
+        sm[(size_t)pe * RLG + l] = v;
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
+    const int l = threadIdx.x;
+    if (l >= lg) return;
+    const int lane = lane0 + l;
+    const c128 *__restrict__ in = sm;
+    auto at = [&](int p, int e) { return in[((size_t)(p - 1) * W + e) * RLG + l]; };
     c128 h[B];
 #pragma unroll
     for (int i = 0; i < B; ++i) h[i] = cmk(0.0, 0.0);
     for (int p = 1; p < P; ++p) {
-        const c128 *b = sm + (size_t)(p - 1) * W;
         c128 g[B];
 #pragma unroll
-        for (int i = 0; i < B; ++i) g[i] = csub(csub(b[3 * B * B + i], b[3 * B * B + B + i]), b[3 * B * B + 2 * B + i]);
+        for (int i = 0; i < B; ++i)
+            g[i] = csub(csub(at(p, 3 * B * B + i), at(p, 3 * B * B + B + i)), at(p, 3 * B * B + 2 * B + i));
         if (p >= 2) {
 #pragma unroll
             for (int i = 0; i < B; ++i)
 #pragma unroll
-                for (int j = 0; j < B; ++j) g[i] = cfnma(g[i], b[i * B + j], h[j]);
+                for (int j = 0; j < B; ++j) g[i] = cfnma(g[i], at(p, i * B + j), h[j]);
         }
-        c128 *hs = const_cast<c128 *>(b) + 3 * B * B;    // keep h_p where g_in was
 #pragma unroll
         for (int i = 0; i < B; ++i) {
             h[i] = g[i];
-            hs[i] = g[i];
+            hsm[((size_t)(p - 1) * B + i) * RLG + l] = g[i];
         }
     }
     c128 x[B];
 #pragma unroll
     for (int i = 0; i < B; ++i) x[i] = cmk(0.0, 0.0);
     for (int p = P - 1; p >= 1; --p) {
-        const c128 *b = sm + (size_t)(p - 1) * W;
         c128 v[B];
 #pragma unroll
-        for (int i = 0; i < B; ++i) v[i] = b[3 * B * B + i];
+        for (int i = 0; i < B; ++i) v[i] = hsm[((size_t)(p - 1) * B + i) * RLG + l];
         if (p + 1 < P) {
 #pragma unroll
             for (int i = 0; i < B; ++i)
 #pragma unroll
-                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], b[2 * B * B + i * B + j], x[j]);
+                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], at(p, 2 * B * B + i * B + j), x[j]);
         }
 #pragma unroll
         for (int i = 0; i < B; ++i) {
             c128 t = cmk(0.0, 0.0);
 #pragma unroll
-            for (int j = 0; j < B; ++j) t = cadd(t, cmul(b[B * B + i * B + j], v[j]));
+            for (int j = 0; j < B; ++j) t = cadd(t, cmul(at(p, B * B + i * B + j), v[j]));
             x[i] = t;
         }
 #pragma unroll
@@ -866,7 +877,7 @@ cudaError_t solve_chain(BandImpl *im, const ShiftDev &S, cudaStream_t st, const 
     else k_band_s1<B><<<grid, nt, 0, st>>>(D, S, rsh, rps);
     if (hook) hook->end();
     if (hook) hook->begin("band_red", 0.0);
-    if (im->staged && D.P > 1) k_band_red_st<B><<<D.kp, 64, rsm, st>>>(D, rsh, rps);
+    if (im->staged && D.P > 1) k_band_red_st<B><<<(D.kp + RLG - 1) / RLG, 256, rsm, st>>>(D, rsh, rps);
     else k_band_red<B><<<(D.kp + 31) / 32, 32, 0, st>>>(D, rsh, rps);
     if (hook) hook->end();
     if (hook) hook->begin("band_s3", 16.0 * lane_rows * ((2 * B + 1) + 2) + (rps ? 16.0 * lane_rows : 16.0 * D.npad));

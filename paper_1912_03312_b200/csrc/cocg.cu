@@ -419,6 +419,9 @@ __device__ __forceinline__ void st_issue(const StLayout &L, int b, int64_t claim
     }
 }
 
+#ifndef CG_STATIC
+#define CG_STATIC 0   // A/B: static claim striding instead of the atomic claim counter
+#endif
 template <bool CPLX>
 #ifndef CG_ST_MINB
 #define CG_ST_MINB 3   // 80 registers: 3 CTAs/SM (swept: scripts/tune_spmv_minb.sh)
@@ -442,7 +445,7 @@ __global__ void __launch_bounds__(CG_NT, CG_ST_MINB) k_cg_spmv_st(CgMat M, CgVec
         mbar_init(L.bar, 1);
         mbar_init(L.bar + 1, 1);
         fence_mbar_init();
-        const int64_t c0 = (int64_t)atomicAdd(Sc.ctr, 1u);
+        const int64_t c0 = CG_STATIC ? (int64_t)blockIdx.x : (int64_t)atomicAdd(Sc.ctr, 1u);
         claim_q[0] = c0;
         if (c0 < g.nclaims) st_issue<CPLX>(L, 0, c0, M, g);
     }
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(CG_NT, CG_ST_MINB) k_cg_spmv_st(CgMat M, CgVec
         const int64_t claim = claim_q[buf];
         if (claim >= g.nclaims) break;
         if (threadIdx.x == 0) {
-            const int64_t cn = (int64_t)atomicAdd(Sc.ctr, 1u);
+            const int64_t cn = CG_STATIC ? claim + gridDim.x : (int64_t)atomicAdd(Sc.ctr, 1u);
             claim_q[buf ^ 1] = cn;
             if (cn < g.nclaims) st_issue<CPLX>(L, buf ^ 1, cn, M, g);
         }

@@ -7,6 +7,7 @@
 //   WIN    : the claim's z rows (3 windows of 34 rows) copied to shared memory
 //            by all threads first, gathers served from shared memory
 // nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o spmv_probe spmv_probe.cu
+#include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -14,6 +15,22 @@ typedef double2 c128;
 __device__ __forceinline__ c128 cmk(double r, double i) { return make_double2(r, i); }
 __device__ __forceinline__ c128 cadd(c128 a, c128 b) { return cmk(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ c128 cmul(c128 a, c128 b) { return cmk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile("{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT_%=;\n}\n"
+                 ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
 
 constexpr int NS = 1023;
 constexpr int N = NS * NS;
@@ -110,6 +127,131 @@ __global__ void __launch_bounds__(256, 3) k_probe(const double *__restrict__ ta,
     }
 }
 
+// work item = (32-row claim, 32-lane group); 8 warps = the 8 sub-blocks
+// (rows w, w+8, w+16, w+24); the item's 3 z windows (row ranges) are copied to
+// shared memory by bulk copies one item ahead (double buffered, one mbarrier
+// per buffer); p, q own rows are register loads issued before the wait
+constexpr int TW_ROWS = 3 * 34;
+constexpr int LW = 32;
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_tmawin(const double *__restrict__ ta, const double *__restrict__ tb,
+                                                  const c128 *__restrict__ z, c128 *__restrict__ p,
+                                                  c128 *__restrict__ q, c128 beta, c128 sg, int nitems,
+                                                  c128 *part) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm);
+    c128 *win = reinterpret_cast<c128 *>(sm + 128);       // [2][TW_ROWS][LW]
+    __shared__ c128 sbp[8 * LW];
+    constexpr int RPW = NT / 256;                          // warps per sub-block
+    const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int sb = warp / RPW, half = warp % RPW;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int item, int b) {
+        const int claim = item >> 1, g = item & 1;
+        const int R0 = claim * 32;
+        uint32_t bytes = 0;
+        for (int w = 0; w < 3; ++w) {
+            const int base = R0 - 1 + (w - 1) * NS;
+            for (int t = 0; t < 34; ++t) {
+                const int r = base + t;
+                if (r >= 0 && r < N) bytes += LW * 16;
+            }
+        }
+        mbar_expect_tx(bar + b, bytes);
+        for (int w = 0; w < 3; ++w) {
+            const int base = R0 - 1 + (w - 1) * NS;
+            for (int t = 0; t < 34; ++t) {
+                const int r = base + t;
+                if (r >= 0 && r < N)
+                    bulk_g2s(win + ((size_t)b * TW_ROWS + w * 34 + t) * LW, z + (size_t)r * KP + g * LW, LW * 16, bar + b);
+            }
+        }
+    };
+    int item = blockIdx.x;
+    if (threadIdx.x == 0 && item < nitems) issue(item, 0);
+    uint32_t ph[2] = {0, 0};
+    int b = 0;
+    for (; item < nitems; item += gridDim.x, b ^= 1) {
+        const int nxt = item + gridDim.x;
+        if (threadIdx.x == 0 && nxt < nitems) issue(nxt, b ^ 1);
+        const int claim = item >> 1, g = item & 1;
+        const int R0 = claim * 32;
+        const int lane = g * LW + l;
+        // own-row loads before the wait
+        c128 zo[4 / RPW], po[4 / RPW], qo[4 / RPW];
+#pragma unroll
+        for (int k = 0; k < 4 / RPW; ++k) {
+            const int i = R0 + sb + 8 * (k * RPW + half);
+            const size_t o = (size_t)i * KP + lane;
+            po[k] = i < N ? p[o] : cmk(0.0, 0.0);
+            qo[k] = i < N ? q[o] : cmk(0.0, 0.0);
+            zo[k] = i < N ? z[o] : cmk(0.0, 0.0);
+        }
+        mbar_wait(bar + b, ph[b]);
+        ph[b] ^= 1u;
+        const c128 *wb = win + (size_t)b * TW_ROWS * LW;
+        c128 mu = cmk(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < 4 / RPW; ++k) {
+            const int i = R0 + sb + 8 * (k * RPW + half);
+            if (i >= N) break;
+            c128 acc = cmk(0.0, 0.0);
+#pragma unroll
+            for (int e = 0; e < NNZ; ++e) {
+                int c = i + OFF[e];
+                int w = OFF[e] < -1 ? 0 : OFF[e] > 1 ? 2 : 1;
+                if (c < 0 || c >= N) { c = i; w = 1; }
+                const int rr = c - (R0 - 1 + (w - 1) * NS);
+                const c128 zz = wb[(w * 34 + rr) * LW + l];
+                const double a = __ldg(ta + (size_t)i * NNZ + e), bb = __ldg(tb + (size_t)i * NNZ + e);
+                const c128 en = cmk(a + sg.y * bb, -(sg.x * bb));
+                acc = cadd(acc, cmul(en, zz));
+            }
+            const size_t o = (size_t)i * KP + lane;
+            const c128 pi = cadd(zo[k], cmul(beta, po[k]));
+            const c128 qi = cadd(acc, cmul(beta, qo[k]));
+            p[o] = pi;
+            q[o] = qi;
+            mu = cadd(mu, cmul(pi, qi));
+        }
+        if (RPW == 1) sbp[sb * LW + l] = mu;
+        __syncthreads();   // all warps done with buffer b (and sbp complete)
+        if (threadIdx.x < LW) {
+            c128 t = cmk(0.0, 0.0);
+            for (int s2 = 0; s2 < 8; ++s2) t = cadd(t, sbp[s2 * LW + threadIdx.x]);
+            part[(size_t)claim * KP + lane] = t;
+        }
+    }
+}
+
+template <int NT>
+static float run_tw(const double *ta, const double *tb, const c128 *z, c128 *p, c128 *q, c128 *part, int sms) {
+    const int nitems = ((N + 31) / 32) * 2;
+    const size_t sm = 128 + 2 * TW_ROWS * LW * sizeof(c128);
+    cudaFuncSetAttribute(k_tmawin<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const c128 beta = make_double2(0.3, 0.1), sg = make_double2(1.5, -2.0);
+    k_tmawin<NT><<<sms, NT, sm>>>(ta, tb, z, p, q, beta, sg, nitems, part);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        k_tmawin<NT><<<sms, NT, sm>>>(ta, tb, z, p, q, beta, sg, nitems, part);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    return best;
+}
+
 template <int MODE>
 static float run(const double *ta, const double *tb, const int *ix, const c128 *z, c128 *p, c128 *q, c128 *part,
                  int sms) {
@@ -176,6 +318,8 @@ int main() {
     t[5] = run<RED>(ta, tb, ix, z, p, q, part, sms);
     t[6] = run<STRIP>(ta, tb, ix, z, p, q, part, sms);
     t[7] = run<STRIP2>(ta, tb, ix, z, p, q, part, sms);
+    const float tw = run_tw<256>(ta, tb, z, p, q, part, sms);
+    printf("%-7s %8.3f ms  %7.0f GB/s\n", "TMAWIN", tw, bytes / (tw * 1e-3) / 1e9);
     for (int m = 0; m < 8; ++m)
         printf("%-7s %8.3f ms  %7.0f GB/s (80 B per row-lane + matrix)\n", names[m], t[m], bytes / (t[m] * 1e-3) / 1e9);
     cudaError_t e = cudaGetLastError();
