@@ -335,65 +335,111 @@ __device__ __forceinline__ void couplings(const BandDev &D, int p, c128 sg, c128
         }
 }
 
-// ---- prepare: the interface system's block LU, one thread per shift -------
+// ---- prepare: the interface system's twisted block LU, one thread per shift --
+// The block-tridiagonal interface system  A_p x_{p-1} + D_p x_p + C_p x_{p+1}
+// = g_p  (p = 1 .. P-1) is eliminated from both ends towards a middle block m
+// (a "twisted" factorization), so a solve runs two dependent chains of half
+// the length side by side.  Per block (rl, rdi, ru):
+//   p < m (top):     L_p = A_p Dh_{p-1}^-1, Dh_p^-1, C_p       (Dh_p = D_p - L_p C_{p-1})
+//   p > m (bottom):  U_p = C_p Eh_{p+1}^-1, Eh_p^-1, A_p       (Eh_p = D_p - U_p A_{p+1})
+//   p = m:           L_m, Dmid^-1, U_m                          (Dmid = D_m - L_m C_{m-1} - U_m A_{m+1})
+__host__ __device__ inline int band_mid(int P) { return P - 1 <= 2 ? P - 1 : 1 + (P - 1) / 2; }
+
+template <int B>
+__device__ __forceinline__ void band_blocks(const BandDev &D, int p, c128 sg, int lane, c128 (&Dp)[B][B],
+                                            c128 (&Cp)[B][B], c128 (&Ap)[B][B]) {
+    const int kp = D.kp;
+    c128 gp[B][B], gc[B][B], sp[B][B];
+    couplings<B>(D, p, sg, Dp, gp, gc);
+    // D_p = S_GG - S_GIprev Fbot_{p-1} - S_GIcur Etop_p
+    load_bb<B>(sp, D.spk + ((size_t)(p - 1) * 4 + 3) * B * B * kp, kp, lane);
+    mm_sub<B>(Dp, gp, sp);
+    load_bb<B>(sp, D.spk + ((size_t)p * 4 + 0) * B * B * kp, kp, lane);
+    mm_sub<B>(Dp, gc, sp);
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            Cp[i][j] = cmk(0.0, 0.0);
+            Ap[i][j] = cmk(0.0, 0.0);
+        }
+    if (p + 1 < D.P) {   // C_p = -S_GIcur Ftop_p
+        load_bb<B>(sp, D.spk + ((size_t)p * 4 + 2) * B * B * kp, kp, lane);
+        mm_sub<B>(Cp, gc, sp);
+    }
+    if (p >= 2) {        // A_p = -S_GIprev Ebot_{p-1}
+        load_bb<B>(sp, D.spk + ((size_t)(p - 1) * 4 + 1) * B * B * kp, kp, lane);
+        mm_sub<B>(Ap, gp, sp);
+    }
+}
+
 template <int B>
 __global__ void k_band_rfactor(BandDev D, ShiftDev S, double *pstat) {
     const int lane = blockIdx.x * blockDim.x + threadIdx.x;
     if (lane >= D.kp) return;
-    const int kp = D.kp;
+    const int kp = D.kp, P = D.P, m = band_mid(P);
     const c128 sg = S.sigma[lane];
-    c128 dinv_prev[B][B], rup_prev[B][B];
     double pmin = INFINITY;
-    for (int p = 1; p < D.P; ++p) {
-        c128 gg[B][B], gp[B][B], gc[B][B], sp[B][B];
-        couplings<B>(D, p, sg, gg, gp, gc);
-        // R_pp = S_GG - S_GIprev Fbot_{p-1} - S_GIcur Etop_p
-        load_bb<B>(sp, D.spk + ((size_t)(p - 1) * 4 + 3) * B * B * kp, kp, lane);
-        mm_sub<B>(gg, gp, sp);
-        load_bb<B>(sp, D.spk + ((size_t)p * 4 + 0) * B * B * kp, kp, lane);
-        mm_sub<B>(gg, gc, sp);
-        // R_{p,p+1} = -S_GIcur Ftop_p
-        c128 rup[B][B];
+    auto note = [&](double pv) { pmin = isfinite(pv) ? fmin(pmin, pv) : 0.0; };
+    c128 Dp[B][B], Cp[B][B], Ap[B][B], T0[B][B], inv[B][B];
+    // bottom part, p = P-1 .. m+1
+    c128 einv_next[B][B], a_next[B][B];
+    for (int p = P - 1; p > m; --p) {
+        band_blocks<B>(D, p, sg, lane, Dp, Cp, Ap);
 #pragma unroll
         for (int i = 0; i < B; ++i)
 #pragma unroll
-            for (int j = 0; j < B; ++j) rup[i][j] = cmk(0.0, 0.0);
-        if (p + 1 < D.P) {
-            load_bb<B>(sp, D.spk + ((size_t)p * 4 + 2) * B * B * kp, kp, lane);
-            mm_sub<B>(rup, gc, sp);
+            for (int j = 0; j < B; ++j) T0[i][j] = cmk(0.0, 0.0);
+        if (p + 1 < P) {
+            mm<B>(T0, Cp, einv_next);       // U_p = C_p Eh_{p+1}^-1
+            mm_sub<B>(Dp, T0, a_next);      // Eh_p = D_p - U_p A_{p+1}
         }
-        c128 L[B][B];
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-            for (int j = 0; j < B; ++j) L[i][j] = cmk(0.0, 0.0);
-        if (p >= 2) {
-            // R_{p,p-1} = -S_GIprev Ebot_{p-1};  L_p = R_{p,p-1} Dh_{p-1}^-1;  Dh_p = R_pp - L_p R_{p-1,p}
-            c128 rlo[B][B];
-#pragma unroll
-            for (int i = 0; i < B; ++i)
-#pragma unroll
-                for (int j = 0; j < B; ++j) rlo[i][j] = cmk(0.0, 0.0);
-            load_bb<B>(sp, D.spk + ((size_t)(p - 1) * 4 + 1) * B * B * kp, kp, lane);
-            mm_sub<B>(rlo, gp, sp);
-            mm<B>(L, rlo, dinv_prev);
-            mm_sub<B>(gg, L, rup_prev);
-        }
-        c128 di[B][B];
-        const double pv = inv_bb<B>(gg, di);
-        pmin = isfinite(pv) ? fmin(pmin, pv) : 0.0;
-        store_bb<B>(L, D.rl + (size_t)p * B * B * kp, kp, lane);
-        store_bb<B>(di, D.rdi + (size_t)p * B * B * kp, kp, lane);
-        store_bb<B>(rup, D.ru + (size_t)p * B * B * kp, kp, lane);
+        note(inv_bb<B>(Dp, inv));
+        store_bb<B>(T0, D.rl + (size_t)p * B * B * kp, kp, lane);
+        store_bb<B>(inv, D.rdi + (size_t)p * B * B * kp, kp, lane);
+        store_bb<B>(Ap, D.ru + (size_t)p * B * B * kp, kp, lane);
 #pragma unroll
         for (int i = 0; i < B; ++i)
 #pragma unroll
             for (int j = 0; j < B; ++j) {
-                dinv_prev[i][j] = di[i][j];
-                rup_prev[i][j] = rup[i][j];
+                einv_next[i][j] = inv[i][j];
+                a_next[i][j] = Ap[i][j];
             }
     }
-    if (D.P > 1)
+    // top part, p = 1 .. m
+    c128 dinv_prev[B][B], c_prev[B][B];
+    for (int p = 1; p <= m; ++p) {
+        band_blocks<B>(D, p, sg, lane, Dp, Cp, Ap);
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+            for (int j = 0; j < B; ++j) T0[i][j] = cmk(0.0, 0.0);
+        if (p >= 2) {
+            mm<B>(T0, Ap, dinv_prev);       // L_p = A_p Dh_{p-1}^-1
+            mm_sub<B>(Dp, T0, c_prev);      // Dh_p = D_p - L_p C_{p-1}
+        }
+        if (p == m && m + 1 < P) {          // the middle also takes the bottom part's Schur term
+            c128 U[B][B];
+            mm<B>(U, Cp, einv_next);        // U_m = C_m Eh_{m+1}^-1
+            mm_sub<B>(Dp, U, a_next);       // Dmid = Dh_m - U_m A_{m+1}
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+                for (int j = 0; j < B; ++j) Cp[i][j] = U[i][j];   // stored in ru for the middle
+        }
+        note(inv_bb<B>(Dp, inv));
+        store_bb<B>(T0, D.rl + (size_t)p * B * B * kp, kp, lane);
+        store_bb<B>(inv, D.rdi + (size_t)p * B * B * kp, kp, lane);
+        store_bb<B>(Cp, D.ru + (size_t)p * B * B * kp, kp, lane);
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                dinv_prev[i][j] = inv[i][j];
+                c_prev[i][j] = Cp[i][j];
+            }
+    }
+    if (P > 1)
         atomicMin(reinterpret_cast<unsigned long long *>(pstat) + lane,
                   (unsigned long long)__double_as_longlong(pmin));
 }
@@ -469,62 +515,151 @@ __global__ void k_band_s1(BandDev D, ShiftDev S, const c128 *__restrict__ rsh, c
     }
 }
 
-// interface system, one thread per shift: block forward / backward substitution
+// twisted interface solve for one shift; blk(p, which) returns block p's
+// stored matrix (0: rl, 1: rdi, 2: ru), g(p) its reduced rhs, hs(p) a scratch
+// vector slot and xs(p) the output slot.  part: 0 = both halves in this
+// thread, 1 = top half only, 2 = bottom half only, 3 = neither (a thread
+// that only joins the two sync() calls: after the eliminations, where the top
+// half solves the middle block, and before the back substitutions)
+template <int B, typename Blk, typename G, typename Hs, typename Xs, typename Sync>
+__device__ __forceinline__ void twisted_solve(int P, int part, Blk blk, G g, Hs hs, Xs xs, Sync sync) {
+    const int m = band_mid(P);
+    const bool top = part == 0 || part == 1, bot = part == 0 || part == 2;
+    c128 M0[B][B];
+    c128 h[B], v[B];
+    if (top) {                   // top: h_p = g_p - L_p h_{p-1}, p = 1 .. m-1
+#pragma unroll
+        for (int i = 0; i < B; ++i) h[i] = cmk(0.0, 0.0);
+        for (int p = 1; p < m; ++p) {
+            g(p, v);
+            if (p >= 2) {
+                blk(p, 0, M0);
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], h[j]);
+            }
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                h[i] = v[i];
+                hs(p)[i] = v[i];
+            }
+        }
+    }
+    if (bot) {                   // bottom: f_p = g_p - U_p f_{p+1}, p = P-1 .. m+1
+#pragma unroll
+        for (int i = 0; i < B; ++i) h[i] = cmk(0.0, 0.0);
+        for (int p = P - 1; p > m; --p) {
+            g(p, v);
+            if (p + 1 < P) {
+                blk(p, 0, M0);
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], h[j]);
+            }
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                h[i] = v[i];
+                hs(p)[i] = v[i];
+            }
+        }
+    }
+    sync();
+    if (top) {                   // middle: x_m = Dmid^-1 (g_m - L_m h_{m-1} - U_m f_{m+1})
+        g(m, v);
+        if (m >= 2) {
+            blk(m, 0, M0);
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], hs(m - 1)[j]);
+        }
+        if (m + 1 < P) {
+            blk(m, 2, M0);
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], hs(m + 1)[j]);
+        }
+        blk(m, 1, M0);
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            c128 t = cmk(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < B; ++j) t = cadd(t, cmul(M0[i][j], v[j]));
+            xs(m)[i] = t;
+        }
+    }
+    sync();
+    if (top) {                   // x_p = Dh_p^-1 (h_p - C_p x_{p+1}), p = m-1 .. 1
+        for (int p = m - 1; p >= 1; --p) {
+#pragma unroll
+            for (int i = 0; i < B; ++i) v[i] = hs(p)[i];
+            blk(p, 2, M0);
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], xs(p + 1)[j]);
+            blk(p, 1, M0);
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                c128 t = cmk(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < B; ++j) t = cadd(t, cmul(M0[i][j], v[j]));
+                xs(p)[i] = t;
+            }
+        }
+    }
+    if (bot) {                   // x_p = Eh_p^-1 (f_p - A_p x_{p-1}), p = m+1 .. P-1
+        for (int p = m + 1; p < P; ++p) {
+#pragma unroll
+            for (int i = 0; i < B; ++i) v[i] = hs(p)[i];
+            blk(p, 2, M0);
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], xs(p - 1)[j]);
+            blk(p, 1, M0);
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                c128 t = cmk(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < B; ++j) t = cadd(t, cmul(M0[i][j], v[j]));
+                xs(p)[i] = t;
+            }
+        }
+    }
+}
+
+// a proxy for a B-vector stored with a lane stride
+struct StridedVec {
+    c128 *base;
+    int stride;
+    __device__ __forceinline__ c128 &operator[](int i) const { return base[(size_t)i * stride]; }
+};
+
+// interface system from HBM, one thread per shift (larger problems)
 template <int B>
 __global__ void k_band_red(BandDev D, const c128 *__restrict__ rsh, const c128 *__restrict__ rps) {
     const int lane = blockIdx.x * blockDim.x + threadIdx.x;
     if (lane >= D.kp) return;
     const int kp = D.kp, M = D.M;
-    c128 h[B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) h[i] = cmk(0.0, 0.0);
-    for (int p = 1; p < D.P; ++p) {
-        c128 g[B];
-        const c128 *gprev = D.gcon + ((size_t)(p - 1) * 2 * B + B) * kp;
-        const c128 *gcur = D.gcon + (size_t)p * 2 * B * kp;
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-            g[i] = csub(csub(rhs_at<B>(D, rsh, rps, (int64_t)p * M + i, lane), __ldg(gprev + (size_t)i * kp + lane)),
-                        __ldg(gcur + (size_t)i * kp + lane));
-        if (p >= 2) {
-            c128 L[B][B];
-            load_bb<B>(L, D.rl + (size_t)p * B * B * kp, kp, lane);
+    c128 *const mats[3] = {D.rl, D.rdi, D.ru};
+    twisted_solve<B>(
+        D.P, 0,
+        [&](int p, int which, c128 (&o)[B][B]) { load_bb<B>(o, mats[which] + (size_t)p * B * B * kp, kp, lane); },
+        [&](int p, c128 (&v)[B]) {
+            const c128 *gprev = D.gcon + ((size_t)(p - 1) * 2 * B + B) * kp;
+            const c128 *gcur = D.gcon + (size_t)p * 2 * B * kp;
 #pragma unroll
             for (int i = 0; i < B; ++i)
-#pragma unroll
-                for (int j = 0; j < B; ++j) g[i] = cfnma(g[i], L[i][j], h[j]);
-        }
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-            h[i] = g[i];
-            D.xg[((size_t)p * B + i) * kp + lane] = g[i];
-        }
-    }
-    c128 x[B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) x[i] = cmk(0.0, 0.0);
-    for (int p = D.P - 1; p >= 1; --p) {
-        c128 v[B], U[B][B], Di[B][B];
-#pragma unroll
-        for (int i = 0; i < B; ++i) v[i] = D.xg[((size_t)p * B + i) * kp + lane];
-        if (p + 1 < D.P) {
-            load_bb<B>(U, D.ru + (size_t)p * B * B * kp, kp, lane);
-#pragma unroll
-            for (int i = 0; i < B; ++i)
-#pragma unroll
-                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], U[i][j], x[j]);
-        }
-        load_bb<B>(Di, D.rdi + (size_t)p * B * B * kp, kp, lane);
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-            c128 s = cmk(0.0, 0.0);
-#pragma unroll
-            for (int j = 0; j < B; ++j) s = cadd(s, cmul(Di[i][j], v[j]));
-            x[i] = s;
-        }
-#pragma unroll
-        for (int i = 0; i < B; ++i) D.xg[((size_t)p * B + i) * kp + lane] = x[i];
-    }
+                v[i] = csub(csub(rhs_at<B>(D, rsh, rps, (int64_t)p * M + i, lane), __ldg(gprev + (size_t)i * kp + lane)),
+                            __ldg(gcur + (size_t)i * kp + lane));
+        },
+        // h / f live in xg until the back substitution overwrites them in order
+        [&](int p) { return StridedVec{D.X + (size_t)p * B * kp + lane, kp}; },
+        [&](int p) { return StridedVec{D.xg + (size_t)p * B * kp + lane, kp}; }, [] {});
 }
 
 // interior solves with the interface values known -> x (all rows) in Xout
@@ -649,18 +784,18 @@ __device__ __forceinline__ void band_stage(const BandDev &D, const c128 *rsh, co
         const int co = cr % (2 * B + 1), rr = cr / (2 * B + 1);
         const int64_t r = r0 + rr;
         const int lane = lane0 + l;
-        c128 v;
-        if (co < B) v = __ldg(D.lo + ((size_t)r * B + co) * kp + lane);
-        else if (co < 2 * B) v = __ldg(D.up + ((size_t)r * B + co - B) * kp + lane);
-        else v = __ldg(D.dinv + (size_t)r * kp + lane);
-        f[idx] = v;
+        const c128 *src = co < B       ? D.lo + ((size_t)r * B + co) * kp + lane
+                          : co < 2 * B ? D.up + ((size_t)r * B + co - B) * kp + lane
+                                       : D.dinv + (size_t)r * kp + lane;
+        cp_async16(f + idx, src);
     }
     if (rsh) {
-        for (int idx = threadIdx.x; idx < m; idx += blockDim.x) rb[idx] = __ldg(rsh + r0 + idx);
+        for (int idx = threadIdx.x; idx < m; idx += blockDim.x) cp_async16(rb + idx, rsh + r0 + idx);
     } else {
         for (int idx = threadIdx.x; idx < m * lg; idx += blockDim.x)
-            rb[idx] = __ldg(rps + (size_t)(r0 + idx / lg) * kp + lane0 + idx % lg);
+            cp_async16(rb + idx, rps + (size_t)(r0 + idx / lg) * kp + lane0 + idx % lg);
     }
+    cp_async_wait_all();
     __syncthreads();
 }
 
@@ -778,7 +913,7 @@ constexpr int RLG = 4;
 template <int B>
 __host__ __device__ inline size_t band_red_smem(int P) {
     const size_t np = (size_t)(P > 1 ? P - 1 : 1);
-    return np * RLG * sizeof(c128) * (3 * B * B + 3 * B + B);
+    return np * RLG * sizeof(c128) * (3 * B * B + 3 * B + 2 * B);
 }
 
 template <int B>
@@ -788,73 +923,57 @@ __global__ void __launch_bounds__(256) k_band_red_st(BandDev D, const c128 *__re
     const int lane0 = blockIdx.x * RLG;
     const int kp = D.kp, M = D.M, P = D.P;
     const int lg = min(RLG, kp - lane0);
-    constexpr int W = 3 * B * B + 3 * B;   // per block: L, Dinv, U, (rhs, gprev, gcur)
+    constexpr int W = 3 * B * B + 3 * B;   // per block: L|U, Dinv|Einv, C|A, (rhs, gprev, gcur)
     c128 *sm = reinterpret_cast<c128 *>(bsm);                 // [P-1][W][RLG]
-    c128 *hsm = sm + (size_t)(P - 1) * W * RLG;               // [P-1][B][RLG]
+    c128 *hsm = sm + (size_t)(P - 1) * W * RLG;               // [P-1][B][RLG]  h / f
+    c128 *xsm = hsm + (size_t)(P - 1) * B * RLG;              // [P-1][B][RLG]  x
     for (int idx = threadIdx.x; idx < (P - 1) * W * lg; idx += blockDim.x) {
         const int l = idx % lg, pe = idx / lg;
         const int p = 1 + pe / W, e = pe % W;
         const int lane = lane0 + l;
-        c128 v;
-        if (e < B * B) v = __ldg(D.rl + ((size_t)p * B * B + e) * kp + lane);
-        else if (e < 2 * B * B) v = __ldg(D.rdi + ((size_t)p * B * B + e - B * B) * kp + lane);
-        else if (e < 3 * B * B) v = __ldg(D.ru + ((size_t)p * B * B + e - 2 * B * B) * kp + lane);
+        const c128 *src;
+        if (e < B * B) src = D.rl + ((size_t)p * B * B + e) * kp + lane;
+        else if (e < 2 * B * B) src = D.rdi + ((size_t)p * B * B + e - B * B) * kp + lane;
+        else if (e < 3 * B * B) src = D.ru + ((size_t)p * B * B + e - 2 * B * B) * kp + lane;
         else {
             const int i = (e - 3 * B * B) % B, which = (e - 3 * B * B) / B;
-            if (which == 0) v = rhs_at<B>(D, rsh, rps, (int64_t)p * M + i, lane);
-            else if (which == 1) v = __ldg(D.gcon + ((size_t)(p - 1) * 2 * B + B + i) * kp + lane);
-            else v = __ldg(D.gcon + ((size_t)p * 2 * B + i) * kp + lane);
+            if (which == 0) src = rsh ? rsh + (int64_t)p * M + i : rps + ((size_t)p * M + i) * kp + lane;
+            else if (which == 1) src = D.gcon + ((size_t)(p - 1) * 2 * B + B + i) * kp + lane;
+            else src = D.gcon + ((size_t)p * 2 * B + i) * kp + lane;
         }
-        sm[(size_t)pe * RLG + l] = v;
+        cp_async16(sm + (size_t)pe * RLG + l, src);
     }
+    cp_async_wait_all();
     __syncthreads();
-    const int l = threadIdx.x;
-    if (l >= lg) return;
-    const int lane = lane0 + l;
+    // thread l < lg: top half of lane l; thread RLG + l: its bottom half
+    const int t = threadIdx.x;
+    const int l = t < RLG ? t : t - RLG;
+    const int part = (t < RLG && l < lg) ? 1 : (t >= RLG && t < 2 * RLG && l < lg) ? 2 : 3;
+    const int ll = part == 3 ? 0 : l;
     const c128 *__restrict__ in = sm;
-    auto at = [&](int p, int e) { return in[((size_t)(p - 1) * W + e) * RLG + l]; };
-    c128 h[B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) h[i] = cmk(0.0, 0.0);
-    for (int p = 1; p < P; ++p) {
-        c128 g[B];
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-            g[i] = csub(csub(at(p, 3 * B * B + i), at(p, 3 * B * B + B + i)), at(p, 3 * B * B + 2 * B + i));
-        if (p >= 2) {
+    twisted_solve<B>(
+        P, part,
+        [&](int p, int which, c128 (&o)[B][B]) {
 #pragma unroll
             for (int i = 0; i < B; ++i)
 #pragma unroll
-                for (int j = 0; j < B; ++j) g[i] = cfnma(g[i], at(p, i * B + j), h[j]);
-        }
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-            h[i] = g[i];
-            hsm[((size_t)(p - 1) * B + i) * RLG + l] = g[i];
-        }
-    }
-    c128 x[B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) x[i] = cmk(0.0, 0.0);
-    for (int p = P - 1; p >= 1; --p) {
-        c128 v[B];
-#pragma unroll
-        for (int i = 0; i < B; ++i) v[i] = hsm[((size_t)(p - 1) * B + i) * RLG + l];
-        if (p + 1 < P) {
+                for (int j = 0; j < B; ++j)
+                    o[i][j] = in[((size_t)(p - 1) * W + which * B * B + i * B + j) * RLG + ll];
+        },
+        [&](int p, c128 (&v)[B]) {
+            const c128 *b = in + (size_t)(p - 1) * W * RLG;
 #pragma unroll
             for (int i = 0; i < B; ++i)
-#pragma unroll
-                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], at(p, 2 * B * B + i * B + j), x[j]);
-        }
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-            c128 t = cmk(0.0, 0.0);
-#pragma unroll
-            for (int j = 0; j < B; ++j) t = cadd(t, cmul(at(p, B * B + i * B + j), v[j]));
-            x[i] = t;
-        }
-#pragma unroll
-        for (int i = 0; i < B; ++i) D.xg[((size_t)p * B + i) * kp + lane] = x[i];
+                v[i] = csub(csub(b[(3 * B * B + i) * RLG + ll], b[(3 * B * B + B + i) * RLG + ll]),
+                            b[(3 * B * B + 2 * B + i) * RLG + ll]);
+        },
+        [&](int p) { return StridedVec{hsm + (size_t)(p - 1) * B * RLG + ll, RLG}; },
+        [&](int p) { return StridedVec{xsm + (size_t)(p - 1) * B * RLG + ll, RLG}; }, [] { __syncthreads(); });
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < (P - 1) * B * lg; idx += blockDim.x) {
+        const int l2 = idx % lg, pi = idx / lg;
+        const int p = 1 + pi / B, i = pi % B;
+        D.xg[((size_t)p * B + i) * kp + lane0 + l2] = xsm[(size_t)pi * RLG + l2];
     }
 }
 
