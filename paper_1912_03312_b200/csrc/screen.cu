@@ -33,56 +33,113 @@ constexpr int SCR_WC_MAX = 32;   // kl + ku + 1 <= 32
 
 __device__ __forceinline__ double cabs1(c128 a) { return fabs(a.x) + fabs(a.y); }
 
-// 1 / b, Smith's algorithm (the oracle's cdiv, oracle/rexi_oracle.c)
+// 1 / b without a division (the screen reproduces the reference's verdict, not
+// its bits): the hardware reciprocal approximation of |b|^2 refined by two
+// Newton steps (~full fp64 accuracy), times conj(b).  A division subroutine
+// per row made the 1M-row chain of config 2 take 0.7 s.
+__device__ __forceinline__ double rcp_nr(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    r = r * fma(-d, r, 2.0);
+    r = r * fma(-d, r, 2.0);
+    return r;
+}
 __device__ __forceinline__ c128 crecip_smith(c128 b) {
-    if (fabs(b.x) >= fabs(b.y)) {
-        const double r = b.y / b.x, den = b.x + r * b.y;
-        return cmk(1.0 / den, -r / den);
-    }
-    const double r = b.x / b.y, den = b.y + r * b.x;
-    return cmk(r / den, -1.0 / den);
+    const double rd = rcp_nr(fma(b.x, b.x, b.y * b.y));   // |b| well inside 1e+-150 here
+    return cmk(b.x * rd, -b.y * rd);
 }
 
 // band[(row * w + (d + kl)) * 3 + {0,1,2}] = fl(tau a), fl(tau a_im), b of entry
 // (row, row + d), zero when absent; w = kl + ku + 1.  KL < 0: runtime extents
 // (window in local memory); otherwise compile-time (window in registers).
+// The row data are the same for every shift (thread): the warp stages chunks
+// of CH rows in shared memory with cp.async, double buffered, so the
+// sequential elimination never waits on a global load.
 template <int KL, int KU>
 __global__ void __launch_bounds__(32) k_band_screen(const double *__restrict__ band, int64_t n, int kl_rt, int ku_rt,
-                                                    const c128 *__restrict__ sigma, int k, double *umin_out,
-                                                    double *umax_out, long long *info_out) {
+                                                    const c128 *__restrict__ sigma, int k, int CH,
+                                                    double *umin_out, double *umax_out, long long *info_out) {
+    extern __shared__ __align__(16) double sbuf[];           // [2][CH * w * 3]
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= k) return;
     constexpr bool RT = KL < 0;
     const int kl = RT ? kl_rt : KL, ku = RT ? ku_rt : KU;
     const int kv = kl + ku, w = kv + 1;
+    const int per_row = w * 3;
+    const int64_t nchunks = (n + CH - 1) / CH;
+    auto stage = [&](int64_t c, int buf) {       // whole warp: rows [c*CH, c*CH + CH)
+        const int64_t r0 = c * CH;
+        const int rows = (int)min((int64_t)CH, n - r0);
+        const int nd = rows * per_row;           // doubles; copy in 16-B pieces (+ a tail)
+        const double *src = band + (size_t)r0 * per_row;
+        double *dst = sbuf + (size_t)buf * CH * per_row;
+        const bool al = ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+        if (al) {
+            for (int t = threadIdx.x; t < nd / 2; t += 32) cp_async16(dst + 2 * t, src + 2 * t);
+            if ((nd & 1) && threadIdx.x == 0) dst[nd - 1] = src[nd - 1];
+        } else {
+            for (int t = threadIdx.x; t < nd; t += 32) dst[t] = src[t];
+        }
+    };
+    stage(0, 0);
+    cp_async_wait_all();
+    __syncwarp();
+    const bool live = j < k;
+    const c128 sg = live ? sigma[j] : cmk(0.0, 0.0);
     constexpr int WR = RT ? SCR_WR_MAX : (KL < 0 ? 1 : KL + 1);
     constexpr int WC = RT ? SCR_WC_MAX : (KL < 0 ? 1 : KL + KU + 1);
     c128 W[WR][WC];
-    const c128 sg = sigma[j];
-    // matrix row r into window row `slot`, window column c = column - col0
+    int64_t cur_chunk = 0;
+    // the entering row's data: buffer eb, offset eo rows (advanced per row, no
+    // 64-bit division on the dependent path)
+    int eb = 0, eo = 0;
+    auto next_row = [&]() {
+        if (++eo == CH) {
+            eo = 0;
+            eb ^= 1;
+        }
+    };
     auto load_row = [&](int64_t r, int slot, int64_t col0) {
 #pragma unroll
         for (int c = 0; c < WC; ++c)
             if (c <= kv) W[slot][c] = cmk(0.0, 0.0);
         if (r >= n) return;
+        const double *e0 = sbuf + (size_t)eb * CH * per_row + (size_t)eo * per_row;
 #pragma unroll
         for (int dd = 0; dd < WC; ++dd) {
             if (dd >= w) break;
             const int64_t col = r + dd - kl;
             const int64_t c = col - col0;
             if (col < 0 || col >= n || c < 0 || c > kv) continue;
-            const double *e = band + ((size_t)r * w + dd) * 3;
-            W[slot][c] = form_entry(__ldg(e), __ldg(e + 1), __ldg(e + 2), sg);
+            const double *e = e0 + dd * 3;
+            W[slot][c] = form_entry(e[0], e[1], e[2], sg);
         }
     };
+    // the window needs rows up to col + kl: keep chunks cur and cur + 1 staged
+    if (nchunks > 1) stage(1, 1);
+    cp_async_wait_all();
+    __syncwarp();
 #pragma unroll
     for (int s = 0; s < WR; ++s)
-        if (s <= kl) load_row(s, s, 0);
-    double umin = INFINITY, umax = 0.0;
+        if (s <= kl) {
+            load_row(s, s, 0);
+            next_row();
+        }
+    double umin = INFINITY, umax = 0.0;     // extremes of |U_ii|^2 (square roots at the end)
     long long info = 0;
+    int col_off = 0;
     for (int64_t col = 0; col < n; ++col) {
+        // entering chunk boundary: the row col + 1 + kl may sit in chunk cur + 1;
+        // once col leaves chunk cur, refill its buffer with chunk cur + 2
+        if (col_off == CH) {
+            col_off = 0;
+            __syncwarp();
+            ++cur_chunk;
+            if (cur_chunk + 1 < nchunks) stage(cur_chunk + 1, (int)((cur_chunk + 1) & 1));
+            cp_async_wait_all();
+            __syncwarp();
+        }
+        ++col_off;
         const int km = (int)min((int64_t)kl, n - 1 - col);
-        // IZAMAX over the diagonal and the km entries below it (first maximum)
         int p = 0;
         double best = cabs1(W[0][0]);
 #pragma unroll
@@ -99,16 +156,16 @@ __global__ void __launch_bounds__(32) k_band_screen(const double *__restrict__ b
         for (int s = 0; s < WR; ++s)
             if (s == p) zero = W[s][0].x == 0.0 && W[s][0].y == 0.0;
         if (!zero) {
-            if (p != 0) {
+            // row swap by selects (the shifts of a warp pivot differently)
 #pragma unroll
-                for (int s = 1; s < WR; ++s)
-                    if (s == p)
+            for (int s = 1; s < WR; ++s) {
+                const bool sw = s == p;
 #pragma unroll
-                        for (int c = 0; c < WC; ++c) {
-                            const c128 t = W[s][c];
-                            W[s][c] = W[0][c];
-                            W[0][c] = t;
-                        }
+                for (int c = 0; c < WC; ++c) {
+                    const c128 a = W[0][c], b2 = W[s][c];
+                    W[0][c] = sw ? b2 : a;
+                    W[s][c] = sw ? a : b2;
+                }
             }
             const c128 rp = crecip_smith(W[0][0]);
 #pragma unroll
@@ -119,15 +176,13 @@ __global__ void __launch_bounds__(32) k_band_screen(const double *__restrict__ b
                 for (int c = 1; c < WC; ++c)
                     if (c <= kv) W[s][c] = csub(W[s][c], cmul(m, W[0][c]));
             }
-            const double u = hypot(W[0][0].x, W[0][0].y);
+            const double u = fma(W[0][0].x, W[0][0].x, W[0][0].y * W[0][0].y);
             umin = fmin(umin, u);
-            umax = fmax(umax, u);
+            umax = isfinite(u) ? fmax(umax, u) : INFINITY;
         } else {
             if (info == 0) info = col + 1;
             umin = 0.0;
         }
-        // slide the window one row down / one column right; the entering row
-        // is the original row col + 1 + kl
 #pragma unroll
         for (int s = 0; s + 1 < WR; ++s) {
             if (s >= kl) break;
@@ -139,9 +194,11 @@ __global__ void __launch_bounds__(32) k_band_screen(const double *__restrict__ b
 #pragma unroll
         for (int s = 0; s < WR; ++s)
             if (s == kl) load_row(col + 1 + kl, s, col + 1);
+        next_row();
     }
-    umin_out[j] = umin;
-    umax_out[j] = umax;
+    if (!live) return;
+    umin_out[j] = sqrt(umin);
+    umax_out[j] = sqrt(umax);
     info_out[j] = info;
 }
 
@@ -192,14 +249,21 @@ int band_screen(const rexi_desc *d, int kl, int ku, const c128 *sigma_dev, cudaS
     SCK(rexi_poison(dinfo, sizeof(long long) * k));
     SCK(cudaMemcpyAsync(dband, band.data(), sizeof(double) * band.size(), cudaMemcpyHostToDevice, st));
     const int grid = (k + 31) / 32;
-    if (kl == 1 && ku == 1)
-        k_band_screen<1, 1><<<grid, 32, 0, st>>>(dband, n, kl, ku, sigma_dev, k, dmin, dmax, dinfo);
-    else if (kl == 2 && ku == 2)
-        k_band_screen<2, 2><<<grid, 32, 0, st>>>(dband, n, kl, ku, sigma_dev, k, dmin, dmax, dinfo);
-    else if (kl == 0 && ku == 0)
-        k_band_screen<0, 0><<<grid, 32, 0, st>>>(dband, n, kl, ku, sigma_dev, k, dmin, dmax, dinfo);
-    else
-        k_band_screen<-1, -1><<<grid, 32, 0, st>>>(dband, n, kl, ku, sigma_dev, k, dmin, dmax, dinfo);
+    // rows per staged chunk: two chunks of row data in <= 96 KB of shared memory,
+    // and at least kl + 2 rows so the window's entering row is always staged
+    int CH = std::max(kl + 2, (int)std::min<int64_t>(1024, (96 * 1024) / (2 * (int64_t)w * 3 * 8)));
+    CH = (CH + 1) & ~1;   // even: every chunk starts 16-B aligned (cp.async)
+    const size_t smem = 2 * (size_t)CH * w * 3 * sizeof(double);
+    auto launch = [&](auto kern) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, 32, smem, st>>>(dband, n, kl, ku, sigma_dev, k, CH, dmin, dmax, dinfo);
+        return cudaGetLastError();
+    };
+    if (kl == 1 && ku == 1) SCK(launch(k_band_screen<1, 1>));
+    else if (kl == 2 && ku == 2) SCK(launch(k_band_screen<2, 2>));
+    else if (kl == 0 && ku == 0) SCK(launch(k_band_screen<0, 0>));
+    else SCK(launch(k_band_screen<-1, -1>));
     SCK(cudaGetLastError());
     std::vector<double> hmin(k), hmax(k);
     std::vector<long long> hinfo(k);

@@ -127,6 +127,94 @@ __global__ void __launch_bounds__(256, 3) k_probe(const double *__restrict__ ta,
     }
 }
 
+// The recomputed-q iteration (no q vector): SPMV2 gathers z and p_old at the
+// 7 columns (p_new = z + beta p_old formed per neighbour), writes p_new, mu;
+// UPD2 gathers p_new again for q = S p_new, updates x and z.  UPD is today's
+// update (x, z read + written, p, q read: 96 B per row-lane).
+template <int MODE>
+__global__ void __launch_bounds__(256, 3) k_iter(const double *__restrict__ ta, const double *__restrict__ tb,
+                                                 const c128 *__restrict__ z, const c128 *__restrict__ pold,
+                                                 c128 *__restrict__ pnew, c128 *__restrict__ x, c128 *__restrict__ zw,
+                                                 const c128 *__restrict__ q, c128 beta, c128 alpha, c128 sg,
+                                                 int nclaims, c128 *part) {
+    __shared__ c128 sbp[8 * KP];
+    const int lane = threadIdx.x & 63, slot = threadIdx.x >> 6;
+    for (int claim = blockIdx.x; claim < nclaims; claim += gridDim.x) {
+        const int R0 = claim * 32;
+        c128 mu[2] = {cmk(0.0, 0.0), cmk(0.0, 0.0)};
+        for (int k = 0; k < 8; ++k) {
+            const int i = R0 + slot + 4 * k;
+            if (i >= N) break;
+            const size_t o = (size_t)i * KP + lane;
+            c128 acc = cmk(0.0, 0.0);
+            if (MODE != 2) {
+                c128 zz[NNZ];
+#pragma unroll
+                for (int e = 0; e < NNZ; ++e) {
+                    int c = i + OFF[e];
+                    if (c < 0 || c >= N) c = i;
+                    const size_t oc = (size_t)c * KP + lane;
+                    zz[e] = MODE == 0 ? cadd(z[oc], cmul(beta, pold[oc])) : pnew[oc];
+                }
+#pragma unroll
+                for (int e = 0; e < NNZ; ++e) {
+                    const double a = __ldg(ta + (size_t)i * NNZ + e), b = __ldg(tb + (size_t)i * NNZ + e);
+                    const c128 en = cmk(a + sg.y * b, -(sg.x * b));
+                    acc = cadd(acc, cmul(en, zz[e]));
+                }
+            }
+            if (MODE == 0) {
+                const c128 pi = cadd(z[o], cmul(beta, pold[o]));
+                pnew[o] = pi;
+                mu[k >> 2] = cadd(mu[k >> 2], cmul(pi, acc));
+            } else {
+                const c128 pp = MODE == 1 ? pnew[o] : pold[o];
+                const c128 qq = MODE == 1 ? acc : q[o];
+                x[o] = cadd(x[o], cmul(alpha, pp));
+                const c128 d = cmk(ta[(size_t)i * NNZ + 3] + sg.y, -sg.x);
+                const double den = fma(d.x, d.x, d.y * d.y), r = 1.0 / den;
+                const c128 di = cmk(d.x * r, -d.y * r);
+                const c128 zn = cadd(zw[o], cmul(cmk(-alpha.x, -alpha.y), cmul(qq, di)));
+                zw[o] = zn;
+                mu[k >> 2] = cadd(mu[k >> 2], cmul(cmul(d, zn), zn));
+            }
+        }
+        sbp[(slot * 2 + 0) * KP + lane] = mu[0];
+        sbp[(slot * 2 + 1) * KP + lane] = mu[1];
+        __syncthreads();
+        if (threadIdx.x < KP) {
+            c128 t = cmk(0.0, 0.0);
+            for (int b = 0; b < 8; ++b) t = cadd(t, sbp[b * KP + threadIdx.x]);
+            part[(size_t)claim * KP + threadIdx.x] = t;
+        }
+        __syncthreads();
+    }
+}
+
+template <int MODE>
+static float run_iter(const double *ta, const double *tb, c128 *z, c128 *p, c128 *p2, c128 *x, c128 *q, c128 *part,
+                      int sms) {
+    const int nclaims = (N + 31) / 32;
+    const int grid = sms * 3;
+    const c128 beta = make_double2(0.3, 0.1), alpha = make_double2(0.2, -0.1), sg = make_double2(1.5, -2.0);
+    auto go = [&] { k_iter<MODE><<<grid, 256>>>(ta, tb, z, p, p2, x, z, q, beta, alpha, sg, nclaims, part); };
+    go();
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        go();
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    return best;
+}
+
 // work item = (32-row claim, 32-lane group); 8 warps = the 8 sub-blocks
 // (rows w, w+8, w+16, w+24); the item's 3 z windows (row ranges) are copied to
 // shared memory by bulk copies one item ahead (double buffered, one mbarrier
@@ -318,6 +406,22 @@ int main() {
     t[5] = run<RED>(ta, tb, ix, z, p, q, part, sms);
     t[6] = run<STRIP>(ta, tb, ix, z, p, q, part, sms);
     t[7] = run<STRIP2>(ta, tb, ix, z, p, q, part, sms);
+    {
+        c128 *p2, *x;
+        cudaMalloc(&p2, sizeof(c128) * (size_t)N * KP);
+        cudaMalloc(&x, sizeof(c128) * (size_t)N * KP);
+        cudaMemset(p2, 0, sizeof(c128) * (size_t)N * KP);
+        cudaMemset(x, 0, sizeof(c128) * (size_t)N * KP);
+        const float s2 = run_iter<0>(ta, tb, z, p, p2, x, q, part, sms);
+        const float u2 = run_iter<1>(ta, tb, z, p, p2, x, q, part, sms);
+        const float u0 = run_iter<2>(ta, tb, z, p, p2, x, q, part, sms);
+        printf("SPMV2 (gather z+p_old, write p: 48 B) %.3f ms | UPD2 (gather p, x z r/w: 80 B) %.3f ms | "
+               "UPD today (96 B) %.3f ms\n", s2, u2, u0);
+        printf("recomputed-q iteration %.3f ms vs today's spmv (RED) + update %.3f ms\n", s2 + u2,
+               run<RED>(ta, tb, ix, z, p, q, part, sms) + u0);
+        cudaFree(p2);
+        cudaFree(x);
+    }
     const float tw = run_tw<256>(ta, tb, z, p, q, part, sms);
     printf("%-7s %8.3f ms  %7.0f GB/s\n", "TMAWIN", tw, bytes / (tw * 1e-3) / 1e9);
     for (int m = 0; m < 8; ++m)
