@@ -63,3 +63,39 @@ def test_complex_potential_solvers_agree(flagship):
     n0 = np.sqrt(np.real(np.vdot(u0, B @ u0)))
     n3 = np.sqrt(np.real(np.vdot(outs[0], B @ outs[0])))
     assert n3 <= n0 * (1 + 1e-9)
+
+
+def _complex_p2_system(n=801):
+    """a pentadiagonal (P2-banded) pencil with an absorbing, complex A"""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from scipy.sparse import csr_matrix, diags
+    from test_oracle import _pencil_1d
+    from paper_1912_03312_b200.types import SystemMatrices
+    s = _pencil_1d(n, p2=True)
+    x = np.linspace(-1, 1, n)
+    absorb = -2.0j * np.clip((np.abs(x) - 0.7) / 0.3, 0.0, None) ** 2
+    A = (s.A + diags(absorb * np.asarray(s.B.diagonal()))).tocsr().astype(complex)
+    return SystemMatrices(A=csr_matrix(A), B=s.B, n_dof=n)
+
+
+@pytest.mark.parametrize("refine", [0, 1])
+def test_complex_potential_band_solver(flagship, refine):
+    """the band solver (P2 pencils) with complex A: against scipy's LU of
+    the same pole sum, and against COCG"""
+    from paper_1912_03312_b200 import rexi_prepare, rexi_step
+    sysm = _complex_p2_system()
+    x = np.linspace(-1, 1, sysm.n_dof)
+    u0 = np.exp(-((x + 0.3) / 0.1) ** 2) * np.exp(20j * x)
+    tau = 1e-4
+    outs = {}
+    for solver in ("band", "cocg"):
+        stp = rexi_prepare(sysm, flagship, tau, sr_value=1e4, override_admissibility=True, solver=solver,
+                           refine=refine if solver == "band" else 1)
+        assert stp.solver == solver
+        outs[solver] = rexi_step(stp, u0)
+        stp.close()
+    ref = _scipy_step(sysm, flagship, tau, u0)
+    assert np.linalg.norm(outs["band"] - ref) <= 1e-9 * np.linalg.norm(ref)
+    assert np.linalg.norm(outs["band"] - outs["cocg"]) <= 3e-9 * np.linalg.norm(ref)
