@@ -220,6 +220,25 @@ def _make_plans(stepper_args, pieces, piece_devs):
     return plans
 
 
+def max_shifts_per_plan(indptr, indices, solver: str = "auto") -> int:
+    """Shifts one native plan takes: 256 for the tridiagonal solver (its
+    level-0 lane tile), 1024 for the band solver, and for COCG the largest
+    power of two keeping n * k_pad below 2^31 (32-bit element offsets)."""
+    indptr = np.asarray(indptr)
+    indices = np.asarray(indices)
+    n = len(indptr) - 1
+    rows = np.repeat(np.arange(n), np.diff(indptr))
+    half_band = 0 if len(indices) == 0 else int(np.max(np.abs(indices - rows)))
+    if solver == "tridiag" or (solver == "auto" and half_band <= 1):
+        return 256
+    if solver == "band" or (solver == "auto" and 2 <= half_band <= 4):
+        return 1024
+    kp = 1
+    while 2 * kp * max(n, 1) < 2 ** 31 - 1:
+        kp *= 2
+    return kp
+
+
 def default_refine(indptr, indices, tau: float, sr_value: float, solver: str = "auto") -> int:
     """The refinement rounds ``rexi_prepare`` uses when ``refine`` is not
     given: the direct solvers (1D tridiagonal, and the band LU for half
@@ -291,6 +310,9 @@ def rexi_prepare(
         refine = default_refine(indptr, indices, tau, sr_value, solver)
     n_pieces = min(workers, k) if workers is not None else min(len(devs), k)
     devs = devs[:n_pieces]          # one concurrent slot (host thread) per entry
+    # a plan holds at most max_shifts_per_plan() shifts (the 1D solver's lane
+    # tile, COCG's 32-bit element offsets): more pieces when K exceeds it
+    n_pieces = max(n_pieces, -(-k // max_shifts_per_plan(indptr, indices, solver)))
     pieces = [list(map(int, c)) for c in np.array_split(np.arange(k), n_pieces) if len(c)]
     piece_devs = [devs[q % len(devs)] for q in range(len(pieces))]
     args = (indptr, indices, a_re, a_im, b_re, shifts, weights, tau, solver, refine, tol, max_iters,

@@ -154,3 +154,24 @@ def test_wide_shift_counts_vs_truth(k, refine):
     truth = orc.step(u, "truth")
     floor = rel_l2(orc.step(u, "reference"), truth)
     assert rel_l2(u1, truth) <= (1e-9 if refine else 10 * floor + 1e-9), (rel_l2(u1, truth), floor)
+
+
+def test_more_shifts_than_one_plan_takes():
+    """K = 300 > the 1D solver's 256-lane tile: rexi_prepare splits into more
+    pieces (double-double partials combined in order) instead of refusing"""
+    from paper_1912_03312_b200 import fixtures, rexi_prepare, rexi_step
+    from paper_1912_03312_b200.types import PartialFractionApproximation
+    from oracle.oracle import OraclePlan, rel_l2
+    sysm = _system(300)
+    a = fixtures.load_poles(128)
+    rng = np.random.default_rng(1)
+    s = np.concatenate([np.asarray(a.shifts), np.asarray(a.shifts) * (1.0 + 0.01j),
+                        np.asarray(a.shifts)[:44] * (1.0 - 0.013j)])
+    w = np.concatenate([np.asarray(a.weights)] * 2 + [np.asarray(a.weights)[:44]]) / 3.0
+    ap = PartialFractionApproximation(s, w, a.domain_radius, 0.0)
+    u = rng.standard_normal(300) + 1j * rng.standard_normal(300)
+    stp = rexi_prepare(sysm, ap, 1e-3, sr_value=1.0, override_admissibility=True)
+    assert len(stp.plans) >= 2 and stp.solver == "tridiag"
+    u1 = rexi_step(stp, u)
+    stp.close()
+    assert rel_l2(u1, OraclePlan(sysm, ap, 1e-3).step(u, "truth")) <= 1e-9
