@@ -317,6 +317,134 @@ __global__ void __launch_bounds__(NT, 1) k_tmawin(const double *__restrict__ ta,
     }
 }
 
+// full-width windows (all 64 lanes: a window of 34 consecutive rows is ONE
+// contiguous 34 KB range -> 3 bulk copies per claim), single buffer per CTA,
+// 2 CTAs/SM; the next claim's copies are issued as soon as every warp is done
+// reading the window (after the claim's last gather), overlapping this
+// claim's p/q traffic and the other CTA's work
+template <int DB>
+__global__ void __launch_bounds__(256, DB ? 1 : 2) k_tma64(const double *__restrict__ ta, const double *__restrict__ tb,
+                                                  const c128 *__restrict__ z, c128 *__restrict__ p,
+                                                  c128 *__restrict__ q, c128 beta, c128 sg, int nclaims,
+                                                  c128 *part) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm);
+    c128 *win = reinterpret_cast<c128 *>(sm + 128);       // [DB+1][3][34][KP]
+    __shared__ c128 sbp[8 * KP];
+    const int lane = threadIdx.x & 63, slot = threadIdx.x >> 6;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int claim, int b) {
+        const int R0 = claim * 32;
+        uint32_t bytes = 0;
+        int lo[3], cnt[3];
+        for (int w = 0; w < 3; ++w) {
+            const int base = R0 - 1 + (w - 1) * NS;
+            lo[w] = base < 0 ? 0 : base;
+            const int hi = min(base + 34, N);
+            cnt[w] = hi > lo[w] ? hi - lo[w] : 0;
+            bytes += cnt[w] * KP * 16;
+        }
+        mbar_expect_tx(bar + b, bytes);
+        for (int w = 0; w < 3; ++w) {
+            const int base = R0 - 1 + (w - 1) * NS;
+            if (cnt[w]) bulk_g2s(win + ((size_t)b * 3 * 34 + w * 34 + (lo[w] - base)) * KP, z + (size_t)lo[w] * KP,
+                                 cnt[w] * KP * 16, bar + b);
+        }
+    };
+    int claim = blockIdx.x;
+    if (threadIdx.x == 0 && claim < nclaims) issue(claim, 0);
+    uint32_t ph[2] = {0, 0};
+    int b = 0;
+    for (; claim < nclaims; claim += gridDim.x) {
+        const int R0 = claim * 32;
+        c128 po[8], qo[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = R0 + slot + 4 * k;
+            const size_t o = (size_t)min(i, N - 1) * KP + lane;
+            po[k] = p[o];
+            qo[k] = q[o];
+        }
+        if (DB && threadIdx.x == 0 && claim + (int)gridDim.x < nclaims) issue(claim + gridDim.x, b ^ 1);
+        mbar_wait(bar + b, ph[b]);
+        ph[b] ^= 1u;
+        const c128 *wb = win + (size_t)b * 3 * 34 * KP;
+        c128 mu[2] = {cmk(0.0, 0.0), cmk(0.0, 0.0)};
+        c128 pi_[8], qi_[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = R0 + slot + 4 * k;
+            c128 acc = cmk(0.0, 0.0);
+            if (i < N) {
+#pragma unroll
+                for (int e = 0; e < NNZ; ++e) {
+                    int c = i + OFF[e];
+                    int w = OFF[e] < -1 ? 0 : OFF[e] > 1 ? 2 : 1;
+                    if (c < 0 || c >= N) { c = i; w = 1; }
+                    const int rr = c - (R0 - 1 + (w - 1) * NS);
+                    const c128 zz = wb[(w * 34 + rr) * KP + lane];
+                    const double a = __ldg(ta + (size_t)i * NNZ + e), bb = __ldg(tb + (size_t)i * NNZ + e);
+                    const c128 en = cmk(a + sg.y * bb, -(sg.x * bb));
+                    acc = cadd(acc, cmul(en, zz));
+                }
+            }
+            const c128 zi = wb[(34 + (i - R0 + 1)) * KP + lane];
+            pi_[k] = cadd(zi, cmul(beta, po[k]));
+            qi_[k] = cadd(acc, cmul(beta, qo[k]));
+            mu[k >> 2] = cadd(mu[k >> 2], cmul(pi_[k], qi_[k]));
+        }
+        __syncthreads();                 // window b fully read
+        if (!DB && threadIdx.x == 0 && claim + (int)gridDim.x < nclaims) issue(claim + gridDim.x, b);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = R0 + slot + 4 * k;
+            if (i < N) {
+                const size_t o = (size_t)i * KP + lane;
+                p[o] = pi_[k];
+                q[o] = qi_[k];
+            }
+        }
+        sbp[(slot * 2 + 0) * KP + lane] = mu[0];
+        sbp[(slot * 2 + 1) * KP + lane] = mu[1];
+        __syncthreads();
+        if (threadIdx.x < KP) {
+            c128 t = cmk(0.0, 0.0);
+            for (int s2 = 0; s2 < 8; ++s2) t = cadd(t, sbp[s2 * KP + threadIdx.x]);
+            part[(size_t)claim * KP + threadIdx.x] = t;
+        }
+        if (DB) b ^= 1;
+    }
+}
+
+template <int DB>
+static float run_t64(const double *ta, const double *tb, const c128 *z, c128 *p, c128 *q, c128 *part, int sms) {
+    const int nclaims = (N + 31) / 32;
+    const size_t sm = 128 + (DB + 1) * 3 * 34 * KP * sizeof(c128);
+    cudaFuncSetAttribute(k_tma64<DB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const c128 beta = make_double2(0.3, 0.1), sg = make_double2(1.5, -2.0);
+    const int grid = sms * (DB ? 1 : 2);
+    k_tma64<DB><<<grid, 256, sm>>>(ta, tb, z, p, q, beta, sg, nclaims, part);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        k_tma64<DB><<<grid, 256, sm>>>(ta, tb, z, p, q, beta, sg, nclaims, part);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    return best;
+}
+
 template <int NT>
 static float run_tw(const double *ta, const double *tb, const c128 *z, c128 *p, c128 *q, c128 *part, int sms) {
     const int nitems = ((N + 31) / 32) * 2;
@@ -422,6 +550,10 @@ int main() {
         cudaFree(p2);
         cudaFree(x);
     }
+    const float t64 = run_t64<0>(ta, tb, z, p, q, part, sms);
+    const float t64d = run_t64<1>(ta, tb, z, p, q, part, sms);
+    printf("TMA64 single-buffer 2 CTA/SM %.3f ms | double-buffer 1 CTA/SM %.3f ms (vs RED %.3f)\n", t64, t64d,
+           run<RED>(ta, tb, ix, z, p, q, part, sms));
     const float tw = run_tw<256>(ta, tb, z, p, q, part, sms);
     printf("%-7s %8.3f ms  %7.0f GB/s\n", "TMAWIN", tw, bytes / (tw * 1e-3) / 1e9);
     for (int m = 0; m < 8; ++m)
