@@ -144,8 +144,11 @@ def _cheb_native(stepper: ChebyshevStepper, u, n_steps: int):
         import torch
         if not u.is_cuda:
             return torch.from_numpy(_cheb_native(stepper, u.detach().cpu().numpy(), n_steps))
-        u_t = u.to(torch.complex128).contiguous()
+        dev = torch.device("cuda", stepper.device)
+        u_t = u.to(device=dev, dtype=torch.complex128).contiguous()
         out = torch.empty_like(u_t)
+        # u_t was produced on torch's current stream: order the pencil's stream after it
+        stepper.pencil.wait_stream(torch.cuda.current_stream(dev).cuda_stream)
         stepper.pencil.cheb_step(stepper.coeffs, stepper.scale, u_t.data_ptr(), out.data_ptr(),
                                  n_steps, _native.MEM_DEVICE, st)
     else:

@@ -128,3 +128,22 @@ def test_spectral_radius_full_size_2d():
     cfg = fixtures.build_config(3)
     est = spectral_radius_estimate(cfg.system)
     assert 0.5 * cfg.sr <= float(est) <= 1.05 * cfg.sr
+
+
+def test_chebyshev_torch_input_from_a_side_stream():
+    """a CUDA tensor produced on a non-default torch stream is consumed after
+    that stream's work (the pencil's stream waits on torch's current one)"""
+    import torch
+    from paper_1912_03312_b200 import chebyshev_prepare, chebyshev_step
+    d, sysm = load_cheb("cheb_cfg1")
+    cs = chebyshev_prepare(sysm, float(d["tau"]), sr_value=float(d["sr"]), override_admissibility=True)
+    ref = chebyshev_step(cs, sysm, d["u0"])
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        big = torch.randn(1 << 24, device="cuda")
+        for _ in range(20):
+            big = big * 1.0000001          # keep the side stream busy
+        u = torch.from_numpy(d["u0"]).to("cuda", non_blocking=False) * 1.0
+        out = chebyshev_step(cs, sysm, u)
+        torch.cuda.current_stream().synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref)
