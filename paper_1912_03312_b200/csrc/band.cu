@@ -48,7 +48,9 @@ struct BandDev {
     const double *ta, *tai, *bb;   // [(2B+1)][npad]: fl(tau a), fl(tau a_im), b of entry (r, r+d)
     c128 *lo, *up, *dinv;          // interior factors: [npad][B][kp], [npad][B][kp], [npad][kp]
     c128 *spk;                     // spikes [P][4][B*B][kp]: Etop, Ebot, Ftop, Fbot
-    c128 *rl, *rdi, *ru;           // interface block LU [P][B*B][kp]: L_p, Dh_p^-1, R_{p,p+1}
+    c128 *rl, *rdi, *ru;           // interface system [P][B*B][kp]: A_j, D_j^-1, C_j at the level block j
+                                   // is eliminated (block cyclic reduction; j = p - 1)
+    c128 *ral, *rga;               // BCR multipliers of the survivors [sum_l ns_l][B*B][kp]
     c128 *gcon;                    // reduced-rhs pieces [P][2][B][kp]
     c128 *xg;                      // interface solution [P][B][kp]
     c128 *X;                       // sweep scratch [npad][kp]
@@ -335,15 +337,31 @@ __device__ __forceinline__ void couplings(const BandDev &D, int p, c128 sg, c128
         }
 }
 
-// ---- prepare: the interface system's twisted block LU, one thread per shift --
-// The block-tridiagonal interface system  A_p x_{p-1} + D_p x_p + C_p x_{p+1}
-// = g_p  (p = 1 .. P-1) is eliminated from both ends towards a middle block m
-// (a "twisted" factorization), so a solve runs two dependent chains of half
-// the length side by side.  Per block (rl, rdi, ru):
-//   p < m (top):     L_p = A_p Dh_{p-1}^-1, Dh_p^-1, C_p       (Dh_p = D_p - L_p C_{p-1})
-//   p > m (bottom):  U_p = C_p Eh_{p+1}^-1, Eh_p^-1, A_p       (Eh_p = D_p - U_p A_{p+1})
-//   p = m:           L_m, Dmid^-1, U_m                          (Dmid = D_m - L_m C_{m-1} - U_m A_{m+1})
-__host__ __device__ inline int band_mid(int P) { return P - 1 <= 2 ? P - 1 : 1 + (P - 1) / 2; }
+// ---- prepare: the interface system's block cyclic reduction, one thread per shift
+// The block-tridiagonal interface system  A_j x_{j-1} + D_j x_j + C_j x_{j+1} = g_j
+// (j = p - 1 = 0 .. nb-1, nb = P - 1) is reduced odd-even: at level l (h = 2^l)
+// the active blocks are the multiples of h, those with j/h odd are eliminated
+// through their neighbours j +- h (multiples of 2h, the survivors), and a
+// survivor s takes  alpha_s = -A_s D_{s-h}^-1,  gamma_s = -C_s D_{s+h}^-1,
+//   A_s <- alpha_s A_{s-h},  C_s <- gamma_s C_{s+h},
+//   D_s <- D_s + alpha_s C_{s-h} + gamma_s A_{s+h},  g_s <- g_s + alpha_s g_{s-h} + gamma_s g_{s+h}.
+// Block 0 is left at the top; the back substitution runs the levels down:
+//   x_e = D_e^-1 (g_e - A_e x_{e-h} - C_e x_{e+h}).
+// A solve is 2 ceil(log2 nb) dependent levels instead of a chain over the
+// blocks.  Stored: per block its (A, D^-1, C) at its elimination level (rl,
+// rdi, ru); per (level, survivor) alpha and gamma (ral, rga, compact).
+__host__ __device__ inline int bcr_levels(int nb) {
+    int L = 0;
+    while ((1 << L) < nb) ++L;
+    return L;
+}
+// survivors of level l: multiples of 2^(l+1) in [0, nb)
+__host__ __device__ inline int bcr_nsurv(int nb, int l) { return (nb - 1) / (2 << l) + 1; }
+__host__ __device__ inline int bcr_off(int nb, int l) {
+    int o = 0;
+    for (int q = 0; q < l; ++q) o += bcr_nsurv(nb, q);
+    return o;
+}
 
 template <int B>
 __device__ __forceinline__ void band_blocks(const BandDev &D, int p, c128 sg, int lane, c128 (&Dp)[B][B],
@@ -374,74 +392,92 @@ __device__ __forceinline__ void band_blocks(const BandDev &D, int p, c128 sg, in
 }
 
 template <int B>
+__device__ __forceinline__ void ldm(c128 (&m)[B][B], const c128 *base, int kp, int lane) {
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int j = 0; j < B; ++j) m[i][j] = base[(size_t)(i * B + j) * kp + lane];
+}
+
+template <int B>
 __global__ void k_band_rfactor(BandDev D, ShiftDev S, double *pstat) {
     const int lane = blockIdx.x * blockDim.x + threadIdx.x;
     if (lane >= D.kp) return;
-    const int kp = D.kp, P = D.P, m = band_mid(P);
+    const int kp = D.kp, nb = D.P - 1;
+    if (nb < 1) return;
     const c128 sg = S.sigma[lane];
     double pmin = INFINITY;
     auto note = [&](double pv) { pmin = isfinite(pv) ? fmin(pmin, pv) : 0.0; };
-    c128 Dp[B][B], Cp[B][B], Ap[B][B], T0[B][B], inv[B][B];
-    // bottom part, p = P-1 .. m+1
-    c128 einv_next[B][B], a_next[B][B];
-    for (int p = P - 1; p > m; --p) {
-        band_blocks<B>(D, p, sg, lane, Dp, Cp, Ap);
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-            for (int j = 0; j < B; ++j) T0[i][j] = cmk(0.0, 0.0);
-        if (p + 1 < P) {
-            mm<B>(T0, Cp, einv_next);       // U_p = C_p Eh_{p+1}^-1
-            mm_sub<B>(Dp, T0, a_next);      // Eh_p = D_p - U_p A_{p+1}
-        }
-        note(inv_bb<B>(Dp, inv));
-        store_bb<B>(T0, D.rl + (size_t)p * B * B * kp, kp, lane);
-        store_bb<B>(inv, D.rdi + (size_t)p * B * B * kp, kp, lane);
-        store_bb<B>(Ap, D.ru + (size_t)p * B * B * kp, kp, lane);
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-            for (int j = 0; j < B; ++j) {
-                einv_next[i][j] = inv[i][j];
-                a_next[i][j] = Ap[i][j];
-            }
+    auto at = [&](c128 *arr, int j) { return arr + (size_t)(j + 1) * B * B * kp; };
+    // level-0 blocks: A in rl, D in rdi (inverted at elimination), C in ru
+    for (int j = 0; j < nb; ++j) {
+        c128 Dp[B][B], Cp[B][B], Ap[B][B];
+        band_blocks<B>(D, j + 1, sg, lane, Dp, Cp, Ap);
+        store_bb<B>(Ap, at(D.rl, j), kp, lane);
+        store_bb<B>(Dp, at(D.rdi, j), kp, lane);
+        store_bb<B>(Cp, at(D.ru, j), kp, lane);
     }
-    // top part, p = 1 .. m
-    c128 dinv_prev[B][B], c_prev[B][B];
-    for (int p = 1; p <= m; ++p) {
-        band_blocks<B>(D, p, sg, lane, Dp, Cp, Ap);
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-            for (int j = 0; j < B; ++j) T0[i][j] = cmk(0.0, 0.0);
-        if (p >= 2) {
-            mm<B>(T0, Ap, dinv_prev);       // L_p = A_p Dh_{p-1}^-1
-            mm_sub<B>(Dp, T0, c_prev);      // Dh_p = D_p - L_p C_{p-1}
+    const int L = bcr_levels(nb);
+    for (int l = 0; l < L; ++l) {
+        const int h = 1 << l;
+        // the eliminated blocks of this level: D^-1 in place
+        for (int e = h; e < nb; e += 2 * h) {
+            c128 Dm[B][B], inv[B][B];
+            ldm<B>(Dm, at(D.rdi, e), kp, lane);
+            note(inv_bb<B>(Dm, inv));
+            store_bb<B>(inv, at(D.rdi, e), kp, lane);
         }
-        if (p == m && m + 1 < P) {          // the middle also takes the bottom part's Schur term
-            c128 U[B][B];
-            mm<B>(U, Cp, einv_next);        // U_m = C_m Eh_{m+1}^-1
-            mm_sub<B>(Dp, U, a_next);       // Dmid = Dh_m - U_m A_{m+1}
+        // the survivors: multipliers and updated blocks
+        for (int s2 = 0; s2 < nb; s2 += 2 * h) {
+            c128 As[B][B], Cs[B][B], Ds[B][B], al[B][B], ga[B][B], t[B][B], m[B][B], nA[B][B], nC[B][B];
+            ldm<B>(As, at(D.rl, s2), kp, lane);
+            ldm<B>(Ds, at(D.rdi, s2), kp, lane);
+            ldm<B>(Cs, at(D.ru, s2), kp, lane);
 #pragma unroll
             for (int i = 0; i < B; ++i)
 #pragma unroll
-                for (int j = 0; j < B; ++j) Cp[i][j] = U[i][j];   // stored in ru for the middle
-        }
-        note(inv_bb<B>(Dp, inv));
-        store_bb<B>(T0, D.rl + (size_t)p * B * B * kp, kp, lane);
-        store_bb<B>(inv, D.rdi + (size_t)p * B * B * kp, kp, lane);
-        store_bb<B>(Cp, D.ru + (size_t)p * B * B * kp, kp, lane);
+                for (int j = 0; j < B; ++j) {
+                    al[i][j] = ga[i][j] = nA[i][j] = nC[i][j] = cmk(0.0, 0.0);
+                }
+            if (s2 - h >= 0) {
+                ldm<B>(m, at(D.rdi, s2 - h), kp, lane);          // D_{s-h}^-1
+                mm_sub<B>(al, As, m);                          // alpha = -A_s D_{s-h}^-1
+                ldm<B>(t, at(D.ru, s2 - h), kp, lane);            // C_{s-h}
+                mm<B>(m, al, t);
 #pragma unroll
-        for (int i = 0; i < B; ++i)
+                for (int i = 0; i < B; ++i)
 #pragma unroll
-            for (int j = 0; j < B; ++j) {
-                dinv_prev[i][j] = inv[i][j];
-                c_prev[i][j] = Cp[i][j];
+                    for (int j = 0; j < B; ++j) Ds[i][j] = cadd(Ds[i][j], m[i][j]);
+                ldm<B>(t, at(D.rl, s2 - h), kp, lane);            // A_{s-h}
+                mm<B>(nA, al, t);
             }
+            if (s2 + h < nb) {
+                ldm<B>(m, at(D.rdi, s2 + h), kp, lane);          // D_{s+h}^-1
+                mm_sub<B>(ga, Cs, m);                          // gamma = -C_s D_{s+h}^-1
+                ldm<B>(t, at(D.rl, s2 + h), kp, lane);            // A_{s+h}
+                mm<B>(m, ga, t);
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) Ds[i][j] = cadd(Ds[i][j], m[i][j]);
+                ldm<B>(t, at(D.ru, s2 + h), kp, lane);            // C_{s+h}
+                mm<B>(nC, ga, t);
+            }
+            const int k = bcr_off(nb, l) + s2 / (2 * h);
+            store_bb<B>(al, D.ral + (size_t)k * B * B * kp, kp, lane);
+            store_bb<B>(ga, D.rga + (size_t)k * B * B * kp, kp, lane);
+            store_bb<B>(nA, at(D.rl, s2), kp, lane);
+            store_bb<B>(Ds, at(D.rdi, s2), kp, lane);
+            store_bb<B>(nC, at(D.ru, s2), kp, lane);
+        }
     }
-    if (P > 1)
-        atomicMin(reinterpret_cast<unsigned long long *>(pstat) + lane,
-                  (unsigned long long)__double_as_longlong(pmin));
+    {   // the top block
+        c128 Dm[B][B], inv[B][B];
+        ldm<B>(Dm, at(D.rdi, 0), kp, lane);
+        note(inv_bb<B>(Dm, inv));
+        store_bb<B>(inv, at(D.rdi, 0), kp, lane);
+    }
+    atomicMin(reinterpret_cast<unsigned long long *>(pstat) + lane, (unsigned long long)__double_as_longlong(pmin));
 }
 
 // ---- step kernels ----------------------------------------------------------
@@ -515,120 +551,81 @@ __global__ void k_band_s1(BandDev D, ShiftDev S, const c128 *__restrict__ rsh, c
     }
 }
 
-// twisted interface solve for one shift; blk(p, which) returns block p's
-// stored matrix (0: rl, 1: rdi, 2: ru), g(p) its reduced rhs, hs(p) a scratch
-// vector slot and xs(p) the output slot.  part: 0 = both halves in this
-// thread, 1 = top half only, 2 = bottom half only, 3 = neither (a thread
-// that only joins the two sync() calls: after the eliminations, where the top
-// half solves the middle block, and before the back substitutions)
-template <int B, typename Blk, typename G, typename Hs, typename Xs, typename Sync>
-__device__ __forceinline__ void twisted_solve(int P, int part, Blk blk, G g, Hs hs, Xs xs, Sync sync) {
-    const int m = band_mid(P);
-    const bool top = part == 0 || part == 1, bot = part == 0 || part == 2;
-    c128 M0[B][B];
-    c128 h[B], v[B];
-    if (top) {                   // top: h_p = g_p - L_p h_{p-1}, p = 1 .. m-1
+// block-cyclic-reduction solve of the interface system for one shift.  The
+// caller supplies accessors: A(j)/Di(j)/C(j) -> B x B blocks, al(k)/ga(k) ->
+// the level multipliers (compact index), g(j)/x(j) -> B-vector slots (g is
+// reduced in place); thread tid of nthr cooperating threads, sync() between
+// levels
+template <int B, typename MA, typename MDi, typename MC, typename MAl, typename MGa, typename VG, typename VX,
+          typename Sync>
+__device__ __forceinline__ void bcr_solve(int nb, int tid, int nthr, MA A, MDi Di, MC C, MAl al, MGa ga, VG g, VX x,
+                                          Sync sync) {
+    const int L = bcr_levels(nb);
+    for (int l = 0; l < L; ++l) {
+        const int h = 1 << l, off = bcr_off(nb, l);
+        for (int s2 = 2 * h * tid; s2 < nb; s2 += 2 * h * nthr) {
+            c128 v[B], M0[B][B];
 #pragma unroll
-        for (int i = 0; i < B; ++i) h[i] = cmk(0.0, 0.0);
-        for (int p = 1; p < m; ++p) {
-            g(p, v);
-            if (p >= 2) {
-                blk(p, 0, M0);
-#pragma unroll
-                for (int i = 0; i < B; ++i)
-#pragma unroll
-                    for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], h[j]);
-            }
-#pragma unroll
-            for (int i = 0; i < B; ++i) {
-                h[i] = v[i];
-                hs(p)[i] = v[i];
-            }
-        }
-    }
-    if (bot) {                   // bottom: f_p = g_p - U_p f_{p+1}, p = P-1 .. m+1
-#pragma unroll
-        for (int i = 0; i < B; ++i) h[i] = cmk(0.0, 0.0);
-        for (int p = P - 1; p > m; --p) {
-            g(p, v);
-            if (p + 1 < P) {
-                blk(p, 0, M0);
+            for (int i = 0; i < B; ++i) v[i] = g(s2)[i];
+            if (s2 - h >= 0) {
+                al(off + s2 / (2 * h), M0);
 #pragma unroll
                 for (int i = 0; i < B; ++i)
 #pragma unroll
-                    for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], h[j]);
+                    for (int j = 0; j < B; ++j) v[i] = cadd(v[i], cmul(M0[i][j], g(s2 - h)[j]));
+            }
+            if (s2 + h < nb) {
+                ga(off + s2 / (2 * h), M0);
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) v[i] = cadd(v[i], cmul(M0[i][j], g(s2 + h)[j]));
             }
 #pragma unroll
-            for (int i = 0; i < B; ++i) {
-                h[i] = v[i];
-                hs(p)[i] = v[i];
-            }
+            for (int i = 0; i < B; ++i) g(s2)[i] = v[i];
         }
+        sync();
     }
-    sync();
-    if (top) {                   // middle: x_m = Dmid^-1 (g_m - L_m h_{m-1} - U_m f_{m+1})
-        g(m, v);
-        if (m >= 2) {
-            blk(m, 0, M0);
-#pragma unroll
-            for (int i = 0; i < B; ++i)
-#pragma unroll
-                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], hs(m - 1)[j]);
-        }
-        if (m + 1 < P) {
-            blk(m, 2, M0);
-#pragma unroll
-            for (int i = 0; i < B; ++i)
-#pragma unroll
-                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], hs(m + 1)[j]);
-        }
-        blk(m, 1, M0);
+    if (tid == 0) {
+        c128 M0[B][B];
+        Di(0, M0);
 #pragma unroll
         for (int i = 0; i < B; ++i) {
             c128 t = cmk(0.0, 0.0);
 #pragma unroll
-            for (int j = 0; j < B; ++j) t = cadd(t, cmul(M0[i][j], v[j]));
-            xs(m)[i] = t;
+            for (int j = 0; j < B; ++j) t = cadd(t, cmul(M0[i][j], g(0)[j]));
+            x(0)[i] = t;
         }
     }
     sync();
-    if (top) {                   // x_p = Dh_p^-1 (h_p - C_p x_{p+1}), p = m-1 .. 1
-        for (int p = m - 1; p >= 1; --p) {
+    for (int l = L - 1; l >= 0; --l) {
+        const int h = 1 << l;
+        for (int e = h + 2 * h * tid; e < nb; e += 2 * h * nthr) {
+            c128 v[B], M0[B][B];
 #pragma unroll
-            for (int i = 0; i < B; ++i) v[i] = hs(p)[i];
-            blk(p, 2, M0);
+            for (int i = 0; i < B; ++i) v[i] = g(e)[i];
+            A(e, M0);
 #pragma unroll
             for (int i = 0; i < B; ++i)
 #pragma unroll
-                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], xs(p + 1)[j]);
-            blk(p, 1, M0);
+                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], x(e - h)[j]);
+            if (e + h < nb) {
+                C(e, M0);
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], x(e + h)[j]);
+            }
+            Di(e, M0);
 #pragma unroll
             for (int i = 0; i < B; ++i) {
                 c128 t = cmk(0.0, 0.0);
 #pragma unroll
                 for (int j = 0; j < B; ++j) t = cadd(t, cmul(M0[i][j], v[j]));
-                xs(p)[i] = t;
+                x(e)[i] = t;
             }
         }
-    }
-    if (bot) {                   // x_p = Eh_p^-1 (f_p - A_p x_{p-1}), p = m+1 .. P-1
-        for (int p = m + 1; p < P; ++p) {
-#pragma unroll
-            for (int i = 0; i < B; ++i) v[i] = hs(p)[i];
-            blk(p, 2, M0);
-#pragma unroll
-            for (int i = 0; i < B; ++i)
-#pragma unroll
-                for (int j = 0; j < B; ++j) v[i] = cfnma(v[i], M0[i][j], xs(p - 1)[j]);
-            blk(p, 1, M0);
-#pragma unroll
-            for (int i = 0; i < B; ++i) {
-                c128 t = cmk(0.0, 0.0);
-#pragma unroll
-                for (int j = 0; j < B; ++j) t = cadd(t, cmul(M0[i][j], v[j]));
-                xs(p)[i] = t;
-            }
-        }
+        sync();
     }
 }
 
@@ -644,22 +641,27 @@ template <int B>
 __global__ void k_band_red(BandDev D, const c128 *__restrict__ rsh, const c128 *__restrict__ rps) {
     const int lane = blockIdx.x * blockDim.x + threadIdx.x;
     if (lane >= D.kp) return;
-    const int kp = D.kp, M = D.M;
-    c128 *const mats[3] = {D.rl, D.rdi, D.ru};
-    twisted_solve<B>(
-        D.P, 0,
-        [&](int p, int which, c128 (&o)[B][B]) { load_bb<B>(o, mats[which] + (size_t)p * B * B * kp, kp, lane); },
-        [&](int p, c128 (&v)[B]) {
-            const c128 *gprev = D.gcon + ((size_t)(p - 1) * 2 * B + B) * kp;
-            const c128 *gcur = D.gcon + (size_t)p * 2 * B * kp;
+    const int kp = D.kp, M = D.M, nb = D.P - 1;
+    if (nb < 1) return;
+    // g_j in the sweep scratch (D.X), x_j in xg (block p = j + 1)
+    for (int j = 0; j < nb; ++j) {
+        const int p = j + 1;
+        const c128 *gprev = D.gcon + ((size_t)(p - 1) * 2 * B + B) * kp;
+        const c128 *gcur = D.gcon + (size_t)p * 2 * B * kp;
 #pragma unroll
-            for (int i = 0; i < B; ++i)
-                v[i] = csub(csub(rhs_at<B>(D, rsh, rps, (int64_t)p * M + i, lane), __ldg(gprev + (size_t)i * kp + lane)),
-                            __ldg(gcur + (size_t)i * kp + lane));
-        },
-        // h / f live in xg until the back substitution overwrites them in order
-        [&](int p) { return StridedVec{D.X + (size_t)p * B * kp + lane, kp}; },
-        [&](int p) { return StridedVec{D.xg + (size_t)p * B * kp + lane, kp}; }, [] {});
+        for (int i = 0; i < B; ++i)
+            D.X[((size_t)j * B + i) * kp + lane] =
+                csub(csub(rhs_at<B>(D, rsh, rps, (int64_t)p * M + i, lane), __ldg(gprev + (size_t)i * kp + lane)),
+                     __ldg(gcur + (size_t)i * kp + lane));
+    }
+    auto blk = [&](const c128 *arr, int j, c128 (&o)[B][B]) { load_bb<B>(o, arr + (size_t)(j + 1) * B * B * kp, kp, lane); };
+    bcr_solve<B>(
+        nb, 0, 1, [&](int j, c128 (&o)[B][B]) { blk(D.rl, j, o); }, [&](int j, c128 (&o)[B][B]) { blk(D.rdi, j, o); },
+        [&](int j, c128 (&o)[B][B]) { blk(D.ru, j, o); },
+        [&](int k, c128 (&o)[B][B]) { load_bb<B>(o, D.ral + (size_t)k * B * B * kp, kp, lane); },
+        [&](int k, c128 (&o)[B][B]) { load_bb<B>(o, D.rga + (size_t)k * B * B * kp, kp, lane); },
+        [&](int j) { return StridedVec{D.X + (size_t)j * B * kp + lane, kp}; },
+        [&](int j) { return StridedVec{D.xg + (size_t)(j + 1) * B * kp + lane, kp}; }, [] {});
 }
 
 // interior solves with the interface values known -> x (all rows) in Xout
@@ -765,7 +767,10 @@ __global__ void k_band_accum(int64_t n, int kp, int k, const c128 *__restrict__ 
 // rows and rhs into shared memory (independent coalesced loads, ~one memory
 // latency), then one thread per lane runs the dependent sweeps out of shared
 // memory instead of paying an HBM/L2 round trip every few rows.
-constexpr int BLG = 16;
+#ifndef BAND_BLG
+#define BAND_BLG 8   // swept (scripts/tune_blg.sh, P2 acceptance step): 16: 45.5 us, 8: 43.7, 4: 43.6
+#endif
+constexpr int BLG = BAND_BLG;
 constexpr int BST_NT = 256;
 
 template <int B>
@@ -904,76 +909,87 @@ __global__ void __launch_bounds__(BST_NT) k_band_s3_st(BandDev D, ShiftDev S, co
         for (int i = 0; i < B; ++i) Xout[(size_t)(ga + i) * kp + lane] = xa[i];
 }
 
-// interface system, a CTA per RLG shifts: all threads stage the shifts' block
-// LU pieces and reduced-rhs pieces in shared memory (RLG-lane runs of each
-// (block, coefficient) row are contiguous), then one thread per shift runs the
-// forward / backward chain out of shared memory; h goes to its own array so
-// the next block's loads are not ordered behind this block's stores
-constexpr int RLG = 4;
+// interface system, a CTA per rlg(B) shifts: all threads stage the shifts'
+// BCR blocks, multipliers and reduced rhs in shared memory (cp.async, every
+// copy in flight), then the CTA's threads split each level's blocks among
+// themselves (256 / rlg threads per shift, a barrier between levels)
+template <int B>
+__host__ __device__ constexpr int band_rlg() { return 1; }   // swept (P2 acceptance): 4 lanes per CTA 27.0 us, 1 lane 18.7 us
+template <int B>
+__host__ __device__ inline size_t band_red_lane_elems(int P) {
+    const int nb = P > 1 ? P - 1 : 1;
+    return (size_t)nb * (3 * B * B + 2 * B) + (size_t)bcr_off(nb, bcr_levels(nb)) * 2 * B * B;
+}
 template <int B>
 __host__ __device__ inline size_t band_red_smem(int P) {
-    const size_t np = (size_t)(P > 1 ? P - 1 : 1);
-    return np * RLG * sizeof(c128) * (3 * B * B + 3 * B + 2 * B);
+    return band_red_lane_elems<B>(P) * band_rlg<B>() * sizeof(c128);
 }
 
 template <int B>
 __global__ void __launch_bounds__(256) k_band_red_st(BandDev D, const c128 *__restrict__ rsh,
                                                      const c128 *__restrict__ rps) {
     extern __shared__ __align__(16) unsigned char bsm[];
-    const int lane0 = blockIdx.x * RLG;
-    const int kp = D.kp, M = D.M, P = D.P;
-    const int lg = min(RLG, kp - lane0);
-    constexpr int W = 3 * B * B + 3 * B;   // per block: L|U, Dinv|Einv, C|A, (rhs, gprev, gcur)
-    c128 *sm = reinterpret_cast<c128 *>(bsm);                 // [P-1][W][RLG]
-    c128 *hsm = sm + (size_t)(P - 1) * W * RLG;               // [P-1][B][RLG]  h / f
-    c128 *xsm = hsm + (size_t)(P - 1) * B * RLG;              // [P-1][B][RLG]  x
-    for (int idx = threadIdx.x; idx < (P - 1) * W * lg; idx += blockDim.x) {
-        const int l = idx % lg, pe = idx / lg;
-        const int p = 1 + pe / W, e = pe % W;
-        const int lane = lane0 + l;
-        const c128 *src;
-        if (e < B * B) src = D.rl + ((size_t)p * B * B + e) * kp + lane;
-        else if (e < 2 * B * B) src = D.rdi + ((size_t)p * B * B + e - B * B) * kp + lane;
-        else if (e < 3 * B * B) src = D.ru + ((size_t)p * B * B + e - 2 * B * B) * kp + lane;
-        else {
-            const int i = (e - 3 * B * B) % B, which = (e - 3 * B * B) / B;
-            if (which == 0) src = rsh ? rsh + (int64_t)p * M + i : rps + ((size_t)p * M + i) * kp + lane;
-            else if (which == 1) src = D.gcon + ((size_t)(p - 1) * 2 * B + B + i) * kp + lane;
-            else src = D.gcon + ((size_t)p * 2 * B + i) * kp + lane;
-        }
-        cp_async16(sm + (size_t)pe * RLG + l, src);
+    constexpr int RL = band_rlg<B>();
+    const int lane0 = blockIdx.x * RL;
+    const int kp = D.kp, M = D.M, nb = D.P - 1;
+    const int lg = min(RL, kp - lane0);
+    const int ns = bcr_off(nb, bcr_levels(nb));
+    const size_t per = band_red_lane_elems<B>(D.P);
+    c128 *sm = reinterpret_cast<c128 *>(bsm);
+    // per lane l: [A | Di | C] nb x 3B^2, [al | ga] ns x 2B^2, g nb x B, x nb x B
+    auto base = [&](int l) { return sm + (size_t)l * per; };
+    const int W3 = 3 * B * B;
+    for (int idx = threadIdx.x; idx < nb * W3 * lg; idx += blockDim.x) {
+        const int l = idx % lg, r = idx / lg;
+        const int j = r / W3, e = r % W3;
+        const c128 *arr = e < B * B ? D.rl : e < 2 * B * B ? D.rdi : D.ru;
+        cp_async16(base(l) + (size_t)j * W3 + e, arr + ((size_t)(j + 1) * B * B + e % (B * B)) * kp + lane0 + l);
+    }
+    for (int idx = threadIdx.x; idx < ns * 2 * B * B * lg; idx += blockDim.x) {
+        const int l = idx % lg, r = idx / lg;
+        const int k = r / (2 * B * B), e = r % (2 * B * B);
+        const c128 *arr = e < B * B ? D.ral : D.rga;
+        cp_async16(base(l) + (size_t)nb * W3 + (size_t)k * 2 * B * B + e,
+                   arr + ((size_t)k * B * B + e % (B * B)) * kp + lane0 + l);
+    }
+    for (int idx = threadIdx.x; idx < nb * B * lg; idx += blockDim.x) {
+        const int l = idx % lg, r = idx / lg;
+        const int j = r / B, i = r % B, p = j + 1, lane = lane0 + l;
+        const c128 *gprev = D.gcon + ((size_t)(p - 1) * 2 * B + B) * kp;
+        const c128 *gcur = D.gcon + (size_t)p * 2 * B * kp;
+        base(l)[(size_t)nb * W3 + (size_t)ns * 2 * B * B + (size_t)j * B + i] =
+            csub(csub(rhs_at<B>(D, rsh, rps, (int64_t)p * M + i, lane), __ldg(gprev + (size_t)i * kp + lane)),
+                 __ldg(gcur + (size_t)i * kp + lane));
     }
     cp_async_wait_all();
     __syncthreads();
-    // thread l < lg: top half of lane l; thread RLG + l: its bottom half
-    const int t = threadIdx.x;
-    const int l = t < RLG ? t : t - RLG;
-    const int part = (t < RLG && l < lg) ? 1 : (t >= RLG && t < 2 * RLG && l < lg) ? 2 : 3;
-    const int ll = part == 3 ? 0 : l;
-    const c128 *__restrict__ in = sm;
-    twisted_solve<B>(
-        P, part,
-        [&](int p, int which, c128 (&o)[B][B]) {
+    constexpr int TPL = 256 / RL;
+    const int l = threadIdx.x / TPL, tid = threadIdx.x % TPL;
+    const int ll = l < lg ? l : 0;                  // idle lanes still join the barriers
+    const int nthr = l < lg ? TPL : 0;
+    c128 *b0 = base(ll);
+    c128 *gv = b0 + (size_t)nb * W3 + (size_t)ns * 2 * B * B;
+    c128 *xv = gv + (size_t)nb * B;
+    auto mat = [&](const c128 *src, c128 (&o)[B][B]) {
 #pragma unroll
-            for (int i = 0; i < B; ++i)
+        for (int i = 0; i < B; ++i)
 #pragma unroll
-                for (int j = 0; j < B; ++j)
-                    o[i][j] = in[((size_t)(p - 1) * W + which * B * B + i * B + j) * RLG + ll];
-        },
-        [&](int p, c128 (&v)[B]) {
-            const c128 *b = in + (size_t)(p - 1) * W * RLG;
-#pragma unroll
-            for (int i = 0; i < B; ++i)
-                v[i] = csub(csub(b[(3 * B * B + i) * RLG + ll], b[(3 * B * B + B + i) * RLG + ll]),
-                            b[(3 * B * B + 2 * B + i) * RLG + ll]);
-        },
-        [&](int p) { return StridedVec{hsm + (size_t)(p - 1) * B * RLG + ll, RLG}; },
-        [&](int p) { return StridedVec{xsm + (size_t)(p - 1) * B * RLG + ll, RLG}; }, [] { __syncthreads(); });
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < (P - 1) * B * lg; idx += blockDim.x) {
-        const int l2 = idx % lg, pi = idx / lg;
-        const int p = 1 + pi / B, i = pi % B;
-        D.xg[((size_t)p * B + i) * kp + lane0 + l2] = xsm[(size_t)pi * RLG + l2];
+            for (int j = 0; j < B; ++j) o[i][j] = src[i * B + j];
+    };
+    bcr_solve<B>(
+        // an idle lane's threads get tid = nb: no work, but the same barriers
+        nb, nthr ? tid : nb, nthr ? TPL : 1, [&](int j, c128 (&o)[B][B]) { mat(b0 + (size_t)j * W3, o); },
+        [&](int j, c128 (&o)[B][B]) { mat(b0 + (size_t)j * W3 + B * B, o); },
+        [&](int j, c128 (&o)[B][B]) { mat(b0 + (size_t)j * W3 + 2 * B * B, o); },
+        [&](int k, c128 (&o)[B][B]) { mat(b0 + (size_t)nb * W3 + (size_t)k * 2 * B * B, o); },
+        [&](int k, c128 (&o)[B][B]) { mat(b0 + (size_t)nb * W3 + (size_t)k * 2 * B * B + B * B, o); },
+        [&](int j) { return StridedVec{gv + (size_t)j * B, 1}; }, [&](int j) { return StridedVec{xv + (size_t)j * B, 1}; },
+        [] { __syncthreads(); });
+    for (int idx = threadIdx.x; idx < nb * B * lg; idx += blockDim.x) {
+        const int l2 = idx % lg, r = idx / lg;
+        const int j = r / B, i = r % B;
+        const c128 *xs = base(l2) + (size_t)nb * W3 + (size_t)ns * 2 * B * B + (size_t)nb * B;
+        D.xg[((size_t)(j + 1) * B + i) * kp + lane0 + l2] = xs[(size_t)j * B + i];
     }
 }
 
@@ -996,7 +1012,8 @@ cudaError_t solve_chain(BandImpl *im, const ShiftDev &S, cudaStream_t st, const 
     else k_band_s1<B><<<grid, nt, 0, st>>>(D, S, rsh, rps);
     if (hook) hook->end();
     if (hook) hook->begin("band_red", 0.0);
-    if (im->staged && D.P > 1) k_band_red_st<B><<<(D.kp + RLG - 1) / RLG, 256, rsm, st>>>(D, rsh, rps);
+    if (im->staged && D.P > 1)
+        k_band_red_st<B><<<(D.kp + band_rlg<B>() - 1) / band_rlg<B>(), 256, rsm, st>>>(D, rsh, rps);
     else k_band_red<B><<<(D.kp + 31) / 32, 32, 0, st>>>(D, rsh, rps);
     if (hook) hook->end();
     if (hook) hook->begin("band_s3", 16.0 * lane_rows * ((2 * B + 1) + 2) + (rps ? 16.0 * lane_rows : 16.0 * D.npad));
@@ -1048,7 +1065,10 @@ static int band_create_t(BandState &bs, BandImpl *im, const rexi_desc *d, const 
     M = std::max(M, 4 * B);
     // the reference's P2 sizes: blocks of 64 rows whose factors fit shared
     // memory, and an interface chain whose pieces fit one CTA's shared memory
-    constexpr int MST = 64;
+#ifndef BAND_MST
+#define BAND_MST 32   // swept (scripts/tune_mst.sh, P2 acceptance step): 64: 43.7 us, 32: 41.5, 16: 53.7
+#endif
+    constexpr int MST = BAND_MST;
     const int64_t pst = (n + MST - 1) / MST;
     if (!getenv("REXI_BAND_NOSTAGE") && band_red_smem<B>((int)std::min<int64_t>(pst, 1 << 20)) <= 200 * 1024 &&
         band_st_smem<B>(MST, std::min(BLG, kp)) <= 200 * 1024) {
@@ -1096,6 +1116,12 @@ static int band_create_t(BandState &bs, BandImpl *im, const rexi_desc *d, const 
     BA(D.rl, sizeof(c128) * (size_t)P * B * B * kp);
     BA(D.rdi, sizeof(c128) * (size_t)P * B * B * kp);
     BA(D.ru, sizeof(c128) * (size_t)P * B * B * kp);
+    {
+        const int nb = std::max(1, P - 1);
+        const size_t ns = (size_t)std::max(1, bcr_off(nb, bcr_levels(nb)));
+        BA(D.ral, sizeof(c128) * ns * B * B * kp);
+        BA(D.rga, sizeof(c128) * ns * B * B * kp);
+    }
     BA(D.gcon, sizeof(c128) * (size_t)P * 2 * B * kp);
     BA(D.xg, sizeof(c128) * (size_t)P * B * kp);
     BA(D.X, sizeof(c128) * rows_kp);
