@@ -859,20 +859,59 @@ __global__ void __launch_bounds__(BST_NT) k_band_s1_st(BandDev D, ShiftDev S, co
     }
 }
 
+// the beta-weighted dd lane sum of the rows [i0, i1) (k_band_accum's
+// operations, bit for bit), for the last interior pass fused into its kernel
+__device__ __forceinline__ void band_lane_sum(int64_t i0, int64_t i1, int64_t n, int kp, int k,
+                                              const c128 *__restrict__ beta, const c128 *x1, const c128 *x2,
+                                              double *acc, c128 *uout) {
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        if (i >= n) break;
+        ddacc re = {0.0, 0.0}, im = {0.0, 0.0};
+        for (int jj = 0; jj < k; ++jj) {
+            const c128 b = beta[jj];
+            c128 x = x1[(size_t)i * kp + jj];
+            ddacc_add(re, fma(b.x, x.x, -b.y * x.y));
+            ddacc_add(im, fma(b.x, x.y, b.y * x.x));
+            if (x2) {
+                x = x2[(size_t)i * kp + jj];
+                ddacc_add(re, fma(b.x, x.x, -b.y * x.y));
+                ddacc_add(im, fma(b.x, x.y, b.y * x.x));
+            }
+        }
+        const dd sre = fast_two_sum(re.hi, re.lo), sim = fast_two_sum(im.hi, im.lo);
+        if (uout) {
+            uout[i] = cmk(__dadd_rn(sre.hi, sre.lo), __dadd_rn(sim.hi, sim.lo));
+        } else {
+            acc[i] = sre.hi;
+            acc[n + i] = sre.lo;
+            acc[2 * n + i] = sim.hi;
+            acc[3 * n + i] = sim.lo;
+        }
+    }
+}
+
+struct BandFuse {      // the last pass's lane sum, fused into k_band_s3_st (lpc == kp)
+    int on, k;
+    const c128 *beta, *x1;   // x1: the first pass's x when this is the correction pass, else null
+    double *acc;
+    c128 *uout;
+};
+
 template <int B>
 __global__ void __launch_bounds__(BST_NT) k_band_s3_st(BandDev D, ShiftDev S, const c128 *__restrict__ rsh,
-                                                       const c128 *__restrict__ rps, c128 *Xout) {
+                                                       const c128 *__restrict__ rps, c128 *Xout, int lpc,
+                                                       BandFuse fu) {
     extern __shared__ __align__(16) unsigned char bsm[];
-    const int p = blockIdx.x, lane0 = blockIdx.y * BLG;
+    const int p = blockIdx.x, lane0 = blockIdx.y * lpc;
     const int kp = D.kp, M = D.M;
-    const int lg = min(BLG, kp - lane0);
+    const int lg = min(lpc, kp - lane0);
     const int64_t r0 = blk_i0(p, M, B), r1 = (int64_t)(p + 1) * M;
     c128 *f = reinterpret_cast<c128 *>(bsm);
     c128 *rb = f + (size_t)M * (2 * B + 1) * lg;
     c128 *yt = rb + (size_t)M * lg;
     band_stage<B>(D, rsh, rps, r0, r1, lane0, lg, f, rb);
     const int ll = threadIdx.x;
-    if (ll >= lg) return;
+    if (ll < lg) {
     const int lane = lane0 + ll;
     const c128 sg = S.sigma[lane];
     c128 xa[B], xb[B];
@@ -907,6 +946,12 @@ __global__ void __launch_bounds__(BST_NT) k_band_s3_st(BandDev D, ShiftDev S, co
     if (p >= 1)
 #pragma unroll
         for (int i = 0; i < B; ++i) Xout[(size_t)(ga + i) * kp + lane] = xa[i];
+    }
+    if (fu.on) {   // every lane of the block's rows is in this CTA: sum them here
+        __syncthreads();
+        band_lane_sum((int64_t)p * M, (int64_t)(p + 1) * M, D.n, kp, fu.k, fu.beta, fu.x1 ? fu.x1 : Xout,
+                      fu.x1 ? Xout : nullptr, fu.acc, fu.uout);
+    }
 }
 
 // interface system, a CTA per rlg(B) shifts: all threads stage the shifts'
@@ -1001,7 +1046,7 @@ int launch_grid(const BandDev &D) {
 
 template <int B>
 cudaError_t solve_chain(BandImpl *im, const ShiftDev &S, cudaStream_t st, const c128 *rsh, const c128 *rps,
-                        c128 *Xout, int64_t *launches, ProfHook *hook, int kreal) {
+                        c128 *Xout, int64_t *launches, ProfHook *hook, int kreal, BandFuse fu = BandFuse{}) {
     BandDev &D = im->D;
     const int nt = launch_nt(D.kp), grid = launch_grid(D);
     const double lane_rows = (double)D.npad * kreal;
@@ -1017,7 +1062,13 @@ cudaError_t solve_chain(BandImpl *im, const ShiftDev &S, cudaStream_t st, const 
     else k_band_red<B><<<(D.kp + 31) / 32, 32, 0, st>>>(D, rsh, rps);
     if (hook) hook->end();
     if (hook) hook->begin("band_s3", 16.0 * lane_rows * ((2 * B + 1) + 2) + (rps ? 16.0 * lane_rows : 16.0 * D.npad));
-    if (im->staged) k_band_s3_st<B><<<sgrid, BST_NT, ssm, st>>>(D, S, rsh, rps, Xout);
+    if (im->staged) {
+        // the last pass of a step sums the lanes in the same kernel: all of a
+        // block's lanes in one CTA
+        const int lpc = fu.on ? D.kp : BLG;
+        const dim3 g3(D.P, (D.kp + lpc - 1) / lpc);
+        k_band_s3_st<B><<<g3, BST_NT, band_st_smem<B>(D.M, std::min(lpc, D.kp)), st>>>(D, S, rsh, rps, Xout, lpc, fu);
+    }
     else k_band_s3<B><<<grid, nt, 0, st>>>(D, S, rsh, rps, Xout);
     if (hook) hook->end();
     *launches += 3;
@@ -1144,7 +1195,7 @@ static int band_create_t(BandState &bs, BandImpl *im, const rexi_desc *d, const 
         BK(cudaFuncSetAttribute(k_band_s1_st<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)band_st_smem<B>(M, std::min(BLG, kp))));
         BK(cudaFuncSetAttribute(k_band_s3_st<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)band_st_smem<B>(M, std::min(BLG, kp))));
+                                (int)std::min<size_t>(band_st_smem<B>(M, std::max(BLG, kp)), 227 * 1024)));
         BK(cudaFuncSetAttribute(k_band_red_st<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)band_red_smem<B>(P)));
     }
@@ -1188,12 +1239,24 @@ int band_create(BandState &bs, const rexi_desc *d, int B, const ShiftDev &S, int
     }
 }
 
+// the last pass sums the lanes in its own kernel when the staged sweeps hold
+// every lane of a block in one CTA (k_band_s3_st, BandFuse)
+template <int B>
+static bool band_can_fuse(const BandImpl *im) {
+    return im->staged && band_st_smem<B>(im->D.M, im->D.kp) <= 200 * 1024;
+}
+
 template <int B>
 static int band_run(BandState &bs, const ShiftDev &S, cudaStream_t st, int64_t *launches, const c128 **x1,
-                    const c128 **x2, std::string &err) {
+                    const c128 **x2, std::string &err, bool *summed = nullptr, double *acc = nullptr,
+                    c128 *uout = nullptr) {
     BandImpl *im = (BandImpl *)bs.impl;
     BandDev &D = im->D;
-    BK(solve_chain<B>(im, S, st, im->rhs, nullptr, im->X1, launches, bs.hook, bs.k));
+    const bool fuse = summed != nullptr && band_can_fuse<B>(im);
+    if (summed) *summed = fuse;
+    BandFuse fu{fuse ? 1 : 0, bs.k, S.beta, nullptr, acc, uout};
+    BK(solve_chain<B>(im, S, st, im->rhs, nullptr, im->X1, launches, bs.hook, bs.k,
+                      bs.refine > 0 ? BandFuse{} : fu));
     *x1 = im->X1;
     *x2 = nullptr;
     if (bs.refine > 0) {
@@ -1203,18 +1266,20 @@ static int band_run(BandState &bs, const ShiftDev &S, cudaStream_t st, int64_t *
         if (bs.hook) bs.hook->end();
         BK(cudaGetLastError());
         ++*launches;
-        BK(solve_chain<B>(im, S, st, nullptr, im->res, im->X2, launches, bs.hook, bs.k));
+        fu.x1 = im->X1;
+        BK(solve_chain<B>(im, S, st, nullptr, im->res, im->X2, launches, bs.hook, bs.k, fu));
         *x2 = im->X2;
     }
     return REXI_OK;
 }
 
 static int band_run_any(BandState &bs, const ShiftDev &S, cudaStream_t st, int64_t *launches, const c128 **x1,
-                        const c128 **x2, std::string &err) {
+                        const c128 **x2, std::string &err, bool *summed = nullptr, double *acc = nullptr,
+                        c128 *uout = nullptr) {
     switch (bs.B) {
-        case 2: return band_run<2>(bs, S, st, launches, x1, x2, err);
-        case 3: return band_run<3>(bs, S, st, launches, x1, x2, err);
-        default: return band_run<4>(bs, S, st, launches, x1, x2, err);
+        case 2: return band_run<2>(bs, S, st, launches, x1, x2, err, summed, acc, uout);
+        case 3: return band_run<3>(bs, S, st, launches, x1, x2, err, summed, acc, uout);
+        default: return band_run<4>(bs, S, st, launches, x1, x2, err, summed, acc, uout);
     }
 }
 
@@ -1233,8 +1298,10 @@ int band_step(BandState &bs, const ShiftDev &S, cudaStream_t st, const c128 *u, 
     BK(cudaGetLastError());
     ++*launches;
     const c128 *x1 = nullptr, *x2 = nullptr;
-    int rc = band_run_any(bs, S, st, launches, &x1, &x2, err);
+    bool summed = false;
+    int rc = band_run_any(bs, S, st, launches, &x1, &x2, err, &summed, acc, uout);
     if (rc) return rc;
+    if (summed) return REXI_OK;
     if (bs.hook) bs.hook->begin("band_accum", (x2 ? 32.0 : 16.0) * D.n * bs.k + 32.0 * D.n);
     k_band_accum<<<(unsigned)((D.n + 255) / 256), 256, 0, st>>>(D.n, D.kp, bs.k, S.beta, x1, x2, acc, uout);
     if (bs.hook) bs.hook->end();
