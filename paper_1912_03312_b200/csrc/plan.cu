@@ -850,7 +850,11 @@ int rexi_plan_step(rexi_plan *plan, const rexi_c128 *u_in, rexi_c128 *u_out, int
     };
     c128 *zc_out = nullptr;
     const bool persist = n_steps > 0 && plan->persist_cs > 0 && !plan->prof;
-    const bool zc_ok = mem == REXI_MEM_HOST && n_steps > 0 && !getenv("REXI_NO_ZEROCOPY");
+    // (the band solver's step has no re-pointable output node: its last step
+    // replays the graph and copies u1 out instead of running its kernels one
+    // by one into the mapped buffer)
+    const bool zc_ok = mem == REXI_MEM_HOST && n_steps > 0 && plan->solver != REXI_SOLVER_BAND &&
+                       !getenv("REXI_NO_ZEROCOPY");
     if (zc_ok) zc_out = mapped(u_out);
     // zero-copy input: a one-step host call of a TMA-path 1D plan reads u from
     // page-locked host memory inside the level-0 S1 kernel (which forms rhs =
