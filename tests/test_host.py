@@ -252,3 +252,30 @@ def test_pencil_create_rejects_bad_descriptor_without_gpu():
     with pytest.raises(ValueError, match="nnz"):
         _native.NativePencil(np.array([0, 2], np.int32), np.array([0], np.int32), np.array([1.0]),
                              np.array([1.0]))
+
+
+def test_solver_selection_policy_without_device():
+    """rexi_prepare's host-side policies: default refinement (direct solvers
+    refine on stiff pencils only, COCG always) and the per-plan shift limit
+    that makes it split K into more pieces"""
+    from scipy.sparse import diags
+    from paper_1912_03312_b200._pattern import shared_pattern
+    from paper_1912_03312_b200.integrate import default_refine, max_shifts_per_plan
+    n = 50
+    tri = diags([np.ones(n - 1), 2 * np.ones(n), np.ones(n - 1)], [-1, 0, 1]).tocsr()
+    penta = diags([np.ones(n - 2), np.ones(n - 1), 4 * np.ones(n), np.ones(n - 1), np.ones(n - 2)],
+                  [-2, -1, 0, 1, 2]).tocsr()
+    wide = diags([np.ones(n - 7), 4 * np.ones(n), np.ones(n - 7)], [-7, 0, 7]).tocsr()
+    for mat, stiff_refine, cap in ((tri, 1, 256), (penta, 1, 1024), (wide, 1, None)):
+        ip, ix = shared_pattern(mat, mat)[:2]
+        assert default_refine(ip, ix, 1.0, 1e6) == stiff_refine
+        lim = max_shifts_per_plan(ip, ix)
+        if cap is not None:
+            assert lim == cap
+        else:
+            assert lim >= 1024 and lim & (lim - 1) == 0 and lim * n < 2 ** 31
+    ip, ix = shared_pattern(tri, tri)[:2]
+    assert default_refine(ip, ix, 1.0, 10.0) == 0            # non-stiff 1D: fp64 suffices
+    assert default_refine(ip, ix, 1.0, 10.0, "cocg") == 1    # COCG always refines
+    ip, ix = shared_pattern(penta, penta)[:2]
+    assert default_refine(ip, ix, 1.0, 10.0) == 0            # P2 band, non-stiff
