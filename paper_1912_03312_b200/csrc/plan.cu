@@ -687,28 +687,35 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
         }
         if (!rc) rc = dalloc(plan, &plan->ubuf[0], (size_t)d->n);
         if (!rc) rc = dalloc(plan, &plan->ubuf[1], (size_t)d->n);
-        if (!rc && plan->bandwidth <= 32 && !getenv("REXI_NO_SCREEN")) {
-            // the reference's singularity screen: it factors every shifted system
-            // with partially pivoted zgbtrf when kl + ku + 1 <= 32 (solvers.py:25,
-            // 108-115) and rejects the first shift j whose factor has a zero
-            // pivot or min|U_ii| < 1e-14 max|U_ii| (solvers.py:52-69).  Same
-            // algorithm on the device (screen.cu), same order, same messages.
-            std::vector<rexi::ScreenResult> scr;
+        // the reference's singularity screen: it factors every shifted system
+        // with partially pivoted zgbtrf when kl + ku + 1 <= 32 (solvers.py:25,
+        // 108-115) and rejects the first shift j whose factor has a zero pivot
+        // or min|U_ii| < 1e-14 max|U_ii| (solvers.py:52-69).  Same algorithm on
+        // the device (screen.cu), same order, same messages; it runs beside
+        // the plan's own factorisation and its verdict takes precedence.
+        rexi::ScreenJob screen;
+        bool screening = !rc && plan->bandwidth <= 32 && !getenv("REXI_NO_SCREEN");
+        if (screening) {
             std::string serr;
-            rc = rexi::band_screen(d, kl, ku, plan->S.sigma, plan->stream, scr, serr);
+            rc = screen.launch(d, kl, ku, plan->S.sigma, plan->stream, serr);
             if (rc) {
                 set_err(plan, rc, serr);
-            } else {
-                for (int j = 0; j < d->k; ++j) {
-                    const std::string v = rexi::screen_verdict(scr[j], d->n);
-                    plan->screen_ratio = std::min(plan->screen_ratio, scr[j].umax > 0 ? scr[j].umin / scr[j].umax : 0.0);
-                    if (!v.empty()) {
-                        rc = set_err(plan, REXI_ERR_SINGULAR, v + " [shift j = " + std::to_string(plan->gid[j]) + "]");
-                        break;
-                    }
-                }
+                screening = false;
             }
         }
+        auto screen_verdict_now = [&]() -> int {
+            std::vector<rexi::ScreenResult> scr;
+            std::string serr;
+            int src = screen.collect(scr, serr);
+            if (src) return set_err(plan, src, serr);
+            for (int j = 0; j < d->k; ++j) {
+                const std::string v = rexi::screen_verdict(scr[j], d->n);
+                plan->screen_ratio = std::min(plan->screen_ratio, scr[j].umax > 0 ? scr[j].umin / scr[j].umax : 0.0);
+                if (!v.empty())
+                    return set_err(plan, REXI_ERR_SINGULAR, v + " [shift j = " + std::to_string(plan->gid[j]) + "]");
+            }
+            return REXI_OK;
+        };
         if (!rc) {
             if (solver == REXI_SOLVER_TRIDIAG) {
                 rc = tri_create(plan, d);
@@ -724,6 +731,14 @@ int rexi_plan_create(const rexi_desc *d, rexi_plan **out) {
                 if (!rc) rc = cocg_create(plan->cg, d, plan->S, plan->refine, plan->stream, plan->err);
                 if (rc) set_err(plan, rc, plan->err);
             }
+        }
+        if (screening) {
+            // the screen's verdict first (the reference raises it from its
+            // factorisation), then whatever the plan's own creation reported
+            const std::string own_err = plan->err;
+            const int src = screen_verdict_now();
+            if (src) rc = src;
+            else if (rc) set_err(plan, rc, own_err);
         }
     }
     if (rc) {

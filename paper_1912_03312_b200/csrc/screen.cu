@@ -204,10 +204,10 @@ __global__ void __launch_bounds__(32) k_band_screen(const double *__restrict__ b
 
 }  // namespace
 
-int band_screen(const rexi_desc *d, int kl, int ku, const c128 *sigma_dev, cudaStream_t st,
-                std::vector<ScreenResult> &out, std::string &err) {
+int ScreenJob::launch(const rexi_desc *d, int kl, int ku, const c128 *sigma_dev, cudaStream_t after,
+                      std::string &err) {
     const int64_t n = d->n;
-    const int k = d->k;
+    k = d->k;
     const int w = kl + ku + 1;
     if (kl >= SCR_WR_MAX || w > SCR_WC_MAX) {
         err = "band screen: bandwidth above the reference's BAND_LIMIT";
@@ -222,23 +222,23 @@ int band_screen(const rexi_desc *d, int kl, int ku, const c128 *sigma_dev, cudaS
             e[1] += d->a_imag ? d->tau * d->a_imag[q] : 0.0;
             e[2] += d->b_vals[q];
         }
-    double *dband = nullptr, *dmin = nullptr, *dmax = nullptr;
-    long long *dinfo = nullptr;
-    auto cleanup = [&]() {
-        cudaFree(dband);
-        cudaFree(dmin);
-        cudaFree(dmax);
-        cudaFree(dinfo);
-    };
-#define SCK(expr)                                                   \
-    do {                                                            \
-        cudaError_t _e = (expr);                                    \
-        if (_e != cudaSuccess) {                                    \
+#define SCK(expr)                                                     \
+    do {                                                              \
+        cudaError_t _e = (expr);                                      \
+        if (_e != cudaSuccess) {                                      \
             err = std::string(#expr) + ": " + cudaGetErrorString(_e); \
-            cleanup();                                              \
-            return REXI_ERR_CUDA;                                   \
-        }                                                           \
+            return REXI_ERR_CUDA;                                     \
+        }                                                             \
     } while (0)
+    // its own stream, ordered after the shifts' upload on the plan's stream:
+    // the screen (a few SMs, sequential over the rows) overlaps the plan's
+    // factorisation
+    SCK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaEvent_t ev;
+    SCK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SCK(cudaEventRecord(ev, after));
+    SCK(cudaStreamWaitEvent(st, ev, 0));
+    cudaEventDestroy(ev);
     SCK(cudaMalloc(&dband, sizeof(double) * band.size()));
     SCK(cudaMalloc(&dmin, sizeof(double) * k));
     SCK(cudaMalloc(&dmax, sizeof(double) * k));
@@ -247,24 +247,29 @@ int band_screen(const rexi_desc *d, int kl, int ku, const c128 *sigma_dev, cudaS
     SCK(rexi_poison(dmin, sizeof(double) * k));
     SCK(rexi_poison(dmax, sizeof(double) * k));
     SCK(rexi_poison(dinfo, sizeof(long long) * k));
+    // synchronous copy: the host staging vector goes out of scope on return
     SCK(cudaMemcpyAsync(dband, band.data(), sizeof(double) * band.size(), cudaMemcpyHostToDevice, st));
+    SCK(cudaStreamSynchronize(st));
     const int grid = (k + 31) / 32;
     // rows per staged chunk: two chunks of row data in <= 96 KB of shared memory,
     // and at least kl + 2 rows so the window's entering row is always staged
     int CH = std::max(kl + 2, (int)std::min<int64_t>(1024, (96 * 1024) / (2 * (int64_t)w * 3 * 8)));
     CH = (CH + 1) & ~1;   // even: every chunk starts 16-B aligned (cp.async)
     const size_t smem = 2 * (size_t)CH * w * 3 * sizeof(double);
-    auto launch = [&](auto kern) -> cudaError_t {
+    auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         kern<<<grid, 32, smem, st>>>(dband, n, kl, ku, sigma_dev, k, CH, dmin, dmax, dinfo);
         return cudaGetLastError();
     };
-    if (kl == 1 && ku == 1) SCK(launch(k_band_screen<1, 1>));
-    else if (kl == 2 && ku == 2) SCK(launch(k_band_screen<2, 2>));
-    else if (kl == 0 && ku == 0) SCK(launch(k_band_screen<0, 0>));
-    else SCK(launch(k_band_screen<-1, -1>));
-    SCK(cudaGetLastError());
+    if (kl == 1 && ku == 1) SCK(go(k_band_screen<1, 1>));
+    else if (kl == 2 && ku == 2) SCK(go(k_band_screen<2, 2>));
+    else if (kl == 0 && ku == 0) SCK(go(k_band_screen<0, 0>));
+    else SCK(go(k_band_screen<-1, -1>));
+    return REXI_OK;
+}
+
+int ScreenJob::collect(std::vector<ScreenResult> &out, std::string &err) {
     std::vector<double> hmin(k), hmax(k);
     std::vector<long long> hinfo(k);
     SCK(cudaMemcpyAsync(hmin.data(), dmin, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
@@ -272,10 +277,18 @@ int band_screen(const rexi_desc *d, int kl, int ku, const c128 *sigma_dev, cudaS
     SCK(cudaMemcpyAsync(hinfo.data(), dinfo, sizeof(long long) * k, cudaMemcpyDeviceToHost, st));
     SCK(cudaStreamSynchronize(st));
 #undef SCK
-    cleanup();
     out.resize(k);
     for (int j = 0; j < k; ++j) out[j] = ScreenResult{hmin[j], hmax[j], hinfo[j]};
     return REXI_OK;
+}
+
+ScreenJob::~ScreenJob() {
+    if (st) cudaStreamSynchronize(st);
+    cudaFree(dband);
+    cudaFree(dmin);
+    cudaFree(dmax);
+    cudaFree(dinfo);
+    if (st) cudaStreamDestroy(st);
 }
 
 // the reference's verdict and message for one shift (solvers.py:52-69); empty
