@@ -36,6 +36,7 @@ struct TriState {
     float *r32[6] = {};           // refinement, TMA path: level-0 sub/sup row data rounded to float
     c64 *l1_inv32 = nullptr, *l1_sup32 = nullptr, *l1_rw32 = nullptr;   // correction pass, level 1 (complex64)
     double *acc = nullptr;
+    double2 *emax = nullptr;      // refinement, TMA path: per level-0 block max |fl(tau a)| and max |b| (K2's aligned residual)
     bool complex_a = false;       // A has an imaginary part: K2 keeps every residual product error-free
 };
 
@@ -256,6 +257,22 @@ int tri_create(rexi_plan *plan, const rexi_desc *d) {
         CK(cudaMemcpyAsync(dz[q], hz[q]->data(), sizeof(double) * n0, cudaMemcpyHostToDevice, plan->stream));
     }
     T.z = L0Dev{dz[0], dz[1], dz[2], dz[3], dz[4], dz[5], dz[6], dz[7], dz[8], dz[2], dz[5], dz[8]};
+    if (plan->refine > 0 && l0v2_supported(plan->kp)) {
+        // K2's aligned residual bounds |Re entry| <= max|fl(tau a)| + |Im sigma| max|b| per block
+        const int64_t nb = n0 / TRI_M;
+        std::vector<double2> em((size_t)nb);
+        for (int64_t p = 0; p < nb; ++p) {
+            double mt = 0.0, mb = 0.0;
+            for (int64_t r = p * TRI_M; r < (p + 1) * TRI_M; ++r) {
+                mt = std::max({mt, std::fabs(a_sub[r]), std::fabs(a_dia[r]), std::fabs(a_sup[r])});
+                mb = std::max({mb, std::fabs(b_sub[r]), std::fabs(b_dia[r]), std::fabs(b_sup[r])});
+            }
+            em[(size_t)p] = make_double2(mt, mb);
+        }
+        DALLOC(T.emax, (size_t)nb);
+        CK(cudaMemcpyAsync(T.emax, em.data(), sizeof(double2) * nb, cudaMemcpyHostToDevice, plan->stream));
+        CK(cudaStreamSynchronize(plan->stream));
+    }
 
     // symmetric pencil (the FEM case): reduced levels keep only sup
     bool sym = true;
@@ -464,7 +481,7 @@ int tri_step_v2(rexi_plan *plan, const c128 *u, c128 *uout) {
     }
     {
         ProfScope ps(plan, "l0_k2");
-        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres32, T.inv32, T.r32, T.n, T.complex_a, st));
+        CK(l0_launch_k2(T.z, T.lv[0], plan->S, T.rhs0, T.lv[1].X, T.acc, T.rres32, T.inv32, T.r32, T.emax, T.n, T.complex_a, st));
     }
     rc = tri_mid(plan, true);
     if (rc) return rc;

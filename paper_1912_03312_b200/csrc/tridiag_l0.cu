@@ -41,6 +41,9 @@ constexpr int K2_UNROLL = K2_RES_UNROLL;
 #ifndef K2_MINB
 #define K2_MINB 4
 #endif
+#ifndef K2_ALIGNED
+#define K2_ALIGNED 1   // real symmetric A: aligned-quantum residual instead of Dot2 (see k2_refine)
+#endif
 struct L0Args {
     L0Dev z;
     LevelDev L;
@@ -51,6 +54,7 @@ struct L0Args {
     c64 *rres_out;        // K2
     const c64 *inv32;     // K3: level-0 inverse pivots rounded to complex64
     const float *r32[6];  // K3: fl(tau a) sub/im/b, sup/im/b rounded to float
+    const double2 *emax;  // K2 (aligned residual): per block max |fl(tau a)|, max |b|
     double *acc;          // dd partial SoA 4*nout
     c128 *uout;
     int64_t nout;         // real n (level 0 is padded to a multiple of M)
@@ -290,6 +294,24 @@ __device__ __forceinline__ void dot2_sub(ddacc &re, ddacc &im, c128 e, c128 x) {
     }
 }
 
+// ---- aligned residual (real symmetric A: the refined cfg 2 path) ----
+// Every Re(entry) of a block-lane is rounded to a multiple of one quantum qE
+// (25 significant bits) and every Re x / Im x to a multiple of qX (26 bits):
+// the products E_h x_h are then multiples of qE*qX below 2^53 of it, so the
+// row sum H = sum E_h x_h is EXACT in plain fp64 (no TwoSum), and d - H is
+// exact by Sterbenz wherever the residual cancels.  The remainders
+// sum (E x - E_h x_h) (~2^-25 of the products) and the Im(entry) terms go
+// into one fp64 word L with an FMA each, rounding at ~2^-77 of |S||x| -- the
+// same budget as the Dot2 form's (its error-free hi parts are what costs).
+__device__ __forceinline__ unsigned hiabs(double v) { return (unsigned)__double2hiint(v) & 0x7fffffffu; }
+// C such that fl(v + C) - C rounds v to a multiple of 2^(e+1-bits), for every
+// |v| < 2^(e+1), e the exponent of the double whose high word is h
+__device__ __forceinline__ double quant_c(unsigned h, int bits) {
+    const int be = min((int)(h >> 20) + 53 - bits, 2046);
+    return __hiloint2double((be << 20) | 0x80000, 0);
+}
+__device__ __forceinline__ double quant(double v, double C) { return __dsub_rn(__dadd_rn(v, C), C); }
+
 struct Ctx {
     int kp, b, j, cnt, lr0;
     int64_t p, P, base, row0;
@@ -472,20 +494,29 @@ __global__ void __launch_bounds__(L0_NT, S3_MINB) k_l0_s3acc(L0Args a) {
 // ---------------------------------------------------------------------------
 template <int M, bool FULL>
 __device__ __forceinline__ void k2_solve(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
-                                         c128 xn, c128 (&y)[M], c128 *xt) {
+                                         c128 xn, c128 (&y)[M], c128 *xt, unsigned &hx, unsigned &hy) {
     const c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
     c128 *tc = xt + (size_t)c.lr0 * c.kp + c.j;   // may alias ti: slot q is read before x_q overwrites it
     const RowView &rv = l.rv;
     const int kp = c.kp;
     y[0] = xs;
+    // hx, hy: largest high word of |Re x|, |Im x| over the block's x_0..x_M (integer pipe)
+    hx = max(hiabs(xs.x), hiabs(xn.x));
+    hy = max(hiabs(xs.y), hiabs(xn.y));
     sweep_fwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, [&](int q) { return rv.rhs[c.lr0 + q]; });
-    sweep_bwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, xn, [&](int q, c128 x) { tc[q * kp] = x; });
+    sweep_bwd<M, FULL>(y, ti, kp, rv, c.lr0, c.cnt, c.sg, xn, [&](int q, c128 x) {
+        tc[q * kp] = x;
+        if (K2_ALIGNED) {
+            hx = max(hx, hiabs(x.x));
+            hy = max(hy, hiabs(x.y));
+        }
+    });
     tc[0] = xs;
 }
 
 template <int M, bool FULL, bool EXACT, bool SYM>
 __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, const Ctx &c, c128 xs,
-                                          c128 xn, c128 (&y)[M], c128 *xt) {
+                                          c128 xn, c128 (&y)[M], c128 *xt, unsigned hx, unsigned hy) {
     static_assert(FULL, "level 0 is padded to full blocks");
     const c128 *ti = l.t0 + (size_t)c.lr0 * c.kp + c.j;
     c128 *tc = xt + (size_t)c.lr0 * c.kp + c.j;
@@ -512,6 +543,57 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
     // rolled loop keeps the kernel's code and register footprint small.  SYM
     // (symmetric pencil, checked bitwise on the formed entries at plan
     // creation): a_q = c_{q-1}, so each off-diagonal entry is formed once.
+    if constexpr (K2_ALIGNED && SYM && !EXACT) {
+        // bits: qE 25, qX 26 -> 3 products of <= 2^(eE+eX+3) on a grid of
+        // 2^(eE+eX+3-51): the partial sums need <= 53 bits (exact)
+        const double2 em = __ldg(a.emax + c.p);
+        const double eb = fma(fabs(c.sg.y), em.y, em.x);
+        const double cE = quant_c(hiabs(eb) + (1u << 20), 25);   // one binade of headroom for the formation's rounding
+        const double cX = quant_c(hx, 26), cY = quant_c(hy, 26);
+        c128 xm = tc[0], x0 = tc[kp];
+        double xmh = quant(xm.x, cX), xmk = quant(xm.y, cY);
+        double x0h = quant(x0.x, cX), x0k = quant(x0.y, cY);
+        double Es = sup0.x, Fs = sup0.y, Esh = quant(Es, cE);
+#pragma unroll K2_UNROLL
+        for (int q = 1; q < M; ++q) {
+            const int lr = c.lr0 + q;
+            const c128 xp = q < cnt ? tc[(q + 1) * kp] : xn;
+            const double xph = quant(xp.x, cX), xpk = quant(xp.y, cY);
+            const c128 d = rv.rhs[lr];
+            // entries with the reference's rounding (form_entry; Im(tau A) = 0 here)
+            const double Ed = __dadd_rn(rv.dr[lr], __dmul_rn(c.sg.y, rv.db[lr]));
+            const double Fd = -__dmul_rn(c.sg.x, rv.db[lr]);
+            const double Eu = __dadd_rn(rv.ur[lr], __dmul_rn(c.sg.y, rv.ub[lr]));
+            const double Fu = -__dmul_rn(c.sg.x, rv.ub[lr]);
+            const double Edh = quant(Ed, cE), Euh = quant(Eu, cE);
+            // Re r = d.x - sum(E X - F Y)
+            double P1 = __dmul_rn(Esh, xmh), P2 = __dmul_rn(Edh, x0h), P3 = __dmul_rn(Euh, xph);
+            double H = __dadd_rn(__dadd_rn(P1, P2), P3);
+            double L = __fma_rn(Es, xm.x, -P1);
+            L = __dadd_rn(L, __fma_rn(Ed, x0.x, -P2));
+            L = __dadd_rn(L, __fma_rn(Eu, xp.x, -P3));
+            L = __fma_rn(-Fs, xm.y, L);
+            L = __fma_rn(-Fd, x0.y, L);
+            L = __fma_rn(-Fu, xp.y, L);
+            const double rre = __dsub_rn(__dsub_rn(d.x, H), L);
+            // Im r = d.y - sum(E Y + F X)
+            P1 = __dmul_rn(Esh, xmk); P2 = __dmul_rn(Edh, x0k); P3 = __dmul_rn(Euh, xpk);
+            H = __dadd_rn(__dadd_rn(P1, P2), P3);
+            L = __fma_rn(Es, xm.y, -P1);
+            L = __dadd_rn(L, __fma_rn(Ed, x0.y, -P2));
+            L = __dadd_rn(L, __fma_rn(Eu, xp.y, -P3));
+            L = __fma_rn(Fs, xm.x, L);
+            L = __fma_rn(Fd, x0.x, L);
+            L = __fma_rn(Fu, xp.x, L);
+            const double rim = __dsub_rn(__dsub_rn(d.y, H), L);
+            const c64 r32 = to_c64(cmk(rre, rim));
+            a.rres_out[(c.base + q) * kp + j] = r32;
+            *reinterpret_cast<c64 *>(tc + (q - 1) * kp) = r32;
+            xm = x0; xmh = x0h; xmk = x0k;
+            x0 = xp; x0h = xph; x0k = xpk;
+            Es = Eu; Fs = Fu; Esh = Euh;
+        }
+    } else {
     c128 xm = tc[0], x0 = tc[kp];
     c128 esub = sup0;
 #pragma unroll K2_UNROLL
@@ -533,6 +615,7 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
         xm = x0;
         x0 = xp;
         esub = eup;
+    }
     }
     // correction reduce: S1 with rhs = r, in complex64 with K3's pivots
     // (K2_ONE_TILE: the complex64 pivot copy in HBM, as K3 reads it; else
@@ -608,8 +691,9 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
     }
     mbar_wait(reinterpret_cast<uint64_t *>(smem), 0);
     c128 y[M];
+    unsigned hx = 0, hy = 0;
     if (c.active) {
-        k2_solve<M, true>(a, l, c, xs, xn, y, xt);
+        k2_solve<M, true>(a, l, c, xs, xn, y, xt, hx, hy);
     } else {
         c128 *tc = xt + (size_t)c.lr0 * c.kp + c.j;
 #pragma unroll
@@ -618,8 +702,8 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
     __syncthreads();
     reduce_rows<M>(xt, a, c.row0);
     if (!c.active) return;
-    if (a.L.sym) k2_refine<M, true, EXACT, true>(a, l, c, xs, xn, y, xt);
-    else k2_refine<M, true, EXACT, false>(a, l, c, xs, xn, y, xt);
+    if (a.L.sym) k2_refine<M, true, EXACT, true>(a, l, c, xs, xn, y, xt, hx, hy);
+    else k2_refine<M, true, EXACT, false>(a, l, c, xs, xn, y, xt, hx, hy);
 }
 
 // ---------------------------------------------------------------------------
@@ -1230,10 +1314,11 @@ cudaError_t l0_launch_s3acc(const L0Dev &z, const LevelDev &L, const ShiftDev &S
 
 cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
                          const c128 *X1, double *acc, c64 *rres, const c64 *inv32, const float *const *r32,
-                         int64_t nout, bool exact_residual, cudaStream_t st) {
+                         const double2 *emax, int64_t nout, bool exact_residual, cudaStream_t st) {
     L0Args a{};
     a.nout = nout;
     a.z = z; a.L = L; a.S = S; a.rhs0 = rhs0; a.X1 = X1; a.acc = acc; a.rres_out = rres; a.inv32 = inv32;
+    a.emax = emax;
     a.acc_add = 0; a.final_out = 0;
     {
         int dev = 0, sms = 148;

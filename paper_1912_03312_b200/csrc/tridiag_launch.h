@@ -71,7 +71,7 @@ cudaError_t l0_launch_s3acc(const L0Dev &z, const LevelDev &L, const ShiftDev &S
                             const c128 *X1, double *acc, c128 *uout, int64_t nout, cudaStream_t st);
 cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *rhs0,
                          const c128 *X1, double *acc, c64 *rres, const c64 *inv32, const float *const *r32,
-                         int64_t nout, bool exact_residual, cudaStream_t st);
+                         const double2 *emax, int64_t nout, bool exact_residual, cudaStream_t st);
 cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *X1,
                          const c64 *inv32, const float *const *r32, const c64 *rres, double *acc, c128 *uout,
                          int64_t nout, cudaStream_t st);
