@@ -84,6 +84,7 @@ struct CgScal {                            // per lane of the current layout
     double2 *rho, *alpha, *beta;
     double *rnorm2, *bnorm2;
     int *active, *iters, *status;
+    int *flush;                            // lane froze with its last x += alpha p still pending (CG_DEFER_X)
     int *nactive;                          // [1]
     double2 *part_a;                       // spmv partials [nchunks][kp]
     double2 *part_b;                       // update partials [grid][kp]
@@ -97,12 +98,25 @@ struct CgScal {                            // per lane of the current layout
 
 struct CgGeom {
     int kp, kw, G, rpw;                    // lanes, lanes per warp group, groups, rows per warp
+    int ld;                                // lanes stored per row (row stride of x, z, p, q): the live
+                                           // prefix rounded up, <= kp; lanes >= ld are padding (never live)
     int slots, P, subs, cpc;               // row slots per pass, passes/claim, sub-blocks/claim, chunks/claim
     int64_t nchunks, nclaims;              // 64-row chunks, claims
     const int *lane_shift;                 // [kp] shift index of each lane
 };
 
 __device__ __forceinline__ c128 cdiv_c(c128 a, c128 b) { return cmul(a, crcp(b)); }
+
+// Deferred x update (SURVEY 8(d)'s 160 B per live row-shift and iteration):
+// x += alpha_k p_k is applied by the NEXT iteration's spmv, which holds p_k in
+// registers anyway, so the update kernel touches only z and q (48 B) and the
+// spmv 112 B, instead of 96 + 80.  A lane that freezes after update k keeps a
+// `flush` flag: the next spmv (or the scatter that takes it out of the layout)
+// applies the pending term.  Same operations in the same order per lane:
+// bitwise identical to the undeferred form (CG_DEFER_X=0).
+#ifndef CG_DEFER_X
+#define CG_DEFER_X 1
+#endif
 
 #ifndef CG_GB
 #define CG_GB 8   // z gathers in flight per thread (global-CSR spmv)
@@ -315,12 +329,15 @@ __global__ void __launch_bounds__(CG_NT, CG_SPMV_MINB) k_cg_spmv(CgMat M, CgVec 
     if (*Sc.nactive == 0) return;
     int lane, slot, slots;
     cta_geom(g, lane, slot, slots);
-    const uint32_t kp = (uint32_t)g.kp;
+    const uint32_t kp = (uint32_t)g.kp, ld = (uint32_t)g.ld;
     const bool act = Sc.active[lane] != 0;
+    const bool fl = CG_DEFER_X && !act && Sc.flush[lane] != 0;
     const c128 sg = S.sigma[g.lane_shift[lane]];
     const c128 beta = Sc.beta[lane];
+    const c128 alpha = Sc.alpha[lane];
     c128 *__restrict__ pv = V.p;
     c128 *__restrict__ qv = V.q;
+    c128 *__restrict__ xv = V.x;
     const c128 *__restrict__ zv = V.z;
     if (threadIdx.x == 0) claim_q[0] = (int64_t)atomicAdd(Sc.ctr, 1u);
     __syncthreads();
@@ -337,13 +354,21 @@ __global__ void __launch_bounds__(CG_NT, CG_SPMV_MINB) k_cg_spmv(CgMat M, CgVec 
             if (act) {
                 const int64_t r1 = min(r0 + CG_SB * CG_CH, M.n);
                 for (int64_t i = r0; i < r1; i += CG_CH) {
-                    const c128 acc = row_sz<CPLX, BATCH>(M, i, zv, kp, lane, sg);
-                    const uint32_t o = (uint32_t)i * kp + lane;
-                    const c128 pi = cadd(zv[o], cmul(beta, pv[o]));
+                    const c128 acc = row_sz<CPLX, BATCH>(M, i, zv, ld, lane, sg);
+                    const uint32_t o = (uint32_t)i * ld + lane;
+                    const c128 po = pv[o];
+                    if (CG_DEFER_X) xv[o] = cadd(xv[o], cmul(alpha, po));
+                    const c128 pi = cadd(zv[o], cmul(beta, po));
                     const c128 qi = cadd(acc, cmul(beta, qv[o]));
                     pv[o] = pi;
                     qv[o] = qi;
                     mu = cadd(mu, cmul(pi, qi));
+                }
+            } else if (fl) {
+                const int64_t r1 = min(r0 + CG_SB * CG_CH, M.n);
+                for (int64_t i = r0; i < r1; i += CG_CH) {
+                    const uint32_t o = (uint32_t)i * ld + lane;
+                    xv[o] = cadd(xv[o], cmul(alpha, pv[o]));
                 }
             }
             sbp[buf][sbl * kp + lane] = mu;
@@ -398,7 +423,8 @@ __device__ __forceinline__ StLayout st_carve(unsigned char *smem, bool cplx) {
 
 // thread 0: stage claim `claim` into buffer `b` (arrays padded by >= 32 B)
 template <bool CPLX>
-__device__ __forceinline__ void st_issue(const StLayout &L, int b, int64_t claim, const CgMat &M, const CgGeom &g) {
+__device__ __forceinline__ void st_issue(const StLayout &L, int b, int64_t claim, const CgMat &M, const CgGeom &g,
+                                         uint32_t extra_tx = 0) {
     const int64_t rows = (int64_t)g.cpc * CG_SB * CG_CH;
     const int64_t R0 = claim * rows, R1 = min(R0 + rows, M.n);
     const int64_t ipb = R0 & ~3ll, ipe = (R1 + 1 + 3) & ~3ll;
@@ -409,7 +435,7 @@ __device__ __forceinline__ void st_issue(const StLayout &L, int b, int64_t claim
     L.meta[b * 4 + 1] = (int)xb;
     L.meta[b * 4 + 2] = (int)vb;
     const uint32_t bip = (uint32_t)((ipe - ipb) * 4), bix = (uint32_t)((xe - xb) * 4), bv = (uint32_t)((ve - vb) * 8);
-    mbar_expect_tx(L.bar + b, bip + bix + bv * (CPLX ? 3 : 2));
+    mbar_expect_tx(L.bar + b, bip + bix + bv * (CPLX ? 3 : 2) + extra_tx);
     bulk_g2s(L.ip + b * CG_ST_ROWS, M.indptr + ipb, bip, L.bar + b);
     if (bix) bulk_g2s(L.ix + b * (CG_ST_NNZ + 8), M.indices + xb, bix, L.bar + b);
     if (bv) {
@@ -434,12 +460,15 @@ __global__ void __launch_bounds__(CG_NT, CG_ST_MINB) k_cg_spmv_st(CgMat M, CgVec
     const StLayout L = st_carve(smem, CPLX);
     int lane, slot, slots;
     cta_geom(g, lane, slot, slots);
-    const uint32_t kp = (uint32_t)g.kp;
+    const uint32_t kp = (uint32_t)g.kp, ld = (uint32_t)g.ld;
     const bool act = Sc.active[lane] != 0;
+    const bool fl = CG_DEFER_X && !act && Sc.flush[lane] != 0;
     const c128 sg = S.sigma[g.lane_shift[lane]];
     const c128 beta = Sc.beta[lane];
+    const c128 alpha = Sc.alpha[lane];
     c128 *__restrict__ pv = V.p;
     c128 *__restrict__ qv = V.q;
+    c128 *__restrict__ xv = V.x;
     const c128 *__restrict__ zv = V.z;
     if (threadIdx.x == 0) {
         mbar_init(L.bar, 1);
@@ -488,7 +517,7 @@ __global__ void __launch_bounds__(CG_NT, CG_ST_MINB) k_cg_spmv_st(CgMat M, CgVec
                         for (int k = 0; k < CG_STB; ++k) cc[k] = qb + k < q1 ? (uint32_t)ix[qb + k - xb] : 0u;
 #pragma unroll
                         for (int k = 0; k < CG_STB; ++k)
-                            zz[k] = qb + k < q1 ? zv[cc[k] * kp + lane] : cmk(0.0, 0.0);
+                            zz[k] = qb + k < q1 ? zv[cc[k] * ld + lane] : cmk(0.0, 0.0);
 #pragma unroll
                         for (int k = 0; k < CG_STB; ++k) {
                             if (qb + k < q1) {
@@ -498,12 +527,20 @@ __global__ void __launch_bounds__(CG_NT, CG_ST_MINB) k_cg_spmv_st(CgMat M, CgVec
                             }
                         }
                     }
-                    const uint32_t o = (uint32_t)i * kp + lane;
-                    const c128 pi = cadd(zv[o], cmul(beta, pv[o]));
+                    const uint32_t o = (uint32_t)i * ld + lane;
+                    const c128 po = pv[o];
+                    if (CG_DEFER_X) xv[o] = cadd(xv[o], cmul(alpha, po));
+                    const c128 pi = cadd(zv[o], cmul(beta, po));
                     const c128 qi = cadd(acc, cmul(beta, qv[o]));
                     pv[o] = pi;
                     qv[o] = qi;
                     mu = cadd(mu, cmul(pi, qi));
+                }
+            } else if (fl) {
+                const int64_t r1 = min(r0 + CG_SB * CG_CH, M.n);
+                for (int64_t i = r0; i < r1; i += CG_CH) {
+                    const uint32_t o = (uint32_t)i * ld + lane;
+                    xv[o] = cadd(xv[o], cmul(alpha, pv[o]));
                 }
             }
             sbp[buf][sbl * kp + lane] = mu;
@@ -513,6 +550,222 @@ __global__ void __launch_bounds__(CG_NT, CG_ST_MINB) k_cg_spmv_st(CgMat M, CgVec
         buf ^= 1;
     }
 }
+
+// ---------------------------------------------------------------------------
+// spmv, widest layouts (kp = 32 or 64, real A): a persistent CTA per SM whose
+// streaming operands never pass through registers.  A producer warp claims
+// row chunks from the same atomic counter and bulk-copies (cp.async.bulk) the
+// claim's p, q and x tiles -- each one contiguous range of 32 KB -- plus its
+// CSR slice into one of two shared-memory stages; 16 consumer warps gather z
+// (two rows' gathers in flight per thread), update the tiles in place and hand
+// the stage back; the producer bulk-stores the three tiles and refills the
+// stage.  The k_cg_spmv_st form keeps ~24 warps x (gathers | own loads) in
+// flight per SM and is latency-bound at ~57 % of HBM; here 96 KB of loads and
+// 96 KB of stores are in flight per SM independent of the gather latency.
+// Same rows per sub-block, same operation order per lane, same partial tree:
+// bitwise identical to the other spmv kernels.
+// ---------------------------------------------------------------------------
+constexpr int CGT_CW = 16;                      // consumer warps
+constexpr int CGT_CT = CGT_CW * 32;             // consumer threads
+constexpr int CGT_NT = CGT_CT + 32;             // + the producer warp
+constexpr int CGT_TILE = CGT_CT * CG_SB;        // row-lanes per claim: 32 KB per vector
+#ifndef CGT_ROWS_PAR
+#define CGT_ROWS_PAR 1                          // swept with CGT_STB: scripts/tune_tma.sh (1 x 8 fastest)
+#endif
+constexpr int CGT_RP = CGT_ROWS_PAR;            // rows whose gathers are in flight together
+#ifndef CGT_STB
+#define CGT_STB 8                               // gathers in flight per row (96 registers, no spills)
+#endif
+
+__host__ __device__ inline size_t tma_smem_bytes() {
+    return 128 + 2 * 3 * (size_t)CGT_TILE * sizeof(c128) + st_smem_bytes(false) + (size_t)(CGT_CT) * sizeof(double2);
+}
+
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(CGT_CT) : "memory"); }
+
+#if CG_DEFER_X
+__global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_tma(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (*Sc.nactive == 0) return;
+    // header: full[2] (the CSR staging layout's barriers), done[2], claim[2]
+    uint64_t *done = reinterpret_cast<uint64_t *>(smem + 64);
+    int64_t *claim_q = reinterpret_cast<int64_t *>(smem + 96);
+    c128 *tiles = reinterpret_cast<c128 *>(smem + 128);
+    unsigned char *stp = smem + 128 + 2 * 3 * (size_t)CGT_TILE * sizeof(c128);
+    const StLayout L = st_carve(stp, false);           // L.bar[2] = full[2]
+    double2 *sbp = reinterpret_cast<double2 *>(stp + st_smem_bytes(false));
+    const uint32_t kp = (uint32_t)g.kp, ld = (uint32_t)g.ld;
+    const int64_t rows_pc = (int64_t)g.cpc * CG_SB * CG_CH;
+    if (threadIdx.x == 0) {
+        mbar_init(L.bar, 1);
+        mbar_init(L.bar + 1, 1);
+        mbar_init(done, 1);
+        mbar_init(done + 1, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x >= CGT_CT) {
+        // ---- producer ----
+        if (threadIdx.x != CGT_CT) return;
+        int64_t prev[2] = {0, 0};
+        uint32_t dph[2] = {0u, 0u};
+        auto tile = [&](int s, int v) { return tiles + ((size_t)s * 3 + v) * CGT_TILE; };
+        auto store = [&](int s, int64_t c) {
+            const int64_t R0 = c * rows_pc, R1 = min(R0 + rows_pc, M.n);
+            const uint32_t tb = (uint32_t)((R1 - R0) * ld * sizeof(c128));
+            const size_t o = (size_t)R0 * ld;
+            bulk_s2g(V.p + o, tile(s, 0), tb);
+            bulk_s2g(V.q + o, tile(s, 1), tb);
+            bulk_s2g(V.x + o, tile(s, 2), tb);
+            bulk_commit();
+        };
+        int i = 0;
+        for (;; ++i) {
+            const int s = i & 1;
+            if (i >= 2) {
+                mbar_wait(done + s, dph[s]);
+                dph[s] ^= 1u;
+                store(s, prev[s]);
+                bulk_wait_read0();   // the stage's tiles have been read out: refill
+            }
+            const int64_t c = (int64_t)atomicAdd(Sc.ctr, 1u);
+            claim_q[s] = c;
+            if (c >= g.nclaims) {
+                mbar_arrive(L.bar + s);
+                break;
+            }
+            prev[s] = c;
+            const int64_t R0 = c * rows_pc, R1 = min(R0 + rows_pc, M.n);
+            const uint32_t tb = (uint32_t)((R1 - R0) * ld * sizeof(c128));
+            const size_t o = (size_t)R0 * ld;
+            st_issue<false>(L, s, c, M, g, 3 * tb);
+            bulk_g2s(tile(s, 0), V.p + o, tb, L.bar + s);
+            bulk_g2s(tile(s, 1), V.q + o, tb, L.bar + s);
+            bulk_g2s(tile(s, 2), V.x + o, tb, L.bar + s);
+        }
+        if (i >= 1) {   // the claim computed last sits in the other stage
+            const int s = (i - 1) & 1;
+            mbar_wait(done + s, dph[s]);
+            store(s, prev[s]);
+        }
+        bulk_wait0();
+        return;
+    }
+    // ---- consumers ----
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int lane = (w % g.G) * g.kw + (l % g.kw);
+    const int sbl = (w / g.G) * g.rpw + l / g.kw;       // sub-block of the claim (one pass)
+    const bool act = Sc.active[lane] != 0;
+    const bool fl = !act && Sc.flush[lane] != 0;
+    const c128 sg = S.sigma[g.lane_shift[lane]];
+    const c128 beta = Sc.beta[lane];
+    const c128 alpha = Sc.alpha[lane];
+    const c128 *__restrict__ zv = V.z;
+    uint32_t fph[2] = {0u, 0u};
+    for (int it = 0;; ++it) {
+        const int s = it & 1;
+        mbar_wait(L.bar + s, fph[s]);
+        fph[s] ^= 1u;
+        const int64_t claim = claim_q[s];
+        if (claim >= g.nclaims) break;
+        c128 *tp = tiles + ((size_t)s * 3 + 0) * CGT_TILE;
+        c128 *tq = tiles + ((size_t)s * 3 + 1) * CGT_TILE;
+        c128 *tx = tiles + ((size_t)s * 3 + 2) * CGT_TILE;
+        const int *ip = L.ip + s * CG_ST_ROWS;
+        const int *ix = L.ix + s * (CG_ST_NNZ + 8);
+        const double *sta = L.ta + s * (CG_ST_NNZ + 8);
+        const double *stb = L.tb + s * (CG_ST_NNZ + 8);
+        const int ipb = L.meta[s * 4 + 0], xb = L.meta[s * 4 + 1], vb = L.meta[s * 4 + 2];
+        const int64_t R0 = claim * rows_pc;
+        const int64_t gsb = claim * g.subs + sbl;   // sub-block b of chunk c: rows c*32 + b + 8k
+        const int64_t r0 = (gsb / CG_CH) * (CG_SB * CG_CH) + gsb % CG_CH;
+        c128 mu = cmk(0.0, 0.0);
+        if (act) {
+#pragma unroll
+            for (int h = 0; h < CG_SB / CGT_RP; ++h) {
+                int32_t q0[CGT_RP], q1[CGT_RP];
+                c128 acc[CGT_RP];
+                int nb = 0;
+#pragma unroll
+                for (int r = 0; r < CGT_RP; ++r) {
+                    const int64_t i = r0 + (int64_t)(h * CGT_RP + r) * CG_CH;
+                    const bool ok = i < M.n;
+                    const int li = ok ? (int)(i - ipb) : 0;
+                    q0[r] = ok ? ip[li] : 0;
+                    q1[r] = ok ? ip[li + 1] : 0;
+                    acc[r] = cmk(0.0, 0.0);
+                    nb = max(nb, q1[r] - q0[r]);
+                }
+                for (int off = 0; off < nb; off += CGT_STB) {
+                    c128 zz[CGT_RP][CGT_STB];
+#pragma unroll
+                    for (int r = 0; r < CGT_RP; ++r)
+#pragma unroll
+                        for (int k = 0; k < CGT_STB; ++k) {
+                            const int32_t q = q0[r] + off + k;
+                            const uint32_t cc = q < q1[r] ? (uint32_t)ix[q - xb] : 0u;
+                            zz[r][k] = q < q1[r] ? zv[cc * ld + lane] : cmk(0.0, 0.0);
+                        }
+#pragma unroll
+                    for (int r = 0; r < CGT_RP; ++r)
+#pragma unroll
+                        for (int k = 0; k < CGT_STB; ++k) {
+                            const int32_t q = q0[r] + off + k;
+                            if (q < q1[r]) {
+                                const c128 e = form_entry(sta[q - vb], 0.0, stb[q - vb], sg);
+                                acc[r] = cadd(acc[r], cmul(e, zz[r][k]));
+                            }
+                        }
+                }
+#pragma unroll
+                for (int r = 0; r < CGT_RP; ++r) {
+                    const int64_t i = r0 + (int64_t)(h * CGT_RP + r) * CG_CH;
+                    if (i < M.n) {
+                        const uint32_t o = (uint32_t)i * ld + lane;
+                        const uint32_t t = (uint32_t)(i - R0) * ld + lane;
+                        const c128 po = tp[t];
+                        tx[t] = cadd(tx[t], cmul(alpha, po));
+                        const c128 pi = cadd(zv[o], cmul(beta, po));
+                        const c128 qi = cadd(acc[r], cmul(beta, tq[t]));
+                        tp[t] = pi;
+                        tq[t] = qi;
+                        mu = cadd(mu, cmul(pi, qi));
+                    }
+                }
+            }
+        } else if (fl) {
+            const int64_t r1 = min(r0 + CG_SB * CG_CH, M.n);
+            for (int64_t i = r0; i < r1; i += CG_CH) {
+                const uint32_t t = (uint32_t)(i - R0) * ld + lane;
+                tx[t] = cadd(tx[t], cmul(alpha, tp[t]));
+            }
+        }
+        bar_consumers();             // the previous claim's chunk partials have been read
+        sbp[sbl * kp + lane] = mu;
+        fence_proxy_async();         // tile writes -> visible to the bulk stores
+        bar_consumers();
+        if (threadIdx.x == 0) mbar_arrive(done + s);
+        if (threadIdx.x < g.cpc * (int)kp) {
+            const int cc = threadIdx.x / (int)kp, ll = threadIdx.x % (int)kp;
+            const int64_t chunk = claim * g.cpc + cc;
+            if (chunk < g.nchunks) {
+                double2 sum = make_double2(0.0, 0.0);
+                for (int b = 0; b < CG_CH; ++b) sum = cadd(sum, sbp[(cc * CG_CH + b) * kp + ll]);
+                Sc.part_a[(size_t)chunk * kp + ll] = sum;
+            }
+        }
+    }
+}
+#endif
 
 // ---------------------------------------------------------------------------
 // Width 1 (one live shift, the tail of a solve): one thread per row, a warp
@@ -552,10 +805,13 @@ template <bool CPLX>
 __global__ void __launch_bounds__(CG1_NT) k_cg_spmv1(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
     if (*Sc.nactive == 0) return;
     const bool act = Sc.active[0] != 0;
+    const bool fl = CG_DEFER_X && !act && Sc.flush[0] != 0;
     const c128 sg = S.sigma[g.lane_shift[0]];
     const c128 beta = Sc.beta[0];
+    const c128 alpha = Sc.alpha[0];
     c128 *__restrict__ pv = V.p;
     c128 *__restrict__ qv = V.q;
+    c128 *__restrict__ xv = V.x;
     const c128 *__restrict__ zv = V.z;
     const int l = threadIdx.x & 31;
     const int64_t wstride = (int64_t)gridDim.x * (CG1_NT / 32);
@@ -564,11 +820,15 @@ __global__ void __launch_bounds__(CG1_NT) k_cg_spmv1(CgMat M, CgVec V, CgScal Sc
         c128 term = cmk(0.0, 0.0);
         if (act && i < M.n) {
             const c128 acc = row_sz<CPLX, true>(M, i, zv, 1u, 0, sg);
-            const c128 pi = cadd(zv[i], cmul(beta, pv[i]));
+            const c128 po = pv[i];
+            if (CG_DEFER_X) xv[i] = cadd(xv[i], cmul(alpha, po));
+            const c128 pi = cadd(zv[i], cmul(beta, po));
             const c128 qi = cadd(acc, cmul(beta, qv[i]));
             pv[i] = pi;
             qv[i] = qi;
             term = cmul(pi, qi);
+        } else if (fl && i < M.n) {
+            xv[i] = cadd(xv[i], cmul(alpha, pv[i]));
         }
         const double2 s = chunk_sum_c(term);
         if (l == 0) Sc.part_a[c] = s;
@@ -587,8 +847,8 @@ __global__ void __launch_bounds__(CG1_NT) k_cg_update1(CgMat M, CgVec V, CgScal 
         c128 trho = cmk(0.0, 0.0);
         double trn = 0.0;
         if (act && i < M.n) {
-            const c128 p = V.p[i], q = V.q[i];
-            V.x[i] = cadd(V.x[i], cmul(alpha, p));
+            const c128 q = V.q[i];
+            if (!CG_DEFER_X) V.x[i] = cadd(V.x[i], cmul(alpha, V.p[i]));
             const c128 d = form_entry(M.dta[i], M.dta_im[i], M.db[i], sg);
             const c128 z = csub(V.z[i], cmul(alpha, cdiv_c(q, d)));
             V.z[i] = z;
@@ -606,8 +866,9 @@ __global__ void __launch_bounds__(CG1_NT) k_cg_update1(CgMat M, CgVec V, CgScal 
 }
 
 // ---------------------------------------------------------------------------
-// update: x += alpha p; z -= alpha D^-1 q; partials of rho' = r^T z, |r|^2 with
-// r = D z (96 B per live row-shift: x, z read + written, p, q read)
+// update: z -= alpha D^-1 q; partials of rho' = r^T z, |r|^2 with r = D z
+// (48 B per live row-shift: z read + written, q read; x += alpha p is deferred
+// to the next spmv, see CG_DEFER_X)
 // (claims statically strided over CTAs: pointwise, no locality to exploit)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
@@ -632,9 +893,9 @@ __global__ void __launch_bounds__(CG_NT) k_cg_update(CgMat M, CgVec V, CgScal Sc
                 const int64_t r1 = min(r0 + CG_SB * CG_CH, M.n);
 #pragma unroll 2
                 for (int64_t i = r0; i < r1; i += CG_CH) {
-                    const size_t o = (size_t)i * kp + lane;
-                    const c128 p = pnew[o], q = V.q[o];
-                    V.x[o] = cadd(V.x[o], cmul(alpha, p));
+                    const size_t o = (size_t)i * g.ld + lane;
+                    const c128 q = V.q[o];
+                    if (!CG_DEFER_X) V.x[o] = cadd(V.x[o], cmul(alpha, pnew[o]));
                     // preconditioned residual recurrence z <- z - alpha D^-1 q;
                     // r = D z is formed for the dots only (16 B per row-shift
                     // less than storing r and z)
@@ -753,10 +1014,13 @@ __device__ __forceinline__ void finish_lane(CgScal &Sc, const CgGeom &g, int l, 
         Sc.bnorm2[l] = sr;
         Sc.rnorm2[l] = sr;
         Sc.beta[l] = make_double2(0.0, 0.0);
+        Sc.alpha[l] = make_double2(0.0, 0.0);
+        Sc.flush[l] = 0;
         Sc.iters[l] = 0;
         Sc.status[l] = 0;
         Sc.active[l] = (g.lane_shift[l] < kreal && sr > 0.0) ? 1 : 0;
     } else if (MODE == 1) {
+        Sc.flush[l] = 0;   // the spmv just run applied a frozen lane's pending x term
         if (Sc.active[l]) {
             const double ms = cabs2(s);
             if (!(ms > 0.0) || !isfinite(ms)) {
@@ -786,6 +1050,7 @@ __device__ __forceinline__ void finish_lane(CgScal &Sc, const CgGeom &g, int l, 
             Sc.beta[l] = cdiv_c(s, rho_old);
             Sc.rho[l] = s;
         }
+        if (CG_DEFER_X && !Sc.active[l]) Sc.flush[l] = 1;   // x += alpha p of this iteration is still pending
     }
 }
 
@@ -864,24 +1129,32 @@ static inline size_t finish_smem(int mode) { return (size_t)CG_FL_MAXV * (sizeof
 // ---------------------------------------------------------------------------
 // compaction: dst[i][l'] = src[i][map[l']] (new width kp_new)
 // ---------------------------------------------------------------------------
-__global__ void k_cg_repack(const c128 *__restrict__ src, c128 *__restrict__ dst, int64_t n, int kp_old,
-                            int kp_new, const int *__restrict__ map) {
+// (ld_old, ld_new: lanes stored per row before / after)
+__global__ void k_cg_repack(const c128 *__restrict__ src, c128 *__restrict__ dst, int64_t n, int ld_old,
+                            int ld_new, const int *__restrict__ map) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n * kp_new) return;
-    const int64_t i = t / kp_new;
-    const int l = (int)(t % kp_new);
-    dst[t] = src[i * kp_old + map[l]];
+    if (t >= n * ld_new) return;
+    const int64_t i = t / ld_new;
+    const int l = (int)(t % ld_new);
+    dst[t] = src[i * ld_old + map[l]];
 }
 
 // x_out[i][lane_shift[l]] = x[i][l] for the lanes in mask
-__global__ void k_cg_scatter_x(const c128 *__restrict__ x, c128 *__restrict__ xout, int64_t n, int kp,
+// (a lane with its last x += alpha p pending gets it here, see CG_DEFER_X)
+__global__ void k_cg_scatter_x(const c128 *__restrict__ x, const c128 *__restrict__ p,
+                               const double2 *__restrict__ alpha, const int *__restrict__ flush,
+                               c128 *__restrict__ xout, int64_t n, int ld,
                                int kp_full, const int *__restrict__ lane_shift,
                                const int *__restrict__ mask) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n * kp) return;
-    const int64_t i = t / kp;
-    const int l = (int)(t % kp);
-    if (mask[l]) xout[i * kp_full + lane_shift[l]] = x[t];
+    if (t >= n * ld) return;
+    const int64_t i = t / ld;
+    const int l = (int)(t % ld);
+    if (mask[l]) {
+        c128 v = x[t];
+        if (CG_DEFER_X && flush[l]) v = cadd(v, cmul(alpha[l], p[t]));
+        xout[i * kp_full + lane_shift[l]] = v;
+    }
 }
 
 // scalars of the kept lanes, in place safe (map[l'] >= l')
@@ -895,6 +1168,7 @@ __global__ void k_cg_repack_scalars(CgScal Sc, int kp_new, const int *__restrict
         Sc.rnorm2[l] = Sc.rnorm2[s];
         Sc.bnorm2[l] = Sc.bnorm2[s];
         Sc.active[l] = Sc.active[s];
+        Sc.flush[l] = Sc.flush[s];
         Sc.iters[l] = Sc.iters[s];
         Sc.status[l] = Sc.status[s];
         Sc.tolsq[l] = Sc.tolsq[s];
@@ -1055,13 +1329,14 @@ static int alloc_(CocgState &cg, void **p, size_t bytes, std::string &err) {
         }                                                                 \
     } while (0)
 
-static CgGeom make_geom(const CocgImpl *im, int kp, int64_t n) {
+static CgGeom make_geom(const CocgImpl *im, int kp, int64_t n, int warps = CG_WARPS, int ld = 0) {
     CgGeom g{};
     g.kp = kp;
+    g.ld = ld > 0 ? ld : kp;
     g.kw = kp < 32 ? kp : 32;
     g.G = kp / g.kw;
     g.rpw = 32 / g.kw;
-    g.slots = (CG_WARPS / g.G) * g.rpw;                 // sub-blocks per CTA pass
+    g.slots = (warps / g.G) * g.rpw;                    // sub-blocks per CTA pass
     g.P = g.slots >= CG_CH ? 1 : CG_CH / g.slots;       // passes per claim
     g.subs = g.slots * g.P;                             // sub-blocks per claim (multiple of CG_CH)
     g.cpc = g.subs / CG_CH;                             // chunks per claim
@@ -1258,6 +1533,7 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     CGA(Sc.active, sizeof(int) * kp);
     CGA(Sc.iters, sizeof(int) * kp);
     CGA(Sc.status, sizeof(int) * kp);
+    CGA(Sc.flush, sizeof(int) * kp);
     CGA(Sc.nactive, sizeof(int));
     int64_t part_max = 1;                     // largest nchunks*kp over the layouts compaction can reach
     for (int w = 1; w <= kp; w *= 2) part_max = std::max<int64_t>(part_max, make_geom(im, w, n).nchunks * w);
@@ -1286,21 +1562,22 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
 }
 
 // repack the live lanes into a layout of width kp_new (host decides the map)
-static int cg_repack(CocgImpl *im, int kp_old, int kp_new, const std::vector<int> &map,
+static int cg_repack(CocgImpl *im, int kp_old, int ld_old, int kp_new, int ld_new, const std::vector<int> &map,
                      const std::vector<int> &drop_mask, std::vector<int> &lane_shift,
                      cudaStream_t st, std::string &err) {
     const int64_t n = im->M.n;
     // 1) frozen lanes being dropped: x -> full-width solution
     CGK(cudaMemcpyAsync(im->mask, drop_mask.data(), sizeof(int) * kp_old, cudaMemcpyHostToDevice, st));
-    const int64_t t_old = n * kp_old;
-    k_cg_scatter_x<<<(unsigned)((t_old + 255) / 256), 256, 0, st>>>(im->V.x, im->xout, n, kp_old, im->kp_full,
+    const int64_t t_old = n * ld_old;
+    k_cg_scatter_x<<<(unsigned)((t_old + 255) / 256), 256, 0, st>>>(im->V.x, im->V.p, im->Sc.alpha, im->Sc.flush,
+                                                                   im->xout, n, ld_old, im->kp_full,
                                                                    im->lane_shift, im->mask);
     // 2) live vectors x, r, z, p(current) -> new width, through the scratch array
     CGK(cudaMemcpyAsync(im->map, map.data(), sizeof(int) * kp_new, cudaMemcpyHostToDevice, st));
-    const int64_t t_new = n * kp_new;
+    const int64_t t_new = n * ld_new;
     c128 **vecs[4] = {&im->V.x, &im->V.z, &im->V.p, &im->V.q};
     for (c128 **v : vecs) {
-        k_cg_repack<<<(unsigned)((t_new + 255) / 256), 256, 0, st>>>(*v, im->scratch, n, kp_old, kp_new, im->map);
+        k_cg_repack<<<(unsigned)((t_new + 255) / 256), 256, 0, st>>>(*v, im->scratch, n, ld_old, ld_new, im->map);
         std::swap(*v, im->scratch);
     }
     k_cg_repack_scalars<<<1, 32, 0, st>>>(im->Sc, kp_new, im->map);
@@ -1334,6 +1611,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
         }
         CGK(cudaMemcpyAsync(im->Sc.tolsq, tsq.data(), sizeof(double) * kp, cudaMemcpyHostToDevice, st));
     }
+    int ld = kp;   // lanes stored per row
     CgGeom g = make_geom(im, kp, n);
     int grid = grid_for(im, g, n);
     const double nnzb = 28.0 * (double)cg.nnz + 4.0 * (double)(n + 1);   // CSR pattern + 3 value arrays
@@ -1377,7 +1655,26 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     static const bool batch_all = getenv("REXI_COCG_BATCH") != nullptr;   // A/B switch
     for (;;) {
         for (int s = 0; s < check_every; ++s) {
-            hook_begin(cg, width_name("cg_spmv", kp), 80.0 * n * live + nnzb);
+            hook_begin(cg, width_name("cg_spmv", kp), (CG_DEFER_X ? 112.0 : 80.0) * n * live + nnzb);
+#if CG_DEFER_X
+            static const bool no_tma = getenv("REXI_COCG_NOTMA") != nullptr;   // A/B switch
+            if (!no_tma && !im->cplx && (kp == 32 || kp == 64) && im->stage_ok[kp / 32 == 2 ? 1 : 2] &&
+                cg.nnz <= (int64_t)CG_GB * n) {
+                // widest layouts, short rows (2D stencils): persistent TMA-pipelined spmv,
+                // one CTA per SM (cfg 3 steps 2-4 -3.6 % with the live-prefix row stride;
+                // 15-entry 3D rows keep the staged kernel, whose larger L1 serves their
+                // gathers: cfg 5 +5 % with this one; scripts/tune_tma.sh, tune_ld.sh)
+                const CgGeom gt = make_geom(im, kp, n, CGT_CW, ld);
+                static bool tma_attr = false;
+                if (!tma_attr) {
+                    CGK(cudaFuncSetAttribute(k_cg_spmv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)tma_smem_bytes()));
+                    tma_attr = true;
+                }
+                const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(gt.nclaims, (int64_t)im->sms));
+                k_cg_spmv_tma<<<gg, CGT_NT, tma_smem_bytes(), st>>>(im->M, im->V, im->Sc, S, gt);
+            } else
+#endif
             if (g.cpc <= 2 && im->stage_ok[g.cpc]) {
                 const size_t sm = st_smem_bytes(im->cplx);
                 static bool attr_set = false;
@@ -1406,7 +1703,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             }
             k_cg_finish<1><<<finish_grid(g), CG_FL_NT, finish_smem(1), st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
-            hook_begin(cg, width_name("cg_update", kp), 96.0 * n * live + 24.0 * n);
+            hook_begin(cg, width_name("cg_update", kp), (CG_DEFER_X ? 48.0 : 96.0) * n * live + 24.0 * n);
             if (g.kp == 1) {
                 const int g1 = (int)std::min<int64_t>((g.nchunks + 7) / 8, (int64_t)im->sms * 16);
                 k_cg_update1<<<g1, CG1_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);
@@ -1466,14 +1763,21 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             }
             const int live = (int)map.size();
             for (int l = live; l < kp_new; ++l) map.push_back(map[0]);
-            int rc = cg_repack(im, kp, kp_new, map, drop, lane_shift, st, err);
+            // rows keep only the live prefix (rounded up to whole 128-B lines on
+            // the wide layouts, to 32-B sectors below): what the kernels stream
+            // -- the TMA spmv moves whole rows -- follows the live lanes
+            static const bool no_ld = getenv("REXI_COCG_NOLD") != nullptr;   // A/B switch
+            const int gran = kp_new >= 16 ? 8 : 2;
+            const int ld_new = no_ld ? kp_new : std::min(kp_new, (live + gran - 1) / gran * gran);
+            int rc = cg_repack(im, kp, ld, kp_new, ld_new, map, drop, lane_shift, st, err);
             if (rc) return rc;
             std::vector<int> act(kp_new, 1);
             valid.assign(kp_new, 1);
             for (int l = live; l < kp_new; ++l) act[l] = valid[l] = 0;
             CGK(cudaMemcpyAsync(im->Sc.active, act.data(), sizeof(int) * kp_new, cudaMemcpyHostToDevice, st));
             kp = kp_new;
-            g = make_geom(im, kp, n);
+            ld = ld_new;
+            g = make_geom(im, kp, n, CG_WARPS, ld);
             grid = grid_for(im, g, n);
         }
     }
@@ -1483,7 +1787,8 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     CGK(cudaMemcpyAsync(h_it.data(), im->Sc.iters, sizeof(int) * kp, cudaMemcpyDeviceToHost, st));
     // remaining valid lanes' x -> full-width solution
     CGK(cudaMemcpyAsync(im->mask, valid.data(), sizeof(int) * kp, cudaMemcpyHostToDevice, st));
-    k_cg_scatter_x<<<(unsigned)((n * kp + 255) / 256), 256, 0, st>>>(im->V.x, im->xout, n, kp, im->kp_full,
+    k_cg_scatter_x<<<(unsigned)((n * ld + 255) / 256), 256, 0, st>>>(im->V.x, im->V.p, im->Sc.alpha, im->Sc.flush,
+                                                                    im->xout, n, ld, im->kp_full,
                                                                     im->lane_shift, im->mask);
     CGK(cudaGetLastError());
     CGK(cudaStreamSynchronize(st));

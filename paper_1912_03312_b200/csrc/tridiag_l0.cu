@@ -223,9 +223,10 @@ __device__ __forceinline__ c128 pick_last(const c128 (&y)[M], int cnt) {
 __device__ __forceinline__ c128 tile_c128(c128 v) { return v; }
 __device__ __forceinline__ c128 tile_c128(c64 v) { return to_c128(v); }
 
-template <int M, typename TT = c128>
+// KP > 0: k_pad known at compile time (the lane loop unrolls, offsets become immediates)
+template <int M, typename TT = c128, int KP = 0>
 __device__ __forceinline__ void reduce_rows(const TT *tile, const L0Args &a, int64_t row0) {
-    const int kp = a.S.kp;
+    const int kp = KP ? KP : a.S.kp;
     const int rows = (L0_NT / kp) * M;
     const int tpr = L0_NT / rows > 0 ? L0_NT / rows : 1;
     const int sub = threadIdx.x % tpr;
@@ -235,6 +236,7 @@ __device__ __forceinline__ void reduce_rows(const TT *tile, const L0Args &a, int
         // the lanes are grouped (k_pad, sharding): a plain fp64 chain here
         // broke the bitwise sharded-vs-single equality of the refined path
         ddacc re = {0.0, 0.0}, im = {0.0, 0.0};
+#pragma unroll
         for (int jj = sub; jj < kp; jj += tpr) {
             const c128 b = a.S.beta[jj];
             const c128 x = tile_c128(tile[r * kp + jj]);
@@ -321,10 +323,10 @@ struct Ctx {
 
 // DIV: integer division (S1: the shift form measured 0.204 -> 0.218 ms there,
 // its register allocation spilling 92 instead of 60 B)
-template <bool DIV = false>
+template <bool DIV = false, int KP = 0>
 __device__ __forceinline__ Ctx make_ctx(const L0Args &a, int M) {
     Ctx c;
-    c.kp = a.S.kp;
+    c.kp = KP ? KP : a.S.kp;
     const int lk = lg2(c.kp);
     const int bpc = DIV ? L0_NT / c.kp : L0_NT >> lk;
     c.b = DIV ? threadIdx.x / c.kp : threadIdx.x >> lk;
@@ -368,20 +370,21 @@ __device__ __forceinline__ void s1_body(const L0Args &a, const L0Layout &l, cons
 // device address space, which makes the host->device transfer of a host-buffer
 // step part of this kernel instead of a separate copy in front of it.  The rhs
 // rows go to rhs0 for K2 / S3ACC (padding rows stay zero).
-template <int M>
+template <int M, int KP>
 #ifndef S1_MINB
 #define S1_MINB 4   // 128 registers + 60 B spills, 7 % faster than 3 CTAs/SM without (scripts/tune_l0minb.sh)
 #endif
 __global__ void __launch_bounds__(L0_NT, S1_MINB) k_l0_s1(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int FL = ST_RHS | ST_BDIA;
-    const L0Layout l = carve(smem, a.S.kp, M, FL);
-    const Ctx c = make_ctx<true>(a, M);
+    const int kp_ = KP ? KP : a.S.kp;
+    const L0Layout l = carve(smem, kp_, M, FL);
+    const Ctx c = make_ctx<true, KP>(a, M);
     uint64_t *bar_u = reinterpret_cast<uint64_t *>(smem) + 1;
     if (threadIdx.x == 0 && a.u_bulk) mbar_init(bar_u, 1);   // fenced with l0_stage's barrier init
     l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, FL & ~ST_RHS);
     // u rows row0-1 .. row0+T, slots outside [0, n) zero
-    c128 *su = reinterpret_cast<c128 *>(smem + ((l0_smem_bytes(a.S.kp, M, FL) + 15) & ~(size_t)15));   // T+2 slots after the carve
+    c128 *su = reinterpret_cast<c128 *>(smem + ((l0_smem_bytes(kp_, M, FL) + 15) & ~(size_t)15));   // T+2 slots after the carve
     const int64_t n = a.nout;
     const int64_t i0 = max(c.row0 - 1, (int64_t)0), i1 = min(c.row0 + (int64_t)l.T + 1, n);
     if (a.u_bulk) {
@@ -656,13 +659,16 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
 }
 
 constexpr int K2_FLAGS = K2_ONE_TILE ? (ST_RHS | ST_DIA | ST_R32) : (ST_RHS | ST_DIA | ST_TILE2 | ST_R32);
-template <int M, bool EXACT>
+// KP: k_pad at compile time for the common K = 64 (0: runtime).  At runtime
+// k_pad a fifth of K2's instructions were integer address arithmetic
+// (ncu source view, profiles/r02_k2_sass_regions.txt).
+template <int M, bool EXACT, int KP>
 __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int flags = K2_FLAGS;
-    const L0Layout l = carve(smem, a.S.kp, M, flags);
+    const L0Layout l = carve(smem, KP ? KP : a.S.kp, M, flags);
     c128 *const xt = K2_ONE_TILE ? l.t0 : l.t1;
-    const Ctx c = make_ctx(a, M);
+    const Ctx c = make_ctx<false, KP>(a, M);
     l0_stage(smem, l, a, a.L.invd, nullptr, c.row0, flags & ~ST_TILE2);
 #ifndef K2_PF
 #define K2_PF 1
@@ -700,7 +706,7 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
         for (int q = 0; q < M; ++q) tc[q * c.kp] = cmk(0.0, 0.0);
     }
     __syncthreads();
-    reduce_rows<M>(xt, a, c.row0);
+    reduce_rows<M, c128, KP>(xt, a, c.row0);
     if (!c.active) return;
     if (a.L.sym) k2_refine<M, true, EXACT, true>(a, l, c, xs, xn, y, xt, hx, hy);
     else k2_refine<M, true, EXACT, false>(a, l, c, xs, xn, y, xt, hx, hy);
@@ -731,15 +737,15 @@ __host__ __device__ inline size_t k3_smem_bytes(int kp, int M) {
     return 128 + (size_t)T * kp * sizeof(c64) + 6 * (size_t)k3_tp4(T) * sizeof(float);
 }
 
-template <int M>
+template <int M, int KP>
 __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int kp = a.S.kp;
+    const int kp = KP ? KP : a.S.kp;
     const int T = (L0_NT >> lg2(kp)) * M, Tp4 = k3_tp4(T);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
     c64 *tile = reinterpret_cast<c64 *>(smem + 128);
     float *rows = reinterpret_cast<float *>(tile + (size_t)T * kp);
-    const Ctx c = make_ctx<K3_DIV>(a, M);
+    const Ctx c = make_ctx<K3_DIV, KP>(a, M);
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
@@ -791,7 +797,7 @@ __global__ void __launch_bounds__(L0_NT, K3_MINB) k_l0_k3(L0Args a) {
         for (int q = 0; q < M; ++q) ti[q * kp] = c64mk(0.f, 0.f);
     }
     __syncthreads();
-    reduce_rows<M, c64>(tile, a, c.row0);
+    reduce_rows<M, c64, KP>(tile, a, c.row0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1257,8 +1263,9 @@ int l0_graph_role(cudaGraphNode_t node) {
     if (cudaGraphNodeGetType(node, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) return 0;
     cudaKernelNodeParams p{};
     if (cudaGraphKernelNodeGetParams(node, &p) != cudaSuccess) return 0;
-    if (p.func == (void *)k_l0_s1<TRI_M>) return 1;
-    if (p.func == (void *)k_l0_k3<TRI_M> || p.func == (void *)k_l0_s3acc<TRI_M>) {
+    if (p.func == (void *)k_l0_s1<TRI_M, 0> || p.func == (void *)k_l0_s1<TRI_M, 64>) return 1;
+    if (p.func == (void *)k_l0_k3<TRI_M, 0> || p.func == (void *)k_l0_k3<TRI_M, 64> ||
+        p.func == (void *)k_l0_s3acc<TRI_M>) {
         const L0Args *a = reinterpret_cast<const L0Args *>(p.kernelParams[0]);
         return a->final_out ? 2 : 0;
     }
@@ -1283,6 +1290,14 @@ cudaError_t l0_graph_patch(cudaGraphExec_t exec, cudaGraphNode_t node, int role,
 }
 
 bool l0v2_supported(int kp) { return kp <= L0_NT; }
+// REXI_L0_KP: bit mask of the level-0 kernels that take their k_pad = 64
+// instantiation (1: S1, 2: K2, 4: K3; A/B switch).  scripts/tune_l0kp.sh on
+// cfg 2: K2 0.70 -> 0.673 ms, K3 0.270 -> 0.249 ms, S1 unchanged (HBM-bound;
+// its k_pad = 64 form spills more), so S1 keeps the runtime form.
+static int l0_kp_mask() {
+    static const int m = getenv("REXI_L0_KP") ? atoi(getenv("REXI_L0_KP")) : 6;
+    return m;
+}
 int64_t l0_row_padding() { return (int64_t)L0_NT * TRI_M + 2 * L0_ROWPAD; }
 
 cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *u, c128 *rhs0,
@@ -1296,7 +1311,7 @@ cudaError_t l0_launch_s1(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
     const int64_t rows = (int64_t)(L0_NT / kp) * TRI_M;
     const int64_t grid = (L.n + rows - 1) / rows;
     const size_t smem = l0_smem_bytes(kp, TRI_M, ST_RHS | ST_BDIA) + extra;
-    auto kern = k_l0_s1<TRI_M>;
+    auto kern = (kp == 64 && (l0_kp_mask() & 1)) ? k_l0_s1<TRI_M, 64> : k_l0_s1<TRI_M, 0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)grid, L0_NT, smem, st>>>(a);
@@ -1328,8 +1343,9 @@ cudaError_t l0_launch_k2(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
         if (const char *e = getenv("REXI_K2_PF")) a.pf_dist = (int64_t)(atof(e) * sms * K2_MINB);
     }
     for (int q = 0; q < 6; ++q) a.r32[q] = r32[q];
-    if (exact_residual) return launch_l0(k_l0_k2<TRI_M, true>, a, K2_FLAGS, st);
-    return launch_l0(k_l0_k2<TRI_M, false>, a, K2_FLAGS, st);
+    if (exact_residual) return launch_l0(k_l0_k2<TRI_M, true, 0>, a, K2_FLAGS, st);
+    if (S.kp == 64 && (l0_kp_mask() & 2)) return launch_l0(k_l0_k2<TRI_M, false, 64>, a, K2_FLAGS, st);
+    return launch_l0(k_l0_k2<TRI_M, false, 0>, a, K2_FLAGS, st);
 }
 
 cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, const c128 *X1,
@@ -1344,7 +1360,7 @@ cudaError_t l0_launch_k3(const L0Dev &z, const LevelDev &L, const ShiftDev &S, c
     const int64_t rows = (int64_t)(L0_NT / kp) * TRI_M;
     const int64_t grid = (L.n + rows - 1) / rows;
     const size_t smem = k3_smem_bytes(kp, TRI_M);
-    auto kern = k_l0_k3<TRI_M>;
+    auto kern = (kp == 64 && (l0_kp_mask() & 4)) ? k_l0_k3<TRI_M, 64> : k_l0_k3<TRI_M, 0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)grid, L0_NT, smem, st>>>(a);
