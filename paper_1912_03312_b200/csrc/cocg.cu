@@ -768,6 +768,237 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_tma(CgMat M, CgVec V, CgS
 #endif
 
 // ---------------------------------------------------------------------------
+// spmv, widest layouts of 2D-like patterns (kp = 64 or 128, real A): every
+// operand arrives by bulk copy.  Rows are processed in stages of R = 1024 / kp
+// rows.  At plan creation the columns of every stage are grouped into at most
+// three runs of consecutive rows ("z windows": for a structured 2D mesh the
+// lines above, around and below the stage's rows), and the stage's matrix
+// slice is packed into one blob (local indptr, the window slot of every
+// entry's column as uint16, fl(tau a), b).  The producer warp claims 32-row
+// chunks from the atomic counter and, per stage, bulk-copies the p, q, x
+// tiles, the z windows and the blob into one of two shared-memory stages; the
+// consumers read every operand from shared memory -- no load latency in the
+// row loop at all -- update the tiles in place, and the producer bulk-stores
+// them.  L2 -> SM traffic equals the gather form's (each z row is fetched by
+// the ~3 stages whose windows hold it); what changes is that ~100 KB of loads
+// per SM are in flight whatever the consumers do.  Same rows per sub-block,
+// same operation order per lane, same partial tree: bitwise identical to the
+// other spmv kernels.
+// ---------------------------------------------------------------------------
+struct WinStage {                 // 64 B per stage
+    int64_t blob_off;             // byte offset of the stage's blob (16-B aligned)
+    int32_t blob_bytes;           // multiple of 16
+    int32_t off_zs, off_ta, off_b;   // byte offsets inside the blob (local indptr at 0)
+    int32_t wstart[3], wrows[3];  // z windows: first row, rows (0: unused)
+    int32_t own0;                 // window slot of the stage's first row
+    int32_t pad[3];
+};
+static_assert(sizeof(WinStage) == 64, "WinStage is one 64-B directory entry");
+
+struct CgWin {
+    const WinStage *dir = nullptr;
+    const unsigned char *blob = nullptr;
+    int blob_max = 0;             // largest blob, rounded up to 128 B
+    int64_t nstages = 0;
+};
+
+template <int KP> struct WinGeom {
+    static constexpr int R = (CGT_CT * 2) / KP;          // rows per stage: two row-lanes per consumer thread
+    static constexpr int NST = (CG_SB * CG_CH) / R;      // stages per 32-row chunk
+    static constexpr int ZMAX = KP == 64 ? 56 : 30;      // z-window rows per stage
+    static constexpr size_t tile_bytes = (size_t)R * KP * sizeof(c128);
+    static constexpr size_t zwin_bytes = (size_t)ZMAX * KP * sizeof(c128);
+};
+template <int KP>
+__host__ __device__ inline size_t win_smem_bytes(int blob_max) {
+    return 128 + 2 * (3 * WinGeom<KP>::tile_bytes + WinGeom<KP>::zwin_bytes + (size_t)blob_max);
+}
+
+#if CG_DEFER_X
+template <int KP>
+__global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g, CgWin W) {
+    using G = WinGeom<KP>;
+    constexpr int R = G::R, NST = G::NST;
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (*Sc.nactive == 0) return;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *done = reinterpret_cast<uint64_t *>(smem + 16);
+    int64_t *slot_q = reinterpret_cast<int64_t *>(smem + 32);
+    int4 *dirq = reinterpret_cast<int4 *>(smem + 64);   // per slot: blob offsets of zs / ta / b, own0
+    const size_t stage_bytes = 3 * G::tile_bytes + G::zwin_bytes + (size_t)W.blob_max;
+    const uint32_t ld = (uint32_t)g.ld;
+    if (threadIdx.x == 0) {
+        mbar_init(full, 1);
+        mbar_init(full + 1, 1);
+        mbar_init(done, 1);
+        mbar_init(done + 1, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x >= CGT_CT) {
+        // ---- producer ----
+        if (threadIdx.x != CGT_CT) return;
+        int64_t prev[2] = {0, 0};
+        uint32_t dph[2] = {0u, 0u};
+        auto store = [&](int s, int64_t gs) {
+            unsigned char *base = smem + 128 + (size_t)s * stage_bytes;
+            const int64_t R0 = gs * R;
+            const int64_t rows = min((int64_t)R, M.n - R0);
+            if (rows > 0) {
+                const uint32_t tb = (uint32_t)(rows * ld * sizeof(c128));
+                const size_t o = (size_t)R0 * ld;
+                bulk_s2g(V.p + o, base, tb);
+                bulk_s2g(V.q + o, base + G::tile_bytes, tb);
+                bulk_s2g(V.x + o, base + 2 * G::tile_bytes, tb);
+            }
+            bulk_commit();
+        };
+        int it = 0;
+        bool ended = false;
+        while (!ended) {
+            const int64_t chunk = (int64_t)atomicAdd(Sc.ctr, 1u);
+            for (int h = 0; h < NST; ++h, ++it) {
+                const int s = it & 1;
+                if (it >= 2) {
+                    mbar_wait(done + s, dph[s]);
+                    dph[s] ^= 1u;
+                    store(s, prev[s]);
+                    bulk_wait_read0();
+                }
+                if (chunk >= g.nchunks) {
+                    slot_q[s] = -1;
+                    mbar_arrive(full + s);
+                    ended = true;
+                    break;
+                }
+                const int64_t gs = chunk * NST + h;
+                slot_q[s] = gs;
+                prev[s] = gs;
+                const int64_t R0 = gs * R;
+                const int64_t rows = min((int64_t)R, M.n - R0);
+                if (rows <= 0) {            // stage past the last row of the last chunk
+                    mbar_arrive(full + s);
+                    continue;
+                }
+                unsigned char *base = smem + 128 + (size_t)s * stage_bytes;
+                const WinStage d = W.dir[gs];
+                dirq[s] = make_int4(d.off_zs, d.off_ta, d.off_b, d.own0);
+                const uint32_t tb = (uint32_t)(rows * ld * sizeof(c128));
+                const uint32_t rb = ld * (uint32_t)sizeof(c128);
+                const uint32_t zb = (uint32_t)(d.wrows[0] + d.wrows[1] + d.wrows[2]) * rb;
+                mbar_expect_tx(full + s, 3 * tb + zb + (uint32_t)d.blob_bytes);
+                const size_t o = (size_t)R0 * ld;
+                bulk_g2s(base, V.p + o, tb, full + s);
+                bulk_g2s(base + G::tile_bytes, V.q + o, tb, full + s);
+                bulk_g2s(base + 2 * G::tile_bytes, V.x + o, tb, full + s);
+                unsigned char *zw = base + 3 * G::tile_bytes;
+                uint32_t zo = 0;
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    if (d.wrows[k] > 0) {
+                        bulk_g2s(zw + zo, V.z + (size_t)d.wstart[k] * ld, (uint32_t)d.wrows[k] * rb, full + s);
+                        zo += (uint32_t)d.wrows[k] * rb;
+                    }
+                bulk_g2s(zw + G::zwin_bytes, W.blob + d.blob_off, (uint32_t)d.blob_bytes, full + s);
+            }
+        }
+        if (it >= 1) {   // the stage computed last sits in the other slot
+            const int s = (it - 1) & 1;
+            mbar_wait(done + s, dph[s]);
+            store(s, prev[s]);
+        }
+        bulk_wait0();
+        return;
+    }
+    // ---- consumers: two row-lanes per thread and stage ----
+    const int lane = threadIdx.x % KP;
+    const int lr0 = threadIdx.x / KP;
+    constexpr int LRS = CGT_CT / KP;                   // local-row distance of a thread's two rows
+    constexpr bool SAME = LRS == CG_CH;                // both rows belong to one sub-block (kp = 64)
+    const bool act = Sc.active[lane] != 0;
+    const bool fl = !act && Sc.flush[lane] != 0;
+    const c128 sg = S.sigma[g.lane_shift[lane]];
+    const c128 beta = Sc.beta[lane];
+    const c128 alpha = Sc.alpha[lane];
+    uint32_t fph[2] = {0u, 0u};
+    c128 mu[2] = {cmk(0.0, 0.0), cmk(0.0, 0.0)};
+    for (int it = 0;; ++it) {
+        const int s = it & 1;
+        mbar_wait(full + s, fph[s]);
+        fph[s] ^= 1u;
+        const int64_t gs = slot_q[s];
+        if (gs < 0) break;
+        const int h = (int)(gs % NST);
+        const int64_t chunk = gs / NST;
+        unsigned char *base = smem + 128 + (size_t)s * stage_bytes;
+        c128 *tp = reinterpret_cast<c128 *>(base);
+        c128 *tq = reinterpret_cast<c128 *>(base + G::tile_bytes);
+        c128 *tx = reinterpret_cast<c128 *>(base + 2 * G::tile_bytes);
+        c128 *zw = reinterpret_cast<c128 *>(base + 3 * G::tile_bytes);
+        const int64_t R0 = gs * R;
+        const int rows = (int)min((int64_t)R, M.n - R0);
+        if (h == 0) mu[0] = mu[1] = cmk(0.0, 0.0);
+        if (rows > 0 && (act || fl)) {
+            const unsigned char *blob = base + 3 * G::tile_bytes + G::zwin_bytes;
+            const int4 dq = dirq[s];
+            const int off_zs = dq.x, off_ta = dq.y, off_b = dq.z, own0 = dq.w;
+            const int *ip = reinterpret_cast<const int *>(blob);
+            const unsigned short *zs = reinterpret_cast<const unsigned short *>(blob + off_zs);
+            const double *sta = reinterpret_cast<const double *>(blob + off_ta);
+            const double *stb = reinterpret_cast<const double *>(blob + off_b);
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int lr = lr0 + r * LRS;
+                if (lr < rows) {
+                    const uint32_t t = (uint32_t)lr * ld + lane;
+                    if (act) {
+                        const int q0 = ip[lr], q1 = ip[lr + 1];
+                        c128 acc = cmk(0.0, 0.0);
+#pragma unroll 4
+                        for (int q = q0; q < q1; ++q) {
+                            const c128 e = form_entry(sta[q], 0.0, stb[q], sg);
+                            acc = cadd(acc, cmul(e, zw[(uint32_t)zs[q] * ld + lane]));
+                        }
+                        const c128 po = tp[t];
+                        tx[t] = cadd(tx[t], cmul(alpha, po));
+                        const c128 pi = cadd(zw[(uint32_t)(own0 + lr) * ld + lane], cmul(beta, po));
+                        const c128 qi = cadd(acc, cmul(beta, tq[t]));
+                        tp[t] = pi;
+                        tq[t] = qi;
+                        mu[SAME ? 0 : r] = cadd(mu[SAME ? 0 : r], cmul(pi, qi));
+                    } else {
+                        tx[t] = cadd(tx[t], cmul(alpha, tp[t]));
+                    }
+                }
+            }
+        }
+        fence_proxy_async();         // tile writes -> visible to the bulk stores
+        bar_consumers();             // every consumer is done with the stage's z windows and tiles
+        if (h == NST - 1) {
+            // chunk partial: the sub-block partials go through the (now dead) z-window area
+            double2 *sbp = reinterpret_cast<double2 *>(zw);
+            if (SAME) {
+                sbp[lr0 * KP + lane] = mu[0];
+            } else {
+                sbp[lr0 * KP + lane] = mu[0];
+                sbp[(lr0 + LRS) * KP + lane] = mu[1];
+            }
+            bar_consumers();
+            if (threadIdx.x < KP) {
+                double2 sum = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int b = 0; b < CG_CH; ++b) sum = cadd(sum, sbp[b * KP + threadIdx.x]);
+                Sc.part_a[(size_t)chunk * KP + threadIdx.x] = sum;
+            }
+            fence_proxy_async();     // the partial slots will be overwritten by the next bulk load
+            bar_consumers();
+        }
+        if (threadIdx.x == 0) mbar_arrive(done + s);
+    }
+}
+#endif
+
+// ---------------------------------------------------------------------------
 // Width 1 (one live shift, the tail of a solve): one thread per row, a warp
 // per 32-row chunk.  The sub-block partial (rows b, b+8, b+16, b+24 summed
 // in that order from 0) and the chunk partial (sub-blocks 0..7 in order) are
@@ -1301,6 +1532,7 @@ struct CocgImpl {
     int *mask = nullptr;       // device [kp_full]
     int *h_buf = nullptr;      // pinned [2 + 2*kp_full]
     bool stage_ok[3] = {false, false, false};   // [cpc]: every claim's CSR slice fits the staging buffers
+    CgWin win[2];              // windowed spmv tables for kp = 64 / 128 (dir == nullptr: not available)
 };
 
 static int alloc_(CocgState &cg, void **p, size_t bytes, std::string &err) {
@@ -1348,6 +1580,102 @@ static CgGeom make_geom(const CocgImpl *im, int kp, int64_t n, int warps = CG_WA
 
 static int grid_for(const CocgImpl *im, const CgGeom &g, int64_t) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(g.nclaims, (int64_t)im->sms * 8));
+}
+
+// stage tables of the windowed spmv for layout width KP (see k_cg_spmv_win);
+// leaves w.dir == nullptr when some stage's columns do not fit three windows
+template <int KP>
+static int build_win(CocgState &cg, CocgImpl *im, const rexi_desc *d, const std::vector<double> &ta,
+                     const std::vector<double> &bb, CgWin &w, cudaStream_t st, std::string &err) {
+    using G = WinGeom<KP>;
+    constexpr int R = G::R;
+    const int64_t n = d->n;
+    const int64_t nchunks = (n + CG_SB * CG_CH - 1) / (CG_SB * CG_CH);
+    const int64_t nstages = nchunks * G::NST;
+    std::vector<WinStage> dir((size_t)nstages);
+    std::vector<unsigned char> blob;
+    blob.reserve((size_t)d->nnz * 19 + (size_t)nstages * 64);
+    int blob_max = 0;
+    std::vector<int32_t> cols;
+    auto al16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
+    for (int64_t gs = 0; gs < nstages; ++gs) {
+        WinStage e{};
+        const int64_t R0 = gs * R, R1 = std::min<int64_t>(n, R0 + R);
+        if (R0 >= n) {
+            dir[(size_t)gs] = e;
+            continue;
+        }
+        const int32_t Q0 = d->indptr[R0], Q1 = d->indptr[R1];
+        cols.assign(d->indices + Q0, d->indices + Q1);
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        std::vector<std::pair<int32_t, int32_t>> runs;   // [first, last]
+        for (int32_t c : cols) {
+            if (!runs.empty() && c == runs.back().second + 1) runs.back().second = c;
+            else runs.push_back({c, c});
+        }
+        while (runs.size() > 3) {   // merge the closest pair
+            size_t best = 0;
+            for (size_t k = 1; k + 1 < runs.size(); ++k)
+                if (runs[k + 1].first - runs[k].second < runs[best + 1].first - runs[best].second) best = k;
+            runs[best].second = runs[best + 1].second;
+            runs.erase(runs.begin() + (long)best + 1);
+        }
+        int total = 0, own0 = -1;
+        for (size_t k = 0; k < runs.size(); ++k) {
+            e.wstart[k] = runs[k].first;
+            e.wrows[k] = runs[k].second - runs[k].first + 1;
+            if (runs[k].first <= R0 && R1 - 1 <= runs[k].second) own0 = total + (int)(R0 - runs[k].first);
+            total += e.wrows[k];
+        }
+        if (total > G::ZMAX || own0 < 0 || Q1 - Q0 > 65535) return REXI_OK;   // not window-shaped: keep the gather kernels
+        e.own0 = own0;
+        const int rows = (int)(R1 - R0), nz = Q1 - Q0;
+        const size_t b_ip = al16(4 * (size_t)(rows + 1)), b_zs = al16(2 * (size_t)nz), b_v = al16(8 * (size_t)nz);
+        e.blob_off = (int64_t)blob.size();
+        e.off_zs = (int32_t)b_ip;
+        e.off_ta = (int32_t)(b_ip + b_zs);
+        e.off_b = (int32_t)(b_ip + b_zs + b_v);
+        e.blob_bytes = (int32_t)(b_ip + b_zs + 2 * b_v);
+        blob.resize(blob.size() + (size_t)e.blob_bytes, 0);
+        unsigned char *bp = blob.data() + e.blob_off;
+        int32_t *ipl = reinterpret_cast<int32_t *>(bp);
+        for (int r = 0; r <= rows; ++r) ipl[r] = d->indptr[R0 + r] - Q0;
+        unsigned short *zs = reinterpret_cast<unsigned short *>(bp + e.off_zs);
+        double *pa = reinterpret_cast<double *>(bp + e.off_ta), *pb = reinterpret_cast<double *>(bp + e.off_b);
+        for (int32_t q = Q0; q < Q1; ++q) {
+            const int32_t c = d->indices[q];
+            int base = 0, slot = -1;
+            for (size_t k = 0; k < runs.size(); ++k) {
+                if (c >= runs[k].first && c <= runs[k].second) {
+                    slot = base + (c - runs[k].first);
+                    break;
+                }
+                base += e.wrows[k];
+            }
+            zs[q - Q0] = (unsigned short)slot;
+            pa[q - Q0] = ta[(size_t)q];
+            pb[q - Q0] = bb[(size_t)q];
+        }
+        blob_max = std::max(blob_max, (int)e.blob_bytes);
+        dir[(size_t)gs] = e;
+    }
+    blob_max = (blob_max + 127) & ~127;
+    if (win_smem_bytes<KP>(blob_max) > 227 * 1024) return REXI_OK;
+    WinStage *ddir;
+    unsigned char *dblob;
+    CGA(ddir, sizeof(WinStage) * dir.size());
+    CGA(dblob, blob.size() + 16);
+    CGK(cudaMemcpyAsync(ddir, dir.data(), sizeof(WinStage) * dir.size(), cudaMemcpyHostToDevice, st));
+    CGK(cudaMemcpyAsync(dblob, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
+    CGK(cudaStreamSynchronize(st));   // the host vectors go out of scope
+    CGK(cudaFuncSetAttribute(k_cg_spmv_win<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)win_smem_bytes<KP>(blob_max)));
+    w.dir = ddir;
+    w.blob = dblob;
+    w.blob_max = blob_max;
+    w.nstages = nstages;
+    return REXI_OK;
 }
 
 int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine, cudaStream_t st,
@@ -1502,6 +1830,15 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
             im->M.classes = cl_;
         }
     }
+#if CG_DEFER_X
+    if (!im->cplx && !getenv("REXI_COCG_NOWIN") && nnz <= (int64_t)CG_GB * n) {
+        // windowed all-TMA spmv for the widest layouts (2D-like patterns)
+        int rc = REXI_OK;
+        if (kp >= 64) rc = build_win<64>(cg, im, d, ta, bb, im->win[0], st, err);
+        if (!rc && kp >= 128) rc = build_win<128>(cg, im, d, ta, bb, im->win[1], st, err);
+        if (rc) return rc;
+    }
+#endif
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&im->sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1658,7 +1995,16 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             hook_begin(cg, width_name("cg_spmv", kp), (CG_DEFER_X ? 112.0 : 80.0) * n * live + nnzb);
 #if CG_DEFER_X
             static const bool no_tma = getenv("REXI_COCG_NOTMA") != nullptr;   // A/B switch
-            if (!no_tma && !im->cplx && (kp == 32 || kp == 64) && im->stage_ok[kp / 32 == 2 ? 1 : 2] &&
+            const CgWin *wn = kp == 64 ? &im->win[0] : kp == 128 ? &im->win[1] : nullptr;
+            if (!no_tma && wn && wn->dir) {
+                // widest layouts of 2D-like patterns: every operand by bulk copy
+                const CgGeom gw = make_geom(im, kp, n, CG_WARPS, ld);
+                const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(gw.nchunks, (int64_t)im->sms));
+                if (kp == 64)
+                    k_cg_spmv_win<64><<<gg, CGT_NT, win_smem_bytes<64>(wn->blob_max), st>>>(im->M, im->V, im->Sc, S, gw, *wn);
+                else
+                    k_cg_spmv_win<128><<<gg, CGT_NT, win_smem_bytes<128>(wn->blob_max), st>>>(im->M, im->V, im->Sc, S, gw, *wn);
+            } else if (!no_tma && !im->cplx && (kp == 32 || kp == 64) && im->stage_ok[kp / 32 == 2 ? 1 : 2] &&
                 cg.nnz <= (int64_t)CG_GB * n) {
                 // widest layouts, short rows (2D stencils): persistent TMA-pipelined spmv,
                 // one CTA per SM (cfg 3 steps 2-4 -3.6 % with the live-prefix row stride;
