@@ -785,39 +785,46 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_tma(CgMat M, CgVec V, CgS
 // same operation order per lane, same partial tree: bitwise identical to the
 // other spmv kernels.
 // ---------------------------------------------------------------------------
-struct WinStage {                 // 64 B per stage
+constexpr int CG_NWIN = 8;        // z windows per stage (2D stencils use 3, 3D ones 7)
+struct WinStage {                 // 128 B per stage
     int64_t blob_off;             // byte offset of the stage's blob (16-B aligned)
     int32_t blob_bytes;           // multiple of 16
     int32_t off_zs, off_ta, off_b;   // byte offsets inside the blob (local indptr at 0)
-    int32_t wstart[3], wrows[3];  // z windows: first row, rows (0: unused)
+    int32_t wstart[CG_NWIN], wrows[CG_NWIN];   // z windows: first row, rows (0: unused)
     int32_t own0;                 // window slot of the stage's first row
-    int32_t pad[3];
+    int32_t pad[9];
 };
-static_assert(sizeof(WinStage) == 64, "WinStage is one 64-B directory entry");
+static_assert(sizeof(WinStage) == 128, "WinStage is one 128-B directory entry");
 
 struct CgWin {
     const WinStage *dir = nullptr;
     const unsigned char *blob = nullptr;
     int blob_max = 0;             // largest blob, rounded up to 128 B
     int64_t nstages = 0;
+    int rl = 2;                   // row-lanes per consumer thread and stage (2: 2D tables, 1: 3D)
 };
 
-template <int KP> struct WinGeom {
-    static constexpr int R = (CGT_CT * 2) / KP;          // rows per stage: two row-lanes per consumer thread
-    static constexpr int NST = (CG_SB * CG_CH) / R;      // stages per 32-row chunk
-    static constexpr int ZMAX = KP == 64 ? 56 : 30;      // z-window rows per stage
+// RL row-lanes per consumer thread and stage: 2 for 2D-like patterns (three
+// windows of R + 1..2 rows), 1 for 3D-like ones (seven windows: half the rows
+// per stage keep them inside the shared-memory budget)
+template <int KP, int RL> struct WinGeom {
+    static constexpr int R = (CGT_CT * RL) / KP;         // rows per stage
+    static constexpr int NST = R >= 32 ? 1 : (CG_SB * CG_CH) / R;   // stages per claim (a 32-row chunk)
+    static constexpr int CPS = R >= 32 ? R / 32 : 1;     // chunks per stage (kp <= 32)
+    // z-window rows per stage (what two ~110-KB stages leave after the tiles)
+    static constexpr int ZMAX = RL == 2 ? (KP == 128 ? 30 : KP == 64 ? 56 : 3 * R + 8) : (KP == 128 ? 44 : 72);
     static constexpr size_t tile_bytes = (size_t)R * KP * sizeof(c128);
     static constexpr size_t zwin_bytes = (size_t)ZMAX * KP * sizeof(c128);
 };
-template <int KP>
+template <int KP, int RL>
 __host__ __device__ inline size_t win_smem_bytes(int blob_max) {
-    return 128 + 2 * (3 * WinGeom<KP>::tile_bytes + WinGeom<KP>::zwin_bytes + (size_t)blob_max);
+    return 128 + 2 * (3 * WinGeom<KP, RL>::tile_bytes + WinGeom<KP, RL>::zwin_bytes + (size_t)blob_max);
 }
 
 #if CG_DEFER_X
-template <int KP>
+template <int KP, int RL>
 __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g, CgWin W) {
-    using G = WinGeom<KP>;
+    using G = WinGeom<KP, RL>;
     constexpr int R = G::R, NST = G::NST;
     extern __shared__ __align__(128) unsigned char smem[];
     if (*Sc.nactive == 0) return;
@@ -855,6 +862,7 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         };
         int it = 0;
         bool ended = false;
+        const int64_t nunits = (g.nchunks + G::CPS - 1) / G::CPS;   // claim unit: a chunk (kp >= 64) or a stage
         while (!ended) {
             const int64_t chunk = (int64_t)atomicAdd(Sc.ctr, 1u);
             for (int h = 0; h < NST; ++h, ++it) {
@@ -865,7 +873,7 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
                     store(s, prev[s]);
                     bulk_wait_read0();
                 }
-                if (chunk >= g.nchunks) {
+                if (chunk >= nunits) {
                     slot_q[s] = -1;
                     mbar_arrive(full + s);
                     ended = true;
@@ -885,7 +893,10 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
                 dirq[s] = make_int4(d.off_zs, d.off_ta, d.off_b, d.own0);
                 const uint32_t tb = (uint32_t)(rows * ld * sizeof(c128));
                 const uint32_t rb = ld * (uint32_t)sizeof(c128);
-                const uint32_t zb = (uint32_t)(d.wrows[0] + d.wrows[1] + d.wrows[2]) * rb;
+                uint32_t zr = 0;
+#pragma unroll
+                for (int k = 0; k < CG_NWIN; ++k) zr += (uint32_t)d.wrows[k];
+                const uint32_t zb = zr * rb;
                 mbar_expect_tx(full + s, 3 * tb + zb + (uint32_t)d.blob_bytes);
                 const size_t o = (size_t)R0 * ld;
                 bulk_g2s(base, V.p + o, tb, full + s);
@@ -894,7 +905,7 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
                 unsigned char *zw = base + 3 * G::tile_bytes;
                 uint32_t zo = 0;
 #pragma unroll
-                for (int k = 0; k < 3; ++k)
+                for (int k = 0; k < CG_NWIN; ++k)
                     if (d.wrows[k] > 0) {
                         bulk_g2s(zw + zo, V.z + (size_t)d.wstart[k] * ld, (uint32_t)d.wrows[k] * rb, full + s);
                         zo += (uint32_t)d.wrows[k] * rb;
@@ -910,11 +921,14 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         bulk_wait0();
         return;
     }
-    // ---- consumers: two row-lanes per thread and stage ----
+    // ---- consumers: RL row-lanes per thread and stage ----
+    static_assert(RL == 2 || KP >= 64, "one row-lane per thread: kp = 64 / 128 only");
     const int lane = threadIdx.x % KP;
     const int lr0 = threadIdx.x / KP;
     constexpr int LRS = CGT_CT / KP;                   // local-row distance of a thread's two rows
-    constexpr bool SAME = LRS == CG_CH;                // both rows belong to one sub-block (kp = 64)
+    constexpr bool SAME = LRS == CG_CH;                // a thread's rows all belong to sub-block lr0 (kp = 64);
+                                                       // kp = 128: to sub-blocks lr0 and lr0 + 4
+    constexpr bool TERMS = KP <= 32;                   // a stage holds whole chunks: per-row terms, summed in tree order
     const bool act = Sc.active[lane] != 0;
     const bool fl = !act && Sc.flush[lane] != 0;
     const c128 sg = S.sigma[g.lane_shift[lane]];
@@ -937,7 +951,7 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         c128 *zw = reinterpret_cast<c128 *>(base + 3 * G::tile_bytes);
         const int64_t R0 = gs * R;
         const int rows = (int)min((int64_t)R, M.n - R0);
-        if (h == 0) mu[0] = mu[1] = cmk(0.0, 0.0);
+        if (h == 0 || TERMS) mu[0] = mu[1] = cmk(0.0, 0.0);
         if (rows > 0 && (act || fl)) {
             const unsigned char *blob = base + 3 * G::tile_bytes + G::zwin_bytes;
             const int4 dq = dirq[s];
@@ -947,11 +961,13 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
             const double *sta = reinterpret_cast<const double *>(blob + off_ta);
             const double *stb = reinterpret_cast<const double *>(blob + off_b);
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
+            for (int r = 0; r < RL; ++r) {
                 const int lr = lr0 + r * LRS;
                 if (lr < rows) {
                     const uint32_t t = (uint32_t)lr * ld + lane;
                     if (act) {
+                        // accumulator of this row's sub-block (row h*R + lr of the chunk)
+                        const int a = SAME ? 0 : (((h * R + lr) % CG_CH) != lr0);
                         const int q0 = ip[lr], q1 = ip[lr + 1];
                         c128 acc = cmk(0.0, 0.0);
 #pragma unroll 4
@@ -965,7 +981,10 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
                         const c128 qi = cadd(acc, cmul(beta, tq[t]));
                         tp[t] = pi;
                         tq[t] = qi;
-                        mu[SAME ? 0 : r] = cadd(mu[SAME ? 0 : r], cmul(pi, qi));
+                        const c128 term = cmul(pi, qi);
+                        if (TERMS) mu[r] = term;
+                        else if (a == 0) mu[0] = cadd(mu[0], term);
+                        else mu[1] = cadd(mu[1], term);
                     } else {
                         tx[t] = cadd(tx[t], cmul(alpha, tp[t]));
                     }
@@ -974,7 +993,33 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         }
         fence_proxy_async();         // tile writes -> visible to the bulk stores
         bar_consumers();             // every consumer is done with the stage's z windows and tiles
-        if (h == NST - 1) {
+        if (TERMS) {
+            // the stage holds G::CPS whole chunks: per-row terms through the (now dead)
+            // z-window area, then each chunk's tree (sub-block b = rows b, b+8, b+16,
+            // b+24 in order from 0; the 8 sub-blocks in order from 0)
+            double2 *trm = reinterpret_cast<double2 *>(zw);
+            trm[lr0 * KP + lane] = mu[0];
+            if (RL == 2) trm[(lr0 + LRS) * KP + lane] = mu[1];
+            bar_consumers();
+            if (threadIdx.x < G::CPS * KP) {
+                const int cc = threadIdx.x / KP, ll = threadIdx.x % KP;
+                const int64_t chunk = gs * G::CPS + cc;
+                if (chunk < g.nchunks) {
+                    const double2 *tc = trm + (size_t)cc * (CG_SB * CG_CH) * KP + ll;
+                    double2 sum = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int b = 0; b < CG_CH; ++b) {
+                        double2 sb = make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int k = 0; k < CG_SB; ++k) sb = cadd(sb, tc[(b + k * CG_CH) * KP]);
+                        sum = cadd(sum, sb);
+                    }
+                    Sc.part_a[(size_t)chunk * KP + ll] = sum;
+                }
+            }
+            fence_proxy_async();
+            bar_consumers();
+        } else if (h == NST - 1) {
             // chunk partial: the sub-block partials go through the (now dead) z-window area
             double2 *sbp = reinterpret_cast<double2 *>(zw);
             if (SAME) {
@@ -989,6 +1034,159 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
 #pragma unroll
                 for (int b = 0; b < CG_CH; ++b) sum = cadd(sum, sbp[b * KP + threadIdx.x]);
                 Sc.part_a[(size_t)chunk * KP + threadIdx.x] = sum;
+            }
+            fence_proxy_async();     // the partial slots will be overwritten by the next bulk load
+            bar_consumers();
+        }
+        if (threadIdx.x == 0) mbar_arrive(done + s);
+    }
+}
+#endif
+
+// ---------------------------------------------------------------------------
+// update, widest layouts (kp = 64 or 128, real A): the same producer /
+// consumer pipeline for the pointwise half of the iteration.  Stages of
+// 2048 / kp rows (the z and q tiles, 32 KB each, plus the rows' diagonal data),
+// three in flight per SM, claims strided over the CTAs; four row-lanes per
+// consumer thread; only the z tile is stored.  Same per-lane arithmetic and
+// partial tree as k_cg_update: bitwise identical.
+// ---------------------------------------------------------------------------
+template <int KP> struct UpdGeom {
+    static constexpr int R = (CGT_CT * 4) / KP;          // rows per stage
+    static constexpr int NST = (CG_SB * CG_CH) / R;      // stages per 32-row chunk (1 or 2)
+    static constexpr int NSTG = 3;                       // pipeline stages
+    static constexpr size_t tile_bytes = (size_t)R * KP * sizeof(c128);
+    static constexpr size_t stage_bytes = 2 * tile_bytes + 512;   // z, q, dta[R], db[R]
+};
+template <int KP>
+__host__ __device__ inline size_t upd_smem_bytes() { return 128 + UpdGeom<KP>::NSTG * UpdGeom<KP>::stage_bytes; }
+
+#if CG_DEFER_X
+template <int KP>
+__global__ void __launch_bounds__(CGT_NT, 1) k_cg_update_tma(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g) {
+    using G = UpdGeom<KP>;
+    constexpr int R = G::R, NST = G::NST, NSTG = G::NSTG;
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (*Sc.nactive == 0) return;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);          // [3]
+    uint64_t *done = reinterpret_cast<uint64_t *>(smem + 32);     // [3]
+    const uint32_t ld = (uint32_t)g.ld;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < NSTG; ++k) {
+            mbar_init(full + k, 1);
+            mbar_init(done + k, 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    // this CTA's stages: chunks blockIdx.x, blockIdx.x + gridDim.x, ... (NST stages each)
+    const int64_t my_chunks = g.nchunks > blockIdx.x ? (g.nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int64_t my_stages = my_chunks * NST;
+    auto stage_of = [&](int64_t it) { return ((int64_t)blockIdx.x + (it / NST) * gridDim.x) * NST + it % NST; };
+    if (threadIdx.x >= CGT_CT) {
+        // ---- producer ----
+        if (threadIdx.x != CGT_CT) return;
+        uint32_t dph[NSTG] = {};
+        for (int64_t it = 0; it < my_stages + NSTG; ++it) {
+            const int s = (int)(it % NSTG);
+            if (it >= NSTG) {
+                // stage it - NSTG has been computed: store its z tile, free the slot
+                const int64_t gp = stage_of(it - NSTG);
+                mbar_wait(done + s, dph[s]);
+                dph[s] ^= 1u;
+                const int64_t R0 = gp * R;
+                const int64_t rows = min((int64_t)R, M.n - R0);
+                if (rows > 0) bulk_s2g(V.z + (size_t)R0 * ld, smem + 128 + (size_t)s * G::stage_bytes, (uint32_t)(rows * ld * sizeof(c128)));
+                bulk_commit();
+                if (it < my_stages) bulk_wait_read0();
+            }
+            if (it >= my_stages) continue;
+            const int64_t gs = stage_of(it);
+            const int64_t R0 = gs * R;
+            const int64_t rows = min((int64_t)R, M.n - R0);
+            if (rows <= 0) {
+                mbar_arrive(full + s);
+                continue;
+            }
+            unsigned char *base = smem + 128 + (size_t)s * G::stage_bytes;
+            const uint32_t tb = (uint32_t)(rows * ld * sizeof(c128));
+            const uint32_t db = (uint32_t)(((rows + 1) & ~(int64_t)1) * sizeof(double));
+            mbar_expect_tx(full + s, 2 * tb + 2 * db);
+            bulk_g2s(base, V.z + (size_t)R0 * ld, tb, full + s);
+            bulk_g2s(base + G::tile_bytes, V.q + (size_t)R0 * ld, tb, full + s);
+            bulk_g2s(base + 2 * G::tile_bytes, M.dta + R0, db, full + s);
+            bulk_g2s(base + 2 * G::tile_bytes + 256, M.db + R0, db, full + s);
+        }
+        bulk_wait0();
+        return;
+    }
+    // ---- consumers: four row-lanes per thread and stage ----
+    const int lane = threadIdx.x % KP;
+    const int lr0 = threadIdx.x / KP;
+    constexpr int LRS = CGT_CT / KP;                   // 8 (kp = 64: one sub-block per thread) or 4
+    const bool act = Sc.active[lane] != 0;
+    const c128 sg = S.sigma[g.lane_shift[lane]];
+    const c128 alpha = Sc.alpha[lane];
+    uint32_t fph[NSTG] = {};
+    c128 rho[2] = {cmk(0.0, 0.0), cmk(0.0, 0.0)};
+    double rn[2] = {0.0, 0.0};
+    for (int64_t it = 0; it < my_stages; ++it) {
+        const int s = (int)(it % NSTG);
+        mbar_wait(full + s, fph[s]);
+        fph[s] ^= 1u;
+        const int64_t gs = stage_of(it);
+        const int h = (int)(it % NST);
+        unsigned char *base = smem + 128 + (size_t)s * G::stage_bytes;
+        c128 *tz = reinterpret_cast<c128 *>(base);
+        c128 *tq = reinterpret_cast<c128 *>(base + G::tile_bytes);
+        const double *sdta = reinterpret_cast<const double *>(base + 2 * G::tile_bytes);
+        const double *sdb = reinterpret_cast<const double *>(base + 2 * G::tile_bytes + 256);
+        const int rows = (int)min((int64_t)R, M.n - gs * R);
+        if (h == 0) {
+            rho[0] = rho[1] = cmk(0.0, 0.0);
+            rn[0] = rn[1] = 0.0;
+        }
+        if (act) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int lr = lr0 + k * LRS;
+                if (lr < rows) {
+                    const uint32_t t = (uint32_t)lr * ld + lane;
+                    const c128 q = tq[t];
+                    const c128 d = form_entry(sdta[lr], 0.0, sdb[lr], sg);
+                    const c128 z = csub(tz[t], cmul(alpha, cdiv_c(q, d)));
+                    tz[t] = z;
+                    const c128 r = cmul(d, z);
+                    const int a = LRS == CG_CH ? 0 : (k & 1);
+                    rho[a] = cadd(rho[a], cmul(r, z));
+                    rn[a] += cabs2(r);
+                }
+            }
+        }
+        fence_proxy_async();         // z tile writes -> visible to the bulk store
+        bar_consumers();
+        if (h == NST - 1) {
+            // chunk partials: the sub-block partials go through the (now dead) q tile
+            double2 *sbc = reinterpret_cast<double2 *>(tq);
+            double *sbr = reinterpret_cast<double *>(sbc + CG_CH * KP);
+            sbc[lr0 * KP + lane] = rho[0];
+            sbr[lr0 * KP + lane] = rn[0];
+            if (LRS != CG_CH) {
+                sbc[(lr0 + LRS) * KP + lane] = rho[1];
+                sbr[(lr0 + LRS) * KP + lane] = rn[1];
+            }
+            bar_consumers();
+            if (threadIdx.x < KP) {
+                const int64_t chunk = gs / NST;
+                double2 sum = make_double2(0.0, 0.0);
+                double sr = 0.0;
+#pragma unroll
+                for (int b = 0; b < CG_CH; ++b) {
+                    sum = cadd(sum, sbc[b * KP + threadIdx.x]);
+                    sr += sbr[b * KP + threadIdx.x];
+                }
+                Sc.part_b[(size_t)chunk * KP + threadIdx.x] = sum;
+                Sc.part_c[(size_t)chunk * KP + threadIdx.x] = sr;
             }
             fence_proxy_async();     // the partial slots will be overwritten by the next bulk load
             bar_consumers();
@@ -1532,7 +1730,7 @@ struct CocgImpl {
     int *mask = nullptr;       // device [kp_full]
     int *h_buf = nullptr;      // pinned [2 + 2*kp_full]
     bool stage_ok[3] = {false, false, false};   // [cpc]: every claim's CSR slice fits the staging buffers
-    CgWin win[2];              // windowed spmv tables for kp = 64 / 128 (dir == nullptr: not available)
+    CgWin win[4];              // windowed spmv tables for kp = 16, 32, 64, 128 (dir == nullptr: not available)
 };
 
 static int alloc_(CocgState &cg, void **p, size_t bytes, std::string &err) {
@@ -1584,14 +1782,14 @@ static int grid_for(const CocgImpl *im, const CgGeom &g, int64_t) {
 
 // stage tables of the windowed spmv for layout width KP (see k_cg_spmv_win);
 // leaves w.dir == nullptr when some stage's columns do not fit three windows
-template <int KP>
+template <int KP, int RL>
 static int build_win(CocgState &cg, CocgImpl *im, const rexi_desc *d, const std::vector<double> &ta,
                      const std::vector<double> &bb, CgWin &w, cudaStream_t st, std::string &err) {
-    using G = WinGeom<KP>;
+    using G = WinGeom<KP, RL>;
     constexpr int R = G::R;
     const int64_t n = d->n;
     const int64_t nchunks = (n + CG_SB * CG_CH - 1) / (CG_SB * CG_CH);
-    const int64_t nstages = nchunks * G::NST;
+    const int64_t nstages = G::R >= 32 ? (nchunks + G::CPS - 1) / G::CPS : nchunks * G::NST;
     std::vector<WinStage> dir((size_t)nstages);
     std::vector<unsigned char> blob;
     blob.reserve((size_t)d->nnz * 19 + (size_t)nstages * 64);
@@ -1614,7 +1812,7 @@ static int build_win(CocgState &cg, CocgImpl *im, const rexi_desc *d, const std:
             if (!runs.empty() && c == runs.back().second + 1) runs.back().second = c;
             else runs.push_back({c, c});
         }
-        while (runs.size() > 3) {   // merge the closest pair
+        while (runs.size() > (size_t)CG_NWIN) {   // merge the closest pair
             size_t best = 0;
             for (size_t k = 1; k + 1 < runs.size(); ++k)
                 if (runs[k + 1].first - runs[k].second < runs[best + 1].first - runs[best].second) best = k;
@@ -1661,7 +1859,7 @@ static int build_win(CocgState &cg, CocgImpl *im, const rexi_desc *d, const std:
         dir[(size_t)gs] = e;
     }
     blob_max = (blob_max + 127) & ~127;
-    if (win_smem_bytes<KP>(blob_max) > 227 * 1024) return REXI_OK;
+    if (win_smem_bytes<KP, RL>(blob_max) > 227 * 1024) return REXI_OK;
     WinStage *ddir;
     unsigned char *dblob;
     CGA(ddir, sizeof(WinStage) * dir.size());
@@ -1669,8 +1867,9 @@ static int build_win(CocgState &cg, CocgImpl *im, const rexi_desc *d, const std:
     CGK(cudaMemcpyAsync(ddir, dir.data(), sizeof(WinStage) * dir.size(), cudaMemcpyHostToDevice, st));
     CGK(cudaMemcpyAsync(dblob, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
     CGK(cudaStreamSynchronize(st));   // the host vectors go out of scope
-    CGK(cudaFuncSetAttribute(k_cg_spmv_win<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)win_smem_bytes<KP>(blob_max)));
+    CGK(cudaFuncSetAttribute(k_cg_spmv_win<KP, RL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)win_smem_bytes<KP, RL>(blob_max)));
+    w.rl = RL;
     w.dir = ddir;
     w.blob = dblob;
     w.blob_max = blob_max;
@@ -1752,9 +1951,11 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
         }
         im->stage_ok[cpc] = ok;
     }
-    CGA(dta_, sizeof(double) * n);
-    CGA(dtai_, sizeof(double) * n);
-    CGA(db_, sizeof(double) * n);
+    CGA(dta_, sizeof(double) * n + 16);   // + padding: the TMA update rounds odd row counts up
+    CGA(dtai_, sizeof(double) * n + 16);
+    CGA(db_, sizeof(double) * n + 16);
+    CGK(cudaMemsetAsync(dta_, 0, sizeof(double) * n + 16, st));
+    CGK(cudaMemsetAsync(db_, 0, sizeof(double) * n + 16, st));
     CGK(cudaMemcpyAsync(ip, d->indptr, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, st));
     CGK(cudaMemcpyAsync(ix, d->indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
     CGK(cudaMemcpyAsync(ta_, ta.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
@@ -1831,11 +2032,17 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
         }
     }
 #if CG_DEFER_X
-    if (!im->cplx && !getenv("REXI_COCG_NOWIN") && nnz <= (int64_t)CG_GB * n) {
-        // windowed all-TMA spmv for the widest layouts (2D-like patterns)
+    if (!im->cplx && !getenv("REXI_COCG_NOWIN")) {
+        // windowed all-TMA spmv for the wide layouts: two row-lanes per thread where the
+        // stages' columns fit the window budget (2D-like patterns), else one (3D-like,
+        // kp >= 64 only), else the gather kernels stay
         int rc = REXI_OK;
-        if (kp >= 64) rc = build_win<64>(cg, im, d, ta, bb, im->win[0], st, err);
-        if (!rc && kp >= 128) rc = build_win<128>(cg, im, d, ta, bb, im->win[1], st, err);
+        if (kp >= 16) rc = build_win<16, 2>(cg, im, d, ta, bb, im->win[0], st, err);
+        if (!rc && kp >= 32) rc = build_win<32, 2>(cg, im, d, ta, bb, im->win[1], st, err);
+        if (!rc && kp >= 64) rc = build_win<64, 2>(cg, im, d, ta, bb, im->win[2], st, err);
+        if (!rc && kp >= 64 && !im->win[2].dir) rc = build_win<64, 1>(cg, im, d, ta, bb, im->win[2], st, err);
+        if (!rc && kp >= 128) rc = build_win<128, 2>(cg, im, d, ta, bb, im->win[3], st, err);
+        if (!rc && kp >= 128 && !im->win[3].dir) rc = build_win<128, 1>(cg, im, d, ta, bb, im->win[3], st, err);
         if (rc) return rc;
     }
 #endif
@@ -1995,15 +2202,22 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             hook_begin(cg, width_name("cg_spmv", kp), (CG_DEFER_X ? 112.0 : 80.0) * n * live + nnzb);
 #if CG_DEFER_X
             static const bool no_tma = getenv("REXI_COCG_NOTMA") != nullptr;   // A/B switch
-            const CgWin *wn = kp == 64 ? &im->win[0] : kp == 128 ? &im->win[1] : nullptr;
+            static const int win_min = getenv("REXI_COCG_WINMIN") ? atoi(getenv("REXI_COCG_WINMIN")) : 16;
+            const CgWin *wn = kp < win_min ? nullptr : kp == 16 ? &im->win[0] : kp == 32 ? &im->win[1]
+                            : kp == 64 ? &im->win[2] : kp == 128 ? &im->win[3] : nullptr;
             if (!no_tma && wn && wn->dir) {
-                // widest layouts of 2D-like patterns: every operand by bulk copy
+                // wide layouts of 2D-like patterns: every operand by bulk copy
                 const CgGeom gw = make_geom(im, kp, n, CG_WARPS, ld);
-                const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(gw.nchunks, (int64_t)im->sms));
-                if (kp == 64)
-                    k_cg_spmv_win<64><<<gg, CGT_NT, win_smem_bytes<64>(wn->blob_max), st>>>(im->M, im->V, im->Sc, S, gw, *wn);
-                else
-                    k_cg_spmv_win<128><<<gg, CGT_NT, win_smem_bytes<128>(wn->blob_max), st>>>(im->M, im->V, im->Sc, S, gw, *wn);
+                const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(wn->nstages, (int64_t)im->sms));
+#define REXI_WIN_LAUNCH(KPV, RLV) \
+    k_cg_spmv_win<KPV, RLV><<<gg, CGT_NT, win_smem_bytes<KPV, RLV>(wn->blob_max), st>>>(im->M, im->V, im->Sc, S, gw, *wn)
+                if (kp == 16) REXI_WIN_LAUNCH(16, 2);
+                else if (kp == 32) REXI_WIN_LAUNCH(32, 2);
+                else if (kp == 64 && wn->rl == 2) REXI_WIN_LAUNCH(64, 2);
+                else if (kp == 64) REXI_WIN_LAUNCH(64, 1);
+                else if (wn->rl == 2) REXI_WIN_LAUNCH(128, 2);
+                else REXI_WIN_LAUNCH(128, 1);
+#undef REXI_WIN_LAUNCH
             } else if (!no_tma && !im->cplx && (kp == 32 || kp == 64) && im->stage_ok[kp / 32 == 2 ? 1 : 2] &&
                 cg.nnz <= (int64_t)CG_GB * n) {
                 // widest layouts, short rows (2D stencils): persistent TMA-pipelined spmv,
@@ -2050,6 +2264,20 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             k_cg_finish<1><<<finish_grid(g), CG_FL_NT, finish_smem(1), st>>>(im->Sc, g, cg.k, cg.max_iters);
             hook_end(cg);
             hook_begin(cg, width_name("cg_update", kp), (CG_DEFER_X ? 48.0 : 96.0) * n * live + 24.0 * n);
+#if CG_DEFER_X
+            static const bool no_utma = getenv("REXI_COCG_NOUTMA") != nullptr;   // A/B switch
+            if (!no_utma && !no_tma && !im->cplx && (kp == 64 || kp == 128)) {
+                static bool uattr = false;
+                if (!uattr) {
+                    CGK(cudaFuncSetAttribute(k_cg_update_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem_bytes<64>()));
+                    CGK(cudaFuncSetAttribute(k_cg_update_tma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem_bytes<128>()));
+                    uattr = true;
+                }
+                const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(g.nchunks, (int64_t)im->sms));
+                if (kp == 64) k_cg_update_tma<64><<<gg, CGT_NT, upd_smem_bytes<64>(), st>>>(im->M, im->V, im->Sc, S, g);
+                else k_cg_update_tma<128><<<gg, CGT_NT, upd_smem_bytes<128>(), st>>>(im->M, im->V, im->Sc, S, g);
+            } else
+#endif
             if (g.kp == 1) {
                 const int g1 = (int)std::min<int64_t>((g.nchunks + 7) / 8, (int64_t)im->sms * 16);
                 k_cg_update1<<<g1, CG1_NT, 0, st>>>(im->M, im->V, im->Sc, S, g);

@@ -15,5 +15,10 @@ for name in ("p1_2d_m16", "p1_3d_m8", "fem_p2", "harness_p2"):
 c = fixtures.config3(m=96)
 stp = rexi_prepare(c.system, c.approx, c.tau, sr_value=c.sr, override_admissibility=True)
 out["cfg3_m96"] = rexi_run(stp, c.u0, 1)
+stp.close()
+c = fixtures.config5(m=28)
+stp = rexi_prepare(c.system, c.approx, c.tau, sr_value=c.sr, override_admissibility=True)
+out["cfg5_m28"] = rexi_run(stp, c.u0, 1)
+stp.close()
 np.savez(sys.argv[1], **out)
 print("saved", list(out))
