@@ -49,3 +49,27 @@ def test_stencil_classes_bitwise(c, m, refine, tmp_path):
     plain = _run(c, m, refine, 2, {"REXI_COCG_NOCLS": "1"}, tmp_path, "nocls")
     assert np.all(np.isfinite(plain))
     assert np.array_equal(classed, plain)
+
+
+# The TMA-pipelined kernels of the wide layouts -- the windowed spmv (p, q, x
+# tiles, z windows and the packed matrix blob by bulk copy; two row-lanes per
+# thread on 2D patterns, one on 3D patterns), the tile-only TMA spmv and the
+# TMA update -- keep the gather kernels' rows per sub-block, per-lane operation
+# order and partial tree: the step must be bitwise identical with each of them
+# switched off, and with the live-prefix row stride switched off.
+@pytest.mark.parametrize("c,m,refine", [(3, 64, 1), (4, 48, 1), (5, 14, 1), (3, 40, 0)])
+@pytest.mark.parametrize("off", ["REXI_COCG_NOTMA", "REXI_COCG_NOWIN", "REXI_COCG_NOUTMA", "REXI_COCG_NOLD"])
+def test_tma_kernels_bitwise(c, m, refine, off, tmp_path):
+    tma = _run(c, m, refine, 2, {}, tmp_path, "tma")
+    plain = _run(c, m, refine, 2, {off: "1"}, tmp_path, off.lower())
+    assert np.all(np.isfinite(plain))
+    assert np.array_equal(tma, plain)
+
+
+def test_window_tables_cover_ragged_sizes(tmp_path):
+    """Row counts that are not multiples of the stage / chunk sizes (the last
+    stage and the last chunk are partial): windowed vs gather kernels."""
+    for m in (33, 50, 71):
+        tma = _run(3, m, 1, 1, {}, tmp_path, f"rag{m}")
+        plain = _run(3, m, 1, 1, {"REXI_COCG_NOTMA": "1"}, tmp_path, f"rag{m}_plain")
+        assert np.array_equal(tma, plain), m
