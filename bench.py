@@ -99,16 +99,12 @@ def api_refine(cfg):
     return default_refine(ip, ix, cfg.tau, cfg.sr)
 
 
-NARROW_ITERS = 8   # cocg.cu cg_solve: check_every iterations per k_cg_narrow launch
-
-
 def cocg_8d_bytes(prof, n, nnz, k, steps):
     """SURVEY.md 8(d)'s algorithmic bytes of a COCG step: per lockstep
     iteration (20 nnz + 4 (N+1)) + 160 K_act N, plus 16 N (2 + 3K) for the
     prologue / epilogue; the refinement's dd-residual SpMVs count as extra
     iterations with K_act = K.  sum(K_act) over the iterations comes from the
-    spmv hooks' own byte counts (112 B per live row-shift + the CSR bytes; a
-    narrow-layout launch covers NARROW_ITERS whole iterations at 160 B)."""
+    spmv hooks' own byte counts (112 B per live row-shift + the CSR bytes)."""
     csr_impl = 28.0 * nnz + 4.0 * (n + 1)
     csr_8d = 20.0 * nnz + 4.0 * (n + 1)
     total, iters, kact_n = 0.0, 0, 0.0
@@ -116,9 +112,6 @@ def cocg_8d_bytes(prof, n, nnz, k, steps):
         if name.startswith("cg_spmv"):
             kact_n += max(0.0, (b - cnt * csr_impl) / 112.0)
             iters += cnt
-        elif name.startswith("cg_narrow"):
-            kact_n += max(0.0, (b - cnt * NARROW_ITERS * (24.0 * n + csr_impl)) / 160.0)
-            iters += cnt * NARROW_ITERS
         elif name.startswith("cg_residual"):
             kact_n += cnt * k * n
             iters += cnt

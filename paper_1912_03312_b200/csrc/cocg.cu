@@ -29,7 +29,6 @@
 // Refinement: r = b - S x with error-free products (double-double), one
 // correction solve, and the step output sum_j beta_j (x_j + dx_j) in
 // double-double.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -1297,279 +1296,6 @@ __global__ void __launch_bounds__(CG1_NT) k_cg_update1(CgMat M, CgVec V, CgScal 
 }
 
 // ---------------------------------------------------------------------------
-// Narrow layouts (kp = 1, 2: the tails of the hard shifts, ~40 % of a 2D
-// step's iterations): whole iterations in ONE cooperative launch.  At these
-// widths an iteration is four short launches (spmv, finish, update, finish:
-// 88 us at one lane of 1M rows, against ~25 us of L2 / HBM traffic); here the
-// phases are separated by grid barriers instead, and the vectors of one or
-// two lanes stay L2-resident across them.  A warp owns (32-row chunk, lane)
-// units; the chunk partials, the ranges of 64 chunks and the fan-in-64 upper
-// levels are summed in the finish kernels' order (upper levels redundantly in
-// every CTA, so every CTA holds alpha / beta and takes the same decisions),
-// and the per-lane scalar updates are finish_lane's.  Bitwise identical to
-// the launch-per-phase kernels.
-// ---------------------------------------------------------------------------
-constexpr int CGN_NT = 256;
-constexpr int CGN_WARPS = CGN_NT / 32;
-constexpr int CGN_MAXL2 = 256;    // level-2 values per lane a CTA can stage (n <= 32 * 64 * 64 * 256 rows)
-
-struct NarrowLane {
-    double2 rho, alpha, beta;
-    double rnorm2, bnorm2, tolsq;
-    int active, flush, iters, status;
-};
-
-// ordered sum (from zero) of src[(c0 .. c1) * stride + l]: the warp loads the
-// <= 64 values coalesced, every lane adds them in order (same result in all lanes)
-__device__ __forceinline__ double2 warp_ordered_sum_c(const double2 *src, int64_t c0, int64_t c1, int stride, int l) {
-    const int t = threadIdx.x & 31;
-    const int cnt = (int)(c1 - c0);
-    const double2 z = make_double2(0.0, 0.0);
-    const double2 v0 = t < cnt ? __ldcg(src + (c0 + t) * stride + l) : z;
-    const double2 v1 = t + 32 < cnt ? __ldcg(src + (c0 + 32 + t) * stride + l) : z;
-    double2 acc = z;
-    for (int k = 0; k < cnt; ++k) acc = cadd(acc, shfl_c(k < 32 ? v0 : v1, k & 31));
-    return acc;
-}
-__device__ __forceinline__ double warp_ordered_sum_r(const double *src, int64_t c0, int64_t c1, int stride, int l) {
-    const int t = threadIdx.x & 31;
-    const int cnt = (int)(c1 - c0);
-    const double v0 = t < cnt ? __ldcg(src + (c0 + t) * stride + l) : 0.0;
-    const double v1 = t + 32 < cnt ? __ldcg(src + (c0 + 32 + t) * stride + l) : 0.0;
-    double acc = 0.0;
-    for (int k = 0; k < cnt; ++k) acc = acc + __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31);
-    return acc;
-}
-
-// level 1 of the tree over the whole grid: range r = chunks [64 r, 64 r + 64)
-template <int KP, bool REAL>
-__device__ __forceinline__ void narrow_level1(const double2 *pa, const double *pc, double2 *pf, double *pg,
-                                              int64_t nchunks) {
-    const int64_t n1 = (nchunks + CG_RANGE - 1) / CG_RANGE;
-    const int64_t gw = (int64_t)blockIdx.x * CGN_WARPS + (threadIdx.x >> 5);
-    const int64_t nw = (int64_t)gridDim.x * CGN_WARPS;
-    for (int64_t u = gw; u < n1 * KP; u += nw) {
-        const int64_t r = u / KP;
-        const int l = (int)(u % KP);
-        const int64_t c0 = r * CG_RANGE, c1 = min(c0 + CG_RANGE, nchunks);
-        const double2 s = warp_ordered_sum_c(pa, c0, c1, KP, l);
-        double sr = 0.0;
-        if (REAL) sr = warp_ordered_sum_r(pc, c0, c1, KP, l);
-        if ((threadIdx.x & 31) == 0) {
-            pf[r * KP + l] = s;
-            if (REAL) pg[r * KP + l] = sr;
-        }
-    }
-}
-
-// upper levels, redundantly in every CTA: fin[l] (and finr[l]) = the tree's final values
-template <int KP, bool REAL>
-__device__ __forceinline__ void narrow_upper(const double2 *pf, const double *pg, int64_t nchunks, double2 *bufc,
-                                             double *bufr, double2 *fin, double *finr) {
-    const int64_t n1 = (nchunks + CG_RANGE - 1) / CG_RANGE;
-    const int t = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (n1 == 1) {
-        if (threadIdx.x < KP) {
-            fin[threadIdx.x] = __ldcg(pf + threadIdx.x);
-            if (REAL) finr[threadIdx.x] = __ldcg(pg + threadIdx.x);
-        }
-        __syncthreads();
-        return;
-    }
-    // level 2 from global (L2): one warp per (group, lane)
-    const int n2 = (int)((n1 + CG_RANGE - 1) / CG_RANGE);
-    for (int u = w; u < n2 * KP; u += CGN_WARPS) {
-        const int gi = u / KP, l = u % KP;
-        const int64_t c0 = (int64_t)gi * CG_RANGE, c1 = min(c0 + CG_RANGE, n1);
-        const double2 s = warp_ordered_sum_c(pf, c0, c1, KP, l);
-        double sr = 0.0;
-        if (REAL) sr = warp_ordered_sum_r(pg, c0, c1, KP, l);
-        if (t == 0) {
-            bufc[gi * KP + l] = s;
-            if (REAL) bufr[gi * KP + l] = sr;
-        }
-    }
-    __syncthreads();
-    // levels 3..: at most CGN_MAXL2 values per lane, in shared memory (ping-pong halves)
-    int ncur = n2, src = 0;
-    while (ncur > 1) {
-        const int nnext = (ncur + CG_RANGE - 1) / CG_RANGE;
-        const int dst = src ^ 1;
-        if (threadIdx.x < nnext * KP) {
-            const int gi = threadIdx.x / KP, l = threadIdx.x % KP;
-            const int c0 = gi * CG_RANGE, c1 = min(c0 + CG_RANGE, ncur);
-            double2 acc = make_double2(0.0, 0.0);
-            double accr = 0.0;
-            for (int c = c0; c < c1; ++c) {
-                acc = cadd(acc, bufc[src * CGN_MAXL2 * KP + c * KP + l]);
-                if (REAL) accr += bufr[src * CGN_MAXL2 * KP + c * KP + l];
-            }
-            bufc[dst * CGN_MAXL2 * KP + gi * KP + l] = acc;
-            if (REAL) bufr[dst * CGN_MAXL2 * KP + gi * KP + l] = accr;
-        }
-        __syncthreads();
-        ncur = nnext;
-        src = dst;
-    }
-    if (threadIdx.x < KP) {
-        fin[threadIdx.x] = bufc[src * CGN_MAXL2 * KP + threadIdx.x];
-        if (REAL) finr[threadIdx.x] = bufr[src * CGN_MAXL2 * KP + threadIdx.x];
-    }
-    __syncthreads();
-}
-
-#if CG_DEFER_X
-template <bool CPLX, int KP>
-__global__ void __launch_bounds__(CGN_NT, 4) k_cg_narrow(CgMat M, CgVec V, CgScal Sc, ShiftDev S, CgGeom g, int kreal,
-                                                         int max_iters, int niter) {
-    namespace cgr = cooperative_groups;
-    cgr::grid_group grid = cgr::this_grid();
-    __shared__ NarrowLane L[KP];
-    __shared__ int s_nactive;
-    __shared__ double2 bufc[2 * CGN_MAXL2 * KP];
-    __shared__ double bufr[2 * CGN_MAXL2 * KP];
-    __shared__ double2 fin[KP];
-    __shared__ double finr[KP];
-    if (threadIdx.x < KP) {
-        const int l = threadIdx.x;
-        NarrowLane &a = L[l];
-        a.rho = Sc.rho[l]; a.alpha = Sc.alpha[l]; a.beta = Sc.beta[l];
-        a.rnorm2 = Sc.rnorm2[l]; a.bnorm2 = Sc.bnorm2[l]; a.tolsq = Sc.tolsq[l];
-        a.active = Sc.active[l]; a.flush = Sc.flush[l]; a.iters = Sc.iters[l]; a.status = Sc.status[l];
-    }
-    if (threadIdx.x == 0) s_nactive = *Sc.nactive;
-    __syncthreads();
-    const int t = threadIdx.x & 31;
-    const int64_t gw = (int64_t)blockIdx.x * CGN_WARPS + (threadIdx.x >> 5);
-    const int64_t nw = (int64_t)gridDim.x * CGN_WARPS;
-    const int64_t nunits = g.nchunks * KP;
-    // contiguous units per warp-slot block: neighbouring warps share chunks / lanes (L1 lines)
-    const uint32_t ld = (uint32_t)g.ld;
-    c128 *__restrict__ pv = V.p;
-    c128 *__restrict__ qv = V.q;
-    c128 *__restrict__ xv = V.x;
-    c128 *__restrict__ zv = V.z;
-    for (int itn = 0; itn < niter && s_nactive != 0; ++itn) {
-        // ---- spmv ----
-        for (int64_t u = gw; u < nunits; u += nw) {
-            const int64_t c = u / KP;
-            const int l = (int)(u % KP);
-            const int64_t i = c * (CG_SB * CG_CH) + t;
-            const bool act = L[l].active != 0;
-            c128 term = cmk(0.0, 0.0);
-            if (act && i < M.n) {
-                const c128 sg = S.sigma[g.lane_shift[l]];
-                const c128 acc = row_sz<CPLX, true>(M, i, zv, ld, l, sg);
-                const uint32_t o = (uint32_t)i * ld + l;
-                const c128 po = pv[o];
-                xv[o] = cadd(xv[o], cmul(L[l].alpha, po));
-                const c128 pi = cadd(zv[o], cmul(L[l].beta, po));
-                const c128 qi = cadd(acc, cmul(L[l].beta, qv[o]));
-                pv[o] = pi;
-                qv[o] = qi;
-                term = cmul(pi, qi);
-            } else if (!act && L[l].flush && i < M.n) {
-                const uint32_t o = (uint32_t)i * ld + l;
-                xv[o] = cadd(xv[o], cmul(L[l].alpha, pv[o]));
-            }
-            const double2 sc = chunk_sum_c(term);
-            if (t == 0) Sc.part_a[(size_t)c * KP + l] = sc;
-        }
-        grid.sync();
-        narrow_level1<KP, false>(Sc.part_a, nullptr, Sc.part_f, nullptr, g.nchunks);
-        grid.sync();
-        narrow_upper<KP, false>(Sc.part_f, nullptr, g.nchunks, bufc, bufr, fin, finr);
-        if (threadIdx.x < KP) {   // finish_lane<1>
-            NarrowLane &a = L[threadIdx.x];
-            a.flush = 0;
-            if (a.active) {
-                const double2 sv = fin[threadIdx.x];
-                const double ms = cabs2(sv);
-                if (!(ms > 0.0) || !isfinite(ms)) {
-                    a.status = isfinite(ms) ? 1 : 2;
-                    a.active = 0;
-                    a.alpha = make_double2(0.0, 0.0);
-                } else {
-                    a.alpha = cdiv_c(a.rho, sv);
-                }
-            }
-        }
-        __syncthreads();
-        // ---- update ----
-        for (int64_t u = gw; u < nunits; u += nw) {
-            const int64_t c = u / KP;
-            const int l = (int)(u % KP);
-            const int64_t i = c * (CG_SB * CG_CH) + t;
-            c128 trho = cmk(0.0, 0.0);
-            double trn = 0.0;
-            if (L[l].active && i < M.n) {
-                const c128 sg = S.sigma[g.lane_shift[l]];
-                const uint32_t o = (uint32_t)i * ld + l;
-                const c128 q = qv[o];
-                const c128 d = form_entry(M.dta[i], M.dta_im[i], M.db[i], sg);
-                const c128 z = csub(zv[o], cmul(L[l].alpha, cdiv_c(q, d)));
-                zv[o] = z;
-                const c128 r = cmul(d, z);
-                trho = cmul(r, z);
-                trn = cabs2(r);
-            }
-            const double2 sc = chunk_sum_c(trho);
-            const double sr = chunk_sum_r(trn);
-            if (t == 0) {
-                Sc.part_b[(size_t)c * KP + l] = sc;
-                Sc.part_c[(size_t)c * KP + l] = sr;
-            }
-        }
-        grid.sync();
-        narrow_level1<KP, true>(Sc.part_b, Sc.part_c, Sc.part_f, Sc.part_g, g.nchunks);
-        grid.sync();
-        narrow_upper<KP, true>(Sc.part_f, Sc.part_g, g.nchunks, bufc, bufr, fin, finr);
-        if (threadIdx.x < KP) {   // finish_lane<2>
-            NarrowLane &a = L[threadIdx.x];
-            if (a.active) {
-                const double2 sv = fin[threadIdx.x];
-                const double sr = finr[threadIdx.x];
-                a.rnorm2 = sr;
-                a.iters += 1;
-                const double2 rho_old = a.rho;
-                if (!isfinite(sr) || !isfinite(sv.x) || !isfinite(sv.y)) {
-                    a.status = 2;
-                    a.active = 0;
-                } else if (sr <= a.tolsq * a.bnorm2) {
-                    a.active = 0;
-                } else if (!(cabs2(rho_old) > 0.0)) {
-                    a.status = 1;
-                    a.active = 0;
-                } else if (a.iters >= max_iters) {
-                    a.status = 3;
-                    a.active = 0;
-                } else {
-                    a.beta = cdiv_c(sv, rho_old);
-                    a.rho = sv;
-                }
-                if (!a.active) a.flush = 1;
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int na = 0;
-            for (int l = 0; l < KP; ++l) na += L[l].active;
-            s_nactive = na;
-        }
-        __syncthreads();
-    }
-    if (blockIdx.x == 0 && threadIdx.x < KP) {
-        const int l = threadIdx.x;
-        const NarrowLane &a = L[l];
-        Sc.rho[l] = a.rho; Sc.alpha[l] = a.alpha; Sc.beta[l] = a.beta;
-        Sc.rnorm2[l] = a.rnorm2;
-        Sc.active[l] = a.active; Sc.flush[l] = a.flush; Sc.iters[l] = a.iters; Sc.status[l] = a.status;
-        if (l == 0) *Sc.nactive = s_nactive;
-    }
-}
-#endif
-
-// ---------------------------------------------------------------------------
 // update: z -= alpha D^-1 q; partials of rho' = r^T z, |r|^2 with r = D z
 // (48 B per live row-shift: z read + written, q read; x += alpha p is deferred
 // to the next spmv, see CG_DEFER_X)
@@ -2005,8 +1731,6 @@ struct CocgImpl {
     int *h_buf = nullptr;      // pinned [2 + 2*kp_full]
     bool stage_ok[3] = {false, false, false};   // [cpc]: every claim's CSR slice fits the staging buffers
     CgWin win[4];              // windowed spmv tables for kp = 16, 32, 64, 128 (dir == nullptr: not available)
-    bool coop = false;         // the device supports cooperative launches (k_cg_narrow)
-    int narrow_bps[4] = {0, 0, 0, 0};   // resident CTAs per SM of k_cg_narrow<cplx, kp> (0: not queried, -1: none)
 };
 
 static int alloc_(CocgState &cg, void **p, size_t bytes, std::string &err) {
@@ -2325,11 +2049,6 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&im->sms, cudaDevAttrMultiProcessorCount, dev);
-    {
-        int coop = 0;
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-        im->coop = coop != 0;
-    }
     if ((double)n * kp >= 2147483647.0) {
         err = "COCG plan too large for 32-bit element offsets (n * k_pad >= 2^31); split the shifts";
         return REXI_ERR_UNSUPPORTED;
@@ -2479,39 +2198,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
     };
     static const bool batch_all = getenv("REXI_COCG_BATCH") != nullptr;   // A/B switch
     for (;;) {
-#if CG_DEFER_X
-        // one or two lanes: check_every whole iterations in one cooperative launch
-        static const bool no_narrow = getenv("REXI_COCG_NONARROW") != nullptr;   // A/B switch
-        const int64_t n2_ = ((g.nchunks + CG_RANGE - 1) / CG_RANGE + CG_RANGE - 1) / CG_RANGE;
-        const bool narrow = !no_narrow && kp <= 2 && im->coop && n2_ <= CGN_MAXL2;
-        if (narrow) {
-            void *fn = kp == 1 ? (im->cplx ? (void *)k_cg_narrow<true, 1> : (void *)k_cg_narrow<false, 1>)
-                               : (im->cplx ? (void *)k_cg_narrow<true, 2> : (void *)k_cg_narrow<false, 2>);
-            int &bps = im->narrow_bps[(kp - 1) * 2 + (im->cplx ? 1 : 0)];
-            if (bps == 0) {
-                CGK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, CGN_NT, 0));
-                if (bps <= 0) bps = -1;
-            }
-            if (bps > 0) {
-                const int64_t units = g.nchunks * kp;
-                const int gg = (int)std::max<int64_t>(1, std::min<int64_t>((units + CGN_WARPS - 1) / CGN_WARPS,
-                                                                           (int64_t)im->sms * bps));
-                int kreal = cg.k, mi = cg.max_iters, ni = check_every;
-                CgGeom gn = g;
-                ShiftDev Sn = S;
-                void *args[] = {&im->M, &im->V, &im->Sc, &Sn, &gn, &kreal, &mi, &ni};
-                hook_begin(cg, width_name("cg_narrow", kp),
-                           check_every * ((160.0 * n * live + 24.0 * n) + nnzb));
-                CGK(cudaLaunchCooperativeKernel(fn, dim3((unsigned)gg), dim3(CGN_NT), args, 0, st));
-                hook_end(cg);
-                *launches += 1;
-                it += check_every;
-            }
-        }
-        for (int s = 0; s < check_every && !(narrow && im->narrow_bps[(kp - 1) * 2 + (im->cplx ? 1 : 0)] > 0); ++s) {
-#else
         for (int s = 0; s < check_every; ++s) {
-#endif
             hook_begin(cg, width_name("cg_spmv", kp), (CG_DEFER_X ? 112.0 : 80.0) * n * live + nnzb);
 #if CG_DEFER_X
             static const bool no_tma = getenv("REXI_COCG_NOTMA") != nullptr;   // A/B switch

@@ -24,8 +24,6 @@ ncu --set full --clock-control none --import-source on -k regex:k_cg_spmv_win -s
     -o gpurun_out/cfg5_k_cg_spmv_win -f python scripts/cfg_step.py 5 > gpurun_out/ncu_cfg5_spmv.log 2>&1; echo "cfg5 spmv rc=$?"
 REXI_COCG_NOTMA=1 ncu --set full --clock-control none --import-source on -k regex:k_cg_spmv_st -s 4 -c 1 \
     -o gpurun_out/cfg3_k_cg_spmv_st -f python scripts/cfg_step.py 3 > gpurun_out/ncu_spmv_st.log 2>&1; echo "cfg3 spmv_st rc=$?"
-ncu --set full --clock-control none -k regex:k_cg_narrow -s 2 -c 1 \
-    -o gpurun_out/cfg3_k_cg_narrow -f python scripts/cfg_step.py 3 > gpurun_out/ncu_narrow.log 2>&1; echo "cfg3 narrow rc=$?"
 for r in gpurun_out/*.ncu-rep; do python scripts/ncu_summary.py raw $r; done > gpurun_out/ncu_raw_summaries.txt 2>&1
 for r in gpurun_out/cfg3_k_cg_spmv_win.ncu-rep gpurun_out/cfg3_k_cg_update_tma.ncu-rep gpurun_out/cfg5_k_cg_spmv_win.ncu-rep; do
   ncu -i $r --page details --csv > ${r%.ncu-rep}_details.csv 2>/dev/null
