@@ -813,7 +813,7 @@ template <int KP, int RL> struct WinGeom {
     static constexpr int NST = R >= 32 ? 1 : (CG_SB * CG_CH) / R;   // stages per claim (a 32-row chunk)
     static constexpr int CPS = R >= 32 ? R / 32 : 1;     // chunks per stage (kp <= 32)
     // z-window rows per stage (what two ~110-KB stages leave after the tiles)
-    static constexpr int ZMAX = RL == 2 ? (KP == 128 ? 30 : KP == 64 ? 56 : 3 * R + 8) : (KP == 128 ? 44 : 72);
+    static constexpr int ZMAX = KP == 128 ? (RL == 2 ? 30 : 44) : KP == 64 ? (RL == 2 ? 56 : 72) : 3 * R + 6;
     static constexpr size_t tile_bytes = (size_t)R * KP * sizeof(c128);
     static constexpr size_t zwin_bytes = (size_t)ZMAX * KP * sizeof(c128);
 };
@@ -923,7 +923,7 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         return;
     }
     // ---- consumers: RL row-lanes per thread and stage ----
-    static_assert(RL == 2 || KP >= 64, "one row-lane per thread: kp = 64 / 128 only");
+    static_assert(RL == 2 || KP >= 64 || G::R >= 32, "one row-lane per thread: whole chunks per stage or kp >= 64");
     const int lane = threadIdx.x % KP;
     const int lr0 = threadIdx.x / KP;
     constexpr int LRS = CGT_CT / KP;                   // local-row distance of a thread's two rows
@@ -1730,7 +1730,7 @@ struct CocgImpl {
     int *mask = nullptr;       // device [kp_full]
     int *h_buf = nullptr;      // pinned [2 + 2*kp_full]
     bool stage_ok[3] = {false, false, false};   // [cpc]: every claim's CSR slice fits the staging buffers
-    CgWin win[4];              // windowed spmv tables for kp = 16, 32, 64, 128 (dir == nullptr: not available)
+    CgWin win[8];              // windowed spmv tables, [log2 kp] for kp = 4 .. 128 (dir == nullptr: not available)
 };
 
 static int alloc_(CocgState &cg, void **p, size_t bytes, std::string &err) {
@@ -2037,13 +2037,23 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
         // stages' columns fit the window budget (2D-like patterns), else one (3D-like,
         // kp >= 64 only), else the gather kernels stay
         int rc = REXI_OK;
-        if (kp >= 16) rc = build_win<16, 2>(cg, im, d, ta, bb, im->win[0], st, err);
-        if (!rc && kp >= 32) rc = build_win<32, 2>(cg, im, d, ta, bb, im->win[1], st, err);
-        if (!rc && kp >= 64) rc = build_win<64, 2>(cg, im, d, ta, bb, im->win[2], st, err);
-        if (!rc && kp >= 64 && !im->win[2].dir) rc = build_win<64, 1>(cg, im, d, ta, bb, im->win[2], st, err);
-        if (!rc && kp >= 128) rc = build_win<128, 2>(cg, im, d, ta, bb, im->win[3], st, err);
-        if (!rc && kp >= 128 && !im->win[3].dir) rc = build_win<128, 1>(cg, im, d, ta, bb, im->win[3], st, err);
+        if (kp >= 4) rc = build_win<4, 1>(cg, im, d, ta, bb, im->win[2], st, err);
+        if (!rc && kp >= 8) rc = build_win<8, 2>(cg, im, d, ta, bb, im->win[3], st, err);
+        if (!rc && kp >= 16) rc = build_win<16, 2>(cg, im, d, ta, bb, im->win[4], st, err);
+        if (!rc && kp >= 32) rc = build_win<32, 2>(cg, im, d, ta, bb, im->win[5], st, err);
+        if (!rc && kp >= 64) rc = build_win<64, 2>(cg, im, d, ta, bb, im->win[6], st, err);
+        if (!rc && kp >= 64 && !im->win[6].dir) rc = build_win<64, 1>(cg, im, d, ta, bb, im->win[6], st, err);
+        if (!rc && kp >= 128) rc = build_win<128, 2>(cg, im, d, ta, bb, im->win[7], st, err);
+        if (!rc && kp >= 128 && !im->win[7].dir) rc = build_win<128, 1>(cg, im, d, ta, bb, im->win[7], st, err);
         if (rc) return rc;
+        if (getenv("REXI_COCG_REQUIRE_WIN")) {   // tests: fail instead of silently keeping the gather kernels
+            int lg = 0;
+            while ((1 << lg) < kp) ++lg;
+            if (kp < 4 || kp > 128 || !im->win[lg].dir) {
+                err = "REXI_COCG_REQUIRE_WIN: no window tables for the " + std::to_string(kp) + "-lane layout";
+                return REXI_ERR_UNSUPPORTED;
+            }
+        }
     }
 #endif
     int dev = 0;
@@ -2202,16 +2212,19 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             hook_begin(cg, width_name("cg_spmv", kp), (CG_DEFER_X ? 112.0 : 80.0) * n * live + nnzb);
 #if CG_DEFER_X
             static const bool no_tma = getenv("REXI_COCG_NOTMA") != nullptr;   // A/B switch
-            static const int win_min = getenv("REXI_COCG_WINMIN") ? atoi(getenv("REXI_COCG_WINMIN")) : 16;
-            const CgWin *wn = kp < win_min ? nullptr : kp == 16 ? &im->win[0] : kp == 32 ? &im->win[1]
-                            : kp == 64 ? &im->win[2] : kp == 128 ? &im->win[3] : nullptr;
+            static const int win_min = getenv("REXI_COCG_WINMIN") ? atoi(getenv("REXI_COCG_WINMIN")) : 4;
+            int lg = 0;
+            while ((1 << lg) < kp) ++lg;
+            const CgWin *wn = kp >= win_min && kp >= 4 && kp <= 128 ? &im->win[lg] : nullptr;
             if (!no_tma && wn && wn->dir) {
-                // wide layouts of 2D-like patterns: every operand by bulk copy
+                // layouts 4..128 wide whose stages fit the z-window budget: every operand by bulk copy
                 const CgGeom gw = make_geom(im, kp, n, CG_WARPS, ld);
                 const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(wn->nstages, (int64_t)im->sms));
 #define REXI_WIN_LAUNCH(KPV, RLV) \
     k_cg_spmv_win<KPV, RLV><<<gg, CGT_NT, win_smem_bytes<KPV, RLV>(wn->blob_max), st>>>(im->M, im->V, im->Sc, S, gw, *wn)
-                if (kp == 16) REXI_WIN_LAUNCH(16, 2);
+                if (kp == 4) REXI_WIN_LAUNCH(4, 1);
+                else if (kp == 8) REXI_WIN_LAUNCH(8, 2);
+                else if (kp == 16) REXI_WIN_LAUNCH(16, 2);
                 else if (kp == 32) REXI_WIN_LAUNCH(32, 2);
                 else if (kp == 64 && wn->rl == 2) REXI_WIN_LAUNCH(64, 2);
                 else if (kp == 64) REXI_WIN_LAUNCH(64, 1);

@@ -73,3 +73,13 @@ def test_window_tables_cover_ragged_sizes(tmp_path):
         tma = _run(3, m, 1, 1, {}, tmp_path, f"rag{m}")
         plain = _run(3, m, 1, 1, {"REXI_COCG_NOTMA": "1"}, tmp_path, f"rag{m}_plain")
         assert np.array_equal(tma, plain), m
+
+
+@pytest.mark.parametrize("c,m", [(3, 64), (4, 48), (5, 14)])
+def test_window_tables_are_built(c, m, tmp_path):
+    """The bitwise tests above compare against the gather kernels; this one
+    makes sure the windowed path is what the default run uses on the 2D
+    (K = 64, K = 128) and 3D fixtures: REXI_COCG_REQUIRE_WIN turns a missing
+    table into an error."""
+    out = _run(c, m, 1, 1, {"REXI_COCG_REQUIRE_WIN": "1"}, tmp_path, "reqwin")
+    assert np.all(np.isfinite(out))
