@@ -1053,14 +1053,22 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
 // partial tree as k_cg_update: bitwise identical.
 // ---------------------------------------------------------------------------
 template <int KP> struct UpdGeom {
-    static constexpr int R = (CGT_CT * 4) / KP;          // rows per stage
-    static constexpr int NST = (CG_SB * CG_CH) / R;      // stages per 32-row chunk (1 or 2)
-    static constexpr int NSTG = 3;                       // pipeline stages
-    static constexpr size_t tile_bytes = (size_t)R * KP * sizeof(c128);
-    static constexpr size_t stage_bytes = 2 * tile_bytes + 512;   // z, q, dta[R], db[R]
+    static constexpr int R = (CGT_CT * 4) / KP;          // rows per stage (four row-lanes per consumer thread)
+    static constexpr int UNIT = R >= 32 ? R : 32;        // rows per claim unit: a stage of whole chunks, or a chunk
+    static constexpr int NST = UNIT / R;                 // stages per unit (kp = 128: 2)
+    static constexpr int CPS = R >= 32 ? R / 32 : 1;     // chunks per stage
+    static constexpr bool TERMS = KP <= 32;              // per-row terms summed in tree order (a thread's rows
+                                                         // belong to several sub-blocks' interleaved rows)
+    static constexpr int NSTG = KP >= 8 ? 3 : 2;         // pipeline stages
+    static constexpr size_t tile_bytes = (size_t)CGT_CT * 4 * sizeof(c128);   // 32 KB
+    static constexpr size_t diag_bytes = ((size_t)R * 8 + 255) & ~(size_t)255;
+    static constexpr size_t stage_bytes = 2 * tile_bytes + 2 * diag_bytes;    // z, q, dta[R], db[R]
+    static constexpr size_t rterm_bytes = TERMS ? (size_t)CGT_CT * 4 * sizeof(double) : 0;
 };
 template <int KP>
-__host__ __device__ inline size_t upd_smem_bytes() { return 128 + UpdGeom<KP>::NSTG * UpdGeom<KP>::stage_bytes; }
+__host__ __device__ inline size_t upd_smem_bytes() {
+    return 128 + UpdGeom<KP>::NSTG * UpdGeom<KP>::stage_bytes + UpdGeom<KP>::rterm_bytes;
+}
 
 #if CG_DEFER_X
 template <int KP>
@@ -1080,9 +1088,10 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_update_tma(CgMat M, CgVec V, C
         fence_mbar_init();
     }
     __syncthreads();
-    // this CTA's stages: chunks blockIdx.x, blockIdx.x + gridDim.x, ... (NST stages each)
-    const int64_t my_chunks = g.nchunks > blockIdx.x ? (g.nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const int64_t my_stages = my_chunks * NST;
+    // this CTA's stages: units blockIdx.x, blockIdx.x + gridDim.x, ... (NST stages each)
+    const int64_t nunits = (M.n + G::UNIT - 1) / G::UNIT;
+    const int64_t my_units = nunits > blockIdx.x ? (nunits - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int64_t my_stages = my_units * NST;
     auto stage_of = [&](int64_t it) { return ((int64_t)blockIdx.x + (it / NST) * gridDim.x) * NST + it % NST; };
     if (threadIdx.x >= CGT_CT) {
         // ---- producer ----
@@ -1116,7 +1125,7 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_update_tma(CgMat M, CgVec V, C
             bulk_g2s(base, V.z + (size_t)R0 * ld, tb, full + s);
             bulk_g2s(base + G::tile_bytes, V.q + (size_t)R0 * ld, tb, full + s);
             bulk_g2s(base + 2 * G::tile_bytes, M.dta + R0, db, full + s);
-            bulk_g2s(base + 2 * G::tile_bytes + 256, M.db + R0, db, full + s);
+            bulk_g2s(base + 2 * G::tile_bytes + G::diag_bytes, M.db + R0, db, full + s);
         }
         bulk_wait0();
         return;
@@ -1124,13 +1133,14 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_update_tma(CgMat M, CgVec V, C
     // ---- consumers: four row-lanes per thread and stage ----
     const int lane = threadIdx.x % KP;
     const int lr0 = threadIdx.x / KP;
-    constexpr int LRS = CGT_CT / KP;                   // 8 (kp = 64: one sub-block per thread) or 4
+    constexpr int LRS = CGT_CT / KP;                   // kp = 64: 8, one sub-block per thread; kp = 128: 4
     const bool act = Sc.active[lane] != 0;
     const c128 sg = S.sigma[g.lane_shift[lane]];
     const c128 alpha = Sc.alpha[lane];
     uint32_t fph[NSTG] = {};
-    c128 rho[2] = {cmk(0.0, 0.0), cmk(0.0, 0.0)};
-    double rn[2] = {0.0, 0.0};
+    c128 rho[G::TERMS ? 4 : 2];
+    double rn[G::TERMS ? 4 : 2];
+    double *rterm = reinterpret_cast<double *>(smem + 128 + NSTG * G::stage_bytes);
     for (int64_t it = 0; it < my_stages; ++it) {
         const int s = (int)(it % NSTG);
         mbar_wait(full + s, fph[s]);
@@ -1141,11 +1151,14 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_update_tma(CgMat M, CgVec V, C
         c128 *tz = reinterpret_cast<c128 *>(base);
         c128 *tq = reinterpret_cast<c128 *>(base + G::tile_bytes);
         const double *sdta = reinterpret_cast<const double *>(base + 2 * G::tile_bytes);
-        const double *sdb = reinterpret_cast<const double *>(base + 2 * G::tile_bytes + 256);
+        const double *sdb = reinterpret_cast<const double *>(base + 2 * G::tile_bytes + G::diag_bytes);
         const int rows = (int)min((int64_t)R, M.n - gs * R);
-        if (h == 0) {
-            rho[0] = rho[1] = cmk(0.0, 0.0);
-            rn[0] = rn[1] = 0.0;
+        if (h == 0 || G::TERMS) {
+#pragma unroll
+            for (int k = 0; k < (G::TERMS ? 4 : 2); ++k) {
+                rho[k] = cmk(0.0, 0.0);
+                rn[k] = 0.0;
+            }
         }
         if (act) {
 #pragma unroll
@@ -1158,15 +1171,56 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_update_tma(CgMat M, CgVec V, C
                     const c128 z = csub(tz[t], cmul(alpha, cdiv_c(q, d)));
                     tz[t] = z;
                     const c128 r = cmul(d, z);
-                    const int a = LRS == CG_CH ? 0 : (k & 1);
-                    rho[a] = cadd(rho[a], cmul(r, z));
-                    rn[a] += cabs2(r);
+                    if (G::TERMS) {
+                        rho[k] = cmul(r, z);
+                        rn[k] = cabs2(r);
+                    } else {
+                        const int a = LRS == CG_CH ? 0 : (k & 1);
+                        rho[a] = cadd(rho[a], cmul(r, z));
+                        rn[a] += cabs2(r);
+                    }
                 }
             }
         }
         fence_proxy_async();         // z tile writes -> visible to the bulk store
         bar_consumers();
-        if (h == NST - 1) {
+        if (G::TERMS) {
+            // whole chunks per stage: per-row terms through the (now dead) q tile and the
+            // real-term buffer, then each chunk's tree in order
+            double2 *trm = reinterpret_cast<double2 *>(tq);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                trm[(lr0 + k * LRS) * KP + lane] = rho[k];
+                rterm[(lr0 + k * LRS) * KP + lane] = rn[k];
+            }
+            bar_consumers();
+            if (threadIdx.x < G::CPS * KP) {
+                const int cc = threadIdx.x / KP, ll = threadIdx.x % KP;
+                const int64_t chunk = gs * G::CPS + cc;
+                if (chunk < g.nchunks) {
+                    const double2 *tc = trm + (size_t)cc * (CG_SB * CG_CH) * KP + ll;
+                    const double *tr = rterm + (size_t)cc * (CG_SB * CG_CH) * KP + ll;
+                    double2 sum = make_double2(0.0, 0.0);
+                    double sr = 0.0;
+#pragma unroll
+                    for (int b = 0; b < CG_CH; ++b) {
+                        double2 sb = make_double2(0.0, 0.0);
+                        double sbr = 0.0;
+#pragma unroll
+                        for (int k = 0; k < CG_SB; ++k) {
+                            sb = cadd(sb, tc[(b + k * CG_CH) * KP]);
+                            sbr += tr[(b + k * CG_CH) * KP];
+                        }
+                        sum = cadd(sum, sb);
+                        sr += sbr;
+                    }
+                    Sc.part_b[(size_t)chunk * KP + ll] = sum;
+                    Sc.part_c[(size_t)chunk * KP + ll] = sr;
+                }
+            }
+            fence_proxy_async();     // the term slots will be overwritten by the next bulk load
+            bar_consumers();
+        } else if (h == NST - 1) {
             // chunk partials: the sub-block partials go through the (now dead) q tile
             double2 *sbc = reinterpret_cast<double2 *>(tq);
             double *sbr = reinterpret_cast<double *>(sbc + CG_CH * KP);
@@ -2037,7 +2091,12 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
         // stages' columns fit the window budget (2D-like patterns), else one (3D-like,
         // kp >= 64 only), else the gather kernels stay
         int rc = REXI_OK;
-        if (kp >= 4) rc = build_win<4, 1>(cg, im, d, ta, bb, im->win[2], st, err);
+        // (one lane: the thread-per-row kernel over stencil classes streams 8 B per entry
+        // against the blob's 18 and measured faster, 54 vs 59 us at 1M rows: table on request)
+        if (getenv("REXI_COCG_WINMIN") && atoi(getenv("REXI_COCG_WINMIN")) <= 1)
+            rc = build_win<1, 1>(cg, im, d, ta, bb, im->win[0], st, err);
+        if (!rc && kp >= 2) rc = build_win<2, 1>(cg, im, d, ta, bb, im->win[1], st, err);
+        if (!rc && kp >= 4) rc = build_win<4, 1>(cg, im, d, ta, bb, im->win[2], st, err);
         if (!rc && kp >= 8) rc = build_win<8, 2>(cg, im, d, ta, bb, im->win[3], st, err);
         if (!rc && kp >= 16) rc = build_win<16, 2>(cg, im, d, ta, bb, im->win[4], st, err);
         if (!rc && kp >= 32) rc = build_win<32, 2>(cg, im, d, ta, bb, im->win[5], st, err);
@@ -2049,7 +2108,7 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
         if (getenv("REXI_COCG_REQUIRE_WIN")) {   // tests: fail instead of silently keeping the gather kernels
             int lg = 0;
             while ((1 << lg) < kp) ++lg;
-            if (kp < 4 || kp > 128 || !im->win[lg].dir) {
+            if (kp > 128 || !im->win[lg].dir) {
                 err = "REXI_COCG_REQUIRE_WIN: no window tables for the " + std::to_string(kp) + "-lane layout";
                 return REXI_ERR_UNSUPPORTED;
             }
@@ -2212,17 +2271,19 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             hook_begin(cg, width_name("cg_spmv", kp), (CG_DEFER_X ? 112.0 : 80.0) * n * live + nnzb);
 #if CG_DEFER_X
             static const bool no_tma = getenv("REXI_COCG_NOTMA") != nullptr;   // A/B switch
-            static const int win_min = getenv("REXI_COCG_WINMIN") ? atoi(getenv("REXI_COCG_WINMIN")) : 4;
+            static const int win_min = getenv("REXI_COCG_WINMIN") ? atoi(getenv("REXI_COCG_WINMIN")) : 2;
             int lg = 0;
             while ((1 << lg) < kp) ++lg;
-            const CgWin *wn = kp >= win_min && kp >= 4 && kp <= 128 ? &im->win[lg] : nullptr;
+            const CgWin *wn = kp >= win_min && kp <= 128 ? &im->win[lg] : nullptr;
             if (!no_tma && wn && wn->dir) {
-                // layouts 4..128 wide whose stages fit the z-window budget: every operand by bulk copy
+                // layouts whose stages fit the z-window budget: every operand by bulk copy
                 const CgGeom gw = make_geom(im, kp, n, CG_WARPS, ld);
                 const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(wn->nstages, (int64_t)im->sms));
 #define REXI_WIN_LAUNCH(KPV, RLV) \
     k_cg_spmv_win<KPV, RLV><<<gg, CGT_NT, win_smem_bytes<KPV, RLV>(wn->blob_max), st>>>(im->M, im->V, im->Sc, S, gw, *wn)
-                if (kp == 4) REXI_WIN_LAUNCH(4, 1);
+                if (kp == 1) REXI_WIN_LAUNCH(1, 1);
+                else if (kp == 2) REXI_WIN_LAUNCH(2, 1);
+                else if (kp == 4) REXI_WIN_LAUNCH(4, 1);
                 else if (kp == 8) REXI_WIN_LAUNCH(8, 2);
                 else if (kp == 16) REXI_WIN_LAUNCH(16, 2);
                 else if (kp == 32) REXI_WIN_LAUNCH(32, 2);
@@ -2279,16 +2340,34 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             hook_begin(cg, width_name("cg_update", kp), (CG_DEFER_X ? 48.0 : 96.0) * n * live + 24.0 * n);
 #if CG_DEFER_X
             static const bool no_utma = getenv("REXI_COCG_NOUTMA") != nullptr;   // A/B switch
-            if (!no_utma && !no_tma && !im->cplx && (kp == 64 || kp == 128)) {
+            static const int utma_min = getenv("REXI_COCG_UTMAMIN") ? atoi(getenv("REXI_COCG_UTMAMIN")) : 2;   // one lane: k_cg_update1 measured faster (33.6 vs 36.2 us)
+            if (!no_utma && !no_tma && !im->cplx && kp >= utma_min && kp <= 128) {
                 static bool uattr = false;
+#define REXI_UPD_ATTR(KPV) \
+    CGK(cudaFuncSetAttribute(k_cg_update_tma<KPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem_bytes<KPV>()))
                 if (!uattr) {
-                    CGK(cudaFuncSetAttribute(k_cg_update_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem_bytes<64>()));
-                    CGK(cudaFuncSetAttribute(k_cg_update_tma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem_bytes<128>()));
+                    REXI_UPD_ATTR(1); REXI_UPD_ATTR(2); REXI_UPD_ATTR(4); REXI_UPD_ATTR(8);
+                    REXI_UPD_ATTR(16); REXI_UPD_ATTR(32); REXI_UPD_ATTR(64); REXI_UPD_ATTR(128);
                     uattr = true;
                 }
-                const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(g.nchunks, (int64_t)im->sms));
-                if (kp == 64) k_cg_update_tma<64><<<gg, CGT_NT, upd_smem_bytes<64>(), st>>>(im->M, im->V, im->Sc, S, g);
-                else k_cg_update_tma<128><<<gg, CGT_NT, upd_smem_bytes<128>(), st>>>(im->M, im->V, im->Sc, S, g);
+#undef REXI_UPD_ATTR
+#define REXI_UPD_LAUNCH(KPV)                                                                              \
+    {                                                                                                     \
+        const int64_t nu = (n + UpdGeom<KPV>::UNIT - 1) / UpdGeom<KPV>::UNIT;                             \
+        const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(nu, (int64_t)im->sms));                \
+        k_cg_update_tma<KPV><<<gg, CGT_NT, upd_smem_bytes<KPV>(), st>>>(im->M, im->V, im->Sc, S, g);       \
+    }
+                switch (kp) {
+                    case 1: REXI_UPD_LAUNCH(1) break;
+                    case 2: REXI_UPD_LAUNCH(2) break;
+                    case 4: REXI_UPD_LAUNCH(4) break;
+                    case 8: REXI_UPD_LAUNCH(8) break;
+                    case 16: REXI_UPD_LAUNCH(16) break;
+                    case 32: REXI_UPD_LAUNCH(32) break;
+                    case 64: REXI_UPD_LAUNCH(64) break;
+                    default: REXI_UPD_LAUNCH(128) break;
+                }
+#undef REXI_UPD_LAUNCH
             } else
 #endif
             if (g.kp == 1) {
