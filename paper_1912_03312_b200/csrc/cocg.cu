@@ -41,6 +41,7 @@
 #include <map>
 #include <unordered_map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "cocg.cuh"
@@ -1836,16 +1837,26 @@ static int grid_for(const CocgImpl *im, const CgGeom &g, int64_t) {
 
 // stage tables of the windowed spmv for layout width KP (see k_cg_spmv_win);
 // leaves w.dir == nullptr when some stage's columns do not fit three windows
+struct WinHost {                  // host image of one width's tables (built on a worker thread)
+    bool ok = false;
+    int rl = 0, blob_max = 0;
+    int64_t nstages = 0;
+    std::vector<WinStage> dir;
+    std::vector<unsigned char> blob;
+};
+
 template <int KP, int RL>
-static int build_win(CocgState &cg, CocgImpl *im, const rexi_desc *d, const std::vector<double> &ta,
-                     const std::vector<double> &bb, CgWin &w, cudaStream_t st, std::string &err) {
+static void win_host(const rexi_desc *d, const std::vector<double> &ta, const std::vector<double> &bb, WinHost &out) {
     using G = WinGeom<KP, RL>;
     constexpr int R = G::R;
+    out.ok = false;
     const int64_t n = d->n;
     const int64_t nchunks = (n + CG_SB * CG_CH - 1) / (CG_SB * CG_CH);
     const int64_t nstages = G::R >= 32 ? (nchunks + G::CPS - 1) / G::CPS : nchunks * G::NST;
-    std::vector<WinStage> dir((size_t)nstages);
-    std::vector<unsigned char> blob;
+    std::vector<WinStage> &dir = out.dir;
+    std::vector<unsigned char> &blob = out.blob;
+    dir.assign((size_t)nstages, WinStage{});
+    blob.clear();
     blob.reserve((size_t)d->nnz * 19 + (size_t)nstages * 64);
     int blob_max = 0;
     std::vector<int32_t> cols;
@@ -1880,7 +1891,7 @@ static int build_win(CocgState &cg, CocgImpl *im, const rexi_desc *d, const std:
             if (runs[k].first <= R0 && R1 - 1 <= runs[k].second) own0 = total + (int)(R0 - runs[k].first);
             total += e.wrows[k];
         }
-        if (total > G::ZMAX || own0 < 0 || Q1 - Q0 > 65535) return REXI_OK;   // not window-shaped: keep the gather kernels
+        if (total > G::ZMAX || own0 < 0 || Q1 - Q0 > 65535) return;   // not window-shaped: keep the gather kernels
         e.own0 = own0;
         const int rows = (int)(R1 - R0), nz = Q1 - Q0;
         const size_t b_ip = al16(4 * (size_t)(rows + 1)), b_zs = al16(2 * (size_t)nz), b_v = al16(8 * (size_t)nz);
@@ -1913,21 +1924,35 @@ static int build_win(CocgState &cg, CocgImpl *im, const rexi_desc *d, const std:
         dir[(size_t)gs] = e;
     }
     blob_max = (blob_max + 127) & ~127;
-    if (win_smem_bytes<KP, RL>(blob_max) > 227 * 1024) return REXI_OK;
+    if (win_smem_bytes<KP, RL>(blob_max) > 227 * 1024) return;
+    out.ok = true;
+    out.rl = RL;
+    out.blob_max = blob_max;
+    out.nstages = nstages;
+}
+
+// two row-lanes per thread where the stages' columns fit the window budget, else one
+// (3D-like patterns; kp >= 64 only)
+template <int KP>
+static void win_host_any(const rexi_desc *d, const std::vector<double> &ta, const std::vector<double> &bb, WinHost &out) {
+    if (KP >= 8) win_host<KP, 2>(d, ta, bb, out);
+    if (!out.ok && (KP >= 64 || KP <= 4)) win_host < KP, KP >= 64 || KP <= 4 ? 1 : 2 > (d, ta, bb, out);
+}
+
+static int win_upload(CocgState &cg, const WinHost &h, CgWin &w, cudaStream_t st, std::string &err) {
+    if (!h.ok) return REXI_OK;
     WinStage *ddir;
     unsigned char *dblob;
-    CGA(ddir, sizeof(WinStage) * dir.size());
-    CGA(dblob, blob.size() + 16);
-    CGK(cudaMemcpyAsync(ddir, dir.data(), sizeof(WinStage) * dir.size(), cudaMemcpyHostToDevice, st));
-    CGK(cudaMemcpyAsync(dblob, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
+    CGA(ddir, sizeof(WinStage) * h.dir.size());
+    CGA(dblob, h.blob.size() + 16);
+    CGK(cudaMemcpyAsync(ddir, h.dir.data(), sizeof(WinStage) * h.dir.size(), cudaMemcpyHostToDevice, st));
+    CGK(cudaMemcpyAsync(dblob, h.blob.data(), h.blob.size(), cudaMemcpyHostToDevice, st));
     CGK(cudaStreamSynchronize(st));   // the host vectors go out of scope
-    CGK(cudaFuncSetAttribute(k_cg_spmv_win<KP, RL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)win_smem_bytes<KP, RL>(blob_max)));
-    w.rl = RL;
+    w.rl = h.rl;
     w.dir = ddir;
     w.blob = dblob;
-    w.blob_max = blob_max;
-    w.nstages = nstages;
+    w.blob_max = h.blob_max;
+    w.nstages = h.nstages;
     return REXI_OK;
 }
 
@@ -2090,20 +2115,23 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
         // windowed all-TMA spmv for the wide layouts: two row-lanes per thread where the
         // stages' columns fit the window budget (2D-like patterns), else one (3D-like,
         // kp >= 64 only), else the gather kernels stay
+        // one host thread per width (the builds are independent passes over the pattern).
+        // One lane: the thread-per-row kernel over stencil classes streams 8 B per entry
+        // against the blob's 18 and measured faster (54 vs 59 us at 1M rows): table on request.
+        WinHost wh[8];
+        std::vector<std::thread> th;
+        const bool want1 = getenv("REXI_COCG_WINMIN") && atoi(getenv("REXI_COCG_WINMIN")) <= 1;
+        if (want1) th.emplace_back([&] { win_host_any<1>(d, ta, bb, wh[0]); });
+        if (kp >= 2) th.emplace_back([&] { win_host_any<2>(d, ta, bb, wh[1]); });
+        if (kp >= 4) th.emplace_back([&] { win_host_any<4>(d, ta, bb, wh[2]); });
+        if (kp >= 8) th.emplace_back([&] { win_host_any<8>(d, ta, bb, wh[3]); });
+        if (kp >= 16) th.emplace_back([&] { win_host_any<16>(d, ta, bb, wh[4]); });
+        if (kp >= 32) th.emplace_back([&] { win_host_any<32>(d, ta, bb, wh[5]); });
+        if (kp >= 64) th.emplace_back([&] { win_host_any<64>(d, ta, bb, wh[6]); });
+        if (kp >= 128) th.emplace_back([&] { win_host_any<128>(d, ta, bb, wh[7]); });
+        for (auto &t : th) t.join();
         int rc = REXI_OK;
-        // (one lane: the thread-per-row kernel over stencil classes streams 8 B per entry
-        // against the blob's 18 and measured faster, 54 vs 59 us at 1M rows: table on request)
-        if (getenv("REXI_COCG_WINMIN") && atoi(getenv("REXI_COCG_WINMIN")) <= 1)
-            rc = build_win<1, 1>(cg, im, d, ta, bb, im->win[0], st, err);
-        if (!rc && kp >= 2) rc = build_win<2, 1>(cg, im, d, ta, bb, im->win[1], st, err);
-        if (!rc && kp >= 4) rc = build_win<4, 1>(cg, im, d, ta, bb, im->win[2], st, err);
-        if (!rc && kp >= 8) rc = build_win<8, 2>(cg, im, d, ta, bb, im->win[3], st, err);
-        if (!rc && kp >= 16) rc = build_win<16, 2>(cg, im, d, ta, bb, im->win[4], st, err);
-        if (!rc && kp >= 32) rc = build_win<32, 2>(cg, im, d, ta, bb, im->win[5], st, err);
-        if (!rc && kp >= 64) rc = build_win<64, 2>(cg, im, d, ta, bb, im->win[6], st, err);
-        if (!rc && kp >= 64 && !im->win[6].dir) rc = build_win<64, 1>(cg, im, d, ta, bb, im->win[6], st, err);
-        if (!rc && kp >= 128) rc = build_win<128, 2>(cg, im, d, ta, bb, im->win[7], st, err);
-        if (!rc && kp >= 128 && !im->win[7].dir) rc = build_win<128, 1>(cg, im, d, ta, bb, im->win[7], st, err);
+        for (int w = 0; w < 8 && !rc; ++w) rc = win_upload(cg, wh[w], im->win[w], st, err);
         if (rc) return rc;
         if (getenv("REXI_COCG_REQUIRE_WIN")) {   // tests: fail instead of silently keeping the gather kernels
             int lg = 0;
@@ -2279,18 +2307,26 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
                 // layouts whose stages fit the z-window budget: every operand by bulk copy
                 const CgGeom gw = make_geom(im, kp, n, CG_WARPS, ld);
                 const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(wn->nstages, (int64_t)im->sms));
-#define REXI_WIN_LAUNCH(KPV, RLV) \
-    k_cg_spmv_win<KPV, RLV><<<gg, CGT_NT, win_smem_bytes<KPV, RLV>(wn->blob_max), st>>>(im->M, im->V, im->Sc, S, gw, *wn)
-                if (kp == 1) REXI_WIN_LAUNCH(1, 1);
-                else if (kp == 2) REXI_WIN_LAUNCH(2, 1);
-                else if (kp == 4) REXI_WIN_LAUNCH(4, 1);
-                else if (kp == 8) REXI_WIN_LAUNCH(8, 2);
-                else if (kp == 16) REXI_WIN_LAUNCH(16, 2);
-                else if (kp == 32) REXI_WIN_LAUNCH(32, 2);
-                else if (kp == 64 && wn->rl == 2) REXI_WIN_LAUNCH(64, 2);
-                else if (kp == 64) REXI_WIN_LAUNCH(64, 1);
-                else if (wn->rl == 2) REXI_WIN_LAUNCH(128, 2);
-                else REXI_WIN_LAUNCH(128, 1);
+#define REXI_WIN_LAUNCH(KPV, RLV)                                                                          \
+    {                                                                                                      \
+        static int attr_for = -1;   /* largest dynamic shared memory size set for this instantiation */   \
+        const int sm_ = (int)win_smem_bytes<KPV, RLV>(wn->blob_max);                                       \
+        if (sm_ > attr_for) {                                                                              \
+            CGK(cudaFuncSetAttribute(k_cg_spmv_win<KPV, RLV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_)); \
+            attr_for = sm_;                                                                                \
+        }                                                                                                  \
+        k_cg_spmv_win<KPV, RLV><<<gg, CGT_NT, sm_, st>>>(im->M, im->V, im->Sc, S, gw, *wn);                \
+    }
+                if (kp == 1) REXI_WIN_LAUNCH(1, 1)
+                else if (kp == 2) REXI_WIN_LAUNCH(2, 1)
+                else if (kp == 4) REXI_WIN_LAUNCH(4, 1)
+                else if (kp == 8) REXI_WIN_LAUNCH(8, 2)
+                else if (kp == 16) REXI_WIN_LAUNCH(16, 2)
+                else if (kp == 32) REXI_WIN_LAUNCH(32, 2)
+                else if (kp == 64 && wn->rl == 2) REXI_WIN_LAUNCH(64, 2)
+                else if (kp == 64) REXI_WIN_LAUNCH(64, 1)
+                else if (wn->rl == 2) REXI_WIN_LAUNCH(128, 2)
+                else REXI_WIN_LAUNCH(128, 1)
 #undef REXI_WIN_LAUNCH
             } else if (!no_tma && !im->cplx && (kp == 32 || kp == 64) && im->stage_ok[kp / 32 == 2 ? 1 : 2] &&
                 cg.nnz <= (int64_t)CG_GB * n) {

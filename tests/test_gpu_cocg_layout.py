@@ -27,7 +27,20 @@ np.save(sys.argv[5], out)
 """
 
 
+_DEFAULT_RUNS = {}   # (c, m, refine, steps) -> output of the default (no switch) run
+
+
 def _run(c, m, refine, steps, env_extra, tmp_path, tag):
+    key = (c, m, refine, steps)
+    if not env_extra and key in _DEFAULT_RUNS:
+        return _DEFAULT_RUNS[key]
+    out = _run_uncached(c, m, refine, steps, env_extra, tmp_path, tag)
+    if not env_extra:
+        _DEFAULT_RUNS[key] = out
+    return out
+
+
+def _run_uncached(c, m, refine, steps, env_extra, tmp_path, tag):
     env = dict(os.environ, **env_extra)
     path = str(tmp_path / f"cocg_{c}_{m}_{refine}_{tag}.npy")
     subprocess.run([sys.executable, "-c", _PROBE % ROOT, str(c), str(m), str(refine), str(steps), path],
