@@ -588,6 +588,30 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
+// L2 eviction-priority hints (createpolicy): the streamed tiles go first, the z
+// windows -- re-read by the stages of the neighbouring grid lines / planes -- last
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void *dst, const void *src, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -802,6 +826,7 @@ struct CgWin {
     const WinStage *dir = nullptr;
     const unsigned char *blob = nullptr;
     int blob_max = 0;             // largest blob, rounded up to 128 B
+    int zrows = 0;                // z-window rows of the largest stage (rounded up to 8)
     int64_t nstages = 0;
     int rl = 2;                   // row-lanes per consumer thread and stage (2: 2D tables, 1: 3D)
 };
@@ -813,15 +838,15 @@ template <int KP, int RL> struct WinGeom {
     static constexpr int R = (CGT_CT * RL) / KP;         // rows per stage
     static constexpr int NST = R >= 32 ? 1 : (CG_SB * CG_CH) / R;   // stages per claim (a 32-row chunk)
     static constexpr int CPS = R >= 32 ? R / 32 : 1;     // chunks per stage (kp <= 32)
-    // z-window rows per stage (what two ~110-KB stages leave after the tiles)
-    static constexpr int ZMAX = KP == 128 ? (RL == 2 ? 30 : 44) : KP == 64 ? (RL == 2 ? 56 : 72) : 3 * R + 6;
     static constexpr size_t tile_bytes = (size_t)R * KP * sizeof(c128);
-    static constexpr size_t zwin_bytes = (size_t)ZMAX * KP * sizeof(c128);
 };
+// two stages of: three tiles, the z windows (zrows rows: the largest stage's, found at
+// plan creation), the matrix blob
 template <int KP, int RL>
-__host__ __device__ inline size_t win_smem_bytes(int blob_max) {
-    return 128 + 2 * (3 * WinGeom<KP, RL>::tile_bytes + WinGeom<KP, RL>::zwin_bytes + (size_t)blob_max);
+__host__ __device__ inline size_t win_smem_bytes(int blob_max, int zrows) {
+    return 128 + 2 * (3 * WinGeom<KP, RL>::tile_bytes + (size_t)zrows * KP * sizeof(c128) + (size_t)blob_max);
 }
+constexpr size_t CG_SMEM_MAX = 227 * 1024;
 
 #if CG_DEFER_X
 template <int KP, int RL>
@@ -834,7 +859,8 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
     uint64_t *done = reinterpret_cast<uint64_t *>(smem + 16);
     int64_t *slot_q = reinterpret_cast<int64_t *>(smem + 32);
     int4 *dirq = reinterpret_cast<int4 *>(smem + 64);   // per slot: blob offsets of zs / ta / b, own0
-    const size_t stage_bytes = 3 * G::tile_bytes + G::zwin_bytes + (size_t)W.blob_max;
+    const size_t zwin_bytes = (size_t)W.zrows * KP * sizeof(c128);
+    const size_t stage_bytes = 3 * G::tile_bytes + zwin_bytes + (size_t)W.blob_max;
     const uint32_t ld = (uint32_t)g.ld;
     if (threadIdx.x == 0) {
         mbar_init(full, 1);
@@ -849,6 +875,22 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         if (threadIdx.x != CGT_CT) return;
         int64_t prev[2] = {0, 0};
         uint32_t dph[2] = {0u, 0u};
+#ifndef CGW_L2HINT
+#define CGW_L2HINT 1   // A/B: eviction-priority hints on the bulk copies
+#endif
+        const uint64_t pol_s = l2_policy_evict_first(), pol_z = l2_policy_evict_last();
+        auto ld_s = [&](void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+            if (CGW_L2HINT) bulk_g2s_hint(dst, src, bytes, bar, pol_s);
+            else bulk_g2s(dst, src, bytes, bar);
+        };
+        auto ld_z = [&](void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+            if (CGW_L2HINT) bulk_g2s_hint(dst, src, bytes, bar, pol_z);
+            else bulk_g2s(dst, src, bytes, bar);
+        };
+        auto st_s = [&](void *dst, const void *src, uint32_t bytes) {
+            if (CGW_L2HINT) bulk_s2g_hint(dst, src, bytes, pol_s);
+            else bulk_s2g(dst, src, bytes);
+        };
         auto store = [&](int s, int64_t gs) {
             unsigned char *base = smem + 128 + (size_t)s * stage_bytes;
             const int64_t R0 = gs * R;
@@ -856,9 +898,9 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
             if (rows > 0) {
                 const uint32_t tb = (uint32_t)(rows * ld * sizeof(c128));
                 const size_t o = (size_t)R0 * ld;
-                bulk_s2g(V.p + o, base, tb);
-                bulk_s2g(V.q + o, base + G::tile_bytes, tb);
-                bulk_s2g(V.x + o, base + 2 * G::tile_bytes, tb);
+                st_s(V.p + o, base, tb);
+                st_s(V.q + o, base + G::tile_bytes, tb);
+                st_s(V.x + o, base + 2 * G::tile_bytes, tb);
             }
             bulk_commit();
         };
@@ -901,18 +943,18 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
                 const uint32_t zb = zr * rb;
                 mbar_expect_tx(full + s, 3 * tb + zb + (uint32_t)d.blob_bytes);
                 const size_t o = (size_t)R0 * ld;
-                bulk_g2s(base, V.p + o, tb, full + s);
-                bulk_g2s(base + G::tile_bytes, V.q + o, tb, full + s);
-                bulk_g2s(base + 2 * G::tile_bytes, V.x + o, tb, full + s);
+                ld_s(base, V.p + o, tb, full + s);
+                ld_s(base + G::tile_bytes, V.q + o, tb, full + s);
+                ld_s(base + 2 * G::tile_bytes, V.x + o, tb, full + s);
                 unsigned char *zw = base + 3 * G::tile_bytes;
                 uint32_t zo = 0;
 #pragma unroll
                 for (int k = 0; k < CG_NWIN; ++k)
                     if (d.wrows[k] > 0) {
-                        bulk_g2s(zw + zo, V.z + (size_t)d.wstart[k] * ld, (uint32_t)d.wrows[k] * rb, full + s);
+                        ld_z(zw + zo, V.z + (size_t)d.wstart[k] * ld, (uint32_t)d.wrows[k] * rb, full + s);
                         zo += (uint32_t)d.wrows[k] * rb;
                     }
-                bulk_g2s(zw + G::zwin_bytes, W.blob + d.blob_off, (uint32_t)d.blob_bytes, full + s);
+                ld_s(zw + zwin_bytes, W.blob + d.blob_off, (uint32_t)d.blob_bytes, full + s);
             }
         }
         if (it >= 1) {   // the stage computed last sits in the other slot
@@ -955,7 +997,7 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         const int rows = (int)min((int64_t)R, M.n - R0);
         if (h == 0 || TERMS) mu[0] = mu[1] = cmk(0.0, 0.0);
         if (rows > 0 && (act || fl)) {
-            const unsigned char *blob = base + 3 * G::tile_bytes + G::zwin_bytes;
+            const unsigned char *blob = base + 3 * G::tile_bytes + zwin_bytes;
             const int4 dq = dirq[s];
             const int off_zs = dq.x, off_ta = dq.y, off_b = dq.z, own0 = dq.w;
             const int *ip = reinterpret_cast<const int *>(blob);
@@ -1839,7 +1881,7 @@ static int grid_for(const CocgImpl *im, const CgGeom &g, int64_t) {
 // leaves w.dir == nullptr when some stage's columns do not fit three windows
 struct WinHost {                  // host image of one width's tables (built on a worker thread)
     bool ok = false;
-    int rl = 0, blob_max = 0;
+    int rl = 0, blob_max = 0, zrows = 0;
     int64_t nstages = 0;
     std::vector<WinStage> dir;
     std::vector<unsigned char> blob;
@@ -1858,7 +1900,7 @@ static void win_host(const rexi_desc *d, const std::vector<double> &ta, const st
     dir.assign((size_t)nstages, WinStage{});
     blob.clear();
     blob.reserve((size_t)d->nnz * 19 + (size_t)nstages * 64);
-    int blob_max = 0;
+    int blob_max = 0, zrows = 0;
     std::vector<int32_t> cols;
     auto al16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
     for (int64_t gs = 0; gs < nstages; ++gs) {
@@ -1891,7 +1933,9 @@ static void win_host(const rexi_desc *d, const std::vector<double> &ta, const st
             if (runs[k].first <= R0 && R1 - 1 <= runs[k].second) own0 = total + (int)(R0 - runs[k].first);
             total += e.wrows[k];
         }
-        if (total > G::ZMAX || own0 < 0 || Q1 - Q0 > 65535) return;   // not window-shaped: keep the gather kernels
+        // not window-shaped (the windows alone would overflow the two stages): keep the gather kernels
+        if (own0 < 0 || Q1 - Q0 > 65535 || win_smem_bytes<KP, RL>(0, total) > CG_SMEM_MAX) return;
+        zrows = std::max(zrows, total);
         e.own0 = own0;
         const int rows = (int)(R1 - R0), nz = Q1 - Q0;
         const size_t b_ip = al16(4 * (size_t)(rows + 1)), b_zs = al16(2 * (size_t)nz), b_v = al16(8 * (size_t)nz);
@@ -1924,19 +1968,22 @@ static void win_host(const rexi_desc *d, const std::vector<double> &ta, const st
         dir[(size_t)gs] = e;
     }
     blob_max = (blob_max + 127) & ~127;
-    if (win_smem_bytes<KP, RL>(blob_max) > 227 * 1024) return;
+    zrows = (zrows + 7) & ~7;
+    if (win_smem_bytes<KP, RL>(blob_max, zrows) > CG_SMEM_MAX) return;
     out.ok = true;
     out.rl = RL;
     out.blob_max = blob_max;
+    out.zrows = zrows;
     out.nstages = nstages;
 }
 
-// two row-lanes per thread where the stages' columns fit the window budget, else one
-// (3D-like patterns; kp >= 64 only)
+// two row-lanes per thread where the stages' windows and blob fit the shared-memory
+// budget, else one (3D-like patterns, and the narrow layouts whose stages are mostly
+// matrix); kp = 32 has no one-row-lane form (its stage would be half a chunk)
 template <int KP>
 static void win_host_any(const rexi_desc *d, const std::vector<double> &ta, const std::vector<double> &bb, WinHost &out) {
     if (KP >= 8) win_host<KP, 2>(d, ta, bb, out);
-    if (!out.ok && (KP >= 64 || KP <= 4)) win_host < KP, KP >= 64 || KP <= 4 ? 1 : 2 > (d, ta, bb, out);
+    if (!out.ok && KP != 32) win_host < KP, KP != 32 ? 1 : 2 > (d, ta, bb, out);
 }
 
 static int win_upload(CocgState &cg, const WinHost &h, CgWin &w, cudaStream_t st, std::string &err) {
@@ -1952,6 +1999,7 @@ static int win_upload(CocgState &cg, const WinHost &h, CgWin &w, cudaStream_t st
     w.dir = ddir;
     w.blob = dblob;
     w.blob_max = h.blob_max;
+    w.zrows = h.zrows;
     w.nstages = h.nstages;
     return REXI_OK;
 }
@@ -2310,7 +2358,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
 #define REXI_WIN_LAUNCH(KPV, RLV)                                                                          \
     {                                                                                                      \
         static int attr_for = -1;   /* largest dynamic shared memory size set for this instantiation */   \
-        const int sm_ = (int)win_smem_bytes<KPV, RLV>(wn->blob_max);                                       \
+        const int sm_ = (int)win_smem_bytes<KPV, RLV>(wn->blob_max, wn->zrows);                            \
         if (sm_ > attr_for) {                                                                              \
             CGK(cudaFuncSetAttribute(k_cg_spmv_win<KPV, RLV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_)); \
             attr_for = sm_;                                                                                \
@@ -2320,8 +2368,10 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
                 if (kp == 1) REXI_WIN_LAUNCH(1, 1)
                 else if (kp == 2) REXI_WIN_LAUNCH(2, 1)
                 else if (kp == 4) REXI_WIN_LAUNCH(4, 1)
-                else if (kp == 8) REXI_WIN_LAUNCH(8, 2)
-                else if (kp == 16) REXI_WIN_LAUNCH(16, 2)
+                else if (kp == 8 && wn->rl == 2) REXI_WIN_LAUNCH(8, 2)
+                else if (kp == 8) REXI_WIN_LAUNCH(8, 1)
+                else if (kp == 16 && wn->rl == 2) REXI_WIN_LAUNCH(16, 2)
+                else if (kp == 16) REXI_WIN_LAUNCH(16, 1)
                 else if (kp == 32) REXI_WIN_LAUNCH(32, 2)
                 else if (kp == 64 && wn->rl == 2) REXI_WIN_LAUNCH(64, 2)
                 else if (kp == 64) REXI_WIN_LAUNCH(64, 1)
