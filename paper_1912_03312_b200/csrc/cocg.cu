@@ -2491,7 +2491,9 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
         while (kp_new > 1 && na <= kp_new / 2) kp_new /= 2;
         bool prefix = false;
         static const bool no_prefix = getenv("REXI_COCG_NOPREFIX") != nullptr;   // A/B switch
-        if (!no_prefix && kp_new == kp && kp >= 16 && packed_live - na >= kp / 8)
+        static const int repack_div = getenv("REXI_COCG_REPACK_DIV") ? std::max(1, atoi(getenv("REXI_COCG_REPACK_DIV"))) : 8;
+        static const int repack_min = getenv("REXI_COCG_REPACK_MINKP") ? atoi(getenv("REXI_COCG_REPACK_MINKP")) : 16;
+        if (!no_prefix && kp_new == kp && kp >= repack_min && packed_live - na >= std::max(1, kp / repack_div))
             for (int l = na; l < kp && !prefix; ++l) prefix = h_act[l] != 0;
         if (kp_new < kp || prefix) {
             if (kp_new < kp) trace_phase(kp, na);
@@ -2519,7 +2521,8 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             // the wide layouts, to 32-B sectors below): what the kernels stream
             // -- the TMA spmv moves whole rows -- follows the live lanes
             static const bool no_ld = getenv("REXI_COCG_NOLD") != nullptr;   // A/B switch
-            const int gran = kp_new >= 16 ? 8 : 2;
+            static const int ld_gran = getenv("REXI_COCG_LDGRAN") ? std::max(1, atoi(getenv("REXI_COCG_LDGRAN"))) : 8;
+            const int gran = kp_new >= 16 ? ld_gran : std::min(2, ld_gran);
             const int ld_new = no_ld ? kp_new : std::min(kp_new, (live + gran - 1) / gran * gran);
             int rc = cg_repack(im, kp, ld, kp_new, ld_new, map, drop, lane_shift, st, err);
             if (rc) return rc;
