@@ -2517,11 +2517,12 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             }
             const int live = (int)map.size();
             for (int l = live; l < kp_new; ++l) map.push_back(map[0]);
-            // rows keep only the live prefix (rounded up to whole 128-B lines on
-            // the wide layouts, to 32-B sectors below): what the kernels stream
-            // -- the TMA spmv moves whole rows -- follows the live lanes
+            // rows keep only the live prefix (rounded up to 32-B sectors): what the
+            // kernels stream -- the TMA kernels move whole rows -- follows the live
+            // lanes.  scripts/tune_repack.sh: 2 lanes against 8 (whole 128-B lines)
+            // cfg 3 -1.2 %, cfg 5 -2 %; repacking twice as often no further gain
             static const bool no_ld = getenv("REXI_COCG_NOLD") != nullptr;   // A/B switch
-            static const int ld_gran = getenv("REXI_COCG_LDGRAN") ? std::max(1, atoi(getenv("REXI_COCG_LDGRAN"))) : 8;
+            static const int ld_gran = getenv("REXI_COCG_LDGRAN") ? std::max(1, atoi(getenv("REXI_COCG_LDGRAN"))) : 2;
             const int gran = kp_new >= 16 ? ld_gran : std::min(2, ld_gran);
             const int ld_new = no_ld ? kp_new : std::min(kp_new, (live + gran - 1) / gran * gran);
             int rc = cg_repack(im, kp, ld, kp_new, ld_new, map, drop, lane_shift, st, err);
