@@ -966,13 +966,15 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         return;
     }
     // ---- consumers: RL row-lanes per thread and stage ----
-    static_assert(RL == 2 || KP >= 64 || G::R >= 32, "one row-lane per thread: whole chunks per stage or kp >= 64");
+    static_assert(RL == 2 || KP >= 32 || G::R >= 32, "one row-lane per thread: whole chunks per stage, or kp >= 32");
+    static_assert(KP > 32 || NST <= 2, "terms over at most two stages per chunk");
     const int lane = threadIdx.x % KP;
     const int lr0 = threadIdx.x / KP;
     constexpr int LRS = CGT_CT / KP;                   // local-row distance of a thread's two rows
     constexpr bool SAME = LRS == CG_CH;                // a thread's rows all belong to sub-block lr0 (kp = 64);
                                                        // kp = 128: to sub-blocks lr0 and lr0 + 4
-    constexpr bool TERMS = KP <= 32;                   // a stage holds whole chunks: per-row terms, summed in tree order
+    constexpr bool TERMS = KP <= 32;                   // per-row terms, summed in tree order: a stage holds whole
+                                                       // chunks (or, kp = 32 with one row-lane, half a chunk: NST = 2)
     const bool act = Sc.active[lane] != 0;
     const bool fl = !act && Sc.flush[lane] != 0;
     const c128 sg = S.sigma[g.lane_shift[lane]];
@@ -995,7 +997,7 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         c128 *zw = reinterpret_cast<c128 *>(base + 3 * G::tile_bytes);
         const int64_t R0 = gs * R;
         const int rows = (int)min((int64_t)R, M.n - R0);
-        if (h == 0 || TERMS) mu[0] = mu[1] = cmk(0.0, 0.0);
+        if (h == 0 || (TERMS && NST == 1)) mu[0] = mu[1] = cmk(0.0, 0.0);
         if (rows > 0 && (act || fl)) {
             const unsigned char *blob = base + 3 * G::tile_bytes + zwin_bytes;
             const int4 dq = dirq[s];
@@ -1026,7 +1028,8 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
                         tp[t] = pi;
                         tq[t] = qi;
                         const c128 term = cmul(pi, qi);
-                        if (TERMS) mu[r] = term;
+                        if (TERMS && NST == 1) mu[r] = term;
+                        else if (TERMS) { if (h == 0) mu[0] = term; else mu[1] = term; }
                         else if (a == 0) mu[0] = cadd(mu[0], term);
                         else mu[1] = cadd(mu[1], term);
                     } else {
@@ -1037,17 +1040,18 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         }
         fence_proxy_async();         // tile writes -> visible to the bulk stores
         bar_consumers();             // every consumer is done with the stage's z windows and tiles
-        if (TERMS) {
-            // the stage holds G::CPS whole chunks: per-row terms through the (now dead)
+        if (TERMS && (NST == 1 || h == NST - 1)) {
+            // the stage holds G::CPS whole chunks (NST = 2: the chunk's second half, the
+            // first half's terms are in mu[0]): per-row terms through the (now dead)
             // z-window area, then each chunk's tree (sub-block b = rows b, b+8, b+16,
             // b+24 in order from 0; the 8 sub-blocks in order from 0)
             double2 *trm = reinterpret_cast<double2 *>(zw);
             trm[lr0 * KP + lane] = mu[0];
-            if (RL == 2) trm[(lr0 + LRS) * KP + lane] = mu[1];
+            if (RL == 2 || NST == 2) trm[(lr0 + (NST == 2 ? R : LRS)) * KP + lane] = mu[1];
             bar_consumers();
             if (threadIdx.x < G::CPS * KP) {
                 const int cc = threadIdx.x / KP, ll = threadIdx.x % KP;
-                const int64_t chunk = gs * G::CPS + cc;
+                const int64_t chunk = NST == 2 ? gs / NST : gs * G::CPS + cc;
                 if (chunk < g.nchunks) {
                     const double2 *tc = trm + (size_t)cc * (CG_SB * CG_CH) * KP + ll;
                     double2 sum = make_double2(0.0, 0.0);
@@ -1968,7 +1972,7 @@ static void win_host(const rexi_desc *d, const std::vector<double> &ta, const st
         dir[(size_t)gs] = e;
     }
     blob_max = (blob_max + 127) & ~127;
-    zrows = (zrows + 7) & ~7;
+    zrows = std::max((zrows + 7) & ~7, CG_SB * CG_CH);   // the dead window area also stages a chunk's terms
     if (win_smem_bytes<KP, RL>(blob_max, zrows) > CG_SMEM_MAX) return;
     out.ok = true;
     out.rl = RL;
@@ -1979,11 +1983,11 @@ static void win_host(const rexi_desc *d, const std::vector<double> &ta, const st
 
 // two row-lanes per thread where the stages' windows and blob fit the shared-memory
 // budget, else one (3D-like patterns, and the narrow layouts whose stages are mostly
-// matrix); kp = 32 has no one-row-lane form (its stage would be half a chunk)
+// matrix)
 template <int KP>
 static void win_host_any(const rexi_desc *d, const std::vector<double> &ta, const std::vector<double> &bb, WinHost &out) {
     if (KP >= 8) win_host<KP, 2>(d, ta, bb, out);
-    if (!out.ok && KP != 32) win_host < KP, KP != 32 ? 1 : 2 > (d, ta, bb, out);
+    if (!out.ok) win_host<KP, 1>(d, ta, bb, out);
 }
 
 static int win_upload(CocgState &cg, const WinHost &h, CgWin &w, cudaStream_t st, std::string &err) {
@@ -2372,7 +2376,8 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
                 else if (kp == 8) REXI_WIN_LAUNCH(8, 1)
                 else if (kp == 16 && wn->rl == 2) REXI_WIN_LAUNCH(16, 2)
                 else if (kp == 16) REXI_WIN_LAUNCH(16, 1)
-                else if (kp == 32) REXI_WIN_LAUNCH(32, 2)
+                else if (kp == 32 && wn->rl == 2) REXI_WIN_LAUNCH(32, 2)
+                else if (kp == 32) REXI_WIN_LAUNCH(32, 1)
                 else if (kp == 64 && wn->rl == 2) REXI_WIN_LAUNCH(64, 2)
                 else if (kp == 64) REXI_WIN_LAUNCH(64, 1)
                 else if (wn->rl == 2) REXI_WIN_LAUNCH(128, 2)
