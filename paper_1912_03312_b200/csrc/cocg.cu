@@ -11,15 +11,25 @@
 // contiguous segment.  Shifted entries tau*a - (1j*sigma)*b are formed on the
 // fly with the reference's rounding.
 //
-// Iteration = two kernels (COCG needs two reductions per iteration):
-//   spmv  : p = z + beta p_old (own row; double-buffered), q = S p with the
-//           neighbours' p recomputed from the gathered z, p_old; mu = p^T q.
-//           Rows are claimed in chunks from an atomic counter, so all SMs
-//           work on one narrow wavefront and the +-n neighbour rows of a 2D/3D
-//           stencil are L2 hits; the per-chunk partials are indexed by chunk,
-//           so the reduction order is fixed (deterministic).
-//   update: x += alpha p, z -= alpha D^-1 q (the preconditioned residual; r =
-//           D z is formed for rho' = r^T z and |r|^2 only).
+// Iteration = two kernels (COCG needs two reductions per iteration), 160 B per
+// live row-shift:
+//   spmv  : x += alpha_prev p (the previous iteration's deferred update, see
+//           CG_DEFER_X), p = z + beta p, q = S z + beta q (= S p by linearity:
+//           only z is gathered), mu = p^T q.  Chunks are claimed from an
+//           atomic counter, so all SMs work on one narrow wavefront and the
+//           +-n neighbour rows of a 2D/3D stencil are L2 hits; the per-chunk
+//           partials are indexed by chunk, so the reduction order is fixed.
+//   update: z -= alpha D^-1 q (the preconditioned residual; r = D z is formed
+//           for rho' = r^T z and |r|^2 only).
+// Kernel families, all with the same rows per sub-block, per-lane operation
+// order and partial tree (bitwise identical results):
+//   k_cg_spmv_win / k_cg_update_tma : persistent producer/consumer pipelines,
+//           every operand by cp.async.bulk into shared-memory stages (the
+//           default wherever the plan has window tables / the layout has
+//           >= 2 lanes);
+//   k_cg_spmv_tma : tiles by bulk copy, z gathered (2D patterns without tables);
+//   k_cg_spmv_st, k_cg_spmv, k_cg_spmv1, k_cg_update, k_cg_update1 : gather
+//           kernels (complex A, patterns that fit no window budget, one lane).
 // The last CTA of each kernel finishes the per-shift scalars (alpha, beta),
 // freezes converged shifts and flags breakdown / non-finite values.
 // Compaction: when at most half of the lanes are live, the live shifts are
