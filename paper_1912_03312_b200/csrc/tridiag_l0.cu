@@ -41,6 +41,10 @@ constexpr int K2_UNROLL = K2_RES_UNROLL;
 #ifndef K2_MINB
 #define K2_MINB 4
 #endif
+#ifndef K2_I32
+#define K2_I32 0   // 1: the correction sweep's complex64 pivots staged with the rest (+16 KB shared memory) instead of
+                   // read from HBM in the sweep -- K2 0.680 -> 0.672 ms but the step no faster (scripts/tune_k2i32.sh)
+#endif
 #ifndef K2_ALIGNED
 #define K2_ALIGNED 1   // real symmetric A: aligned-quantum residual instead of Dot2 (see k2_refine)
 #endif
@@ -85,12 +89,14 @@ struct RowView {
     __device__ __forceinline__ c128 sup(int lr, c128 sg) const { return form_entry(ur[lr], ui[lr], ub[lr], sg); }
 };
 
-enum { ST_RHS = 1, ST_DIA = 2, ST_TILE2 = 4, ST_BDIA = 8, ST_T32 = 16, ST_R32 = 32 };
-// ST_T32: t0 holds complex64; ST_R32: + float copies of the sub/sup row data
+enum { ST_RHS = 1, ST_DIA = 2, ST_TILE2 = 4, ST_BDIA = 8, ST_T32 = 16, ST_R32 = 32, ST_I32 = 64 };
+// ST_T32: t0 holds complex64; ST_R32: + float copies of the sub/sup row data;
+// ST_I32: + the complex64 copy of the inverse-pivot tile (K2's correction sweep)
 
 struct L0Layout {
     int kp, T, Tp;
     c128 *t0, *t1;
+    const c64 *i32;   // ST_I32
     RowView rv;
 };
 
@@ -119,11 +125,15 @@ __device__ __forceinline__ L0Layout carve(unsigned char *smem, int kp, int M, in
     r.dr = r.di = r.db = nullptr;
     if (flags & ST_DIA) { r.dr = d; d += l.Tp; r.di = d; d += l.Tp; r.db = d; d += l.Tp; }
     else if (flags & ST_BDIA) { r.db = d; d += l.Tp; }
+    float *fend = reinterpret_cast<float *>(d);
     if (flags & ST_R32) {
         float *f = reinterpret_cast<float *>(d);
         const int tp4 = (l.Tp + 3) & ~3;
         for (int q = 0; q < 6; ++q) r.f[q] = f + q * tp4;
+        fend = f + 6 * tp4;
     }
+    l.i32 = nullptr;
+    if (flags & ST_I32) l.i32 = reinterpret_cast<const c64 *>((reinterpret_cast<uintptr_t>(fend) + 15) & ~(uintptr_t)15);
     return l;
 }
 
@@ -133,6 +143,7 @@ __host__ __device__ inline size_t l0_smem_bytes(int kp, int M, int flags) {
     if (flags & ST_RHS) b += Tp * 16;
     b += Tp * 8 * ((flags & ST_DIA) ? 9 : (flags & ST_BDIA) ? 7 : 6);
     if (flags & ST_R32) b += 6 * ((Tp + 3) & ~(size_t)3) * sizeof(float);
+    if (flags & ST_I32) b = ((b + 15) & ~(size_t)15) + T * kp * sizeof(c64);
     return b;
 }
 
@@ -153,9 +164,12 @@ __device__ __forceinline__ void l0_stage(unsigned char *smem, const L0Layout &l,
         const uint32_t tb0 = (uint32_t)((row1 - row0) * l.kp * esz);
         const uint32_t rb8 = (uint32_t)(l.Tp * 8), rb16 = (uint32_t)(l.Tp * 16);
         const uint32_t rb4 = (uint32_t)(((l.Tp + 3) & ~3) * sizeof(float));
+        const uint32_t tb32 = (uint32_t)((row1 - row0) * l.kp * sizeof(c64));
         uint32_t total = tb0 + ((flags & ST_TILE2) ? tb : 0) + ((flags & ST_RHS) ? rb16 : 0) +
-                         rb8 * ((flags & ST_DIA) ? 9 : (flags & ST_BDIA) ? 7 : 6) + ((flags & ST_R32) ? 6 * rb4 : 0);
+                         rb8 * ((flags & ST_DIA) ? 9 : (flags & ST_BDIA) ? 7 : 6) + ((flags & ST_R32) ? 6 * rb4 : 0) +
+                         ((flags & ST_I32) ? tb32 : 0);
         mbar_expect_tx(bar, total);
+        if (flags & ST_I32) bulk_g2s((void *)l.i32, a.inv32 + row0 * l.kp, tb32, bar);
         bulk_g2s(l.t0, reinterpret_cast<const unsigned char *>(g_t0) + (size_t)row0 * l.kp * esz, tb0, bar);
         if (flags & ST_TILE2) bulk_g2s(l.t1, g_t1 + row0 * l.kp, tb, bar);
         if (flags & ST_RHS) bulk_g2s((void *)l.rv.rhs, a.rhs0 + row0, rb16, bar);
@@ -235,6 +249,16 @@ __device__ __forceinline__ void reduce_rows(const TT *tile, const L0Args &a, int
         // the dd accumulation keeps the rounded row sum independent of how
         // the lanes are grouped (k_pad, sharding): a plain fp64 chain here
         // broke the bitwise sharded-vs-single equality of the refined path
+        // K3 adds to the partial K2 left: its four words are loaded before the lane
+        // loop (the ncu source view had 8.8 % of K3's stall samples on the first
+        // dd_add below when they were loaded there)
+        const int64_t row = row0 + r;
+        const bool lead = sub == 0 && row < n;
+        dd pre = {0.0, 0.0}, pim = {0.0, 0.0};
+        if (a.acc_add && lead) {
+            pre = dd{a.acc[row], a.acc[n + row]};
+            pim = dd{a.acc[2 * n + row], a.acc[3 * n + row]};
+        }
         ddacc re = {0.0, 0.0}, im = {0.0, 0.0};
 #pragma unroll
         for (int jj = sub; jj < kp; jj += tpr) {
@@ -253,11 +277,10 @@ __device__ __forceinline__ void reduce_rows(const TT *tile, const L0Args &a, int
             sre = dd_add(sre, ore);
             sim = dd_add(sim, oim);
         }
-        const int64_t row = row0 + r;
-        if (sub == 0 && row < n) {
+        if (lead) {
             if (a.acc_add) {
-                sre = dd_add(sre, dd{a.acc[row], a.acc[n + row]});
-                sim = dd_add(sim, dd{a.acc[2 * n + row], a.acc[3 * n + row]});
+                sre = dd_add(sre, pre);
+                sim = dd_add(sim, pim);
             }
             if (a.final_out) {
                 a.uout[row] = cmk(__dadd_rn(sre.hi, sre.lo), __dadd_rn(sim.hi, sim.lo));
@@ -627,8 +650,14 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
     (void)y;
     (void)ti;
     const c64 sg32 = to_c64(c.sg);
+    // (K2_I32: staged by the CTA's bulk copies -- the ncu source view had 8.7 % of
+    // K2's stall samples on the first two uses of these pivots when they were
+    // loaded from HBM here)
     const c64 *iv32 = a.inv32 + c.base * kp + j;
-    auto piv = [&](int q) -> c64 { return K2_ONE_TILE ? __ldg(iv32 + q * kp) : to_c64(ti[q * kp]); };
+    const c64 *sv32 = l.i32 + (size_t)c.lr0 * kp + j;
+    auto piv = [&](int q) -> c64 {
+        return !K2_ONE_TILE ? to_c64(ti[q * kp]) : K2_I32 ? sv32[q * kp] : __ldg(iv32 + q * kp);
+    };
     c64 yf[M];
     yf[0] = c64mk(0.f, 0.f);
 #pragma unroll
@@ -658,7 +687,8 @@ __device__ __forceinline__ void k2_refine(const L0Args &a, const L0Layout &l, co
     if (c.p == 0) a.L.lcdd[j] = cdh_pack(cdd_zero());
 }
 
-constexpr int K2_FLAGS = K2_ONE_TILE ? (ST_RHS | ST_DIA | ST_R32) : (ST_RHS | ST_DIA | ST_TILE2 | ST_R32);
+constexpr int K2_FLAGS = (K2_ONE_TILE ? (ST_RHS | ST_DIA | ST_R32) : (ST_RHS | ST_DIA | ST_TILE2 | ST_R32)) |
+                         (K2_ONE_TILE && K2_I32 ? ST_I32 : 0);
 // KP: k_pad at compile time for the common K = 64 (0: runtime).  At runtime
 // k_pad a fifth of K2's instructions were integer address arithmetic
 // (ncu source view, profiles/r02_k2_sass_regions.txt).
@@ -682,6 +712,10 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
         if (r0 < a.L.n) {
             const int64_t r1 = min(r0 + (int64_t)l.T, a.L.n);
             bulk_prefetch_l2(a.L.invd + r0 * l.kp, (uint32_t)((r1 - r0) * l.kp * sizeof(c128)));
+#ifndef K2_PF32
+#define K2_PF32 1   // also the complex64 pivot tile the correction sweep reads
+#endif
+            if (K2_ONE_TILE && K2_PF32) bulk_prefetch_l2(a.inv32 + r0 * l.kp, (uint32_t)((r1 - r0) * l.kp * sizeof(c64)));
             const uint32_t rb8 = (uint32_t)(l.Tp * 8);
             bulk_prefetch_l2(a.rhs0 + r0, (uint32_t)(l.Tp * 16));
             const double *rows[9] = {a.z.ta_sub, a.z.ta_sub_im, a.z.b_sub, a.z.ta_sup, a.z.ta_sup_im,
