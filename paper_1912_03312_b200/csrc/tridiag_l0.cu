@@ -712,10 +712,6 @@ __global__ void __launch_bounds__(L0_NT, K2_MINB) k_l0_k2(L0Args a) {
         if (r0 < a.L.n) {
             const int64_t r1 = min(r0 + (int64_t)l.T, a.L.n);
             bulk_prefetch_l2(a.L.invd + r0 * l.kp, (uint32_t)((r1 - r0) * l.kp * sizeof(c128)));
-#ifndef K2_PF32
-#define K2_PF32 1   // also the complex64 pivot tile the correction sweep reads
-#endif
-            if (K2_ONE_TILE && K2_PF32) bulk_prefetch_l2(a.inv32 + r0 * l.kp, (uint32_t)((r1 - r0) * l.kp * sizeof(c64)));
             const uint32_t rb8 = (uint32_t)(l.Tp * 8);
             bulk_prefetch_l2(a.rhs0 + r0, (uint32_t)(l.Tp * 16));
             const double *rows[9] = {a.z.ta_sub, a.z.ta_sub_im, a.z.b_sub, a.z.ta_sup, a.z.ta_sup_im,
