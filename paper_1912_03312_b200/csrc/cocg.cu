@@ -917,33 +917,57 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         int it = 0;
         bool ended = false;
         const int64_t nunits = (g.nchunks + G::CPS - 1) / G::CPS;   // claim unit: a chunk (kp >= 64) or a stage
-        while (!ended) {
-            const int64_t chunk = (int64_t)atomicAdd(Sc.ctr, 1u);
-            for (int h = 0; h < NST; ++h, ++it) {
-                const int s = it & 1;
-                if (it >= 2) {
-                    mbar_wait(done + s, dph[s]);
-                    dph[s] ^= 1u;
+        // The refill of a stage sits on the consumers' critical path, so nothing
+        // with a global round trip stays in it: the next unit is claimed one unit
+        // ahead and the next stage's directory entry is loaded one stage ahead
+        // (CGW_LOOKAHEAD=0: both inside the refill, the first form of this kernel).
+#ifndef CGW_LOOKAHEAD
+#define CGW_LOOKAHEAD 1
+#endif
+        auto has_rows = [&](int64_t ch, int hh) { return ch < nunits && (ch * NST + hh) * R < M.n; };
+        int64_t chunk = (int64_t)atomicAdd(Sc.ctr, 1u), chunk_nx = 0;
+        bool nx_claimed = false;
+        int h = 0;
+        WinStage d{};
+        if (CGW_LOOKAHEAD && has_rows(chunk, 0)) d = W.dir[chunk * NST];
+#ifndef CGW_ZFIRST
+#define CGW_ZFIRST 0   // refill: z windows and blob first (their area is free at `done`), the tiles after
+                       // the previous stage's stores have been read out (0: everything after the stores)
+#endif
+        for (;; ++it) {
+            const int s = it & 1;
+            bool pending_store = false;
+            if (it >= 2) {
+                mbar_wait(done + s, dph[s]);
+                dph[s] ^= 1u;
+                if (CGW_ZFIRST && chunk < nunits) {
+                    pending_store = true;
+                } else {
                     store(s, prev[s]);
                     bulk_wait_read0();
                 }
-                if (chunk >= nunits) {
-                    slot_q[s] = -1;
-                    mbar_arrive(full + s);
-                    ended = true;
-                    break;
+            }
+            if (chunk >= nunits) {
+                slot_q[s] = -1;
+                mbar_arrive(full + s);
+                ended = true;
+                break;
+            }
+            const int64_t gs = chunk * NST + h;
+            const int64_t gs_prev = prev[s];
+            slot_q[s] = gs;
+            prev[s] = gs;
+            const int64_t R0 = gs * R;
+            const int64_t rows = min((int64_t)R, M.n - R0);
+            if (rows <= 0) {            // stage past the last row of the last chunk
+                if (pending_store) {
+                    store(s, gs_prev);
+                    bulk_wait_read0();
                 }
-                const int64_t gs = chunk * NST + h;
-                slot_q[s] = gs;
-                prev[s] = gs;
-                const int64_t R0 = gs * R;
-                const int64_t rows = min((int64_t)R, M.n - R0);
-                if (rows <= 0) {            // stage past the last row of the last chunk
-                    mbar_arrive(full + s);
-                    continue;
-                }
+                mbar_arrive(full + s);
+            } else {
                 unsigned char *base = smem + 128 + (size_t)s * stage_bytes;
-                const WinStage d = W.dir[gs];
+                if (!CGW_LOOKAHEAD) d = W.dir[gs];
                 dirq[s] = make_int4(d.off_zs, d.off_ta, d.off_b, d.own0);
                 const uint32_t tb = (uint32_t)(rows * ld * sizeof(c128));
                 const uint32_t rb = ld * (uint32_t)sizeof(c128);
@@ -953,9 +977,6 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
                 const uint32_t zb = zr * rb;
                 mbar_expect_tx(full + s, 3 * tb + zb + (uint32_t)d.blob_bytes);
                 const size_t o = (size_t)R0 * ld;
-                ld_s(base, V.p + o, tb, full + s);
-                ld_s(base + G::tile_bytes, V.q + o, tb, full + s);
-                ld_s(base + 2 * G::tile_bytes, V.x + o, tb, full + s);
                 unsigned char *zw = base + 3 * G::tile_bytes;
                 uint32_t zo = 0;
 #pragma unroll
@@ -965,8 +986,27 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
                         zo += (uint32_t)d.wrows[k] * rb;
                     }
                 ld_s(zw + zwin_bytes, W.blob + d.blob_off, (uint32_t)d.blob_bytes, full + s);
+                if (pending_store) {   // the tile area: once the previous stage's stores have read it out
+                    store(s, gs_prev);
+                    bulk_wait_read0();
+                }
+                ld_s(base, V.p + o, tb, full + s);
+                ld_s(base + G::tile_bytes, V.q + o, tb, full + s);
+                ld_s(base + 2 * G::tile_bytes, V.x + o, tb, full + s);
             }
+            // the stage after this one
+            if (CGW_LOOKAHEAD && !nx_claimed) {
+                chunk_nx = (int64_t)atomicAdd(Sc.ctr, 1u);
+                nx_claimed = true;
+            }
+            if (++h == NST) {
+                h = 0;
+                chunk = CGW_LOOKAHEAD ? chunk_nx : (int64_t)atomicAdd(Sc.ctr, 1u);
+                nx_claimed = false;
+            }
+            if (CGW_LOOKAHEAD && has_rows(chunk, h)) d = W.dir[chunk * NST + h];
         }
+        (void)ended;
         if (it >= 1) {   // the stage computed last sits in the other slot
             const int s = (it - 1) & 1;
             mbar_wait(done + s, dph[s]);
