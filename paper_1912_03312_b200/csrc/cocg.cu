@@ -930,22 +930,13 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
         int h = 0;
         WinStage d{};
         if (CGW_LOOKAHEAD && has_rows(chunk, 0)) d = W.dir[chunk * NST];
-#ifndef CGW_ZFIRST
-#define CGW_ZFIRST 0   // refill: z windows and blob first (their area is free at `done`), the tiles after
-                       // the previous stage's stores have been read out (0: everything after the stores)
-#endif
         for (;; ++it) {
             const int s = it & 1;
-            bool pending_store = false;
             if (it >= 2) {
                 mbar_wait(done + s, dph[s]);
                 dph[s] ^= 1u;
-                if (CGW_ZFIRST && chunk < nunits) {
-                    pending_store = true;
-                } else {
-                    store(s, prev[s]);
-                    bulk_wait_read0();
-                }
+                store(s, prev[s]);
+                bulk_wait_read0();
             }
             if (chunk >= nunits) {
                 slot_q[s] = -1;
@@ -954,16 +945,11 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
                 break;
             }
             const int64_t gs = chunk * NST + h;
-            const int64_t gs_prev = prev[s];
             slot_q[s] = gs;
             prev[s] = gs;
             const int64_t R0 = gs * R;
             const int64_t rows = min((int64_t)R, M.n - R0);
             if (rows <= 0) {            // stage past the last row of the last chunk
-                if (pending_store) {
-                    store(s, gs_prev);
-                    bulk_wait_read0();
-                }
                 mbar_arrive(full + s);
             } else {
                 unsigned char *base = smem + 128 + (size_t)s * stage_bytes;
@@ -986,10 +972,6 @@ __global__ void __launch_bounds__(CGT_NT, 1) k_cg_spmv_win(CgMat M, CgVec V, CgS
                         zo += (uint32_t)d.wrows[k] * rb;
                     }
                 ld_s(zw + zwin_bytes, W.blob + d.blob_off, (uint32_t)d.blob_bytes, full + s);
-                if (pending_store) {   // the tile area: once the previous stage's stores have read it out
-                    store(s, gs_prev);
-                    bulk_wait_read0();
-                }
                 ld_s(base, V.p + o, tb, full + s);
                 ld_s(base + G::tile_bytes, V.q + o, tb, full + s);
                 ld_s(base + 2 * G::tile_bytes, V.x + o, tb, full + s);
