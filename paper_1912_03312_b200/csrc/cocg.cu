@@ -2040,6 +2040,42 @@ static int win_upload(CocgState &cg, const WinHost &h, CgWin &w, cudaStream_t st
     return REXI_OK;
 }
 
+// Dynamic shared-memory limits of the big-shared-memory kernels.  Function
+// attributes are per device, so this runs at every plan creation on the plan's
+// device (a process-wide "done" flag would leave the other GPUs of an
+// in-process multi-GPU stepper without them).
+static cudaError_t cocg_set_smem_attrs() {
+    cudaError_t e = cudaSuccess;
+#define REXI_ATTR(fn, bytes)                                                                          \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))
+    REXI_ATTR(k_cg_spmv_st<true>, st_smem_bytes(true));
+    REXI_ATTR(k_cg_spmv_st<false>, st_smem_bytes(false));
+#if CG_DEFER_X
+    REXI_ATTR(k_cg_spmv_tma, tma_smem_bytes());
+    REXI_ATTR(k_cg_update_tma<1>, upd_smem_bytes<1>());
+    REXI_ATTR(k_cg_update_tma<2>, upd_smem_bytes<2>());
+    REXI_ATTR(k_cg_update_tma<4>, upd_smem_bytes<4>());
+    REXI_ATTR(k_cg_update_tma<8>, upd_smem_bytes<8>());
+    REXI_ATTR(k_cg_update_tma<16>, upd_smem_bytes<16>());
+    REXI_ATTR(k_cg_update_tma<32>, upd_smem_bytes<32>());
+    REXI_ATTR(k_cg_update_tma<64>, upd_smem_bytes<64>());
+    REXI_ATTR(k_cg_update_tma<128>, upd_smem_bytes<128>());
+    // the windowed spmv's need depends on the plan's tables: allow the per-block maximum
+    auto w1 = k_cg_spmv_win<1, 1>;   auto w2 = k_cg_spmv_win<2, 1>;   auto w4 = k_cg_spmv_win<4, 1>;
+    auto w8a = k_cg_spmv_win<8, 2>;  auto w8b = k_cg_spmv_win<8, 1>;  auto w16a = k_cg_spmv_win<16, 2>;
+    auto w16b = k_cg_spmv_win<16, 1>; auto w32a = k_cg_spmv_win<32, 2>; auto w32b = k_cg_spmv_win<32, 1>;
+    auto w64a = k_cg_spmv_win<64, 2>; auto w64b = k_cg_spmv_win<64, 1>; auto w128a = k_cg_spmv_win<128, 2>;
+    auto w128b = k_cg_spmv_win<128, 1>;
+    REXI_ATTR(w1, CG_SMEM_MAX);   REXI_ATTR(w2, CG_SMEM_MAX);   REXI_ATTR(w4, CG_SMEM_MAX);
+    REXI_ATTR(w8a, CG_SMEM_MAX);  REXI_ATTR(w8b, CG_SMEM_MAX);  REXI_ATTR(w16a, CG_SMEM_MAX);
+    REXI_ATTR(w16b, CG_SMEM_MAX); REXI_ATTR(w32a, CG_SMEM_MAX); REXI_ATTR(w32b, CG_SMEM_MAX);
+    REXI_ATTR(w64a, CG_SMEM_MAX); REXI_ATTR(w64b, CG_SMEM_MAX); REXI_ATTR(w128a, CG_SMEM_MAX);
+    REXI_ATTR(w128b, CG_SMEM_MAX);
+#endif
+#undef REXI_ATTR
+    return e;
+}
+
 int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine, cudaStream_t st,
                 std::string &err) {
     CocgImpl *im = new CocgImpl();
@@ -2230,6 +2266,7 @@ int cocg_create(CocgState &cg, const rexi_desc *d, const ShiftDev &S, int refine
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&im->sms, cudaDevAttrMultiProcessorCount, dev);
+    CGK(cocg_set_smem_attrs());
     if ((double)n * kp >= 2147483647.0) {
         err = "COCG plan too large for 32-bit element offsets (n * k_pad >= 2^31); split the shifts";
         return REXI_ERR_UNSUPPORTED;
@@ -2393,12 +2430,7 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
                 const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(wn->nstages, (int64_t)im->sms));
 #define REXI_WIN_LAUNCH(KPV, RLV)                                                                          \
     {                                                                                                      \
-        static int attr_for = -1;   /* largest dynamic shared memory size set for this instantiation */   \
         const int sm_ = (int)win_smem_bytes<KPV, RLV>(wn->blob_max, wn->zrows);                            \
-        if (sm_ > attr_for) {                                                                              \
-            CGK(cudaFuncSetAttribute(k_cg_spmv_win<KPV, RLV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_)); \
-            attr_for = sm_;                                                                                \
-        }                                                                                                  \
         k_cg_spmv_win<KPV, RLV><<<gg, CGT_NT, sm_, st>>>(im->M, im->V, im->Sc, S, gw, *wn);                \
     }
                 if (kp == 1) REXI_WIN_LAUNCH(1, 1)
@@ -2422,26 +2454,12 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
                 // 15-entry 3D rows keep the staged kernel, whose larger L1 serves their
                 // gathers: cfg 5 +5 % with this one; scripts/tune_tma.sh, tune_ld.sh)
                 const CgGeom gt = make_geom(im, kp, n, CGT_CW, ld);
-                static bool tma_attr = false;
-                if (!tma_attr) {
-                    CGK(cudaFuncSetAttribute(k_cg_spmv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)tma_smem_bytes()));
-                    tma_attr = true;
-                }
                 const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(gt.nclaims, (int64_t)im->sms));
                 k_cg_spmv_tma<<<gg, CGT_NT, tma_smem_bytes(), st>>>(im->M, im->V, im->Sc, S, gt);
             } else
 #endif
             if (g.cpc <= 2 && im->stage_ok[g.cpc]) {
                 const size_t sm = st_smem_bytes(im->cplx);
-                static bool attr_set = false;
-                if (!attr_set) {
-                    CGK(cudaFuncSetAttribute(k_cg_spmv_st<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)st_smem_bytes(true)));
-                    CGK(cudaFuncSetAttribute(k_cg_spmv_st<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)st_smem_bytes(false)));
-                    attr_set = true;
-                }
                 if (im->cplx) k_cg_spmv_st<true><<<grid, CG_NT, sm, st>>>(im->M, im->V, im->Sc, S, g);
                 else k_cg_spmv_st<false><<<grid, CG_NT, sm, st>>>(im->M, im->V, im->Sc, S, g);
             } else if (g.kp == 1 && cg.nnz <= (int64_t)CG_GB * n) {
@@ -2465,15 +2483,6 @@ static int cg_solve(CocgState &cg, CocgImpl *im, const ShiftDev &S, cudaStream_t
             static const bool no_utma = getenv("REXI_COCG_NOUTMA") != nullptr;   // A/B switch
             static const int utma_min = getenv("REXI_COCG_UTMAMIN") ? atoi(getenv("REXI_COCG_UTMAMIN")) : 2;   // one lane: k_cg_update1 measured faster (33.6 vs 36.2 us)
             if (!no_utma && !no_tma && !im->cplx && kp >= utma_min && kp <= 128) {
-                static bool uattr = false;
-#define REXI_UPD_ATTR(KPV) \
-    CGK(cudaFuncSetAttribute(k_cg_update_tma<KPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem_bytes<KPV>()))
-                if (!uattr) {
-                    REXI_UPD_ATTR(1); REXI_UPD_ATTR(2); REXI_UPD_ATTR(4); REXI_UPD_ATTR(8);
-                    REXI_UPD_ATTR(16); REXI_UPD_ATTR(32); REXI_UPD_ATTR(64); REXI_UPD_ATTR(128);
-                    uattr = true;
-                }
-#undef REXI_UPD_ATTR
 #define REXI_UPD_LAUNCH(KPV)                                                                              \
     {                                                                                                     \
         const int64_t nu = (n + UpdGeom<KPV>::UNIT - 1) / UpdGeom<KPV>::UNIT;                             \
